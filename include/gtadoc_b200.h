@@ -1,0 +1,173 @@
+/*
+ * gtadoc_b200.h — C-ABI of the B200-native analytics-on-compression library
+ * (libgtadoc_b200.so).  Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * What it replaces in the reference (pure-Python package `gtadoc`, paths
+ * relative to /root/reference/pkg/src/gtadoc):
+ *
+ *   gt_open          grammar.py:193-228  deserialize_grammar(data) -> Grammar
+ *                    dag.py:131-230      build_dag(grammar) -> Dag
+ *                    (plus the level schedule that engine.py:196-227 and
+ *                    engine.py:313-335 discover round by round)
+ *   gt_run           tasks.py:171-185    run_task(dag, task, cfg, seq_len)
+ *                    i.e. tasks.py:122-168 word_count / sort_by_frequency /
+ *                    inverted_index / term_vector / sequence_count /
+ *                    ranked_inverted_index, and underneath them the kernel
+ *                    plugin backend.py:26-46 (_kernels.py:61-309 round kernels)
+ *   gt_result_view   the output containers tasks.py:61-88, as compact arrays
+ *                    already in the order render() (tasks.py:233-263) prints
+ *   gt_last_error    the exception message; the status code selects the
+ *                    class of errors.py:11-46 (see gt_status below)
+ *
+ * The reference's own kernel plugin API (backend.kernels(name) returning a
+ * module of 11 numba round functions over host int64 arrays) cannot host a
+ * device backend without editing the reference (backend names are validated
+ * against auto|numba|python, backend.py:30-31) and would force a host round
+ * trip per round, so the boundary sits one level up, at the task entry
+ * points, exactly as BASELINE.json north_star prescribes.  The Python facade
+ * paper_2106_06889_b200/tasks.py mirrors tasks.py names and containers on top
+ * of this ABI; INTEGRATION.md shows the ctypes binding.
+ *
+ * Threading: a gt_ctx is single-threaded (one CUDA stream on one device).
+ * Different contexts (e.g. one per device / rank) may be used concurrently.
+ */
+#ifndef GTADOC_B200_H
+#define GTADOC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GT_ABI_VERSION 1
+
+/* Status codes.  Exception class (errors.py) and CLI exit code in brackets. */
+enum gt_status {
+  GT_OK = 0,
+  GT_E_USAGE = 1,      /* UsageError        [exit 1]  errors.py:15-16 */
+  GT_E_RESOURCE = 2,   /* ResourceError     [exit 2]  errors.py:25-28 */
+  GT_E_FORMAT = 3,     /* FormatError       [exit 3]  errors.py:31-34 */
+  GT_E_CORRUPTION = 4, /* CorruptionError   [exit 3]  errors.py:37-40 */
+  GT_E_DEVICE = 5      /* CUDA failure      -> ResourceError [exit 2]  */
+};
+
+/* Task ids: tasks.py:47-56 HOOKS order. */
+enum gt_task {
+  GT_WORDCOUNT = 0,
+  GT_SORT = 1,
+  GT_INVERTEDINDEX = 2,
+  GT_TERMVECTOR = 3,
+  GT_SEQCOUNT = 4,
+  GT_RANKEDINVERTEDINDEX = 5
+};
+
+/* engine.py:31 STRATEGIES */
+enum gt_strategy { GT_AUTO = 0, GT_TOPDOWN = 1, GT_BOTTOMUP = 2 };
+
+typedef struct gt_ctx gt_ctx;
+typedef struct gt_result gt_result;
+
+/* Corpus / DAG statistics (SURVEY.md §8 notation). */
+typedef struct gt_info {
+  uint64_t num_words;      /* V  = dictionary.num_words                       */
+  uint64_t num_splitters;  /*      dictionary.num_splitters                   */
+  uint64_t num_rules;      /* R                                              */
+  uint64_t num_files;      /* F  = len(dag.segments)                          */
+  uint64_t total_elements; /* E  = dag.total_elements                         */
+  uint64_t root_len;       /* L0                                              */
+  uint64_t sub_pairs;      /* E_sub = len(dag.sub_ids)                        */
+  uint64_t own_pairs;      /* E_own = len(dag.own_ids)                        */
+  uint64_t words;          /* W  = exp_len[0] (uncompressed-equivalent words) */
+  int64_t depth;           /* dag.depth = height of the root                  */
+  int64_t td_levels;       /* top-down levels (= reference top-down rounds)   */
+  int64_t bu_levels;       /* bottom-up levels (= reference bottom-up rounds) */
+  uint64_t device_bytes;   /* device memory held by the context               */
+  double init_ms;          /* gt_open wall time (the "initialization" phase)  */
+} gt_info;
+
+/*
+ * Result view.  Arrays are owned by the gt_result (host memory) and stay
+ * valid until gt_result_free.  Layout per task:
+ *
+ *  WORDCOUNT  n records (id = word, count), ascending word id.
+ *  SORT       n records (id = word, count), (-count, word) order.
+ *  INVERTEDINDEX  n_groups words (group_id = word, ascending); records
+ *             group_off[g]..group_off[g+1] hold id = file (ascending).
+ *             count == NULL.
+ *  TERMVECTOR n_groups = F files; records of file f are group_off[f].. with
+ *             (id = word, count) in (-count, word) order.
+ *  SEQCOUNT   n_groups = F files; records of file f: gram + count in
+ *             (-count, gram) order.  wbits > 0: gram packed big-endian in
+ *             key[i] (wbits bits per word, sequence.py:229-256); wbits == 0
+ *             (gram mode, seq_len*wbits > 63): gram[i*seq_len + j].
+ *  RANKEDINVERTEDINDEX  n_groups grams in ascending gram order (group_key or
+ *             group_gram); records of gram g: (id = file, count) in
+ *             (-count, file) order.
+ */
+typedef struct gt_view {
+  int32_t task;
+  int32_t seq_len;
+  int32_t wbits;
+  int32_t strategy; /* the concrete strategy that ran (GT_TOPDOWN/GT_BOTTOMUP) */
+  uint64_t n_groups;
+  const uint64_t* group_off;  /* n_groups + 1 entries, or NULL */
+  const uint32_t* group_id;   /* II: word id per group */
+  const uint64_t* group_key;  /* RII packed gram per group */
+  const uint32_t* group_gram; /* RII gram mode: seq_len words per group */
+  uint64_t n;                 /* records */
+  const uint32_t* id;         /* word id or file id per record */
+  const uint64_t* key;        /* SC packed gram per record */
+  const uint32_t* gram;       /* SC gram mode: seq_len words per record */
+  const uint64_t* count;      /* per record; NULL for INVERTEDINDEX */
+  /* timings of this run */
+  double device_ms; /* device time of the traversal + assembly kernels      */
+  double d2h_ms;    /* device->host copy of the compact result              */
+  double total_ms;  /* wall time of gt_run                                  */
+  uint64_t d2h_bytes;
+  uint64_t kernel_launches; /* kernels launched by this gt_run              */
+} gt_view;
+
+int gt_abi_version(void);
+const char* gt_last_error(void); /* message of the last failing call on this thread */
+
+/* Parse + validate GTDC bytes, build the device DAG and level schedule on
+ * CUDA device `device`.  file_lo/file_hi restrict per-file work and root
+ * segments to files [file_lo, file_hi) (multi-GPU sharding);
+ * pass 0, UINT64_MAX for the whole corpus. */
+int gt_open(const uint8_t* gtdc, size_t nbytes, int device, uint64_t file_lo,
+            uint64_t file_hi, gt_ctx** out);
+int gt_info_get(const gt_ctx* ctx, gt_info* out);
+
+/* Run one analytics task (tasks.py:171-185).  strategy: gt_strategy;
+ * file_set_width: TraversalConfig.file_set_width (engine.py:39, default 64).
+ * seq_len is used by SEQCOUNT / RANKEDINVERTEDINDEX only. */
+int gt_run(gt_ctx* ctx, int task, int seq_len, int strategy, int file_set_width,
+           gt_result** out);
+int gt_result_view(const gt_result* res, gt_view* out);
+void gt_result_free(gt_result* res);
+void gt_close(gt_ctx* ctx);
+
+/* Dense global word counts left on the device by the last WORDCOUNT/SORT run
+ * (u64[num_words]); for NCCL all-reduce across shards.  Returns the device
+ * pointer or NULL. */
+uint64_t* gt_device_word_counts(gt_ctx* ctx);
+
+/* Test/diagnostic export of a DAG array as int64 (same content as the
+ * reference Dag field): name in {own_ids, own_freqs, own_off,
+ * own_token_count, sub_ids, sub_freqs, sub_off, par_ids, par_freqs, par_off,
+ * num_in_edge, num_out_edge, root_freq, exp_len, segments, td_level,
+ * bu_level, weight}.  Returns the element count (call with out=NULL to
+ * size), or -1 on error. */
+int64_t gt_dag_array(gt_ctx* ctx, const char* name, int64_t* out, int64_t cap);
+
+/* Evict L2 (writes a buffer larger than L2 on the context's stream). */
+int gt_flush_l2(gt_ctx* ctx);
+/* Synchronize the context's stream. */
+int gt_sync(gt_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GTADOC_B200_H */
