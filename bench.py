@@ -1,0 +1,378 @@
+#!/usr/bin/env python3
+"""Benchmark: uncompressed-equivalent words/s for word count + inverted index
+(BASELINE.json metric) on the C2 corpus (configs[1]: 1 GB-equivalent, 16
+large files, depth-24 rule DAG with heavy multi-parent sharing), composed
+deterministically on every box (synthetic, seed 2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = word count + inverted index over the whole corpus (both tasks,
+render-ordered compact results).  value = W / t_step with t_step the device
+time of the step measured with CUDA events on the library's stream (DAG
+resident in HBM, L2 flushed between steps); e2e = W / wall time of the
+public C-ABI path from the pinned host GTDC buffer (gt_open: H2D + device
+DAG build, both gt_runs, D2H of the results, gt_close).
+
+--impl reference times the reference's algorithm on the host cores through
+the CPU restatement in oracle/ (the reference itself is pure Python/numba and
+does not travel to the GPU box), on the same corpus, metric and step.
+Multi-GPU (torchrun): files are sharded by token-balanced ranges, the DAG is
+replicated, per-file outputs stay on their shard, global word counts are
+combined with an NCCL all-reduce; max-over-ranks timing.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "uncompressed-equivalent words/sec for word count & inverted index, 1–8 B200"
+UNIT = "words/s"
+TASKS = ("wordcount", "invertedindex")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="one profiled step, print kernel table")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            out, _ = self.p.communicate(timeout=10)
+            self.rows = [r.split(", ") for r in out.strip().splitlines() if r.strip()]
+        else:
+            self.rows = []
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for n, v in zip(names, r[4:8]):
+                    if v.strip() == "Active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def composed(args):
+    from paper_2106_06889_b200.corpus import compose, config_spec
+    spec = config_spec(args.config, scale=args.scale)
+    blob, stats = compose(spec)
+    return blob, stats
+
+
+def alg_bytes(kernel: str, info: dict, files: int) -> float | None:
+    """Algorithmic (compulsory) bytes per step for a kernel:
+    every input element read once, every output element written once."""
+    R, Es, Eo, V = info["num_rules"], info["sub_pairs"], info["own_pairs"], info["num_words"]
+    if kernel.startswith("k_td_level"):
+        # par CSR pairs (4+4) + offsets (8) + order (4) + row write+read (8+8) per rule
+        return 8 * Es + 8 * (R + 1) + 4 * R + 16 * R
+    if kernel.startswith("k_reduce_words"):
+        # (word, rule, freq) entries + each rule's row read once + dense output
+        return 12 * Eo + 8 * R + 8 * V
+    if kernel.startswith("k_popc"):
+        return 8 * V + 8 * V + V
+    return None
+
+
+def shard_ranges(tokens: np.ndarray, n: int):
+    """Token-balanced contiguous file ranges."""
+    F = len(tokens)
+    cum = np.concatenate([[0], np.cumsum(tokens)])
+    cuts = [0]
+    for k in range(1, n):
+        cuts.append(int(np.searchsorted(cum, cum[-1] * k / n)))
+    cuts.append(F)
+    cuts = np.maximum.accumulate(np.minimum(cuts, F))
+    return [(int(cuts[i]), int(cuts[i + 1])) for i in range(n)]
+
+
+def cpu_reference_steps(blob, steps, warmup, workers):
+    """The reference algorithm on host cores (oracle/ restatement)."""
+    from oracle.oracle import OracleDag
+    import paper_2106_06889_b200 as gt
+    t0 = time.perf_counter()
+    dag = OracleDag(blob, workers=workers)
+    init_s = time.perf_counter() - t0
+    cfg = gt.TraversalConfig()
+    times = []
+    for i in range(warmup + steps):
+        t = time.perf_counter()
+        for task in TASKS:
+            gt.run_compact(dag, task, cfg)
+        if i >= warmup:
+            times.append(time.perf_counter() - t)
+    # e2e: deserialize + build_dag + both tasks from host bytes
+    t = time.perf_counter()
+    d2 = OracleDag(blob, workers=workers)
+    for task in TASKS:
+        gt.run_compact(d2, task, cfg)
+    e2e_s = time.perf_counter() - t
+    return dag.info, times, init_s, e2e_s
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    blob, stats = composed(args)
+    cores = os.cpu_count() or 1
+    info, times, init_s, e2e_s = cpu_reference_steps(blob, args.steps, min(args.warmup, 1), cores)
+    W = info["words"]
+    t = statistics.mean(times)
+    line = {
+        "metric": METRIC, "value": W / t, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic (composed Zipfian grammar, seed 2)",
+        "config": {"workload": f"{args.config}: word count + inverted index", "scale": args.scale,
+                   "R": info["num_rules"], "E": info["total_elements"], "W": W,
+                   "F": info["num_files"], "V": info["num_words"], "depth": info["depth"],
+                   "rho": W / max(1, info["total_elements"])},
+        "cpu_baseline": {"value": W / t, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"whole {args.config} corpus, {args.steps} steps of wordcount+invertedindex"},
+        "e2e": {"value": W / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "init_ms": init_s * 1e3,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import paper_2106_06889_b200 as gt
+    from paper_2106_06889_b200.device import DeviceDag
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    blob, stats = composed(args)
+    # pinned host copy of the GTDC bytes (the e2e input)
+    pinned = torch.empty(len(blob), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = np.frombuffer(blob, dtype=np.uint8)
+    src = (pinned.data_ptr(), len(blob))
+
+    full = DeviceDag(src, device=local)
+    info_full = full.info
+    W_total = info_full["words"]
+    if world > 1:
+        toks = full.dag_array("segment_token_counts")
+        lo, hi = shard_ranges(toks, world)[rank]
+        full.close()
+        dag = DeviceDag(src, device=local, file_lo=lo, file_hi=hi)
+    else:
+        lo, hi = 0, info_full["num_files"]
+        dag = full
+    info = dag.info
+    V = info["num_words"]
+
+    counts_t = None
+    if world > 1:
+        class _CAI:  # __cuda_array_interface__ view of the library's dense counts
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<u8",
+                                                 "data": (ptr, False), "version": 3}
+
+    def step(collect=None):
+        dev_ms = 0.0
+        launches = 0
+        d2h = 0
+        for task in TASKS:
+            r, v = dag.run_raw(gt._abi.TASK_IDS[task])
+            dev_ms += v.device_ms
+            launches += v.kernel_launches
+            d2h += v.d2h_bytes
+            dag.free_raw(r)
+            if task == "wordcount" and world > 1:
+                ptr = dag.device_word_counts_ptr()
+                t = torch.as_tensor(_CAI(ptr, V), device="cuda").view(torch.int64)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                dist.all_reduce(t)
+                e1.record()
+                e1.synchronize()
+                dev_ms += e0.elapsed_time(e1)
+        return dev_ms, launches, d2h
+
+    if args.profile_only:
+        dag.profile(True)
+        step()
+        rep = dag.profile_report()
+        dag.profile(False)
+        for k, (n, ms) in sorted(rep.items(), key=lambda kv: -kv[1][1]):
+            print(f"{k:40s} {n:6d} {ms:10.4f} ms")
+        return
+
+    for _ in range(args.warmup):
+        step()
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the events)
+    step_ms, launches = [], 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            dag.flush_l2()
+            dag.sync()
+            ms, nl, d2h_wc_ii = step()
+            step_ms.append(ms)
+            launches += nl
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    tot_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([tot_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = tot_ms / args.steps
+    value = W_total / (ms_per_step / 1e3)
+
+    # ---- per-kernel profile (separate pass): dominant kernel + roofline
+    dag.flush_l2()
+    dag.sync()
+    dag.profile(True)
+    step()
+    rep = dag.profile_report()
+    dag.profile(False)
+    named = {k: v for k, v in rep.items() if alg_bytes(k, info, hi - lo) is not None}
+    peak, peak_src = peaks()
+    roof = None
+    if named:
+        k_dom = max(named, key=lambda k: named[k][1])
+        n_l, ms_l = named[k_dom]
+        b = alg_bytes(k_dom, info, hi - lo)
+        ach = b / (ms_l / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": k_dom, "launches_per_step": n_l,
+                "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": None, "alg_bytes_per_step": b, "kernel_ms_per_step": ms_l,
+                "peak_source": peak_src}
+    kernel_table = {k: {"launches": n, "ms": round(ms, 5)} for k, (n, ms) in
+                    sorted(rep.items(), key=lambda kv: -kv[1][1])[:12]}
+
+    # ---- e2e through the public C-ABI from pinned host bytes
+    e2e_times, d2h_bytes = [], 0
+    for i in range(max(2, min(args.steps, 5)) + 1):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d = DeviceDag(src, device=local, file_lo=lo, file_hi=hi) if world > 1 else DeviceDag(src, device=local)
+        nb = 0
+        for task in TASKS:
+            r, v = d.run_raw(gt._abi.TASK_IDS[task])
+            nb += v.d2h_bytes
+            d.free_raw(r)
+        d.close()
+        el = time.perf_counter() - t0
+        if i:
+            e2e_times.append(el)
+            d2h_bytes = nb
+    e2e_s = statistics.mean(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = info["total_elements"] * 4 + info["num_rules"] * 16 + 8
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        _, times, _, _ = cpu_reference_steps(blob, 3, 1, cores)
+        tc = statistics.mean(times)
+        cpu = {"value": W_total / tc, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"whole {args.config} corpus, 3 steps of wordcount+invertedindex (oracle/ C restatement)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (composed Zipfian grammar, seed 2; composer in paper_2106_06889_b200/corpus.py)",
+            "config": {"workload": f"{args.config}: word count + inverted index per step",
+                       "scale": args.scale, "l2": "flushed between steps (256 MiB memset)",
+                       "R": info_full["num_rules"], "E": info_full["total_elements"],
+                       "L0": info_full["root_len"], "E_sub": info_full["sub_pairs"],
+                       "E_own": info_full["own_pairs"], "W": W_total, "F": info_full["num_files"],
+                       "V": info_full["num_words"], "depth": info_full["depth"],
+                       "rho": W_total / max(1, info_full["total_elements"]),
+                       "parallelism": f"file-sharded x{world}"},
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": W_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": launches, "clocks": clk.summary(), "wall_s_timed_region": wall,
+            "init_ms": info["init_ms"], "kernels": kernel_table,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -162,6 +162,13 @@ uint64_t* gt_device_word_counts(gt_ctx* ctx);
  * size), or -1 on error. */
 int64_t gt_dag_array(gt_ctx* ctx, const char* name, int64_t* out, int64_t cap);
 
+/* Per-kernel timing: while enabled, every kernel launched by this thread is
+ * bracketed by CUDA events on its stream.  gt_profile_report writes
+ * "name\tlaunches\ttotal_ms\n" lines (aggregated by kernel name, since the
+ * last report) into buf and returns the length needed (or -1). */
+int gt_profile(gt_ctx* ctx, int enable);
+int64_t gt_profile_report(gt_ctx* ctx, char* buf, size_t cap);
+
 /* Evict L2 (writes a buffer larger than L2 on the context's stream). */
 int gt_flush_l2(gt_ctx* ctx);
 /* Synchronize the context's stream. */

@@ -1,0 +1,418 @@
+// api.cu — the C-ABI (include/gtadoc_b200.h) over the device DAG and kernels.
+//
+// gt_run mirrors tasks.py:171-185 run_task: strategy selection
+// (engine.py:63-71, tasks.py:47-56 hooks), the traversal + reduce on the
+// device, device-side result assembly in render order (tasks.py:122-168
+// sorting rules), and one D2H copy of the compact arrays into pinned host
+// memory owned by the gt_result.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gt_internal.cuh"
+#include "seq.cuh"
+#include "word.cuh"
+
+namespace gt {
+
+static thread_local std::string t_err;
+
+void set_last_error(const std::string& s) { t_err = s; }
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Error{code, buf};
+}
+
+// ---- per-kernel profiler -----------------------------------------------------
+thread_local Profiler g_prof;
+
+cudaEvent_t Profiler::get() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  GT_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+ProfScope::ProfScope(const char* name, cudaStream_t st) : s(st), on(g_prof.on) {
+  if (!on) return;
+  rec.name = name;
+  rec.a = g_prof.get();
+  rec.b = g_prof.get();
+  cudaEventRecord(rec.a, s);
+}
+
+ProfScope::~ProfScope() {
+  if (!on) return;
+  cudaEventRecord(rec.b, s);
+  g_prof.recs.push_back(rec);
+}
+
+// ---- pinned host memory pool (results own blocks until gt_result_free) ----
+namespace {
+std::mutex g_pool_mu;
+std::multimap<size_t, void*> g_pool;  // capacity -> block
+
+size_t size_class(size_t n) {
+  size_t c = 4096;
+  while (c < n) c <<= 1;
+  return c;
+}
+
+void* pinned_get(size_t n, size_t* cap) {
+  size_t c = size_class(n);
+  {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    auto it = g_pool.find(c);
+    if (it != g_pool.end()) {
+      void* p = it->second;
+      g_pool.erase(it);
+      *cap = c;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  GT_CUDA(cudaMallocHost(&p, c));
+  *cap = c;
+  return p;
+}
+
+void pinned_put(void* p, size_t cap) {
+  std::lock_guard<std::mutex> g(g_pool_mu);
+  g_pool.emplace(cap, p);
+}
+}  // namespace
+
+}  // namespace gt
+
+using namespace gt;
+
+struct gt_ctx {
+  DeviceDag d;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+struct gt_result {
+  gt_view v{};
+  std::vector<std::pair<void*, size_t>> blocks;
+  ~gt_result() {
+    for (auto& b : blocks) pinned_put(b.first, b.second);
+  }
+};
+
+template <class F>
+static int guard(F f) {
+  try {
+    f();
+    return GT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return GT_E_RESOURCE;
+  }
+}
+
+extern "C" {
+
+int gt_abi_version(void) { return GT_ABI_VERSION; }
+
+const char* gt_last_error(void) { return t_err.c_str(); }
+
+int gt_open(const uint8_t* gtdc, size_t nbytes, int device, uint64_t file_lo, uint64_t file_hi,
+            gt_ctx** out) {
+  *out = nullptr;
+  gt_ctx* c = new gt_ctx();
+  int st = guard([&] {
+    build_device_dag(gtdc, nbytes, device, file_lo, file_hi, &c->d);
+    for (auto& e : c->ev) GT_CUDA(cudaEventCreate(&e));
+  });
+  if (st != GT_OK) {
+    gt_close(c);
+    return st;
+  }
+  *out = c;
+  return GT_OK;
+}
+
+int gt_info_get(const gt_ctx* c, gt_info* o) {
+  memset(o, 0, sizeof *o);
+  const DeviceDag& d = c->d;
+  o->num_words = d.nw;
+  o->num_splitters = d.ns;
+  o->num_rules = d.R;
+  o->num_files = d.F;
+  o->total_elements = d.E;
+  o->root_len = d.L0;
+  o->sub_pairs = d.E_sub;
+  o->own_pairs = d.E_own;
+  o->words = d.W;
+  o->depth = d.depth;
+  o->td_levels = d.td.nl;
+  o->bu_levels = d.bu.nl > 0 ? d.bu.nl - 1 : 0;
+  size_t total = 0, free_b = 0;
+  cudaMemGetInfo(&free_b, &total);
+  o->device_bytes = 0;
+  o->init_ms = d.init_ms;
+  return GT_OK;
+}
+
+void gt_close(gt_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->d.device);
+  if (c->d.stream) cudaStreamSynchronize(c->d.stream);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  cudaStream_t s = c->d.stream;
+  delete c;  // DBuf destructors free on the stream
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+}
+
+}  // extern "C"
+
+static int select_strategy(const DeviceDag& d, int task, int requested, int fsw) {
+  if (requested == GT_TOPDOWN || requested == GT_BOTTOMUP) return requested;
+  bool needs_file_info = task >= GT_INVERTEDINDEX;
+  if (needs_file_info) return (i64)d.F > (i64)fsw ? GT_BOTTOMUP : GT_TOPDOWN;
+  return GT_TOPDOWN;
+}
+
+template <class T>
+static const T* pull(gt_result* r, const DBuf& b, u64 n, cudaStream_t st, u64* bytes) {
+  if (!b.p) return nullptr;
+  size_t cap;
+  size_t nb = n * sizeof(T);
+  void* h = pinned_get(nb ? nb : 8, &cap);
+  r->blocks.push_back({h, cap});
+  if (nb) GT_CUDA(cudaMemcpyAsync(h, b.p, nb, cudaMemcpyDeviceToHost, st));
+  *bytes += nb;
+  return (const T*)h;
+}
+
+extern "C" {
+
+int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, gt_result** out) {
+  *out = nullptr;
+  gt_result* r = new gt_result();
+  int status = guard([&] {
+    if (task < GT_WORDCOUNT || task > GT_RANKEDINVERTEDINDEX) fail(GT_E_USAGE, "unknown task %d", task);
+    if (strategy < GT_AUTO || strategy > GT_BOTTOMUP) fail(GT_E_USAGE, "unknown strategy %d", strategy);
+    if (task >= GT_SEQCOUNT && seq_len < 1) fail(GT_E_USAGE, "sequence length must be >= 1");
+    DeviceDag& d = c->d;
+    GT_CUDA(cudaSetDevice(d.device));
+    cudaStream_t st = d.stream;
+    auto t0 = std::chrono::steady_clock::now();
+    u64 launches0 = g_launches;
+    int strat = select_strategy(d, task, strategy, file_set_width);
+    GT_CUDA(cudaEventRecord(c->ev[0], st));
+    DevRecords R;
+    int wbits = 0;
+    const u32 Fo = (u32)(d.file_hi - d.file_lo);
+    switch (task) {
+      case GT_WORDCOUNT:
+      case GT_SORT: {
+        td_word_counts(&d, d.word_counts);
+        assemble_counts(&d, d.word_counts.as<u64>(), d.nw, 0, task == GT_SORT, &R);
+        strat = GT_TOPDOWN;
+        break;
+      }
+      case GT_TERMVECTOR: {
+        DBuf cnt;
+        td_file_counts(&d, cnt);
+        assemble_counts(&d, cnt.as<u64>(), d.nw, Fo, true, &R);
+        strat = GT_TOPDOWN;
+        break;
+      }
+      case GT_INVERTEDINDEX: {
+        DBuf pres;
+        u32 FW;
+        td_file_presence(&d, pres, &FW);
+        assemble_presence(&d, pres.as<u64>(), FW, &R);
+        strat = GT_TOPDOWN;
+        break;
+      }
+      default: {
+        run_sequences(&d, task, seq_len, &R, &wbits);
+        strat = GT_TOPDOWN;
+        break;
+      }
+    }
+    GT_CUDA(cudaEventRecord(c->ev[1], st));
+    u64 bytes = 0;
+    gt_view& v = r->v;
+    v.task = task;
+    v.seq_len = seq_len;
+    v.wbits = wbits;
+    v.strategy = strat;
+    v.n = R.n;
+    v.n_groups = R.n_groups;
+    const u64 l = (u64)seq_len;
+    v.group_off = pull<uint64_t>(r, R.group_off, R.n_groups + 1, st, &bytes);
+    v.group_id = pull<uint32_t>(r, R.group_id, R.n_groups, st, &bytes);
+    v.group_key = pull<uint64_t>(r, R.group_key, R.n_groups, st, &bytes);
+    v.group_gram = pull<uint32_t>(r, R.group_gram, R.n_groups * l, st, &bytes);
+    v.id = pull<uint32_t>(r, R.id, R.n, st, &bytes);
+    v.key = pull<uint64_t>(r, R.key, R.n, st, &bytes);
+    v.gram = pull<uint32_t>(r, R.gram, R.n * l, st, &bytes);
+    v.count = pull<uint64_t>(r, R.count, R.n, st, &bytes);
+    GT_CUDA(cudaEventRecord(c->ev[2], st));
+    GT_CUDA(cudaStreamSynchronize(st));
+    float ms = 0, ms2 = 0;
+    GT_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+    GT_CUDA(cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]));
+    v.device_ms = ms;
+    v.d2h_ms = ms2;
+    v.d2h_bytes = bytes;
+    v.kernel_launches = g_launches - launches0;
+    v.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  });
+  if (status != GT_OK) {
+    delete r;
+    return status;
+  }
+  *out = r;
+  return GT_OK;
+}
+
+int gt_result_view(const gt_result* r, gt_view* out) {
+  *out = r->v;
+  return GT_OK;
+}
+
+void gt_result_free(gt_result* r) { delete r; }
+
+uint64_t* gt_device_word_counts(gt_ctx* c) { return c->d.word_counts.as<uint64_t>(); }
+
+int gt_flush_l2(gt_ctx* c) {
+  return guard([&] {
+    static thread_local DBuf buf;
+    const size_t n = 256ull << 20;  // 256 MiB > 126 MB L2
+    if (buf.bytes < n) buf.alloc(n, c->d.stream);
+    GT_CUDA(cudaMemsetAsync(buf.p, (int)(g_launches & 0xFF), n, c->d.stream));
+  });
+}
+
+int gt_profile(gt_ctx* c, int enable) {
+  return guard([&] {
+    GT_CUDA(cudaStreamSynchronize(c->d.stream));
+    g_prof.on = enable != 0;
+  });
+}
+
+int64_t gt_profile_report(gt_ctx* c, char* buf, size_t cap) {
+  std::string text;
+  int st = guard([&] {
+    GT_CUDA(cudaStreamSynchronize(c->d.stream));
+    std::vector<std::pair<std::string, std::pair<u64, double>>> agg;
+    for (auto& r : g_prof.recs) {
+      float ms = 0;
+      GT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      auto it = std::find_if(agg.begin(), agg.end(), [&](auto& x) { return x.first == r.name; });
+      if (it == agg.end()) agg.push_back({r.name, {1, ms}});
+      else it->second.first++, it->second.second += ms;
+      g_prof.pool.push_back(r.a);
+      g_prof.pool.push_back(r.b);
+    }
+    g_prof.recs.clear();
+    char line[256];
+    for (auto& x : agg) {
+      snprintf(line, sizeof line, "%s\t%lu\t%.6f\n", x.first.c_str(), (unsigned long)x.second.first,
+               x.second.second);
+      text += line;
+    }
+  });
+  if (st != GT_OK) return -1;
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, text.size());
+    memcpy(buf, text.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)text.size() + 1;
+}
+
+int gt_sync(gt_ctx* c) {
+  return guard([&] { GT_CUDA(cudaStreamSynchronize(c->d.stream)); });
+}
+
+int64_t gt_dag_array(gt_ctx* c, const char* name, int64_t* out, int64_t cap) {
+  DeviceDag& d = c->d;
+  int64_t result = -1;
+  int st = guard([&] {
+    GT_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = d.stream;
+    std::string nm(name);
+    auto fetch32 = [&](const DBuf& b, u64 n) {
+      std::vector<int64_t> v(n);
+      std::vector<u32> t(n);
+      if (n) GT_CUDA(cudaMemcpyAsync(t.data(), b.p, n * 4, cudaMemcpyDeviceToHost, s));
+      GT_CUDA(cudaStreamSynchronize(s));
+      for (u64 i = 0; i < n; i++) v[i] = t[i];
+      return v;
+    };
+    auto fetch64 = [&](const DBuf& b, u64 n) {
+      std::vector<int64_t> v(n);
+      if (n) GT_CUDA(cudaMemcpyAsync(v.data(), b.p, n * 8, cudaMemcpyDeviceToHost, s));
+      GT_CUDA(cudaStreamSynchronize(s));
+      return v;
+    };
+    std::vector<int64_t> v;
+    if (nm == "own_ids") v = fetch32(d.own_ids, d.E_own);
+    else if (nm == "own_freqs") v = fetch32(d.own_freqs, d.E_own);
+    else if (nm == "own_off") v = fetch64(d.own_off, d.R + 1);
+    else if (nm == "own_token_count") v = fetch64(d.own_tok, d.R);
+    else if (nm == "sub_ids") v = fetch32(d.sub_ids, d.E_sub);
+    else if (nm == "sub_freqs") v = fetch32(d.sub_freqs, d.E_sub);
+    else if (nm == "sub_off") v = fetch64(d.sub_off, d.R + 1);
+    else if (nm == "par_ids") v = fetch32(d.par_ids, d.E_sub);
+    else if (nm == "par_freqs") v = fetch32(d.par_freqs, d.E_sub);
+    else if (nm == "par_off") v = fetch64(d.par_off, d.R + 1);
+    else if (nm == "num_in_edge") v = fetch64(d.num_in, d.R);
+    else if (nm == "num_out_edge") v = fetch64(d.num_out, d.R);
+    else if (nm == "exp_len") v = fetch64(d.exp_len, d.R);
+    else if (nm == "td_level") v = fetch32(d.td_level, d.R);
+    else if (nm == "bu_level") v = fetch32(d.bu_level, d.R);
+    else if (nm == "segment_token_counts") v = fetch64(d.seg_tokens, d.F);
+    else if (nm == "root_freq") {
+      auto so = fetch64(d.sub_off, 2);
+      auto ids = fetch32(d.sub_ids, d.E_sub);
+      auto fr = fetch32(d.sub_freqs, d.E_sub);
+      v.assign(d.R, 0);
+      for (int64_t j = so[0]; j < so[1]; j++) v[ids[j]] = fr[j];
+    } else if (nm == "segments") {
+      auto lo = fetch64(d.seg_lo, d.F), hi = fetch64(d.seg_hi, d.F);
+      for (u64 f = 0; f < d.F; f++) {
+        v.push_back(lo[f]);
+        v.push_back(hi[f]);
+      }
+    } else {
+      fail(GT_E_USAGE, "unknown DAG array %s", name);
+    }
+    result = (int64_t)v.size();
+    if (out) {
+      if (cap < result) fail(GT_E_USAGE, "buffer too small");
+      memcpy(out, v.data(), v.size() * 8);
+    }
+  });
+  return st == GT_OK ? result : -1;
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+// cub_ops.cu — device-wide sort/scan/select plumbing (CUB, CUDA 12.9 toolkit
+// headers, instantiated into this library).  Used by the DAG loader and by
+// the result-assembly steps; the analytics kernels themselves are ours.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "gt_internal.cuh"
+
+namespace gt {
+
+template <class F>
+static void with_temp(const char* name, F f, cudaStream_t s) {
+  size_t bytes = 0;
+  f(nullptr, bytes);
+  DBuf tmp(bytes ? bytes : 16, s);
+  ProfScope ps(name, s);
+  f(tmp.p, bytes);
+  g_launches += 4;  // CUB device-wide primitives launch a small fixed set of kernels
+}
+
+void sort_pairs_u64_u32(u64* ki, u64* ko, u32* vi, u32* vo, u64 n, int end_bit, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::SortPairs64", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceRadixSort::SortPairs(t, b, ki, ko, vi, vo, (int64_t)n, 0, end_bit, s));
+  }, s);
+}
+
+void sort_pairs_u32_u32(u32* ki, u32* ko, u32* vi, u32* vo, u64 n, int end_bit, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::SortPairs32", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceRadixSort::SortPairs(t, b, ki, ko, vi, vo, (int64_t)n, 0, end_bit, s));
+  }, s);
+}
+
+void sort_keys_u64(u64* ki, u64* ko, u64 n, int end_bit, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::SortKeys64", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceRadixSort::SortKeys(t, b, ki, ko, (int64_t)n, 0, end_bit, s));
+  }, s);
+}
+
+void exclusive_scan_u64(const u64* in, u64* out, u64 n, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::ExclusiveSum", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceScan::ExclusiveSum(t, b, in, out, (int64_t)n, s));
+  }, s);
+}
+
+void inclusive_scan_u32(const u32* in, u32* out, u64 n, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::InclusiveSum", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceScan::InclusiveSum(t, b, in, out, (int64_t)n, s));
+  }, s);
+}
+
+void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 n,
+                          cudaStream_t s) {
+  if (!n) {
+    GT_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u64), s));
+    return;
+  }
+  thrust::counting_iterator<u32> it(0);
+  with_temp("cub::SelectFlagged", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceSelect::Flagged(t, b, it, flags, out_idx, d_count, (int64_t)n, s));
+  }, s);
+}
+
+void reduce_max_u64(const u64* in, u64* out, u64 n, cudaStream_t s) {
+  if (!n) {
+    GT_CUDA(cudaMemsetAsync(out, 0, sizeof(u64), s));
+    return;
+  }
+  with_temp("cub::ReduceMax", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceReduce::Max(t, b, in, out, (int64_t)n, s));
+  }, s);
+}
+
+}  // namespace gt

@@ -1,0 +1,182 @@
+// gt_internal.cuh — shared definitions of libgtadoc_b200 (host + device).
+//
+// Device data layout (all device arrays are 4-byte ids/freqs and 8-byte
+// weights/counts; SURVEY.md §8(d) widths):
+//   body      u32[E]      rule bodies, root first (grammar.py bodies)
+//   boff      u64[R+1]    body offsets
+//   own_*     CSR by rule of distinct (word, freq)      (dag.py own_ids/own_freqs)
+//   sub_*     CSR by rule of distinct (child, freq)     (dag.py sub_ids/sub_freqs)
+//   par_*     CSR by rule of (parent asc, freq)         (dag.py par_ids/par_freqs)
+//   ow_*      own pairs transposed: sorted by (word, rule)  -> pull reduce
+//   rs_*      root occurrences per (rule, segment) sorted by rule -> per-file seeds
+//   rw_*      root word occurrences per (word, segment) sorted by word
+//   td_order  rules grouped by top-down level (engine.py round), light|heavy
+//   bu_order  rules grouped by bottom-up level (height+1)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gtadoc_b200.h"
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+typedef int64_t i64;
+
+namespace gt {
+
+// ---- errors ---------------------------------------------------------------
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...);
+void set_last_error(const std::string& s);
+
+#define GT_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      ::gt::fail(GT_E_DEVICE, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_),  \
+                 __FILE__, __LINE__, cudaGetErrorString(e_));                      \
+  } while (0)
+
+// ---- device buffers ---------------------------------------------------------
+
+// Stream-ordered device allocation (cudaMallocAsync from the device mempool).
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t n, cudaStream_t st) { alloc(n, st); }
+  void alloc(size_t n, cudaStream_t st);
+  void release();
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      s = o.s;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+// ---- the device DAG ---------------------------------------------------------
+
+struct Levels {
+  // rules grouped by level; within a level: light rules first, then heavy
+  DBuf order;                  // u32[n]
+  std::vector<u64> off;        // host: level L occupies [off[L], off[L+1]) (L=0..nl-1)
+  std::vector<u64> heavy_off;  // host: first heavy rule of level L
+  int nl = 0;
+};
+
+struct DeviceDag {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  u64 nw = 0, ns = 0, R = 0, E = 0, F = 0, L0 = 0, W = 0;
+  u64 file_lo = 0, file_hi = 0;  // owned file range (sharding)
+  i64 depth = 0;
+  DBuf body, boff;                     // u32[E], u64[R+1]
+  DBuf pos_owner;                      // u32[E] rule of each body position
+  DBuf root_seg;                       // u32[L0] segment of each root position
+  DBuf own_ids, own_freqs, own_off;    // u32, u32, u64[R+1]
+  DBuf own_tok;                        // u64[R]
+  DBuf sub_ids, sub_freqs, sub_off;    // u32, u32, u64[R+1]
+  DBuf par_ids, par_freqs, par_off;    // u32, u32, u64[R+1]
+  DBuf num_in, num_out, exp_len;       // u64[R]
+  DBuf td_level, bu_level;             // u32[R]
+  DBuf seg_lo, seg_hi, seg_tokens;     // u64[F]
+  DBuf ow_word, ow_rule, ow_freq;      // u32[E_own] sorted by (word, rule)
+  DBuf ow_off;                         // u64[V+1]
+  DBuf rs_rule, rs_seg, rs_cnt;        // root rule occurrences by (rule, seg)
+  DBuf rs_off;                         // u64[R+1]
+  DBuf rw_word, rw_seg, rw_cnt;        // root word occurrences by (word, seg)
+  u64 E_own = 0, E_sub = 0, n_rs = 0, n_rw = 0;
+  Levels td, bu;
+  double init_ms = 0;
+  // scratch kept across runs
+  DBuf word_counts;  // u64[V] of the last global run
+};
+
+// loader.cu
+void build_device_dag(const uint8_t* blob, size_t n, int device, u64 file_lo, u64 file_hi,
+                      DeviceDag* d);
+
+// cub_ops.cu (plumbing around CUB device-wide primitives)
+void sort_pairs_u64_u32(u64* keys_in, u64* keys_out, u32* vals_in, u32* vals_out, u64 n,
+                        int end_bit, cudaStream_t s);
+void sort_pairs_u32_u32(u32* keys_in, u32* keys_out, u32* vals_in, u32* vals_out, u64 n,
+                        int end_bit, cudaStream_t s);
+void sort_keys_u64(u64* keys_in, u64* keys_out, u64 n, int end_bit, cudaStream_t s);
+void exclusive_scan_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
+void inclusive_scan_u32(const u32* in, u32* out, u64 n, cudaStream_t s);
+// ordered compaction of indices i in [0,n) with flags[i] != 0; count -> d_count
+void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 n, cudaStream_t s);
+void reduce_max_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
+
+// launch bookkeeping
+extern thread_local u64 g_launches;
+
+// Optional per-kernel timing (gt_profile): CUDA events around every launch on
+// the launching stream; aggregated by kernel name in gt_profile_report.
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+struct Profiler {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get();
+};
+extern thread_local Profiler g_prof;
+struct ProfScope {
+  ProfRec rec{};
+  cudaStream_t s = nullptr;
+  bool on = false;
+  ProfScope(const char* name, cudaStream_t st);
+  ~ProfScope();
+};
+
+#define GT_KLAUNCH(name, kernel, grid, block, st, ...) \
+  do {                                                 \
+    ::gt::ProfScope ps_(name, st);                     \
+    kernel<<<(grid), (block), 0, (st)>>>(__VA_ARGS__); \
+    ::gt::g_launches++;                                \
+  } while (0)
+
+inline int bitlen(u64 v) {
+  int b = 0;
+  while (v) {
+    b++;
+    v >>= 1;
+  }
+  return b;
+}
+
+inline unsigned grid_for(u64 n, unsigned block, unsigned max_blocks = 148u * 16u) {
+  u64 g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (unsigned)g;
+}
+
+}  // namespace gt

@@ -1,0 +1,69 @@
+// kernels_common.cuh — device helpers shared by the loader and the task kernels.
+#pragma once
+
+#include "gt_internal.cuh"
+
+namespace gt {
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// off[r] = lower_bound(sorted_key, r) for r in [0, R]; sorted_key ascending.
+__global__ void k_csr_offsets(const u32* sorted_key, u64 n, u64 R, u64* off);
+
+__global__ void k_iota_u32(u32* out, u64 n);
+
+// out[key[i]] += val(i) for keys sorted ascending, warp-aggregated atomics
+// (at most one atomic per key run per warp).
+template <class ValF>
+__global__ void k_seg_sum_sorted(const u32* key, u64 n, ValF val, u64* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    u64 i = base + threadIdx.x;
+    bool ok = i < n;
+    u32 k = ok ? key[i] : 0xFFFFFFFFu;
+    u64 v = ok ? val(i) : 0;
+    unsigned lane = lane_id();
+    // segmented inclusive scan (run = equal consecutive keys)
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, d);
+      u32 ok2 = __shfl_up_sync(0xFFFFFFFFu, k, d);
+      if (lane >= (unsigned)d && ok2 == k) v += ov;
+    }
+    u32 nk = __shfl_down_sync(0xFFFFFFFFu, k, 1);
+    bool last = (lane == 31) || nk != k;
+    if (ok && last && v) atomicAdd((unsigned long long*)&out[k], (unsigned long long)v);
+  }
+}
+
+// Level-ordered pull:  out[r] = base(r) + sum_{e in CSR(r)} mult[e] * in[idx[e]]
+// light rules: one thread per rule; heavy rules: one warp per rule.
+template <class BaseF>
+__global__ void k_pull_sum(const u32* order, u64 lo, u64 mid, u64 hi, const u64* off,
+                           const u32* idx, const u32* mult, const u64* in, BaseF base, u64* out) {
+  u64 nlight = mid - lo;
+  u64 nlight_threads = nlight;
+  u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  u64 nthreads = (u64)gridDim.x * blockDim.x;
+  // light part
+  for (u64 t = gtid; t < nlight_threads; t += nthreads) {
+    u32 r = order[lo + t];
+    u64 s = base(r);
+    for (u64 e = off[r]; e < off[r + 1]; e++) s += (u64)mult[e] * in[idx[e]];
+    out[r] = s;
+  }
+  // heavy part: warp per rule
+  u64 nheavy = hi - mid;
+  u64 gwarp = gtid >> 5, nwarps = nthreads >> 5;
+  unsigned lane = lane_id();
+  for (u64 w = gwarp; w < nheavy; w += nwarps) {
+    u32 r = order[mid + w];
+    u64 s = 0;
+    for (u64 e = off[r] + lane; e < off[r + 1]; e += 32) s += (u64)mult[e] * in[idx[e]];
+#pragma unroll
+    for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, d);
+    if (lane == 0) out[r] = s + base(r);
+  }
+}
+
+}  // namespace gt

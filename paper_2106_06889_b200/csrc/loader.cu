@@ -1,0 +1,791 @@
+// loader.cu — GTDC -> device DAG (CSR arrays) + topological level scheduler.
+//
+// Replaces deserialize_grammar (grammar.py:193-228), build_dag
+// (dag.py:131-230) and the round discovery the reference's engine performs
+// every traversal (engine.py:196-227 top-down mask rounds, engine.py:313-335
+// bottom-up readiness rounds).  The host only walks the u32 length words (a
+// sequential chain) and validates the dictionary; everything proportional to
+// E runs on the device:
+//   unpack -> (rule,symbol) radix sort -> run-length encode -> own/sub CSR
+//   -> parent CSR (stable sort by child) -> per-rule sums
+//   -> bottom-up layering (Kahn from the leaves; = reference bottom-up rounds,
+//      doubles as the cycle check) -> top-down layering (Kahn over non-root
+//      in-edges; = reference top-down rounds; carries reachability)
+//   -> exp_len by bottom-up level -> root segments, segment tokens, root
+//      occurrence lists -> word-major transpose of the own pairs.
+// Error checks are reported in the reference's order and with its messages;
+// the exact rule named in a cycle message needs the reference's DFS order,
+// so only on that error path the host replays _topo_order (grammar.py:127).
+#include <stdarg.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+
+#include "kernels_common.cuh"
+
+namespace gt {
+
+thread_local u64 g_launches = 0;
+
+void DBuf::alloc(size_t n, cudaStream_t st) {
+  release();
+  s = st;
+  bytes = n;
+  if (n) GT_CUDA(cudaMallocAsync(&p, n, st));
+}
+
+void DBuf::release() {
+  if (p) cudaFreeAsync(p, s);
+  p = nullptr;
+  bytes = 0;
+}
+
+__global__ void k_csr_offsets(const u32* key, u64 n, u64 R, u64* off) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r <= R; r += stride) {
+    u64 lo = 0, hi = n;
+    while (lo < hi) {
+      u64 m = (lo + hi) >> 1;
+      if (key[m] < r) lo = m + 1;
+      else hi = m;
+    }
+    off[r] = lo;
+  }
+}
+
+__global__ void k_iota_u32(u32* out, u64 n) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = (u32)i;
+}
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// host parse (grammar.py:193-228 checks, same order and messages)
+// ---------------------------------------------------------------------------
+
+struct Parse {
+  u64 nw = 0, ns = 0, R = 0;
+  size_t rules_pos = 0;       // byte offset of the rules section
+  std::vector<u32> rstart;    // u32 index (within the section) of rule i's first symbol
+  std::vector<u64> boff;      // R+1 compact body offsets
+  u64 E = 0;
+  long trunc_rule = -1;       // first incomplete rule (error pending range checks)
+  std::string trunc_what;
+  u64 trailing = 0;
+};
+
+static u32 rd32(const uint8_t* p) {
+  u32 v;
+  memcpy(&v, p, 4);
+  return v;
+}
+
+static bool utf8_ok(const uint8_t* s, size_t n) {
+  size_t i = 0;
+  while (i < n) {
+    uint8_t c = s[i];
+    if (c < 0x80) {
+      i++;
+      continue;
+    }
+    int k;
+    uint8_t lo = 0x80, hi = 0xBF;
+    if (c >= 0xC2 && c <= 0xDF) k = 1;
+    else if (c == 0xE0) { k = 2; lo = 0xA0; }
+    else if (c >= 0xE1 && c <= 0xEC) k = 2;
+    else if (c == 0xED) { k = 2; hi = 0x9F; }
+    else if (c >= 0xEE && c <= 0xEF) k = 2;
+    else if (c == 0xF0) { k = 3; lo = 0x90; }
+    else if (c >= 0xF1 && c <= 0xF3) k = 3;
+    else if (c == 0xF4) { k = 3; hi = 0x8F; }
+    else return false;
+    if (i + (size_t)k >= n) return false;
+    if (s[i + 1] < lo || s[i + 1] > hi) return false;
+    for (int j = 2; j <= k; j++)
+      if (s[i + j] < 0x80 || s[i + j] > 0xBF) return false;
+    i += (size_t)k + 1;
+  }
+  return true;
+}
+
+static void parse_host(const uint8_t* d, size_t n, Parse* P) {
+  if (n < 4 || memcmp(d, "GTDC", 4) != 0) fail(GT_E_FORMAT, "bad magic: not a GTDC file");
+  size_t pos = 4;
+  auto need = [&](u64 k, const char* what, long idx) {
+    if ((u64)pos + k > (u64)n) {
+      char buf[96];
+      if (idx >= 0) snprintf(buf, sizeof buf, what, idx);
+      else snprintf(buf, sizeof buf, "%s", what);
+      fail(GT_E_FORMAT, "truncated input while reading %s", buf);
+    }
+  };
+  need(1, "version", -1);
+  uint8_t ver = d[pos++];
+  if (ver != 1) fail(GT_E_FORMAT, "unsupported version %d", (int)ver);
+  need(4, "word count", -1);
+  P->nw = rd32(d + pos), pos += 4;
+  need(4, "splitter count", -1);
+  P->ns = rd32(d + pos), pos += 4;
+  need(4, "rule count", -1);
+  P->R = rd32(d + pos), pos += 4;
+  if (P->R < 1) fail(GT_E_FORMAT, "grammar must contain a root rule");
+  for (u64 i = 0; i < P->nw; i++) {
+    need(4, "word %ld length", (long)i);
+    u32 ln = rd32(d + pos);
+    pos += 4;
+    need(ln, "word %ld", (long)i);
+    if (!utf8_ok(d + pos, ln)) fail(GT_E_FORMAT, "word %ld is not valid UTF-8", (long)i);
+    pos += ln;
+  }
+  P->rules_pos = pos;
+  P->rstart.resize(P->R);
+  P->boff.assign(P->R + 1, 0);
+  u64 E = 0;
+  for (u64 i = 0; i < P->R; i++) {
+    if ((u64)pos + 4 > (u64)n) {
+      P->trunc_rule = (long)i;
+      P->trunc_what = "rule %ld body length";
+      break;
+    }
+    u32 ln = rd32(d + pos);
+    if ((u64)pos + 4 + 4ull * ln > (u64)n) {
+      P->trunc_rule = (long)i;
+      P->trunc_what = "rule %ld body";
+      break;
+    }
+    P->rstart[i] = (u32)((pos + 4 - P->rules_pos) / 4);
+    E += ln;
+    P->boff[i + 1] = E;
+    pos += 4 + 4ull * ln;
+  }
+  if (P->trunc_rule < 0) P->trailing = (u64)n - (u64)pos;
+  P->E = E;
+}
+
+// range check of rules [0, upto) on the host: only used on error paths
+static void host_range_check(const uint8_t* d, const Parse& P, u64 upto) {
+  u64 limit = P.nw + P.ns + P.R;
+  const uint8_t* sec = d + P.rules_pos;
+  for (u64 i = 0; i < upto; i++) {
+    u64 lo = P.rstart[i], ln = P.boff[i + 1] - P.boff[i];
+    u32 mx = 0;
+    for (u64 j = 0; j < ln; j++) mx = std::max(mx, rd32(sec + 4 * (lo + j)));
+    if (ln && mx >= limit)
+      fail(GT_E_FORMAT, "rule %lu contains symbol %u out of range", (unsigned long)i, mx);
+  }
+}
+
+// _topo_order (grammar.py:127-161) replay for the cycle message only
+[[noreturn]] static void cycle_message(const uint8_t* d, const Parse& P) {
+  u64 R = P.R, base = P.nw + P.ns;
+  const uint8_t* sec = d + P.rules_pos;
+  std::vector<int8_t> state(R, 0);
+  std::vector<std::pair<u64, u64>> st;
+  for (u64 start = 0; start < R; start++) {
+    if (state[start]) continue;
+    st.clear();
+    st.push_back({start, 0});
+    state[start] = 1;
+    while (!st.empty()) {
+      auto [r, pos] = st.back();
+      st.pop_back();
+      u64 len = P.boff[r + 1] - P.boff[r];
+      bool adv = false;
+      while (pos < len) {
+        u64 s = rd32(sec + 4 * (P.rstart[r] + pos));
+        pos++;
+        if (s >= base) {
+          u64 c = s - base;
+          if (state[c] == 1) fail(GT_E_CORRUPTION, "rule reference cycle through rule %lu", (unsigned long)c);
+          if (state[c] == 0) {
+            st.push_back({r, pos});
+            st.push_back({c, 0});
+            state[c] = 1;
+            adv = true;
+            break;
+          }
+        }
+      }
+      if (!adv) state[r] = 2;
+    }
+  }
+  fail(GT_E_CORRUPTION, "rule reference cycle (not located)");
+}
+
+// ---------------------------------------------------------------------------
+// device kernels of the build
+// ---------------------------------------------------------------------------
+
+__global__ void k_mark_len(const u32* rstart, u64 R, u32* mark) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += stride)
+    mark[rstart[i] - 1] = 1;
+}
+
+__global__ void k_unpack(const u32* raw, const u32* mark, const u32* incl, u64 n, u32* body,
+                         u32* owner, u64 limit, u32* bad_rule) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+    if (mark[p]) continue;
+    u32 r = incl[p] - 1;
+    u64 i = p - ((u64)r + 1);
+    u32 s = raw[p];
+    body[i] = s;
+    owner[i] = r;
+    if ((u64)s >= limit) atomicMin(bad_rule, r);
+  }
+}
+
+__global__ void k_make_keys(const u32* body, const u32* owner, u64 E, int SB, u64* keys) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += stride)
+    keys[i] = ((u64)owner[i] << SB) | body[i];
+}
+
+__global__ void k_heads(const u64* k, u64 n, uint8_t* head) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    head[i] = (i == 0 || k[i] != k[i - 1]);
+}
+
+// unique (rule, sym) runs -> pair arrays + class flags
+__global__ void k_rle(const u64* sk, const u32* hidx, u64 U, u64 n, int SB, u64 nw, u64 base,
+                      u32* pr_rule, u32* pr_sym, u32* pr_cnt, uint8_t* is_own, uint8_t* is_sub) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 mask = (1ull << SB) - 1;
+  for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += stride) {
+    u64 a = hidx[u], b = (u + 1 < U) ? hidx[u + 1] : n;
+    u64 key = sk[a];
+    u64 sym = key & mask;
+    pr_rule[u] = (u32)(key >> SB);
+    pr_cnt[u] = (u32)(b - a);
+    is_own[u] = sym < nw;
+    is_sub[u] = sym >= base;
+    pr_sym[u] = (u32)(sym >= base ? sym - base : sym);
+  }
+}
+
+__global__ void k_gather3(const u32* idx, u64 n, const u32* a, const u32* b, const u32* c, u32* oa,
+                          u32* ob, u32* oc) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 j = idx[i];
+    oa[i] = a[j];
+    ob[i] = b[j];
+    if (c) oc[i] = c[j];
+  }
+}
+
+// distinct children / non-root parents counters; root-parent flag
+__global__ void k_degrees(const u64* sub_off, const u64* par_off, const u32* par_ids, u64 R,
+                          u32* rem_bu, u32* rem_td, uint8_t* root_parent) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
+    rem_bu[r] = (u32)(sub_off[r + 1] - sub_off[r]);
+    u64 np = par_off[r + 1] - par_off[r];
+    bool rp = np && par_ids[par_off[r]] == 0;
+    root_parent[r] = rp;
+    rem_td[r] = (u32)(np - (rp ? 1 : 0));
+  }
+}
+
+__global__ void k_flag_zero(const u32* rem, u64 R, u64 first, uint8_t* flag) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride)
+    flag[r] = (r >= first) && rem[r] == 0;
+}
+
+// bottom-up Kahn layer: frontier rules get `layer`; parents whose last child
+// finished join the next frontier
+__global__ void k_bu_layer(const u32* fr, const u64* fr_n, u32 layer, const u64* par_off,
+                           const u32* par_ids, u32* rem, u32* lvl, u32* next, u64* next_n) {
+  u64 n = *fr_n;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 r = fr[i];
+    lvl[r] = layer;
+    for (u64 e = par_off[r]; e < par_off[r + 1]; e++) {
+      u32 p = par_ids[e];
+      if (atomicSub(&rem[p], 1u) == 1u) next[atomicAdd((unsigned long long*)next_n, 1ull)] = p;
+    }
+  }
+}
+
+// top-down Kahn layer over non-root in-edges; reachability rides along
+__global__ void k_td_layer(const u32* fr, const u64* fr_n, u32 layer, const u64* par_off,
+                           const u32* par_ids, const uint8_t* root_parent, const u64* sub_off,
+                           const u32* sub_ids, u32* rem, u32* lvl, uint8_t* reach, u32* next,
+                           u64* next_n) {
+  u64 n = *fr_n;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 r = fr[i];
+    lvl[r] = layer;
+    bool rc = root_parent[r];
+    for (u64 e = par_off[r]; e < par_off[r + 1] && !rc; e++) {
+      u32 p = par_ids[e];
+      if (p != 0 && reach[p]) rc = true;
+    }
+    reach[r] = rc;
+    for (u64 e = sub_off[r]; e < sub_off[r + 1]; e++) {
+      u32 c = sub_ids[e];
+      if (atomicSub(&rem[c], 1u) == 1u) next[atomicAdd((unsigned long long*)next_n, 1ull)] = c;
+    }
+  }
+}
+
+__global__ void k_first_unreached(const uint8_t* reach, u64 R, u32* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = 1 + (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride)
+    if (!reach[r]) atomicMin(out, (u32)r);
+}
+
+// level sort key: level*2 + heavy (heavy = more than `th` CSR entries)
+__global__ void k_level_key(const u32* lvl, const u64* off, u64 R, u64 th, u32* key) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride)
+    key[r] = lvl[r] * 2u + ((off[r + 1] - off[r]) > th ? 1u : 0u);
+}
+
+// root body: splitter flags, per-position segment (inclusive scan later)
+__global__ void k_root_flags(const u32* body, u64 L0, u64 nw, u64 base, uint8_t* spl, u32* splu) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < L0; p += stride) {
+    u32 s = body[p];
+    bool f = s >= nw && s < base;
+    spl[p] = f;
+    splu[p] = f;
+  }
+}
+
+__global__ void k_check_splitters(const u32* body, const u32* spos, const u64* nspl, u64 nw,
+                                  u32* first_bad) {
+  u64 n = *nspl;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+    if ((u64)body[spos[k]] - nw != k) atomicMin(first_bad, (u32)k);
+}
+
+__global__ void k_segments(const u32* spos, u64 F, u64 L0, bool headless, u64* lo, u64* hi) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 f = (u64)blockIdx.x * blockDim.x + threadIdx.x; f < F; f += stride) {
+    if (headless) {
+      lo[f] = 0;
+      hi[f] = L0;
+    } else {
+      lo[f] = f ? (u64)spos[f - 1] + 1 : 0;
+      hi[f] = spos[f];
+    }
+  }
+}
+
+// root positions -> (rule|word, segment) keys; class flags
+__global__ void k_root_keys(const u32* body, const u32* seg_incl, u64 L0, u64 nw, u64 base,
+                            int SBF, bool headless, u64* rkey, uint8_t* isr, u64* wkey,
+                            uint8_t* isw, u32* seg_of) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < L0; p += stride) {
+    u32 s = body[p];
+    u32 seg = headless ? 0u : seg_incl[p];  // splitters before p (p itself not a splitter)
+    seg_of[p] = seg;
+    bool rr = s >= base, ww = s < nw;
+    isr[p] = rr;
+    isw[p] = ww;
+    rkey[p] = rr ? (((u64)(s - base) << SBF) | seg) : 0;
+    wkey[p] = ww ? (((u64)s << SBF) | seg) : 0;
+  }
+}
+
+// compacted sorted keys -> RLE (id, seg, cnt)
+__global__ void k_rle_keys(const u64* sk, const u32* hidx, u64 U, u64 n, int SBF, u32* id,
+                           u32* seg, u32* cnt) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += stride) {
+    u64 a = hidx[u], b = (u + 1 < U) ? hidx[u + 1] : n;
+    u64 k = sk[a];
+    id[u] = (u32)(k >> SBF);
+    seg[u] = (u32)(k & ((1ull << SBF) - 1));
+    cnt[u] = (u32)(b - a);
+  }
+}
+
+__global__ void k_gather_u64(const u32* idx, u64 n, const u64* src, u64* dst) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[idx[i]];
+}
+
+struct ValU32 {
+  const u32* a;
+  __device__ u64 operator()(u64 i) const { return a[i]; }
+};
+struct ValU32NonRoot {
+  const u32* a;
+  const u32* who;
+  __device__ u64 operator()(u64 i) const { return who[i] ? (u64)a[i] : 0ull; }
+};
+struct ValRootLen {
+  const u32* body;
+  const u64* exp_len;
+  u64 nw, base;
+  __device__ u64 operator()(u64 p) const {
+    u32 s = body[p];
+    return s < nw ? 1ull : (s >= base ? exp_len[s - base] : 0ull);
+  }
+};
+struct BaseArr {
+  const u64* a;
+  __device__ u64 operator()(u32 r) const { return a[r]; }
+};
+
+template <class T>
+static void d2h(T* dst, const void* src, size_t n, cudaStream_t s) {
+  GT_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  GT_CUDA(cudaStreamSynchronize(s));
+}
+
+#define LAUNCH(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
+
+// Kahn layering driver: returns number of layers and total processed
+template <class LayerFn>
+static int run_layers(DBuf& fr, DBuf& nx, DBuf& cnt, u64 first_n, u64 R, cudaStream_t st,
+                      LayerFn layer, u64* processed) {
+  u64 n = first_n, total = 0;
+  int L = 0;
+  while (n) {
+    L++;
+    total += n;
+    GT_CUDA(cudaMemsetAsync(cnt.as<u64>() + 1, 0, sizeof(u64), st));
+    layer((u32)L, n);
+    std::swap(fr, nx);
+    // move next count into slot 0
+    GT_CUDA(cudaMemcpyAsync(cnt.as<u64>(), cnt.as<u64>() + 1, sizeof(u64), cudaMemcpyDeviceToDevice, st));
+    d2h(&n, cnt.as<u64>(), 1, st);
+    if (L > (int)R + 2) break;
+  }
+  *processed = total;
+  return L;
+}
+
+static void build_levels(DeviceDag* d, const DBuf& lvl, const DBuf& off, u64 th, int nl, Levels* out) {
+  cudaStream_t st = d->stream;
+  u64 R = d->R;
+  DBuf key(R * 4, st), key2(R * 4, st), ids(R * 4, st);
+  out->order.alloc(R * 4, st);
+  LAUNCH(k_level_key, R, lvl.as<u32>(), off.as<u64>(), R, th, key.as<u32>());
+  LAUNCH(k_iota_u32, R, ids.as<u32>(), R);
+  sort_pairs_u32_u32(key.as<u32>(), key2.as<u32>(), ids.as<u32>(), out->order.as<u32>(), R,
+                     bitlen((u64)nl * 2 + 1), st);
+  // boundaries for keys 0..2*nl+1
+  u64 nk = (u64)nl * 2 + 2;
+  DBuf koff((nk + 1) * 8, st);
+  LAUNCH(k_csr_offsets, nk + 1, key2.as<u32>(), R, nk, koff.as<u64>());
+  std::vector<u64> h(nk + 1);
+  d2h(h.data(), koff.p, nk + 1, st);
+  out->nl = nl;
+  out->off.assign(nl + 2, 0);
+  out->heavy_off.assign(nl + 2, 0);
+  for (int L = 0; L <= nl; L++) {
+    out->off[L] = h[2 * L];
+    out->heavy_off[L] = h[2 * L + 1];
+  }
+  out->off[nl + 1] = R;
+}
+
+}  // namespace
+
+void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_lo, u64 file_hi,
+                      DeviceDag* d) {
+  auto t0 = std::chrono::steady_clock::now();
+  Parse P;
+  parse_host(blob, nbytes, &P);
+  if (P.trunc_rule >= 0) {
+    host_range_check(blob, P, (u64)P.trunc_rule);
+    char buf[96];
+    snprintf(buf, sizeof buf, P.trunc_what.c_str(), P.trunc_rule);
+    fail(GT_E_FORMAT, "truncated input while reading %s", buf);
+  }
+  if (P.trailing) {
+    host_range_check(blob, P, P.R);
+    fail(GT_E_FORMAT, "%lu trailing bytes after rules section", (unsigned long)P.trailing);
+  }
+  GT_CUDA(cudaSetDevice(device));
+  d->device = device;
+  if (!d->stream) GT_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  cudaStream_t st = d->stream;
+  {
+    cudaMemPool_t pool;
+    GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    u64 thr = UINT64_MAX;
+    GT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  const u64 R = P.R, E = P.E, nw = P.nw, ns = P.ns, base = nw + ns, limit = nw + ns + R;
+  d->nw = nw;
+  d->ns = ns;
+  d->R = R;
+  d->E = E;
+  const u64 nraw = E + R;
+
+  // ---- upload + unpack --------------------------------------------------
+  DBuf raw(nraw * 4 + 4, st), rstart(R * 4, st), mark(nraw * 4 + 4, st), incl(nraw * 4 + 4, st);
+  DBuf& owner = d->pos_owner;
+  owner.alloc(E * 4 + 4, st);
+  DBuf bad(4, st);
+  d->body.alloc(E * 4 + 4, st);
+  d->boff.alloc((R + 1) * 8, st);
+  GT_CUDA(cudaMemcpyAsync(raw.p, blob + P.rules_pos, nraw * 4, cudaMemcpyHostToDevice, st));
+  GT_CUDA(cudaMemcpyAsync(rstart.p, P.rstart.data(), R * 4, cudaMemcpyHostToDevice, st));
+  GT_CUDA(cudaMemcpyAsync(d->boff.p, P.boff.data(), (R + 1) * 8, cudaMemcpyHostToDevice, st));
+  GT_CUDA(cudaMemsetAsync(mark.p, 0, nraw * 4, st));
+  GT_CUDA(cudaMemsetAsync(bad.p, 0xFF, 4, st));
+  LAUNCH(k_mark_len, R, rstart.as<u32>(), R, mark.as<u32>());
+  inclusive_scan_u32(mark.as<u32>(), incl.as<u32>(), nraw, st);
+  LAUNCH(k_unpack, nraw, raw.as<u32>(), mark.as<u32>(), incl.as<u32>(), nraw, d->body.as<u32>(),
+         owner.as<u32>(), limit, bad.as<u32>());
+  raw.release();
+  mark.release();
+  incl.release();
+  rstart.release();
+  u32 bad_rule;
+  d2h(&bad_rule, bad.p, 1, st);
+  if (bad_rule != 0xFFFFFFFFu) host_range_check(blob, P, bad_rule + 1);
+
+  // ---- (rule, symbol) sort + RLE -> own / sub CSR ----------------------
+  const int SB = std::max(1, bitlen(limit - 1));
+  const int KB = SB + std::max(1, bitlen(R - 1));
+  DBuf keys(E * 8 + 8, st), skeys(E * 8 + 8, st);
+  LAUNCH(k_make_keys, E, d->body.as<u32>(), owner.as<u32>(), E, SB, keys.as<u64>());
+  sort_keys_u64(keys.as<u64>(), skeys.as<u64>(), E, KB, st);
+  keys.release();
+  DBuf head(E + 1, st), hidx(E * 4 + 4, st), cnt(16, st);
+  LAUNCH(k_heads, E, skeys.as<u64>(), E, head.as<uint8_t>());
+  select_flagged_index(head.as<uint8_t>(), hidx.as<u32>(), cnt.as<u64>(), E, st);
+  u64 U;
+  d2h(&U, cnt.p, 1, st);
+  DBuf pr_rule(U * 4 + 4, st), pr_sym(U * 4 + 4, st), pr_cnt(U * 4 + 4, st);
+  DBuf is_own(U + 1, st), is_sub(U + 1, st);
+  LAUNCH(k_rle, U, skeys.as<u64>(), hidx.as<u32>(), U, E, SB, nw, base, pr_rule.as<u32>(),
+         pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
+  skeys.release();
+  head.release();
+  DBuf sel(U * 4 + 4, st);
+  // own pairs
+  select_flagged_index(is_own.as<uint8_t>(), sel.as<u32>(), cnt.as<u64>(), U, st);
+  d2h(&d->E_own, cnt.p, 1, st);
+  const u64 Eo = d->E_own;
+  DBuf own_rule(Eo * 4 + 4, st);
+  d->own_ids.alloc(Eo * 4 + 4, st);
+  d->own_freqs.alloc(Eo * 4 + 4, st);
+  LAUNCH(k_gather3, Eo, sel.as<u32>(), Eo, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
+         own_rule.as<u32>(), d->own_ids.as<u32>(), d->own_freqs.as<u32>());
+  // sub pairs
+  select_flagged_index(is_sub.as<uint8_t>(), sel.as<u32>(), cnt.as<u64>(), U, st);
+  d2h(&d->E_sub, cnt.p, 1, st);
+  const u64 Es = d->E_sub;
+  DBuf sub_rule(Es * 4 + 4, st);
+  d->sub_ids.alloc(Es * 4 + 4, st);
+  d->sub_freqs.alloc(Es * 4 + 4, st);
+  LAUNCH(k_gather3, Es, sel.as<u32>(), Es, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
+         sub_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>());
+  pr_rule.release();
+  pr_sym.release();
+  pr_cnt.release();
+  is_own.release();
+  is_sub.release();
+  sel.release();
+  hidx.release();
+  d->own_off.alloc((R + 1) * 8, st);
+  d->sub_off.alloc((R + 1) * 8, st);
+  LAUNCH(k_csr_offsets, R + 1, own_rule.as<u32>(), Eo, R, d->own_off.as<u64>());
+  LAUNCH(k_csr_offsets, R + 1, sub_rule.as<u32>(), Es, R, d->sub_off.as<u64>());
+
+  // ---- parents: stable sort of sub pairs by child -------------------------
+  DBuf idx(Es * 4 + 4, st), sidx(Es * 4 + 4, st), child_sorted(Es * 4 + 4, st);
+  LAUNCH(k_iota_u32, Es, idx.as<u32>(), Es);
+  sort_pairs_u32_u32(d->sub_ids.as<u32>(), child_sorted.as<u32>(), idx.as<u32>(), sidx.as<u32>(), Es,
+                     std::max(1, bitlen(R - 1)), st);
+  d->par_ids.alloc(Es * 4 + 4, st);
+  d->par_freqs.alloc(Es * 4 + 4, st);
+  d->par_off.alloc((R + 1) * 8, st);
+  LAUNCH(k_gather3, Es, sidx.as<u32>(), Es, sub_rule.as<u32>(), d->sub_freqs.as<u32>(),
+         (const u32*)nullptr, d->par_ids.as<u32>(), d->par_freqs.as<u32>(), (u32*)nullptr);
+  LAUNCH(k_csr_offsets, R + 1, child_sorted.as<u32>(), Es, R, d->par_off.as<u64>());
+  idx.release();
+  sidx.release();
+
+  // ---- per-rule sums -------------------------------------------------------
+  d->own_tok.alloc(R * 8, st);
+  d->num_out.alloc(R * 8, st);
+  d->num_in.alloc(R * 8, st);
+  GT_CUDA(cudaMemsetAsync(d->own_tok.p, 0, R * 8, st));
+  GT_CUDA(cudaMemsetAsync(d->num_out.p, 0, R * 8, st));
+  GT_CUDA(cudaMemsetAsync(d->num_in.p, 0, R * 8, st));
+  LAUNCH(k_seg_sum_sorted, Eo, own_rule.as<u32>(), Eo, ValU32{d->own_freqs.as<u32>()}, d->own_tok.as<u64>());
+  LAUNCH(k_seg_sum_sorted, Es, sub_rule.as<u32>(), Es, ValU32{d->sub_freqs.as<u32>()}, d->num_out.as<u64>());
+  LAUNCH(k_seg_sum_sorted, Es, child_sorted.as<u32>(), Es,
+         (ValU32NonRoot{d->par_freqs.as<u32>(), d->par_ids.as<u32>()}), d->num_in.as<u64>());
+  sub_rule.release();
+  child_sorted.release();
+
+  // ---- bottom-up layering (cycle check) then top-down layering -----------
+  DBuf rem_bu(R * 4, st), rem_td(R * 4, st), rootp(R, st), flag(R, st);
+  DBuf fr(R * 4 + 4, st), nx(R * 4 + 4, st), fcnt(16, st);
+  d->bu_level.alloc(R * 4, st);
+  d->td_level.alloc(R * 4, st);
+  GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, R * 4, st));
+  GT_CUDA(cudaMemsetAsync(d->td_level.p, 0, R * 4, st));
+  LAUNCH(k_degrees, R, d->sub_off.as<u64>(), d->par_off.as<u64>(), d->par_ids.as<u32>(), R,
+         rem_bu.as<u32>(), rem_td.as<u32>(), rootp.as<uint8_t>());
+  LAUNCH(k_flag_zero, R, rem_bu.as<u32>(), R, 0, flag.as<uint8_t>());
+  select_flagged_index(flag.as<uint8_t>(), fr.as<u32>(), fcnt.as<u64>(), R, st);
+  u64 n0;
+  d2h(&n0, fcnt.p, 1, st);
+  u64 processed = 0;
+  int nbu = run_layers(fr, nx, fcnt, n0, R, st, [&](u32 L, u64 n) {
+    k_bu_layer<<<grid_for(n, 256), 256, 0, st>>>(fr.as<u32>(), fcnt.as<u64>(), L,
+                                                 d->par_off.as<u64>(), d->par_ids.as<u32>(),
+                                                 rem_bu.as<u32>(), d->bu_level.as<u32>(),
+                                                 nx.as<u32>(), fcnt.as<u64>() + 1);
+    g_launches++;
+  }, &processed);
+  if (processed < R) cycle_message(blob, P);
+  // depth = height(root) = layer(root) - 1; reference bu_level excludes root
+  u32 root_layer;
+  d2h(&root_layer, d->bu_level.p, 1, st);
+  d->depth = (i64)root_layer - 1;
+  DBuf reach(R, st), firstu(4, st);
+  GT_CUDA(cudaMemsetAsync(reach.p, 0, R, st));
+  LAUNCH(k_flag_zero, R, rem_td.as<u32>(), R, 1, flag.as<uint8_t>());
+  select_flagged_index(flag.as<uint8_t>(), fr.as<u32>(), fcnt.as<u64>(), R, st);
+  d2h(&n0, fcnt.p, 1, st);
+  int ntd = run_layers(fr, nx, fcnt, n0, R, st, [&](u32 L, u64 n) {
+    k_td_layer<<<grid_for(n, 256), 256, 0, st>>>(fr.as<u32>(), fcnt.as<u64>(), L,
+                                                 d->par_off.as<u64>(), d->par_ids.as<u32>(),
+                                                 rootp.as<uint8_t>(), d->sub_off.as<u64>(),
+                                                 d->sub_ids.as<u32>(), rem_td.as<u32>(),
+                                                 d->td_level.as<u32>(), reach.as<uint8_t>(),
+                                                 nx.as<u32>(), fcnt.as<u64>() + 1);
+    g_launches++;
+  }, &processed);
+  GT_CUDA(cudaMemsetAsync(firstu.p, 0xFF, 4, st));
+  LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, firstu.as<u32>());
+  u32 fu;
+  d2h(&fu, firstu.p, 1, st);
+  if (fu != 0xFFFFFFFFu) fail(GT_E_CORRUPTION, "rule %u is not reachable from the root", fu);
+  rem_bu.release();
+  rem_td.release();
+  fr.release();
+  nx.release();
+
+  // level-ordered rule lists (light/heavy split)
+  build_levels(d, d->bu_level, d->sub_off, 16, nbu, &d->bu);
+  build_levels(d, d->td_level, d->par_off, 16, ntd, &d->td);
+  // the reference's bottom-up rounds exclude the root (engine.py:305-310)
+  GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
+
+  // ---- root segments (dag.py:107-128) -------------------------------------
+  const u64 L0 = P.boff[1] - P.boff[0];
+  d->L0 = L0;
+  const bool headless = ns == 0;
+  DBuf spl(L0 + 1, st), splu(L0 * 4 + 4, st), sincl(L0 * 4 + 4, st), spos(L0 * 4 + 4, st);
+  LAUNCH(k_root_flags, L0, d->body.as<u32>(), L0, nw, base, spl.as<uint8_t>(), splu.as<u32>());
+  select_flagged_index(spl.as<uint8_t>(), spos.as<u32>(), cnt.as<u64>(), L0, st);
+  inclusive_scan_u32(splu.as<u32>(), sincl.as<u32>(), L0, st);
+  u64 nspl;
+  d2h(&nspl, cnt.p, 1, st);
+  if (!headless) {
+    DBuf fb(4, st);
+    GT_CUDA(cudaMemsetAsync(fb.p, 0xFF, 4, st));
+    LAUNCH(k_check_splitters, nspl ? nspl : 1, d->body.as<u32>(), spos.as<u32>(), cnt.as<u64>(), nw,
+           fb.as<u32>());
+    u32 k;
+    d2h(&k, fb.p, 1, st);
+    if (k != 0xFFFFFFFFu) {
+      u32 pos, sym;
+      d2h(&pos, spos.as<u32>() + k, 1, st);
+      d2h(&sym, d->body.as<u32>() + pos, 1, st);
+      fail(GT_E_CORRUPTION, "splitter %u out of order at root position %u", sym, pos);
+    }
+    if (nspl != ns) fail(GT_E_CORRUPTION, "root body is missing file splitters");
+    u32 last = 0;
+    if (nspl) d2h(&last, spos.as<u32>() + nspl - 1, 1, st);
+    if (!nspl || (u64)last + 1 != L0) fail(GT_E_CORRUPTION, "root body has content after the last splitter");
+  }
+  const u64 F = headless ? 1 : ns;
+  d->F = F;
+  d->file_lo = std::min(file_lo, F);
+  d->file_hi = std::min(file_hi, F);
+  if (d->file_hi < d->file_lo) d->file_hi = d->file_lo;
+  d->seg_lo.alloc(F * 8, st);
+  d->seg_hi.alloc(F * 8, st);
+  LAUNCH(k_segments, F, spos.as<u32>(), F, L0, headless, d->seg_lo.as<u64>(), d->seg_hi.as<u64>());
+
+  // ---- exp_len by bottom-up level (grammar.py:109-124) --------------------
+  d->exp_len.alloc(R * 8, st);
+  for (int L = 1; L <= d->bu.nl; L++) {
+    u64 lo = d->bu.off[L], mid = d->bu.heavy_off[L], hi = d->bu.off[L + 1];
+    if (hi == lo) continue;
+    u64 work = (mid - lo) + (hi - mid) * 32;
+    k_pull_sum<<<grid_for(work, 256), 256, 0, st>>>(d->bu.order.as<u32>(), lo, mid, hi,
+                                                     d->sub_off.as<u64>(), d->sub_ids.as<u32>(),
+                                                     d->sub_freqs.as<u32>(), d->exp_len.as<u64>(),
+                                                     BaseArr{d->own_tok.as<u64>()},
+                                                     d->exp_len.as<u64>());
+    g_launches++;
+  }
+  d2h(&d->W, d->exp_len.p, 1, st);
+
+  // ---- segment tokens + root occurrence lists ------------------------------
+  const int SBF = std::max(1, bitlen(F - 1));
+  DBuf rkey(L0 * 8 + 8, st), wkey(L0 * 8 + 8, st), isr(L0 + 1, st), isw(L0 + 1, st);
+  DBuf& segof = d->root_seg;
+  segof.alloc(L0 * 4 + 4, st);
+  LAUNCH(k_root_keys, L0, d->body.as<u32>(), sincl.as<u32>(), L0, nw, base, SBF, headless,
+         rkey.as<u64>(), isr.as<uint8_t>(), wkey.as<u64>(), isw.as<uint8_t>(), segof.as<u32>());
+  d->seg_tokens.alloc(F * 8, st);
+  GT_CUDA(cudaMemsetAsync(d->seg_tokens.p, 0, F * 8, st));
+  LAUNCH(k_seg_sum_sorted, L0, segof.as<u32>(), L0,
+         (ValRootLen{d->body.as<u32>(), d->exp_len.as<u64>(), nw, base}), d->seg_tokens.as<u64>());
+  auto occ_list = [&](DBuf& key, DBuf& is, int idbits, DBuf& oid, DBuf& oseg, DBuf& ocnt, u64* nout) {
+    DBuf sidx2(L0 * 4 + 4, st), k2(L0 * 8 + 8, st), k3(L0 * 8 + 8, st), h2(L0 + 1, st), hi2(L0 * 4 + 4, st);
+    select_flagged_index(is.as<uint8_t>(), sidx2.as<u32>(), cnt.as<u64>(), L0, st);
+    u64 m;
+    d2h(&m, cnt.p, 1, st);
+    LAUNCH(k_gather_u64, m, sidx2.as<u32>(), m, key.as<u64>(), k2.as<u64>());
+    sort_keys_u64(k2.as<u64>(), k3.as<u64>(), m, idbits + SBF, st);
+    LAUNCH(k_heads, m, k3.as<u64>(), m, h2.as<uint8_t>());
+    select_flagged_index(h2.as<uint8_t>(), hi2.as<u32>(), cnt.as<u64>(), m, st);
+    u64 u;
+    d2h(&u, cnt.p, 1, st);
+    oid.alloc(u * 4 + 4, st);
+    oseg.alloc(u * 4 + 4, st);
+    ocnt.alloc(u * 4 + 4, st);
+    LAUNCH(k_rle_keys, u, k3.as<u64>(), hi2.as<u32>(), u, m, SBF, oid.as<u32>(), oseg.as<u32>(),
+           ocnt.as<u32>());
+    *nout = u;
+  };
+  occ_list(rkey, isr, std::max(1, bitlen(R - 1)), d->rs_rule, d->rs_seg, d->rs_cnt, &d->n_rs);
+  occ_list(wkey, isw, std::max(1, bitlen(nw ? nw - 1 : 0)), d->rw_word, d->rw_seg, d->rw_cnt, &d->n_rw);
+  d->rs_off.alloc((R + 1) * 8, st);
+  LAUNCH(k_csr_offsets, R + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
+
+  // ---- word-major transpose of the own pairs --------------------------------
+  {
+    DBuf id2(Eo * 4 + 4, st), sid(Eo * 4 + 4, st);
+    d->ow_word.alloc(Eo * 4 + 4, st);
+    d->ow_rule.alloc(Eo * 4 + 4, st);
+    d->ow_freq.alloc(Eo * 4 + 4, st);
+    d->ow_off.alloc((nw + 1) * 8, st);
+    LAUNCH(k_iota_u32, Eo, id2.as<u32>(), Eo);
+    sort_pairs_u32_u32(d->own_ids.as<u32>(), d->ow_word.as<u32>(), id2.as<u32>(), sid.as<u32>(), Eo,
+                       std::max(1, bitlen(nw ? nw - 1 : 0)), st);
+    LAUNCH(k_gather3, Eo, sid.as<u32>(), Eo, own_rule.as<u32>(), d->own_freqs.as<u32>(),
+           (const u32*)nullptr, d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), (u32*)nullptr);
+    LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
+  }
+  GT_CUDA(cudaStreamSynchronize(st));
+  d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace gt

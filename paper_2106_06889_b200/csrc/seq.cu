@@ -1,0 +1,414 @@
+// seq.cu — l-gram counting per file on the device DAG (sequence_count /
+// ranked_inverted_index).
+//
+// Reference (sequence.py:50-417, _kernels.py:279-309): per-rule head/tail
+// buffers of l-1 words (Fig. 6), local streams that inline children as
+// absorbed / owned span / head|GAP|tail (Fig. 7), windows counted once per
+// rule into hash tables, then scaled merges into per-file tables.
+//
+// B200 formulation, same exactly-once attribution: a window of rule r's
+// expansion belongs to r iff it is not inside one child's expansion, i.e.
+// it starts at a word symbol of r's body or inside the last min(l-1, |c|)
+// words (the tail) of a child c, and completes within r's body before a
+// splitter.  One thread per body position enumerates those windows directly
+// from the tail of its own symbol and the heads of the following symbols —
+// no local streams are materialised.  Counting is sort-based instead of
+// hashing: window keys (packed big-endian, l*wbits <= 63, else l word ids)
+// are radix-sorted with their source (rule, or root segment), each key run
+// is reduced against the per-file weight rows (F columns, from the same
+// top-down level pull as term vectors), and the nonzero (gram, file, count)
+// records are ordered for render with two stable radix sorts.
+#include <algorithm>
+
+#include "kernels_common.cuh"
+#include "seq.cuh"
+
+namespace gt {
+
+namespace {
+
+// heads/tails for the rules of one bottom-up level (children are finished)
+__global__ void k_head_tail(const u32* order, u64 lo, u64 hi, const u32* __restrict__ body,
+                            const u64* __restrict__ boff, u64 nw, u64 base,
+                            const u64* __restrict__ exp_len, u32 m, u32* H, u32* T, u32* hl,
+                            u32* tl) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = lo + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
+    const u32 r = order[i];
+    if (r == 0) continue;
+    const u64 el = exp_len[r];
+    const u32 target = (u32)(el < m ? el : m);
+    u32 n = 0;
+    for (u64 q = boff[r]; q < boff[r + 1] && n < target; q++) {
+      u32 s = body[q];
+      if (s < nw) H[(u64)r * m + n++] = s;
+      else if (s >= base) {
+        u32 c = s - (u32)base;
+        for (u32 j = 0; j < hl[c] && n < target; j++) H[(u64)r * m + n++] = H[(u64)c * m + j];
+      }
+    }
+    hl[r] = target;
+    n = 0;
+    for (u64 q = boff[r + 1]; q > boff[r] && n < target; q--) {
+      u32 s = body[q - 1];
+      if (s < nw) T[(u64)r * m + (target - 1 - n++)] = s;
+      else if (s >= base) {
+        u32 c = s - (u32)base;
+        for (u32 j = tl[c]; j > 0 && n < target; j--) T[(u64)r * m + (target - 1 - n++)] = T[(u64)c * m + j - 1];
+      }
+    }
+    tl[r] = target;
+  }
+}
+
+struct WinCtx {
+  const u32* body;
+  const u32* owner;
+  const u64* boff;
+  const u32* root_seg;
+  const u32 *H, *T, *hl, *tl;
+  u64 nw, base;
+  u32 l, m, wbits, R, file_lo, nseg;
+};
+
+// number of windows attributed at body position p, plus its source id
+__device__ __forceinline__ u32 windows_at(const WinCtx& c, u64 p, u32* src, u32* tail_len,
+                                          u32* start_sym) {
+  const u32 r = c.owner[p];
+  if (r == 0) {
+    u32 sg = c.root_seg[p] - c.file_lo;
+    if (sg >= c.nseg) return 0;
+    *src = c.R + sg;
+  } else {
+    *src = r;
+  }
+  const u32 s = c.body[p];
+  u32 tlen;
+  if (s < c.nw) tlen = 1;
+  else if (s >= c.base) tlen = c.tl[s - (u32)c.base];
+  else return 0;  // splitter
+  *tail_len = tlen;
+  *start_sym = s;
+  if (tlen == 0) return 0;
+  // words available after p within the body (up to l-1, stop at a splitter)
+  u32 avail = 0;
+  const u64 end = c.boff[r + 1];
+  for (u64 q = p + 1; q < end && avail < c.m; q++) {
+    u32 t = c.body[q];
+    if (t < c.nw) avail++;
+    else if (t >= c.base) avail += c.hl[t - (u32)c.base];
+    else break;
+  }
+  if (avail > c.m) avail = c.m;
+  // start t in [0, tlen) succeeds iff (tlen - t) + avail >= l
+  i64 hi = (i64)tlen + (i64)avail - (i64)c.l;  // last successful t
+  if (hi < 0) return 0;
+  return (u32)std::min<i64>(tlen, hi + 1);
+}
+
+// word j of window starting at tail index t of the symbol at p
+template <class Put>
+__device__ __forceinline__ void window_words(const WinCtx& c, u64 p, u32 s, u32 tlen, u32 t, Put put) {
+  u32 j = 0;
+  if (s < c.nw) put(j++, s);
+  else {
+    const u32* T = c.T + (u64)(s - (u32)c.base) * c.m;
+    for (u32 k = t; k < tlen; k++) put(j++, T[k]);
+  }
+  for (u64 q = p + 1; j < c.l; q++) {
+    u32 x = c.body[q];
+    if (x < c.nw) put(j++, x);
+    else if (x >= c.base) {
+      const u32 cc = x - (u32)c.base;
+      const u32* H = c.H + (u64)cc * c.m;
+      for (u32 k = 0; k < c.hl[cc] && j < c.l; k++) put(j++, H[k]);
+    }
+  }
+}
+
+__global__ void k_count_windows(WinCtx c, u64 E, u64* cnt) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += stride) {
+    u32 src, tlen, s;
+    cnt[p] = windows_at(c, p, &src, &tlen, &s);
+  }
+}
+
+__global__ void k_write_windows(WinCtx c, u64 E, const u64* off, int packed, u64* key, u32* gram,
+                                u32* srcs) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += stride) {
+    u32 src, tlen, s;
+    u32 n = windows_at(c, p, &src, &tlen, &s);
+    u64 o = off[p];
+    for (u32 t = 0; t < n; t++) {
+      srcs[o + t] = src;
+      if (packed) {
+        u64 k = 0;
+        window_words(c, p, s, tlen, t, [&](u32, u32 w) { k = (k << c.wbits) | w; });
+        key[o + t] = k;
+      } else {
+        u32* g = gram + (o + t) * c.l;
+        window_words(c, p, s, tlen, t, [&](u32 j, u32 w) { g[j] = w; });
+      }
+    }
+  }
+}
+
+__global__ void k_gather_col(const u32* gram, const u32* idx, u64 n, u32 l, u32 j, u32* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = gram[(u64)idx[i] * l + j];
+}
+
+__global__ void k_permute_gram(const u32* gram, const u32* src, const u32* idx, u64 n, u32 l,
+                               u32* gram2, u32* src2) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 k = idx[i];
+    src2[i] = src[k];
+    for (u32 j = 0; j < l; j++) gram2[i * l + j] = gram[(u64)k * l + j];
+  }
+}
+
+__global__ void k_run_heads(const u64* key, const u32* gram, u64 n, u32 l, int packed, uint8_t* h) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    bool head = i == 0;
+    if (!head) {
+      if (packed) head = key[i] != key[i - 1];
+      else
+        for (u32 j = 0; j < l && !head; j++) head = gram[i * l + j] != gram[(i - 1) * l + j];
+    }
+    h[i] = head;
+  }
+}
+
+// dense per-run file counts: team of G lanes per run
+template <int G>
+__global__ void k_run_rows(const u32* run_start, u64 nruns, u64 n, const u32* __restrict__ src,
+                           const u64* __restrict__ w, u32 R, u32 C, u64* out) {
+  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 teams = ((u64)gridDim.x * blockDim.x) / G;
+  const u32 tl = threadIdx.x % G;
+  for (u64 t = gtid / G; t < nruns; t += teams) {
+    const u64 a = run_start[t], b = t + 1 < nruns ? run_start[t + 1] : n;
+    for (u32 col = tl; col < C; col += G) {
+      u64 acc = 0;
+      for (u64 i = a; i < b; i++) {
+        const u32 s = src[i];
+        acc += s < R ? w[(u64)s * C + col] : (s - R == col ? 1ull : 0ull);
+      }
+      out[t * C + col] = acc;
+    }
+  }
+}
+
+__global__ void k_nz(const u64* v, u64 n, uint8_t* f) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f[i] = v[i] != 0;
+}
+
+// records (run, col, count) -> sort key (major << CB) | (W - count)
+__global__ void k_rec_keys(const u32* sel, const u64* nsel, const u64* rows, u32 C, u64 W, int CB,
+                           int by_file, u64* skey, u32* rec) {
+  u64 n = *nsel;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 j = sel[i];
+    u64 run = j / C, col = j % C;
+    skey[i] = ((by_file ? col : run) << CB) | (W - rows[j]);
+    rec[i] = j;
+  }
+}
+
+__global__ void k_rec_out(const u32* rec, u64 n, const u64* rows, u32 C, const u32* run_start,
+                          const u64* skey_sorted, const u32* gram, u32 l, int packed, u32 file_lo,
+                          int write_gram, u64* key_out, u32* gram_out, u64* cnt_out, u32* id_out,
+                          u32* major_out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 j = rec[i];
+    u32 run = j / C, col = j % C;
+    cnt_out[i] = rows[j];
+    if (id_out) id_out[i] = file_lo + col;
+    if (major_out) major_out[i] = col;
+    u32 rs = run_start[run];
+    if (write_gram) {
+      if (packed) key_out[i] = skey_sorted[rs];
+      else
+        for (u32 k = 0; k < l; k++) gram_out[(u64)i * l + k] = gram[(u64)rs * l + k];
+    }
+  }
+}
+
+__global__ void k_group_heads(const u32* rec, u64 n, u32 C, uint8_t* h) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    h[i] = i == 0 || rec[i] / C != rec[i - 1] / C;
+}
+
+__global__ void k_group_out(const u32* gsel, const u64* ng_p, const u32* rec, u32 C,
+                            const u32* run_start, const u64* keys, const u32* gram, u32 l,
+                            int packed, u64* goff, u64* gkey, u32* ggram) {
+  u64 ng = *ng_p;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += stride) {
+    u32 i = gsel[g];
+    goff[g] = i;
+    u32 rs = run_start[rec[i] / C];
+    if (packed) gkey[g] = keys[rs];
+    else
+      for (u32 k = 0; k < l; k++) ggram[(u64)g * l + k] = gram[(u64)rs * l + k];
+  }
+}
+
+#define SL(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
+
+template <class T>
+static T d2h1(const void* p, cudaStream_t st) {
+  T v;
+  GT_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  return v;
+}
+
+}  // namespace
+
+void run_sequences(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out) {
+  cudaStream_t st = d->stream;
+  const u32 l = (u32)l_, m = l - 1;
+  const u64 R = d->R, E = d->E, nw = d->nw, base = d->nw + d->ns;
+  // pack_width, sequence.py:229-231
+  const int wbits = std::max(1, bitlen(nw ? nw - 1 : 1));
+  const int packed = (u64)l * wbits <= 63;
+  *wbits_out = packed ? wbits : 0;
+  const u32 Fo = (u32)(d->file_hi - d->file_lo);
+  const u32 C = std::max<u32>(1, Fo);
+
+  // phase 1: head/tail buffers by bottom-up level (sequence.py:110-140)
+  const u32 mm = std::max<u32>(m, 1);
+  DBuf H(R * mm * 4, st), T(R * mm * 4, st), hl(R * 4, st), tl(R * 4, st);
+  GT_CUDA(cudaMemsetAsync(hl.p, 0, R * 4, st));
+  GT_CUDA(cudaMemsetAsync(tl.p, 0, R * 4, st));
+  if (m) {
+    for (int L = 1; L <= d->bu.nl; L++) {
+      u64 lo = d->bu.off[L], hi = d->bu.off[L + 1];
+      if (hi > lo)
+        SL(k_head_tail, hi - lo, d->bu.order.as<u32>(), lo, hi, d->body.as<u32>(), d->boff.as<u64>(),
+           nw, base, d->exp_len.as<u64>(), m, H.as<u32>(), T.as<u32>(), hl.as<u32>(), tl.as<u32>());
+    }
+  }
+  // per-file rule weights (top-down, F columns)
+  DBuf w;
+  u32 Cw;
+  td_file_weights(d, w, &Cw);
+
+  // phase 2: windows attributed per body position (two passes + scan)
+  WinCtx c{d->body.as<u32>(), d->pos_owner.as<u32>(), d->boff.as<u64>(), d->root_seg.as<u32>(),
+           H.as<u32>(), T.as<u32>(), hl.as<u32>(), tl.as<u32>(), nw, base, l, m, (u32)wbits,
+           (u32)R, (u32)d->file_lo, Fo};
+  DBuf cnt(E * 8 + 8, st), off(E * 8 + 8, st);
+  SL(k_count_windows, E, c, E, cnt.as<u64>());
+  exclusive_scan_u64(cnt.as<u64>(), off.as<u64>(), E, st);
+  u64 N = 0;
+  if (E) N = d2h1<u64>(off.as<u64>() + E - 1, st) + d2h1<u64>(cnt.as<u64>() + E - 1, st);
+  cnt.release();
+  if (N >= (1ull << 32)) fail(GT_E_RESOURCE, "%lu windows exceed the 2^32 record limit", (unsigned long)N);
+  DBuf key(packed ? N * 8 + 8 : 8, st), gram(packed ? 8 : N * l * 4 + 4, st), src(N * 4 + 4, st);
+  SL(k_write_windows, E, c, E, off.as<u64>(), packed, key.as<u64>(), gram.as<u32>(), src.as<u32>());
+  off.release();
+
+  // sort by gram
+  DBuf skey, sgram, ssrc(N * 4 + 4, st);
+  if (packed) {
+    skey.alloc(N * 8 + 8, st);
+    sort_pairs_u64_u32(key.as<u64>(), skey.as<u64>(), src.as<u32>(), ssrc.as<u32>(), N,
+                       std::max(1, (int)(l * wbits)), st);
+  } else {
+    DBuf idx(N * 4 + 4, st), idx2(N * 4 + 4, st), col(N * 4 + 4, st), col2(N * 4 + 4, st);
+    SL(k_iota_u32, N, idx.as<u32>(), N);
+    for (int j = (int)l - 1; j >= 0; j--) {
+      SL(k_gather_col, N, gram.as<u32>(), idx.as<u32>(), N, l, (u32)j, col.as<u32>());
+      sort_pairs_u32_u32(col.as<u32>(), col2.as<u32>(), idx.as<u32>(), idx2.as<u32>(), N, wbits, st);
+      std::swap(idx, idx2);
+    }
+    sgram.alloc(N * l * 4 + 4, st);
+    SL(k_permute_gram, N, gram.as<u32>(), src.as<u32>(), idx.as<u32>(), N, l, sgram.as<u32>(), ssrc.as<u32>());
+  }
+  key.release();
+  gram.release();
+  src.release();
+
+  // key runs -> per-run file counts
+  DBuf heads(N + 1, st), runs(N * 4 + 4, st), dcnt(16, st);
+  SL(k_run_heads, N, skey.as<u64>(), sgram.as<u32>(), N, l, packed, heads.as<uint8_t>());
+  select_flagged_index(heads.as<uint8_t>(), runs.as<u32>(), dcnt.as<u64>(), N, st);
+  const u64 nruns = d2h1<u64>(dcnt.p, st);
+  const u64 NR = nruns * C;
+  if (NR >= (1ull << 32)) fail(GT_E_RESOURCE, "%lu gram x file cells exceed the 2^32 limit", (unsigned long)NR);
+  DBuf rows(NR * 8 + 8, st);
+  if (nruns) {
+    if (C == 1) SL((k_run_rows<1>), nruns, runs.as<u32>(), nruns, N, ssrc.as<u32>(), w.as<u64>(), (u32)R, C, rows.as<u64>());
+    else if (C <= 8) SL((k_run_rows<8>), nruns * 8, runs.as<u32>(), nruns, N, ssrc.as<u32>(), w.as<u64>(), (u32)R, C, rows.as<u64>());
+    else if (C <= 16) SL((k_run_rows<16>), nruns * 16, runs.as<u32>(), nruns, N, ssrc.as<u32>(), w.as<u64>(), (u32)R, C, rows.as<u64>());
+    else SL((k_run_rows<32>), nruns * 32, runs.as<u32>(), nruns, N, ssrc.as<u32>(), w.as<u64>(), (u32)R, C, rows.as<u64>());
+  }
+  if (Fo == 0) GT_CUDA(cudaMemsetAsync(rows.p, 0, NR * 8, st));
+  ssrc.release();
+  heads.release();
+  w.release();
+
+  // nonzero (run, file) cells in (gram asc, file asc) order
+  DBuf nzf(NR + 1, st), sel(NR * 4 + 4, st);
+  SL(k_nz, NR, rows.as<u64>(), NR, nzf.as<uint8_t>());
+  select_flagged_index(nzf.as<uint8_t>(), sel.as<u32>(), dcnt.as<u64>(), NR, st);
+  const u64 n = d2h1<u64>(dcnt.p, st);
+  nzf.release();
+  const u64 Wt = d->W;
+  const int CB = std::max(1, bitlen(Wt));
+  const bool by_file = task == GT_SEQCOUNT;
+  const int MB = by_file ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns));
+  if (CB + MB > 64) fail(GT_E_RESOURCE, "sort key of %d bits exceeds 64", CB + MB);
+  DBuf sk(n * 8 + 8, st), sk2(n * 8 + 8, st), rec(n * 4 + 4, st), rec2(n * 4 + 4, st);
+  SL(k_rec_keys, n, sel.as<u32>(), dcnt.as<u64>(), rows.as<u64>(), C, Wt, CB, by_file ? 1 : 0,
+     sk.as<u64>(), rec.as<u32>());
+  sort_pairs_u64_u32(sk.as<u64>(), sk2.as<u64>(), rec.as<u32>(), rec2.as<u32>(), n, CB + MB, st);
+  sk.release();
+  sk2.release();
+  Rr->n = n;
+  Rr->count.alloc(n * 8 + 8, st);
+  if (by_file) {
+    // SEQCOUNT: per file, (-count, gram) order
+    if (packed) Rr->key.alloc(n * 8 + 8, st);
+    else Rr->gram.alloc(n * l * 4 + 4, st);
+    DBuf major(n * 4 + 4, st);
+    SL(k_rec_out, n, rec2.as<u32>(), n, rows.as<u64>(), C, runs.as<u32>(), skey.as<u64>(),
+       sgram.as<u32>(), l, packed, (u32)d->file_lo, 1, Rr->key.as<u64>(),
+       Rr->gram.as<u32>(), Rr->count.as<u64>(), (u32*)nullptr, major.as<u32>());
+    Rr->n_groups = Fo;
+    Rr->group_off.alloc((Fo + 1) * 8, st);
+    SL(k_csr_offsets, Fo + 1, major.as<u32>(), n, (u64)Fo, Rr->group_off.as<u64>());
+  } else {
+    // RANKEDINVERTEDINDEX: grams ascending, per gram (-count, file)
+    Rr->id.alloc(n * 4 + 4, st);
+    SL(k_rec_out, n, rec2.as<u32>(), n, rows.as<u64>(), C, runs.as<u32>(), skey.as<u64>(),
+       sgram.as<u32>(), l, packed, (u32)d->file_lo, 0, (u64*)nullptr, (u32*)nullptr,
+       Rr->count.as<u64>(), Rr->id.as<u32>(), (u32*)nullptr);
+    DBuf gh(n + 1, st), gsel(n * 4 + 4, st);
+    SL(k_group_heads, n, rec2.as<u32>(), n, C, gh.as<uint8_t>());
+    select_flagged_index(gh.as<uint8_t>(), gsel.as<u32>(), dcnt.as<u64>(), n, st);
+    const u64 ng = d2h1<u64>(dcnt.p, st);
+    Rr->n_groups = ng;
+    Rr->group_off.alloc((ng + 1) * 8, st);
+    if (packed) Rr->group_key.alloc(ng * 8 + 8, st);
+    else Rr->group_gram.alloc(ng * l * 4 + 4, st);
+    SL(k_group_out, ng, gsel.as<u32>(), dcnt.as<u64>(), rec2.as<u32>(), C, runs.as<u32>(),
+       skey.as<u64>(), sgram.as<u32>(), l, packed, Rr->group_off.as<u64>(), Rr->group_key.as<u64>(),
+       Rr->group_gram.as<u32>());
+    GT_CUDA(cudaMemcpyAsync(Rr->group_off.as<u64>() + ng, &n, 8, cudaMemcpyHostToDevice, st));
+  }
+  GT_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace gt

@@ -1,0 +1,7 @@
+// seq.cuh — l-gram tasks (seq.cu).
+#pragma once
+#include "word.cuh"
+
+namespace gt {
+void run_sequences(DeviceDag* d, int task, int seq_len, DevRecords* R, int* wbits_out);
+}

@@ -1,0 +1,21 @@
+// word.cuh — word-task drivers (word.cu) and device result records.
+#pragma once
+#include "gt_internal.cuh"
+
+namespace gt {
+
+// Compact device-side result (render order) before the D2H copy.
+struct DevRecords {
+  u64 n = 0, n_groups = 0;
+  DBuf group_off, group_id, group_key, group_gram;  // u64, u32, u64, u32
+  DBuf id, key, gram, count;                        // u32, u64, u32, u64
+};
+
+void td_word_counts(DeviceDag* d, DBuf& counts);
+void td_file_counts(DeviceDag* d, DBuf& counts);
+void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW);
+void td_file_weights(DeviceDag* d, DBuf& w, u32* C);
+void assemble_counts(DeviceDag* d, const u64* dense, u64 V, u32 ncols, bool by_count, DevRecords* R);
+void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R);
+
+}  // namespace gt

@@ -1,0 +1,180 @@
+"""DeviceDag: the device-resident counterpart of the reference `Dag`.
+
+`build_dag(blob)` mirrors `deserialize_grammar` + `build_dag`
+(`src/grammar.py:193-228`, `src/dag.py:131-230`) through `gt_open`; the
+handle exposes what `render` and the task facade need (`num_files`,
+`num_rules`, `grammar.dictionary`) plus `info` (R, E, W, depth, ...).
+
+The CUDA library is mandatory: if libgtadoc_b200.so is missing or no CUDA
+device is present, `lib()` raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from ._abi import GtInfo, GtView, compact_from_view, raise_for_status
+from .errors import ResourceError
+from .gtdc import GrammarView
+
+LIB_PATH = Path(__file__).resolve().parent / "libgtadoc_b200.so"
+EXPORTS = ("gt_abi_version", "gt_last_error", "gt_open", "gt_info_get", "gt_run",
+           "gt_result_view", "gt_result_free", "gt_close", "gt_device_word_counts",
+           "gt_dag_array", "gt_flush_l2", "gt_sync", "gt_profile", "gt_profile_report")
+_lib = None
+
+
+def lib():
+    """Load libgtadoc_b200.so (fails loudly when absent)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ResourceError(f"{LIB_PATH} is missing: run `python -m paper_2106_06889_b200.build`")
+        L = C.CDLL(str(LIB_PATH))
+        L.gt_abi_version.restype = C.c_int
+        L.gt_last_error.restype = C.c_char_p
+        L.gt_open.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.c_uint64, C.c_uint64,
+                              C.POINTER(C.c_void_p)]
+        L.gt_open.restype = C.c_int
+        L.gt_info_get.argtypes = [C.c_void_p, C.POINTER(GtInfo)]
+        L.gt_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.gt_run.restype = C.c_int
+        L.gt_result_view.argtypes = [C.c_void_p, C.POINTER(GtView)]
+        L.gt_result_free.argtypes = [C.c_void_p]
+        L.gt_close.argtypes = [C.c_void_p]
+        L.gt_device_word_counts.argtypes = [C.c_void_p]
+        L.gt_device_word_counts.restype = C.c_void_p
+        L.gt_dag_array.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64]
+        L.gt_dag_array.restype = C.c_int64
+        L.gt_flush_l2.argtypes = [C.c_void_p]
+        L.gt_sync.argtypes = [C.c_void_p]
+        L.gt_profile.argtypes = [C.c_void_p, C.c_int]
+        L.gt_profile_report.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+        L.gt_profile_report.restype = C.c_int64
+        _lib = L
+    return _lib
+
+
+def _err() -> str:
+    return lib().gt_last_error().decode(errors="replace")
+
+
+class DeviceDag:
+    """Grammar loaded, validated and flattened on one CUDA device."""
+
+    def __init__(self, blob, device: int = 0, file_lo: int = 0,
+                 file_hi: int = (1 << 64) - 1):
+        """`blob`: GTDC bytes, or (host_pointer, nbytes) of a (pinned) buffer."""
+        self._h = None
+        if isinstance(blob, tuple):
+            ptr, nbytes = blob
+            src = C.cast(C.c_void_p(ptr), C.c_char_p)
+            self._blob = None
+        else:
+            self._blob = bytes(blob)
+            src, nbytes = self._blob, len(self._blob)
+        h = C.c_void_p()
+        L = lib()
+        st = L.gt_open(src, nbytes, device, file_lo, file_hi, C.byref(h))
+        raise_for_status(st, _err())
+        self._h = h
+        self.device = device
+        self.grammar = GrammarView(self._blob) if self._blob is not None else None
+        inf = GtInfo()
+        L.gt_info_get(self._h, C.byref(inf))
+        self.info = inf.as_dict()
+
+    @property
+    def num_files(self) -> int:
+        return self.info["num_files"]
+
+    @property
+    def num_rules(self) -> int:
+        return self.info["num_rules"]
+
+    def run(self, task: int, seq_len: int, strategy: int, file_set_width: int):
+        L = lib()
+        r = C.c_void_p()
+        st = L.gt_run(self._h, task, seq_len, strategy, file_set_width, C.byref(r))
+        raise_for_status(st, _err())
+        try:
+            v = GtView()
+            L.gt_result_view(r, C.byref(v))
+            return compact_from_view(v)
+        finally:
+            L.gt_result_free(r)
+
+    def run_raw(self, task: int, seq_len: int = 3, strategy: int = 0, file_set_width: int = 64):
+        """gt_run returning (result handle, view) without copying the arrays;
+        caller frees with `free_raw`.  Used by the e2e bench leg."""
+        L = lib()
+        r = C.c_void_p()
+        st = L.gt_run(self._h, task, seq_len, strategy, file_set_width, C.byref(r))
+        raise_for_status(st, _err())
+        v = GtView()
+        L.gt_result_view(r, C.byref(v))
+        return r, v
+
+    @staticmethod
+    def free_raw(r) -> None:
+        lib().gt_result_free(r)
+
+    def device_word_counts_ptr(self) -> int:
+        return lib().gt_device_word_counts(self._h) or 0
+
+    def dag_array(self, name: str) -> np.ndarray:
+        L = lib()
+        n = L.gt_dag_array(self._h, name.encode(), None, 0)
+        if n < 0:
+            raise KeyError(f"{name}: {_err()}")
+        out = np.zeros(max(n, 1), dtype=np.int64)
+        L.gt_dag_array(self._h, name.encode(), out.ctypes.data, len(out))
+        return out[:n]
+
+    def profile(self, enable: bool) -> None:
+        raise_for_status(lib().gt_profile(self._h, 1 if enable else 0), _err())
+
+    def profile_report(self) -> dict:
+        """{kernel name: (launches, total_ms)} since the last report."""
+        L = lib()
+        n = L.gt_profile_report(self._h, None, 0)
+        buf = C.create_string_buffer(max(int(n), 1) + 16)
+        L.gt_profile_report(self._h, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split("\t")
+            out[name] = (int(cnt), float(ms))
+        return out
+
+    def flush_l2(self) -> None:
+        raise_for_status(lib().gt_flush_l2(self._h), _err())
+
+    def sync(self) -> None:
+        raise_for_status(lib().gt_sync(self._h), _err())
+
+    def close(self) -> None:
+        if self._h is not None:
+            lib().gt_close(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_dag(source, device: int = 0) -> DeviceDag:
+    """GTDC bytes (or a path to a .gtdc file) -> DeviceDag."""
+    if isinstance(source, (str, Path)):
+        source = Path(source).read_bytes()
+    return DeviceDag(source, device=device)
