@@ -165,7 +165,9 @@ int64_t gt_dag_array(gt_ctx* ctx, const char* name, int64_t* out, int64_t cap);
 /* Per-kernel timing: while enabled, every kernel launched by this thread is
  * bracketed by CUDA events on its stream.  gt_profile_report writes
  * "name\tlaunches\ttotal_ms\n" lines (aggregated by kernel name, since the
- * last report) into buf and returns the length needed (or -1). */
+ * last report) into buf and returns the length needed (or -1); the report
+ * is consumed only by a call with buf != NULL.  ctx may be NULL (profile a
+ * gt_open: enable before it, report after it). */
 int gt_profile(gt_ctx* ctx, int enable);
 int64_t gt_profile_report(gt_ctx* ctx, char* buf, size_t cap);
 

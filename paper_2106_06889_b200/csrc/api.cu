@@ -313,16 +313,20 @@ int gt_flush_l2(gt_ctx* c) {
 
 int gt_profile(gt_ctx* c, int enable) {
   return guard([&] {
-    GT_CUDA(cudaStreamSynchronize(c->d.stream));
+    if (c) GT_CUDA(cudaStreamSynchronize(c->d.stream));
     g_prof.on = enable != 0;
   });
 }
 
 int64_t gt_profile_report(gt_ctx* c, char* buf, size_t cap) {
+  // records are drained into a per-thread aggregate; the aggregate is only
+  // cleared when it is actually copied out (buf != NULL), so the usual
+  // size-query-then-read call pair sees the same report
+  static thread_local std::vector<std::pair<std::string, std::pair<u64, double>>> agg;
   std::string text;
   int st = guard([&] {
-    GT_CUDA(cudaStreamSynchronize(c->d.stream));
-    std::vector<std::pair<std::string, std::pair<u64, double>>> agg;
+    if (c) GT_CUDA(cudaStreamSynchronize(c->d.stream));
+    else GT_CUDA(cudaDeviceSynchronize());
     for (auto& r : g_prof.recs) {
       float ms = 0;
       GT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
@@ -345,6 +349,7 @@ int64_t gt_profile_report(gt_ctx* c, char* buf, size_t cap) {
     size_t n = std::min(cap - 1, text.size());
     memcpy(buf, text.data(), n);
     buf[n] = 0;
+    agg.clear();
   }
   return (int64_t)text.size() + 1;
 }

@@ -17,6 +17,8 @@
 // the exact rule named in a cycle message needs the reference's DFS order,
 // so only on that error path the host replays _topo_order (grammar.py:127).
 #include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -493,13 +495,30 @@ static void build_levels(DeviceDag* d, const DBuf& lvl, const DBuf& off, u64 th,
   out->off[nl + 1] = R;
 }
 
+// GT_TRACE=1: synchronising phase timer of gt_open on stderr
+struct Phases {
+  bool on;
+  cudaStream_t st = nullptr;
+  std::chrono::steady_clock::time_point t;
+  Phases() : on(getenv("GT_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    if (st) cudaStreamSynchronize(st);
+    auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[gt_open] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 }  // namespace
 
 void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_lo, u64 file_hi,
                       DeviceDag* d) {
   auto t0 = std::chrono::steady_clock::now();
+  Phases ph;
   Parse P;
   parse_host(blob, nbytes, &P);
+  ph.mark("host parse");
   if (P.trunc_rule >= 0) {
     host_range_check(blob, P, (u64)P.trunc_rule);
     char buf[96];
@@ -514,6 +533,8 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   d->device = device;
   if (!d->stream) GT_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
   cudaStream_t st = d->stream;
+  ph.st = st;
+  ph.mark("stream");
   {
     cudaMemPool_t pool;
     GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -550,6 +571,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   u32 bad_rule;
   d2h(&bad_rule, bad.p, 1, st);
   if (bad_rule != 0xFFFFFFFFu) host_range_check(blob, P, bad_rule + 1);
+  ph.mark("upload+unpack");
 
   // ---- (rule, symbol) sort + RLE -> own / sub CSR ----------------------
   const int SB = std::max(1, bitlen(limit - 1));
@@ -599,6 +621,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   d->sub_off.alloc((R + 1) * 8, st);
   LAUNCH(k_csr_offsets, R + 1, own_rule.as<u32>(), Eo, R, d->own_off.as<u64>());
   LAUNCH(k_csr_offsets, R + 1, sub_rule.as<u32>(), Es, R, d->sub_off.as<u64>());
+  ph.mark("own/sub CSR");
 
   // ---- parents: stable sort of sub pairs by child -------------------------
   DBuf idx(Es * 4 + 4, st), sidx(Es * 4 + 4, st), child_sorted(Es * 4 + 4, st);
@@ -613,6 +636,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   LAUNCH(k_csr_offsets, R + 1, child_sorted.as<u32>(), Es, R, d->par_off.as<u64>());
   idx.release();
   sidx.release();
+  ph.mark("parent CSR");
 
   // ---- per-rule sums -------------------------------------------------------
   d->own_tok.alloc(R * 8, st);
@@ -650,6 +674,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     g_launches++;
   }, &processed);
   if (processed < R) cycle_message(blob, P);
+  ph.mark("bottom-up layering");
   // depth = height(root) = layer(root) - 1; reference bu_level excludes root
   u32 root_layer;
   d2h(&root_layer, d->bu_level.p, 1, st);
@@ -673,6 +698,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   u32 fu;
   d2h(&fu, firstu.p, 1, st);
   if (fu != 0xFFFFFFFFu) fail(GT_E_CORRUPTION, "rule %u is not reachable from the root", fu);
+  ph.mark("top-down layering");
   rem_bu.release();
   rem_td.release();
   fr.release();
@@ -683,6 +709,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   build_levels(d, d->td_level, d->par_off, 16, ntd, &d->td);
   // the reference's bottom-up rounds exclude the root (engine.py:305-310)
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
+  ph.mark("level lists");
 
   // ---- root segments (dag.py:107-128) -------------------------------------
   const u64 L0 = P.boff[1] - P.boff[0];
@@ -735,6 +762,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     g_launches++;
   }
   d2h(&d->W, d->exp_len.p, 1, st);
+  ph.mark("segments+exp_len");
 
   // ---- segment tokens + root occurrence lists ------------------------------
   const int SBF = std::max(1, bitlen(F - 1));
@@ -769,6 +797,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   occ_list(wkey, isw, std::max(1, bitlen(nw ? nw - 1 : 0)), d->rw_word, d->rw_seg, d->rw_cnt, &d->n_rw);
   d->rs_off.alloc((R + 1) * 8, st);
   LAUNCH(k_csr_offsets, R + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
+  ph.mark("root occurrence lists");
 
   // ---- word-major transpose of the own pairs --------------------------------
   {
@@ -785,6 +814,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
   }
   GT_CUDA(cudaStreamSynchronize(st));
+  ph.mark("own transpose");
   d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 

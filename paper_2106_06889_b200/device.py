@@ -135,19 +135,11 @@ class DeviceDag:
         return out[:n]
 
     def profile(self, enable: bool) -> None:
-        raise_for_status(lib().gt_profile(self._h, 1 if enable else 0), _err())
+        profile(enable, self._h)
 
     def profile_report(self) -> dict:
         """{kernel name: (launches, total_ms)} since the last report."""
-        L = lib()
-        n = L.gt_profile_report(self._h, None, 0)
-        buf = C.create_string_buffer(max(int(n), 1) + 16)
-        L.gt_profile_report(self._h, buf, len(buf))
-        out = {}
-        for line in buf.value.decode().splitlines():
-            name, cnt, ms = line.split("\t")
-            out[name] = (int(cnt), float(ms))
-        return out
+        return profile_report(self._h)
 
     def flush_l2(self) -> None:
         raise_for_status(lib().gt_flush_l2(self._h), _err())
@@ -171,6 +163,25 @@ class DeviceDag:
             self.close()
         except Exception:
             pass
+
+
+def profile(enable: bool, handle=None) -> None:
+    """Per-kernel CUDA-event timing on the calling thread (gt_profile); with
+    no handle it can bracket a gt_open (DeviceDag construction)."""
+    raise_for_status(lib().gt_profile(handle, 1 if enable else 0), _err())
+
+
+def profile_report(handle=None) -> dict:
+    """{kernel name: (launches, total_ms)} since the last report."""
+    L = lib()
+    n = L.gt_profile_report(handle, None, 0)
+    buf = C.create_string_buffer(max(int(n), 1) + 16)
+    L.gt_profile_report(handle, buf, len(buf))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split("\t")
+        out[name] = (int(cnt), float(ms))
+    return out
 
 
 def build_dag(source, device: int = 0) -> DeviceDag:
