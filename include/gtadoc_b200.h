@@ -85,6 +85,7 @@ typedef struct gt_info {
   int64_t bu_levels;       /* bottom-up levels (= reference bottom-up rounds) */
   uint64_t device_bytes;   /* device memory held by the context               */
   double init_ms;          /* gt_open wall time (the "initialization" phase)  */
+  uint64_t td_edges;       /* non-root parent edges (top-down pass items)     */
 } gt_info;
 
 /*

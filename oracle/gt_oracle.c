@@ -1806,6 +1806,7 @@ int gto_info(const OCtx* c, gt_info* o) {
   o->td_levels = d->td_levels;
   o->bu_levels = d->bu_levels;
   o->init_ms = c->init_ms;
+  o->td_edges = (u64)(d->sub_off[d->R] - d->sub_off[d->R > 1 ? 1 : d->R]);
   return GT_OK;
 }
 

@@ -57,6 +57,7 @@ class GtInfo(C.Structure):
         ("bu_levels", C.c_int64),
         ("device_bytes", C.c_uint64),
         ("init_ms", C.c_double),
+        ("td_edges", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

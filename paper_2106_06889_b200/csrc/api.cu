@@ -166,10 +166,9 @@ int gt_info_get(const gt_ctx* c, gt_info* o) {
   o->depth = d.depth;
   o->td_levels = d.td.nl;
   o->bu_levels = d.bu.nl > 0 ? d.bu.nl - 1 : 0;
-  size_t total = 0, free_b = 0;
-  cudaMemGetInfo(&free_b, &total);
-  o->device_bytes = 0;
+  o->device_bytes = d.bytes_held();
   o->init_ms = d.init_ms;
+  o->td_edges = d.te_off.empty() ? 0 : d.te_off.back();
   return GT_OK;
 }
 

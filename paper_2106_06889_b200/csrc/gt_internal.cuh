@@ -111,9 +111,28 @@ struct DeviceDag {
   DBuf rw_word, rw_seg, rw_cnt;        // root word occurrences by (word, seg)
   u64 E_own = 0, E_sub = 0, n_rs = 0, n_rw = 0;
   Levels td, bu;
+  // level-ordered edge lists for the segmented gather-reduce (segreduce.cuh)
+  //   te_*: non-root parent edges (child, parent, freq) by (td level, child, parent)
+  //   be_*: child edges (rule, child, freq) by (bu level, rule, child)
+  DBuf te_child, te_par, te_freq;
+  std::vector<u64> te_off;  // host: td level L items [te_off[L], te_off[L+1])
+  DBuf be_rule, be_child, be_freq;
+  std::vector<u64> be_off;  // host: bu level L items [be_off[L], be_off[L+1])
   double init_ms = 0;
   // scratch kept across runs
   DBuf word_counts;  // u64[V] of the last global run
+
+  u64 bytes_held() const {
+    const DBuf* all[] = {&body, &boff, &pos_owner, &root_seg, &own_ids, &own_freqs, &own_off,
+                         &own_tok, &sub_ids, &sub_freqs, &sub_off, &par_ids, &par_freqs, &par_off,
+                         &num_in, &num_out, &exp_len, &td_level, &bu_level, &seg_lo, &seg_hi,
+                         &seg_tokens, &ow_word, &ow_rule, &ow_freq, &ow_off, &rs_rule, &rs_seg,
+                         &rs_cnt, &rs_off, &rw_word, &rw_seg, &rw_cnt, &td.order, &bu.order,
+                         &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts};
+    u64 t = 0;
+    for (const DBuf* b : all) t += b->bytes;
+    return t;
+  }
 };
 
 // loader.cu

@@ -36,34 +36,4 @@ __global__ void k_seg_sum_sorted(const u32* key, u64 n, ValF val, u64* out) {
   }
 }
 
-// Level-ordered pull:  out[r] = base(r) + sum_{e in CSR(r)} mult[e] * in[idx[e]]
-// light rules: one thread per rule; heavy rules: one warp per rule.
-template <class BaseF>
-__global__ void k_pull_sum(const u32* order, u64 lo, u64 mid, u64 hi, const u64* off,
-                           const u32* idx, const u32* mult, const u64* in, BaseF base, u64* out) {
-  u64 nlight = mid - lo;
-  u64 nlight_threads = nlight;
-  u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  u64 nthreads = (u64)gridDim.x * blockDim.x;
-  // light part
-  for (u64 t = gtid; t < nlight_threads; t += nthreads) {
-    u32 r = order[lo + t];
-    u64 s = base(r);
-    for (u64 e = off[r]; e < off[r + 1]; e++) s += (u64)mult[e] * in[idx[e]];
-    out[r] = s;
-  }
-  // heavy part: warp per rule
-  u64 nheavy = hi - mid;
-  u64 gwarp = gtid >> 5, nwarps = nthreads >> 5;
-  unsigned lane = lane_id();
-  for (u64 w = gwarp; w < nheavy; w += nwarps) {
-    u32 r = order[mid + w];
-    u64 s = 0;
-    for (u64 e = off[r] + lane; e < off[r + 1]; e += 32) s += (u64)mult[e] * in[idx[e]];
-#pragma unroll
-    for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, d);
-    if (lane == 0) out[r] = s + base(r);
-  }
-}
-
 }  // namespace gt

@@ -23,8 +23,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <memory>
 
 #include "kernels_common.cuh"
+#include "segreduce.cuh"
 
 namespace gt {
 
@@ -70,8 +72,11 @@ namespace {
 struct Parse {
   u64 nw = 0, ns = 0, R = 0;
   size_t rules_pos = 0;       // byte offset of the rules section
-  std::vector<u32> rstart;    // u32 index (within the section) of rule i's first symbol
-  std::vector<u64> boff;      // R+1 compact body offsets
+  u32* rstart = nullptr;      // u32 index (within the section) of rule i's first symbol (pinned)
+  // body offset of rule i = rstart[i] - (i + 1) (one length word per rule)
+  u64 Rp = 0;                 // rules fully parsed (R unless truncated)
+  u64 boff(u64 i) const { return i < Rp ? (u64)rstart[i] - (i + 1) : E; }
+  u64 blen(u64 i) const { return boff(i + 1) - boff(i); }
   u64 E = 0;
   long trunc_rule = -1;       // first incomplete rule (error pending range checks)
   std::string trunc_what;
@@ -112,7 +117,7 @@ static bool utf8_ok(const uint8_t* s, size_t n) {
   return true;
 }
 
-static void parse_host(const uint8_t* d, size_t n, Parse* P) {
+static void parse_dict(const uint8_t* d, size_t n, Parse* P) {
   if (n < 4 || memcmp(d, "GTDC", 4) != 0) fail(GT_E_FORMAT, "bad magic: not a GTDC file");
   size_t pos = 4;
   auto need = [&](u64 k, const char* what, long idx) {
@@ -142,10 +147,16 @@ static void parse_host(const uint8_t* d, size_t n, Parse* P) {
     pos += ln;
   }
   P->rules_pos = pos;
-  P->rstart.resize(P->R);
-  P->boff.assign(P->R + 1, 0);
-  u64 E = 0;
-  for (u64 i = 0; i < P->R; i++) {
+}
+
+// The rules section is a chain of (length, body) records: walking it is the
+// one inherently sequential step of the load, so it runs on the host while
+// the section itself is already streaming to the device.
+static void parse_rules(const uint8_t* d, size_t n, Parse* P) {
+  size_t pos = P->rules_pos;
+  u32* rs = P->rstart;
+  u64 E = 0, i = 0;
+  for (; i < P->R; i++) {
     if ((u64)pos + 4 > (u64)n) {
       P->trunc_rule = (long)i;
       P->trunc_what = "rule %ld body length";
@@ -157,11 +168,11 @@ static void parse_host(const uint8_t* d, size_t n, Parse* P) {
       P->trunc_what = "rule %ld body";
       break;
     }
-    P->rstart[i] = (u32)((pos + 4 - P->rules_pos) / 4);
+    rs[i] = (u32)((pos + 4 - P->rules_pos) / 4);
     E += ln;
-    P->boff[i + 1] = E;
     pos += 4 + 4ull * ln;
   }
+  P->Rp = i;
   if (P->trunc_rule < 0) P->trailing = (u64)n - (u64)pos;
   P->E = E;
 }
@@ -171,7 +182,7 @@ static void host_range_check(const uint8_t* d, const Parse& P, u64 upto) {
   u64 limit = P.nw + P.ns + P.R;
   const uint8_t* sec = d + P.rules_pos;
   for (u64 i = 0; i < upto; i++) {
-    u64 lo = P.rstart[i], ln = P.boff[i + 1] - P.boff[i];
+    u64 lo = P.rstart[i], ln = P.blen(i);
     u32 mx = 0;
     for (u64 j = 0; j < ln; j++) mx = std::max(mx, rd32(sec + 4 * (lo + j)));
     if (ln && mx >= limit)
@@ -193,7 +204,7 @@ static void host_range_check(const uint8_t* d, const Parse& P, u64 upto) {
     while (!st.empty()) {
       auto [r, pos] = st.back();
       st.pop_back();
-      u64 len = P.boff[r + 1] - P.boff[r];
+      u64 len = P.blen(r);
       bool adv = false;
       while (pos < len) {
         u64 s = rd32(sec + 4 * (P.rstart[r] + pos));
@@ -224,6 +235,12 @@ __global__ void k_mark_len(const u32* rstart, u64 R, u32* mark) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += stride)
     mark[rstart[i] - 1] = 1;
+}
+
+__global__ void k_boff(const u32* rstart, u64 R, u64 E, u64* boff) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= R; i += stride)
+    boff[i] = i < R ? (u64)rstart[i] - (i + 1) : E;
 }
 
 __global__ void k_unpack(const u32* raw, const u32* mark, const u32* incl, u64 n, u32* body,
@@ -299,43 +316,108 @@ __global__ void k_flag_zero(const u32* rem, u64 R, u64 first, uint8_t* flag) {
     flag[r] = (r >= first) && rem[r] == 0;
 }
 
-// bottom-up Kahn layer: frontier rules get `layer`; parents whose last child
-// finished join the next frontier
-__global__ void k_bu_layer(const u32* fr, const u64* fr_n, u32 layer, const u64* par_off,
-                           const u32* par_ids, u32* rem, u32* lvl, u32* next, u64* next_n) {
-  u64 n = *fr_n;
-  u64 stride = (u64)gridDim.x * blockDim.x;
+// Warp-aggregated "decrement and detect completion": lanes hitting the same
+// counter subtract together (one atomic per distinct counter per warp, so a
+// rule with 10^5 parents finishing in one layer does not serialise 10^5
+// same-address atomics); exactly one lane reports the counter reaching zero.
+// Must be called by every lane of the warp.
+__device__ __forceinline__ bool dec_to_zero(u32* rem, u32 key, bool active) {
+  const unsigned act = __ballot_sync(0xFFFFFFFFu, active);
+  if (!active) return false;
+  const unsigned peers = __match_any_sync(act, key);
+  const unsigned lane = threadIdx.x & 31u;
+  if ((int)lane != __ffs(peers) - 1) return false;
+  const u32 k = (u32)__popc(peers);
+  return atomicSub(&rem[key], k) == k;
+}
+
+// frontier bookkeeping: level of each frontier rule and its parent count
+__global__ void k_bu_frontier(const u32* fr, const u64* fr_n, u32 layer, const u64* par_off, u32* lvl,
+                              u64* deg) {
+  const u64 n = *fr_n;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    u32 r = fr[i];
+    const u32 r = fr[i];
     lvl[r] = layer;
-    for (u64 e = par_off[r]; e < par_off[r + 1]; e++) {
-      u32 p = par_ids[e];
-      if (atomicSub(&rem[p], 1u) == 1u) next[atomicAdd((unsigned long long*)next_n, 1ull)] = p;
-    }
+    deg[i] = par_off[r + 1] - par_off[r];
   }
 }
 
-// top-down Kahn layer over non-root in-edges; reachability rides along
+// bottom-up Kahn layer, edge-balanced: one thread per (frontier rule, parent)
+// edge, located by binary search in the exclusive scan of the frontier's
+// parent counts (a rule with 10^6 parents spreads over the whole grid);
+// parents whose last child finished join the next frontier.
+__global__ void k_bu_edges(const u32* fr, const u64* fr_n, const u64* pos, const u64* deg,
+                           const u64* par_off, const u32* par_ids, u32* rem, u32* next, u64* next_n) {
+  const u64 n = *fr_n;
+  if (!n) return;
+  const u64 T = pos[n - 1] + deg[n - 1];
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 base = (u64)blockIdx.x * blockDim.x; base < T; base += stride) {
+    const u64 e = base + (threadIdx.x & ~31u) + (threadIdx.x & 31u);
+    const bool active = e < T;
+    u32 p = 0;
+    if (active) {
+      u64 lo = 0, hi = n;  // last i with pos[i] <= e
+      while (hi - lo > 1) {
+        const u64 m = (lo + hi) >> 1;
+        if (pos[m] <= e) lo = m;
+        else hi = m;
+      }
+      const u32 r = fr[lo];
+      p = par_ids[par_off[r] + (e - pos[lo])];
+    }
+    if (dec_to_zero(rem, p, active)) next[atomicAdd((unsigned long long*)next_n, 1ull)] = p;
+  }
+}
+
+// top-down Kahn layer over non-root in-edges (children per rule are few);
+// reachability rides along
 __global__ void k_td_layer(const u32* fr, const u64* fr_n, u32 layer, const u64* par_off,
                            const u32* par_ids, const uint8_t* root_parent, const u64* sub_off,
                            const u32* sub_ids, u32* rem, u32* lvl, uint8_t* reach, u32* next,
                            u64* next_n) {
-  u64 n = *fr_n;
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    u32 r = fr[i];
-    lvl[r] = layer;
-    bool rc = root_parent[r];
-    for (u64 e = par_off[r]; e < par_off[r + 1] && !rc; e++) {
-      u32 p = par_ids[e];
-      if (p != 0 && reach[p]) rc = true;
+  const u64 n = *fr_n;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const u64 i = base + threadIdx.x;
+    const bool active = i < n;
+    u32 r = 0;
+    u64 e0 = 0, e1 = 0;
+    if (active) {
+      r = fr[i];
+      lvl[r] = layer;
+      bool rc = root_parent[r];
+      for (u64 e = par_off[r]; e < par_off[r + 1] && !rc; e++) {
+        const u32 p = par_ids[e];
+        if (p != 0 && reach[p]) rc = true;
+      }
+      reach[r] = rc;
+      e0 = sub_off[r];
+      e1 = sub_off[r + 1];
     }
-    reach[r] = rc;
-    for (u64 e = sub_off[r]; e < sub_off[r + 1]; e++) {
-      u32 c = sub_ids[e];
-      if (atomicSub(&rem[c], 1u) == 1u) next[atomicAdd((unsigned long long*)next_n, 1ull)] = c;
+    // children, one per step, warp-uniform trip count
+    u64 len = e1 - e0, mx = len;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, d));
+    for (u64 k = 0; k < mx; k++) {
+      const bool a = k < len;
+      const u32 c = a ? sub_ids[e0 + k] : 0u;
+      if (dec_to_zero(rem, c, a)) next[atomicAdd((unsigned long long*)next_n, 1ull)] = c;
     }
   }
+}
+
+// level-ordered edge lists: key = level of the grouping rule of each edge
+__global__ void k_edge_level_keys(const u32* idx, u64 n, const u32* group_of, const u32* lvl, u32* key) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    key[i] = lvl[group_of[idx ? idx[i] : i]];
+}
+
+__global__ void k_flag_nonzero_u32(const u32* v, u64 n, uint8_t* f) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f[i] = v[i] != 0;
 }
 
 __global__ void k_first_unreached(const uint8_t* reach, u64 R, u32* out) {
@@ -436,10 +518,6 @@ struct ValRootLen {
     return s < nw ? 1ull : (s >= base ? exp_len[s - base] : 0ull);
   }
 };
-struct BaseArr {
-  const u64* a;
-  __device__ u64 operator()(u32 r) const { return a[r]; }
-};
 
 template <class T>
 static void d2h(T* dst, const void* src, size_t n, cudaStream_t s) {
@@ -495,6 +573,21 @@ static void build_levels(DeviceDag* d, const DBuf& lvl, const DBuf& off, u64 th,
   out->off[nl + 1] = R;
 }
 
+// grow-only pinned host buffer (the rule-start table of the chain walk)
+struct PinnedU32 {
+  u32* p = nullptr;
+  u64 cap = 0;
+  u32* get(u64 n) {
+    if (n > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = std::max<u64>(n, 1u << 16);
+      GT_CUDA(cudaMallocHost(&p, cap * 4));
+    }
+    return p;
+  }
+};
+
 // GT_TRACE=1: synchronising phase timer of gt_open on stderr
 struct Phases {
   bool on;
@@ -517,29 +610,40 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   auto t0 = std::chrono::steady_clock::now();
   Phases ph;
   Parse P;
-  parse_host(blob, nbytes, &P);
-  ph.mark("host parse");
+  parse_dict(blob, nbytes, &P);
+  ph.mark("host parse: dictionary");
+  GT_CUDA(cudaSetDevice(device));
+  d->device = device;
+  if (!d->stream) GT_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  cudaStream_t st = d->stream;
+  ph.st = st;
+  {
+    cudaMemPool_t pool;
+    GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    u64 thr = UINT64_MAX;
+    GT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  ph.mark("stream");
+  // start the upload of the whole rules section, then walk the length chain
+  // on the host while it is in flight (overlaps when `blob` is pinned)
+  const u64 nsec = (nbytes - P.rules_pos) / 4;
+  DBuf raw(nsec * 4 + 4, st);
+  if (nsec) GT_CUDA(cudaMemcpyAsync(raw.p, blob + P.rules_pos, nsec * 4, cudaMemcpyHostToDevice, st));
+  static thread_local PinnedU32 rstart_host;
+  P.rstart = rstart_host.get(P.R);
+  parse_rules(blob, nbytes, &P);
+  ph.mark("host parse: rule chain");
   if (P.trunc_rule >= 0) {
+    GT_CUDA(cudaStreamSynchronize(st));
     host_range_check(blob, P, (u64)P.trunc_rule);
     char buf[96];
     snprintf(buf, sizeof buf, P.trunc_what.c_str(), P.trunc_rule);
     fail(GT_E_FORMAT, "truncated input while reading %s", buf);
   }
   if (P.trailing) {
+    GT_CUDA(cudaStreamSynchronize(st));
     host_range_check(blob, P, P.R);
     fail(GT_E_FORMAT, "%lu trailing bytes after rules section", (unsigned long)P.trailing);
-  }
-  GT_CUDA(cudaSetDevice(device));
-  d->device = device;
-  if (!d->stream) GT_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
-  cudaStream_t st = d->stream;
-  ph.st = st;
-  ph.mark("stream");
-  {
-    cudaMemPool_t pool;
-    GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    u64 thr = UINT64_MAX;
-    GT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   }
   const u64 R = P.R, E = P.E, nw = P.nw, ns = P.ns, base = nw + ns, limit = nw + ns + R;
   d->nw = nw;
@@ -549,15 +653,14 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   const u64 nraw = E + R;
 
   // ---- upload + unpack --------------------------------------------------
-  DBuf raw(nraw * 4 + 4, st), rstart(R * 4, st), mark(nraw * 4 + 4, st), incl(nraw * 4 + 4, st);
+  DBuf rstart(R * 4, st), mark(nraw * 4 + 4, st), incl(nraw * 4 + 4, st);
   DBuf& owner = d->pos_owner;
   owner.alloc(E * 4 + 4, st);
   DBuf bad(4, st);
   d->body.alloc(E * 4 + 4, st);
   d->boff.alloc((R + 1) * 8, st);
-  GT_CUDA(cudaMemcpyAsync(raw.p, blob + P.rules_pos, nraw * 4, cudaMemcpyHostToDevice, st));
-  GT_CUDA(cudaMemcpyAsync(rstart.p, P.rstart.data(), R * 4, cudaMemcpyHostToDevice, st));
-  GT_CUDA(cudaMemcpyAsync(d->boff.p, P.boff.data(), (R + 1) * 8, cudaMemcpyHostToDevice, st));
+  GT_CUDA(cudaMemcpyAsync(rstart.p, P.rstart, R * 4, cudaMemcpyHostToDevice, st));
+  LAUNCH(k_boff, R + 1, rstart.as<u32>(), R, E, d->boff.as<u64>());
   GT_CUDA(cudaMemsetAsync(mark.p, 0, nraw * 4, st));
   GT_CUDA(cudaMemsetAsync(bad.p, 0xFF, 4, st));
   LAUNCH(k_mark_len, R, rstart.as<u32>(), R, mark.as<u32>());
@@ -649,8 +752,6 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   LAUNCH(k_seg_sum_sorted, Es, sub_rule.as<u32>(), Es, ValU32{d->sub_freqs.as<u32>()}, d->num_out.as<u64>());
   LAUNCH(k_seg_sum_sorted, Es, child_sorted.as<u32>(), Es,
          (ValU32NonRoot{d->par_freqs.as<u32>(), d->par_ids.as<u32>()}), d->num_in.as<u64>());
-  sub_rule.release();
-  child_sorted.release();
 
   // ---- bottom-up layering (cycle check) then top-down layering -----------
   DBuf rem_bu(R * 4, st), rem_td(R * 4, st), rootp(R, st), flag(R, st);
@@ -666,13 +767,18 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   u64 n0;
   d2h(&n0, fcnt.p, 1, st);
   u64 processed = 0;
+  DBuf fdeg(R * 8 + 8, st), fpos(R * 8 + 8, st);
   int nbu = run_layers(fr, nx, fcnt, n0, R, st, [&](u32 L, u64 n) {
-    k_bu_layer<<<grid_for(n, 256), 256, 0, st>>>(fr.as<u32>(), fcnt.as<u64>(), L,
-                                                 d->par_off.as<u64>(), d->par_ids.as<u32>(),
-                                                 rem_bu.as<u32>(), d->bu_level.as<u32>(),
-                                                 nx.as<u32>(), fcnt.as<u64>() + 1);
-    g_launches++;
+    k_bu_frontier<<<grid_for(n, 256), 256, 0, st>>>(fr.as<u32>(), fcnt.as<u64>(), L, d->par_off.as<u64>(),
+                                                    d->bu_level.as<u32>(), fdeg.as<u64>());
+    exclusive_scan_u64(fdeg.as<u64>(), fpos.as<u64>(), n, st);
+    k_bu_edges<<<148 * 16, 256, 0, st>>>(fr.as<u32>(), fcnt.as<u64>(), fpos.as<u64>(), fdeg.as<u64>(),
+                                         d->par_off.as<u64>(), d->par_ids.as<u32>(), rem_bu.as<u32>(),
+                                         nx.as<u32>(), fcnt.as<u64>() + 1);
+    g_launches += 2;
   }, &processed);
+  fdeg.release();
+  fpos.release();
   if (processed < R) cycle_message(blob, P);
   ph.mark("bottom-up layering");
   // depth = height(root) = layer(root) - 1; reference bu_level excludes root
@@ -707,12 +813,52 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // level-ordered rule lists (light/heavy split)
   build_levels(d, d->bu_level, d->sub_off, 16, nbu, &d->bu);
   build_levels(d, d->td_level, d->par_off, 16, ntd, &d->td);
+
+  // ---- level-ordered edge lists (radix sort is stable: within a level the
+  // edges keep (child, parent) resp. (rule, child) order) -------------------
+  auto level_edges = [&](const u32* group_of, const uint8_t* keep, const u32* lvl, int nl,
+                         const u32* a_src, const u32* b_src, const u32* f_src, DBuf& oa, DBuf& ob,
+                         DBuf& of, std::vector<u64>& off) {
+    DBuf idx(Es * 4 + 4, st), key(Es * 4 + 4, st), key2(Es * 4 + 4, st), idx2(Es * 4 + 4, st);
+    u64 m = Es;
+    if (keep) {
+      select_flagged_index(keep, idx.as<u32>(), cnt.as<u64>(), Es, st);
+      d2h(&m, cnt.p, 1, st);
+    } else {
+      LAUNCH(k_iota_u32, Es, idx.as<u32>(), Es);
+    }
+    LAUNCH(k_edge_level_keys, m, idx.as<u32>(), m, group_of, lvl, key.as<u32>());
+    sort_pairs_u32_u32(key.as<u32>(), key2.as<u32>(), idx.as<u32>(), idx2.as<u32>(), m,
+                       std::max(1, bitlen((u64)nl + 1)), st);
+    oa.alloc(m * 4 + 4, st);
+    ob.alloc(m * 4 + 4, st);
+    of.alloc(m * 4 + 4, st);
+    LAUNCH(k_gather3, m, idx2.as<u32>(), m, a_src, b_src, f_src, oa.as<u32>(), ob.as<u32>(), of.as<u32>());
+    DBuf koff(((u64)nl + 3) * 8, st);
+    LAUNCH(k_csr_offsets, (u64)nl + 3, key2.as<u32>(), m, (u64)nl + 2, koff.as<u64>());
+    off.assign((size_t)nl + 3, 0);
+    d2h(off.data(), koff.p, (size_t)nl + 3, st);
+  };
+  {
+    // td: par entries (grouped by child) whose parent is not the root
+    DBuf keep(Es + 1, st);
+    LAUNCH(k_flag_nonzero_u32, Es, d->par_ids.as<u32>(), Es, keep.as<uint8_t>());
+    level_edges(child_sorted.as<u32>(), keep.as<uint8_t>(), d->td_level.as<u32>(), ntd,
+                child_sorted.as<u32>(), d->par_ids.as<u32>(), d->par_freqs.as<u32>(), d->te_child,
+                d->te_par, d->te_freq, d->te_off);
+    // bu: sub entries (grouped by rule) by the rule's bottom-up layer
+    level_edges(sub_rule.as<u32>(), nullptr, d->bu_level.as<u32>(), nbu, sub_rule.as<u32>(),
+                d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), d->be_rule, d->be_child, d->be_freq,
+                d->be_off);
+  }
+  sub_rule.release();
+  child_sorted.release();
   // the reference's bottom-up rounds exclude the root (engine.py:305-310)
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
   ph.mark("level lists");
 
   // ---- root segments (dag.py:107-128) -------------------------------------
-  const u64 L0 = P.boff[1] - P.boff[0];
+  const u64 L0 = P.blen(0);
   d->L0 = L0;
   const bool headless = ns == 0;
   DBuf spl(L0 + 1, st), splu(L0 * 4 + 4, st), sincl(L0 * 4 + 4, st), spos(L0 * 4 + 4, st);
@@ -750,16 +896,12 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
 
   // ---- exp_len by bottom-up level (grammar.py:109-124) --------------------
   d->exp_len.alloc(R * 8, st);
-  for (int L = 1; L <= d->bu.nl; L++) {
-    u64 lo = d->bu.off[L], mid = d->bu.heavy_off[L], hi = d->bu.off[L + 1];
-    if (hi == lo) continue;
-    u64 work = (mid - lo) + (hi - mid) * 32;
-    k_pull_sum<<<grid_for(work, 256), 256, 0, st>>>(d->bu.order.as<u32>(), lo, mid, hi,
-                                                     d->sub_off.as<u64>(), d->sub_ids.as<u32>(),
-                                                     d->sub_freqs.as<u32>(), d->exp_len.as<u64>(),
-                                                     BaseArr{d->own_tok.as<u64>()},
-                                                     d->exp_len.as<u64>());
-    g_launches++;
+  GT_CUDA(cudaMemcpyAsync(d->exp_len.p, d->own_tok.p, R * 8, cudaMemcpyDeviceToDevice, st));
+  for (int L = 1; L <= nbu; L++) {
+    const u64 a = d->be_off[L], n = d->be_off[L + 1] - a;
+    seg_reduce<SumMode>("k_exp_len", d->be_rule.as<u32>() + a, d->be_child.as<u32>() + a,
+                        d->be_freq.as<u32>() + a, n, 1, RowSrc{d->exp_len.as<u64>(), 1},
+                        OutRowMajor{d->exp_len.as<u64>(), 1}, st);
   }
   d2h(&d->W, d->exp_len.p, 1, st);
   ph.mark("segments+exp_len");

@@ -1,0 +1,226 @@
+// segreduce.cuh — the load-balanced segmented gather-reduce every traversal
+// step of the library is built from.
+//
+//   out[dst[i], col] (+)= combine(freq[i], in(src[i], col))   for i in [0, n)
+//
+// over an item list sorted by dst.  It is the B200 form of the reference's
+// work partitioning (engine.py:74-106 partition_work: rules longer than
+// chunk_factor x average are split into contiguous ranges
+// "fine-grained thread-level partitioning"): items, not rules, are dealt out
+// in fixed-size chunks, so a rule with 10^6 parents costs 10^6/chunk chunks
+// spread over the whole GPU instead of one serial warp.  A run of equal dst
+// interior to a chunk is owned by that chunk and updated with a plain
+// read-modify-write; a run touching a chunk boundary is combined atomically
+// (u64 atomicAdd / atomicOr), so a hot destination costs one atomic per
+// chunk, not one per item (the warp aggregation of north_star).
+//
+// Uses:  top-down level propagation (dst = child, src = parent; items = the
+//        level's non-root parent edges), bottom-up sums (dst = rule, src =
+//        child), reduce-by-word (dst = word, src = rule), gram-run rows
+//        (dst = run, src = rule or root segment).
+#pragma once
+
+#include <algorithm>
+
+#include "kernels_common.cuh"
+
+namespace gt {
+
+struct SumMode {
+  __device__ static __forceinline__ u64 combine(u32 f, u64 x) { return (u64)f * x; }
+  __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a + b; }
+  __device__ static __forceinline__ void atomic(u64* p, u64 v) {
+    if (v) atomicAdd((unsigned long long*)p, (unsigned long long)v);
+  }
+};
+
+struct OrMode {
+  __device__ static __forceinline__ u64 combine(u32, u64 x) { return x; }
+  __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a | b; }
+  __device__ static __forceinline__ void atomic(u64* p, u64 v) {
+    if (v) atomicOr((unsigned long long*)p, (unsigned long long)v);
+  }
+};
+
+// ---- source row functors ----------------------------------------------------
+struct RowSrc {  // in[src*C + col]
+  const u64* in;
+  u32 C;
+  __device__ __forceinline__ u64 operator()(u32 s, u32 col) const { return in[(u64)s * C + col]; }
+};
+
+// ---- output address functors --------------------------------------------------
+struct OutRowMajor {  // out[dst*C + col]
+  u64* out;
+  u32 C;
+  __device__ __forceinline__ u64* operator()(u32 d, u32 col) const { return out + (u64)d * C + col; }
+};
+struct OutColMajor {  // out[col*V + dst]
+  u64* out;
+  u64 V;
+  __device__ __forceinline__ u64* operator()(u32 d, u32 col) const { return out + (u64)col * V + d; }
+};
+
+__device__ __forceinline__ u32 item_freq(const u32* freq, u64 i) { return freq ? freq[i] : 1u; }
+
+// ---------------------------------------------------------------------------
+// one column: a warp owns tiles of 32*K consecutive items; runs are combined
+// with a shuffle segmented scan and carried across the K steps of the tile.
+// ---------------------------------------------------------------------------
+template <class Mode, class Src, class Out>
+__global__ void __launch_bounds__(256) k_segred1(const u32* __restrict__ dst,
+                                                 const u32* __restrict__ src,
+                                                 const u32* __restrict__ freq, u64 n, int K,
+                                                 Src in, Out out) {
+  const unsigned lane = threadIdx.x & 31u;
+  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u64 TILE = 32ull * K;
+  for (u64 t0 = warp * TILE; t0 < n; t0 += nwarps * TILE) {
+    const u32 first = dst[t0];
+    const bool first_shared = t0 > 0 && dst[t0 - 1] == first;
+    const u64 tend = t0 + TILE < n ? t0 + TILE : n;
+    const bool last_shared = tend < n && dst[tend] == dst[tend - 1];
+    const u32 last = dst[tend - 1];
+    u32 carry_d = 0xFFFFFFFFu;
+    u64 carry_v = 0;
+    // software pipeline: values of step k+1 are loaded while step k reduces
+    u64 i = t0 + lane;
+    u32 d_n = i < n ? dst[i] : 0xFFFFFFFFu;
+    u64 v_n = i < n ? Mode::combine(item_freq(freq, i), in(src[i], 0)) : 0;
+#pragma unroll 1
+    for (int k = 0; k < K; k++) {
+      const u32 d = d_n;
+      u64 v = v_n;
+      const bool ok = d != 0xFFFFFFFFu;
+      const u64 j = i + 32;
+      if (k + 1 < K) {
+        d_n = j < tend ? dst[j] : 0xFFFFFFFFu;
+        v_n = j < tend ? Mode::combine(item_freq(freq, j), in(src[j], 0)) : 0;
+      }
+      i = j;
+      const u32 d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+      if (carry_d != 0xFFFFFFFFu && d0 != carry_d) {  // the carried run ended at the last step
+        if (lane == 0) {
+          u64* p = out(carry_d, 0);
+          if (carry_d == first && first_shared) Mode::atomic(p, carry_v);
+          else *p = Mode::merge(*p, carry_v);
+        }
+        carry_d = 0xFFFFFFFFu;
+        carry_v = 0;
+      }
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, s);
+        const u32 od = __shfl_up_sync(0xFFFFFFFFu, d, s);
+        if (lane >= (unsigned)s && od == d) v = Mode::merge(v, ov);
+      }
+      if (d == carry_d) v = Mode::merge(v, carry_v);
+      const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
+      if (ok && lane != 31 && dn != d) {  // run ends inside this step
+        u64* p = out(d, 0);
+        if ((d == first && first_shared) || (d == last && last_shared)) Mode::atomic(p, v);
+        else *p = Mode::merge(*p, v);
+      }
+      carry_d = __shfl_sync(0xFFFFFFFFu, d, 31);
+      carry_v = __shfl_sync(0xFFFFFFFFu, v, 31);
+    }
+    if (lane == 0 && carry_d != 0xFFFFFFFFu) {
+      u64* p = out(carry_d, 0);
+      if ((carry_d == first && first_shared) || (carry_d == last && last_shared)) Mode::atomic(p, carry_v);
+      else *p = Mode::merge(*p, carry_v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// C columns: a team of G lanes owns chunks of K consecutive items and walks
+// them with the lanes spread over the columns (coalesced row gathers); item
+// values are fetched B at a time ahead of the run bookkeeping.
+// ---------------------------------------------------------------------------
+template <int G, class Mode, class Src, class Out>
+__global__ void __launch_bounds__(256) k_segredG(const u32* __restrict__ dst,
+                                                 const u32* __restrict__ src,
+                                                 const u32* __restrict__ freq, u64 n, u32 K, u32 C,
+                                                 Src in, Out out) {
+  constexpr int B = 8;
+  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 teams = ((u64)gridDim.x * blockDim.x) / G;
+  const u32 tl = threadIdx.x % G;
+  for (u64 t = gtid / G; t * K < n; t += teams) {
+    const u64 a = t * K, b = a + K < n ? a + K : n;  // K: items per team (runtime)
+    const u32 dfirst = dst[a], dlast = dst[b - 1];
+    const bool first_shared = a > 0 && dst[a - 1] == dfirst;
+    const bool last_shared = b < n && dst[b] == dlast;
+    for (u32 col = tl; col < C; col += G) {
+      u32 cd = dfirst;
+      u64 acc = 0;
+      for (u64 i0 = a; i0 < b; i0 += B) {
+        u64 v[B];
+        u32 dd[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+          const u64 i = i0 + j;
+          dd[j] = i < b ? dst[i] : 0xFFFFFFFFu;
+          v[j] = i < b ? Mode::combine(item_freq(freq, i), in(src[i], col)) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+          if (dd[j] == 0xFFFFFFFFu) break;
+          if (dd[j] != cd) {
+            u64* p = out(cd, col);
+            if (cd == dfirst && first_shared) Mode::atomic(p, acc);
+            else *p = Mode::merge(*p, acc);
+            cd = dd[j];
+            acc = 0;
+          }
+          acc = Mode::merge(acc, v[j]);
+        }
+      }
+      u64* p = out(cd, col);
+      if ((cd == dfirst && first_shared) || (cd == dlast && last_shared)) Mode::atomic(p, acc);
+      else *p = Mode::merge(*p, acc);
+    }
+  }
+}
+
+// Items per warp tile / team chunk: as large as possible (fewer boundary
+// atomics, longer carried runs) while still giving every SM a full load of
+// resident threads; small levels therefore run one step per warp instead of
+// a handful of warps walking long tiles serially.
+constexpr u64 kResidentThreads = 148ull * 2048ull;
+
+inline u64 pow2_floor(u64 x) {
+  u64 p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
+}
+
+// host launcher: picks the variant for C columns; n == 0 is a no-op.
+template <class Mode, class Src, class Out>
+void seg_reduce(const char* name, const u32* dst, const u32* src, const u32* freq, u64 n, u32 C,
+                Src in, Out out, cudaStream_t st) {
+  if (!n || !C) return;
+  if (C == 1) {
+    const int K = (int)std::min<u64>(16, std::max<u64>(1, pow2_floor(n / kResidentThreads)));
+    const u64 tiles = (n + 32ull * K - 1) / (32ull * K);
+    GT_KLAUNCH(name, (k_segred1<Mode, Src, Out>), grid_for(tiles * 32, 256, 148u * 32u), 256, st,
+               dst, src, freq, n, K, in, out);
+    return;
+  }
+#define GT_SEGRED_G(GG)                                                                           \
+  do {                                                                                            \
+    const u32 K = (u32)std::min<u64>(64, std::max<u64>(8, pow2_floor(n * GG / kResidentThreads))); \
+    const u64 chunks = (n + K - 1) / K;                                                           \
+    GT_KLAUNCH(name, (k_segredG<GG, Mode, Src, Out>), grid_for(chunks * GG, 256, 148u * 64u), 256, \
+               st, dst, src, freq, n, K, C, in, out);                                             \
+  } while (0)
+  if (C <= 2) GT_SEGRED_G(2);
+  else if (C <= 4) GT_SEGRED_G(4);
+  else if (C <= 8) GT_SEGRED_G(8);
+  else if (C <= 16) GT_SEGRED_G(16);
+  else GT_SEGRED_G(32);
+#undef GT_SEGRED_G
+}
+
+}  // namespace gt

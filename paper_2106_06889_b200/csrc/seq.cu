@@ -21,6 +21,7 @@
 #include <algorithm>
 
 #include "kernels_common.cuh"
+#include "segreduce.cuh"
 #include "seq.cuh"
 
 namespace gt {
@@ -184,24 +185,25 @@ __global__ void k_run_heads(const u64* key, const u32* gram, u64 n, u32 l, int p
   }
 }
 
-// dense per-run file counts: team of G lanes per run
-template <int G>
-__global__ void k_run_rows(const u32* run_start, u64 nruns, u64 n, const u32* __restrict__ src,
-                           const u64* __restrict__ w, u32 R, u32 C, u64* out) {
-  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  const u64 teams = ((u64)gridDim.x * blockDim.x) / G;
-  const u32 tl = threadIdx.x % G;
-  for (u64 t = gtid / G; t < nruns; t += teams) {
-    const u64 a = run_start[t], b = t + 1 < nruns ? run_start[t + 1] : n;
-    for (u32 col = tl; col < C; col += G) {
-      u64 acc = 0;
-      for (u64 i = a; i < b; i++) {
-        const u32 s = src[i];
-        acc += s < R ? w[(u64)s * C + col] : (s - R == col ? 1ull : 0ull);
-      }
-      out[t * C + col] = acc;
-    }
+// gram-run rows: an occurrence from rule s < R adds that rule's per-file
+// weight row; an occurrence counted directly in root segment s-R adds 1 to
+// that file's column
+struct SeqSrc {
+  const u64* w;
+  u32 R, C;
+  __device__ __forceinline__ u64 operator()(u32 s, u32 col) const {
+    return s < R ? w[(u64)s * C + col] : (s - R == col ? 1ull : 0ull);
   }
+};
+
+__global__ void k_heads_u32(const uint8_t* h, u64 n, u32* o) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) o[i] = h[i];
+}
+
+__global__ void k_dec_u32(u32* v, u64 n) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) v[i] -= 1;
 }
 
 __global__ void k_nz(const u64* v, u64 n, uint8_t* f) {
@@ -348,13 +350,16 @@ void run_sequences(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_ou
   const u64 NR = nruns * C;
   if (NR >= (1ull << 32)) fail(GT_E_RESOURCE, "%lu gram x file cells exceed the 2^32 limit", (unsigned long)NR);
   DBuf rows(NR * 8 + 8, st);
+  GT_CUDA(cudaMemsetAsync(rows.p, 0, NR * 8, st));
   if (nruns) {
-    if (C == 1) SL((k_run_rows<1>), nruns, runs.as<u32>(), nruns, N, ssrc.as<u32>(), w.as<u64>(), (u32)R, C, rows.as<u64>());
-    else if (C <= 8) SL((k_run_rows<8>), nruns * 8, runs.as<u32>(), nruns, N, ssrc.as<u32>(), w.as<u64>(), (u32)R, C, rows.as<u64>());
-    else if (C <= 16) SL((k_run_rows<16>), nruns * 16, runs.as<u32>(), nruns, N, ssrc.as<u32>(), w.as<u64>(), (u32)R, C, rows.as<u64>());
-    else SL((k_run_rows<32>), nruns * 32, runs.as<u32>(), nruns, N, ssrc.as<u32>(), w.as<u64>(), (u32)R, C, rows.as<u64>());
+    // run id of every occurrence = inclusive scan of the run heads - 1
+    DBuf h32(N * 4 + 4, st), rid(N * 4 + 4, st);
+    SL(k_heads_u32, N, heads.as<uint8_t>(), N, h32.as<u32>());
+    inclusive_scan_u32(h32.as<u32>(), rid.as<u32>(), N, st);
+    SL(k_dec_u32, N, rid.as<u32>(), N);
+    seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
+                        SeqSrc{w.as<u64>(), (u32)R, C}, OutRowMajor{rows.as<u64>(), C}, st);
   }
-  if (Fo == 0) GT_CUDA(cudaMemsetAsync(rows.p, 0, NR * 8, st));
   ssrc.release();
   heads.release();
   w.release();

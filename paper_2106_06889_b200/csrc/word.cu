@@ -23,207 +23,51 @@
 #include <type_traits>
 
 #include "kernels_common.cuh"
+#include "segreduce.cuh"
 #include "word.cuh"
 
 namespace gt {
 
-struct SumMode {
-  __device__ static __forceinline__ u64 combine(u64 acc, u32 f, u64 x) { return acc + (u64)f * x; }
-  __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a + b; }
-  __device__ static __forceinline__ void seed(u64& acc, u32 col, u32 seg_rel, u32 cnt) {
-    if (seg_rel == col) acc += cnt;
-  }
-  __device__ static __forceinline__ void atomic(u64* p, u64 v) {
-    if (v) atomicAdd((unsigned long long*)p, (unsigned long long)v);
-  }
-};
-
-struct OrMode {
-  __device__ static __forceinline__ u64 combine(u64 acc, u32, u64 x) { return acc | x; }
-  __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a | b; }
-  __device__ static __forceinline__ void seed(u64& acc, u32 col, u32 seg_rel, u32) {
-    if ((seg_rel >> 6) == col) acc |= 1ull << (seg_rel & 63u);
-  }
-  __device__ static __forceinline__ void atomic(u64* p, u64 v) {
-    if (v) atomicOr((unsigned long long*)p, (unsigned long long)v);
-  }
-};
-
+// Seeds of the top-down pass: the root's direct references, per owned
+// segment (rs lists sorted by (rule, segment)).  Global mode adds every owned
+// segment's count into row[rule]; per-file mode into row[rule*C + segment];
+// presence (OrMode) sets bit segment%64 of row[rule*C + segment/64].  Lanes
+// of a warp hitting the same cell are combined with a segmented shuffle scan
+// (keys ascend along the list), one atomic per run.
 template <class Mode>
-__device__ __forceinline__ u64 seed1(u64 acc, u32 col, u32 sg, u32 cnt) {
-  Mode::seed(acc, col, sg, cnt);
-  return acc;
-}
-
-// ---------------------------------------------------------------------------
-// level pull: rows out[c*C .. c*C+C) for the rules of one top-down level
-//   row(c) = seed(c) (+|) Σ_{p in parents(c), p != 0} f(p,c) · row(p)
-// ---------------------------------------------------------------------------
-template <int G, class Mode>
-__global__ void __launch_bounds__(256) k_td_level(const u32* __restrict__ order, u64 lo, u64 mid,
-                                                  u64 hi, const u64* __restrict__ par_off,
-                                                  const u32* __restrict__ par_ids,
-                                                  const u32* __restrict__ par_freqs,
-                                                  const u64* __restrict__ rs_off,
-                                                  const u32* __restrict__ rs_seg,
-                                                  const u32* __restrict__ rs_cnt, u32 file_lo,
-                                                  u32 nseg, u32 C, u32 per_file,
-                                                  u64* __restrict__ row) {
-  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  const u64 nthreads = (u64)gridDim.x * blockDim.x;
+__global__ void __launch_bounds__(256) k_seed(const u32* __restrict__ rs_rule, const u32* __restrict__ rs_seg,
+                                              const u32* __restrict__ rs_cnt, u64 n, u32 file_lo,
+                                              u32 nseg, int per_file, u32 C, u64* __restrict__ row) {
   const unsigned lane = threadIdx.x & 31u;
-  const u64 nlight = mid - lo;
-  // light rules: one team of G lanes per rule
-  {
-    const u64 teams = nthreads / G;
-    const u32 tl = lane % G;
-    for (u64 t = gtid / G; t < nlight; t += teams) {
-      const u32 c = order[lo + t];
-      const u64 e0 = par_off[c], e1 = par_off[c + 1];
-      const u64 s0 = rs_off[c], s1 = rs_off[c + 1];
-      for (u32 col = tl; col < C; col += G) {
-        u64 acc = 0;
-        for (u64 s = s0; s < s1; s++) {
-          u32 sg = rs_seg[s] - file_lo;
-          if (sg < nseg) acc = per_file ? seed1<Mode>(acc, col, sg, rs_cnt[s]) : Mode::merge(acc, (u64)rs_cnt[s]);
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const bool is_or = std::is_same<Mode, OrMode>::value;
+  for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const u64 i = base + threadIdx.x;
+    u64 key = ~0ull, v = 0;
+    if (i < n) {
+      const u32 sg = rs_seg[i] - file_lo;
+      if (sg < nseg) {
+        const u64 r = rs_rule[i];
+        if (!per_file) {
+          key = r;
+          v = rs_cnt[i];
+        } else if (is_or) {
+          key = r * C + (sg >> 6);
+          v = 1ull << (sg & 63u);
+        } else {
+          key = r * C + sg;
+          v = rs_cnt[i];
         }
-        for (u64 e = e0; e < e1; e++) {
-          const u32 p = par_ids[e];
-          if (p) acc = Mode::combine(acc, par_freqs[e], row[(u64)p * C + col]);
-        }
-        row[(u64)c * C + col] = acc;
       }
     }
-  }
-  // heavy rules: one warp per rule; 32/G stripes split the parent list
-  {
-    constexpr u32 S = 32 / G;
-    const u64 nheavy = hi - mid;
-    const u64 nw = nthreads >> 5;
-    const u32 col0 = lane % G, stripe = lane / G;
-    for (u64 w = gtid >> 5; w < nheavy; w += nw) {
-      const u32 c = order[mid + w];
-      const u64 e0 = par_off[c], e1 = par_off[c + 1];
-      const u64 s0 = rs_off[c], s1 = rs_off[c + 1];
-      for (u32 cb = 0; cb < C; cb += G) {
-        const u32 col = cb + col0;
-        const bool ok = col < C;
-        u64 acc = 0;
-        if (ok) {
-          for (u64 e = e0 + stripe; e < e1; e += S) {
-            const u32 p = par_ids[e];
-            if (p) acc = Mode::combine(acc, par_freqs[e], row[(u64)p * C + col]);
-          }
-        }
 #pragma unroll
-        for (u32 d = G; d < 32; d <<= 1) acc = Mode::merge(acc, __shfl_xor_sync(0xFFFFFFFFu, acc, d));
-        if (ok && stripe == 0) {
-          for (u64 s = s0; s < s1; s++) {
-            u32 sg = rs_seg[s] - file_lo;
-            if (sg < nseg) acc = per_file ? seed1<Mode>(acc, col, sg, rs_cnt[s]) : Mode::merge(acc, (u64)rs_cnt[s]);
-          }
-          row[(u64)c * C + col] = acc;
-        }
-      }
+    for (int d = 1; d < 32; d <<= 1) {
+      const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, d);
+      const u64 ok = __shfl_up_sync(0xFFFFFFFFu, key, d);
+      if (lane >= (unsigned)d && ok == key) v = Mode::merge(v, ov);
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// reduce-by-word, one column (global word count / F<=64 presence):
-//   out[v] = Σ_{(v,r,f) in ow, r != 0} f · row[r]   (Mode combine)
-// warp tiles of 32*K entries; runs interior to a tile are stored, runs that
-// touch a tile boundary are combined atomically.
-// ---------------------------------------------------------------------------
-template <int K, class Mode>
-__global__ void __launch_bounds__(256) k_reduce_words_1(const u32* __restrict__ ow_word,
-                                                        const u32* __restrict__ ow_rule,
-                                                        const u32* __restrict__ ow_freq, u64 n,
-                                                        const u64* __restrict__ row,
-                                                        u64* __restrict__ out) {
-  const unsigned lane = threadIdx.x & 31u;
-  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
-  constexpr u64 TILE = 32ull * K;
-  for (u64 t0 = warp * TILE; t0 < n; t0 += nwarps * TILE) {
-    const u32 first_word = ow_word[t0];
-    u32 carry_w = 0xFFFFFFFFu;
-    u64 carry_v = 0;
-#pragma unroll 4
-    for (int k = 0; k < K; k++) {
-      const u64 i = t0 + (u64)k * 32 + lane;
-      const bool ok = i < n;
-      const u32 wd = ok ? ow_word[i] : 0xFFFFFFFFu;
-      const u32 w0 = __shfl_sync(0xFFFFFFFFu, wd, 0);
-      if (carry_w != 0xFFFFFFFFu && w0 != carry_w) {  // carried run ended at the previous step
-        if (lane == 0) {
-          if (carry_w == first_word) Mode::atomic(&out[carry_w], carry_v);
-          else out[carry_w] = carry_v;
-        }
-        carry_w = 0xFFFFFFFFu;
-        carry_v = 0;
-      }
-      u64 v = 0;
-      if (ok) {
-        const u32 r = ow_rule[i];
-        if (r) v = Mode::combine(0, ow_freq[i], row[r]);
-      }
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, d);
-        u32 ow = __shfl_up_sync(0xFFFFFFFFu, wd, d);
-        if (lane >= (unsigned)d && ow == wd) v = Mode::merge(v, ov);
-      }
-      if (wd == carry_w) v = Mode::merge(v, carry_v);
-      const u32 nxt = __shfl_down_sync(0xFFFFFFFFu, wd, 1);
-      const bool last = lane == 31 || nxt != wd;
-      if (ok && last && lane != 31) {
-        if (wd == first_word) Mode::atomic(&out[wd], v);
-        else out[wd] = v;
-      }
-      carry_w = __shfl_sync(0xFFFFFFFFu, wd, 31);
-      carry_v = __shfl_sync(0xFFFFFFFFu, v, 31);
-    }
-    if (lane == 0 && carry_w != 0xFFFFFFFFu) Mode::atomic(&out[carry_w], carry_v);
-  }
-}
-
-// reduce-by-word, C columns: team of G lanes walks a chunk of K entries
-//   out[col*V + v] = Σ f · row[r*C + col]
-template <int G, int K, class Mode>
-__global__ void __launch_bounds__(256) k_reduce_words_cols(const u32* __restrict__ ow_word,
-                                                           const u32* __restrict__ ow_rule,
-                                                           const u32* __restrict__ ow_freq,
-                                                           u64 n, const u64* __restrict__ row,
-                                                           u32 C, u64 V, u64* __restrict__ out) {
-  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  const u64 teams = ((u64)gridDim.x * blockDim.x) / G;
-  const u32 tl = threadIdx.x % G;
-  for (u64 t = gtid / G; t * K < n; t += teams) {
-    const u64 a = t * K, b = min(n, a + K);
-    const u32 wfirst = ow_word[a];
-    const u32 wlast = ow_word[b - 1];
-    const bool shared_first = a > 0 && ow_word[a - 1] == wfirst;
-    const bool shared_last = b < n && ow_word[b] == wlast;
-    for (u32 col = tl; col < C; col += G) {
-      u32 cw = wfirst;
-      u64 acc = 0;
-      for (u64 i = a; i < b; i++) {
-        const u32 wd = ow_word[i];
-        if (wd != cw) {
-          u64* dst = &out[(u64)col * V + cw];
-          if (cw == wfirst && shared_first) Mode::atomic(dst, acc);
-          else *dst = acc;
-          cw = wd;
-          acc = 0;
-        }
-        const u32 r = ow_rule[i];
-        if (r) acc = Mode::combine(acc, ow_freq[i], row[(u64)r * C + col]);
-      }
-      u64* dst = &out[(u64)col * V + cw];
-      if ((cw == wfirst && shared_first) || shared_last) Mode::atomic(dst, acc);
-      else *dst = acc;
-    }
+    const u64 nk = __shfl_down_sync(0xFFFFFFFFu, key, 1);
+    if (key != ~0ull && (lane == 31 || nk != key)) Mode::atomic(&row[key], v);
   }
 }
 
@@ -238,12 +82,12 @@ __global__ void k_root_words(const u32* __restrict__ rw_word, const u32* __restr
     if (sg >= nseg) continue;
     u32 w = rw_word[i];
     if (!per_file) {
-      Mode::atomic(&out[w], Mode::combine(0, rw_cnt[i], 1ull));
+      Mode::atomic(&out[w], Mode::combine(rw_cnt[i], 1ull));
     } else {
-      u64 acc = 0;
-      u32 col = std::is_same<Mode, OrMode>::value ? (sg >> 6) : sg;
-      Mode::seed(acc, col, sg, rw_cnt[i]);
-      Mode::atomic(&out[(u64)col * V + w], acc);
+      const bool is_or = std::is_same<Mode, OrMode>::value;
+      const u32 col = is_or ? (sg >> 6) : sg;
+      const u64 v = is_or ? (1ull << (sg & 63u)) : (u64)rw_cnt[i];
+      Mode::atomic(&out[(u64)col * V + w], v);
     }
   }
 }
@@ -320,51 +164,33 @@ __global__ void k_ii_write(const u32* words, const u64* ngroups, const u64* pres
 
 #define KL(k, grid, ...) GT_KLAUNCH(#k, k, grid, 256, st, __VA_ARGS__)
 
-template <int G, class Mode>
-static void td_levels_G(const DeviceDag* d, u32 C, u32 per_file, u64* row) {
+// Top-down weights (Alg. 1, engine.py:196-227): rows of C columns per rule,
+// seeded from the root references, then one segmented gather-reduce launch
+// per top-down level over that level's non-root parent edges.
+template <class Mode>
+static void td_levels(const DeviceDag* d, u32 C, u64* row, u32 per_file = 1) {
   cudaStream_t st = d->stream;
-  const u32 nseg = (u32)(d->file_hi - d->file_lo);
+  GT_CUDA(cudaMemsetAsync(row, 0, sizeof(u64) * C * d->R, st));
+  if (d->n_rs)
+    KL(k_seed<Mode>, grid_for(d->n_rs, 256), d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(),
+       d->n_rs, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row);
   for (int L = 1; L <= d->td.nl; L++) {
-    u64 lo = d->td.off[L], mid = d->td.heavy_off[L], hi = d->td.off[L + 1];
-    if (hi == lo) continue;
-    u64 work = (mid - lo) * G + (hi - mid) * 32;
-    KL((k_td_level<G, Mode>), grid_for(work, 256, 148u * 64u), d->td.order.as<u32>(), lo, mid, hi,
-       d->par_off.as<u64>(), d->par_ids.as<u32>(), d->par_freqs.as<u32>(), d->rs_off.as<u64>(),
-       d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), (u32)d->file_lo, nseg, C, per_file, row);
+    const u64 a = d->te_off[L], n = d->te_off[L + 1] - a;
+    seg_reduce<Mode>("k_td_level", d->te_child.as<u32>() + a, d->te_par.as<u32>() + a,
+                     d->te_freq.as<u32>() + a, n, C, RowSrc{row, C}, OutRowMajor{row, C}, st);
   }
 }
 
-template <class Mode>
-static void td_levels(const DeviceDag* d, u32 C, u64* row, u32 per_file = 1) {
-  // root row stays zero: its own words are counted per segment (rw lists)
-  GT_CUDA(cudaMemsetAsync(row, 0, sizeof(u64) * C, d->stream));
-  if (C <= 1) td_levels_G<1, Mode>(d, C, per_file, row);
-  else if (C <= 2) td_levels_G<2, Mode>(d, C, per_file, row);
-  else if (C <= 4) td_levels_G<4, Mode>(d, C, per_file, row);
-  else if (C <= 8) td_levels_G<8, Mode>(d, C, per_file, row);
-  else if (C <= 16) td_levels_G<16, Mode>(d, C, per_file, row);
-  else td_levels_G<32, Mode>(d, C, per_file, row);
-}
-
+// Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
+// as a gather-reduce over the word-major own pairs, then the root's plain
+// words per owned segment (root_words_round, _kernels.py:175-188).
 template <class Mode>
 static void reduce_words(const DeviceDag* d, u32 C, const u64* row, u64* out, bool per_file) {
   cudaStream_t st = d->stream;
-  const u64 V = d->nw, n = d->E_own;
+  const u64 V = d->nw;
   GT_CUDA(cudaMemsetAsync(out, 0, sizeof(u64) * V * C, st));
-  if (n) {
-    if (C == 1) {
-      constexpr int K = 16;
-      u64 tiles = (n + 32 * K - 1) / (32 * K);
-      KL((k_reduce_words_1<K, Mode>), grid_for(tiles * 32, 256, 148u * 16u), d->ow_word.as<u32>(),
-         d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), n, row, out);
-    } else {
-      constexpr int K = 64;
-      u64 chunks = (n + K - 1) / K;
-      if (C <= 8) KL((k_reduce_words_cols<8, K, Mode>), grid_for(chunks * 8, 256, 148u * 32u), d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), n, row, C, V, out);
-      else if (C <= 16) KL((k_reduce_words_cols<16, K, Mode>), grid_for(chunks * 16, 256, 148u * 32u), d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), n, row, C, V, out);
-      else KL((k_reduce_words_cols<32, K, Mode>), grid_for(chunks * 32, 256, 148u * 32u), d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), n, row, C, V, out);
-    }
-  }
+  seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(),
+                   d->E_own, C, RowSrc{row, C}, OutColMajor{out, V}, st);
   if (d->n_rw)
     KL(k_root_words<Mode>, grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
        d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo),
