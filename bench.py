@@ -16,9 +16,14 @@ DAG build, both gt_runs, D2H of the results, gt_close).
 --impl reference times the reference's algorithm on the host cores through
 the CPU restatement in oracle/ (the reference itself is pure Python/numba and
 does not travel to the GPU box), on the same corpus, metric and step.
-Multi-GPU (torchrun): files are sharded by token-balanced ranges, the DAG is
-replicated, per-file outputs stay on their shard, global word counts are
-combined with an NCCL all-reduce; max-over-ranks timing.
+Multi-GPU (torchrun, one process per GPU, NCCL): by default (--shard-mode
+corpus, weak scaling) the collection is partitioned by files into N
+C2-shaped 16-file partitions, one grammar per GPU (rank 0's partition is the
+N=1 workload); the vocabulary count vectors are summed with an NCCL
+all-reduce (exact integer sums) and rank 0 assembles the global word count,
+per-file inverted-index outputs stay on their rank.  --shard-mode files
+(strong scaling) shards ONE corpus by token-balanced file ranges with the
+DAG replicated (gt_set_files).  Device time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -52,6 +57,9 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one profiled step, print kernel table")
+    ap.add_argument("--shard-mode", default="corpus", choices=["corpus", "files"],
+                    help="N>1: each rank owns its own 16-file partition of the collection "
+                         "(weak scaling, default) or a file range of one corpus (strong)")
     return ap.parse_args()
 
 
@@ -146,18 +154,6 @@ def alg_bytes(kernel: str, info: dict, files: int, tasks=TASKS) -> float | None:
     return tot
 
 
-def shard_ranges(tokens: np.ndarray, n: int):
-    """Token-balanced contiguous file ranges."""
-    F = len(tokens)
-    cum = np.concatenate([[0], np.cumsum(tokens)])
-    cuts = [0]
-    for k in range(1, n):
-        cuts.append(int(np.searchsorted(cum, cum[-1] * k / n)))
-    cuts.append(F)
-    cuts = np.maximum.accumulate(np.minimum(cuts, F))
-    return [(int(cuts[i]), int(cuts[i + 1])) for i in range(n)]
-
-
 def cpu_reference_steps(blob, steps, warmup, workers):
     """The reference algorithm on host cores (oracle/ restatement)."""
     from oracle.oracle import OracleDag
@@ -218,64 +214,81 @@ def main():
 
     import torch
     import paper_2106_06889_b200 as gt
+    from paper_2106_06889_b200.corpus import compose, config_spec
     from paper_2106_06889_b200.device import DeviceDag
+    from paper_2106_06889_b200.shard import shard_ranges
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    corpus_mode = world == 1 or args.shard_mode == "corpus"
 
-    blob, stats = composed(args)
-    # pinned host copy of the GTDC bytes (the e2e input)
+    # rank r's input: its own 16-file partition of the collection (corpus
+    # mode, weak scaling; rank 0's is the N=1 workload) or the whole corpus
+    # with a token-balanced file range (files mode, strong scaling)
+    base = config_spec(args.config, scale=args.scale)
+    seed = base.seed + (rank if corpus_mode else 0)
+    blob, stats = compose(config_spec(args.config, seed=seed, scale=args.scale))
     pinned = torch.empty(len(blob), dtype=torch.uint8, pin_memory=True)
     pinned.numpy()[:] = np.frombuffer(blob, dtype=np.uint8)
     src = (pinned.data_ptr(), len(blob))
 
-    full = DeviceDag(src, device=local)
-    info_full = full.info
-    W_total = info_full["words"]
-    if world > 1:
-        toks = full.dag_array("segment_token_counts")
-        lo, hi = shard_ranges(toks, world)[rank]
-        full.close()
-        dag = DeviceDag(src, device=local, file_lo=lo, file_hi=hi)
-    else:
-        lo, hi = 0, info_full["num_files"]
-        dag = full
+    dag = DeviceDag(src, device=local)
     info = dag.info
     V = info["num_words"]
+    if corpus_mode:
+        lo, hi = 0, info["num_files"]
+        W_rank = info["words"]
+    else:
+        toks = dag.dag_array("segment_token_counts")
+        lo, hi = shard_ranges(toks, world)[rank]
+        dag.set_files(lo, hi)
+        W_rank = int(toks[lo:hi].sum())
+    W_total = W_rank
+    if dist:
+        t = torch.tensor([W_rank], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        W_total = int(t.item())
+        if not corpus_mode:
+            assert W_total == info["words"]
 
-    counts_t = None
-    if world > 1:
-        class _CAI:  # __cuda_array_interface__ view of the library's dense counts
-            def __init__(self, ptr, n):
-                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<u8",
-                                                 "data": (ptr, False), "version": 3}
+    def counts_view(d):
+        ptr = d.device_word_counts_ptr()
 
-    def step(collect=None):
-        dev_ms = 0.0
-        launches = 0
-        d2h = 0
+        class _CAI:  # __cuda_array_interface__ view of the library's u64[V] counts
+            __cuda_array_interface__ = {"shape": (V,), "typestr": "<i8", "data": (ptr, False),
+                                        "version": 3}
+        return torch.as_tensor(_CAI(), device="cuda")
+
+    def step(d):
+        """word count (+ all-reduce of the vocab counts + rank-0 assembly when
+        N > 1) and inverted index; returns (device ms, launches, d2h bytes)."""
+        dev_ms, launches, d2h = 0.0, 0, 0
         for task in TASKS:
-            r, v = dag.run_raw(gt._abi.TASK_IDS[task])
+            r, v = d.run_raw(gt._abi.TASK_IDS[task])
             dev_ms += v.device_ms
             launches += v.kernel_launches
             d2h += v.d2h_bytes
-            dag.free_raw(r)
-            if task == "wordcount" and world > 1:
-                ptr = dag.device_word_counts_ptr()
-                t = torch.as_tensor(_CAI(ptr, V), device="cuda").view(torch.int64)
+            d.free_raw(r)
+            if task == "wordcount" and dist:
+                t = counts_view(d)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                dist.all_reduce(t)
+                dist.all_reduce(t)  # exact integer sums over NVLink
                 e1.record()
                 e1.synchronize()
                 dev_ms += e0.elapsed_time(e1)
+                if rank == 0:  # the global word-count result, render order
+                    c = d.assemble_counts(t.data_ptr(), gt._abi.TASK_IDS["wordcount"])
+                    dev_ms += c.timings["device_ms"]
+                    launches += c.timings["kernel_launches"]
+                    d2h += c.timings["d2h_bytes"]
         return dev_ms, launches, d2h
 
     if args.profile_only:
         dag.profile(True)
-        step()
+        step(dag)
         rep = dag.profile_report()
         dag.profile(False)
         for k, (n, ms) in sorted(rep.items(), key=lambda kv: -kv[1][1]):
@@ -283,7 +296,7 @@ def main():
         return
 
     for _ in range(args.warmup):
-        step()
+        step(dag)
 
     # ---- timed region: K steps, L2 flushed between steps (outside the events)
     step_ms, launches = [], 0
@@ -299,7 +312,7 @@ def main():
         for _ in range(args.steps):
             dag.flush_l2()
             dag.sync()
-            ms, nl, d2h_wc_ii = step()
+            ms, nl, _ = step(dag)
             step_ms.append(ms)
             launches += nl
     torch.cuda.synchronize()
@@ -317,13 +330,14 @@ def main():
 
     # ---- dominant kernel of the timed region + roofline
     K = args.steps
-    named = {k: v for k, v in rep.items() if alg_bytes(k, info, hi - lo) is not None}
+    Fo = hi - lo
+    named = {k: v for k, v in rep.items() if alg_bytes(k, info, Fo) is not None}
     peak, peak_src = peaks()
     roof = None
     if named:
         k_dom = max(named, key=lambda k: named[k][1])
         n_l, ms_l = named[k_dom]
-        b = alg_bytes(k_dom, info, hi - lo)  # per step
+        b = alg_bytes(k_dom, info, Fo)  # per step
         ach = b * K / (ms_l / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": k_dom, "launches_per_step": n_l / K,
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
@@ -332,19 +346,18 @@ def main():
     kernel_table = {k: {"launches_per_step": n / K, "ms_per_step": round(ms / K, 5)} for k, (n, ms) in
                     sorted(rep.items(), key=lambda kv: -kv[1][1])[:12]}
 
-    # ---- e2e through the public C-ABI from pinned host bytes
+    # ---- e2e through the public C-ABI from pinned host bytes: gt_open (H2D +
+    # device DAG build) + the step (+ collective) + D2H of results + gt_close
     e2e_times, d2h_bytes = [], 0
     for i in range(max(2, min(args.steps, 5)) + 1):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        d = DeviceDag(src, device=local, file_lo=lo, file_hi=hi) if world > 1 else DeviceDag(src, device=local)
-        nb = 0
-        for task in TASKS:
-            r, v = d.run_raw(gt._abi.TASK_IDS[task])
-            nb += v.d2h_bytes
-            d.free_raw(r)
+        d = DeviceDag(src, device=local)
+        if not corpus_mode:
+            d.set_files(lo, hi)
+        _, _, nb = step(d)
         d.close()
         el = time.perf_counter() - t0
         if i:
@@ -355,30 +368,33 @@ def main():
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    h2d = info["total_elements"] * 4 + info["num_rules"] * 16 + 8
+    h2d = len(blob)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         _, times, _, _ = cpu_reference_steps(blob, 3, 1, cores)
         tc = statistics.mean(times)
-        cpu = {"value": W_total / tc, "unit": UNIT, "cores": cores, "kind": "port",
+        cpu = {"value": W_rank / tc, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"whole {args.config} corpus, 3 steps of wordcount+invertedindex (oracle/ C restatement)"}
 
     if rank == 0:
+        par = (f"{world} corpus partitions x 1 GPU (weak)" if corpus_mode and world > 1 else
+               f"file-range shards x{world}, DAG replicated (strong)" if world > 1 else "1 GPU")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic (composed Zipfian grammar, seed 2; composer in paper_2106_06889_b200/corpus.py)",
+            "scaling": "weak" if corpus_mode else "strong", "vs_baseline": None, "dtype": "u64",
+            "data": f"synthetic (composed Zipfian grammar, seed {base.seed}{'+rank' if corpus_mode and world > 1 else ''}; "
+                    "composer in paper_2106_06889_b200/corpus.py)",
             "config": {"workload": f"{args.config}: word count + inverted index per step",
                        "scale": args.scale, "l2": "flushed between steps (256 MiB memset)",
-                       "R": info_full["num_rules"], "E": info_full["total_elements"],
-                       "L0": info_full["root_len"], "E_sub": info_full["sub_pairs"],
-                       "E_own": info_full["own_pairs"], "W": W_total, "F": info_full["num_files"],
-                       "V": info_full["num_words"], "depth": info_full["depth"],
-                       "rho": W_total / max(1, info_full["total_elements"]),
-                       "parallelism": f"file-sharded x{world}"},
+                       "R": info["num_rules"], "E": info["total_elements"],
+                       "L0": info["root_len"], "E_sub": info["sub_pairs"],
+                       "E_own": info["own_pairs"], "E_td": info["td_edges"], "W": W_total,
+                       "W_rank0": W_rank, "F": info["num_files"], "V": V, "depth": info["depth"],
+                       "rho": info["words"] / max(1, info["total_elements"]),
+                       "parallelism": par},
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": W_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_s * 1e3},

@@ -150,6 +150,16 @@ int gt_result_view(const gt_result* res, gt_view* out);
 void gt_result_free(gt_result* res);
 void gt_close(gt_ctx* ctx);
 
+/* Multi-GPU sharding: restrict per-file work and root seeds of
+ * subsequent gt_run calls to files [file_lo, file_hi) (clamped to F); the
+ * DAG itself is replicated in every context. */
+int gt_set_files(gt_ctx* ctx, uint64_t file_lo, uint64_t file_hi);
+
+/* WORDCOUNT / SORT result from a dense u64[num_words] DEVICE vector on the
+ * context's device (e.g. the NCCL all-reduce of every shard's
+ * gt_device_word_counts): the assembly half of gt_run. */
+int gt_assemble_counts(gt_ctx* ctx, int task, const uint64_t* dev_counts, gt_result** out);
+
 /* Dense global word counts left on the device by the last WORDCOUNT/SORT run
  * (u64[num_words]); for NCCL all-reduce across shards.  Returns the device
  * pointer or NULL. */

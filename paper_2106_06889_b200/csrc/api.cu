@@ -207,6 +207,38 @@ static const T* pull(gt_result* r, const DBuf& b, u64 n, cudaStream_t st, u64* b
   return (const T*)h;
 }
 
+static void finish(gt_ctx* c, gt_result* r, DevRecords& R, int task, int seq_len, int wbits,
+                   int strat, std::chrono::steady_clock::time_point t0, u64 launches0) {
+  cudaStream_t st = c->d.stream;
+  u64 bytes = 0;
+  gt_view& v = r->v;
+  v.task = task;
+  v.seq_len = seq_len;
+  v.wbits = wbits;
+  v.strategy = strat;
+  v.n = R.n;
+  v.n_groups = R.n_groups;
+  const u64 l = (u64)seq_len;
+  v.group_off = pull<uint64_t>(r, R.group_off, R.n_groups + 1, st, &bytes);
+  v.group_id = pull<uint32_t>(r, R.group_id, R.n_groups, st, &bytes);
+  v.group_key = pull<uint64_t>(r, R.group_key, R.n_groups, st, &bytes);
+  v.group_gram = pull<uint32_t>(r, R.group_gram, R.n_groups * l, st, &bytes);
+  v.id = pull<uint32_t>(r, R.id, R.n, st, &bytes);
+  v.key = pull<uint64_t>(r, R.key, R.n, st, &bytes);
+  v.gram = pull<uint32_t>(r, R.gram, R.n * l, st, &bytes);
+  v.count = pull<uint64_t>(r, R.count, R.n, st, &bytes);
+  GT_CUDA(cudaEventRecord(c->ev[2], st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  float ms = 0, ms2 = 0;
+  GT_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  GT_CUDA(cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]));
+  v.device_ms = ms;
+  v.d2h_ms = ms2;
+  v.d2h_bytes = bytes;
+  v.kernel_launches = g_launches - launches0;
+  v.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 extern "C" {
 
 int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, gt_result** out) {
@@ -226,7 +258,18 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
     DevRecords R;
     int wbits = 0;
     const u32 Fo = (u32)(d.file_hi - d.file_lo);
-    switch (task) {
+    // an empty shard has no per-file output (word counts stay a zero vector)
+    const bool empty_shard = Fo == 0 && task != GT_WORDCOUNT && task != GT_SORT;
+    switch (empty_shard ? -1 : task) {
+      case -1: {
+        if (task == GT_TERMVECTOR || task == GT_SEQCOUNT || task == GT_RANKEDINVERTEDINDEX ||
+            task == GT_INVERTEDINDEX) {
+          R.group_off.alloc(8, st);
+          GT_CUDA(cudaMemsetAsync(R.group_off.p, 0, 8, st));
+        }
+        if (task >= GT_SEQCOUNT) wbits = (u64)seq_len * std::max(1, bitlen(d.nw ? d.nw - 1 : 1)) <= 63 ? std::max(1, bitlen(d.nw ? d.nw - 1 : 1)) : 0;
+        break;
+      }
       case GT_WORDCOUNT:
       case GT_SORT: {
         td_word_counts(&d, d.word_counts);
@@ -256,33 +299,39 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
       }
     }
     GT_CUDA(cudaEventRecord(c->ev[1], st));
-    u64 bytes = 0;
-    gt_view& v = r->v;
-    v.task = task;
-    v.seq_len = seq_len;
-    v.wbits = wbits;
-    v.strategy = strat;
-    v.n = R.n;
-    v.n_groups = R.n_groups;
-    const u64 l = (u64)seq_len;
-    v.group_off = pull<uint64_t>(r, R.group_off, R.n_groups + 1, st, &bytes);
-    v.group_id = pull<uint32_t>(r, R.group_id, R.n_groups, st, &bytes);
-    v.group_key = pull<uint64_t>(r, R.group_key, R.n_groups, st, &bytes);
-    v.group_gram = pull<uint32_t>(r, R.group_gram, R.n_groups * l, st, &bytes);
-    v.id = pull<uint32_t>(r, R.id, R.n, st, &bytes);
-    v.key = pull<uint64_t>(r, R.key, R.n, st, &bytes);
-    v.gram = pull<uint32_t>(r, R.gram, R.n * l, st, &bytes);
-    v.count = pull<uint64_t>(r, R.count, R.n, st, &bytes);
-    GT_CUDA(cudaEventRecord(c->ev[2], st));
-    GT_CUDA(cudaStreamSynchronize(st));
-    float ms = 0, ms2 = 0;
-    GT_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-    GT_CUDA(cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]));
-    v.device_ms = ms;
-    v.d2h_ms = ms2;
-    v.d2h_bytes = bytes;
-    v.kernel_launches = g_launches - launches0;
-    v.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    finish(c, r, R, task, seq_len, wbits, strat, t0, launches0);
+  });
+  if (status != GT_OK) {
+    delete r;
+    return status;
+  }
+  *out = r;
+  return GT_OK;
+}
+
+int gt_set_files(gt_ctx* c, uint64_t file_lo, uint64_t file_hi) {
+  return guard([&] {
+    DeviceDag& d = c->d;
+    if (file_lo > file_hi) fail(GT_E_USAGE, "file range [%lu, %lu) is empty-reversed", (unsigned long)file_lo, (unsigned long)file_hi);
+    d.file_lo = std::min<u64>(file_lo, d.F);
+    d.file_hi = std::min<u64>(file_hi, d.F);
+  });
+}
+
+int gt_assemble_counts(gt_ctx* c, int task, const uint64_t* dev_counts, gt_result** out) {
+  *out = nullptr;
+  gt_result* r = new gt_result();
+  int status = guard([&] {
+    if (task != GT_WORDCOUNT && task != GT_SORT) fail(GT_E_USAGE, "gt_assemble_counts: task %d is not wordcount/sort", task);
+    DeviceDag& d = c->d;
+    GT_CUDA(cudaSetDevice(d.device));
+    auto t0 = std::chrono::steady_clock::now();
+    u64 launches0 = g_launches;
+    GT_CUDA(cudaEventRecord(c->ev[0], d.stream));
+    DevRecords R;
+    assemble_counts(&d, dev_counts, d.nw, 0, task == GT_SORT, &R);
+    GT_CUDA(cudaEventRecord(c->ev[1], d.stream));
+    finish(c, r, R, task, 3, 0, GT_TOPDOWN, t0, launches0);
   });
   if (status != GT_OK) {
     delete r;
@@ -303,10 +352,14 @@ uint64_t* gt_device_word_counts(gt_ctx* c) { return c->d.word_counts.as<uint64_t
 
 int gt_flush_l2(gt_ctx* c) {
   return guard([&] {
-    static thread_local DBuf buf;
-    const size_t n = 256ull << 20;  // 256 MiB > 126 MB L2
-    if (buf.bytes < n) buf.alloc(n, c->d.stream);
-    GT_CUDA(cudaMemsetAsync(buf.p, (int)(g_launches & 0xFF), n, c->d.stream));
+    // one 256 MiB (> 126 MB L2) scratch per device, deliberately never freed:
+    // a static destructor calling into CUDA after context teardown at exit
+    // would crash the process
+    static void* bufs[64] = {};
+    const size_t n = 256ull << 20;
+    void*& buf = bufs[c->d.device & 63];
+    if (!buf) GT_CUDA(cudaMalloc(&buf, n));
+    GT_CUDA(cudaMemsetAsync(buf, (int)(g_launches & 0xFF), n, c->d.stream));
   });
 }
 

@@ -23,7 +23,8 @@ from .gtdc import GrammarView
 LIB_PATH = Path(__file__).resolve().parent / "libgtadoc_b200.so"
 EXPORTS = ("gt_abi_version", "gt_last_error", "gt_open", "gt_info_get", "gt_run",
            "gt_result_view", "gt_result_free", "gt_close", "gt_device_word_counts",
-           "gt_dag_array", "gt_flush_l2", "gt_sync", "gt_profile", "gt_profile_report")
+           "gt_dag_array", "gt_flush_l2", "gt_sync", "gt_profile", "gt_profile_report",
+           "gt_set_files", "gt_assemble_counts")
 _lib = None
 
 
@@ -54,6 +55,8 @@ def lib():
         L.gt_profile.argtypes = [C.c_void_p, C.c_int]
         L.gt_profile_report.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
         L.gt_profile_report.restype = C.c_int64
+        L.gt_set_files.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+        L.gt_assemble_counts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
         _lib = L
     return _lib
 
@@ -121,6 +124,22 @@ class DeviceDag:
     @staticmethod
     def free_raw(r) -> None:
         lib().gt_result_free(r)
+
+    def set_files(self, file_lo: int, file_hi: int) -> None:
+        """Restrict subsequent runs to files [file_lo, file_hi) (gt_set_files)."""
+        raise_for_status(lib().gt_set_files(self._h, file_lo, file_hi), _err())
+
+    def assemble_counts(self, dev_ptr: int, task: int):
+        """wordcount/sort result from a dense u64[V] device vector (gt_assemble_counts)."""
+        L = lib()
+        r = C.c_void_p()
+        raise_for_status(L.gt_assemble_counts(self._h, task, C.c_void_p(dev_ptr), C.byref(r)), _err())
+        try:
+            v = GtView()
+            L.gt_result_view(r, C.byref(v))
+            return compact_from_view(v)
+        finally:
+            L.gt_result_free(r)
 
     def device_word_counts_ptr(self) -> int:
         return lib().gt_device_word_counts(self._h) or 0

@@ -1,0 +1,63 @@
+"""Device file-range shards (gt_set_files) combined == the whole-corpus result,
+for every task, on one GPU (the multi-GPU run differs only in where the
+shards live).  Word counts are combined on the device like the NCCL
+all-reduce: the shards' dense count vectors are summed in a torch tensor and
+assembled with gt_assemble_counts."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import gtdc
+from test_shard_cpu import TASKS, same_compact
+
+pytestmark = pytest.mark.gpu
+
+
+def composed(name, scale):
+    from paper_2106_06889_b200.corpus import compose, config_spec
+    return compose(config_spec(name, scale=scale))[0]
+
+
+@pytest.mark.parametrize("src", ["g1", "many_files_70", "composed_2", "c2@0.003", "c3@0.003"])
+@pytest.mark.parametrize("nshards", [2, 3, 5])
+def test_device_shards_combine_to_whole(src, nshards):
+    import torch
+
+    import paper_2106_06889_b200 as gt
+    from paper_2106_06889_b200._abi import TASK_IDS
+    from paper_2106_06889_b200.shard import DeviceRunner, combine
+    blob = composed(*src.split("@")[0:1], float(src.split("@")[1])) if "@" in src else gtdc(src)
+    dag = gt.DeviceDag(blob)
+    V = dag.info["num_words"]
+    for l in (2, 3):
+        full = {t: gt.run_compact(dag, t, gt.TraversalConfig(), l) for t in TASKS}
+        for task in TASKS:
+            if task in ("wordcount", "sort"):
+                acc = torch.zeros(V, dtype=torch.int64, device="cuda")
+                for rank in range(nshards):
+                    r = DeviceRunner(dag, rank, nshards)
+                    r.run(TASK_IDS["wordcount"], l, 0, 64)
+                    acc += r.counts_tensor()
+                got = r.assemble(acc, task)
+            else:
+                parts = []
+                for rank in range(nshards):
+                    r = DeviceRunner(dag, rank, nshards)
+                    parts.append(r.run(TASK_IDS[task], l, 0, 64))
+                got = combine(parts, task, V)
+            same_compact(got, full[task])
+        dag.set_files(0, 1 << 62)
+    dag.close()
+
+
+def test_empty_shard_outputs_are_empty():
+    import paper_2106_06889_b200 as gt
+    with gt.DeviceDag(gtdc("many_files_70")) as dag:
+        dag.set_files(5, 5)
+        for task in TASKS:
+            c = gt.run_compact(dag, task, gt.TraversalConfig(), 3)
+            assert c.n == 0, task
+        dag.set_files(0, 1 << 62)
+        assert gt.run_compact(dag, "wordcount", gt.TraversalConfig()).n > 0
