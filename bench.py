@@ -217,11 +217,18 @@ def main():
     from paper_2106_06889_b200.corpus import compose, config_spec
     from paper_2106_06889_b200.device import DeviceDag
     from paper_2106_06889_b200.shard import shard_ranges
+    # GT_BENCH_BACKEND=gloo lets a 1-GPU box exercise the N>1 code path
+    # (ranks share device local % device_count); real runs use NCCL
+    backend = os.environ.get("GT_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     corpus_mode = world == 1 or args.shard_mode == "corpus"
 
     # rank r's input: its own 16-file partition of the collection (corpus

@@ -63,8 +63,10 @@ enum gt_task {
   GT_RANKEDINVERTEDINDEX = 5
 };
 
-/* engine.py:31 STRATEGIES */
-enum gt_strategy { GT_AUTO = 0, GT_TOPDOWN = 1, GT_BOTTOMUP = 2 };
+/* engine.py:31 STRATEGIES (requests).  gt_view.strategy reports what ran:
+ * GT_TOPDOWN_SPARSE is the presence-guided sparse per-file top-down pass the
+ * library uses where the reference goes bottom-up for many files. */
+enum gt_strategy { GT_AUTO = 0, GT_TOPDOWN = 1, GT_BOTTOMUP = 2, GT_TOPDOWN_SPARSE = 3 };
 
 typedef struct gt_ctx gt_ctx;
 typedef struct gt_result gt_result;

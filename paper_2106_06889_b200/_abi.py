@@ -26,6 +26,7 @@ TASK_IDS = {
 TASK_NAMES = tuple(TASK_IDS)
 STRATEGY_IDS = {"auto": 0, "topdown": 1, "bottomup": 2}
 STRATEGY_NAMES = {v: k for k, v in STRATEGY_IDS.items()}
+STRATEGY_NAMES[3] = "topdown-sparse"  # GT_TOPDOWN_SPARSE (reported, not requested)
 
 _EXC = {
     GT_E_USAGE: UsageError,

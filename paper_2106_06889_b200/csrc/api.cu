@@ -18,6 +18,7 @@
 
 #include "gt_internal.cuh"
 #include "seq.cuh"
+#include "sparse.cuh"
 #include "word.cuh"
 
 namespace gt {
@@ -278,10 +279,17 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
         break;
       }
       case GT_TERMVECTOR: {
-        DBuf cnt;
-        td_file_counts(&d, cnt);
-        assemble_counts(&d, cnt.as<u64>(), d.nw, Fo, true, &R);
-        strat = GT_TOPDOWN;
+        // the reference goes bottom-up for F > file_set_width; the device
+        // equivalent is the presence-guided sparse per-file pass (sparse.cu)
+        if (strat == GT_BOTTOMUP || (u64)Fo * d.nw >= (1ull << 32)) {
+          sparse_term_vector(&d, &R);
+          strat = GT_TOPDOWN_SPARSE;
+        } else {
+          DBuf cnt;
+          td_file_counts(&d, cnt);
+          assemble_counts(&d, cnt.as<u64>(), d.nw, Fo, true, &R);
+          strat = GT_TOPDOWN;
+        }
         break;
       }
       case GT_INVERTEDINDEX: {
@@ -293,8 +301,9 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
         break;
       }
       default: {
-        run_sequences(&d, task, seq_len, &R, &wbits);
-        strat = GT_TOPDOWN;
+        const bool sparse = strat == GT_BOTTOMUP;
+        run_sequences(&d, task, seq_len, sparse, &R, &wbits);
+        strat = sparse ? GT_TOPDOWN_SPARSE : GT_TOPDOWN;
         break;
       }
     }

@@ -65,6 +65,25 @@ void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 
   }, s);
 }
 
+void sort_pairs_u64_u64(u64* ki, u64* ko, u64* vi, u64* vo, u64 n, int end_bit, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::SortPairs64x64", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceRadixSort::SortPairs(t, b, ki, ko, vi, vo, (int64_t)n, 0, end_bit, s));
+  }, s);
+}
+
+void reduce_by_key_u64(const u64* keys, const u64* vals, u64* ukeys, u64* sums, u64* d_nruns, u64 n,
+                       cudaStream_t s) {
+  if (!n) {
+    GT_CUDA(cudaMemsetAsync(d_nruns, 0, sizeof(u64), s));
+    return;
+  }
+  with_temp("cub::ReduceByKey", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceReduce::ReduceByKey(t, b, keys, ukeys, vals, sums, d_nruns, ::cuda::std::plus<u64>(),
+                                           (int64_t)n, s));
+  }, s);
+}
+
 void reduce_max_u64(const u64* in, u64* out, u64 n, cudaStream_t s) {
   if (!n) {
     GT_CUDA(cudaMemsetAsync(out, 0, sizeof(u64), s));

@@ -150,6 +150,11 @@ void inclusive_scan_u32(const u32* in, u32* out, u64 n, cudaStream_t s);
 // ordered compaction of indices i in [0,n) with flags[i] != 0; count -> d_count
 void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 n, cudaStream_t s);
 void reduce_max_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
+void sort_pairs_u64_u64(u64* keys_in, u64* keys_out, u64* vals_in, u64* vals_out, u64 n, int end_bit,
+                        cudaStream_t s);
+// runs of equal keys (sorted input) -> unique keys, sums, run count (device)
+void reduce_by_key_u64(const u64* keys, const u64* vals, u64* ukeys, u64* sums, u64* d_nruns, u64 n,
+                       cudaStream_t s);
 
 // launch bookkeeping
 extern thread_local u64 g_launches;

@@ -23,6 +23,7 @@
 #include "kernels_common.cuh"
 #include "segreduce.cuh"
 #include "seq.cuh"
+#include "sparse.cuh"
 
 namespace gt {
 
@@ -211,31 +212,50 @@ __global__ void k_nz(const u64* v, u64 n, uint8_t* f) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f[i] = v[i] != 0;
 }
 
-// records (run, col, count) -> sort key (major << CB) | (W - count)
-__global__ void k_rec_keys(const u32* sel, const u64* nsel, const u64* rows, u32 C, u64 W, int CB,
-                           int by_file, u64* skey, u32* rec) {
+// dense rows -> cells: selected index j = run*C + col
+__global__ void k_cells_dense(const u32* sel, const u64* nsel, const u64* rows, u32 C, u32* crun,
+                              u32* ccol, u64* ccnt) {
   u64 n = *nsel;
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    u32 j = sel[i];
-    u64 run = j / C, col = j % C;
-    skey[i] = ((by_file ? col : run) << CB) | (W - rows[j]);
-    rec[i] = j;
+    const u32 j = sel[i];
+    crun[i] = j / C;
+    ccol[i] = j % C;
+    ccnt[i] = rows[j];
   }
 }
 
-__global__ void k_rec_out(const u32* rec, u64 n, const u64* rows, u32 C, const u32* run_start,
-                          const u64* skey_sorted, const u32* gram, u32 l, int packed, u32 file_lo,
-                          int write_gram, u64* key_out, u32* gram_out, u64* cnt_out, u32* id_out,
-                          u32* major_out) {
+// sparse cells: key = run << FB | col
+__global__ void k_cells_keys(const u64* key, u64 n, int FB, u32* crun, u32* ccol) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    u32 j = rec[i];
-    u32 run = j / C, col = j % C;
-    cnt_out[i] = rows[j];
+    crun[i] = (u32)(key[i] >> FB);
+    ccol[i] = (u32)(key[i] & ((1ull << FB) - 1));
+  }
+}
+
+// cells (run, col, count) -> sort key (major << CB) | (W - count)
+__global__ void k_rec_keys(const u32* crun, const u32* ccol, const u64* ccnt, u64 n, u64 W, int CB,
+                           int by_file, u64* skey, u32* rec) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    skey[i] = ((u64)(by_file ? ccol[i] : crun[i]) << CB) | (W - ccnt[i]);
+    rec[i] = (u32)i;
+  }
+}
+
+__global__ void k_rec_out(const u32* rec, u64 n, const u32* crun, const u32* ccol, const u64* ccnt,
+                          const u32* run_start, const u64* skey_sorted, const u32* gram, u32 l,
+                          int packed, u32 file_lo, int write_gram, u64* key_out, u32* gram_out,
+                          u64* cnt_out, u32* id_out, u32* major_out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 j = rec[i];
+    const u32 run = crun[j], col = ccol[j];
+    cnt_out[i] = ccnt[j];
     if (id_out) id_out[i] = file_lo + col;
     if (major_out) major_out[i] = col;
-    u32 rs = run_start[run];
+    const u32 rs = run_start[run];
     if (write_gram) {
       if (packed) key_out[i] = skey_sorted[rs];
       else
@@ -244,13 +264,13 @@ __global__ void k_rec_out(const u32* rec, u64 n, const u64* rows, u32 C, const u
   }
 }
 
-__global__ void k_group_heads(const u32* rec, u64 n, u32 C, uint8_t* h) {
+__global__ void k_group_heads(const u32* rec, u64 n, const u32* crun, uint8_t* h) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    h[i] = i == 0 || rec[i] / C != rec[i - 1] / C;
+    h[i] = i == 0 || crun[rec[i]] != crun[rec[i - 1]];
 }
 
-__global__ void k_group_out(const u32* gsel, const u64* ng_p, const u32* rec, u32 C,
+__global__ void k_group_out(const u32* gsel, const u64* ng_p, const u32* rec, const u32* crun,
                             const u32* run_start, const u64* keys, const u32* gram, u32 l,
                             int packed, u64* goff, u64* gkey, u32* ggram) {
   u64 ng = *ng_p;
@@ -258,7 +278,7 @@ __global__ void k_group_out(const u32* gsel, const u64* ng_p, const u32* rec, u3
   for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += stride) {
     u32 i = gsel[g];
     goff[g] = i;
-    u32 rs = run_start[rec[i] / C];
+    u32 rs = run_start[crun[rec[i]]];
     if (packed) gkey[g] = keys[rs];
     else
       for (u32 k = 0; k < l; k++) ggram[(u64)g * l + k] = gram[(u64)rs * l + k];
@@ -277,7 +297,7 @@ static T d2h1(const void* p, cudaStream_t st) {
 
 }  // namespace
 
-void run_sequences(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out) {
+void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, int* wbits_out) {
   cudaStream_t st = d->stream;
   const u32 l = (u32)l_, m = l - 1;
   const u64 R = d->R, E = d->E, nw = d->nw, base = d->nw + d->ns;
@@ -301,10 +321,17 @@ void run_sequences(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_ou
            nw, base, d->exp_len.as<u64>(), m, H.as<u32>(), T.as<u32>(), hl.as<u32>(), tl.as<u32>());
     }
   }
-  // per-file rule weights (top-down, F columns)
+  // per-file rule weights: dense top-down rows (F columns) or, for many
+  // files, the presence-guided sparse (rule, file) weights (sparse.cu)
   DBuf w;
-  u32 Cw;
-  td_file_weights(d, w, &Cw);
+  SparseW sw;
+  if (sparse) {
+    u32 FW;
+    sparse_file_weights(d, &sw, nullptr, &FW);
+  } else {
+    u32 Cw;
+    td_file_weights(d, w, &Cw);
+  }
 
   // phase 2: windows attributed per body position (two passes + scan)
   WinCtx c{d->body.as<u32>(), d->pos_owner.as<u32>(), d->boff.as<u64>(), d->root_seg.as<u32>(),
@@ -347,36 +374,54 @@ void run_sequences(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_ou
   SL(k_run_heads, N, skey.as<u64>(), sgram.as<u32>(), N, l, packed, heads.as<uint8_t>());
   select_flagged_index(heads.as<uint8_t>(), runs.as<u32>(), dcnt.as<u64>(), N, st);
   const u64 nruns = d2h1<u64>(dcnt.p, st);
-  const u64 NR = nruns * C;
-  if (NR >= (1ull << 32)) fail(GT_E_RESOURCE, "%lu gram x file cells exceed the 2^32 limit", (unsigned long)NR);
-  DBuf rows(NR * 8 + 8, st);
-  GT_CUDA(cudaMemsetAsync(rows.p, 0, NR * 8, st));
+  // run id of every occurrence = inclusive scan of the run heads - 1
+  DBuf rid(N * 4 + 4, st);
   if (nruns) {
-    // run id of every occurrence = inclusive scan of the run heads - 1
-    DBuf h32(N * 4 + 4, st), rid(N * 4 + 4, st);
+    DBuf h32(N * 4 + 4, st);
     SL(k_heads_u32, N, heads.as<uint8_t>(), N, h32.as<u32>());
     inclusive_scan_u32(h32.as<u32>(), rid.as<u32>(), N, st);
     SL(k_dec_u32, N, rid.as<u32>(), N);
-    seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
-                        SeqSrc{w.as<u64>(), (u32)R, C}, OutRowMajor{rows.as<u64>(), C}, st);
+  }
+  heads.release();
+  // nonzero (run, file) cells in (gram asc, file asc) order
+  DBuf crun, ccol, ccnt;
+  u64 n = 0;
+  if (sparse) {
+    const int FB = std::max(1, bitlen(C - 1));
+    DBuf ckey;
+    n = sparse_run_cells(d, sw, rid.as<u32>(), ssrc.as<u32>(), nruns ? N : 0, FB, ckey, ccnt);
+    crun.alloc(n * 4 + 4, st);
+    ccol.alloc(n * 4 + 4, st);
+    SL(k_cells_keys, n, ckey.as<u64>(), n, FB, crun.as<u32>(), ccol.as<u32>());
+    sw = SparseW();
+  } else {
+    const u64 NR = nruns * C;
+    if (NR >= (1ull << 32)) fail(GT_E_RESOURCE, "%lu gram x file cells exceed the 2^32 limit", (unsigned long)NR);
+    DBuf rows(NR * 8 + 8, st);
+    GT_CUDA(cudaMemsetAsync(rows.p, 0, NR * 8, st));
+    if (nruns)
+      seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
+                          SeqSrc{w.as<u64>(), (u32)R, C}, OutRowMajor{rows.as<u64>(), C}, st);
+    w.release();
+    DBuf nzf(NR + 1, st), sel(NR * 4 + 4, st);
+    SL(k_nz, NR, rows.as<u64>(), NR, nzf.as<uint8_t>());
+    select_flagged_index(nzf.as<uint8_t>(), sel.as<u32>(), dcnt.as<u64>(), NR, st);
+    n = d2h1<u64>(dcnt.p, st);
+    crun.alloc(n * 4 + 4, st);
+    ccol.alloc(n * 4 + 4, st);
+    ccnt.alloc(n * 8 + 8, st);
+    SL(k_cells_dense, n, sel.as<u32>(), dcnt.as<u64>(), rows.as<u64>(), C, crun.as<u32>(),
+       ccol.as<u32>(), ccnt.as<u64>());
   }
   ssrc.release();
-  heads.release();
-  w.release();
-
-  // nonzero (run, file) cells in (gram asc, file asc) order
-  DBuf nzf(NR + 1, st), sel(NR * 4 + 4, st);
-  SL(k_nz, NR, rows.as<u64>(), NR, nzf.as<uint8_t>());
-  select_flagged_index(nzf.as<uint8_t>(), sel.as<u32>(), dcnt.as<u64>(), NR, st);
-  const u64 n = d2h1<u64>(dcnt.p, st);
-  nzf.release();
+  rid.release();
   const u64 Wt = d->W;
   const int CB = std::max(1, bitlen(Wt));
   const bool by_file = task == GT_SEQCOUNT;
   const int MB = by_file ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns));
   if (CB + MB > 64) fail(GT_E_RESOURCE, "sort key of %d bits exceeds 64", CB + MB);
   DBuf sk(n * 8 + 8, st), sk2(n * 8 + 8, st), rec(n * 4 + 4, st), rec2(n * 4 + 4, st);
-  SL(k_rec_keys, n, sel.as<u32>(), dcnt.as<u64>(), rows.as<u64>(), C, Wt, CB, by_file ? 1 : 0,
+  SL(k_rec_keys, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
      sk.as<u64>(), rec.as<u32>());
   sort_pairs_u64_u32(sk.as<u64>(), sk2.as<u64>(), rec.as<u32>(), rec2.as<u32>(), n, CB + MB, st);
   sk.release();
@@ -388,8 +433,8 @@ void run_sequences(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_ou
     if (packed) Rr->key.alloc(n * 8 + 8, st);
     else Rr->gram.alloc(n * l * 4 + 4, st);
     DBuf major(n * 4 + 4, st);
-    SL(k_rec_out, n, rec2.as<u32>(), n, rows.as<u64>(), C, runs.as<u32>(), skey.as<u64>(),
-       sgram.as<u32>(), l, packed, (u32)d->file_lo, 1, Rr->key.as<u64>(),
+    SL(k_rec_out, n, rec2.as<u32>(), n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), runs.as<u32>(),
+       skey.as<u64>(), sgram.as<u32>(), l, packed, (u32)d->file_lo, 1, Rr->key.as<u64>(),
        Rr->gram.as<u32>(), Rr->count.as<u64>(), (u32*)nullptr, major.as<u32>());
     Rr->n_groups = Fo;
     Rr->group_off.alloc((Fo + 1) * 8, st);
@@ -397,18 +442,18 @@ void run_sequences(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_ou
   } else {
     // RANKEDINVERTEDINDEX: grams ascending, per gram (-count, file)
     Rr->id.alloc(n * 4 + 4, st);
-    SL(k_rec_out, n, rec2.as<u32>(), n, rows.as<u64>(), C, runs.as<u32>(), skey.as<u64>(),
-       sgram.as<u32>(), l, packed, (u32)d->file_lo, 0, (u64*)nullptr, (u32*)nullptr,
+    SL(k_rec_out, n, rec2.as<u32>(), n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), runs.as<u32>(),
+       skey.as<u64>(), sgram.as<u32>(), l, packed, (u32)d->file_lo, 0, (u64*)nullptr, (u32*)nullptr,
        Rr->count.as<u64>(), Rr->id.as<u32>(), (u32*)nullptr);
     DBuf gh(n + 1, st), gsel(n * 4 + 4, st);
-    SL(k_group_heads, n, rec2.as<u32>(), n, C, gh.as<uint8_t>());
+    SL(k_group_heads, n, rec2.as<u32>(), n, crun.as<u32>(), gh.as<uint8_t>());
     select_flagged_index(gh.as<uint8_t>(), gsel.as<u32>(), dcnt.as<u64>(), n, st);
     const u64 ng = d2h1<u64>(dcnt.p, st);
     Rr->n_groups = ng;
     Rr->group_off.alloc((ng + 1) * 8, st);
     if (packed) Rr->group_key.alloc(ng * 8 + 8, st);
     else Rr->group_gram.alloc(ng * l * 4 + 4, st);
-    SL(k_group_out, ng, gsel.as<u32>(), dcnt.as<u64>(), rec2.as<u32>(), C, runs.as<u32>(),
+    SL(k_group_out, ng, gsel.as<u32>(), dcnt.as<u64>(), rec2.as<u32>(), crun.as<u32>(), runs.as<u32>(),
        skey.as<u64>(), sgram.as<u32>(), l, packed, Rr->group_off.as<u64>(), Rr->group_key.as<u64>(),
        Rr->group_gram.as<u32>());
     GT_CUDA(cudaMemcpyAsync(Rr->group_off.as<u64>() + ng, &n, 8, cudaMemcpyHostToDevice, st));

@@ -3,5 +3,5 @@
 #include "word.cuh"
 
 namespace gt {
-void run_sequences(DeviceDag* d, int task, int seq_len, DevRecords* R, int* wbits_out);
+void run_sequences(DeviceDag* d, int task, int seq_len, bool sparse, DevRecords* R, int* wbits_out);
 }

@@ -1,0 +1,372 @@
+// sparse.cu — presence-guided sparse per-file weights, for corpora with many
+// files (F > file_set_width; config C3: 10^5 files).
+//
+// The reference switches to its bottom-up strategy for F > 64
+// (engine.py:63-71): dense R x F weight matrices (dag.py:79, engine.py:164)
+// do not fit, and it rebuilds per-rule local word tables bottom-up and merges
+// them into per-file tables (engine.py:338-518).  At 10^5 files that merge is
+// the bulk of the work (Σ over root references of the child table size,
+// ~10^9 inserts at C3).  The B200 formulation keeps the top-down direction
+// but makes it sparse, guided by a cheap dense structure:
+//
+//   1. presence bitsets, 1 bit per (rule, file): the top-down pass in OrMode
+//      (word.cu), 8·⌈F/64⌉ B per rule;
+//   2. the (rule, file) pairs with a set bit, as a CSR sorted by file within
+//      each rule (popcount + scan + warp-cooperative bit expansion);
+//   3. u64 weights on exactly those pairs: root seeds, then per top-down level
+//      every non-root parent edge (c, p, f) adds f·w(p, file) into
+//      w(c, file) for every file of p (edge-balanced expansion; the target
+//      slot found by binary search in c's file list, which contains p's);
+//   4. outputs: term-vector cells (word, file) are exactly the inverted-index
+//      presence cells, so they are allocated from the word presence bitsets
+//      and filled with Σ own_freq·w(rule, file) + root words; sequence tasks
+//      expand gram occurrences over their rule's files and reduce by
+//      (gram run, file).
+// Work is proportional to the nonzero (rule, file) and (word, file) pairs,
+// not to R·F or to Σ local-table sizes.  All sums are integer: bit-exact.
+#include <algorithm>
+
+#include "kernels_common.cuh"
+#include "sparse.cuh"
+
+namespace gt {
+
+namespace {
+
+__device__ __forceinline__ u64 lower_bound_u32(const u32* a, u64 n, u32 x) {
+  u64 lo = 0, hi = n;
+  while (lo < hi) {
+    const u64 m = (lo + hi) >> 1;
+    if (a[m] < x) lo = m + 1;
+    else hi = m;
+  }
+  return lo;
+}
+
+// last g with pos[g] <= i (pos = exclusive scan of the group sizes)
+__device__ __forceinline__ u64 find_group(const u64* pos, u64 G, u64 i) {
+  u64 lo = 0, hi = G;
+  while (hi - lo > 1) {
+    const u64 m = (lo + hi) >> 1;
+    if (pos[m] <= i) lo = m;
+    else hi = m;
+  }
+  return lo;
+}
+
+// popcount of each bitset row (warp per row): row r has FW words at stride
+// `rs` words, word j at r*rs_row + j*rs_col
+__global__ void k_popc_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col,
+                            u64* __restrict__ cnt) {
+  const unsigned lane = threadIdx.x & 31u;
+  const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 r = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows; r += nw) {
+    u64 c = 0;
+    for (u32 j = lane; j < FW; j += 32) c += __popcll(bits[r * rs_row + (u64)j * rs_col]);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
+    if (lane == 0) cnt[r] = c;
+  }
+}
+
+// set bits of each row -> ascending column indices at off[r] (warp per row,
+// 32 words per step, ballot-free: popcount prefix by shuffle scan)
+__global__ void k_expand_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col,
+                              const u64* __restrict__ off, u32* __restrict__ col,
+                              u32* __restrict__ row_of) {
+  const unsigned lane = threadIdx.x & 31u;
+  const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 r = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows; r += nw) {
+    u64 o = off[r];
+    if (off[r + 1] == o) continue;
+    for (u32 j0 = 0; j0 < FW; j0 += 32) {
+      const u32 j = j0 + lane;
+      u64 b = j < FW ? bits[r * rs_row + (u64)j * rs_col] : 0ull;
+      const u32 c = (u32)__popcll(b);
+      u32 inc = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= (unsigned)d) inc += t;
+      }
+      u64 q = o + inc - c;
+      while (b) {
+        const int t = __ffsll((long long)b) - 1;
+        col[q] = j * 64u + (u32)t;
+        if (row_of) row_of[q] = (u32)r;
+        q++;
+        b &= b - 1;
+      }
+      o += __shfl_sync(0xFFFFFFFFu, inc, 31);
+    }
+  }
+}
+
+// root seeds: w(rule, seg) += cnt for owned segments
+__global__ void k_sparse_seed(const u32* __restrict__ rs_rule, const u32* __restrict__ rs_seg,
+                              const u32* __restrict__ rs_cnt, u64 n, u32 file_lo, u32 nseg,
+                              const u64* __restrict__ off, const u32* __restrict__ file,
+                              u64* __restrict__ wt) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 sg = rs_seg[i] - file_lo;
+    if (sg >= nseg) continue;
+    const u32 r = rs_rule[i];
+    const u64 a = off[r];
+    const u64 q = a + lower_bound_u32(file + a, off[r + 1] - a, sg);
+    atomicAdd((unsigned long long*)&wt[q], (unsigned long long)rs_cnt[i]);
+  }
+}
+
+// group sizes: |files(key[i])|
+__global__ void k_list_len(const u32* __restrict__ key, u64 n, const u64* __restrict__ off,
+                           u64* __restrict__ deg) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    deg[i] = off[key[i] + 1] - off[key[i]];
+}
+
+// one top-down level: for every edge (c, p, f) and every file of p:
+//   w(c, file) += f · w(p, file)
+__global__ void k_sparse_level(const u32* __restrict__ child, const u32* __restrict__ par,
+                               const u32* __restrict__ freq, u64 n, const u64* __restrict__ pos,
+                               const u64* __restrict__ deg, const u64* __restrict__ off,
+                               const u32* __restrict__ file, u64* __restrict__ wt) {
+  if (!n) return;
+  const u64 T = pos[n - 1] + deg[n - 1];
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += stride) {
+    const u64 e = find_group(pos, n, i);
+    const u32 p = par[e], c = child[e];
+    const u64 k = off[p] + (i - pos[e]);
+    const u64 v = (u64)freq[e] * wt[k];
+    const u64 a = off[c];
+    const u64 q = a + lower_bound_u32(file + a, off[c + 1] - a, file[k]);
+    atomicAdd((unsigned long long*)&wt[q], (unsigned long long)v);
+  }
+}
+
+// term-vector cells: every own pair (w, r, f) adds f · w(r, file) to cell
+// (w, file) for every file of r
+__global__ void k_tv_own(const u32* __restrict__ ow_word, const u32* __restrict__ ow_rule,
+                         const u32* __restrict__ ow_freq, u64 n, const u64* __restrict__ pos,
+                         const u64* __restrict__ deg, const u64* __restrict__ off,
+                         const u32* __restrict__ file, const u64* __restrict__ wt,
+                         const u64* __restrict__ woff, const u32* __restrict__ wfile,
+                         u64* __restrict__ cnt) {
+  if (!n) return;
+  const u64 T = pos[n - 1] + deg[n - 1];
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += stride) {
+    const u64 e = find_group(pos, n, i);
+    const u32 r = ow_rule[e], w = ow_word[e];
+    const u64 k = off[r] + (i - pos[e]);
+    const u64 a = woff[w];
+    const u64 q = a + lower_bound_u32(wfile + a, woff[w + 1] - a, file[k]);
+    atomicAdd((unsigned long long*)&cnt[q], (unsigned long long)((u64)ow_freq[e] * wt[k]));
+  }
+}
+
+__global__ void k_tv_root(const u32* __restrict__ rw_word, const u32* __restrict__ rw_seg,
+                          const u32* __restrict__ rw_cnt, u64 n, u32 file_lo, u32 nseg,
+                          const u64* __restrict__ woff, const u32* __restrict__ wfile,
+                          u64* __restrict__ cnt) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 sg = rw_seg[i] - file_lo;
+    if (sg >= nseg) continue;
+    const u32 w = rw_word[i];
+    const u64 a = woff[w];
+    const u64 q = a + lower_bound_u32(wfile + a, woff[w + 1] - a, sg);
+    atomicAdd((unsigned long long*)&cnt[q], (unsigned long long)rw_cnt[i]);
+  }
+}
+
+// (file, W - count) sort keys of the word-major cells
+__global__ void k_tv_keys(const u32* __restrict__ wfile, const u64* __restrict__ cnt, u64 n, u64 W,
+                          int CB, u64* __restrict__ key) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    key[i] = ((u64)wfile[i] << CB) | (W - cnt[i]);
+}
+
+__global__ void k_tv_unkey(const u64* __restrict__ key, u64 n, u64 W, int CB, u64* __restrict__ cnt,
+                           u32* __restrict__ file) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 m = (1ull << CB) - 1;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    cnt[i] = W - (key[i] & m);
+    file[i] = (u32)(key[i] >> CB);
+  }
+}
+
+// gram occurrences -> (run << FB | file, weight) items: an occurrence from
+// rule s < R expands over the files of s; one from root segment s - R is a
+// single item of weight 1
+__global__ void k_occ_deg(const u32* __restrict__ src, u64 N, u32 R, const u64* __restrict__ off,
+                          u64* __restrict__ deg) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+    const u32 s = src[i];
+    deg[i] = s < R ? off[s + 1] - off[s] : 1ull;
+  }
+}
+
+__global__ void k_occ_items(const u32* __restrict__ rid, const u32* __restrict__ src, u64 N, u32 R,
+                            const u64* __restrict__ pos, const u64* __restrict__ deg,
+                            const u64* __restrict__ off, const u32* __restrict__ file,
+                            const u64* __restrict__ wt, int FB, u64* __restrict__ key,
+                            u64* __restrict__ val) {
+  if (!N) return;
+  const u64 T = pos[N - 1] + deg[N - 1];
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += stride) {
+    const u64 o = find_group(pos, N, i);
+    const u32 s = src[o];
+    u32 f;
+    u64 v;
+    if (s < R) {
+      const u64 k = off[s] + (i - pos[o]);
+      f = file[k];
+      v = wt[k];
+    } else {
+      f = s - R;
+      v = 1;
+    }
+    key[i] = ((u64)rid[o] << FB) | f;
+    val[i] = v;
+  }
+}
+
+#define SK(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
+#define SKW(k, nwarps, ...) GT_KLAUNCH(#k, k, grid_for((u64)(nwarps) * 32, 256, 148u * 64u), 256, st, __VA_ARGS__)
+#define SKE(k, ...) GT_KLAUNCH(#k, k, 148u * 16u, 256, st, __VA_ARGS__)
+
+template <class T>
+T d2h1(const void* p, cudaStream_t st) {
+  T v;
+  GT_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  return v;
+}
+
+// rows of bitsets -> CSR (off, col[, row_of]); returns the pair count
+u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& col,
+                DBuf* row_of, cudaStream_t st) {
+  DBuf cnt(nrows * 8 + 8, st);
+  off.alloc((nrows + 1) * 8, st);
+  SKW(k_popc_rows, nrows, bits, nrows, FW, rs_row, rs_col, cnt.as<u64>());
+  GT_CUDA(cudaMemsetAsync(cnt.as<u64>() + nrows, 0, 8, st));
+  exclusive_scan_u64(cnt.as<u64>(), off.as<u64>(), nrows + 1, st);
+  const u64 P = d2h1<u64>(off.as<u64>() + nrows, st);
+  col.alloc(P * 4 + 4, st);
+  if (row_of) row_of->alloc(P * 4 + 4, st);
+  SKW(k_expand_rows, nrows, bits, nrows, FW, rs_row, rs_col, off.as<u64>(), col.as<u32>(),
+      row_of ? row_of->as<u32>() : (u32*)nullptr);
+  return P;
+}
+
+}  // namespace
+
+void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW_out) {
+  cudaStream_t st = d->stream;
+  const u64 R = d->R;
+  DBuf pres, rows;
+  u32 FW;
+  td_file_presence(d, pres, &FW, &rows);
+  if (word_pres) *word_pres = std::move(pres);
+  *FW_out = FW;
+  s->P = bits_to_csr(rows.as<u64>(), R, FW, FW, 1, s->off, s->file, nullptr, st);
+  rows.release();
+  s->wt.alloc(s->P * 8 + 8, st);
+  GT_CUDA(cudaMemsetAsync(s->wt.p, 0, s->P * 8 + 8, st));
+  const u32 nseg = (u32)(d->file_hi - d->file_lo);
+  if (d->n_rs)
+    SK(k_sparse_seed, d->n_rs, d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs,
+       (u32)d->file_lo, nseg, s->off.as<u64>(), s->file.as<u32>(), s->wt.as<u64>());
+  const u64 Etd = d->te_off.empty() ? 0 : d->te_off.back();
+  DBuf deg(Etd * 8 + 8, st), pos(Etd * 8 + 8, st);
+  for (int L = 1; L <= d->td.nl; L++) {
+    const u64 a = d->te_off[L], n = d->te_off[L + 1] - a;
+    if (!n) continue;
+    SK(k_list_len, n, d->te_par.as<u32>() + a, n, s->off.as<u64>(), deg.as<u64>());
+    exclusive_scan_u64(deg.as<u64>(), pos.as<u64>(), n, st);
+    SKE(k_sparse_level, d->te_child.as<u32>() + a, d->te_par.as<u32>() + a, d->te_freq.as<u32>() + a, n,
+        pos.as<u64>(), deg.as<u64>(), s->off.as<u64>(), s->file.as<u32>(), s->wt.as<u64>());
+  }
+}
+
+void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
+  cudaStream_t st = d->stream;
+  const u64 V = d->nw;
+  const u32 Fo = (u32)(d->file_hi - d->file_lo);
+  SparseW s;
+  DBuf pres;
+  u32 FW;
+  sparse_file_weights(d, &s, &pres, &FW);
+  // (word, file) cells = word presence bits; word-major, files ascending
+  DBuf woff, wfile, wword;
+  const u64 O = bits_to_csr(pres.as<u64>(), V, FW, 1, V, woff, wfile, &wword, st);
+  pres.release();
+  DBuf cnt(O * 8 + 8, st);
+  GT_CUDA(cudaMemsetAsync(cnt.p, 0, O * 8 + 8, st));
+  const u64 Eo = d->E_own;
+  if (Eo) {
+    DBuf deg(Eo * 8 + 8, st), pos(Eo * 8 + 8, st);
+    SK(k_list_len, Eo, d->ow_rule.as<u32>(), Eo, s.off.as<u64>(), deg.as<u64>());
+    exclusive_scan_u64(deg.as<u64>(), pos.as<u64>(), Eo, st);
+    SKE(k_tv_own, d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), Eo, pos.as<u64>(),
+        deg.as<u64>(), s.off.as<u64>(), s.file.as<u32>(), s.wt.as<u64>(), woff.as<u64>(),
+        wfile.as<u32>(), cnt.as<u64>());
+  }
+  if (d->n_rw)
+    SK(k_tv_root, d->n_rw, d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(), d->n_rw,
+       (u32)d->file_lo, Fo, woff.as<u64>(), wfile.as<u32>(), cnt.as<u64>());
+  s = SparseW();
+  // file-major, (-count, word) within a file: one stable radix sort of the
+  // word-major cells on (file, W - count)
+  const u64 W = d->W;
+  const int CB = std::max(1, bitlen(W));
+  const int FB = std::max(1, bitlen(Fo ? Fo - 1 : 0));
+  DBuf k1(O * 8 + 8, st), k2(O * 8 + 8, st);
+  SK(k_tv_keys, O, wfile.as<u32>(), cnt.as<u64>(), O, W, CB, k1.as<u64>());
+  Rr->n = O;
+  Rr->id.alloc(O * 4 + 4, st);
+  sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), wword.as<u32>(), Rr->id.as<u32>(), O, CB + FB, st);
+  Rr->count = std::move(cnt);
+  SK(k_tv_unkey, O, k2.as<u64>(), O, W, CB, Rr->count.as<u64>(), wfile.as<u32>());
+  Rr->n_groups = Fo;
+  Rr->group_off.alloc(((u64)Fo + 1) * 8, st);
+  SK(k_csr_offsets, (u64)Fo + 1, wfile.as<u32>(), O, (u64)Fo, Rr->group_off.as<u64>());
+}
+
+u64 sparse_run_cells(DeviceDag* d, const SparseW& s, const u32* rid, const u32* src, u64 N, int FB,
+                     DBuf& cell_key, DBuf& cell_cnt) {
+  cudaStream_t st = d->stream;
+  if (!N) return 0;
+  DBuf deg(N * 8 + 8, st), pos(N * 8 + 8, st);
+  SK(k_occ_deg, N, src, N, (u32)d->R, s.off.as<u64>(), deg.as<u64>());
+  exclusive_scan_u64(deg.as<u64>(), pos.as<u64>(), N, st);
+  const u64 T = d2h1<u64>(pos.as<u64>() + N - 1, st) + d2h1<u64>(deg.as<u64>() + N - 1, st);
+  DBuf key(T * 8 + 8, st), val(T * 8 + 8, st);
+  SKE(k_occ_items, rid, src, N, (u32)d->R, pos.as<u64>(), deg.as<u64>(), s.off.as<u64>(),
+      s.file.as<u32>(), s.wt.as<u64>(), FB, key.as<u64>(), val.as<u64>());
+  deg.release();
+  pos.release();
+  DBuf k2(T * 8 + 8, st), v2(T * 8 + 8, st);
+  u32 nruns_bits = 1;
+  {
+    u32 last_rid = d2h1<u32>(rid + N - 1, st);
+    nruns_bits = (u32)std::max(1, bitlen(last_rid));
+  }
+  sort_pairs_u64_u64(key.as<u64>(), k2.as<u64>(), val.as<u64>(), v2.as<u64>(), T, FB + (int)nruns_bits, st);
+  key.release();
+  val.release();
+  cell_key.alloc(T * 8 + 8, st);
+  cell_cnt.alloc(T * 8 + 8, st);
+  DBuf nc(8, st);
+  reduce_by_key_u64(k2.as<u64>(), v2.as<u64>(), cell_key.as<u64>(), cell_cnt.as<u64>(), nc.as<u64>(), T, st);
+  return d2h1<u64>(nc.p, st);
+}
+
+}  // namespace gt

@@ -1,0 +1,28 @@
+// sparse.cuh — presence-guided sparse per-file weights (sparse.cu).
+#pragma once
+#include "word.cuh"
+
+namespace gt {
+
+// (rule, file) pairs with nonzero per-file weight, CSR by rule, files
+// (relative to file_lo) ascending within a rule
+struct SparseW {
+  DBuf off;   // u64[R+1]
+  DBuf file;  // u32[P]
+  DBuf wt;    // u64[P]
+  u64 P = 0;
+};
+
+// presence pass + pairs + weights; optionally hands back the word presence
+// bitsets u64[FW][V] of the same pass
+void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW);
+
+// term vector for many files (render order: file, -count, word)
+void sparse_term_vector(DeviceDag* d, DevRecords* R);
+
+// gram occurrences (run id, source) -> reduced (run << FB | file, count)
+// cells in (run, file) order; returns the cell count
+u64 sparse_run_cells(DeviceDag* d, const SparseW& s, const u32* rid, const u32* src, u64 N, int FB,
+                     DBuf& cell_key, DBuf& cell_cnt);
+
+}  // namespace gt

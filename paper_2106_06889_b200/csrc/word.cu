@@ -224,8 +224,9 @@ void td_file_weights(DeviceDag* d, DBuf& w, u32* C_out) {
   *C_out = C;
 }
 
-// per-file presence bitsets -> dense u64[FW][V]
-void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out) {
+// per-file presence bitsets -> dense u64[FW][V]; the rule rows (u64[R][FW])
+// are handed back in *rows_out when requested (sparse per-file path)
+void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out, DBuf* rows_out) {
   cudaStream_t st = d->stream;
   const u32 Fo = (u32)(d->file_hi - d->file_lo);
   const u32 FW = std::max<u32>(1, (Fo + 63) / 64);
@@ -234,6 +235,7 @@ void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out) {
   pres.alloc(d->nw * 8 * (u64)FW + 8, st);
   reduce_words<OrMode>(d, FW, m.as<u64>(), pres.as<u64>(), true);
   *FW_out = FW;
+  if (rows_out) *rows_out = std::move(m);
 }
 
 // ---- assembly -------------------------------------------------------------

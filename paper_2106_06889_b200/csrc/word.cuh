@@ -13,7 +13,7 @@ struct DevRecords {
 
 void td_word_counts(DeviceDag* d, DBuf& counts);
 void td_file_counts(DeviceDag* d, DBuf& counts);
-void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW);
+void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW, DBuf* rows_out = nullptr);
 void td_file_weights(DeviceDag* d, DBuf& w, u32* C);
 void assemble_counts(DeviceDag* d, const u64* dense, u64 V, u32 ncols, bool by_count, DevRecords* R);
 void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R);
