@@ -145,7 +145,7 @@ def alg_bytes(kernel: str, info: dict, files: int, tasks=TASKS) -> float | None:
     tot = 0
     for t in tasks:
         C = task_columns(t, files)
-        if kernel == "k_td_level":
+        if kernel in ("k_td_level", "k_td_levels"):
             tot += 12 * Te + 16 * C * (R - 1)
         elif kernel == "k_reduce_words":
             tot += 12 * Eo + 8 * C * R + 8 * C * V

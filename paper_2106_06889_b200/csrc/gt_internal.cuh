@@ -116,8 +116,10 @@ struct DeviceDag {
   //   be_*: child edges (rule, child, freq) by (bu level, rule, child)
   DBuf te_child, te_par, te_freq;
   std::vector<u64> te_off;  // host: td level L items [te_off[L], te_off[L+1])
+  DBuf te_off_dev;          // device copy (persistent level loops)
   DBuf be_rule, be_child, be_freq;
   std::vector<u64> be_off;  // host: bu level L items [be_off[L], be_off[L+1])
+  DBuf be_off_dev;
   double init_ms = 0;
   // scratch kept across runs
   DBuf word_counts;  // u64[V] of the last global run
@@ -128,7 +130,8 @@ struct DeviceDag {
                          &num_in, &num_out, &exp_len, &td_level, &bu_level, &seg_lo, &seg_hi,
                          &seg_tokens, &ow_word, &ow_rule, &ow_freq, &ow_off, &rs_rule, &rs_seg,
                          &rs_cnt, &rs_off, &rw_word, &rw_seg, &rw_cnt, &td.order, &bu.order,
-                         &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts};
+                         &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts,
+                         &te_off_dev, &be_off_dev};
     u64 t = 0;
     for (const DBuf* b : all) t += b->bytes;
     return t;

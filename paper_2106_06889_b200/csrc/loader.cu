@@ -818,7 +818,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // edges keep (child, parent) resp. (rule, child) order) -------------------
   auto level_edges = [&](const u32* group_of, const uint8_t* keep, const u32* lvl, int nl,
                          const u32* a_src, const u32* b_src, const u32* f_src, DBuf& oa, DBuf& ob,
-                         DBuf& of, std::vector<u64>& off) {
+                         DBuf& of, std::vector<u64>& off, DBuf& off_dev) {
     DBuf idx(Es * 4 + 4, st), key(Es * 4 + 4, st), key2(Es * 4 + 4, st), idx2(Es * 4 + 4, st);
     u64 m = Es;
     if (keep) {
@@ -838,6 +838,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     LAUNCH(k_csr_offsets, (u64)nl + 3, key2.as<u32>(), m, (u64)nl + 2, koff.as<u64>());
     off.assign((size_t)nl + 3, 0);
     d2h(off.data(), koff.p, (size_t)nl + 3, st);
+    off_dev = std::move(koff);
   };
   {
     // td: par entries (grouped by child) whose parent is not the root
@@ -845,11 +846,11 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     LAUNCH(k_flag_nonzero_u32, Es, d->par_ids.as<u32>(), Es, keep.as<uint8_t>());
     level_edges(child_sorted.as<u32>(), keep.as<uint8_t>(), d->td_level.as<u32>(), ntd,
                 child_sorted.as<u32>(), d->par_ids.as<u32>(), d->par_freqs.as<u32>(), d->te_child,
-                d->te_par, d->te_freq, d->te_off);
+                d->te_par, d->te_freq, d->te_off, d->te_off_dev);
     // bu: sub entries (grouped by rule) by the rule's bottom-up layer
     level_edges(sub_rule.as<u32>(), nullptr, d->bu_level.as<u32>(), nbu, sub_rule.as<u32>(),
                 d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), d->be_rule, d->be_child, d->be_freq,
-                d->be_off);
+                d->be_off, d->be_off_dev);
   }
   sub_rule.release();
   child_sorted.release();
@@ -897,12 +898,11 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // ---- exp_len by bottom-up level (grammar.py:109-124) --------------------
   d->exp_len.alloc(R * 8, st);
   GT_CUDA(cudaMemcpyAsync(d->exp_len.p, d->own_tok.p, R * 8, cudaMemcpyDeviceToDevice, st));
-  for (int L = 1; L <= nbu; L++) {
-    const u64 a = d->be_off[L], n = d->be_off[L + 1] - a;
-    seg_reduce<SumMode>("k_exp_len", d->be_rule.as<u32>() + a, d->be_child.as<u32>() + a,
-                        d->be_freq.as<u32>() + a, n, 1, RowSrc{d->exp_len.as<u64>(), 1},
-                        OutRowMajor{d->exp_len.as<u64>(), 1}, st);
-  }
+  // exp_len[r] = own tokens + Σ f · exp_len[child], bottom-up levels 2..nbu
+  // in one persistent launch (level 1 = leaves, no items)
+  seg_reduce_levels<SumMode>("k_exp_len", d->be_rule.as<u32>(), d->be_child.as<u32>(),
+                             d->be_freq.as<u32>(), d->be_off_dev.as<u64>(), 2, nbu, 1,
+                             RowSrc{d->exp_len.as<u64>(), 1}, OutRowMajor{d->exp_len.as<u64>(), 1}, st);
   d2h(&d->W, d->exp_len.p, 1, st);
   ph.mark("segments+exp_len");
 

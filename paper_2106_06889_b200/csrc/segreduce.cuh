@@ -20,9 +20,13 @@
 //        (dst = run, src = rule or root segment).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "kernels_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gt {
 
@@ -43,10 +47,17 @@ struct OrMode {
 };
 
 // ---- source row functors ----------------------------------------------------
+// Row and output reads go through L2 (ld.global.cg): the level loops of a
+// persistent launch read rows other SMs wrote before the grid barrier, and a
+// line cached in a non-coherent L1 earlier could be stale.
+__device__ __forceinline__ u64 ldcg(const u64* p) {
+  return (u64)__ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+
 struct RowSrc {  // in[src*C + col]
   const u64* in;
   u32 C;
-  __device__ __forceinline__ u64 operator()(u32 s, u32 col) const { return in[(u64)s * C + col]; }
+  __device__ __forceinline__ u64 operator()(u32 s, u32 col) const { return ldcg(in + (u64)s * C + col); }
 };
 
 // ---- output address functors --------------------------------------------------
@@ -68,13 +79,10 @@ __device__ __forceinline__ u32 item_freq(const u32* freq, u64 i) { return freq ?
 // with a shuffle segmented scan and carried across the K steps of the tile.
 // ---------------------------------------------------------------------------
 template <class Mode, class Src, class Out>
-__global__ void __launch_bounds__(256) k_segred1(const u32* __restrict__ dst,
-                                                 const u32* __restrict__ src,
-                                                 const u32* __restrict__ freq, u64 n, int K,
-                                                 Src in, Out out) {
+__device__ __forceinline__ void segred1_body(const u32* __restrict__ dst, const u32* __restrict__ src,
+                                             const u32* __restrict__ freq, u64 n, int K, Src in,
+                                             Out out, u64 warp, u64 nwarps) {
   const unsigned lane = threadIdx.x & 31u;
-  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const u64 TILE = 32ull * K;
   for (u64 t0 = warp * TILE; t0 < n; t0 += nwarps * TILE) {
     const u32 first = dst[t0];
@@ -104,7 +112,7 @@ __global__ void __launch_bounds__(256) k_segred1(const u32* __restrict__ dst,
         if (lane == 0) {
           u64* p = out(carry_d, 0);
           if (carry_d == first && first_shared) Mode::atomic(p, carry_v);
-          else *p = Mode::merge(*p, carry_v);
+          else *p = Mode::merge(ldcg(p), carry_v);
         }
         carry_d = 0xFFFFFFFFu;
         carry_v = 0;
@@ -120,7 +128,7 @@ __global__ void __launch_bounds__(256) k_segred1(const u32* __restrict__ dst,
       if (ok && lane != 31 && dn != d) {  // run ends inside this step
         u64* p = out(d, 0);
         if ((d == first && first_shared) || (d == last && last_shared)) Mode::atomic(p, v);
-        else *p = Mode::merge(*p, v);
+        else *p = Mode::merge(ldcg(p), v);
       }
       carry_d = __shfl_sync(0xFFFFFFFFu, d, 31);
       carry_v = __shfl_sync(0xFFFFFFFFu, v, 31);
@@ -128,9 +136,18 @@ __global__ void __launch_bounds__(256) k_segred1(const u32* __restrict__ dst,
     if (lane == 0 && carry_d != 0xFFFFFFFFu) {
       u64* p = out(carry_d, 0);
       if ((carry_d == first && first_shared) || (carry_d == last && last_shared)) Mode::atomic(p, carry_v);
-      else *p = Mode::merge(*p, carry_v);
+      else *p = Mode::merge(ldcg(p), carry_v);
     }
   }
+}
+
+template <class Mode, class Src, class Out>
+__global__ void __launch_bounds__(256) k_segred1(const u32* __restrict__ dst,
+                                                 const u32* __restrict__ src,
+                                                 const u32* __restrict__ freq, u64 n, int K,
+                                                 Src in, Out out) {
+  segred1_body<Mode>(dst, src, freq, n, K, in, out, ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                     ((u64)gridDim.x * blockDim.x) >> 5);
 }
 
 // ---------------------------------------------------------------------------
@@ -139,13 +156,11 @@ __global__ void __launch_bounds__(256) k_segred1(const u32* __restrict__ dst,
 // values are fetched B at a time ahead of the run bookkeeping.
 // ---------------------------------------------------------------------------
 template <int G, class Mode, class Src, class Out>
-__global__ void __launch_bounds__(256) k_segredG(const u32* __restrict__ dst,
-                                                 const u32* __restrict__ src,
-                                                 const u32* __restrict__ freq, u64 n, u32 K, u32 C,
-                                                 Src in, Out out) {
+__device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const u32* __restrict__ src,
+                                             const u32* __restrict__ freq, u64 n, u32 K, u32 C, Src in,
+                                             Out out, u64 gtid, u64 nthreads) {
   constexpr int B = 8;
-  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  const u64 teams = ((u64)gridDim.x * blockDim.x) / G;
+  const u64 teams = nthreads / G;
   const u32 tl = threadIdx.x % G;
   for (u64 t = gtid / G; t * K < n; t += teams) {
     const u64 a = t * K, b = a + K < n ? a + K : n;  // K: items per team (runtime)
@@ -170,7 +185,7 @@ __global__ void __launch_bounds__(256) k_segredG(const u32* __restrict__ dst,
           if (dd[j] != cd) {
             u64* p = out(cd, col);
             if (cd == dfirst && first_shared) Mode::atomic(p, acc);
-            else *p = Mode::merge(*p, acc);
+            else *p = Mode::merge(ldcg(p), acc);
             cd = dd[j];
             acc = 0;
           }
@@ -179,8 +194,52 @@ __global__ void __launch_bounds__(256) k_segredG(const u32* __restrict__ dst,
       }
       u64* p = out(cd, col);
       if ((cd == dfirst && first_shared) || (cd == dlast && last_shared)) Mode::atomic(p, acc);
-      else *p = Mode::merge(*p, acc);
+      else *p = Mode::merge(ldcg(p), acc);
     }
+  }
+}
+
+template <int G, class Mode, class Src, class Out>
+__global__ void __launch_bounds__(256) k_segredG(const u32* __restrict__ dst,
+                                                 const u32* __restrict__ src,
+                                                 const u32* __restrict__ freq, u64 n, u32 K, u32 C,
+                                                 Src in, Out out) {
+  segredG_body<G, Mode>(dst, src, freq, n, K, C, in, out, (u64)blockIdx.x * blockDim.x + threadIdx.x,
+                        (u64)gridDim.x * blockDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent level loop: ONE cooperative launch runs levels [L0, L1] of a
+// level-ordered item list (lvl_off on the device), the whole grid resident
+// and separated by grid-wide barriers instead of kernel boundaries.  Level
+// sizes follow the DAG (a handful to 10^6 items), so the per-level work is
+// re-dealt over all resident warps/teams each time.
+// ---------------------------------------------------------------------------
+template <int G, class Mode, class Src, class Out>
+__global__ void __launch_bounds__(256) k_segred_levels(const u32* __restrict__ dst,
+                                                       const u32* __restrict__ src,
+                                                       const u32* __restrict__ freq,
+                                                       const u64* __restrict__ lvl_off, int L0, int L1,
+                                                       u32 C, Src in, Out out) {
+  cg::grid_group grid = cg::this_grid();
+  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 nthreads = (u64)gridDim.x * blockDim.x;
+  for (int L = L0; L <= L1; L++) {
+    const u64 a = lvl_off[L], n = lvl_off[L + 1] - a;
+    if (n) {
+      if (G == 1) {
+        const u64 nwarps = nthreads >> 5;
+        int K = (int)((n + 32 * nwarps - 1) / (32 * nwarps));
+        K = K < 1 ? 1 : (K > 16 ? 16 : K);
+        segred1_body<Mode>(dst + a, src + a, freq ? freq + a : nullptr, n, K, in, out, gtid >> 5, nwarps);
+      } else {
+        const u64 teams = nthreads / G;
+        u32 K = (u32)((n + teams - 1) / teams);
+        K = K < 8 ? 8 : (K > 64 ? 64 : K);
+        segredG_body<G, Mode>(dst + a, src + a, freq ? freq + a : nullptr, n, K, C, in, out, gtid, nthreads);
+      }
+    }
+    if (L < L1) grid.sync();
   }
 }
 
@@ -221,6 +280,41 @@ void seg_reduce(const char* name, const u32* dst, const u32* src, const u32* fre
   else if (C <= 16) GT_SEGRED_G(16);
   else GT_SEGRED_G(32);
 #undef GT_SEGRED_G
+}
+
+// Host launcher of the persistent level loop: levels [L0, L1] of the item
+// list (dst/src/freq base pointers; lvl_off_dev = device copy of the level
+// offsets).  One cooperative launch with every block resident.
+template <int G, class Mode, class Src, class Out>
+void seg_reduce_levels_G(const char* name, const u32* dst, const u32* src, const u32* freq,
+                         const u64* lvl_off_dev, int L0, int L1, u32 C, Src in, Out out, cudaStream_t st) {
+  auto kern = k_segred_levels<G, Mode, Src, Out>;
+  static int per_sm = -1;  // per instantiation
+  if (per_sm < 0) {
+    GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    if (per_sm < 1) per_sm = 1;
+  }
+  int dev = 0, nsm = 148;
+  GT_CUDA(cudaGetDevice(&dev));
+  GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  dim3 grid((unsigned)(nsm * per_sm)), block(256);
+  void* args[] = {(void*)&dst, (void*)&src, (void*)&freq, (void*)&lvl_off_dev, (void*)&L0, (void*)&L1,
+                  (void*)&C, (void*)&in, (void*)&out};
+  ProfScope ps(name, st);
+  GT_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, block, args, 0, st));
+  g_launches++;
+}
+
+template <class Mode, class Src, class Out>
+void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u32* freq,
+                       const u64* lvl_off_dev, int L0, int L1, u32 C, Src in, Out out, cudaStream_t st) {
+  if (L1 < L0 || !C) return;
+  if (C == 1) seg_reduce_levels_G<1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
+  else if (C <= 2) seg_reduce_levels_G<2, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
+  else if (C <= 4) seg_reduce_levels_G<4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
+  else if (C <= 8) seg_reduce_levels_G<8, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
+  else if (C <= 16) seg_reduce_levels_G<16, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
+  else seg_reduce_levels_G<32, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
 }
 
 }  // namespace gt

@@ -72,7 +72,7 @@ __global__ void k_popc_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u64
 // set bits of each row -> ascending column indices at off[r] (warp per row,
 // 32 words per step, ballot-free: popcount prefix by shuffle scan)
 __global__ void k_expand_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col,
-                              const u64* __restrict__ off, u32* __restrict__ col,
+                              const u64* __restrict__ off, u32 col_base, u32* __restrict__ col,
                               u32* __restrict__ row_of) {
   const unsigned lane = threadIdx.x & 31u;
   const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
@@ -92,7 +92,7 @@ __global__ void k_expand_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u
       u64 q = o + inc - c;
       while (b) {
         const int t = __ffsll((long long)b) - 1;
-        col[q] = j * 64u + (u32)t;
+        col[q] = col_base + j * 64u + (u32)t;
         if (row_of) row_of[q] = (u32)r;
         q++;
         b &= b - 1;
@@ -238,10 +238,13 @@ __global__ void k_occ_items(const u32* __restrict__ rid, const u32* __restrict__
   }
 }
 
+}  // namespace
+
 #define SK(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
 #define SKW(k, nwarps, ...) GT_KLAUNCH(#k, k, grid_for((u64)(nwarps) * 32, 256, 148u * 64u), 256, st, __VA_ARGS__)
 #define SKE(k, ...) GT_KLAUNCH(#k, k, 148u * 16u, 256, st, __VA_ARGS__)
 
+namespace {
 template <class T>
 T d2h1(const void* p, cudaStream_t st) {
   T v;
@@ -250,9 +253,11 @@ T d2h1(const void* p, cudaStream_t st) {
   return v;
 }
 
+}  // namespace
+
 // rows of bitsets -> CSR (off, col[, row_of]); returns the pair count
 u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& col,
-                DBuf* row_of, cudaStream_t st) {
+                DBuf* row_of, cudaStream_t st, u32 col_base, DBuf* row_cnt) {
   DBuf cnt(nrows * 8 + 8, st);
   off.alloc((nrows + 1) * 8, st);
   SKW(k_popc_rows, nrows, bits, nrows, FW, rs_row, rs_col, cnt.as<u64>());
@@ -261,12 +266,11 @@ u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf
   const u64 P = d2h1<u64>(off.as<u64>() + nrows, st);
   col.alloc(P * 4 + 4, st);
   if (row_of) row_of->alloc(P * 4 + 4, st);
-  SKW(k_expand_rows, nrows, bits, nrows, FW, rs_row, rs_col, off.as<u64>(), col.as<u32>(),
+  SKW(k_expand_rows, nrows, bits, nrows, FW, rs_row, rs_col, off.as<u64>(), col_base, col.as<u32>(),
       row_of ? row_of->as<u32>() : (u32*)nullptr);
+  if (row_cnt) *row_cnt = std::move(cnt);
   return P;
 }
-
-}  // namespace
 
 void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW_out) {
   cudaStream_t st = d->stream;

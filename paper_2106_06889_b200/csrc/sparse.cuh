@@ -13,6 +13,12 @@ struct SparseW {
   u64 P = 0;
 };
 
+// rows of bitsets -> CSR: row r's words at bits[r*rs_row + j*rs_col]
+// (j < FW); off u64[nrows+1], col = col_base + set-bit index, ascending;
+// optional row id per pair and per-row counts.  Returns the pair count.
+u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& col,
+                DBuf* row_of, cudaStream_t st, u32 col_base = 0, DBuf* row_cnt = nullptr);
+
 // presence pass + pairs + weights; optionally hands back the word presence
 // bitsets u64[FW][V] of the same pass
 void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW);

@@ -24,6 +24,7 @@
 
 #include "kernels_common.cuh"
 #include "segreduce.cuh"
+#include "sparse.cuh"
 #include "word.cuh"
 
 namespace gt {
@@ -127,33 +128,22 @@ __global__ void k_unkey(const u64* key, u64 n, u64 W, int CB, u64* cnt) {
     cnt[i] = W - (key[i] & m);
 }
 
-// presence bitsets -> per-word file counts
-__global__ void k_popc(const u64* pres, u64 V, u32 FW, u64* pc, uint8_t* nz) {
+__global__ void k_nz_u64(const u64* v, u64 n, uint8_t* f) {
   u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
-    u64 c = 0;
-    for (u32 j = 0; j < FW; j++) c += __popcll(pres[(u64)j * V + v]);
-    pc[v] = c;
-    nz[v] = c != 0;
-  }
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f[i] = v[i] != 0;
 }
 
-__global__ void k_ii_write(const u32* words, const u64* ngroups, const u64* pres, const u64* pc_off,
-                           u64 V, u32 FW, u32 file_lo, u32* gid, u64* goff, u32* files) {
-  u64 n = *ngroups;
+// inverted-index groups: the words with at least one file
+__global__ void k_ii_groups(const u32* words, const u64* ngroups, const u64* off, u64 n, u32* gid,
+                            u64* goff) {
+  const u64 ng = *ngroups;
   u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += stride) {
-    u32 v = words[g];
-    gid[g] = v;
-    u64 o = pc_off[v];
-    goff[g] = o;
-    for (u32 j = 0; j < FW; j++) {
-      u64 b = pres[(u64)j * V + v];
-      while (b) {
-        int t = __ffsll((long long)b) - 1;
-        files[o++] = file_lo + j * 64 + (u32)t;
-        b &= b - 1;
-      }
+  for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g <= ng; g += stride) {
+    if (g == ng) {
+      goff[g] = n;
+    } else {
+      gid[g] = words[g];
+      goff[g] = off[words[g]];
     }
   }
 }
@@ -174,11 +164,9 @@ static void td_levels(const DeviceDag* d, u32 C, u64* row, u32 per_file = 1) {
   if (d->n_rs)
     KL(k_seed<Mode>, grid_for(d->n_rs, 256), d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(),
        d->n_rs, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row);
-  for (int L = 1; L <= d->td.nl; L++) {
-    const u64 a = d->te_off[L], n = d->te_off[L + 1] - a;
-    seg_reduce<Mode>("k_td_level", d->te_child.as<u32>() + a, d->te_par.as<u32>() + a,
-                     d->te_freq.as<u32>() + a, n, C, RowSrc{row, C}, OutRowMajor{row, C}, st);
-  }
+  // all levels in one persistent launch, grid barriers between levels
+  seg_reduce_levels<Mode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
+                          d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrc{row, C}, OutRowMajor{row, C}, st);
 }
 
 // Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
@@ -276,30 +264,27 @@ void assemble_counts(DeviceDag* d, const u64* dense, u64 V, u32 ncols, bool by_c
   }
 }
 
+// inverted index from the word presence bitsets u64[FW][V]: per word, the
+// ascending global file ids of its set bits (warp-cooperative expansion,
+// sparse.cu bits_to_csr), grouped by word in ascending word order
 void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R) {
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
-  DBuf pc(V * 8 + 8, st), pco(V * 8 + 8, st), nz(V + 1, st), words(V * 4 + 4, st), cnt(8, st);
-  KL(k_popc, grid_for(V, 256), pres, V, FW, pc.as<u64>(), nz.as<uint8_t>());
-  exclusive_scan_u64(pc.as<u64>(), pco.as<u64>(), V, st);
+  DBuf off, files, pc;
+  const u64 n = bits_to_csr(pres, V, FW, 1, V, off, files, nullptr, st, (u32)d->file_lo, &pc);
+  DBuf nz(V + 1, st), words(V * 4 + 4, st), cnt(8, st);
+  KL(k_nz_u64, grid_for(V, 256), pc.as<u64>(), V, nz.as<uint8_t>());
   select_flagged_index(nz.as<uint8_t>(), words.as<u32>(), cnt.as<u64>(), V, st);
-  u64 ng = 0, last_off = 0, last_pc = 0;
+  u64 ng = 0;
   GT_CUDA(cudaMemcpyAsync(&ng, cnt.p, 8, cudaMemcpyDeviceToHost, st));
-  if (V) {
-    GT_CUDA(cudaMemcpyAsync(&last_off, pco.as<u64>() + V - 1, 8, cudaMemcpyDeviceToHost, st));
-    GT_CUDA(cudaMemcpyAsync(&last_pc, pc.as<u64>() + V - 1, 8, cudaMemcpyDeviceToHost, st));
-  }
   GT_CUDA(cudaStreamSynchronize(st));
-  const u64 n = last_off + last_pc;
   R->n = n;
   R->n_groups = ng;
   R->group_id.alloc(ng * 4 + 4, st);
   R->group_off.alloc((ng + 1) * 8, st);
-  R->id.alloc(n * 4 + 4, st);
-  KL(k_ii_write, grid_for(ng, 256), words.as<u32>(), cnt.as<u64>(), pres, pco.as<u64>(), V, FW,
-     (u32)d->file_lo, R->group_id.as<u32>(), R->group_off.as<u64>(), R->id.as<u32>());
-  GT_CUDA(cudaMemcpyAsync(R->group_off.as<u64>() + ng, &n, 8, cudaMemcpyHostToDevice, st));
-  GT_CUDA(cudaStreamSynchronize(st));
+  KL(k_ii_groups, grid_for(ng + 1, 256), words.as<u32>(), cnt.as<u64>(), off.as<u64>(), n,
+     R->group_id.as<u32>(), R->group_off.as<u64>());
+  R->id = std::move(files);
 }
 
 }  // namespace gt
