@@ -16,6 +16,10 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <chrono>
 
 #include <string>
 #include <vector>
@@ -189,6 +193,24 @@ struct ProfScope {
     kernel<<<(grid), (block), 0, (st)>>>(__VA_ARGS__); \
     ::gt::g_launches++;                                \
   } while (0)
+
+// GT_TRACE=1: synchronising phase timer on stderr (diagnostics only)
+struct Phases {
+  bool on;
+  const char* tag;
+  cudaStream_t st = nullptr;
+  std::chrono::steady_clock::time_point t;
+  explicit Phases(const char* tg, cudaStream_t s = nullptr)
+      : on(getenv("GT_TRACE") && getenv("GT_TRACE")[0] != '0'), tag(tg), st(s),
+        t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    if (st) cudaStreamSynchronize(st);
+    auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[%s] %-28s %9.3f ms\n", tag, what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 inline int bitlen(u64 v) {
   int b = 0;

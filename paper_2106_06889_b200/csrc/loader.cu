@@ -573,6 +573,37 @@ static void build_levels(DeviceDag* d, const DBuf& lvl, const DBuf& off, u64 th,
   out->off[nl + 1] = R;
 }
 
+// The stream-ordered pool keeps freed memory (release threshold = inf) and,
+// once per device, is grown to GT_POOL_RESERVE_FRAC (default 0.4) of the HBM
+// in one allocation: the task paths allocate and free multi-GB scratch whose
+// sizes vary run to run, and growing the pool on demand (mapping physical
+// pages inside a run) costs 10^2 ms per GB-scale step and fragments it.
+static void reserve_pool(int device, cudaStream_t st) {
+  static bool done[64] = {};
+  cudaMemPool_t pool;
+  GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  u64 thr = UINT64_MAX;
+  GT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  if (done[device & 63]) return;
+  done[device & 63] = true;
+  double frac = 0.4;
+  if (const char* e = getenv("GT_POOL_RESERVE_FRAC")) frac = atof(e);
+  size_t free_b = 0, total_b = 0;
+  GT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  size_t want = (size_t)(frac * (double)total_b);
+  if (want > free_b / 10 * 9) want = free_b / 10 * 9;
+  u64 cur = 0;
+  GT_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &cur));
+  if (want <= cur || want < (64ull << 20)) return;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, want, st) == cudaSuccess) {
+    GT_CUDA(cudaFreeAsync(p, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+  } else {
+    cudaGetLastError();  // best effort: the pool then grows on demand
+  }
+}
+
 // grow-only pinned host buffer (the rule-start table of the chain walk)
 struct PinnedU32 {
   u32* p = nullptr;
@@ -588,27 +619,12 @@ struct PinnedU32 {
   }
 };
 
-// GT_TRACE=1: synchronising phase timer of gt_open on stderr
-struct Phases {
-  bool on;
-  cudaStream_t st = nullptr;
-  std::chrono::steady_clock::time_point t;
-  Phases() : on(getenv("GT_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
-  void mark(const char* what) {
-    if (!on) return;
-    if (st) cudaStreamSynchronize(st);
-    auto n = std::chrono::steady_clock::now();
-    fprintf(stderr, "[gt_open] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
-    t = n;
-  }
-};
-
 }  // namespace
 
 void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_lo, u64 file_hi,
                       DeviceDag* d) {
   auto t0 = std::chrono::steady_clock::now();
-  Phases ph;
+  Phases ph("gt_open");
   Parse P;
   parse_dict(blob, nbytes, &P);
   ph.mark("host parse: dictionary");
@@ -617,12 +633,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   if (!d->stream) GT_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
   cudaStream_t st = d->stream;
   ph.st = st;
-  {
-    cudaMemPool_t pool;
-    GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    u64 thr = UINT64_MAX;
-    GT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-  }
+  reserve_pool(device, st);
   ph.mark("stream");
   // start the upload of the whole rules section, then walk the length chain
   // on the host while it is in flight (overlaps when `blob` is pinned)

@@ -299,6 +299,7 @@ static T d2h1(const void* p, cudaStream_t st) {
 
 void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, int* wbits_out) {
   cudaStream_t st = d->stream;
+  Phases ph("seq", st);
   const u32 l = (u32)l_, m = l - 1;
   const u64 R = d->R, E = d->E, nw = d->nw, base = d->nw + d->ns;
   // pack_width, sequence.py:229-231
@@ -321,6 +322,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
            nw, base, d->exp_len.as<u64>(), m, H.as<u32>(), T.as<u32>(), hl.as<u32>(), tl.as<u32>());
     }
   }
+  ph.mark("heads/tails");
   // per-file rule weights: dense top-down rows (F columns) or, for many
   // files, the presence-guided sparse (rule, file) weights (sparse.cu)
   DBuf w;
@@ -333,6 +335,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
     td_file_weights(d, w, &Cw);
   }
 
+  ph.mark("weights");
   // phase 2: windows attributed per body position (two passes + scan)
   WinCtx c{d->body.as<u32>(), d->pos_owner.as<u32>(), d->boff.as<u64>(), d->root_seg.as<u32>(),
            H.as<u32>(), T.as<u32>(), hl.as<u32>(), tl.as<u32>(), nw, base, l, m, (u32)wbits,
@@ -348,6 +351,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   SL(k_write_windows, E, c, E, off.as<u64>(), packed, key.as<u64>(), gram.as<u32>(), src.as<u32>());
   off.release();
 
+  ph.mark("windows");
   // sort by gram
   DBuf skey, sgram, ssrc(N * 4 + 4, st);
   if (packed) {
@@ -365,6 +369,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
     sgram.alloc(N * l * 4 + 4, st);
     SL(k_permute_gram, N, gram.as<u32>(), src.as<u32>(), idx.as<u32>(), N, l, sgram.as<u32>(), ssrc.as<u32>());
   }
+  ph.mark("gram sort");
   key.release();
   gram.release();
   src.release();
@@ -383,6 +388,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
     SL(k_dec_u32, N, rid.as<u32>(), N);
   }
   heads.release();
+  ph.mark("runs");
   // nonzero (run, file) cells in (gram asc, file asc) order
   DBuf crun, ccol, ccnt;
   u64 n = 0;
@@ -415,6 +421,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   }
   ssrc.release();
   rid.release();
+  ph.mark("cells");
   const u64 Wt = d->W;
   const int CB = std::max(1, bitlen(Wt));
   const bool by_file = task == GT_SEQCOUNT;
@@ -426,6 +433,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   sort_pairs_u64_u32(sk.as<u64>(), sk2.as<u64>(), rec.as<u32>(), rec2.as<u32>(), n, CB + MB, st);
   sk.release();
   sk2.release();
+  ph.mark("record sort");
   Rr->n = n;
   Rr->count.alloc(n * 8 + 8, st);
   if (by_file) {
@@ -459,6 +467,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
     GT_CUDA(cudaMemcpyAsync(Rr->group_off.as<u64>() + ng, &n, 8, cudaMemcpyHostToDevice, st));
   }
   GT_CUDA(cudaStreamSynchronize(st));
+  ph.mark("records");
 }
 
 }  // namespace gt

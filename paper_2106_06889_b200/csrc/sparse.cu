@@ -274,12 +274,14 @@ u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf
 
 void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW_out) {
   cudaStream_t st = d->stream;
+  Phases ph("sparse-w", st);
   const u64 R = d->R;
   DBuf pres, rows;
   u32 FW;
   td_file_presence(d, pres, &FW, &rows);
   if (word_pres) *word_pres = std::move(pres);
   *FW_out = FW;
+  ph.mark("presence");
   s->P = bits_to_csr(rows.as<u64>(), R, FW, FW, 1, s->off, s->file, nullptr, st);
   rows.release();
   s->wt.alloc(s->P * 8 + 8, st);
@@ -288,6 +290,7 @@ void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW_out)
   if (d->n_rs)
     SK(k_sparse_seed, d->n_rs, d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs,
        (u32)d->file_lo, nseg, s->off.as<u64>(), s->file.as<u32>(), s->wt.as<u64>());
+  ph.mark("pairs+seeds");
   const u64 Etd = d->te_off.empty() ? 0 : d->te_off.back();
   DBuf deg(Etd * 8 + 8, st), pos(Etd * 8 + 8, st);
   for (int L = 1; L <= d->td.nl; L++) {
@@ -298,16 +301,19 @@ void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW_out)
     SKE(k_sparse_level, d->te_child.as<u32>() + a, d->te_par.as<u32>() + a, d->te_freq.as<u32>() + a, n,
         pos.as<u64>(), deg.as<u64>(), s->off.as<u64>(), s->file.as<u32>(), s->wt.as<u64>());
   }
+  ph.mark("levels");
 }
 
 void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
   cudaStream_t st = d->stream;
+  Phases ph("tv-sparse", st);
   const u64 V = d->nw;
   const u32 Fo = (u32)(d->file_hi - d->file_lo);
   SparseW s;
   DBuf pres;
   u32 FW;
   sparse_file_weights(d, &s, &pres, &FW);
+  ph.mark("weights");
   // (word, file) cells = word presence bits; word-major, files ascending
   DBuf woff, wfile, wword;
   const u64 O = bits_to_csr(pres.as<u64>(), V, FW, 1, V, woff, wfile, &wword, st);
@@ -326,6 +332,7 @@ void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
   if (d->n_rw)
     SK(k_tv_root, d->n_rw, d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(), d->n_rw,
        (u32)d->file_lo, Fo, woff.as<u64>(), wfile.as<u32>(), cnt.as<u64>());
+  ph.mark("cells");
   s = SparseW();
   // file-major, (-count, word) within a file: one stable radix sort of the
   // word-major cells on (file, W - count)
@@ -342,6 +349,7 @@ void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
   Rr->n_groups = Fo;
   Rr->group_off.alloc(((u64)Fo + 1) * 8, st);
   SK(k_csr_offsets, (u64)Fo + 1, wfile.as<u32>(), O, (u64)Fo, Rr->group_off.as<u64>());
+  ph.mark("sort");
 }
 
 u64 sparse_run_cells(DeviceDag* d, const SparseW& s, const u32* rid, const u32* src, u64 N, int FB,
