@@ -28,6 +28,8 @@
 #include "kernels_common.cuh"
 #include "segreduce.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace gt {
 
 thread_local u64 g_launches = 0;
@@ -331,80 +333,121 @@ __device__ __forceinline__ bool dec_to_zero(u32* rem, u32 key, bool active) {
   return atomicSub(&rem[key], k) == k;
 }
 
-// frontier bookkeeping: level of each frontier rule and its parent count
-__global__ void k_bu_frontier(const u32* fr, const u64* fr_n, u32 layer, const u64* par_off, u32* lvl,
-                              u64* deg) {
-  const u64 n = *fr_n;
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const u32 r = fr[i];
-    lvl[r] = layer;
-    deg[i] = par_off[r + 1] - par_off[r];
-  }
+// ---------------------------------------------------------------------------
+// Persistent Kahn layering: ONE cooperative launch runs every layer, frontier
+// counts live on the device, layers are separated by grid barriers (no host
+// round trip per layer).  Bottom-up (TD = false): frontier = rules whose
+// children all finished, edges = parents (par CSR).  Top-down (TD = true):
+// frontier = rules whose non-root parents all finished, edges = children
+// (sub CSR), reachability from the root carried along.  A rule with more
+// than kLight edges is split into chunk tasks of kChunk edges that every
+// warp of the grid shares after a second barrier (a rule with 10^6 parents
+// is never one warp's serial loop).
+// ---------------------------------------------------------------------------
+constexpr u32 kLight = 8, kChunk = 256;
+
+// warp-aggregated append of the lanes with `take` set (one atomic per warp
+// on the shared frontier counter instead of one per completed rule; must be
+// called by every lane of the warp)
+__device__ __forceinline__ void warp_append(bool take, u32 v, u32* q, u64* cnt) {
+  const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
+  if (!m) return;
+  const unsigned lane = threadIdx.x & 31u;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if ((int)lane == leader) base = atomicAdd((unsigned long long*)cnt, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xFFFFFFFFu, base, leader);
+  if (take) q[base + __popc(m & ((1u << lane) - 1u))] = v;
 }
 
-// bottom-up Kahn layer, edge-balanced: one thread per (frontier rule, parent)
-// edge, located by binary search in the exclusive scan of the frontier's
-// parent counts (a rule with 10^6 parents spreads over the whole grid);
-// parents whose last child finished join the next frontier.
-__global__ void k_bu_edges(const u32* fr, const u64* fr_n, const u64* pos, const u64* deg,
-                           const u64* par_off, const u32* par_ids, u32* rem, u32* next, u64* next_n) {
-  const u64 n = *fr_n;
-  if (!n) return;
-  const u64 T = pos[n - 1] + deg[n - 1];
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 base = (u64)blockIdx.x * blockDim.x; base < T; base += stride) {
-    const u64 e = base + (threadIdx.x & ~31u) + (threadIdx.x & 31u);
-    const bool active = e < T;
-    u32 p = 0;
-    if (active) {
-      u64 lo = 0, hi = n;  // last i with pos[i] <= e
-      while (hi - lo > 1) {
-        const u64 m = (lo + hi) >> 1;
-        if (pos[m] <= e) lo = m;
-        else hi = m;
-      }
-      const u32 r = fr[lo];
-      p = par_ids[par_off[r] + (e - pos[lo])];
-    }
-    if (dec_to_zero(rem, p, active)) next[atomicAdd((unsigned long long*)next_n, 1ull)] = p;
-  }
+struct KahnCtl {
+  u64 cnt[3];    // rotating frontier counts: layer L reads cnt[L%3], appends to cnt[(L+1)%3]
+  u64 ntask[2];  // heavy-task counts, layer L uses ntask[L&1]
+  u64 processed;
+  u64 layers;
+};
+
+__device__ __forceinline__ u64 ld_cg64(const u64* p) {
+  return (u64)__ldcg(reinterpret_cast<const unsigned long long*>(p));
 }
 
-// top-down Kahn layer over non-root in-edges (children per rule are few);
-// reachability rides along
-__global__ void k_td_layer(const u32* fr, const u64* fr_n, u32 layer, const u64* par_off,
-                           const u32* par_ids, const uint8_t* root_parent, const u64* sub_off,
-                           const u32* sub_ids, u32* rem, u32* lvl, uint8_t* reach, u32* next,
-                           u64* next_n) {
-  const u64 n = *fr_n;
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const u64 i = base + threadIdx.x;
-    const bool active = i < n;
-    u32 r = 0;
-    u64 e0 = 0, e1 = 0;
-    if (active) {
-      r = fr[i];
-      lvl[r] = layer;
-      bool rc = root_parent[r];
-      for (u64 e = par_off[r]; e < par_off[r + 1] && !rc; e++) {
-        const u32 p = par_ids[e];
-        if (p != 0 && reach[p]) rc = true;
-      }
-      reach[r] = rc;
-      e0 = sub_off[r];
-      e1 = sub_off[r + 1];
+template <bool TD>
+__global__ void __launch_bounds__(256) k_kahn(KahnCtl* ctl, u32* q0, u32* q1, const u64* __restrict__ off,
+                                              const u32* __restrict__ ids, u32* rem, u32* lvl,
+                                              const u64* __restrict__ par_off,
+                                              const u32* __restrict__ par_ids,
+                                              const uint8_t* __restrict__ root_parent, uint8_t* reach,
+                                              uint2* tasks, u64 max_layers) {
+  cg::grid_group grid = cg::this_grid();
+  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 nthreads = (u64)gridDim.x * blockDim.x;
+  const unsigned lane = threadIdx.x & 31u;
+  u64 total = 0, L = 1;
+  for (;; L++) {
+    const u64 n = ld_cg64(&ctl->cnt[L % 3]);
+    if (n == 0 || L > max_layers) break;
+    total += n;
+    if (gtid == 0) {
+      ctl->cnt[(L + 2) % 3] = 0;
+      ctl->ntask[(L + 1) & 1] = 0;
     }
-    // children, one per step, warp-uniform trip count
-    u64 len = e1 - e0, mx = len;
+    const u32* cur = (L & 1) ? q1 : q0;
+    u32* nxt = (L & 1) ? q0 : q1;
+    u64* ncnt = &ctl->cnt[(L + 1) % 3];
+    u64* ntask = &ctl->ntask[L & 1];
+    // phase A: light rules inline, heavy rules -> chunk tasks
+    for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += nthreads) {
+      const u64 i = base + threadIdx.x;
+      const bool active = i < n;
+      u32 r = 0;
+      u64 e0 = 0, len = 0;
+      if (active) {
+        r = __ldcg(cur + i);
+        lvl[r] = (u32)L;
+        if (TD) {
+          bool rc = root_parent[r];
+          const volatile uint8_t* rv = reach;
+          for (u64 e = par_off[r]; e < par_off[r + 1] && !rc; e++) {
+            const u32 p = par_ids[e];
+            if (p != 0 && rv[p]) rc = true;
+          }
+          reach[r] = rc;
+        }
+        e0 = off[r];
+        len = off[r + 1] - e0;
+        if (len > kLight) {
+          const u64 nch = (len + kChunk - 1) / kChunk;
+          const u64 t0 = atomicAdd((unsigned long long*)ntask, (unsigned long long)nch);
+          for (u64 k = 0; k < nch; k++) tasks[t0 + k] = make_uint2(r, (u32)(k * kChunk));
+          len = 0;
+        }
+      }
+      u64 mx = len;
 #pragma unroll
-    for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, d));
-    for (u64 k = 0; k < mx; k++) {
-      const bool a = k < len;
-      const u32 c = a ? sub_ids[e0 + k] : 0u;
-      if (dec_to_zero(rem, c, a)) next[atomicAdd((unsigned long long*)next_n, 1ull)] = c;
+      for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, d));
+      for (u64 k = 0; k < mx; k++) {
+        const bool a = k < len;
+        const u32 c = a ? ids[e0 + k] : 0u;
+        warp_append(dec_to_zero(rem, c, a), c, nxt, ncnt);
+      }
     }
+    grid.sync();
+    // phase B: chunk tasks, one warp per task
+    const u64 nt = ld_cg64(ntask);
+    for (u64 t = gtid >> 5; t < nt; t += nthreads >> 5) {
+      const uint2 tk = __ldcg(tasks + t);
+      const u64 a = off[tk.x] + tk.y, b = min(off[tk.x + 1], a + kChunk);
+      for (u64 e = a; e < b; e += 32) {
+        const bool act = e + lane < b;
+        const u32 c = act ? ids[e + lane] : 0u;
+        warp_append(dec_to_zero(rem, c, act), c, nxt, ncnt);
+      }
+    }
+    grid.sync();
+  }
+  if (gtid == 0) {
+    ctl->processed = total;
+    ctl->layers = L - 1;
   }
 }
 
@@ -526,27 +569,6 @@ static void d2h(T* dst, const void* src, size_t n, cudaStream_t s) {
 }
 
 #define LAUNCH(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
-
-// Kahn layering driver: returns number of layers and total processed
-template <class LayerFn>
-static int run_layers(DBuf& fr, DBuf& nx, DBuf& cnt, u64 first_n, u64 R, cudaStream_t st,
-                      LayerFn layer, u64* processed) {
-  u64 n = first_n, total = 0;
-  int L = 0;
-  while (n) {
-    L++;
-    total += n;
-    GT_CUDA(cudaMemsetAsync(cnt.as<u64>() + 1, 0, sizeof(u64), st));
-    layer((u32)L, n);
-    std::swap(fr, nx);
-    // move next count into slot 0
-    GT_CUDA(cudaMemcpyAsync(cnt.as<u64>(), cnt.as<u64>() + 1, sizeof(u64), cudaMemcpyDeviceToDevice, st));
-    d2h(&n, cnt.as<u64>(), 1, st);
-    if (L > (int)R + 2) break;
-  }
-  *processed = total;
-  return L;
-}
 
 static void build_levels(DeviceDag* d, const DBuf& lvl, const DBuf& off, u64 th, int nl, Levels* out) {
   cudaStream_t st = d->stream;
@@ -773,43 +795,60 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   GT_CUDA(cudaMemsetAsync(d->td_level.p, 0, R * 4, st));
   LAUNCH(k_degrees, R, d->sub_off.as<u64>(), d->par_off.as<u64>(), d->par_ids.as<u32>(), R,
          rem_bu.as<u32>(), rem_td.as<u32>(), rootp.as<uint8_t>());
-  LAUNCH(k_flag_zero, R, rem_bu.as<u32>(), R, 0, flag.as<uint8_t>());
-  select_flagged_index(flag.as<uint8_t>(), fr.as<u32>(), fcnt.as<u64>(), R, st);
-  u64 n0;
-  d2h(&n0, fcnt.p, 1, st);
+  // persistent Kahn layering, bottom-up (doubles as the cycle check), then
+  // top-down (carries reachability): one cooperative launch each
+  const u64 ntask_max = Es / kChunk + R + 1;
+  DBuf tasks(ntask_max * 8, st), ctl_b(sizeof(KahnCtl), st);
+  KahnCtl* ctl = ctl_b.as<KahnCtl>();
+  DBuf reach(R, st), firstu(4, st);
+  GT_CUDA(cudaMemsetAsync(reach.p, 0, R, st));
+  auto kahn = [&](bool td, DBuf& rem, const DBuf& off, const DBuf& ids, DBuf& lvl, u64* processed) {
+    GT_CUDA(cudaMemsetAsync(ctl, 0, sizeof(KahnCtl), st));
+    LAUNCH(k_flag_zero, R, rem.as<u32>(), R, td ? 1 : 0, flag.as<uint8_t>());
+    // first frontier -> q1 (layer 1 reads q1), its count -> cnt[1]
+    select_flagged_index(flag.as<uint8_t>(), nx.as<u32>(), &ctl->cnt[1], R, st);
+    const void* kern = td ? (const void*)k_kahn<true> : (const void*)k_kahn<false>;
+    static int per_sm[2] = {-1, -1};
+    int& ps = per_sm[td ? 1 : 0];
+    if (ps < 0) {
+      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, 256, 0));
+      ps = std::max(ps, 1);
+    }
+    int nsm = 148;
+    GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    u32* q0 = fr.as<u32>();
+    u32* q1 = nx.as<u32>();
+    const u64* po = d->par_off.as<u64>();
+    const u32* pi = d->par_ids.as<u32>();
+    const uint8_t* rp = rootp.as<uint8_t>();
+    uint8_t* rc = reach.as<uint8_t>();
+    uint2* tk = tasks.as<uint2>();
+    const u64* o = off.as<u64>();
+    const u32* ii = ids.as<u32>();
+    u32* rm = rem.as<u32>();
+    u32* lv = lvl.as<u32>();
+    u64 maxl = R + 2;
+    void* args[] = {(void*)&ctl, (void*)&q0, (void*)&q1, (void*)&o, (void*)&ii, (void*)&rm, (void*)&lv,
+                    (void*)&po, (void*)&pi, (void*)&rp, (void*)&rc, (void*)&tk, (void*)&maxl};
+    {
+      ProfScope ps_(td ? "k_kahn<td>" : "k_kahn<bu>", st);
+      GT_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)(nsm * ps)), dim3(256), args, 0, st));
+      g_launches++;
+    }
+    KahnCtl h;
+    d2h(&h, ctl, 1, st);
+    *processed = h.processed;
+    return (int)h.layers;
+  };
   u64 processed = 0;
-  DBuf fdeg(R * 8 + 8, st), fpos(R * 8 + 8, st);
-  int nbu = run_layers(fr, nx, fcnt, n0, R, st, [&](u32 L, u64 n) {
-    k_bu_frontier<<<grid_for(n, 256), 256, 0, st>>>(fr.as<u32>(), fcnt.as<u64>(), L, d->par_off.as<u64>(),
-                                                    d->bu_level.as<u32>(), fdeg.as<u64>());
-    exclusive_scan_u64(fdeg.as<u64>(), fpos.as<u64>(), n, st);
-    k_bu_edges<<<148 * 16, 256, 0, st>>>(fr.as<u32>(), fcnt.as<u64>(), fpos.as<u64>(), fdeg.as<u64>(),
-                                         d->par_off.as<u64>(), d->par_ids.as<u32>(), rem_bu.as<u32>(),
-                                         nx.as<u32>(), fcnt.as<u64>() + 1);
-    g_launches += 2;
-  }, &processed);
-  fdeg.release();
-  fpos.release();
+  int nbu = kahn(false, rem_bu, d->par_off, d->par_ids, d->bu_level, &processed);
   if (processed < R) cycle_message(blob, P);
   ph.mark("bottom-up layering");
   // depth = height(root) = layer(root) - 1; reference bu_level excludes root
   u32 root_layer;
   d2h(&root_layer, d->bu_level.p, 1, st);
   d->depth = (i64)root_layer - 1;
-  DBuf reach(R, st), firstu(4, st);
-  GT_CUDA(cudaMemsetAsync(reach.p, 0, R, st));
-  LAUNCH(k_flag_zero, R, rem_td.as<u32>(), R, 1, flag.as<uint8_t>());
-  select_flagged_index(flag.as<uint8_t>(), fr.as<u32>(), fcnt.as<u64>(), R, st);
-  d2h(&n0, fcnt.p, 1, st);
-  int ntd = run_layers(fr, nx, fcnt, n0, R, st, [&](u32 L, u64 n) {
-    k_td_layer<<<grid_for(n, 256), 256, 0, st>>>(fr.as<u32>(), fcnt.as<u64>(), L,
-                                                 d->par_off.as<u64>(), d->par_ids.as<u32>(),
-                                                 rootp.as<uint8_t>(), d->sub_off.as<u64>(),
-                                                 d->sub_ids.as<u32>(), rem_td.as<u32>(),
-                                                 d->td_level.as<u32>(), reach.as<uint8_t>(),
-                                                 nx.as<u32>(), fcnt.as<u64>() + 1);
-    g_launches++;
-  }, &processed);
+  int ntd = kahn(true, rem_td, d->sub_off, d->sub_ids, d->td_level, &processed);
   GT_CUDA(cudaMemsetAsync(firstu.p, 0xFF, 4, st));
   LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, firstu.as<u32>());
   u32 fu;

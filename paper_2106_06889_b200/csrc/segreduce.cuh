@@ -8,11 +8,14 @@
 // chunk_factor x average are split into contiguous ranges
 // "fine-grained thread-level partitioning"): items, not rules, are dealt out
 // in fixed-size chunks, so a rule with 10^6 parents costs 10^6/chunk chunks
-// spread over the whole GPU instead of one serial warp.  A run of equal dst
-// interior to a chunk is owned by that chunk and updated with a plain
-// read-modify-write; a run touching a chunk boundary is combined atomically
-// (u64 atomicAdd / atomicOr), so a hot destination costs one atomic per
-// chunk, not one per item (the warp aggregation of north_star).
+// spread over the whole GPU instead of one serial warp.  Runs of equal dst
+// are combined in registers (warp shuffle segmented scan, or a team's
+// sequential walk) and each run is flushed with ONE fire-and-forget u64
+// reduction (atomicAdd / atomicOr without return -> RED at L2): no
+// read-modify-write round trip on the critical path, and a hot destination
+// costs one reduction per chunk, not one per item (the warp aggregation of
+// north_star).  Outputs may be pre-seeded; everything is an integer sum or
+// bitwise OR, so the result is order-independent and bit-exact.
 //
 // Uses:  top-down level propagation (dst = child, src = parent; items = the
 //        level's non-root parent edges), bottom-up sums (dst = rule, src =
@@ -82,61 +85,61 @@ template <class Mode, class Src, class Out>
 __device__ __forceinline__ void segred1_body(const u32* __restrict__ dst, const u32* __restrict__ src,
                                              const u32* __restrict__ freq, u64 n, int K, Src in,
                                              Out out, u64 warp, u64 nwarps) {
+  // K 32-item steps per tile; the (up to) U steps of a group are
+  // loaded together (U independent row gathers in flight per lane), then
+  // reduced one after the other with the carried run
+  constexpr int U = 4;
   const unsigned lane = threadIdx.x & 31u;
   const u64 TILE = 32ull * K;
   for (u64 t0 = warp * TILE; t0 < n; t0 += nwarps * TILE) {
-    const u32 first = dst[t0];
-    const bool first_shared = t0 > 0 && dst[t0 - 1] == first;
     const u64 tend = t0 + TILE < n ? t0 + TILE : n;
-    const bool last_shared = tend < n && dst[tend] == dst[tend - 1];
-    const u32 last = dst[tend - 1];
     u32 carry_d = 0xFFFFFFFFu;
     u64 carry_v = 0;
-    // software pipeline: values of step k+1 are loaded while step k reduces
-    u64 i = t0 + lane;
-    u32 d_n = i < n ? dst[i] : 0xFFFFFFFFu;
-    u64 v_n = i < n ? Mode::combine(item_freq(freq, i), in(src[i], 0)) : 0;
 #pragma unroll 1
-    for (int k = 0; k < K; k++) {
-      const u32 d = d_n;
-      u64 v = v_n;
-      const bool ok = d != 0xFFFFFFFFu;
-      const u64 j = i + 32;
-      if (k + 1 < K) {
-        d_n = j < tend ? dst[j] : 0xFFFFFFFFu;
-        v_n = j < tend ? Mode::combine(item_freq(freq, j), in(src[j], 0)) : 0;
-      }
-      i = j;
-      const u32 d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
-      if (carry_d != 0xFFFFFFFFu && d0 != carry_d) {  // the carried run ended at the last step
-        if (lane == 0) {
-          u64* p = out(carry_d, 0);
-          if (carry_d == first && first_shared) Mode::atomic(p, carry_v);
-          else *p = Mode::merge(ldcg(p), carry_v);
-        }
-        carry_d = 0xFFFFFFFFu;
-        carry_v = 0;
+    for (int k0 = 0; k0 < K; k0 += U) {
+      u32 dd[U];
+      u64 vv[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const u64 i = t0 + (u64)(k0 + u) * 32 + lane;
+        const bool in_tile = k0 + u < K && i < tend;
+        dd[u] = in_tile ? dst[i] : 0xFFFFFFFFu;
+        vv[u] = in_tile ? Mode::combine(item_freq(freq, i), in(src[i], 0)) : 0;
       }
 #pragma unroll
-      for (int s = 1; s < 32; s <<= 1) {
-        const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, s);
-        const u32 od = __shfl_up_sync(0xFFFFFFFFu, d, s);
-        if (lane >= (unsigned)s && od == d) v = Mode::merge(v, ov);
+      for (int u = 0; u < U; u++) {
+        if (k0 + u >= K) break;  // warp-uniform
+        const u32 d = dd[u];
+        u64 v = vv[u];
+        const bool ok = d != 0xFFFFFFFFu;
+        const u32 d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+        if (carry_d != 0xFFFFFFFFu && d0 != carry_d) {  // the carried run ended at the last step
+          if (lane == 0) {
+            u64* p = out(carry_d, 0);
+            Mode::atomic(p, carry_v);
+          }
+          carry_d = 0xFFFFFFFFu;
+          carry_v = 0;
+        }
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+          const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, s);
+          const u32 od = __shfl_up_sync(0xFFFFFFFFu, d, s);
+          if (lane >= (unsigned)s && od == d) v = Mode::merge(v, ov);
+        }
+        if (d == carry_d) v = Mode::merge(v, carry_v);
+        const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
+        if (ok && lane != 31 && dn != d) {  // run ends inside this step
+          u64* p = out(d, 0);
+          Mode::atomic(p, v);
+        }
+        carry_d = __shfl_sync(0xFFFFFFFFu, d, 31);
+        carry_v = __shfl_sync(0xFFFFFFFFu, v, 31);
       }
-      if (d == carry_d) v = Mode::merge(v, carry_v);
-      const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
-      if (ok && lane != 31 && dn != d) {  // run ends inside this step
-        u64* p = out(d, 0);
-        if ((d == first && first_shared) || (d == last && last_shared)) Mode::atomic(p, v);
-        else *p = Mode::merge(ldcg(p), v);
-      }
-      carry_d = __shfl_sync(0xFFFFFFFFu, d, 31);
-      carry_v = __shfl_sync(0xFFFFFFFFu, v, 31);
     }
     if (lane == 0 && carry_d != 0xFFFFFFFFu) {
       u64* p = out(carry_d, 0);
-      if ((carry_d == first && first_shared) || (carry_d == last && last_shared)) Mode::atomic(p, carry_v);
-      else *p = Mode::merge(ldcg(p), carry_v);
+      Mode::atomic(p, carry_v);
     }
   }
 }
@@ -164,9 +167,7 @@ __device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const 
   const u32 tl = threadIdx.x % G;
   for (u64 t = gtid / G; t * K < n; t += teams) {
     const u64 a = t * K, b = a + K < n ? a + K : n;  // K: items per team (runtime)
-    const u32 dfirst = dst[a], dlast = dst[b - 1];
-    const bool first_shared = a > 0 && dst[a - 1] == dfirst;
-    const bool last_shared = b < n && dst[b] == dlast;
+    const u32 dfirst = dst[a];
     for (u32 col = tl; col < C; col += G) {
       u32 cd = dfirst;
       u64 acc = 0;
@@ -184,8 +185,7 @@ __device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const 
           if (dd[j] == 0xFFFFFFFFu) break;
           if (dd[j] != cd) {
             u64* p = out(cd, col);
-            if (cd == dfirst && first_shared) Mode::atomic(p, acc);
-            else *p = Mode::merge(ldcg(p), acc);
+            Mode::atomic(p, acc);
             cd = dd[j];
             acc = 0;
           }
@@ -193,8 +193,7 @@ __device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const 
         }
       }
       u64* p = out(cd, col);
-      if ((cd == dfirst && first_shared) || (cd == dlast && last_shared)) Mode::atomic(p, acc);
-      else *p = Mode::merge(ldcg(p), acc);
+      Mode::atomic(p, acc);
     }
   }
 }
