@@ -463,6 +463,23 @@ __global__ void k_flag_nonzero_u32(const u32* v, u64 n, uint8_t* f) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f[i] = v[i] != 0;
 }
 
+__global__ void k_root_cycle(const u64* par_off, const u32* par_ids, const uint8_t* reach, u32* bad) {
+  for (u64 e = par_off[0] + threadIdx.x; e < par_off[1]; e += blockDim.x) {
+    const u32 p = par_ids[e];
+    if (p == 0 || reach[p]) *bad = 1;
+  }
+}
+
+__global__ void k_fill_u64(u64* a, u64 n, u64 v) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = v;
+}
+
+__global__ void k_u64_to_u32(const u64* a, u64 n, u32* b) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) b[i] = (u32)a[i];
+}
+
 __global__ void k_first_unreached(const uint8_t* reach, u64 R, u32* out) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 r = 1 + (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride)
@@ -840,15 +857,21 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     *processed = h.processed;
     return (int)h.layers;
   };
+  // top-down Kahn layering: the frontier never reaches a rule on (or below)
+  // a reference cycle, so an incomplete layering is the cycle check
+  // (grammar.py:127-161 order: cycles before unreachable rules, dag.py:173-184)
   u64 processed = 0;
-  int nbu = kahn(false, rem_bu, d->par_off, d->par_ids, d->bu_level, &processed);
-  if (processed < R) cycle_message(blob, P);
-  ph.mark("bottom-up layering");
-  // depth = height(root) = layer(root) - 1; reference bu_level excludes root
-  u32 root_layer;
-  d2h(&root_layer, d->bu_level.p, 1, st);
-  d->depth = (i64)root_layer - 1;
   int ntd = kahn(true, rem_td, d->sub_off, d->sub_ids, d->td_level, &processed);
+  // every rule but the root must be layered, and no reachable rule (nor the
+  // root itself) may reference the root: either way there is a cycle
+  {
+    DBuf bad(4, st);
+    GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+    LAUNCH(k_root_cycle, 1, d->par_off.as<u64>(), d->par_ids.as<u32>(), reach.as<uint8_t>(), bad.as<u32>());
+    u32 rb = 0;
+    d2h(&rb, bad.p, 1, st);
+    if (processed + 1 < R || rb) cycle_message(blob, P);
+  }
   GT_CUDA(cudaMemsetAsync(firstu.p, 0xFF, 4, st));
   LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, firstu.as<u32>());
   u32 fu;
@@ -859,10 +882,6 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   rem_td.release();
   fr.release();
   nx.release();
-
-  // level-ordered rule lists (light/heavy split)
-  build_levels(d, d->bu_level, d->sub_off, 16, nbu, &d->bu);
-  build_levels(d, d->td_level, d->par_off, 16, ntd, &d->td);
 
   // ---- level-ordered edge lists (radix sort is stable: within a level the
   // edges keep (child, parent) resp. (rule, child) order) -------------------
@@ -897,13 +916,34 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     level_edges(child_sorted.as<u32>(), keep.as<uint8_t>(), d->td_level.as<u32>(), ntd,
                 child_sorted.as<u32>(), d->par_ids.as<u32>(), d->par_freqs.as<u32>(), d->te_child,
                 d->te_par, d->te_freq, d->te_off, d->te_off_dev);
-    // bu: sub entries (grouped by rule) by the rule's bottom-up layer
-    level_edges(sub_rule.as<u32>(), nullptr, d->bu_level.as<u32>(), nbu, sub_rule.as<u32>(),
+    // be: sub entries (grouped by rule) by the rule's TOP-DOWN level; walked
+    // in decreasing level order every child is finished before its parents
+    // (a child's td level exceeds each parent's), which is all the bottom-up
+    // sums need.  The root (td level 0) comes last.
+    level_edges(sub_rule.as<u32>(), nullptr, d->td_level.as<u32>(), ntd, sub_rule.as<u32>(),
                 d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), d->be_rule, d->be_child, d->be_freq,
                 d->be_off, d->be_off_dev);
   }
   sub_rule.release();
   child_sorted.release();
+  // bottom-up levels = heights (leaf = 1; the reference's bottom-up rounds,
+  // engine.py:313-335), one persistent max pass in decreasing td level order
+  int nbu = 0;
+  {
+    DBuf hgt(R * 8, st);
+    LAUNCH(k_fill_u64, R, hgt.as<u64>(), R, 1ull);
+    seg_reduce_levels<HeightMode>("k_heights", d->be_rule.as<u32>(), d->be_child.as<u32>(),
+                                  d->be_freq.as<u32>(), d->be_off_dev.as<u64>(), 0, ntd, 1,
+                                  RowSrc{hgt.as<u64>(), 1}, OutRowMajor{hgt.as<u64>(), 1}, st, true);
+    LAUNCH(k_u64_to_u32, R, hgt.as<u64>(), R, d->bu_level.as<u32>());
+    u64 h0 = 0;
+    d2h(&h0, hgt.p, 1, st);  // height of the root, the highest rule
+    nbu = (int)h0;
+    d->depth = (i64)h0 - 1;
+  }
+  // level-ordered rule lists (light/heavy split)
+  build_levels(d, d->bu_level, d->sub_off, 16, nbu, &d->bu);
+  build_levels(d, d->td_level, d->par_off, 16, ntd, &d->td);
   // the reference's bottom-up rounds exclude the root (engine.py:305-310)
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
   ph.mark("level lists");
@@ -948,11 +988,12 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // ---- exp_len by bottom-up level (grammar.py:109-124) --------------------
   d->exp_len.alloc(R * 8, st);
   GT_CUDA(cudaMemcpyAsync(d->exp_len.p, d->own_tok.p, R * 8, cudaMemcpyDeviceToDevice, st));
-  // exp_len[r] = own tokens + Σ f · exp_len[child], bottom-up levels 2..nbu
-  // in one persistent launch (level 1 = leaves, no items)
+  // exp_len[r] = own tokens + Σ f · exp_len[child], in decreasing top-down
+  // level order (children first) in one persistent launch
   seg_reduce_levels<SumMode>("k_exp_len", d->be_rule.as<u32>(), d->be_child.as<u32>(),
-                             d->be_freq.as<u32>(), d->be_off_dev.as<u64>(), 2, nbu, 1,
-                             RowSrc{d->exp_len.as<u64>(), 1}, OutRowMajor{d->exp_len.as<u64>(), 1}, st);
+                             d->be_freq.as<u32>(), d->be_off_dev.as<u64>(), 0, ntd, 1,
+                             RowSrc{d->exp_len.as<u64>(), 1}, OutRowMajor{d->exp_len.as<u64>(), 1}, st,
+                             true);
   d2h(&d->W, d->exp_len.p, 1, st);
   ph.mark("segments+exp_len");
 

@@ -49,6 +49,16 @@ struct OrMode {
   }
 };
 
+// height pass (bottom-up levels without Kahn): height(r) = max(height(r),
+// 1 + height(child)), combined with u64 atomicMax
+struct HeightMode {
+  __device__ static __forceinline__ u64 combine(u32, u64 x) { return x + 1; }
+  __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a > b ? a : b; }
+  __device__ static __forceinline__ void atomic(u64* p, u64 v) {
+    atomicMax((unsigned long long*)p, (unsigned long long)v);
+  }
+};
+
 // ---- source row functors ----------------------------------------------------
 // Row and output reads go through L2 (ld.global.cg): the level loops of a
 // persistent launch read rows other SMs wrote before the grid barrier, and a
@@ -219,11 +229,12 @@ __global__ void __launch_bounds__(256) k_segred_levels(const u32* __restrict__ d
                                                        const u32* __restrict__ src,
                                                        const u32* __restrict__ freq,
                                                        const u64* __restrict__ lvl_off, int L0, int L1,
-                                                       u32 C, Src in, Out out) {
+                                                       int reverse, u32 C, Src in, Out out) {
   cg::grid_group grid = cg::this_grid();
   const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   const u64 nthreads = (u64)gridDim.x * blockDim.x;
-  for (int L = L0; L <= L1; L++) {
+  for (int it = 0; it <= L1 - L0; it++) {
+    const int L = reverse ? L1 - it : L0 + it;
     const u64 a = lvl_off[L], n = lvl_off[L + 1] - a;
     if (n) {
       if (G == 1) {
@@ -238,7 +249,7 @@ __global__ void __launch_bounds__(256) k_segred_levels(const u32* __restrict__ d
         segredG_body<G, Mode>(dst + a, src + a, freq ? freq + a : nullptr, n, K, C, in, out, gtid, nthreads);
       }
     }
-    if (L < L1) grid.sync();
+    if (it < L1 - L0) grid.sync();
   }
 }
 
@@ -286,7 +297,8 @@ void seg_reduce(const char* name, const u32* dst, const u32* src, const u32* fre
 // offsets).  One cooperative launch with every block resident.
 template <int G, class Mode, class Src, class Out>
 void seg_reduce_levels_G(const char* name, const u32* dst, const u32* src, const u32* freq,
-                         const u64* lvl_off_dev, int L0, int L1, u32 C, Src in, Out out, cudaStream_t st) {
+                         const u64* lvl_off_dev, int L0, int L1, int reverse, u32 C, Src in, Out out,
+                         cudaStream_t st) {
   auto kern = k_segred_levels<G, Mode, Src, Out>;
   static int per_sm = -1;  // per instantiation
   if (per_sm < 0) {
@@ -298,22 +310,25 @@ void seg_reduce_levels_G(const char* name, const u32* dst, const u32* src, const
   GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   dim3 grid((unsigned)(nsm * per_sm)), block(256);
   void* args[] = {(void*)&dst, (void*)&src, (void*)&freq, (void*)&lvl_off_dev, (void*)&L0, (void*)&L1,
-                  (void*)&C, (void*)&in, (void*)&out};
+                  (void*)&reverse, (void*)&C, (void*)&in, (void*)&out};
   ProfScope ps(name, st);
   GT_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, block, args, 0, st));
   g_launches++;
 }
 
+// levels [L0, L1] in increasing order, or decreasing with reverse = true
 template <class Mode, class Src, class Out>
 void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u32* freq,
-                       const u64* lvl_off_dev, int L0, int L1, u32 C, Src in, Out out, cudaStream_t st) {
+                       const u64* lvl_off_dev, int L0, int L1, u32 C, Src in, Out out, cudaStream_t st,
+                       bool reverse = false) {
   if (L1 < L0 || !C) return;
-  if (C == 1) seg_reduce_levels_G<1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
-  else if (C <= 2) seg_reduce_levels_G<2, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
-  else if (C <= 4) seg_reduce_levels_G<4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
-  else if (C <= 8) seg_reduce_levels_G<8, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
-  else if (C <= 16) seg_reduce_levels_G<16, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
-  else seg_reduce_levels_G<32, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, C, in, out, st);
+  const int rv = reverse ? 1 : 0;
+  if (C == 1) seg_reduce_levels_G<1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
+  else if (C <= 2) seg_reduce_levels_G<2, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
+  else if (C <= 4) seg_reduce_levels_G<4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
+  else if (C <= 8) seg_reduce_levels_G<8, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
+  else if (C <= 16) seg_reduce_levels_G<16, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
+  else seg_reduce_levels_G<32, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
 }
 
 }  // namespace gt
