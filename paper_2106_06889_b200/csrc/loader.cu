@@ -239,6 +239,47 @@ __global__ void k_mark_len(const u32* rstart, u64 R, u32* mark) {
     mark[rstart[i] - 1] = 1;
 }
 
+// ---- rule-chain parse on the device (pointer doubling) ----------------------
+// The rules section is a chain of (length, body) records: record i starts at
+// p_i, p_{i+1} = p_i + 1 + len(p_i).  With J_0(j) = j + 1 + raw[j] (clamped
+// to the end n) for EVERY word j and J_{k+1} = J_k o J_k, the start of rule i
+// is J applied along the binary digits of i to p_0 = 0: log2(R) doubling
+// passes over the section plus log2(R) passes over the rules, all parallel.
+__global__ void k_jump0(const u32* raw, u64 n, u32* J) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += stride) {
+    const u64 nx = j < n ? j + 1 + (u64)raw[j] : n;
+    J[j] = (u32)(nx < n ? nx : n);
+  }
+}
+
+__global__ void k_jump_double(const u32* __restrict__ Jk, u64 n, u32* __restrict__ Jk1) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += stride) Jk1[j] = Jk[Jk[j]];
+}
+
+// rule starts i = t*step (known) -> i + half
+__global__ void k_chain_level(const u32* __restrict__ Jk, u64 R, u64 step, u64 half, u32* pos) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t * step + half < R; t += stride)
+    pos[t * step + half] = Jk[pos[t * step]];
+}
+
+// every rule start inside the section, the last record ending exactly at the
+// end; rstart = first symbol of each rule
+__global__ void k_chain_check(const u32* pos, const u32* raw, u64 R, u64 n, u32* bad, u32* rstart) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += stride) {
+    const u64 p = pos[i];
+    if (p >= n) {
+      *bad = 1;
+      continue;
+    }
+    rstart[i] = (u32)(p + 1);
+    if (i + 1 == R && p + 1 + (u64)raw[p] != n) *bad = 1;
+  }
+}
+
 __global__ void k_boff(const u32* rstart, u64 R, u64 E, u64* boff) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= R; i += stride)
@@ -679,22 +720,59 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   const u64 nsec = (nbytes - P.rules_pos) / 4;
   DBuf raw(nsec * 4 + 4, st);
   if (nsec) GT_CUDA(cudaMemcpyAsync(raw.p, blob + P.rules_pos, nsec * 4, cudaMemcpyHostToDevice, st));
+  // the rule-start table: on the device by pointer doubling; the host walk
+  // (parse_rules, the reference's sequential reader) runs only to produce the
+  // exact error of a malformed section, or when an error path needs it
   static thread_local PinnedU32 rstart_host;
-  P.rstart = rstart_host.get(P.R);
-  parse_rules(blob, nbytes, &P);
-  ph.mark("host parse: rule chain");
-  if (P.trunc_rule >= 0) {
+  bool host_chain = false;
+  auto need_host_chain = [&]() {
+    if (host_chain) return;
     GT_CUDA(cudaStreamSynchronize(st));
-    host_range_check(blob, P, (u64)P.trunc_rule);
-    char buf[96];
-    snprintf(buf, sizeof buf, P.trunc_what.c_str(), P.trunc_rule);
-    fail(GT_E_FORMAT, "truncated input while reading %s", buf);
+    P.rstart = rstart_host.get(P.R);
+    parse_rules(blob, nbytes, &P);
+    host_chain = true;
+  };
+  DBuf rstart(P.R * 4 + 4, st);
+  {
+    const u64 n = nsec;
+    const int K = bitlen(P.R - 1);  // J_0 .. J_{K-1}
+    bool ok = n >= 1 && n < 0xFFFFFFFFull && (nbytes - P.rules_pos) % 4 == 0;
+    if (ok) {
+      DBuf J((u64)std::max(K, 1) * (n + 1) * 4, st), pos(P.R * 4, st), bad(4, st);
+      u32* Jb = J.as<u32>();
+      LAUNCH(k_jump0, n + 1, raw.as<u32>(), n, Jb);
+      for (int k = 1; k < K; k++)
+        LAUNCH(k_jump_double, n + 1, Jb + (u64)(k - 1) * (n + 1), n, Jb + (u64)k * (n + 1));
+      GT_CUDA(cudaMemsetAsync(pos.p, 0, 4, st));
+      for (int k = K - 1; k >= 0; k--) {
+        const u64 half = 1ull << k, step = half << 1;
+        LAUNCH(k_chain_level, (P.R + step - 1) / step, Jb + (u64)k * (n + 1), P.R, step, half, pos.as<u32>());
+      }
+      GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+      LAUNCH(k_chain_check, P.R, pos.as<u32>(), raw.as<u32>(), P.R, n, bad.as<u32>(), rstart.as<u32>());
+      u32 b = 0;
+      d2h(&b, bad.p, 1, st);
+      ok = b == 0;
+    }
+    if (ok) {
+      P.E = n - P.R;
+      P.Rp = P.R;
+      P.trailing = 0;
+    } else {
+      need_host_chain();  // malformed: reproduce the reference's error
+      if (P.trunc_rule >= 0) {
+        host_range_check(blob, P, (u64)P.trunc_rule);
+        char buf[96];
+        snprintf(buf, sizeof buf, P.trunc_what.c_str(), P.trunc_rule);
+        fail(GT_E_FORMAT, "truncated input while reading %s", buf);
+      }
+      if (P.trailing) {
+        host_range_check(blob, P, P.R);
+        fail(GT_E_FORMAT, "%lu trailing bytes after rules section", (unsigned long)P.trailing);
+      }
+    }
   }
-  if (P.trailing) {
-    GT_CUDA(cudaStreamSynchronize(st));
-    host_range_check(blob, P, P.R);
-    fail(GT_E_FORMAT, "%lu trailing bytes after rules section", (unsigned long)P.trailing);
-  }
+  ph.mark("rule chain (device)");
   const u64 R = P.R, E = P.E, nw = P.nw, ns = P.ns, base = nw + ns, limit = nw + ns + R;
   d->nw = nw;
   d->ns = ns;
@@ -702,14 +780,14 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   d->E = E;
   const u64 nraw = E + R;
 
-  // ---- upload + unpack --------------------------------------------------
-  DBuf rstart(R * 4, st), mark(nraw * 4 + 4, st), incl(nraw * 4 + 4, st);
+  // ---- unpack --------------------------------------------------------------
+  DBuf mark(nraw * 4 + 4, st), incl(nraw * 4 + 4, st);
   DBuf& owner = d->pos_owner;
   owner.alloc(E * 4 + 4, st);
   DBuf bad(4, st);
   d->body.alloc(E * 4 + 4, st);
   d->boff.alloc((R + 1) * 8, st);
-  GT_CUDA(cudaMemcpyAsync(rstart.p, P.rstart, R * 4, cudaMemcpyHostToDevice, st));
+  if (host_chain) GT_CUDA(cudaMemcpyAsync(rstart.p, P.rstart, R * 4, cudaMemcpyHostToDevice, st));
   LAUNCH(k_boff, R + 1, rstart.as<u32>(), R, E, d->boff.as<u64>());
   GT_CUDA(cudaMemsetAsync(mark.p, 0, nraw * 4, st));
   GT_CUDA(cudaMemsetAsync(bad.p, 0xFF, 4, st));
@@ -723,7 +801,10 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   rstart.release();
   u32 bad_rule;
   d2h(&bad_rule, bad.p, 1, st);
-  if (bad_rule != 0xFFFFFFFFu) host_range_check(blob, P, bad_rule + 1);
+  if (bad_rule != 0xFFFFFFFFu) {
+    need_host_chain();
+    host_range_check(blob, P, bad_rule + 1);
+  }
   ph.mark("upload+unpack");
 
   // ---- (rule, symbol) sort + RLE -> own / sub CSR ----------------------
@@ -870,7 +951,10 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     LAUNCH(k_root_cycle, 1, d->par_off.as<u64>(), d->par_ids.as<u32>(), reach.as<uint8_t>(), bad.as<u32>());
     u32 rb = 0;
     d2h(&rb, bad.p, 1, st);
-    if (processed + 1 < R || rb) cycle_message(blob, P);
+    if (processed + 1 < R || rb) {
+    need_host_chain();
+    cycle_message(blob, P);
+  }
   }
   GT_CUDA(cudaMemsetAsync(firstu.p, 0xFF, 4, st));
   LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, firstu.as<u32>());
@@ -949,7 +1033,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   ph.mark("level lists");
 
   // ---- root segments (dag.py:107-128) -------------------------------------
-  const u64 L0 = P.blen(0);
+  const u64 L0 = R ? rd32(blob + P.rules_pos) : 0;  // the root's body length
   d->L0 = L0;
   const bool headless = ns == 0;
   DBuf spl(L0 + 1, st), splu(L0 * 4 + 4, st), sincl(L0 * 4 + 4, st), spos(L0 * 4 + 4, st);
