@@ -146,6 +146,9 @@ struct DeviceDag {
 void build_device_dag(const uint8_t* blob, size_t n, int device, u64 file_lo, u64 file_hi,
                       DeviceDag* d);
 
+// bottom-up rule lists by level (built on first use)
+void ensure_bu_levels(DeviceDag* d);
+
 // cub_ops.cu (plumbing around CUB device-wide primitives)
 void sort_pairs_u64_u32(u64* keys_in, u64* keys_out, u32* vals_in, u32* vals_out, u64 n,
                         int end_bit, cudaStream_t s);

@@ -145,7 +145,18 @@ static void parse_dict(const uint8_t* d, size_t n, Parse* P) {
     u32 ln = rd32(d + pos);
     pos += 4;
     need(ln, "word %ld", (long)i);
-    if (!utf8_ok(d + pos, ln)) fail(GT_E_FORMAT, "word %ld is not valid UTF-8", (long)i);
+    // ASCII fast path (8 bytes at a time), full UTF-8 validation otherwise
+    const uint8_t* w = d + pos;
+    u64 hi = 0;
+    u32 k = 0;
+    for (; k + 8 <= ln; k += 8) {
+      u64 x;
+      memcpy(&x, w + k, 8);
+      hi |= x;
+    }
+    for (; k < ln; k++) hi |= w[k];
+    if ((hi & 0x8080808080808080ull) && !utf8_ok(w, ln))
+      fail(GT_E_FORMAT, "word %ld is not valid UTF-8", (long)i);
     pos += ln;
   }
   P->rules_pos = pos;
@@ -701,6 +712,13 @@ struct PinnedU32 {
 
 }  // namespace
 
+void ensure_bu_levels(DeviceDag* d) {
+  if (d->bu.order.p || d->R == 0) return;
+  GT_CUDA(cudaSetDevice(d->device));
+  const int nl = d->bu.nl;
+  build_levels(d, d->bu_level, d->sub_off, 16, nl, &d->bu);
+}
+
 void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_lo, u64 file_hi,
                       DeviceDag* d) {
   auto t0 = std::chrono::steady_clock::now();
@@ -1025,9 +1043,11 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     nbu = (int)h0;
     d->depth = (i64)h0 - 1;
   }
-  // level-ordered rule lists (light/heavy split)
-  build_levels(d, d->bu_level, d->sub_off, 16, nbu, &d->bu);
-  build_levels(d, d->td_level, d->par_off, 16, ntd, &d->td);
+  // level counts; the bottom-up rule lists (sequence tasks' head/tail pass)
+  // are built on first use (ensure_bu_levels), the top-down pass runs over
+  // the te edge lists and needs no rule lists
+  d->bu.nl = nbu;
+  d->td.nl = ntd;
   // the reference's bottom-up rounds exclude the root (engine.py:305-310)
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
   ph.mark("level lists");

@@ -315,6 +315,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   GT_CUDA(cudaMemsetAsync(hl.p, 0, R * 4, st));
   GT_CUDA(cudaMemsetAsync(tl.p, 0, R * 4, st));
   if (m) {
+    ensure_bu_levels(d);
     for (int L = 1; L <= d->bu.nl; L++) {
       u64 lo = d->bu.off[L], hi = d->bu.off[L + 1];
       if (hi > lo)
