@@ -19,6 +19,7 @@
 #include "gt_internal.cuh"
 #include "seq.cuh"
 #include "sparse.cuh"
+#include "bottomup.cuh"
 #include "word.cuh"
 
 namespace gt {
@@ -273,15 +274,23 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
       }
       case GT_WORDCOUNT:
       case GT_SORT: {
-        td_word_counts(&d, d.word_counts);
+        // a forced bottom-up runs Alg. 2 with the pooled hash tables; auto
+        // and top-down run Alg. 1 (engine.py:63-71 picks top-down here)
+        if (strat == GT_BOTTOMUP && strategy == GT_BOTTOMUP && bu_word_counts(&d, d.word_counts, scratch_budget(&d))) {
+          strat = GT_BOTTOMUP;
+        } else {
+          td_word_counts(&d, d.word_counts);
+          strat = GT_TOPDOWN;
+        }
         assemble_counts(&d, d.word_counts.as<u64>(), d.nw, 0, task == GT_SORT, &R);
-        strat = GT_TOPDOWN;
         break;
       }
       case GT_TERMVECTOR: {
         // the reference goes bottom-up for F > file_set_width; the device
         // equivalent is the presence-guided sparse per-file pass (sparse.cu)
-        if (strat == GT_BOTTOMUP || (u64)Fo * d.nw >= (1ull << 32)) {
+        if (strategy == GT_BOTTOMUP && bu_file_tables(&d, GT_TERMVECTOR, &R, scratch_budget(&d))) {
+          strat = GT_BOTTOMUP;
+        } else if (strat == GT_BOTTOMUP || (u64)Fo * d.nw >= (1ull << 32)) {
           sparse_term_vector(&d, &R);
           strat = GT_TOPDOWN_SPARSE;
         } else {
@@ -293,11 +302,15 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
         break;
       }
       case GT_INVERTEDINDEX: {
-        DBuf pres;
-        u32 FW;
-        td_file_presence(&d, pres, &FW);
-        assemble_presence(&d, pres.as<u64>(), FW, &R);
-        strat = GT_TOPDOWN;
+        if (strategy == GT_BOTTOMUP && bu_file_tables(&d, GT_INVERTEDINDEX, &R, scratch_budget(&d))) {
+          strat = GT_BOTTOMUP;
+        } else {
+          DBuf pres;
+          u32 FW;
+          td_file_presence(&d, pres, &FW);
+          assemble_presence(&d, pres.as<u64>(), FW, &R);
+          strat = GT_TOPDOWN;
+        }
         break;
       }
       default: {

@@ -25,6 +25,7 @@
 #include "kernels_common.cuh"
 #include "segreduce.cuh"
 #include "sparse.cuh"
+#include "bottomup.cuh"
 #include "word.cuh"
 
 namespace gt {
@@ -183,6 +184,32 @@ static void reduce_words(const DeviceDag* d, u32 C, const u64* row, u64* out, bo
     KL(k_root_words<Mode>, grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
        d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo),
        per_file ? 1 : 0, C, V, out);
+}
+
+void bu_root_words_dense(DeviceDag* d, u64* out) {
+  cudaStream_t st = d->stream;
+  if (d->n_rw)
+    KL(k_root_words<SumMode>, grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
+       d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), 0, 1u, d->nw, out);
+}
+
+void td_root_seeds(DeviceDag* d, u64* row) {
+  cudaStream_t st = d->stream;
+  GT_CUDA(cudaMemsetAsync(row, 0, sizeof(u64) * d->R, st));
+  if (d->n_rs)
+    KL(k_seed<SumMode>, grid_for(d->n_rs, 256), d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(),
+       d->n_rs, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), 0, 1u, row);
+}
+
+u64 scratch_budget(const DeviceDag* d) {
+  size_t free_b = 0, total_b = 0;
+  GT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  cudaMemPool_t pool;
+  GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, d->device));
+  u64 res = 0, used = 0;
+  GT_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res));
+  GT_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  return (u64)((double)(free_b + (res > used ? res - used : 0)) * 0.8);
 }
 
 // global word counts (corpus or owned shard) -> dense u64[V]

@@ -50,11 +50,13 @@ def test_composed_all_tasks_match_oracle(name, scale, seed):
     for task in TASKS:
         lens = (2, 3, 4) if task in ("seqcount", "rankedinvertedindex") else (3,)
         for l in lens:
-            for strategy in ("auto", "topdown"):
+            for strategy in ("auto", "topdown", "bottomup"):
                 cfg = gt.TraversalConfig(strategy=strategy)
                 got = gt.run_compact(dag, task, cfg, l)
                 exp = gt.run_compact(ref, task, gt.TraversalConfig(strategy="topdown"), l)
                 assert_same(got, exp, (name, scale, task, l, strategy))
+                if strategy == "bottomup" and task in ("wordcount", "sort", "invertedindex", "termvector"):
+                    assert got.strategy == "bottomup"  # the pooled hash-table path ran
     dag.close()
 
 
