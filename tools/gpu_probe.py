@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--tasks", default="wordcount,sort,invertedindex,termvector,seqcount,rankedinvertedindex")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--strategy", default="auto", choices=["auto", "topdown", "bottomup"])
     ap.add_argument("--pinned", action="store_true", help="open from a pinned host copy (as bench e2e)")
     a = ap.parse_args()
     import paper_2106_06889_b200 as gt
@@ -60,8 +61,8 @@ def main():
             try:
                 for rep in range(a.reps):
                     dag.profile(rep == a.reps - 1)
-                    r, v = dag.run_raw(gt._abi.TASK_IDS[task])
-                    line = (f"  {task:20s} device {v.device_ms:9.3f} ms  d2h {v.d2h_ms:8.3f} ms "
+                    r, v = dag.run_raw(gt._abi.TASK_IDS[task], 3, gt._abi.STRATEGY_IDS[a.strategy])
+                    line = (f"  {task:20s} [{gt._abi.STRATEGY_NAMES.get(v.strategy)}] device {v.device_ms:9.3f} ms  d2h {v.d2h_ms:8.3f} ms "
                             f"total {v.total_ms:9.3f} ms  n={v.n} groups={v.n_groups} "
                             f"launches={v.kernel_launches} W/s={dag.info['words'] / (v.device_ms / 1e3):.3e}")
                     dag.free_raw(r)
