@@ -224,8 +224,10 @@ __global__ void __launch_bounds__(256) k_segredG(const u32* __restrict__ dst,
 // sizes follow the DAG (a handful to 10^6 items), so the per-level work is
 // re-dealt over all resident warps/teams each time.
 // ---------------------------------------------------------------------------
+constexpr int kLevelBlock = 1024;  // one block per SM: the grid barrier spans 148 arrivals
+
 template <int G, class Mode, class Src, class Out>
-__global__ void __launch_bounds__(256) k_segred_levels(const u32* __restrict__ dst,
+__global__ void __launch_bounds__(kLevelBlock) k_segred_levels(const u32* __restrict__ dst,
                                                        const u32* __restrict__ src,
                                                        const u32* __restrict__ freq,
                                                        const u64* __restrict__ lvl_off, int L0, int L1,
@@ -302,13 +304,13 @@ void seg_reduce_levels_G(const char* name, const u32* dst, const u32* src, const
   auto kern = k_segred_levels<G, Mode, Src, Out>;
   static int per_sm = -1;  // per instantiation
   if (per_sm < 0) {
-    GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLevelBlock, 0));
     if (per_sm < 1) per_sm = 1;
   }
   int dev = 0, nsm = 148;
   GT_CUDA(cudaGetDevice(&dev));
   GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  dim3 grid((unsigned)(nsm * per_sm)), block(256);
+  dim3 grid((unsigned)(nsm * per_sm)), block(kLevelBlock);
   void* args[] = {(void*)&dst, (void*)&src, (void*)&freq, (void*)&lvl_off_dev, (void*)&L0, (void*)&L1,
                   (void*)&reverse, (void*)&C, (void*)&in, (void*)&out};
   ProfScope ps(name, st);

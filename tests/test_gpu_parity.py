@@ -95,3 +95,71 @@ def test_c2_full_sequence_properties():
     assert int(rii.count.sum()) == int(sc.count.sum())
     assert rii.n == sc.n
     dag.close()
+
+
+def _check_properties(gt, dag, W, tasks, l=3):
+    """Size-independent properties of the six outputs (SURVEY §8 edge-case
+    contract + test_acceptance criteria): weight conservation, per-file
+    totals, ordering, and cross-task consistency."""
+    toks = dag.dag_array("segment_token_counts")
+    F = len(toks)
+    cfg = gt.TraversalConfig()
+    out = {}
+    if "wordcount" in tasks or "sort" in tasks:
+        wc = gt.run_compact(dag, "wordcount", cfg)
+        assert int(wc.count.sum()) == W and np.all(wc.count > 0) and np.all(np.diff(wc.id) > 0)
+        srt = gt.run_compact(dag, "sort", cfg)
+        assert srt.n == wc.n and int(srt.count.sum()) == W
+        assert np.all((np.diff(srt.count) < 0) | ((np.diff(srt.count) == 0) & (np.diff(srt.id) > 0)))
+        out["wc"] = wc
+    if "termvector" in tasks:
+        tv = gt.run_compact(dag, "termvector", cfg)
+        off = tv.group_off
+        assert tv.n_groups == F and off[-1] == tv.n
+        per_file = np.add.reduceat(tv.count, off[:-1]) if tv.n else np.zeros(F, np.int64)
+        per_file = np.where(np.diff(off) > 0, per_file, 0)
+        assert np.array_equal(per_file, toks)
+        fid = np.repeat(np.arange(F), np.diff(off))
+        same_file = fid[1:] == fid[:-1]
+        dc, di = np.diff(tv.count), np.diff(tv.id)
+        assert np.all(~same_file | (dc < 0) | ((dc == 0) & (di > 0)))
+        out["tv"] = tv
+        if "wc" in out:
+            dense = np.zeros(dag.info["num_words"], np.int64)
+            np.add.at(dense, tv.id, tv.count)
+            assert np.array_equal(np.flatnonzero(dense), out["wc"].id)
+    if "invertedindex" in tasks:
+        ii = gt.run_compact(dag, "invertedindex", cfg)
+        assert np.all(np.diff(ii.group_id) > 0)
+        gidx = np.repeat(np.arange(ii.n_groups), np.diff(ii.group_off))
+        assert np.all((gidx[1:] != gidx[:-1]) | (np.diff(ii.id) > 0))
+        if "tv" in out:  # the same (word, file) cells as the term vector
+            tv = out["tv"]
+            a = np.sort(np.repeat(np.arange(F), np.diff(tv.group_off)).astype(np.int64) * (1 << 32) + tv.id)
+            b = np.sort(ii.id.astype(np.int64) * (1 << 32) + np.repeat(ii.group_id, np.diff(ii.group_off)))
+            assert np.array_equal(a, b)
+    if "seqcount" in tasks:
+        sc = gt.run_compact(dag, "seqcount", cfg, l)
+        off = sc.group_off
+        per_file = np.add.reduceat(sc.count, off[:-1]) if sc.n else np.zeros(F, np.int64)
+        per_file = np.where(np.diff(off) > 0, per_file, 0)
+        assert np.array_equal(per_file, np.maximum(toks - (l - 1), 0))
+        rii = gt.run_compact(dag, "rankedinvertedindex", cfg, l)
+        assert rii.n == sc.n and int(rii.count.sum()) == int(sc.count.sum())
+
+
+@pytest.mark.parametrize("name,tasks", [
+    ("c3", ("wordcount", "sort", "invertedindex", "termvector", "seqcount")),
+    ("c4", ("wordcount", "invertedindex", "termvector", "seqcount")),
+    ("c5", ("wordcount", "sort", "invertedindex", "seqcount")),
+])
+def test_full_size_properties(name, tasks):
+    """BASELINE configs 2-4 at full size on the device (the oracle cannot
+    hold them): properties that do not depend on an oracle."""
+    import paper_2106_06889_b200 as gt
+    blob, stats = composed(name, 1.0)
+    dag = gt.DeviceDag(blob)
+    try:
+        _check_properties(gt, dag, stats["W"], tasks)
+    finally:
+        dag.close()
