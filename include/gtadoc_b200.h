@@ -189,6 +189,21 @@ int gt_flush_l2(gt_ctx* ctx);
 /* Synchronize the context's stream. */
 int gt_sync(gt_ctx* ctx);
 
+/* ---- native rendering (host only; works without a GPU) -------------------
+ * Byte-identical to tasks.py:233-263 render(); the SHA-256 of the rendering
+ * is the reference CLI manifest's outputDigest (cli.py:121-133).  A gt_dict
+ * holds the word strings of a GTDC blob (grammar.py:193-228 layout). */
+typedef struct gt_dict gt_dict;
+int gt_dict_open(const uint8_t* gtdc, size_t nbytes, gt_dict** out);
+void gt_dict_close(gt_dict* dict);
+/* render a result view (gt_result_view, or arrays built by the caller);
+ * *text is malloc'd, NUL-terminated, released with gt_free_text */
+int gt_render_view(const gt_dict* dict, const gt_view* view, char** text, uint64_t* len);
+void gt_free_text(char* text);
+/* SHA-256 of the rendering without materialising it; *len = its byte count */
+int gt_digest_view(const gt_dict* dict, const gt_view* view, uint8_t sha256[32], uint64_t* len);
+int gt_sha256(const void* data, uint64_t nbytes, uint8_t out[32]);
+
 #ifdef __cplusplus
 }
 #endif

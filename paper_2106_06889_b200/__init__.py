@@ -11,8 +11,9 @@ from .errors import (CorruptionError, DivergenceError, FormatError, GtadocError,
                      IngestError, ResourceError, UsageError)
 from .tasks import (TASK_NAMES, InvertedIndex, RankedInvertedIndex, SequenceCounts,
                     SortedWords, TermVectors, TraversalConfig, WordCounts, first_divergence,
-                    inverted_index, ranked_inverted_index, render, run_compact, run_task,
-                    sequence_count, sort_by_frequency, term_vector, word_count)
+                    inverted_index, output_digest, ranked_inverted_index, render, render_native,
+                    run_compact, run_task, sequence_count, sort_by_frequency, term_vector,
+                    word_count)
 
 __version__ = "0.1.0"
 
@@ -22,5 +23,5 @@ __all__ = [
     "sequence_count", "ranked_inverted_index", "WordCounts", "SortedWords", "InvertedIndex",
     "TermVectors", "SequenceCounts", "RankedInvertedIndex", "TASK_NAMES", "GtadocError",
     "UsageError", "IngestError", "ResourceError", "FormatError", "CorruptionError",
-    "DivergenceError",
+    "DivergenceError", "output_digest", "render_native",
 ]

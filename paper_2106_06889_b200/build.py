@@ -29,7 +29,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-re
 
 
 def _sources():
-    return sorted(CSRC.glob("*.cu"))
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def _digest() -> str:
@@ -47,14 +47,14 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     dig = _digest()
     if LIB.exists() and stamp.exists() and stamp.read_text() == dig and not force:
         return LIB
-    hdrs = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "gtadoc_b200.h"]
+    hdrs = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "gtadoc_b200.h"]
     hdr_time = max(p.stat().st_mtime for p in hdrs)
 
     def compile_one(src: Path) -> Path:
         obj = OBJ / (src.stem + ".o")
         if obj.exists() and obj.stat().st_mtime > max(src.stat().st_mtime, hdr_time) and not force:
             return obj
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *FLAGS, "-Xcompiler", "-pthread", "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
@@ -64,7 +64,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(compile_one, _sources()))
     tmp = LIB.with_suffix(".so.tmp")
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"],
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart", "-lpthread"],
                    check=True)
     tmp.replace(LIB)
     stamp.write_text(dig)

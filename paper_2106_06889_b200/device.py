@@ -24,7 +24,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libgtadoc_b200.so"
 EXPORTS = ("gt_abi_version", "gt_last_error", "gt_open", "gt_info_get", "gt_run",
            "gt_result_view", "gt_result_free", "gt_close", "gt_device_word_counts",
            "gt_dag_array", "gt_flush_l2", "gt_sync", "gt_profile", "gt_profile_report",
-           "gt_set_files", "gt_assemble_counts")
+           "gt_set_files", "gt_assemble_counts", "gt_dict_open", "gt_dict_close", "gt_render_view",
+           "gt_free_text", "gt_digest_view", "gt_sha256")
 _lib = None
 
 
@@ -56,6 +57,13 @@ def lib():
         L.gt_profile_report.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
         L.gt_profile_report.restype = C.c_int64
         L.gt_set_files.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+        L.gt_dict_open.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]
+        L.gt_dict_close.argtypes = [C.c_void_p]
+        L.gt_render_view.argtypes = [C.c_void_p, C.POINTER(GtView), C.POINTER(C.c_void_p),
+                                     C.POINTER(C.c_uint64)]
+        L.gt_free_text.argtypes = [C.c_void_p]
+        L.gt_digest_view.argtypes = [C.c_void_p, C.POINTER(GtView), C.c_char_p, C.POINTER(C.c_uint64)]
+        L.gt_sha256.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p]
         L.gt_assemble_counts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
         _lib = L
     return _lib

@@ -84,6 +84,22 @@ def run_compact(dag, task: str, cfg: TraversalConfig | None = None,
     return dag.run(TASK_IDS[task], seq_len, STRATEGY_IDS[cfg.strategy], cfg.file_set_width)
 
 
+def output_digest(dag, task: str, cfg: TraversalConfig | None = None,
+                  seq_len: int = DEFAULT_SEQ_LEN) -> tuple[str, int]:
+    """sha256 hex + byte length of `render(run_task(...))` — the reference
+    CLI manifest's outputDigest (cli.py:121-133) — rendered natively
+    (render.cpp) without building the Python containers or the text."""
+    from .native import NativeDict
+    return NativeDict(dag.grammar.blob).digest(run_compact(dag, task, cfg, seq_len))
+
+
+def render_native(dag, task: str, cfg: TraversalConfig | None = None,
+                  seq_len: int = DEFAULT_SEQ_LEN) -> str:
+    """`render(run_task(...), dag.grammar.dictionary)`, rendered natively."""
+    from .native import NativeDict
+    return NativeDict(dag.grammar.blob).render(run_compact(dag, task, cfg, seq_len))
+
+
 def word_count(dag, cfg: TraversalConfig) -> WordCounts:
     return to_container(run_compact(dag, "wordcount", cfg))
 
