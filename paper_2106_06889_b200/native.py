@@ -63,7 +63,8 @@ class NativeDict:
         p, n = C.c_void_p(), C.c_uint64()
         raise_for_status(lib().gt_render_view(self._h, C.byref(v), C.byref(p), C.byref(n)), "render failed")
         try:
-            return C.string_at(p, n.value).decode("utf-8")
+            # (ctypes.string_at takes a C int size: > 2 GiB outputs need a view)
+            return bytes((C.c_char * n.value).from_address(p.value)).decode("utf-8") if n.value else ""
         finally:
             lib().gt_free_text(p)
 
