@@ -189,9 +189,9 @@ def run_reference(args, rank):
     line = {
         "metric": METRIC, "value": W / t, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic (composed Zipfian grammar, seed 2)",
-        "config": {"workload": f"{args.config}: word count + inverted index", "scale": args.scale,
+        "config": {"workload": f"{args.config}: word count + inverted index per step", "scale": args.scale,
                    "R": info["num_rules"], "E": info["total_elements"], "W": W,
                    "F": info["num_files"], "V": info["num_words"], "depth": info["depth"],
                    "rho": W / max(1, info["total_elements"])},

@@ -269,11 +269,16 @@ __global__ void k_jump_double(const u32* __restrict__ Jk, u64 n, u32* __restrict
   for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += stride) Jk1[j] = Jk[Jk[j]];
 }
 
-// rule starts i = t*step (known) -> i + half
-__global__ void k_chain_level(const u32* __restrict__ Jk, u64 R, u64 step, u64 half, u32* pos) {
+// start of rule i = J applied along the binary digits of i to p_0 = 0 (one
+// thread per rule, K dependent table lookups)
+__global__ void k_chain_pos(const u32* __restrict__ J, u64 n, int K, u64 R, u32* pos) {
   u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t * step + half < R; t += stride)
-    pos[t * step + half] = Jk[pos[t * step]];
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += stride) {
+    u32 p = 0;
+    for (int k = K - 1; k >= 0; k--)
+      if ((i >> k) & 1) p = J[(u64)k * (n + 1) + p];
+    pos[i] = p;
+  }
 }
 
 // every rule start inside the section, the last record ending exactly at the
@@ -474,12 +479,30 @@ __global__ void __launch_bounds__(256) k_kahn(KahnCtl* ctl, u32* q0, u32* q1, co
           len = 0;
         }
       }
-      u64 mx = len;
+      // the warp's light edges dealt round-robin over its lanes: exclusive
+      // scan of the per-lane counts, then lane j takes edge k*32 + j and finds
+      // its owning lane by a shuffle binary search (no lane walks a long list)
+      u32 inc = (u32)len;
 #pragma unroll
-      for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, d));
-      for (u64 k = 0; k < mx; k++) {
-        const bool a = k < len;
-        const u32 c = a ? ids[e0 + k] : 0u;
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= (unsigned)d) inc += t;
+      }
+      const u32 excl = inc - (u32)len;
+      const u32 tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
+      for (u32 k0 = 0; k0 < tot; k0 += 32) {
+        const u32 q = k0 + lane;
+        // owner = last lane whose exclusive start <= q
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+          const u32 st_ex = __shfl_sync(0xFFFFFFFFu, excl, lo + step);
+          if (st_ex <= q) lo += step;
+        }
+        const u32 own_start = __shfl_sync(0xFFFFFFFFu, excl, lo);
+        const u64 own_e0 = __shfl_sync(0xFFFFFFFFu, e0, lo);
+        const bool a = q < tot;
+        const u32 c = a ? ids[own_e0 + (q - own_start)] : 0u;
         warp_append(dec_to_zero(rem, c, a), c, nxt, ncnt);
       }
     }
@@ -724,8 +747,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   auto t0 = std::chrono::steady_clock::now();
   Phases ph("gt_open");
   Parse P;
-  parse_dict(blob, nbytes, &P);
-  ph.mark("host parse: dictionary");
+  if (nbytes < 4 || memcmp(blob, "GTDC", 4) != 0) fail(GT_E_FORMAT, "bad magic: not a GTDC file");
   GT_CUDA(cudaSetDevice(device));
   d->device = device;
   if (!d->stream) GT_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
@@ -733,11 +755,17 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   ph.st = st;
   reserve_pool(device, st);
   ph.mark("stream");
-  // start the upload of the whole rules section, then walk the length chain
-  // on the host while it is in flight (overlaps when `blob` is pinned)
+  // the whole blob streams to the device while the host validates the
+  // header and dictionary (overlaps when `blob` is pinned); the rules section
+  // is then re-aligned on the device (the dictionary has byte lengths)
+  DBuf dblob(nbytes + 4, st);
+  GT_CUDA(cudaMemcpyAsync(dblob.p, blob, nbytes, cudaMemcpyHostToDevice, st));
+  parse_dict(blob, nbytes, &P);
+  ph.mark("host parse: dictionary");
   const u64 nsec = (nbytes - P.rules_pos) / 4;
   DBuf raw(nsec * 4 + 4, st);
-  if (nsec) GT_CUDA(cudaMemcpyAsync(raw.p, blob + P.rules_pos, nsec * 4, cudaMemcpyHostToDevice, st));
+  if (nsec) GT_CUDA(cudaMemcpyAsync(raw.p, dblob.as<uint8_t>() + P.rules_pos, nsec * 4, cudaMemcpyDeviceToDevice, st));
+  dblob.release();
   // the rule-start table: on the device by pointer doubling; the host walk
   // (parse_rules, the reference's sequential reader) runs only to produce the
   // exact error of a malformed section, or when an error path needs it
@@ -761,11 +789,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
       LAUNCH(k_jump0, n + 1, raw.as<u32>(), n, Jb);
       for (int k = 1; k < K; k++)
         LAUNCH(k_jump_double, n + 1, Jb + (u64)(k - 1) * (n + 1), n, Jb + (u64)k * (n + 1));
-      GT_CUDA(cudaMemsetAsync(pos.p, 0, 4, st));
-      for (int k = K - 1; k >= 0; k--) {
-        const u64 half = 1ull << k, step = half << 1;
-        LAUNCH(k_chain_level, (P.R + step - 1) / step, Jb + (u64)k * (n + 1), P.R, step, half, pos.as<u32>());
-      }
+      LAUNCH(k_chain_pos, P.R, Jb, n, K, P.R, pos.as<u32>());
       GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
       LAUNCH(k_chain_check, P.R, pos.as<u32>(), raw.as<u32>(), P.R, n, bad.as<u32>(), rstart.as<u32>());
       u32 b = 0;
