@@ -428,8 +428,10 @@ __device__ __forceinline__ u64 ld_cg64(const u64* p) {
   return (u64)__ldcg(reinterpret_cast<const unsigned long long*>(p));
 }
 
+constexpr int kKahnBlock = 1024;  // few, large blocks: cheaper grid barriers
+
 template <bool TD>
-__global__ void __launch_bounds__(256) k_kahn(KahnCtl* ctl, u32* q0, u32* q1, const u64* __restrict__ off,
+__global__ void __launch_bounds__(kKahnBlock) k_kahn(KahnCtl* ctl, u32* q0, u32* q1, const u64* __restrict__ off,
                                               const u32* __restrict__ ids, u32* rem, u32* lvl,
                                               const u64* __restrict__ par_off,
                                               const u32* __restrict__ par_ids,
@@ -507,8 +509,10 @@ __global__ void __launch_bounds__(256) k_kahn(KahnCtl* ctl, u32* q0, u32* q1, co
       }
     }
     grid.sync();
-    // phase B: chunk tasks, one warp per task
+    // phase B: chunk tasks, one warp per task (most top-down layers have none:
+    // then the second barrier is skipped, uniformly across the grid)
     const u64 nt = ld_cg64(ntask);
+    if (nt == 0) continue;
     for (u64 t = gtid >> 5; t < nt; t += nthreads >> 5) {
       const uint2 tk = __ldcg(tasks + t);
       const u64 a = off[tk.x] + tk.y, b = min(off[tk.x + 1], a + kChunk);
@@ -951,7 +955,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     static int per_sm[2] = {-1, -1};
     int& ps = per_sm[td ? 1 : 0];
     if (ps < 0) {
-      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, 256, 0));
+      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, kKahnBlock, 0));
       ps = std::max(ps, 1);
     }
     int nsm = 148;
@@ -972,7 +976,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
                     (void*)&po, (void*)&pi, (void*)&rp, (void*)&rc, (void*)&tk, (void*)&maxl};
     {
       ProfScope ps_(td ? "k_kahn<td>" : "k_kahn<bu>", st);
-      GT_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)(nsm * ps)), dim3(256), args, 0, st));
+      GT_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)(nsm * ps)), dim3(kKahnBlock), args, 0, st));
       g_launches++;
     }
     KahnCtl h;
