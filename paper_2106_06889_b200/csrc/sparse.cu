@@ -102,6 +102,28 @@ __global__ void k_expand_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u
   }
 }
 
+// FW == 1 (at most 64 files): one thread per row
+__global__ void k_popc_rows1(const u64* __restrict__ bits, u64 nrows, u64 rs_row, u64* __restrict__ cnt) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += stride)
+    cnt[r] = __popcll(bits[r * rs_row]);
+}
+
+__global__ void k_expand_rows1(const u64* __restrict__ bits, u64 nrows, u64 rs_row, const u64* __restrict__ off,
+                               u32 col_base, u32* __restrict__ col, u32* __restrict__ row_of) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += stride) {
+    u64 b = bits[r * rs_row], q = off[r];
+    while (b) {
+      const int t = __ffsll((long long)b) - 1;
+      col[q] = col_base + (u32)t;
+      if (row_of) row_of[q] = (u32)r;
+      q++;
+      b &= b - 1;
+    }
+  }
+}
+
 // root seeds: w(rule, seg) += cnt for owned segments
 __global__ void k_sparse_seed(const u32* __restrict__ rs_rule, const u32* __restrict__ rs_seg,
                               const u32* __restrict__ rs_cnt, u64 n, u32 file_lo, u32 nseg,
@@ -256,18 +278,34 @@ T d2h1(const void* p, cudaStream_t st) {
 }  // namespace
 
 // rows of bitsets -> CSR (off, col[, row_of]); returns the pair count
-u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& col,
-                DBuf* row_of, cudaStream_t st, u32 col_base, DBuf* row_cnt) {
-  DBuf cnt(nrows * 8 + 8, st);
+void bits_count(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& cnt,
+                cudaStream_t st) {
+  cnt.alloc(nrows * 8 + 8, st);
   off.alloc((nrows + 1) * 8, st);
-  SKW(k_popc_rows, nrows, bits, nrows, FW, rs_row, rs_col, cnt.as<u64>());
+  if (FW == 1) SK(k_popc_rows1, nrows, bits, nrows, rs_row, cnt.as<u64>());
+  else SKW(k_popc_rows, nrows, bits, nrows, FW, rs_row, rs_col, cnt.as<u64>());
   GT_CUDA(cudaMemsetAsync(cnt.as<u64>() + nrows, 0, 8, st));
   exclusive_scan_u64(cnt.as<u64>(), off.as<u64>(), nrows + 1, st);
-  const u64 P = d2h1<u64>(off.as<u64>() + nrows, st);
+}
+
+void bits_expand(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, const DBuf& off, u64 P,
+                 DBuf& col, DBuf* row_of, cudaStream_t st, u32 col_base) {
   col.alloc(P * 4 + 4, st);
   if (row_of) row_of->alloc(P * 4 + 4, st);
-  SKW(k_expand_rows, nrows, bits, nrows, FW, rs_row, rs_col, off.as<u64>(), col_base, col.as<u32>(),
-      row_of ? row_of->as<u32>() : (u32*)nullptr);
+  if (FW == 1)
+    SK(k_expand_rows1, nrows, bits, nrows, rs_row, off.as<u64>(), col_base, col.as<u32>(),
+       row_of ? row_of->as<u32>() : (u32*)nullptr);
+  else
+    SKW(k_expand_rows, nrows, bits, nrows, FW, rs_row, rs_col, off.as<u64>(), col_base, col.as<u32>(),
+        row_of ? row_of->as<u32>() : (u32*)nullptr);
+}
+
+u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& col,
+                DBuf* row_of, cudaStream_t st, u32 col_base, DBuf* row_cnt) {
+  DBuf cnt;
+  bits_count(bits, nrows, FW, rs_row, rs_col, off, cnt, st);
+  const u64 P = d2h1<u64>(off.as<u64>() + nrows, st);
+  bits_expand(bits, nrows, FW, rs_row, rs_col, off, P, col, row_of, st, col_base);
   if (row_cnt) *row_cnt = std::move(cnt);
   return P;
 }

@@ -19,6 +19,13 @@ struct SparseW {
 u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& col,
                 DBuf* row_of, cudaStream_t st, u32 col_base = 0, DBuf* row_cnt = nullptr);
 
+// the two halves of bits_to_csr (count + scan, then expansion once the
+// caller knows P = off[nrows]) for callers that batch their host syncs
+void bits_count(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& cnt,
+                cudaStream_t st);
+void bits_expand(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, const DBuf& off, u64 P,
+                 DBuf& col, DBuf* row_of, cudaStream_t st, u32 col_base = 0);
+
 // presence pass + pairs + weights; optionally hands back the word presence
 // bitsets u64[FW][V] of the same pass
 void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW);

@@ -298,13 +298,17 @@ void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R) {
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
   DBuf off, files, pc;
-  const u64 n = bits_to_csr(pres, V, FW, 1, V, off, files, nullptr, st, (u32)d->file_lo, &pc);
-  DBuf nz(V + 1, st), words(V * 4 + 4, st), cnt(8, st);
+  bits_count(pres, V, FW, 1, V, off, pc, st);
+  DBuf nz(V + 1, st), words(V * 4 + 4, st), cnt(16, st);
   KL(k_nz_u64, grid_for(V, 256), pc.as<u64>(), V, nz.as<uint8_t>());
   select_flagged_index(nz.as<uint8_t>(), words.as<u32>(), cnt.as<u64>(), V, st);
-  u64 ng = 0;
-  GT_CUDA(cudaMemcpyAsync(&ng, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+  // one host round trip for both sizes: records n and groups ng
+  GT_CUDA(cudaMemcpyAsync(cnt.as<u64>() + 1, off.as<u64>() + V, 8, cudaMemcpyDeviceToDevice, st));
+  u64 h[2] = {0, 0};
+  GT_CUDA(cudaMemcpyAsync(h, cnt.p, 16, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
+  const u64 ng = h[0], n = h[1];
+  bits_expand(pres, V, FW, 1, V, off, n, files, nullptr, st, (u32)d->file_lo);
   R->n = n;
   R->n_groups = ng;
   R->group_id.alloc(ng * 4 + 4, st);
