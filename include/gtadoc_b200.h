@@ -184,6 +184,15 @@ int64_t gt_dag_array(gt_ctx* ctx, const char* name, int64_t* out, int64_t cap);
 int gt_profile(gt_ctx* ctx, int enable);
 int64_t gt_profile_report(gt_ctx* ctx, char* buf, size_t cap);
 
+/* Test hook of the pooled hash tables' insert path (bottomup.cu), the
+ * analogue of the reference's add_batch stress kernel (_kernels.py:117-126,
+ * pkg/tests/test_table.py:145-164): n concurrent (key, delta) inserts into
+ * one open-addressing table of `capacity` (power of two) slots on `device`;
+ * copies back the slot arrays (empty key = 0xFFFFFFFF).  GT_E_RESOURCE when
+ * the table overflowed (the reference's FULL status). */
+int gt_table_add_batch(int device, const uint32_t* keys, const uint64_t* deltas, uint64_t n,
+                       uint32_t capacity, uint32_t* out_keys, uint64_t* out_counts);
+
 /* Evict L2 (writes a buffer larger than L2 on the context's stream). */
 int gt_flush_l2(gt_ctx* ctx);
 /* Synchronize the context's stream. */

@@ -363,6 +363,14 @@ int gt_assemble_counts(gt_ctx* c, int task, const uint64_t* dev_counts, gt_resul
   return GT_OK;
 }
 
+int gt_table_add_batch(int device, const uint32_t* keys, const uint64_t* deltas, uint64_t n, uint32_t capacity,
+                       uint32_t* out_keys, uint64_t* out_counts) {
+  int rc = GT_OK;
+  int st = guard([&] { rc = table_add_batch(device, keys, deltas, n, capacity, out_keys, out_counts); });
+  if (st == GT_OK && rc != GT_OK) set_last_error("table full");
+  return st != GT_OK ? st : rc;
+}
+
 int gt_result_view(const gt_result* r, gt_view* out) {
   *out = r->v;
   return GT_OK;

@@ -412,7 +412,54 @@ bool build_rule_tables(DeviceDag* d, RuleTables* T, u64 budget) {
   return true;
 }
 
+__global__ void k_table_batch(const u32* keys_in, const u64* deltas, u64 n, u32* keys, u64* vals, const u64* toff,
+                              const u32* tcap, u32* full) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const u64 i = base + threadIdx.x;
+    const bool a = i < n;
+    ht_add_warp(keys, vals, toff, tcap, 0, a ? keys_in[i] : 0, a ? deltas[i] : 0, a, full);
+  }
+}
+
 }  // namespace
+
+// add_batch (_kernels.py:117-126, the reference's table stress kernel): n
+// (key, delta) inserts from all warps concurrently into one table of `cap`
+// slots; returns the occupied (key, count) slots.  Test hook for the pooled
+// tables' insert path.
+int table_add_batch(int device, const u32* h_keys, const u64* h_deltas, u64 n, u32 cap, u32* h_out_keys,
+                    u64* h_out_vals) {
+  if (cap == 0 || (cap & (cap - 1))) fail(GT_E_USAGE, "table capacity must be a power of two");
+  GT_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  GT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  u32 full_h = 0;
+  {
+    DBuf k(n * 4 + 4, st), dl(n * 8 + 8, st), keys((u64)cap * 4, st), vals((u64)cap * 8, st), toff(16, st),
+        tcap(8, st), full(4, st);
+    if (n) {
+      GT_CUDA(cudaMemcpyAsync(k.p, h_keys, n * 4, cudaMemcpyHostToDevice, st));
+      GT_CUDA(cudaMemcpyAsync(dl.p, h_deltas, n * 8, cudaMemcpyHostToDevice, st));
+    }
+    const u64 toff_h[2] = {0, cap};
+    GT_CUDA(cudaMemcpyAsync(toff.p, toff_h, 16, cudaMemcpyHostToDevice, st));
+    GT_CUDA(cudaMemcpyAsync(tcap.p, &cap, 4, cudaMemcpyHostToDevice, st));
+    GT_CUDA(cudaMemsetAsync(keys.p, 0xFF, (u64)cap * 4, st));
+    GT_CUDA(cudaMemsetAsync(vals.p, 0, (u64)cap * 8, st));
+    GT_CUDA(cudaMemsetAsync(full.p, 0, 4, st));
+    if (n)
+      GT_KLAUNCH("k_table_batch", k_table_batch, grid_for(n, 256), 256, st, k.as<u32>(), dl.as<u64>(), n,
+                 keys.as<u32>(), vals.as<u64>(), toff.as<u64>(), tcap.as<u32>(), full.as<u32>());
+    GT_CUDA(cudaMemcpyAsync(h_out_keys, keys.p, (u64)cap * 4, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaMemcpyAsync(h_out_vals, vals.p, (u64)cap * 8, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaMemcpyAsync(&full_h, full.p, 4, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return full_h ? GT_E_RESOURCE : GT_OK;
+}
 
 bool bu_word_counts(DeviceDag* d, DBuf& counts, u64 budget) {
   cudaStream_t st = d->stream;

@@ -17,6 +17,10 @@ bool bu_file_tables(DeviceDag* d, int task, DevRecords* R, u64 budget);
 void bu_root_words_dense(DeviceDag* d, u64* out);
 void td_root_seeds(DeviceDag* d, u64* row);
 
+// add_batch test hook (see gt_table_add_batch)
+int table_add_batch(int device, const u32* keys, const u64* deltas, u64 n, u32 cap, u32* out_keys,
+                    u64* out_vals);
+
 // device bytes the task paths may use (free device memory + unused pool)
 u64 scratch_budget(const DeviceDag* d);
 

@@ -25,7 +25,7 @@ EXPORTS = ("gt_abi_version", "gt_last_error", "gt_open", "gt_info_get", "gt_run"
            "gt_result_view", "gt_result_free", "gt_close", "gt_device_word_counts",
            "gt_dag_array", "gt_flush_l2", "gt_sync", "gt_profile", "gt_profile_report",
            "gt_set_files", "gt_assemble_counts", "gt_dict_open", "gt_dict_close", "gt_render_view",
-           "gt_free_text", "gt_digest_view", "gt_sha256")
+           "gt_free_text", "gt_digest_view", "gt_sha256", "gt_table_add_batch")
 _lib = None
 
 
@@ -64,6 +64,8 @@ def lib():
         L.gt_free_text.argtypes = [C.c_void_p]
         L.gt_digest_view.argtypes = [C.c_void_p, C.POINTER(GtView), C.c_char_p, C.POINTER(C.c_uint64)]
         L.gt_sha256.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p]
+        L.gt_table_add_batch.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
+                                         C.c_void_p, C.c_void_p]
         L.gt_assemble_counts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
         _lib = L
     return _lib
@@ -209,6 +211,20 @@ def profile_report(handle=None) -> dict:
         name, cnt, ms = line.split("\t")
         out[name] = (int(cnt), float(ms))
     return out
+
+
+def table_add_batch(keys, deltas, capacity: int, device: int = 0):
+    """gt_table_add_batch: concurrent inserts into one device hash table;
+    returns {key: count} of the occupied slots (raises ResourceError when full)."""
+    k = np.ascontiguousarray(keys, dtype=np.uint32)
+    dl = np.ascontiguousarray(deltas, dtype=np.uint64)
+    ok = np.empty(capacity, dtype=np.uint32)
+    ov = np.empty(capacity, dtype=np.uint64)
+    st = lib().gt_table_add_batch(device, k.ctypes.data, dl.ctypes.data, len(k), capacity,
+                                  ok.ctypes.data, ov.ctypes.data)
+    raise_for_status(st, _err())
+    occ = ok != 0xFFFFFFFF
+    return dict(zip(ok[occ].tolist(), ov[occ].tolist())), ok, ov
 
 
 def build_dag(source, device: int = 0) -> DeviceDag:
