@@ -23,7 +23,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
+#include <initializer_list>
 #include <memory>
+#include <thread>
 
 #include "kernels_common.cuh"
 #include "segreduce.cuh"
@@ -722,6 +725,11 @@ static void reserve_pool(int device, cudaStream_t st) {
   }
 }
 
+// buffers allocated on a helper stream are released on the context stream
+static void rebind_stream(cudaStream_t st, std::initializer_list<DBuf*> bufs) {
+  for (DBuf* b : bufs) b->s = st;
+}
+
 // grow-only pinned host buffer (the rule-start table of the chain walk)
 struct PinnedU32 {
   u32* p = nullptr;
@@ -853,6 +861,128 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   }
   ph.mark("upload+unpack");
 
+  // ---- root side (splitters, segments, root occurrence lists): only needs
+  // the root body, so it runs on its own stream and host thread while the
+  // main pipeline builds the CSR, the layering and the level lists; its
+  // errors are raised after the main pipeline's, in the reference's order
+  // (dag.py:131-230: cycle, unreachable, then _segments_of_root)
+  const u64 L0 = R ? rd32(blob + P.rules_pos) : 0;  // the root's body length
+  d->L0 = L0;
+  cudaEvent_t ev_body;
+  GT_CUDA(cudaEventCreateWithFlags(&ev_body, cudaEventDisableTiming));
+  GT_CUDA(cudaEventRecord(ev_body, st));
+  Error root_err{GT_OK, ""};
+  cudaStream_t s_root = nullptr;
+  GT_CUDA(cudaStreamCreateWithFlags(&s_root, cudaStreamNonBlocking));
+  auto root_side = [&]() {
+    try {
+      GT_CUDA(cudaSetDevice(device));
+      cudaStream_t st = s_root;
+      GT_CUDA(cudaStreamWaitEvent(st, ev_body, 0));
+      DBuf cnt(16, st);
+  // ---- root segments (dag.py:107-128) -------------------------------------
+    const bool headless = ns == 0;
+    DBuf spl(L0 + 1, st), splu(L0 * 4 + 4, st), sincl(L0 * 4 + 4, st), spos(L0 * 4 + 4, st);
+    LAUNCH(k_root_flags, L0, d->body.as<u32>(), L0, nw, base, spl.as<uint8_t>(), splu.as<u32>());
+    select_flagged_index(spl.as<uint8_t>(), spos.as<u32>(), cnt.as<u64>(), L0, st);
+    inclusive_scan_u32(splu.as<u32>(), sincl.as<u32>(), L0, st);
+    u64 nspl;
+    d2h(&nspl, cnt.p, 1, st);
+    if (!headless) {
+      DBuf fb(4, st);
+      GT_CUDA(cudaMemsetAsync(fb.p, 0xFF, 4, st));
+      LAUNCH(k_check_splitters, nspl ? nspl : 1, d->body.as<u32>(), spos.as<u32>(), cnt.as<u64>(), nw,
+             fb.as<u32>());
+      u32 k;
+      d2h(&k, fb.p, 1, st);
+      if (k != 0xFFFFFFFFu) {
+        u32 pos, sym;
+        d2h(&pos, spos.as<u32>() + k, 1, st);
+        d2h(&sym, d->body.as<u32>() + pos, 1, st);
+        fail(GT_E_CORRUPTION, "splitter %u out of order at root position %u", sym, pos);
+      }
+      if (nspl != ns) fail(GT_E_CORRUPTION, "root body is missing file splitters");
+      u32 last = 0;
+      if (nspl) d2h(&last, spos.as<u32>() + nspl - 1, 1, st);
+      if (!nspl || (u64)last + 1 != L0) fail(GT_E_CORRUPTION, "root body has content after the last splitter");
+    }
+    const u64 F = headless ? 1 : ns;
+    d->F = F;
+    d->file_lo = std::min(file_lo, F);
+    d->file_hi = std::min(file_hi, F);
+    if (d->file_hi < d->file_lo) d->file_hi = d->file_lo;
+    d->seg_lo.alloc(F * 8, st);
+    d->seg_hi.alloc(F * 8, st);
+    LAUNCH(k_segments, F, spos.as<u32>(), F, L0, headless, d->seg_lo.as<u64>(), d->seg_hi.as<u64>());
+  // ---- segment tokens + root occurrence lists ------------------------------
+    const int SBF = std::max(1, bitlen(F - 1));
+    DBuf rkey(L0 * 8 + 8, st), wkey(L0 * 8 + 8, st), isr(L0 + 1, st), isw(L0 + 1, st);
+    DBuf& segof = d->root_seg;
+    segof.alloc(L0 * 4 + 4, st);
+    LAUNCH(k_root_keys, L0, d->body.as<u32>(), sincl.as<u32>(), L0, nw, base, SBF, headless,
+           rkey.as<u64>(), isr.as<uint8_t>(), wkey.as<u64>(), isw.as<uint8_t>(), segof.as<u32>());
+    auto occ_list = [&](DBuf& key, DBuf& is, int idbits, DBuf& oid, DBuf& oseg, DBuf& ocnt, u64* nout) {
+      DBuf sidx2(L0 * 4 + 4, st), k2(L0 * 8 + 8, st), k3(L0 * 8 + 8, st), h2(L0 + 1, st), hi2(L0 * 4 + 4, st);
+      select_flagged_index(is.as<uint8_t>(), sidx2.as<u32>(), cnt.as<u64>(), L0, st);
+      u64 m;
+      d2h(&m, cnt.p, 1, st);
+      LAUNCH(k_gather_u64, m, sidx2.as<u32>(), m, key.as<u64>(), k2.as<u64>());
+      sort_keys_u64(k2.as<u64>(), k3.as<u64>(), m, idbits + SBF, st);
+      LAUNCH(k_heads, m, k3.as<u64>(), m, h2.as<uint8_t>());
+      select_flagged_index(h2.as<uint8_t>(), hi2.as<u32>(), cnt.as<u64>(), m, st);
+      u64 u;
+      d2h(&u, cnt.p, 1, st);
+      oid.alloc(u * 4 + 4, st);
+      oseg.alloc(u * 4 + 4, st);
+      ocnt.alloc(u * 4 + 4, st);
+      LAUNCH(k_rle_keys, u, k3.as<u64>(), hi2.as<u32>(), u, m, SBF, oid.as<u32>(), oseg.as<u32>(),
+             ocnt.as<u32>());
+      *nout = u;
+    };
+    occ_list(rkey, isr, std::max(1, bitlen(R - 1)), d->rs_rule, d->rs_seg, d->rs_cnt, &d->n_rs);
+    occ_list(wkey, isw, std::max(1, bitlen(nw ? nw - 1 : 0)), d->rw_word, d->rw_seg, d->rw_cnt, &d->n_rw);
+    d->rs_off.alloc((R + 1) * 8, st);
+    LAUNCH(k_csr_offsets, R + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
+      GT_CUDA(cudaStreamSynchronize(st));
+    } catch (const Error& e) {
+      root_err = e;
+    } catch (const std::bad_alloc&) {
+      root_err = Error{GT_E_RESOURCE, "out of host memory"};
+    }
+  };
+  std::thread root_thread(root_side);
+  bool root_joined = false;
+  auto join_root = [&]() {
+    if (root_joined) return;
+    root_thread.join();
+    root_joined = true;
+    cudaEventDestroy(ev_body);
+    rebind_stream(st, {&d->seg_lo, &d->seg_hi, &d->root_seg, &d->rs_rule, &d->rs_seg, &d->rs_cnt, &d->rs_off,
+                       &d->rw_word, &d->rw_seg, &d->rw_cnt});
+    cudaStreamDestroy(s_root);
+    if (root_err.code != GT_OK) throw root_err;
+  };
+  struct JoinGuard {
+    std::function<void()> f;
+    ~JoinGuard() {
+      try {
+        f();
+      } catch (...) {
+      }
+    }
+  } join_guard{[&] {
+    if (!root_joined) {  // error path of the main pipeline
+      root_thread.join();
+      root_joined = true;
+      cudaStreamSynchronize(s_root);
+      cudaEventDestroy(ev_body);
+      rebind_stream(st, {&d->seg_lo, &d->seg_hi, &d->root_seg, &d->rs_rule, &d->rs_seg, &d->rs_cnt,
+                         &d->rs_off, &d->rw_word, &d->rw_seg, &d->rw_cnt});
+      cudaStreamDestroy(s_root);
+    }
+  }};
+
+
   // ---- (rule, symbol) sort + RLE -> own / sub CSR ----------------------
   const int SB = std::max(1, bitlen(limit - 1));
   const int KB = SB + std::max(1, bitlen(R - 1));
@@ -902,6 +1032,40 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   LAUNCH(k_csr_offsets, R + 1, own_rule.as<u32>(), Eo, R, d->own_off.as<u64>());
   LAUNCH(k_csr_offsets, R + 1, sub_rule.as<u32>(), Es, R, d->sub_off.as<u64>());
   ph.mark("own/sub CSR");
+
+  // ---- word-major transpose of the own pairs (no host sync: side stream) ----
+  cudaStream_t s_own = nullptr;
+  GT_CUDA(cudaStreamCreateWithFlags(&s_own, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s, main;
+    DeviceDag* d;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      rebind_stream(main, {&d->ow_word, &d->ow_rule, &d->ow_freq, &d->ow_off});
+      cudaStreamDestroy(s);
+    }
+  } own_guard{s_own, st, d};
+  {
+    cudaEvent_t ev;
+    GT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    GT_CUDA(cudaEventRecord(ev, st));
+    GT_CUDA(cudaStreamWaitEvent(s_own, ev, 0));
+    cudaEventDestroy(ev);
+  }
+    {
+    cudaStream_t st = s_own;
+    DBuf id2(Eo * 4 + 4, st), sid(Eo * 4 + 4, st);
+    d->ow_word.alloc(Eo * 4 + 4, st);
+    d->ow_rule.alloc(Eo * 4 + 4, st);
+    d->ow_freq.alloc(Eo * 4 + 4, st);
+    d->ow_off.alloc((nw + 1) * 8, st);
+    LAUNCH(k_iota_u32, Eo, id2.as<u32>(), Eo);
+    sort_pairs_u32_u32(d->own_ids.as<u32>(), d->ow_word.as<u32>(), id2.as<u32>(), sid.as<u32>(), Eo,
+                       std::max(1, bitlen(nw ? nw - 1 : 0)), st);
+    LAUNCH(k_gather3, Eo, sid.as<u32>(), Eo, own_rule.as<u32>(), d->own_freqs.as<u32>(),
+           (const u32*)nullptr, d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), (u32*)nullptr);
+    LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
+  }
 
   // ---- parents: stable sort of sub pairs by child -------------------------
   DBuf idx(Es * 4 + 4, st), sidx(Es * 4 + 4, st), child_sorted(Es * 4 + 4, st);
@@ -1080,43 +1244,6 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
   ph.mark("level lists");
 
-  // ---- root segments (dag.py:107-128) -------------------------------------
-  const u64 L0 = R ? rd32(blob + P.rules_pos) : 0;  // the root's body length
-  d->L0 = L0;
-  const bool headless = ns == 0;
-  DBuf spl(L0 + 1, st), splu(L0 * 4 + 4, st), sincl(L0 * 4 + 4, st), spos(L0 * 4 + 4, st);
-  LAUNCH(k_root_flags, L0, d->body.as<u32>(), L0, nw, base, spl.as<uint8_t>(), splu.as<u32>());
-  select_flagged_index(spl.as<uint8_t>(), spos.as<u32>(), cnt.as<u64>(), L0, st);
-  inclusive_scan_u32(splu.as<u32>(), sincl.as<u32>(), L0, st);
-  u64 nspl;
-  d2h(&nspl, cnt.p, 1, st);
-  if (!headless) {
-    DBuf fb(4, st);
-    GT_CUDA(cudaMemsetAsync(fb.p, 0xFF, 4, st));
-    LAUNCH(k_check_splitters, nspl ? nspl : 1, d->body.as<u32>(), spos.as<u32>(), cnt.as<u64>(), nw,
-           fb.as<u32>());
-    u32 k;
-    d2h(&k, fb.p, 1, st);
-    if (k != 0xFFFFFFFFu) {
-      u32 pos, sym;
-      d2h(&pos, spos.as<u32>() + k, 1, st);
-      d2h(&sym, d->body.as<u32>() + pos, 1, st);
-      fail(GT_E_CORRUPTION, "splitter %u out of order at root position %u", sym, pos);
-    }
-    if (nspl != ns) fail(GT_E_CORRUPTION, "root body is missing file splitters");
-    u32 last = 0;
-    if (nspl) d2h(&last, spos.as<u32>() + nspl - 1, 1, st);
-    if (!nspl || (u64)last + 1 != L0) fail(GT_E_CORRUPTION, "root body has content after the last splitter");
-  }
-  const u64 F = headless ? 1 : ns;
-  d->F = F;
-  d->file_lo = std::min(file_lo, F);
-  d->file_hi = std::min(file_hi, F);
-  if (d->file_hi < d->file_lo) d->file_hi = d->file_lo;
-  d->seg_lo.alloc(F * 8, st);
-  d->seg_hi.alloc(F * 8, st);
-  LAUNCH(k_segments, F, spos.as<u32>(), F, L0, headless, d->seg_lo.as<u64>(), d->seg_hi.as<u64>());
-
   // ---- exp_len by bottom-up level (grammar.py:109-124) --------------------
   d->exp_len.alloc(R * 8, st);
   GT_CUDA(cudaMemcpyAsync(d->exp_len.p, d->own_tok.p, R * 8, cudaMemcpyDeviceToDevice, st));
@@ -1129,57 +1256,21 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   d2h(&d->W, d->exp_len.p, 1, st);
   ph.mark("segments+exp_len");
 
-  // ---- segment tokens + root occurrence lists ------------------------------
-  const int SBF = std::max(1, bitlen(F - 1));
-  DBuf rkey(L0 * 8 + 8, st), wkey(L0 * 8 + 8, st), isr(L0 + 1, st), isw(L0 + 1, st);
-  DBuf& segof = d->root_seg;
-  segof.alloc(L0 * 4 + 4, st);
-  LAUNCH(k_root_keys, L0, d->body.as<u32>(), sincl.as<u32>(), L0, nw, base, SBF, headless,
-         rkey.as<u64>(), isr.as<uint8_t>(), wkey.as<u64>(), isw.as<uint8_t>(), segof.as<u32>());
-  d->seg_tokens.alloc(F * 8, st);
-  GT_CUDA(cudaMemsetAsync(d->seg_tokens.p, 0, F * 8, st));
-  LAUNCH(k_seg_sum_sorted, L0, segof.as<u32>(), L0,
-         (ValRootLen{d->body.as<u32>(), d->exp_len.as<u64>(), nw, base}), d->seg_tokens.as<u64>());
-  auto occ_list = [&](DBuf& key, DBuf& is, int idbits, DBuf& oid, DBuf& oseg, DBuf& ocnt, u64* nout) {
-    DBuf sidx2(L0 * 4 + 4, st), k2(L0 * 8 + 8, st), k3(L0 * 8 + 8, st), h2(L0 + 1, st), hi2(L0 * 4 + 4, st);
-    select_flagged_index(is.as<uint8_t>(), sidx2.as<u32>(), cnt.as<u64>(), L0, st);
-    u64 m;
-    d2h(&m, cnt.p, 1, st);
-    LAUNCH(k_gather_u64, m, sidx2.as<u32>(), m, key.as<u64>(), k2.as<u64>());
-    sort_keys_u64(k2.as<u64>(), k3.as<u64>(), m, idbits + SBF, st);
-    LAUNCH(k_heads, m, k3.as<u64>(), m, h2.as<uint8_t>());
-    select_flagged_index(h2.as<uint8_t>(), hi2.as<u32>(), cnt.as<u64>(), m, st);
-    u64 u;
-    d2h(&u, cnt.p, 1, st);
-    oid.alloc(u * 4 + 4, st);
-    oseg.alloc(u * 4 + 4, st);
-    ocnt.alloc(u * 4 + 4, st);
-    LAUNCH(k_rle_keys, u, k3.as<u64>(), hi2.as<u32>(), u, m, SBF, oid.as<u32>(), oseg.as<u32>(),
-           ocnt.as<u32>());
-    *nout = u;
-  };
-  occ_list(rkey, isr, std::max(1, bitlen(R - 1)), d->rs_rule, d->rs_seg, d->rs_cnt, &d->n_rs);
-  occ_list(wkey, isw, std::max(1, bitlen(nw ? nw - 1 : 0)), d->rw_word, d->rw_seg, d->rw_cnt, &d->n_rw);
-  d->rs_off.alloc((R + 1) * 8, st);
-  LAUNCH(k_csr_offsets, R + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
-  ph.mark("root occurrence lists");
-
-  // ---- word-major transpose of the own pairs --------------------------------
+  // ---- join the root side; segment tokens need exp_len ----------------------
+  join_root();
   {
-    DBuf id2(Eo * 4 + 4, st), sid(Eo * 4 + 4, st);
-    d->ow_word.alloc(Eo * 4 + 4, st);
-    d->ow_rule.alloc(Eo * 4 + 4, st);
-    d->ow_freq.alloc(Eo * 4 + 4, st);
-    d->ow_off.alloc((nw + 1) * 8, st);
-    LAUNCH(k_iota_u32, Eo, id2.as<u32>(), Eo);
-    sort_pairs_u32_u32(d->own_ids.as<u32>(), d->ow_word.as<u32>(), id2.as<u32>(), sid.as<u32>(), Eo,
-                       std::max(1, bitlen(nw ? nw - 1 : 0)), st);
-    LAUNCH(k_gather3, Eo, sid.as<u32>(), Eo, own_rule.as<u32>(), d->own_freqs.as<u32>(),
-           (const u32*)nullptr, d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), (u32*)nullptr);
-    LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
+    DBuf& segof = d->root_seg;
+    d->seg_tokens.alloc(d->F * 8, st);
+    GT_CUDA(cudaMemsetAsync(d->seg_tokens.p, 0, d->F * 8, st));
+    LAUNCH(k_seg_sum_sorted, d->L0, segof.as<u32>(), d->L0,
+           (ValRootLen{d->body.as<u32>(), d->exp_len.as<u64>(), nw, base}), d->seg_tokens.as<u64>());
   }
+  ph.mark("root side joined");
+
   GT_CUDA(cudaStreamSynchronize(st));
-  ph.mark("own transpose");
+  GT_CUDA(cudaStreamSynchronize(s_own));
+  own_rule.release();
+  ph.mark("finish");
   d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
