@@ -152,6 +152,14 @@ int gt_result_view(const gt_result* res, gt_view* out);
 void gt_result_free(gt_result* res);
 void gt_close(gt_ctx* ctx);
 
+/* Decompress-then-count on the device: the reference's naive counterparts
+ * (oracle_task, tasks.py:191-227; oracle.py:19-60) — expand the grammar to
+ * the token stream and count plainly — as an independent ground truth at
+ * corpus sizes the CPU oracles cannot hold.  Same result
+ * layout as gt_run; verification only (gt_run never uses it).  Sequence
+ * tasks need packed grams (seq_len * wbits <= 63). */
+int gt_run_naive(gt_ctx* ctx, int task, int seq_len, gt_result** out);
+
 /* Multi-GPU sharding: restrict per-file work and root seeds of
  * subsequent gt_run calls to files [file_lo, file_hi) (clamped to F); the
  * DAG itself is replicated in every context. */

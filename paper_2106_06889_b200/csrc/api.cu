@@ -20,6 +20,7 @@
 #include "seq.cuh"
 #include "sparse.cuh"
 #include "bottomup.cuh"
+#include "naive.cuh"
 #include "word.cuh"
 
 namespace gt {
@@ -322,6 +323,31 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
     }
     GT_CUDA(cudaEventRecord(c->ev[1], st));
     finish(c, r, R, task, seq_len, wbits, strat, t0, launches0);
+  });
+  if (status != GT_OK) {
+    delete r;
+    return status;
+  }
+  *out = r;
+  return GT_OK;
+}
+
+int gt_run_naive(gt_ctx* c, int task, int seq_len, gt_result** out) {
+  *out = nullptr;
+  gt_result* r = new gt_result();
+  int status = guard([&] {
+    if (task < GT_WORDCOUNT || task > GT_RANKEDINVERTEDINDEX) fail(GT_E_USAGE, "unknown task %d", task);
+    if (task >= GT_SEQCOUNT && seq_len < 1) fail(GT_E_USAGE, "sequence length must be >= 1");
+    DeviceDag& d = c->d;
+    GT_CUDA(cudaSetDevice(d.device));
+    auto t0 = std::chrono::steady_clock::now();
+    u64 launches0 = g_launches;
+    GT_CUDA(cudaEventRecord(c->ev[0], d.stream));
+    DevRecords R;
+    int wbits = 0;
+    naive_run(&d, task, seq_len, &R, &wbits);
+    GT_CUDA(cudaEventRecord(c->ev[1], d.stream));
+    finish(c, r, R, task, seq_len, wbits, GT_AUTO, t0, launches0);
   });
   if (status != GT_OK) {
     delete r;
