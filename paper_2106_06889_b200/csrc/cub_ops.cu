@@ -2,6 +2,7 @@
 // headers, instantiated into this library).  Used by the DAG loader and by
 // the result-assembly steps; the analytics kernels themselves are ours.
 #include <cub/cub.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
 #include "gt_internal.cuh"
@@ -81,6 +82,13 @@ void reduce_by_key_u64(const u64* keys, const u64* vals, u64* ukeys, u64* sums, 
   with_temp("cub::ReduceByKey", [&](void* t, size_t& b) {
     GT_CUDA(cub::DeviceReduce::ReduceByKey(t, b, keys, ukeys, vals, sums, d_nruns, ::cuda::std::plus<u64>(),
                                            (int64_t)n, s));
+  }, s);
+}
+
+void sort_segments_u32(const u32* ki, u32* ko, u64 n, u64 nseg, const u64* off, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::SegmentedSort32", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceSegmentedSort::SortKeys(t, b, ki, ko, (int)n, (int)nseg, off, off + 1, s));
   }, s);
 }
 

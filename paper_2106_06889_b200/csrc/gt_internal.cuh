@@ -160,6 +160,8 @@ void inclusive_scan_u32(const u32* in, u32* out, u64 n, cudaStream_t s);
 // ordered compaction of indices i in [0,n) with flags[i] != 0; count -> d_count
 void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 n, cudaStream_t s);
 void reduce_max_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
+// sort the keys of each segment [off[i], off[i+1]) independently (n < 2^31)
+void sort_segments_u32(const u32* keys_in, u32* keys_out, u64 n, u64 nseg, const u64* off, cudaStream_t s);
 void sort_pairs_u64_u64(u64* keys_in, u64* keys_out, u64* vals_in, u64* vals_out, u64 n, int end_bit,
                         cudaStream_t s);
 // runs of equal keys (sorted input) -> unique keys, sums, run count (device)

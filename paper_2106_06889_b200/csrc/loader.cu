@@ -331,6 +331,26 @@ __global__ void k_heads(const u64* k, u64 n, uint8_t* head) {
     head[i] = (i == 0 || k[i] != k[i - 1]);
 }
 
+__global__ void k_heads_seg(const u32* sym, const u32* owner, u64 n, uint8_t* head) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    head[i] = (i == 0 || sym[i] != sym[i - 1] || owner[i] != owner[i - 1]);
+}
+
+__global__ void k_rle_seg(const u32* sym_sorted, const u32* owner, const u32* hidx, u64 U, u64 n, u64 nw,
+                          u64 base, u32* pr_rule, u32* pr_sym, u32* pr_cnt, uint8_t* is_own, uint8_t* is_sub) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += stride) {
+    const u64 a = hidx[u], b = (u + 1 < U) ? hidx[u + 1] : n;
+    const u64 sym = sym_sorted[a];
+    pr_rule[u] = owner[a];
+    pr_cnt[u] = (u32)(b - a);
+    is_own[u] = sym < nw;
+    is_sub[u] = sym >= base;
+    pr_sym[u] = (u32)(sym >= base ? sym - base : sym);
+  }
+}
+
 // unique (rule, sym) runs -> pair arrays + class flags
 __global__ void k_rle(const u64* sk, const u32* hidx, u64 U, u64 n, int SB, u64 nw, u64 base,
                       u32* pr_rule, u32* pr_sym, u32* pr_cnt, uint8_t* is_own, uint8_t* is_sub) {
@@ -984,21 +1004,38 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
 
 
   // ---- (rule, symbol) sort + RLE -> own / sub CSR ----------------------
+  // bodies are contiguous per rule, so the (rule, symbol) order is a
+  // segmented sort of the body by symbol (one pass for the short bodies);
+  // a 64-bit global radix sort of (rule << SB | symbol) beyond 2^31 symbols
   const int SB = std::max(1, bitlen(limit - 1));
-  const int KB = SB + std::max(1, bitlen(R - 1));
-  DBuf keys(E * 8 + 8, st), skeys(E * 8 + 8, st);
-  LAUNCH(k_make_keys, E, d->body.as<u32>(), owner.as<u32>(), E, SB, keys.as<u64>());
-  sort_keys_u64(keys.as<u64>(), skeys.as<u64>(), E, KB, st);
-  keys.release();
   DBuf head(E + 1, st), hidx(E * 4 + 4, st), cnt(16, st);
-  LAUNCH(k_heads, E, skeys.as<u64>(), E, head.as<uint8_t>());
+  DBuf sbody, skeys;
+  // (measured: the global sort wins on C2-sized grammars, the segmented one from ~10^7 symbols)
+  const bool segmented = E >= (8ull << 20) && E < (1ull << 31) && R < (1ull << 31);
+  if (segmented) {
+    sbody.alloc(E * 4 + 4, st);
+    sort_segments_u32(d->body.as<u32>(), sbody.as<u32>(), E, R, d->boff.as<u64>(), st);
+    LAUNCH(k_heads_seg, E, sbody.as<u32>(), owner.as<u32>(), E, head.as<uint8_t>());
+  } else {
+    const int KB = SB + std::max(1, bitlen(R - 1));
+    DBuf keys(E * 8 + 8, st);
+    skeys.alloc(E * 8 + 8, st);
+    LAUNCH(k_make_keys, E, d->body.as<u32>(), owner.as<u32>(), E, SB, keys.as<u64>());
+    sort_keys_u64(keys.as<u64>(), skeys.as<u64>(), E, KB, st);
+    LAUNCH(k_heads, E, skeys.as<u64>(), E, head.as<uint8_t>());
+  }
   select_flagged_index(head.as<uint8_t>(), hidx.as<u32>(), cnt.as<u64>(), E, st);
   u64 U;
   d2h(&U, cnt.p, 1, st);
   DBuf pr_rule(U * 4 + 4, st), pr_sym(U * 4 + 4, st), pr_cnt(U * 4 + 4, st);
   DBuf is_own(U + 1, st), is_sub(U + 1, st);
-  LAUNCH(k_rle, U, skeys.as<u64>(), hidx.as<u32>(), U, E, SB, nw, base, pr_rule.as<u32>(),
-         pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
+  if (segmented)
+    LAUNCH(k_rle_seg, U, sbody.as<u32>(), owner.as<u32>(), hidx.as<u32>(), U, E, nw, base, pr_rule.as<u32>(),
+           pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
+  else
+    LAUNCH(k_rle, U, skeys.as<u64>(), hidx.as<u32>(), U, E, SB, nw, base, pr_rule.as<u32>(),
+           pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
+  sbody.release();
   skeys.release();
   head.release();
   DBuf sel(U * 4 + 4, st);
