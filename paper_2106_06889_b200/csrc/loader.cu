@@ -26,6 +26,7 @@
 #include <functional>
 #include <initializer_list>
 #include <memory>
+#include <mutex>
 #include <thread>
 
 #include "kernels_common.cuh"
@@ -720,6 +721,8 @@ static void build_levels(DeviceDag* d, const DBuf& lvl, const DBuf& off, u64 th,
 // sizes vary run to run, and growing the pool on demand (mapping physical
 // pages inside a run) costs 10^2 ms per GB-scale step and fragments it.
 static void reserve_pool(int device, cudaStream_t st) {
+  static std::mutex mu;  // contexts may be opened from several threads (one per device)
+  std::lock_guard<std::mutex> lock(mu);
   static bool done[64] = {};
   cudaMemPool_t pool;
   GT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

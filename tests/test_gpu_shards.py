@@ -22,7 +22,8 @@ def composed(name, scale):
 
 @pytest.mark.parametrize("src", ["g1", "many_files_70", "composed_2", "c2@0.003", "c3@0.003"])
 @pytest.mark.parametrize("nshards", [2, 3, 5])
-def test_device_shards_combine_to_whole(src, nshards):
+@pytest.mark.parametrize("strategy", ["auto", "bottomup"])
+def test_device_shards_combine_to_whole(src, nshards, strategy):
     import torch
 
     import paper_2106_06889_b200 as gt
@@ -31,6 +32,7 @@ def test_device_shards_combine_to_whole(src, nshards):
     blob = composed(*src.split("@")[0:1], float(src.split("@")[1])) if "@" in src else gtdc(src)
     dag = gt.DeviceDag(blob)
     V = dag.info["num_words"]
+    sid = gt._abi.STRATEGY_IDS[strategy]
     for l in (2, 3):
         full = {t: gt.run_compact(dag, t, gt.TraversalConfig(), l) for t in TASKS}
         for task in TASKS:
@@ -38,14 +40,14 @@ def test_device_shards_combine_to_whole(src, nshards):
                 acc = torch.zeros(V, dtype=torch.int64, device="cuda")
                 for rank in range(nshards):
                     r = DeviceRunner(dag, rank, nshards)
-                    r.run(TASK_IDS["wordcount"], l, 0, 64)
+                    r.run(TASK_IDS["wordcount"], l, sid, 64)
                     acc += r.counts_tensor()
                 got = r.assemble(acc, task)
             else:
                 parts = []
                 for rank in range(nshards):
                     r = DeviceRunner(dag, rank, nshards)
-                    parts.append(r.run(TASK_IDS[task], l, 0, 64))
+                    parts.append(r.run(TASK_IDS[task], l, sid, 64))
                 got = combine(parts, task, V)
             same_compact(got, full[task])
         dag.set_files(0, 1 << 62)
