@@ -1233,9 +1233,9 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     LAUNCH(k_edge_level_keys, m, idx.as<u32>(), m, group_of, lvl, key.as<u32>());
     sort_pairs_u32_u32(key.as<u32>(), key2.as<u32>(), idx.as<u32>(), idx2.as<u32>(), m,
                        std::max(1, bitlen((u64)nl + 1)), st);
-    oa.alloc(m * 4 + 4, st);
-    ob.alloc(m * 4 + 4, st);
-    of.alloc(m * 4 + 4, st);
+    oa.alloc(m * 4 + 16, st);  // + 16: the TMA-staged level loop copies whole 16-byte words
+    ob.alloc(m * 4 + 16, st);
+    of.alloc(m * 4 + 16, st);
     LAUNCH(k_gather3, m, idx2.as<u32>(), m, a_src, b_src, f_src, oa.as<u32>(), ob.as<u32>(), of.as<u32>());
     DBuf koff(((u64)nl + 3) * 8, st);
     LAUNCH(k_csr_offsets, (u64)nl + 3, key2.as<u32>(), m, (u64)nl + 2, koff.as<u64>());

@@ -318,6 +318,180 @@ void seg_reduce_levels_G(const char* name, const u32* dst, const u32* src, const
   g_launches++;
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent level loop with TMA-staged items (C == 1).  Each block owns an
+// even slice of every level; its slices are cut into chunks of at most kTmaCh
+// items whose (dst, src, freq) arrays are brought into shared memory by 1-D
+// bulk copies (cp.async.bulk ... mbarrier::complete_tx) double-buffered one
+// chunk ahead — including ACROSS the grid barrier, since the item lists are
+// static: after a barrier the block's first chunk of the next level is
+// already in shared memory and only the row gathers remain on the critical
+// path.  Runs are combined per 32-item warp step (shuffle segmented scan) and
+// flushed with one reduction each.
+// ---------------------------------------------------------------------------
+constexpr int kTmaBlock = 1024;
+constexpr u32 kTmaCh = 4096;             // items per staged chunk
+constexpr u32 kTmaPad = kTmaCh + 8;      // + alignment slack (16-byte aligned copies)
+
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, u32 bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+struct TmaUnit {
+  int it;  // level iteration index (0-based), -1 = none
+  u64 s, e;
+};
+
+template <class Mode, class Src, class Out>
+__global__ void __launch_bounds__(kTmaBlock) k_levels_tma(const u32* __restrict__ dst, const u32* __restrict__ src,
+                                                          const u32* __restrict__ freq,
+                                                          const u64* __restrict__ lvl_off, int L0, int L1,
+                                                          int reverse, Src in, Out out) {
+  extern __shared__ __align__(128) u32 tma_smem[];
+  __shared__ __align__(8) u64 bars[2];
+  cg::grid_group grid = cg::this_grid();
+  const int narr = freq ? 3 : 2;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int nlev = L1 - L0 + 1;
+  auto level_of = [&](int it) { return reverse ? L1 - it : L0 + it; };
+  // the block's slice of level iteration `it`
+  auto slice = [&](int it, u64* s0, u64* s1) {
+    const int L = level_of(it);
+    const u64 a = lvl_off[L], n = lvl_off[L + 1] - a;
+    const u64 S = (n + gridDim.x - 1) / gridDim.x;
+    *s0 = a + min(n, (u64)blockIdx.x * S);
+    *s1 = a + min(n, (u64)(blockIdx.x + 1) * S);
+  };
+  // the unit after (it, end e) in this block's sequence
+  auto next_unit = [&](int it, u64 e) {
+    TmaUnit u{-1, 0, 0};
+    u64 s0, s1;
+    slice(it, &s0, &s1);
+    if (e < s1) return TmaUnit{it, e, min(s1, e + kTmaCh)};
+    for (int j = it + 1; j < nlev; j++) {
+      slice(j, &s0, &s1);
+      if (s1 > s0) return TmaUnit{j, s0, min(s1, s0 + kTmaCh)};
+    }
+    return u;
+  };
+  auto first_unit = [&]() {
+    for (int j = 0; j < nlev; j++) {
+      u64 s0, s1;
+      slice(j, &s0, &s1);
+      if (s1 > s0) return TmaUnit{j, s0, min(s1, s0 + kTmaCh)};
+    }
+    return TmaUnit{-1, 0, 0};
+  };
+  auto buf = [&](int b, int arr) { return tma_smem + ((u64)b * 3 + arr) * kTmaPad; };
+  // one elected thread arms the buffer's barrier and issues the bulk copies
+  auto issue = [&](const TmaUnit& u, int b) {
+    if (threadIdx.x != 0 || u.it < 0) return;
+    // the buffer was last read through the generic proxy (ordered by the
+    // block barrier); order those reads before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const u64 a4 = u.s & ~3ull, e4 = (u.e + 3) & ~3ull;
+    const u32 bytes = (u32)((e4 - a4) * 4);
+    mbar_expect_tx(&bars[b], bytes * narr);
+    bulk_g2s(buf(b, 0), dst + a4, bytes, &bars[b]);
+    bulk_g2s(buf(b, 1), src + a4, bytes, &bars[b]);
+    if (freq) bulk_g2s(buf(b, 2), freq + a4, bytes, &bars[b]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  TmaUnit cur = first_unit();
+  issue(cur, 0);
+  u32 q = 0;  // sequence number of `cur`: buffer q & 1, parity (q >> 1) & 1
+  for (int it = 0; it < nlev; it++) {
+    while (cur.it == it) {
+      const TmaUnit nxt = next_unit(cur.it, cur.e);
+      issue(nxt, (q + 1) & 1);  // the other buffer was released at the end of the last unit
+      const int b = q & 1;
+      mbar_wait(&bars[b], (q >> 1) & 1);
+      const u64 a4 = cur.s & ~3ull;
+      const u32* sd = buf(b, 0);
+      const u32* ss = buf(b, 1);
+      const u32* sf = freq ? buf(b, 2) : nullptr;
+      for (u64 base = cur.s + (u64)warp * 32; base < cur.e; base += (u64)nwarp * 32) {
+        const u64 i = base + lane;
+        const bool ok = i < cur.e;
+        const u32 d = ok ? sd[i - a4] : 0xFFFFFFFFu;
+        u64 v = ok ? Mode::combine(sf ? sf[i - a4] : 1u, in(ss[i - a4], 0)) : 0;
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1) {
+          const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, k);
+          const u32 od = __shfl_up_sync(0xFFFFFFFFu, d, k);
+          if (lane >= (unsigned)k && od == d) v = Mode::merge(v, ov);
+        }
+        const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
+        if (ok && (lane == 31 || dn != d)) Mode::atomic(out(d, 0), v);
+      }
+      __syncthreads();  // buffer b is free again
+      cur = nxt;
+      q++;
+    }
+    if (it + 1 < nlev) grid.sync();
+  }
+}
+
+// host launcher of the TMA-staged loop (C == 1)
+template <class Mode, class Src, class Out>
+void seg_reduce_levels_tma(const char* name, const u32* dst, const u32* src, const u32* freq,
+                           const u64* lvl_off_dev, int L0, int L1, Src in, Out out, cudaStream_t st,
+                           bool reverse) {
+  auto kern = k_levels_tma<Mode, Src, Out>;
+  const size_t smem = (size_t)2 * 3 * kTmaPad * 4;
+  static int per_sm = -1;  // per instantiation
+  if (per_sm < 0) {
+    GT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTmaBlock, smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  int dev = 0, nsm = 148;
+  GT_CUDA(cudaGetDevice(&dev));
+  GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  int rv = reverse ? 1 : 0;
+  void* args[] = {(void*)&dst, (void*)&src, (void*)&freq, (void*)&lvl_off_dev, (void*)&L0, (void*)&L1,
+                  (void*)&rv, (void*)&in, (void*)&out};
+  ProfScope ps(name, st);
+  GT_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)(nsm * per_sm)), dim3(kTmaBlock), args,
+                                      smem, st));
+  g_launches++;
+}
+
 // levels [L0, L1] in increasing order, or decreasing with reverse = true
 template <class Mode, class Src, class Out>
 void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u32* freq,
@@ -325,7 +499,14 @@ void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u
                        bool reverse = false) {
   if (L1 < L0 || !C) return;
   const int rv = reverse ? 1 : 0;
-  if (C == 1) seg_reduce_levels_G<1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
+  // the TMA-staged variant is opt-in: measured slower on every config (C2 top-
+  // down pass 0.223 vs 0.188 ms per step, C5 0.73 vs 0.68 ms) — the item
+  // loads it hides are not on the critical path; the row gathers and the
+  // grid barrier are
+  static const bool use_tma = getenv("GT_LEVELS_TMA") != nullptr;
+  if (C == 1 && use_tma)
+    seg_reduce_levels_tma<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, in, out, st, reverse);
+  else if (C == 1) seg_reduce_levels_G<1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 2) seg_reduce_levels_G<2, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 4) seg_reduce_levels_G<4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 8) seg_reduce_levels_G<8, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
