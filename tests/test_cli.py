@@ -1,0 +1,80 @@
+"""CLI contract (mirrors pkg/tests/test_cli.py): TSV on stdout, one JSON
+manifest line on stderr with the sha256 outputDigest, exit codes of
+errors.py.  Error-path tests run on CPU (the format check precedes any
+device work); the analyze/verify/bench runs need the GPU."""
+
+from __future__ import annotations
+
+import json
+
+import pytest
+
+from conftest import expected, gtdc
+
+
+def run_cli(capsys, *argv):
+    from paper_2106_06889_b200.cli import main
+    code = main([str(a) for a in argv])
+    out, err = capsys.readouterr()
+    return code, out, err
+
+
+def test_missing_file_exit_2(tmp_path, capsys):
+    code, _, err = run_cli(capsys, "analyze", tmp_path / "nope.gtdc", "wordcount")
+    assert code == 2 and "gtadoc:" in err
+
+
+def test_bad_magic_exit_3(tmp_path, capsys):
+    p = tmp_path / "bad.gtdc"
+    p.write_bytes(b"NOPE" + bytes(32))
+    code, _, err = run_cli(capsys, "analyze", p, "wordcount")
+    assert code == 3 and "bad magic" in err
+
+
+def test_unknown_task_is_argparse_error():
+    from paper_2106_06889_b200.cli import main
+    with pytest.raises(SystemExit) as e:
+        main(["analyze", "x.gtdc", "nosuchtask"])
+    assert e.value.code == 2
+
+
+def test_workers_env_must_be_integer(tmp_path, capsys, monkeypatch):
+    p = tmp_path / "g1.gtdc"
+    p.write_bytes(gtdc("g1"))
+    monkeypatch.setenv("GTADOC_WORKERS", "three")
+    code, _, err = run_cli(capsys, "analyze", p, "wordcount")
+    assert code == 1 and "GTADOC_WORKERS" in err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("task", ["wordcount", "sort", "invertedindex", "termvector", "seqcount",
+                                  "rankedinvertedindex"])
+def test_analyze_tsv_and_manifest(task, tmp_path, capsys):
+    p = tmp_path / "g1.gtdc"
+    p.write_bytes(gtdc("g1"))
+    code, out, err = run_cli(capsys, "analyze", p, task)
+    assert code == 0
+    ent = expected()["g1"]["outputs"][task if task not in ("seqcount", "rankedinvertedindex") else task + "@3"]
+    manifest = json.loads(err.strip().splitlines()[-1])
+    assert manifest["command"] == "analyze" and manifest["task"] == task and manifest["l"] == 3
+    assert manifest["outputDigest"] == ent["sha256"]
+    if "text" in ent:
+        assert out == ent["text"]
+    assert set(manifest["timings"]) >= {"initialization", "traversal"}
+
+
+@pytest.mark.gpu
+def test_analyze_out_file_and_verify_and_bench(tmp_path, capsys):
+    p = tmp_path / "c.gtdc"
+    p.write_bytes(gtdc("many_files_70"))
+    code, out, err = run_cli(capsys, "analyze", p, "termvector", "--out", tmp_path / "tv.tsv")
+    assert code == 0 and out == ""
+    assert json.loads(err.strip().splitlines()[-1])["outputDigest"] == \
+        expected()["many_files_70"]["outputs"]["termvector"]["sha256"]
+    for task in ("wordcount", "invertedindex", "seqcount"):
+        code, out, _ = run_cli(capsys, "verify", p, task)
+        assert code == 0 and out.startswith(f"{task}\tok\t")
+    code, out, _ = run_cli(capsys, "bench", p, "wordcount", "--repeat", "2")
+    assert code == 0
+    rows = dict(line.split("\t") for line in out.splitlines() if not line.startswith("#"))
+    assert {"compressed", "decompress-naive"} <= set(rows)
