@@ -221,6 +221,20 @@ void gt_free_text(char* text);
 int gt_digest_view(const gt_dict* dict, const gt_view* view, uint8_t sha256[32], uint64_t* len);
 int gt_sha256(const void* data, uint64_t nbytes, uint8_t out[32]);
 
+/* ---- native compressor (host only) ------------------------------------------
+ * Ingest (ingest.py:30-121: strict UTF-8, Python str.split() whitespace,
+ * first-appearance word ids, one splitter after each file) + Sequitur
+ * (sequitur.py:46-258, lowest-free rule ids) + GTDC serialization
+ * (grammar.py:164-174): the same bytes as the reference's compress command.
+ * files[i] / lens[i]: the corpus files in order.  *out is malloc'd (release
+ * with gt_compress_free).  stats (optional, 4 entries): files, rules, words,
+ * stream symbols.  Status 101 = invalid UTF-8 (IngestError; stats[0] = the
+ * file index, gt_compress_last_error has the byte offset). */
+int gt_compress(const uint8_t* const* files, const uint64_t* lens, uint64_t nfiles, uint8_t** out,
+                uint64_t* out_len, uint64_t* stats);
+void gt_compress_free(uint8_t* p);
+const char* gt_compress_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

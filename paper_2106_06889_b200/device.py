@@ -25,7 +25,8 @@ EXPORTS = ("gt_abi_version", "gt_last_error", "gt_open", "gt_info_get", "gt_run"
            "gt_result_view", "gt_result_free", "gt_close", "gt_device_word_counts",
            "gt_dag_array", "gt_flush_l2", "gt_sync", "gt_profile", "gt_profile_report",
            "gt_set_files", "gt_assemble_counts", "gt_dict_open", "gt_dict_close", "gt_render_view",
-           "gt_free_text", "gt_digest_view", "gt_sha256", "gt_table_add_batch", "gt_run_naive")
+           "gt_free_text", "gt_digest_view", "gt_sha256", "gt_table_add_batch", "gt_run_naive",
+           "gt_compress", "gt_compress_free", "gt_compress_last_error")
 _lib = None
 
 
@@ -64,6 +65,10 @@ def lib():
         L.gt_free_text.argtypes = [C.c_void_p]
         L.gt_digest_view.argtypes = [C.c_void_p, C.POINTER(GtView), C.c_char_p, C.POINTER(C.c_uint64)]
         L.gt_sha256.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p]
+        L.gt_compress.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p),
+                                  C.POINTER(C.c_uint64), C.c_void_p]
+        L.gt_compress_free.argtypes = [C.c_void_p]
+        L.gt_compress_last_error.restype = C.c_char_p
         L.gt_run_naive.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.gt_table_add_batch.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                          C.c_void_p, C.c_void_p]

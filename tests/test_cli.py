@@ -78,3 +78,32 @@ def test_analyze_out_file_and_verify_and_bench(tmp_path, capsys):
     assert code == 0
     rows = dict(line.split("\t") for line in out.splitlines() if not line.startswith("#"))
     assert {"compressed", "decompress-naive"} <= set(rows)
+
+
+def test_compress_command_matches_reference_bytes(tmp_path, capsys):
+    d = tmp_path / "g1"
+    d.mkdir()
+    (d / "A.txt").write_text("a b a b c")
+    (d / "B.txt").write_text("a b c")
+    out = tmp_path / "g1.gtdc"
+    code, stdout, _ = run_cli(capsys, "compress", d, out)
+    assert code == 0
+    assert out.read_bytes() == gtdc("g1")
+    rows = dict(line.split("\t") for line in stdout.splitlines())
+    assert rows["files"] == "2" and rows["rules"] == "3" and rows["vocabulary"] == "3"
+
+
+def test_compress_empty_dir_usage_error(tmp_path, capsys):
+    empty = tmp_path / "empty"
+    empty.mkdir()
+    code, _, err = run_cli(capsys, "compress", empty, tmp_path / "x.gtdc")
+    assert code == 1 and "no regular files" in err
+
+
+def test_compress_invalid_utf8_ingest_error(tmp_path, capsys):
+    corpus = tmp_path / "bad"
+    corpus.mkdir()
+    (corpus / "a.txt").write_bytes(b"ok bytes")
+    (corpus / "b.txt").write_bytes(b"bad \xff\xfe here")
+    code, _, err = run_cli(capsys, "compress", corpus, tmp_path / "x.gtdc")
+    assert code == 2 and "b.txt" in err and "byte offset 4" in err
