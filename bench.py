@@ -154,6 +154,40 @@ def alg_bytes(kernel: str, info: dict, files: int, tasks=TASKS) -> float | None:
     return tot
 
 
+def ncu_traffic(kernel: str, tasks=TASKS):
+    """DRAM bytes per step of the dominant kernel from the newest committed
+    ncu metrics capture (profiles/*metrics.csv, tools/profile_round.sh):
+    mean dram__bytes_read.sum + dram__bytes_write.sum per launch of each
+    task's pass, summed over the step's passes; None without a capture."""
+    import csv
+    caps = sorted((ROOT / "profiles").glob("*metrics.csv"))
+    if not caps or kernel not in ("k_td_level", "k_td_levels"):
+        return None, None
+    rows = list(csv.reader(caps[-1].open()))
+    try:
+        i = next(k for k, r in enumerate(rows) if r and r[0] == "ID")
+    except StopIteration:
+        return None, None
+    hdr = rows[i]
+    per = {}
+    for r in rows[i + 1:]:
+        d = dict(zip(hdr, r))
+        name = d.get("Kernel Name", "")
+        if "TdRows" not in name or not d.get("Metric Name", "").startswith("dram__bytes_"):
+            continue
+        mode = "SumMode" if "SumMode" in name else "OrMode"
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(d["Metric Unit"], 1.0)
+        per.setdefault(mode, {}).setdefault(d["ID"], 0.0)
+        per[mode][d["ID"]] += float(d["Metric Value"].replace(",", "")) * scale
+    if not per:
+        return None, None
+    mean = {m: sum(v.values()) / len(v) for m, v in per.items()}
+    modes = ["SumMode" if t in ("wordcount", "sort") else "OrMode" for t in tasks]
+    if not all(m in mean for m in modes):
+        return None, None
+    return sum(mean[m] for m in modes), caps[-1].name
+
+
 def cpu_reference_steps(blob, steps, warmup, workers):
     """The reference algorithm on host cores (oracle/ restatement)."""
     from oracle.oracle import OracleDag
@@ -346,9 +380,11 @@ def main():
         n_l, ms_l = named[k_dom]
         b = alg_bytes(k_dom, info, Fo)  # per step
         ach = b * K / (ms_l / 1e3) / 1e9
+        traffic, src = ncu_traffic(k_dom)
         roof = {"bound": "hbm", "kernel": k_dom, "launches_per_step": n_l / K,
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": None, "alg_bytes_per_step": b, "kernel_ms_per_step": ms_l / K,
+                "traffic": traffic, "traffic_unit": "bytes per step (ncu dram read+write)",
+                "traffic_source": src, "alg_bytes_per_step": b, "kernel_ms_per_step": ms_l / K,
                 "share_of_step": (ms_l / K) / ms_per_step, "peak_source": peak_src}
     kernel_table = {k: {"launches_per_step": n / K, "ms_per_step": round(ms / K, 5)} for k, (n, ms) in
                     sorted(rep.items(), key=lambda kv: -kv[1][1])[:12]}

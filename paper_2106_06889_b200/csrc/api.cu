@@ -191,6 +191,12 @@ void gt_close(gt_ctx* c) {
 
 }  // extern "C"
 
+// GT_FORCE_SPARSE=1: per-file tasks take the sparse path at any F (diagnostics)
+static bool force_sparse() {
+  static const bool v = getenv("GT_FORCE_SPARSE") != nullptr;
+  return v;
+}
+
 static int select_strategy(const DeviceDag& d, int task, int requested, int fsw) {
   if (requested == GT_TOPDOWN || requested == GT_BOTTOMUP) return requested;
   bool needs_file_info = task >= GT_INVERTEDINDEX;
@@ -291,7 +297,7 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
         // equivalent is the presence-guided sparse per-file pass (sparse.cu)
         if (strategy == GT_BOTTOMUP && bu_file_tables(&d, GT_TERMVECTOR, &R, scratch_budget(&d))) {
           strat = GT_BOTTOMUP;
-        } else if (strat == GT_BOTTOMUP || (u64)Fo * d.nw >= (1ull << 32)) {
+        } else if (strat == GT_BOTTOMUP || (u64)Fo * d.nw >= (1ull << 32) || force_sparse()) {
           sparse_term_vector(&d, &R);
           strat = GT_TOPDOWN_SPARSE;
         } else {
@@ -315,7 +321,7 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
         break;
       }
       default: {
-        const bool sparse = strat == GT_BOTTOMUP;
+        const bool sparse = strat == GT_BOTTOMUP || force_sparse();
         run_sequences(&d, task, seq_len, sparse, &R, &wbits);
         strat = sparse ? GT_TOPDOWN_SPARSE : GT_TOPDOWN;
         break;

@@ -79,6 +79,11 @@ struct OutRowMajor {  // out[dst*C + col]
   u32 C;
   __device__ __forceinline__ u64* operator()(u32 d, u32 col) const { return out + (u64)d * C + col; }
 };
+struct TdRows {  // out[dst*C + col] for the top-down pass (a distinct kernel name in ncu)
+  u64* out;
+  u32 C;
+  __device__ __forceinline__ u64* operator()(u32 d, u32 col) const { return out + (u64)d * C + col; }
+};
 struct OutColMajor {  // out[col*V + dst]
   u64* out;
   u64 V;

@@ -167,7 +167,7 @@ static void td_levels(const DeviceDag* d, u32 C, u64* row, u32 per_file = 1) {
        d->n_rs, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row);
   // all levels in one persistent launch, grid barriers between levels
   seg_reduce_levels<Mode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
-                          d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrc{row, C}, OutRowMajor{row, C}, st);
+                          d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrc{row, C}, TdRows{row, C}, st);
 }
 
 // Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
