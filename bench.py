@@ -380,11 +380,11 @@ def main():
         n_l, ms_l = named[k_dom]
         b = alg_bytes(k_dom, info, Fo)  # per step
         ach = b * K / (ms_l / 1e3) / 1e9
-        traffic, src = ncu_traffic(k_dom)
+        traffic, traffic_src = ncu_traffic(k_dom)
         roof = {"bound": "hbm", "kernel": k_dom, "launches_per_step": n_l / K,
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "traffic_unit": "bytes per step (ncu dram read+write)",
-                "traffic_source": src, "alg_bytes_per_step": b, "kernel_ms_per_step": ms_l / K,
+                "traffic_source": traffic_src, "alg_bytes_per_step": b, "kernel_ms_per_step": ms_l / K,
                 "share_of_step": (ms_l / K) / ms_per_step, "peak_source": peak_src}
     kernel_table = {k: {"launches_per_step": n / K, "ms_per_step": round(ms / K, 5)} for k, (n, ms) in
                     sorted(rep.items(), key=lambda kv: -kv[1][1])[:12]}

@@ -554,6 +554,51 @@ __global__ void __launch_bounds__(kKahnBlock) k_kahn(KahnCtl* ctl, u32* q0, u32*
   }
 }
 
+// Bottom-up sums in ONE persistent reverse-level pass over the child edges
+// (children before parents): height(r) = max(1, 1 + height(child)) (the
+// reference's bottom-up round, engine.py:313-335) and exp_len(r) = own tokens
+// + Σ f · exp_len(child) (grammar.py:109-124).  Per 32-item warp step both
+// values are combined by dst with shuffle scans and flushed with one atomicMax
+// and one atomicAdd per run.
+__global__ void __launch_bounds__(1024) k_bu_pair(const u32* __restrict__ rule, const u32* __restrict__ child,
+                                                  const u32* __restrict__ freq, const u64* __restrict__ lvl_off,
+                                                  int L1, u64* hgt, u64* elen) {
+  cg::grid_group grid = cg::this_grid();
+  const unsigned lane = threadIdx.x & 31u;
+  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (int L = L1; L >= 0; L--) {
+    const u64 a = lvl_off[L], n = lvl_off[L + 1] - a;
+    for (u64 base = a + warp * 32; base < a + n; base += nwarps * 32) {
+      const u64 i = base + lane;
+      const bool ok = i < a + n;
+      const u32 d = ok ? rule[i] : 0xFFFFFFFFu;
+      u64 hv = 0, ev = 0;
+      if (ok) {
+        const u32 c = child[i];
+        hv = ld_cg64(hgt + c) + 1;
+        ev = (u64)freq[i] * ld_cg64(elen + c);
+      }
+#pragma unroll
+      for (int k = 1; k < 32; k <<= 1) {
+        const u64 oh = __shfl_up_sync(0xFFFFFFFFu, hv, k);
+        const u64 oe = __shfl_up_sync(0xFFFFFFFFu, ev, k);
+        const u32 od = __shfl_up_sync(0xFFFFFFFFu, d, k);
+        if (lane >= (unsigned)k && od == d) {
+          hv = hv > oh ? hv : oh;
+          ev += oe;
+        }
+      }
+      const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
+      if (ok && (lane == 31 || dn != d)) {
+        atomicMax((unsigned long long*)&hgt[d], (unsigned long long)hv);
+        if (ev) atomicAdd((unsigned long long*)&elen[d], (unsigned long long)ev);
+      }
+    }
+    if (L > 0) grid.sync();
+  }
+}
+
 // level-ordered edge lists: key = level of the grouping rule of each edge
 __global__ void k_edge_level_keys(const u32* idx, u64 n, const u32* group_of, const u32* lvl, u32* key) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
@@ -1150,7 +1195,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   KahnCtl* ctl = ctl_b.as<KahnCtl>();
   DBuf reach(R, st), firstu(4, st);
   GT_CUDA(cudaMemsetAsync(reach.p, 0, R, st));
-  auto kahn = [&](bool td, DBuf& rem, const DBuf& off, const DBuf& ids, DBuf& lvl, u64* processed) {
+  auto kahn = [&](bool td, DBuf& rem, const DBuf& off, const DBuf& ids, DBuf& lvl) {
     GT_CUDA(cudaMemsetAsync(ctl, 0, sizeof(KahnCtl), st));
     LAUNCH(k_flag_zero, R, rem.as<u32>(), R, td ? 1 : 0, flag.as<uint8_t>());
     // first frontier -> q1 (layer 1 reads q1), its count -> cnt[1]
@@ -1183,34 +1228,34 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
       GT_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)(nsm * ps)), dim3(kKahnBlock), args, 0, st));
       g_launches++;
     }
-    KahnCtl h;
-    d2h(&h, ctl, 1, st);
-    *processed = h.processed;
-    return (int)h.layers;
   };
   // top-down Kahn layering: the frontier never reaches a rule on (or below)
   // a reference cycle, so an incomplete layering is the cycle check
   // (grammar.py:127-161 order: cycles before unreachable rules, dag.py:173-184)
   u64 processed = 0;
-  int ntd = kahn(true, rem_td, d->sub_off, d->sub_ids, d->td_level, &processed);
+  kahn(true, rem_td, d->sub_off, d->sub_ids, d->td_level);
   // every rule but the root must be layered, and no reachable rule (nor the
-  // root itself) may reference the root: either way there is a cycle
+  // root itself) may reference the root: either way there is a cycle; then
+  // the first unreachable rule.  One host round trip for all three checks.
+  KahnCtl h;
+  u32 chk[2];
   {
-    DBuf bad(4, st);
-    GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
-    LAUNCH(k_root_cycle, 1, d->par_off.as<u64>(), d->par_ids.as<u32>(), reach.as<uint8_t>(), bad.as<u32>());
-    u32 rb = 0;
-    d2h(&rb, bad.p, 1, st);
-    if (processed + 1 < R || rb) {
+    DBuf cd(8, st);
+    GT_CUDA(cudaMemsetAsync(cd.p, 0, 4, st));
+    GT_CUDA(cudaMemsetAsync(cd.as<u32>() + 1, 0xFF, 4, st));
+    LAUNCH(k_root_cycle, 1, d->par_off.as<u64>(), d->par_ids.as<u32>(), reach.as<uint8_t>(), cd.as<u32>());
+    LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, cd.as<u32>() + 1);
+    GT_CUDA(cudaMemcpyAsync(&h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaMemcpyAsync(chk, cd.p, 8, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+  }
+  processed = h.processed;
+  const int ntd = (int)h.layers;
+  if (processed + 1 < R || chk[0]) {
     need_host_chain();
     cycle_message(blob, P);
   }
-  }
-  GT_CUDA(cudaMemsetAsync(firstu.p, 0xFF, 4, st));
-  LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, firstu.as<u32>());
-  u32 fu;
-  d2h(&fu, firstu.p, 1, st);
-  if (fu != 0xFFFFFFFFu) fail(GT_E_CORRUPTION, "rule %u is not reachable from the root", fu);
+  if (chk[1] != 0xFFFFFFFFu) fail(GT_E_CORRUPTION, "rule %u is not reachable from the root", chk[1]);
   ph.mark("top-down layering");
   rem_bu.release();
   rem_td.release();
@@ -1262,18 +1307,42 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   child_sorted.release();
   // bottom-up levels = heights (leaf = 1; the reference's bottom-up rounds,
   // engine.py:313-335), one persistent max pass in decreasing td level order
+  // heights (bottom-up levels) and exp_len in one persistent reverse pass
   int nbu = 0;
+  d->exp_len.alloc(R * 8, st);
   {
     DBuf hgt(R * 8, st);
     LAUNCH(k_fill_u64, R, hgt.as<u64>(), R, 1ull);
-    seg_reduce_levels<HeightMode>("k_heights", d->be_rule.as<u32>(), d->be_child.as<u32>(),
-                                  d->be_freq.as<u32>(), d->be_off_dev.as<u64>(), 0, ntd, 1,
-                                  RowSrc{hgt.as<u64>(), 1}, OutRowMajor{hgt.as<u64>(), 1}, st, true);
+    GT_CUDA(cudaMemcpyAsync(d->exp_len.p, d->own_tok.p, R * 8, cudaMemcpyDeviceToDevice, st));
+    {
+      static int per_sm = -1;
+      if (per_sm < 0) {
+        GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bu_pair, 1024, 0));
+        per_sm = std::max(per_sm, 1);
+      }
+      int nsm = 148;
+      GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+      const u32* br = d->be_rule.as<u32>();
+      const u32* bc = d->be_child.as<u32>();
+      const u32* bf = d->be_freq.as<u32>();
+      const u64* bo = d->be_off_dev.as<u64>();
+      int L1 = ntd;
+      u64* hg = hgt.as<u64>();
+      u64* el = d->exp_len.as<u64>();
+      void* args[] = {(void*)&br, (void*)&bc, (void*)&bf, (void*)&bo, (void*)&L1, (void*)&hg, (void*)&el};
+      ProfScope ps_("k_bu_pair", st);
+      GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_bu_pair, dim3((unsigned)(nsm * per_sm)), dim3(1024), args,
+                                          0, st));
+      g_launches++;
+    }
     LAUNCH(k_u64_to_u32, R, hgt.as<u64>(), R, d->bu_level.as<u32>());
-    u64 h0 = 0;
-    d2h(&h0, hgt.p, 1, st);  // height of the root, the highest rule
-    nbu = (int)h0;
-    d->depth = (i64)h0 - 1;
+    u64 hw[2] = {0, 0};  // height of the root (the highest rule) and W
+    GT_CUDA(cudaMemcpyAsync(&hw[0], hgt.p, 8, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaMemcpyAsync(&hw[1], d->exp_len.p, 8, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+    nbu = (int)hw[0];
+    d->depth = (i64)hw[0] - 1;
+    d->W = hw[1];
   }
   // level counts; the bottom-up rule lists (sequence tasks' head/tail pass)
   // are built on first use (ensure_bu_levels), the top-down pass runs over
@@ -1285,15 +1354,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   ph.mark("level lists");
 
   // ---- exp_len by bottom-up level (grammar.py:109-124) --------------------
-  d->exp_len.alloc(R * 8, st);
-  GT_CUDA(cudaMemcpyAsync(d->exp_len.p, d->own_tok.p, R * 8, cudaMemcpyDeviceToDevice, st));
-  // exp_len[r] = own tokens + Σ f · exp_len[child], in decreasing top-down
-  // level order (children first) in one persistent launch
-  seg_reduce_levels<SumMode>("k_exp_len", d->be_rule.as<u32>(), d->be_child.as<u32>(),
-                             d->be_freq.as<u32>(), d->be_off_dev.as<u64>(), 0, ntd, 1,
-                             RowSrc{d->exp_len.as<u64>(), 1}, OutRowMajor{d->exp_len.as<u64>(), 1}, st,
-                             true);
-  d2h(&d->W, d->exp_len.p, 1, st);
+  // (exp_len computed with the heights above)
   ph.mark("segments+exp_len");
 
   // ---- join the root side; segment tokens need exp_len ----------------------
