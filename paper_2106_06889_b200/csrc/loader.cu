@@ -338,8 +338,9 @@ __global__ void k_heads_seg(const u32* sym, const u32* owner, u64 n, uint8_t* he
     head[i] = (i == 0 || sym[i] != sym[i - 1] || owner[i] != owner[i - 1]);
 }
 
-__global__ void k_rle_seg(const u32* sym_sorted, const u32* owner, const u32* hidx, u64 U, u64 n, u64 nw,
+__global__ void k_rle_seg(const u32* sym_sorted, const u32* owner, const u32* hidx, const u64* Ud, u64 n, u64 nw,
                           u64 base, u32* pr_rule, u32* pr_sym, u32* pr_cnt, uint8_t* is_own, uint8_t* is_sub) {
+  const u64 U = *Ud;
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += stride) {
     const u64 a = hidx[u], b = (u + 1 < U) ? hidx[u + 1] : n;
@@ -353,8 +354,9 @@ __global__ void k_rle_seg(const u32* sym_sorted, const u32* owner, const u32* hi
 }
 
 // unique (rule, sym) runs -> pair arrays + class flags
-__global__ void k_rle(const u64* sk, const u32* hidx, u64 U, u64 n, int SB, u64 nw, u64 base,
+__global__ void k_rle(const u64* sk, const u32* hidx, const u64* Ud, u64 n, int SB, u64 nw, u64 base,
                       u32* pr_rule, u32* pr_sym, u32* pr_cnt, uint8_t* is_own, uint8_t* is_sub) {
+  const u64 U = *Ud;
   u64 stride = (u64)gridDim.x * blockDim.x;
   u64 mask = (1ull << SB) - 1;
   for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += stride) {
@@ -599,11 +601,13 @@ __global__ void __launch_bounds__(1024) k_bu_pair(const u32* __restrict__ rule, 
   }
 }
 
-// level-ordered edge lists: key = level of the grouping rule of each edge
-__global__ void k_edge_level_keys(const u32* idx, u64 n, const u32* group_of, const u32* lvl, u32* key) {
+
+// level key of every edge; edges not kept (root parents) sort after all levels
+__global__ void k_edge_level_keys2(const u32* group_of, const uint8_t* keep, const u32* lvl, u32 drop_key, u64 n,
+                                   u32* key) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    key[i] = lvl[group_of[idx ? idx[i] : i]];
+    key[i] = (keep && !keep[i]) ? drop_key : lvl[group_of[i]];
 }
 
 __global__ void k_flag_nonzero_u32(const u32* v, u64 n, uint8_t* f) {
@@ -797,6 +801,20 @@ static void reserve_pool(int device, cudaStream_t st) {
 static void rebind_stream(cudaStream_t st, std::initializer_list<DBuf*> bufs) {
   for (DBuf* b : bufs) b->s = st;
 }
+
+struct PinnedU64 {  // grow-only pinned host buffer (deferred read-backs)
+  u64* p = nullptr;
+  u64 cap = 0;
+  u64* get(u64 n) {
+    if (n > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = std::max<u64>(n, 1u << 12);
+      GT_CUDA(cudaMallocHost(&p, cap * 8));
+    }
+    return p;
+  }
+};
 
 // grow-only pinned host buffer (the rule-start table of the chain walk)
 struct PinnedU32 {
@@ -1072,45 +1090,50 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     sort_keys_u64(keys.as<u64>(), skeys.as<u64>(), E, KB, st);
     LAUNCH(k_heads, E, skeys.as<u64>(), E, head.as<uint8_t>());
   }
-  select_flagged_index(head.as<uint8_t>(), hidx.as<u32>(), cnt.as<u64>(), E, st);
-  u64 U;
-  d2h(&U, cnt.p, 1, st);
-  DBuf pr_rule(U * 4 + 4, st), pr_sym(U * 4 + 4, st), pr_cnt(U * 4 + 4, st);
-  DBuf is_own(U + 1, st), is_sub(U + 1, st);
+  // runs of equal (rule, symbol), sized by the worst case E so the only host
+  // round trip of this phase is the one for the own / sub pair counts
+  DBuf cnt3(32, st);
+  select_flagged_index(head.as<uint8_t>(), hidx.as<u32>(), cnt3.as<u64>(), E, st);
+  DBuf pr_rule(E * 4 + 4, st), pr_sym(E * 4 + 4, st), pr_cnt(E * 4 + 4, st);
+  DBuf is_own(E + 1, st), is_sub(E + 1, st);
+  GT_CUDA(cudaMemsetAsync(is_own.p, 0, E + 1, st));
+  GT_CUDA(cudaMemsetAsync(is_sub.p, 0, E + 1, st));
   if (segmented)
-    LAUNCH(k_rle_seg, U, sbody.as<u32>(), owner.as<u32>(), hidx.as<u32>(), U, E, nw, base, pr_rule.as<u32>(),
-           pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
+    LAUNCH(k_rle_seg, E, sbody.as<u32>(), owner.as<u32>(), hidx.as<u32>(), cnt3.as<u64>(), E, nw, base,
+           pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
   else
-    LAUNCH(k_rle, U, skeys.as<u64>(), hidx.as<u32>(), U, E, SB, nw, base, pr_rule.as<u32>(),
+    LAUNCH(k_rle, E, skeys.as<u64>(), hidx.as<u32>(), cnt3.as<u64>(), E, SB, nw, base, pr_rule.as<u32>(),
            pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
   sbody.release();
   skeys.release();
   head.release();
-  DBuf sel(U * 4 + 4, st);
-  // own pairs
-  select_flagged_index(is_own.as<uint8_t>(), sel.as<u32>(), cnt.as<u64>(), U, st);
-  d2h(&d->E_own, cnt.p, 1, st);
-  const u64 Eo = d->E_own;
+  DBuf selO(E * 4 + 4, st), selS(E * 4 + 4, st);
+  select_flagged_index(is_own.as<uint8_t>(), selO.as<u32>(), cnt3.as<u64>() + 1, E, st);
+  select_flagged_index(is_sub.as<uint8_t>(), selS.as<u32>(), cnt3.as<u64>() + 2, E, st);
+  {
+    u64 h[2];
+    d2h(h, cnt3.as<u64>() + 1, 2, st);
+    d->E_own = h[0];
+    d->E_sub = h[1];
+  }
+  const u64 Eo = d->E_own, Es = d->E_sub;
   DBuf own_rule(Eo * 4 + 4, st);
   d->own_ids.alloc(Eo * 4 + 4, st);
   d->own_freqs.alloc(Eo * 4 + 4, st);
-  LAUNCH(k_gather3, Eo, sel.as<u32>(), Eo, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
+  LAUNCH(k_gather3, Eo, selO.as<u32>(), Eo, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
          own_rule.as<u32>(), d->own_ids.as<u32>(), d->own_freqs.as<u32>());
-  // sub pairs
-  select_flagged_index(is_sub.as<uint8_t>(), sel.as<u32>(), cnt.as<u64>(), U, st);
-  d2h(&d->E_sub, cnt.p, 1, st);
-  const u64 Es = d->E_sub;
   DBuf sub_rule(Es * 4 + 4, st);
   d->sub_ids.alloc(Es * 4 + 4, st);
   d->sub_freqs.alloc(Es * 4 + 4, st);
-  LAUNCH(k_gather3, Es, sel.as<u32>(), Es, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
+  LAUNCH(k_gather3, Es, selS.as<u32>(), Es, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
          sub_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>());
+  selO.release();
+  selS.release();
   pr_rule.release();
   pr_sym.release();
   pr_cnt.release();
   is_own.release();
   is_sub.release();
-  sel.release();
   hidx.release();
   d->own_off.alloc((R + 1) * 8, st);
   d->sub_off.alloc((R + 1) * 8, st);
@@ -1264,28 +1287,27 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
 
   // ---- level-ordered edge lists (radix sort is stable: within a level the
   // edges keep (child, parent) resp. (rule, child) order) -------------------
+  // host values read back once at the end of gt_open (one pinned staging
+  // buffer: te and be level offsets, root height, W)
+  static thread_local PinnedU64 stage_host;
+  u64* stage = stage_host.get(2 * ((u64)ntd + 3) + 2);
   auto level_edges = [&](const u32* group_of, const uint8_t* keep, const u32* lvl, int nl,
                          const u32* a_src, const u32* b_src, const u32* f_src, DBuf& oa, DBuf& ob,
-                         DBuf& of, std::vector<u64>& off, DBuf& off_dev) {
+                         DBuf& of, u64* off_stage, DBuf& off_dev) {
+    // every edge is sorted (dropped ones under key nl + 1, after all levels),
+    // so no count has to come back to the host first
     DBuf idx(Es * 4 + 4, st), key(Es * 4 + 4, st), key2(Es * 4 + 4, st), idx2(Es * 4 + 4, st);
-    u64 m = Es;
-    if (keep) {
-      select_flagged_index(keep, idx.as<u32>(), cnt.as<u64>(), Es, st);
-      d2h(&m, cnt.p, 1, st);
-    } else {
-      LAUNCH(k_iota_u32, Es, idx.as<u32>(), Es);
-    }
-    LAUNCH(k_edge_level_keys, m, idx.as<u32>(), m, group_of, lvl, key.as<u32>());
-    sort_pairs_u32_u32(key.as<u32>(), key2.as<u32>(), idx.as<u32>(), idx2.as<u32>(), m,
+    LAUNCH(k_iota_u32, Es, idx.as<u32>(), Es);
+    LAUNCH(k_edge_level_keys2, Es, group_of, keep, lvl, (u32)nl + 1, Es, key.as<u32>());
+    sort_pairs_u32_u32(key.as<u32>(), key2.as<u32>(), idx.as<u32>(), idx2.as<u32>(), Es,
                        std::max(1, bitlen((u64)nl + 1)), st);
-    oa.alloc(m * 4 + 16, st);  // + 16: the TMA-staged level loop copies whole 16-byte words
-    ob.alloc(m * 4 + 16, st);
-    of.alloc(m * 4 + 16, st);
-    LAUNCH(k_gather3, m, idx2.as<u32>(), m, a_src, b_src, f_src, oa.as<u32>(), ob.as<u32>(), of.as<u32>());
+    oa.alloc(Es * 4 + 16, st);  // + 16: the TMA-staged level loop copies whole 16-byte words
+    ob.alloc(Es * 4 + 16, st);
+    of.alloc(Es * 4 + 16, st);
+    LAUNCH(k_gather3, Es, idx2.as<u32>(), Es, a_src, b_src, f_src, oa.as<u32>(), ob.as<u32>(), of.as<u32>());
     DBuf koff(((u64)nl + 3) * 8, st);
-    LAUNCH(k_csr_offsets, (u64)nl + 3, key2.as<u32>(), m, (u64)nl + 2, koff.as<u64>());
-    off.assign((size_t)nl + 3, 0);
-    d2h(off.data(), koff.p, (size_t)nl + 3, st);
+    LAUNCH(k_csr_offsets, (u64)nl + 3, key2.as<u32>(), Es, (u64)nl + 2, koff.as<u64>());
+    GT_CUDA(cudaMemcpyAsync(off_stage, koff.p, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
     off_dev = std::move(koff);
   };
   {
@@ -1294,14 +1316,14 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     LAUNCH(k_flag_nonzero_u32, Es, d->par_ids.as<u32>(), Es, keep.as<uint8_t>());
     level_edges(child_sorted.as<u32>(), keep.as<uint8_t>(), d->td_level.as<u32>(), ntd,
                 child_sorted.as<u32>(), d->par_ids.as<u32>(), d->par_freqs.as<u32>(), d->te_child,
-                d->te_par, d->te_freq, d->te_off, d->te_off_dev);
+                d->te_par, d->te_freq, stage, d->te_off_dev);
     // be: sub entries (grouped by rule) by the rule's TOP-DOWN level; walked
     // in decreasing level order every child is finished before its parents
     // (a child's td level exceeds each parent's), which is all the bottom-up
     // sums need.  The root (td level 0) comes last.
     level_edges(sub_rule.as<u32>(), nullptr, d->td_level.as<u32>(), ntd, sub_rule.as<u32>(),
                 d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), d->be_rule, d->be_child, d->be_freq,
-                d->be_off, d->be_off_dev);
+                stage + (ntd + 3), d->be_off_dev);
   }
   sub_rule.release();
   child_sorted.release();
@@ -1336,18 +1358,14 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
       g_launches++;
     }
     LAUNCH(k_u64_to_u32, R, hgt.as<u64>(), R, d->bu_level.as<u32>());
-    u64 hw[2] = {0, 0};  // height of the root (the highest rule) and W
+    // height of the root (the highest rule) and W, read back at the end
+    u64* hw = stage + 2 * ((u64)ntd + 3);
     GT_CUDA(cudaMemcpyAsync(&hw[0], hgt.p, 8, cudaMemcpyDeviceToHost, st));
     GT_CUDA(cudaMemcpyAsync(&hw[1], d->exp_len.p, 8, cudaMemcpyDeviceToHost, st));
-    GT_CUDA(cudaStreamSynchronize(st));
-    nbu = (int)hw[0];
-    d->depth = (i64)hw[0] - 1;
-    d->W = hw[1];
   }
-  // level counts; the bottom-up rule lists (sequence tasks' head/tail pass)
-  // are built on first use (ensure_bu_levels), the top-down pass runs over
-  // the te edge lists and needs no rule lists
-  d->bu.nl = nbu;
+  // level counts (bu.nl set from the root height at the end); the bottom-up
+  // rule lists (sequence tasks' head/tail pass) are built on first use
+  // (ensure_bu_levels), the top-down pass runs over the te edge lists
   d->td.nl = ntd;
   // the reference's bottom-up rounds exclude the root (engine.py:305-310)
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
@@ -1371,6 +1389,15 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   GT_CUDA(cudaStreamSynchronize(st));
   GT_CUDA(cudaStreamSynchronize(s_own));
   own_rule.release();
+  {
+    d->te_off.assign(stage, stage + ntd + 3);
+    d->be_off.assign(stage + ntd + 3, stage + 2 * (ntd + 3));
+    const u64* hw = stage + 2 * ((u64)ntd + 3);
+    nbu = (int)hw[0];
+    d->depth = (i64)hw[0] - 1;
+    d->W = hw[1];
+    d->bu.nl = nbu;
+  }
   ph.mark("finish");
   d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
