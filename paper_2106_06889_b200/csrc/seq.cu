@@ -244,6 +244,54 @@ __global__ void k_rec_keys(const u32* crun, const u32* ccol, const u64* ccnt, u6
   }
 }
 
+// payload-carrying record sort (packed grams)
+__global__ void k_rec_keys2(const u32* crun, const u32* ccol, const u64* ccnt, u64 n, u64 W, int CB, int by_file,
+                            u64* skey) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    skey[i] = ((u64)(by_file ? ccol[i] : crun[i]) << CB) | (W - ccnt[i]);
+}
+
+__global__ void k_cell_grams(const u32* crun, u64 n, const u32* run_start, const u64* skey_sorted, u64* gk) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) gk[i] = skey_sorted[run_start[crun[i]]];
+}
+
+// sorted (major << CB | W - count) -> count, major
+__global__ void k_unkey2(const u64* key, u64 n, u64 W, int CB, u64* cnt, u32* major, u32) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 m = (1ull << CB) - 1;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    cnt[i] = W - (key[i] & m);
+    major[i] = (u32)(key[i] >> CB);
+  }
+}
+
+__global__ void k_add_u32_base(u32* a, u64 n, u32 v) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] += v;
+}
+
+__global__ void k_heads_u32v(const u32* g, u64 n, uint8_t* h) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) h[i] = i == 0 || g[i] != g[i - 1];
+}
+
+__global__ void k_group_out2(const u32* gsel, const u64* ng_p, u64 n, const u32* run, const u32* run_start,
+                             const u64* skey_sorted, u64* goff, u64* gkey) {
+  const u64 ng = *ng_p;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g <= ng; g += stride) {
+    if (g == ng) {
+      goff[g] = n;
+      continue;
+    }
+    const u32 i = gsel[g];
+    goff[g] = i;
+    gkey[g] = skey_sorted[run_start[run[i]]];
+  }
+}
+
 __global__ void k_rec_out(const u32* rec, u64 n, const u32* crun, const u32* ccol, const u64* ccnt,
                           const u32* run_start, const u64* skey_sorted, const u32* gram, u32 l,
                           int packed, u32 file_lo, int write_gram, u64* key_out, u32* gram_out,
@@ -428,6 +476,42 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   const bool by_file = task == GT_SEQCOUNT;
   const int MB = by_file ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns));
   if (CB + MB > 64) fail(GT_E_RESOURCE, "sort key of %d bits exceeds 64", CB + MB);
+  if (packed) {
+    // the sort carries its payload: SEQCOUNT sorts (file | W - count) with the
+    // packed gram as the value, RII (run | W - count) with the file — every
+    // output field comes out of the sorted arrays, no permutation gathers
+    DBuf sk(n * 8 + 8, st), sk2(n * 8 + 8, st);
+    SL(k_rec_keys2, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
+       sk.as<u64>());
+    Rr->n = n;
+    Rr->count.alloc(n * 8 + 8, st);
+    if (by_file) {
+      DBuf gk(n * 8 + 8, st);
+      Rr->key.alloc(n * 8 + 8, st);
+      SL(k_cell_grams, n, crun.as<u32>(), n, runs.as<u32>(), skey.as<u64>(), gk.as<u64>());
+      sort_pairs_u64_u64(sk.as<u64>(), sk2.as<u64>(), gk.as<u64>(), Rr->key.as<u64>(), n, CB + MB, st);
+      DBuf major(n * 4 + 4, st);
+      SL(k_unkey2, n, sk2.as<u64>(), n, Wt, CB, Rr->count.as<u64>(), major.as<u32>(), 0u);
+      Rr->n_groups = Fo;
+      Rr->group_off.alloc((Fo + 1) * 8, st);
+      SL(k_csr_offsets, Fo + 1, major.as<u32>(), n, (u64)Fo, Rr->group_off.as<u64>());
+    } else {
+      Rr->id.alloc(n * 4 + 4, st);
+      sort_pairs_u64_u32(sk.as<u64>(), sk2.as<u64>(), ccol.as<u32>(), Rr->id.as<u32>(), n, CB + MB, st);
+      DBuf rn(n * 4 + 4, st), gh(n + 1, st), gsel(n * 4 + 4, st);
+      SL(k_unkey2, n, sk2.as<u64>(), n, Wt, CB, Rr->count.as<u64>(), rn.as<u32>(), (u32)d->file_lo);
+      SL(k_add_u32_base, n, Rr->id.as<u32>(), n, (u32)d->file_lo);
+      SL(k_heads_u32v, n, rn.as<u32>(), n, gh.as<uint8_t>());
+      select_flagged_index(gh.as<uint8_t>(), gsel.as<u32>(), dcnt.as<u64>(), n, st);
+      const u64 ng = d2h1<u64>(dcnt.p, st);
+      Rr->n_groups = ng;
+      Rr->group_off.alloc((ng + 1) * 8, st);
+      Rr->group_key.alloc(ng * 8 + 8, st);
+      SL(k_group_out2, ng + 1, gsel.as<u32>(), dcnt.as<u64>(), n, rn.as<u32>(), runs.as<u32>(), skey.as<u64>(),
+         Rr->group_off.as<u64>(), Rr->group_key.as<u64>());
+    }
+    ph.mark("record sort");
+  } else {
   DBuf sk(n * 8 + 8, st), sk2(n * 8 + 8, st), rec(n * 4 + 4, st), rec2(n * 4 + 4, st);
   SL(k_rec_keys, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
      sk.as<u64>(), rec.as<u32>());
@@ -466,6 +550,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
        skey.as<u64>(), sgram.as<u32>(), l, packed, Rr->group_off.as<u64>(), Rr->group_key.as<u64>(),
        Rr->group_gram.as<u32>());
     GT_CUDA(cudaMemcpyAsync(Rr->group_off.as<u64>() + ng, &n, 8, cudaMemcpyHostToDevice, st));
+  }
   }
   GT_CUDA(cudaStreamSynchronize(st));
   ph.mark("records");
