@@ -73,6 +73,19 @@ struct RowSrc {  // in[src*C + col]
   __device__ __forceinline__ u64 operator()(u32 s, u32 col) const { return ldcg(in + (u64)s * C + col); }
 };
 
+// two adjacent columns of a source row (col even): one 16-byte load for
+// RowSrc, two scalar reads otherwise
+template <class Src>
+__device__ __forceinline__ void load_pair(const Src& in, u32 s, u32 col, u64* a, u64* b) {
+  *a = in(s, col);
+  *b = in(s, col + 1);
+}
+__device__ __forceinline__ void load_pair(const RowSrc& in, u32 s, u32 col, u64* a, u64* b) {
+  const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(in.in + (u64)s * in.C + col));
+  *a = v.x;
+  *b = v.y;
+}
+
 // ---- output address functors --------------------------------------------------
 struct OutRowMajor {  // out[dst*C + col]
   u64* out;
@@ -180,6 +193,51 @@ __device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const 
   constexpr int B = 8;
   const u64 teams = nthreads / G;
   const u32 tl = threadIdx.x % G;
+  if (C == 2u * G) {
+    // two ADJACENT columns per lane: the team reads a whole row with 16-byte
+    // loads (C = 64: one 512-byte access per item), 8 items in flight
+    constexpr int BB = 8;
+    const u32 c0 = 2 * tl;
+    for (u64 t = gtid / G; t * K < n; t += teams) {
+      const u64 a = t * K, b = a + K < n ? a + K : n;
+      u32 cd = dst[a];
+      u64 acc0 = 0, acc1 = 0;
+      for (u64 i0 = a; i0 < b; i0 += BB) {
+        u32 dd[BB];
+        u64 v0[BB], v1[BB];
+#pragma unroll
+        for (int j = 0; j < BB; j++) {
+          const u64 i = i0 + j;
+          const bool ok = i < b;
+          dd[j] = ok ? dst[i] : 0xFFFFFFFFu;
+          u64 x = 0, y = 0;
+          if (ok) {
+            load_pair(in, src[i], c0, &x, &y);
+            const u32 f = item_freq(freq, i);
+            x = Mode::combine(f, x);
+            y = Mode::combine(f, y);
+          }
+          v0[j] = x;
+          v1[j] = y;
+        }
+#pragma unroll
+        for (int j = 0; j < BB; j++) {
+          if (dd[j] == 0xFFFFFFFFu) break;
+          if (dd[j] != cd) {
+            Mode::atomic(out(cd, c0), acc0);
+            Mode::atomic(out(cd, c0 + 1), acc1);
+            acc0 = acc1 = 0;
+            cd = dd[j];
+          }
+          acc0 = Mode::merge(acc0, v0[j]);
+          acc1 = Mode::merge(acc1, v1[j]);
+        }
+      }
+      Mode::atomic(out(cd, c0), acc0);
+      Mode::atomic(out(cd, c0 + 1), acc1);
+    }
+    return;
+  }
   if (MULTI && C <= 4u * G) {
     // (persistent level loops only: measured faster there — C4 64-file
     // top-down pass 7.5 -> 3.9 ms — and slower for the flat launches)
