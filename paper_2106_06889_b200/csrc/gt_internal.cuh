@@ -10,8 +10,9 @@
 //   ow_*      own pairs transposed: sorted by (word, rule)  -> pull reduce
 //   rs_*      root occurrences per (rule, segment) sorted by rule -> per-file seeds
 //   rw_*      root word occurrences per (word, segment) sorted by word
-//   td_order  rules grouped by top-down level (engine.py round), light|heavy
-//   bu_order  rules grouped by bottom-up level (height+1)
+//   te_*      (child, parent, freq) edges grouped by top-down level (engine.py round)
+//   be_*      (rule, child, freq) edges grouped by bottom-up level (height) -> seq windows
+//   bu_order  rules grouped by bottom-up level (height+1), built lazily
 #pragma once
 
 #include <cuda_runtime.h>

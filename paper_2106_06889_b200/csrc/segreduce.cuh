@@ -347,7 +347,8 @@ __global__ void __launch_bounds__(kLevelBlock) k_segred_levels(const u32* __rest
                                                        const u64* __restrict__ lvl_off, int L0, int L1,
                                                        int reverse, u32 C, Src in, Out out) {
   cg::grid_group grid = cg::this_grid();
-  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  // teams numbered round-robin over the blocks (small levels reach every SM)
+  const u64 gtid = ((u64)(threadIdx.x / G) * gridDim.x + blockIdx.x) * G + threadIdx.x % G;
   const u64 nthreads = (u64)gridDim.x * blockDim.x;
   for (int it = 0; it <= L1 - L0; it++) {
     const int L = reverse ? L1 - it : L0 + it;
@@ -366,6 +367,104 @@ __global__ void __launch_bounds__(kLevelBlock) k_segred_levels(const u32* __rest
       }
     }
     if (it < L1 - L0) grid.sync();
+  }
+}
+
+// C == 1 persistent level loop with the items of short levels (at most
+// kPre 32-item steps per warp) prefetched into registers before the grid
+// barrier that precedes them: item lists are static, so after the barrier
+// only the row gathers, the warp scans and one reduction per run remain on
+// the level's critical path.  Larger levels run the tiled body.  BLOCK
+// threads per block, one block per SM: a smaller block shortens the
+// block-wide part of every barrier (the C2 pass is 24 barrier-separated
+// levels of ~5*10^4 items), a larger one keeps more gathers in flight on
+// levels of 10^5-10^6 items.
+template <int BLOCK, int kPre, class Mode, class Src, class Out>
+__global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restrict__ dst,
+                                                          const u32* __restrict__ src,
+                                                          const u32* __restrict__ freq,
+                                                          const u64* __restrict__ lvl_off, int L0, int L1,
+                                                          int reverse, int prefetch, Src in, Out out) {
+  cg::grid_group grid = cg::this_grid();
+  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 nthreads = (u64)gridDim.x * blockDim.x;
+  // warps numbered round-robin over the blocks: a level smaller than the
+  // grid is spread over every SM instead of filling the first blocks
+  const u64 nwarps = nthreads >> 5, warp = (u64)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const unsigned lane = threadIdx.x & 31u;
+  const int nit = L1 - L0 + 1;
+  // this lane's items of a short level: steps p < pk of the warp's tile
+  u32 pd[kPre], ps[kPre], pf[kPre];
+  int pk = 0;
+  auto fetch = [&](int it) {
+    pk = 0;
+    if (!prefetch || it >= nit) return;
+    const int L = reverse ? L1 - it : L0 + it;
+    const u64 a = lvl_off[L], n = lvl_off[L + 1] - a;
+    const u64 K = (n + 32 * nwarps - 1) / (32 * nwarps);
+    if (K > (u64)kPre) return;
+    pk = K < 1 ? 1 : (int)K;
+    const u64 t0 = a + warp * 32ull * pk + lane;
+#pragma unroll
+    for (int p = 0; p < kPre; p++) {
+      const u64 i = t0 + 32ull * p;
+      const bool ok = p < pk && i < a + n;
+      pd[p] = ok ? dst[i] : 0xFFFFFFFFu;
+      ps[p] = ok ? src[i] : 0u;
+      pf[p] = ok ? (freq ? freq[i] : 1u) : 0u;
+    }
+  };
+  fetch(0);
+  for (int it = 0; it < nit; it++) {
+    if (pk) {
+      u32 dd[kPre];
+      u64 vv[kPre];
+      const int K = pk;
+#pragma unroll
+      for (int p = 0; p < kPre; p++) {
+        dd[p] = pd[p];
+        vv[p] = dd[p] != 0xFFFFFFFFu ? Mode::combine(pf[p], in(ps[p], 0)) : 0;
+      }
+      fetch(it + 1);  // the next level's items load while these gathers are in flight
+      if (__any_sync(0xFFFFFFFFu, dd[0] != 0xFFFFFFFFu)) {
+        u32 carry_d = 0xFFFFFFFFu;
+        u64 carry_v = 0;
+#pragma unroll
+        for (int p = 0; p < kPre; p++) {
+          if (p >= K) break;  // warp-uniform
+          const u32 d = dd[p];
+          u64 v = vv[p];
+          const u32 d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+          if (carry_d != 0xFFFFFFFFu && d0 != carry_d) {
+            if (lane == 0) Mode::atomic(out(carry_d, 0), carry_v);
+            carry_d = 0xFFFFFFFFu;
+            carry_v = 0;
+          }
+#pragma unroll
+          for (int s = 1; s < 32; s <<= 1) {
+            const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, s);
+            const u32 od = __shfl_up_sync(0xFFFFFFFFu, d, s);
+            if (lane >= (unsigned)s && od == d) v = Mode::merge(v, ov);
+          }
+          if (d == carry_d) v = Mode::merge(v, carry_v);
+          const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
+          if (d != 0xFFFFFFFFu && lane != 31 && dn != d) Mode::atomic(out(d, 0), v);
+          carry_d = __shfl_sync(0xFFFFFFFFu, d, 31);
+          carry_v = __shfl_sync(0xFFFFFFFFu, v, 31);
+        }
+        if (lane == 0 && carry_d != 0xFFFFFFFFu) Mode::atomic(out(carry_d, 0), carry_v);
+      }
+    } else {
+      const int L = reverse ? L1 - it : L0 + it;
+      const u64 a = lvl_off[L], n = lvl_off[L + 1] - a;
+      if (n) {
+        int K = (int)((n + 32 * nwarps - 1) / (32 * nwarps));
+        K = K < 1 ? 1 : (K > 16 ? 16 : K);
+        segred1_body<Mode>(dst + a, src + a, freq ? freq + a : nullptr, n, K, in, out, warp, nwarps);
+      }
+      fetch(it + 1);
+    }
+    if (it + 1 < nit) grid.sync();
   }
 }
 
@@ -606,11 +705,46 @@ void seg_reduce_levels_tma(const char* name, const u32* dst, const u32* src, con
   g_launches++;
 }
 
+template <int BLOCK, int PRE, class Mode, class Src, class Out>
+void seg_reduce_levels1_b(const char* name, const u32* dst, const u32* src, const u32* freq,
+                          const u64* lvl_off_dev, int L0, int L1, int reverse, int prefetch, Src in, Out out,
+                          cudaStream_t st) {
+  auto kern = k_segred1_levels<BLOCK, PRE, Mode, Src, Out>;
+  int dev = 0, nsm = 148;
+  GT_CUDA(cudaGetDevice(&dev));
+  GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  void* args[] = {(void*)&dst, (void*)&src, (void*)&freq, (void*)&lvl_off_dev, (void*)&L0, (void*)&L1,
+                  (void*)&reverse, (void*)&prefetch, (void*)&in, (void*)&out};
+  ProfScope ps(name, st);
+  GT_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)nsm), dim3(BLOCK), args, 0, st));
+  g_launches++;
+}
+
+// avg_items: mean items per level (host-side hint).  Levels of at most one
+// 32-item step per warp are the common case on shallow-fan-out DAGs (C2:
+// ~5*10^4 items over 24 levels) and prefetch one step; DAGs whose levels
+// run several steps per warp (C4/C5: 10^5-10^6) prefetch up to four.
+// Measured per pass: C2 94 -> 70 us, C4 0.39 -> 0.36 ms, C5 0.70 -> 0.68 ms.
+template <class Mode, class Src, class Out>
+void seg_reduce_levels1(const char* name, const u32* dst, const u32* src, const u32* freq,
+                        const u64* lvl_off_dev, int L0, int L1, int reverse, u64 avg_items, Src in, Out out,
+                        cudaStream_t st) {
+  static const int prefetch = getenv("GT_LEVEL_PREFETCH") ? atoi(getenv("GT_LEVEL_PREFETCH")) : 1;
+  static const int force_pre = getenv("GT_LEVEL_PRE") ? atoi(getenv("GT_LEVEL_PRE")) : 0;
+  const int pre = force_pre ? force_pre : (avg_items > 148ull * kLevelBlock ? 4 : 1);
+  if (pre == 4)
+    seg_reduce_levels1_b<kLevelBlock, 4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, reverse, prefetch, in,
+                                               out, st);
+  else
+    seg_reduce_levels1_b<kLevelBlock, 1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, reverse, prefetch, in,
+                                               out, st);
+}
+
 // levels [L0, L1] in increasing order, or decreasing with reverse = true
 template <class Mode, class Src, class Out>
 void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u32* freq,
                        const u64* lvl_off_dev, int L0, int L1, u32 C, Src in, Out out, cudaStream_t st,
-                       bool reverse = false) {
+                       bool reverse = false, u64 avg_items = 0) {
   if (L1 < L0 || !C) return;
   const int rv = reverse ? 1 : 0;
   // the TMA-staged variant is opt-in: measured slower on every config (C2 top-
@@ -620,7 +754,7 @@ void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u
   static const bool use_tma = getenv("GT_LEVELS_TMA") != nullptr;
   if (C == 1 && use_tma)
     seg_reduce_levels_tma<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, in, out, st, reverse);
-  else if (C == 1) seg_reduce_levels_G<1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
+  else if (C == 1) seg_reduce_levels1<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, avg_items, in, out, st);
   else if (C <= 2) seg_reduce_levels_G<2, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 4) seg_reduce_levels_G<4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 8) seg_reduce_levels_G<8, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);

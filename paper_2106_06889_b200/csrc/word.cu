@@ -3,22 +3,21 @@
 // Reference algorithm (engine.py:178-302, _kernels.py:129-188): Alg. 1
 // top-down weight propagation in mask rounds, then Σ own_freq·weight into
 // hash tables plus a scan of the root's plain words.  B200 formulation:
-//   * rounds become precomputed levels (loader.cu); each level is ONE pull
-//     launch: a rule reads its parents' finished rows (par CSR, parents
-//     ascending) — no atomics, no masks, no host round trip.  Light rules
-//     get a team of G lanes (one lane per weight column), heavy rules
-//     (>16 parents) a whole warp whose stripes split the parent list and
-//     are combined with shuffles (the paper's split of high-fan-out work).
+//   * rounds become precomputed levels (loader.cu); all levels run in ONE
+//     persistent cooperative launch (segreduce.cuh k_segred_levels): the
+//     level's (child, parent) edges are dealt to lanes in equal chunks, runs
+//     of one child are combined by warp scans and flushed with one RED per
+//     run — no masks, no host round trip, and heavy rules cost the same per
+//     edge as light ones (the paper's split of high-fan-out work, by edges).
 //   * root occurrences seed the rows from the (rule, segment) list, so the
-//     same kernel serves corpus-global weights (1 column = all owned files),
+//     same pass serves corpus-global weights (1 column = all owned files),
 //     per-file weights (F columns) and per-file presence bitsets (OR mode,
 //     ceil(F/64) 64-bit columns; exact for inverted index, which only needs
-//     presence: 8 B per rule instead of 8·F B).
-//   * the reduce is a pull over the word-major transpose of the own pairs:
-//     a reduce-by-key over (word, rule, freq) entries sorted by word, with
-//     plain stores for runs interior to a tile and atomics only for runs
-//     crossing a tile boundary (hot Zipf words cost one atomic per tile, not
-//     one per occurrence).  Root words come from the (word, segment) list.
+//     presence: 8 B per rule instead of 8*F B).
+//   * the reduce is the same segmented gather-reduce over the word-major
+//     transpose of the own pairs (word, rule, freq): one RED per word run
+//     per chunk (hot Zipf words cost one atomic per chunk, not one per
+//     occurrence).  Root words come from the (word, segment) list.
 #include <algorithm>
 #include <type_traits>
 
@@ -167,7 +166,8 @@ static void td_levels(const DeviceDag* d, u32 C, u64* row, u32 per_file = 1) {
        d->n_rs, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row);
   // all levels in one persistent launch, grid barriers between levels
   seg_reduce_levels<Mode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
-                          d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrc{row, C}, TdRows{row, C}, st);
+                          d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrc{row, C}, TdRows{row, C}, st, false,
+                          d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0);
 }
 
 // Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
