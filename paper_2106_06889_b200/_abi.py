@@ -59,6 +59,7 @@ class GtInfo(C.Structure):
         ("device_bytes", C.c_uint64),
         ("init_ms", C.c_double),
         ("td_edges", C.c_uint64),
+        ("load_flags", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

@@ -172,6 +172,7 @@ int gt_info_get(const gt_ctx* c, gt_info* o) {
   o->device_bytes = d.bytes_held();
   o->init_ms = d.init_ms;
   o->td_edges = d.te_off.empty() ? 0 : d.te_off.back();
+  o->load_flags = d.load_flags;
   return GT_OK;
 }
 
@@ -182,10 +183,11 @@ void gt_close(gt_ctx* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t s = c->d.stream;
+  const int dev = c->d.device;
   delete c;  // DBuf destructors free on the stream
   if (s) {
     cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
+    stream_release(dev, s);
   }
 }
 

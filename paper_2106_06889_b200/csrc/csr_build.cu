@@ -1,0 +1,379 @@
+// csr_build.cu — per-rule (symbol, multiplicity) lists: the own / sub CSR of
+// dag.py:131-230 (own_ids/own_freqs: distinct words of a body with their
+// counts, ascending; sub_ids/sub_freqs: distinct child rules) built without a
+// global sort of the grammar.
+//
+// Bodies are contiguous per rule, so the (rule, symbol) order only needs each
+// body sorted by symbol.  Sequitur bodies are short (digram rules: 2 symbols;
+// the composed configs: <= 6), so
+//   * bodies of <= 32 symbols (all but a handful of rules) are sorted in
+//     registers by one thread with a bitonic network and run-length encoded
+//     on the spot;
+//   * bodies of 33..kGiant symbols go through a segmented sort (CUB, only
+//     those segments), bodies above kGiant (typically the root of a
+//     many-file corpus) through one radix sort of their (rule, symbol) keys;
+//     their runs are then found element-parallel (head flags, select).
+// Every rule writes its runs in place at its body offset (own words first,
+// then the child rules: words sort below splitters below rules), the per-rule
+// counts are scanned into own_off / sub_off directly, and one element-
+// parallel pass compacts the runs into the CSR arrays.  own_tok (words in a
+// body) and num_out (child references) fall out of the same pass.
+#include <algorithm>
+
+#include "kernels_common.cuh"
+
+namespace gt {
+
+constexpr u32 kShort = 32;
+constexpr u64 kGiant = 4096;  // above: one device-wide radix sort (a block-per-segment sort of 10^5 is slow)
+
+template <int N>
+__device__ __forceinline__ void bitonic_sort(u32 (&v)[N]) {
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < N; i++) {
+        const int l = i ^ j;
+        if (l > i) {
+          const u32 a = v[i], b = v[l];
+          const u32 lo = a < b ? a : b, hi = a < b ? b : a;
+          if ((i & k) == 0) {
+            v[i] = lo;
+            v[l] = hi;
+          } else {
+            v[i] = hi;
+            v[l] = lo;
+          }
+        }
+      }
+}
+
+struct RunOut {
+  u32* tsym;
+  u32* tcnt;
+  u64 nw, base;
+  u32 no = 0, nsu = 0;
+  u64 otok = 0, nout = 0;
+  u64 at;  // body offset of the rule
+  __device__ __forceinline__ void emit(u32 sym, u32 c) {
+    if (sym < nw) {
+      tsym[at + no] = sym;
+      tcnt[at + no] = c;
+      no++;
+      otok += c;
+    } else if (sym >= base) {
+      tsym[at + no + nsu] = (u32)(sym - base);
+      tcnt[at + no + nsu] = c;
+      nsu++;
+      nout += c;
+    }  // splitters (root only) are neither
+  }
+};
+
+template <int N>
+__device__ __forceinline__ void short_rule(const u32* __restrict__ body, u64 b, u32 len, RunOut& o) {
+  u32 v[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) v[i] = (u32)i < len ? body[b + i] : 0xFFFFFFFFu;
+  bitonic_sort<N>(v);
+  u32 cur = v[0], c = 1;
+#pragma unroll
+  for (int i = 1; i < N; i++) {
+    if ((u32)i < len) {
+      if (v[i] == cur) {
+        c++;
+      } else {
+        o.emit(cur, c);
+        cur = v[i];
+        c = 1;
+      }
+    }
+  }
+  o.emit(cur, c);
+}
+
+// one thread per rule: short bodies done here; longer ones flagged
+// (lflag: 1 = segmented sort, 2 = giant)
+__global__ void k_rules_short(const u32* __restrict__ body, const u64* __restrict__ boff, u64 R, u64 nw, u64 base,
+                              u32* tsym, u32* tcnt, u32* n_own, u32* n_sub, u64* own_tok, u64* num_out,
+                              uint8_t* lflag) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
+    const u64 b = boff[r], len = boff[r + 1] - b;
+    RunOut o{tsym, tcnt, nw, base};
+    o.at = b;
+    uint8_t f = 0;
+    if (len == 0) {
+    } else if (len <= 4) {
+      short_rule<4>(body, b, (u32)len, o);
+    } else if (len <= 8) {
+      short_rule<8>(body, b, (u32)len, o);
+    } else if (len <= 16) {
+      short_rule<16>(body, b, (u32)len, o);
+    } else if (len <= kShort) {
+      short_rule<32>(body, b, (u32)len, o);
+    } else {
+      f = len > kGiant ? 2 : 1;
+    }
+    lflag[r] = f;
+    n_own[r] = o.no;
+    n_sub[r] = o.nsu;
+    own_tok[r] = o.otok;
+    num_out[r] = o.nout;
+  }
+}
+
+__global__ void k_eq_u8(const uint8_t* a, u64 n, uint8_t v, uint8_t* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = a[i] == v;
+}
+
+__global__ void k_giant_elems(const u32* __restrict__ owner, const uint8_t* __restrict__ lflag, u64 E,
+                              uint8_t* gflag) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += stride) gflag[p] = lflag[owner[p]] == 2;
+}
+
+__global__ void k_seg_bounds(const u32* __restrict__ ids, u64 n, const u64* __restrict__ boff, int* beg, int* end) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 r = ids[i];
+    beg[i] = (int)boff[r];
+    end[i] = (int)boff[r + 1];
+  }
+}
+
+__global__ void k_scatter_rank(const u32* __restrict__ ids, u64 n, u32* rank) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) rank[ids[i]] = (u32)i;
+}
+
+// key = (rank of the giant rule, symbol): log2(#giants) + SB bits, so a
+// single giant (the usual root) sorts on the symbol bits alone
+__global__ void k_giant_keys(const u32* __restrict__ pos, u64 n, const u32* __restrict__ owner,
+                             const u32* __restrict__ grank, const u32* __restrict__ body, int SB, u64* key) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 p = pos[i];
+    key[i] = ((u64)grank[owner[p]] << SB) | body[p];
+  }
+}
+
+// the sorted keys of the giant rules go back to their (contiguous, rule-
+// ordered) positions
+__global__ void k_giant_scatter(const u64* __restrict__ key, const u32* __restrict__ pos, u64 n, int SB, u32* sbody) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 m = (1ull << SB) - 1;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) sbody[pos[i]] = (u32)(key[i] & m);
+}
+
+__global__ void k_long_heads(const u32* __restrict__ owner, const uint8_t* __restrict__ lflag,
+                             const u64* __restrict__ boff, const u32* __restrict__ sbody, u64 E, uint8_t* head) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += stride) {
+    const u32 r = owner[p];
+    head[p] = lflag[r] && (p == boff[r] || sbody[p - 1] != sbody[p]);
+  }
+}
+
+// warp segmented sum over lanes with equal ascending keys; true on the last
+// lane of each key run
+__device__ __forceinline__ bool warp_key_sum(u32 key, u64& v) {
+  const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, s);
+    const u32 ok = __shfl_up_sync(0xFFFFFFFFu, key, s);
+    if (lane >= (unsigned)s && ok == key) v += ov;
+  }
+  const u32 nk = __shfl_down_sync(0xFFFFFFFFu, key, 1);
+  return lane == 31 || nk != key;
+}
+
+struct LongRun {
+  u32 r, sym, cnt;
+  bool ok;
+};
+
+__device__ __forceinline__ LongRun long_run(u64 u, u64 nh, const u32* hidx, const u32* owner, const u64* boff,
+                                            const u32* sbody) {
+  LongRun x{0xFFFFFFFFu, 0, 0, false};
+  if (u >= nh) return x;
+  const u32 j = hidx[u];
+  x.r = owner[j];
+  const u64 nx = (u + 1 < nh && owner[hidx[u + 1]] == x.r) ? hidx[u + 1] : boff[x.r + 1];
+  x.cnt = (u32)(nx - j);
+  x.sym = sbody[j];
+  x.ok = true;
+  return x;
+}
+
+// per long rule: runs by class (own / splitter / sub), symbol totals, and the
+// index of its first run
+__global__ void k_long_count(const u32* __restrict__ hidx, const u64* __restrict__ nh_d,
+                             const u32* __restrict__ owner, const u64* __restrict__ boff,
+                             const u32* __restrict__ sbody, u64 nw, u64 base, u32* n_own, u32* n_sub, u32* n_spl,
+                             u64* own_tok, u64* num_out, u32* rfirst) {
+  const u64 nh = *nh_d;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 b0 = (u64)blockIdx.x * blockDim.x; b0 < nh; b0 += stride) {
+    const u64 u = b0 + threadIdx.x;
+    const LongRun x = long_run(u, nh, hidx, owner, boff, sbody);
+    if (x.ok && hidx[u] == boff[x.r]) rfirst[x.r] = (u32)u;
+    const bool own = x.ok && x.sym < nw, sub = x.ok && x.sym >= base, spl = x.ok && !own && !sub;
+    u64 a = own, b = sub, c = spl, t = own ? x.cnt : 0, o = sub ? x.cnt : 0;
+    bool last = warp_key_sum(x.r, a);
+    warp_key_sum(x.r, b);
+    warp_key_sum(x.r, c);
+    warp_key_sum(x.r, t);
+    warp_key_sum(x.r, o);
+    if (x.ok && last) {
+      if (a) atomicAdd(&n_own[x.r], (u32)a);
+      if (b) atomicAdd(&n_sub[x.r], (u32)b);
+      if (c) atomicAdd(&n_spl[x.r], (u32)c);
+      if (t) atomicAdd((unsigned long long*)&own_tok[x.r], (unsigned long long)t);
+      if (o) atomicAdd((unsigned long long*)&num_out[x.r], (unsigned long long)o);
+    }
+  }
+}
+
+__global__ void k_long_write(const u32* __restrict__ hidx, const u64* __restrict__ nh_d,
+                             const u32* __restrict__ owner, const u64* __restrict__ boff,
+                             const u32* __restrict__ sbody, u64 nw, u64 base, const u32* __restrict__ n_spl,
+                             const u32* __restrict__ rfirst, u32* tsym, u32* tcnt) {
+  const u64 nh = *nh_d;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < nh; u += stride) {
+    const LongRun x = long_run(u, nh, hidx, owner, boff, sbody);
+    const u64 k = u - rfirst[x.r], at = boff[x.r];
+    if (x.sym < nw) {
+      tsym[at + k] = x.sym;
+      tcnt[at + k] = x.cnt;
+    } else if (x.sym >= base) {
+      tsym[at + k - n_spl[x.r]] = (u32)(x.sym - base);
+      tcnt[at + k - n_spl[x.r]] = x.cnt;
+    }
+  }
+}
+
+__global__ void k_widen_u32(const u32* a, u64 n, u64* b) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) b[i] = i < n ? a[i] : 0;
+}
+
+// element-parallel compaction of the in-place runs into the CSR arrays
+__global__ void k_rules_compact(const u32* __restrict__ owner, const u64* __restrict__ boff, u64 E,
+                                const u32* __restrict__ n_own, const u32* __restrict__ n_sub,
+                                const u64* __restrict__ own_off, const u64* __restrict__ sub_off,
+                                const u32* __restrict__ tsym, const u32* __restrict__ tcnt, u32* own_ids,
+                                u32* own_freqs, u32* own_rule, u32* sub_ids, u32* sub_freqs, u32* sub_rule) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < E; p += stride) {
+    const u32 r = owner[p];
+    const u64 k = p - boff[r];
+    const u32 no = n_own[r];
+    if (k < no) {
+      const u64 i = own_off[r] + k;
+      own_ids[i] = tsym[p];
+      own_freqs[i] = tcnt[p];
+      own_rule[i] = r;
+    } else if (k < (u64)no + n_sub[r]) {
+      const u64 i = sub_off[r] + (k - no);
+      sub_ids[i] = tsym[p];
+      sub_freqs[i] = tcnt[p];
+      sub_rule[i] = r;
+    }
+  }
+}
+
+#define CK(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
+
+void build_rule_pairs(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_rule, cudaStream_t st) {
+  const u64 R = d->R, E = d->E, nw = d->nw, base = d->nw + d->ns;
+  const u32* body = d->body.as<u32>();
+  const u64* boff = d->boff.as<u64>();
+  DBuf tsym(E * 4 + 4, st), tcnt(E * 4 + 4, st), n_own(R * 4 + 4, st), n_sub(R * 4 + 4, st), lflag(R + 1, st);
+  d->own_tok.alloc(R * 8, st);
+  d->num_out.alloc(R * 8, st);
+  CK(k_rules_short, R, body, boff, R, nw, base, tsym.as<u32>(), tcnt.as<u32>(), n_own.as<u32>(), n_sub.as<u32>(),
+     d->own_tok.as<u64>(), d->num_out.as<u64>(), lflag.as<uint8_t>());
+  // the longer bodies: one host round trip for their number and size
+  DBuf gflag(E + 1, st), lids(R * 4 + 4, st), gids(R * 4 + 4, st), gpos(E * 4 + 4, st), cnt(32, st);
+  {
+    DBuf medf(R + 1, st);
+    CK(k_eq_u8, R, lflag.as<uint8_t>(), R, (uint8_t)1, medf.as<uint8_t>());
+    select_flagged_index(medf.as<uint8_t>(), lids.as<u32>(), cnt.as<u64>(), R, st);
+    CK(k_eq_u8, R, lflag.as<uint8_t>(), R, (uint8_t)2, medf.as<uint8_t>());
+    select_flagged_index(medf.as<uint8_t>(), gids.as<u32>(), cnt.as<u64>() + 3, R, st);
+  }
+  CK(k_giant_elems, E, owner, lflag.as<uint8_t>(), E, gflag.as<uint8_t>());
+  select_flagged_index(gflag.as<uint8_t>(), gpos.as<u32>(), cnt.as<u64>() + 1, E, st);
+  gflag.release();
+  u64 h[4];
+  GT_CUDA(cudaMemcpyAsync(h, cnt.p, 32, cudaMemcpyDeviceToHost, st));
+  stream_sync(st);
+  const u64 nmed = h[0], ngel = h[1], ngiant = h[3];
+  DBuf n_spl, rfirst;
+  if (nmed || ngel) {
+    DBuf sbody(E * 4 + 4, st);
+    if (nmed) {
+      DBuf beg(nmed * 4, st), end(nmed * 4, st);
+      CK(k_seg_bounds, nmed, lids.as<u32>(), nmed, boff, beg.as<int>(), end.as<int>());
+      sort_segments_listed_u32(body, sbody.as<u32>(), E, nmed, beg.as<int>(), end.as<int>(), st);
+    }
+    if (ngel) {
+      const int SB = std::max(1, bitlen(d->nw + d->ns + R - 1));
+      const int KB = SB + bitlen(ngiant - 1);
+      DBuf k1(ngel * 8, st), k2(ngel * 8, st), grank(R * 4 + 4, st);
+      CK(k_scatter_rank, ngiant, gids.as<u32>(), ngiant, grank.as<u32>());
+      CK(k_giant_keys, ngel, gpos.as<u32>(), ngel, owner, grank.as<u32>(), body, SB, k1.as<u64>());
+      sort_keys_u64(k1.as<u64>(), k2.as<u64>(), ngel, KB, st);
+      CK(k_giant_scatter, ngel, k2.as<u64>(), gpos.as<u32>(), ngel, SB, sbody.as<u32>());
+    }
+    DBuf head(E + 1, st), hidx(E * 4 + 4, st);
+    CK(k_long_heads, E, owner, lflag.as<uint8_t>(), boff, sbody.as<u32>(), E, head.as<uint8_t>());
+    select_flagged_index(head.as<uint8_t>(), hidx.as<u32>(), cnt.as<u64>() + 2, E, st);
+    head.release();
+    n_spl.alloc(R * 4 + 4, st);
+    rfirst.alloc(R * 4 + 4, st);
+    GT_CUDA(cudaMemsetAsync(n_spl.p, 0, R * 4 + 4, st));
+    CK(k_long_count, E, hidx.as<u32>(), cnt.as<u64>() + 2, owner, boff, sbody.as<u32>(), nw, base,
+       n_own.as<u32>(), n_sub.as<u32>(), n_spl.as<u32>(), d->own_tok.as<u64>(), d->num_out.as<u64>(),
+       rfirst.as<u32>());
+    CK(k_long_write, E, hidx.as<u32>(), cnt.as<u64>() + 2, owner, boff, sbody.as<u32>(), nw, base,
+       n_spl.as<u32>(), rfirst.as<u32>(), tsym.as<u32>(), tcnt.as<u32>());
+  }
+  lids.release();
+  gids.release();
+  gpos.release();
+  // per-rule counts -> CSR offsets (no search: the scan IS the offsets)
+  {
+    DBuf wide((R + 1) * 8, st);
+    d->own_off.alloc((R + 1) * 8, st);
+    d->sub_off.alloc((R + 1) * 8, st);
+    CK(k_widen_u32, R + 1, n_own.as<u32>(), R, wide.as<u64>());
+    exclusive_scan_u64(wide.as<u64>(), d->own_off.as<u64>(), R + 1, st);
+    CK(k_widen_u32, R + 1, n_sub.as<u32>(), R, wide.as<u64>());
+    exclusive_scan_u64(wide.as<u64>(), d->sub_off.as<u64>(), R + 1, st);
+  }
+  u64 tot[2];
+  GT_CUDA(cudaMemcpyAsync(&tot[0], d->own_off.as<u64>() + R, 8, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(&tot[1], d->sub_off.as<u64>() + R, 8, cudaMemcpyDeviceToHost, st));
+  stream_sync(st);
+  d->E_own = tot[0];
+  d->E_sub = tot[1];
+  const u64 Eo = tot[0], Es = tot[1];
+  d->own_ids.alloc(Eo * 4 + 4, st);
+  d->own_freqs.alloc(Eo * 4 + 4, st);
+  own_rule.alloc(Eo * 4 + 4, st);
+  d->sub_ids.alloc(Es * 4 + 4, st);
+  d->sub_freqs.alloc(Es * 4 + 4, st);
+  sub_rule.alloc(Es * 4 + 4, st);
+  CK(k_rules_compact, E, owner, boff, E, n_own.as<u32>(), n_sub.as<u32>(), d->own_off.as<u64>(),
+     d->sub_off.as<u64>(), tsym.as<u32>(), tcnt.as<u32>(), d->own_ids.as<u32>(), d->own_freqs.as<u32>(),
+     own_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), sub_rule.as<u32>());
+}
+
+}  // namespace gt

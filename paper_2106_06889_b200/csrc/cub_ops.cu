@@ -33,6 +33,20 @@ void sort_pairs_u32_u32(u32* ki, u32* ko, u32* vi, u32* vo, u64 n, int end_bit, 
   }, s);
 }
 
+void sort_pairs_u32_u64(u32* ki, u32* ko, u64* vi, u64* vo, u64 n, int end_bit, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::SortPairs32x64", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceRadixSort::SortPairs(t, b, ki, ko, vi, vo, (int64_t)n, 0, end_bit, s));
+  }, s);
+}
+
+void sort_pairs_u32_u3(u32* ki, u32* ko, U3* vi, U3* vo, u64 n, int end_bit, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::SortPairs32x96", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceRadixSort::SortPairs(t, b, ki, ko, vi, vo, (int64_t)n, 0, end_bit, s));
+  }, s);
+}
+
 void sort_keys_u64(u64* ki, u64* ko, u64 n, int end_bit, cudaStream_t s) {
   if (!n) return;
   with_temp("cub::SortKeys64", [&](void* t, size_t& b) {
@@ -89,6 +103,16 @@ void sort_segments_u32(const u32* ki, u32* ko, u64 n, u64 nseg, const u64* off, 
   if (!n) return;
   with_temp("cub::SegmentedSort32", [&](void* t, size_t& b) {
     GT_CUDA(cub::DeviceSegmentedSort::SortKeys(t, b, ki, ko, (int)n, (int)nseg, off, off + 1, s));
+  }, s);
+}
+
+// sort the listed segments [beg[i], end[i]) of ki into ko (other positions of
+// ko are left undefined)
+void sort_segments_listed_u32(const u32* ki, u32* ko, u64 n, u64 nseg, const int* beg, const int* end,
+                              cudaStream_t s) {
+  if (!n || !nseg) return;
+  with_temp("cub::SegmentedSort32", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceSegmentedSort::SortKeys(t, b, ki, ko, (int)n, (int)nseg, beg, end, s));
   }, s);
 }
 

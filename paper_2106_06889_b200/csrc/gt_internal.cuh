@@ -125,6 +125,7 @@ struct DeviceDag {
   DBuf be_rule, be_child, be_freq;
   std::vector<u64> be_off;  // host: bu level L items [be_off[L], be_off[L+1])
   DBuf be_off_dev;
+  u64 load_flags = 0;  // gt_info.load_flags
   double init_ms = 0;
   // scratch kept across runs
   DBuf word_counts;  // u64[V] of the last global run
@@ -163,6 +164,15 @@ void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 
 void reduce_max_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
 // sort the keys of each segment [off[i], off[i+1]) independently (n < 2^31)
 void sort_segments_u32(const u32* keys_in, u32* keys_out, u64 n, u64 nseg, const u64* off, cudaStream_t s);
+struct U3 {
+  u32 a, b, c;
+};
+void sort_pairs_u32_u64(u32* ki, u32* ko, u64* vi, u64* vo, u64 n, int end_bit, cudaStream_t s);
+void sort_pairs_u32_u3(u32* ki, u32* ko, U3* vi, U3* vo, u64 n, int end_bit, cudaStream_t s);
+void sort_segments_listed_u32(const u32* ki, u32* ko, u64 n, u64 nseg, const int* beg, const int* end,
+                              cudaStream_t s);
+struct DeviceDag;
+void build_rule_pairs(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_rule, cudaStream_t st);
 void sort_pairs_u64_u64(u64* keys_in, u64* keys_out, u64* vals_in, u64* vals_out, u64 n, int end_bit,
                         cudaStream_t s);
 // runs of equal keys (sorted input) -> unique keys, sums, run count (device)
@@ -200,21 +210,100 @@ struct ProfScope {
     ::gt::g_launches++;                                \
   } while (0)
 
-// GT_TRACE=1: synchronising phase timer on stderr (diagnostics only)
+// Per-device pool of non-blocking streams: creating and destroying a stream
+// costs ~100 us of host time (tools/api_cost.cu), more than a small grammar's
+// whole traversal, so contexts and the loader's helper streams reuse them.
+// A stream is released idle (synchronised) and may serve any later context.
+cudaStream_t stream_acquire(int device);
+void stream_release(int device, cudaStream_t s);
+
+// host-side stream sync; under GT_TRACE=2 the time the calling thread spent
+// waiting is accumulated (Phases prints it: wall - wait = host work)
+struct SyncStats {
+  double wait_ms = 0, alloc_ms = 0;
+  int n = 0, nalloc = 0, nfree = 0;
+  u64 launches0 = 0;
+};
+inline SyncStats& sync_stats() {
+  static thread_local SyncStats s;
+  return s;
+}
+inline void stream_sync(cudaStream_t s) {
+  static const bool tr = getenv("GT_TRACE") && atoi(getenv("GT_TRACE")) == 2;
+  if (!tr) {
+    GT_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  auto a = std::chrono::steady_clock::now();
+  GT_CUDA(cudaStreamSynchronize(s));
+  sync_stats().wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  sync_stats().n++;
+}
+
+// GT_TRACE=1: synchronising phase timer on stderr (diagnostics only).
+// GT_TRACE=2: non-intrusive timeline: at each mark the host time and a
+// stream event are recorded without a sync; printed at destruction as
+// (host ms, device ms) since construction — device > host means the GPU
+// was the bottleneck up to that point, host >> device means it sat idle.
 struct Phases {
-  bool on;
+  int mode;
   const char* tag;
   cudaStream_t st = nullptr;
-  std::chrono::steady_clock::time_point t;
+  std::chrono::steady_clock::time_point t, t0;
+  cudaEvent_t e0 = nullptr;
+  struct Mark {
+    const char* what;
+    double host_ms;
+    cudaEvent_t ev;
+  };
+  std::vector<Mark> marks;
   explicit Phases(const char* tg, cudaStream_t s = nullptr)
-      : on(getenv("GT_TRACE") && getenv("GT_TRACE")[0] != '0'), tag(tg), st(s),
-        t(std::chrono::steady_clock::now()) {}
+      : mode(getenv("GT_TRACE") ? atoi(getenv("GT_TRACE")) : 0), tag(tg), st(s),
+        t(std::chrono::steady_clock::now()), t0(t) {
+    if (mode == 2 && st) {
+      cudaEventCreate(&e0);
+      cudaEventRecord(e0, st);
+    }
+  }
+  void bind(cudaStream_t s) {
+    st = s;
+    t0 = t = std::chrono::steady_clock::now();
+    if (mode == 2 && !e0) {
+      cudaEventCreate(&e0);
+      cudaEventRecord(e0, st);
+      sync_stats() = SyncStats{};
+      sync_stats().launches0 = g_launches;
+    }
+  }
   void mark(const char* what) {
-    if (!on) return;
-    if (st) cudaStreamSynchronize(st);
+    if (!mode) return;
     auto n = std::chrono::steady_clock::now();
+    if (mode == 2) {
+      if (!st) return;
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      cudaEventRecord(ev, st);
+      marks.push_back({what, std::chrono::duration<double, std::milli>(n - t0).count(), ev});
+      return;
+    }
+    if (st) cudaStreamSynchronize(st);
+    n = std::chrono::steady_clock::now();
     fprintf(stderr, "[%s] %-28s %9.3f ms\n", tag, what, std::chrono::duration<double, std::milli>(n - t).count());
     t = n;
+  }
+  ~Phases() {
+    if (mode != 2 || !e0) return;
+    cudaEventSynchronize(marks.empty() ? e0 : marks.back().ev);
+    for (auto& m : marks) {
+      float dm = 0;
+      cudaEventElapsedTime(&dm, e0, m.ev);
+      fprintf(stderr, "[%s] %-28s host %8.3f ms  device %8.3f ms\n", tag, m.what, m.host_ms, dm);
+      cudaEventDestroy(m.ev);
+    }
+    fprintf(stderr, "[%s] host waited %.3f ms in %d syncs; %d allocs + %d frees took %.3f ms; %llu launches\n", tag,
+            sync_stats().wait_ms, sync_stats().n, sync_stats().nalloc, sync_stats().nfree, sync_stats().alloc_ms,
+            (unsigned long long)(g_launches - sync_stats().launches0));
+    cudaEventDestroy(e0);
   }
 };
 

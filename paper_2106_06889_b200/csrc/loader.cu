@@ -38,15 +38,37 @@ namespace gt {
 
 thread_local u64 g_launches = 0;
 
+static bool trace2() {
+  static const bool v = getenv("GT_TRACE") && atoi(getenv("GT_TRACE")) == 2;
+  return v;
+}
+
 void DBuf::alloc(size_t n, cudaStream_t st) {
   release();
   s = st;
   bytes = n;
-  if (n) GT_CUDA(cudaMallocAsync(&p, n, st));
+  if (!n) return;
+  if (!trace2()) {
+    GT_CUDA(cudaMallocAsync(&p, n, st));
+    return;
+  }
+  auto a = std::chrono::steady_clock::now();
+  GT_CUDA(cudaMallocAsync(&p, n, st));
+  sync_stats().alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  sync_stats().nalloc++;
 }
 
 void DBuf::release() {
-  if (p) cudaFreeAsync(p, s);
+  if (p) {
+    if (!trace2()) {
+      cudaFreeAsync(p, s);
+    } else {
+      auto a = std::chrono::steady_clock::now();
+      cudaFreeAsync(p, s);
+      sync_stats().alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+      sync_stats().nfree++;
+    }
+  }
   p = nullptr;
   bytes = 0;
 }
@@ -61,6 +83,48 @@ __global__ void k_csr_offsets(const u32* key, u64 n, u64 R, u64* off) {
       else hi = m;
     }
     off[r] = lo;
+  }
+}
+
+// CSR row offsets of a sorted key list in one coalesced pass: element i
+// writes the offsets of the rows (key[i-1], key[i]] (O(n + R); the binary
+// search above is kept for a handful of rows over long lists)
+__global__ void k_csr_offsets_lin(const u32* __restrict__ key, u64 n, u64 R, u64* off) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) {
+    const u64 lo = i == 0 ? 0 : (u64)key[i - 1] + 1;
+    const u64 hi = i == n ? R : (u64)key[i];
+    for (u64 r = lo; r <= hi; r++) off[r] = i;
+  }
+}
+
+__global__ void k_pack2(const u32* __restrict__ a, const u32* __restrict__ b, u64 n, u64* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = ((u64)a[i] << 32) | b[i];
+}
+
+__global__ void k_unpack2(const u64* __restrict__ in, u64 n, u32* a, u32* b) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u64 v = in[i];
+    a[i] = (u32)(v >> 32);
+    b[i] = (u32)v;
+  }
+}
+
+__global__ void k_pack3(const u32* __restrict__ a, const u32* __restrict__ b, const u32* __restrict__ c, u64 n,
+                        U3* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = U3{a[i], b[i], c[i]};
+}
+
+__global__ void k_unpack3(const U3* __restrict__ in, u64 n, u32* a, u32* b, u32* c) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const U3 v = in[i];
+    a[i] = v.a;
+    b[i] = v.b;
+    c[i] = v.c;
   }
 }
 
@@ -300,6 +364,147 @@ __global__ void k_chain_check(const u32* pos, const u32* raw, u64 R, u64 n, u32*
   }
 }
 
+// ---- rule-chain parse, chunked form (the common case) ----------------------
+// After the root record the section is cut into chunks of kChunkB words.
+// If every non-root record is shorter than kWin words, the chain enters
+// chunk c at one of its first kWin words, so each chunk is summarised by a
+// kWin-entry table: entry offset -> (entry offset into chunk c+1, records
+// started in c) — one warp per chunk, one lane per candidate entry, walking
+// the chunk through L1.  Pointer doubling then runs over chunk STATES
+// (nchunks*kWin + END, ~n/32 of them, log2(nchunks) passes) instead of over
+// every word of the section (log2(R) passes over n words), and a final walk
+// per chunk writes the rule starts.  A table entry that would need a wider
+// window is INVALID; if the true chain meets one (a record of >= kWin words
+// other than the root) or the section is malformed, the word-level doubling
+// above runs instead, and after it the host walk for the exact error.
+constexpr u32 kChunkB = 1024, kWin = 32, kStInvalid = 0xFFFFFFFFu;
+constexpr u32 kMaskW = kChunkB / 32;  // 32-bit words of one candidate's start mask
+
+// one warp per chunk: lane o walks the chain from entry offset o, records its
+// exit state and record count, and marks the record starts it visits in a
+// 1024-bit mask (shared memory, then stored so that the final pass only reads
+// the mask of the true entry)
+constexpr int kTabWarps = 8;
+__global__ void __launch_bounds__(kTabWarps * 32) k_chunk_tables(const u32* __restrict__ raw, u64 n, u64 p1,
+                                                                  u64 nch, u32* nxt, u32* cnt, u32* mask) {
+  __shared__ u32 sm[kTabWarps][kWin][kMaskW + 1];
+  const u32 wib = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const u64 warp = (u64)blockIdx.x * kTabWarps + wib;
+  const u64 nwarps = (u64)gridDim.x * kTabWarps;
+  const u32 END = (u32)(nch * kWin);
+  u32(*m)[kMaskW + 1] = sm[wib];
+  for (u64 c = warp; c < nch; c += nwarps) {
+    for (u32 w = 0; w < kMaskW; w++) m[lane][w] = 0;
+    const u64 cs = p1 + c * kChunkB, ce = cs + kChunkB < n ? cs + kChunkB : n;
+    u64 p = cs + lane;
+    u32 k = 0, state;
+    if (p >= ce) {
+      state = kStInvalid;  // an entry past the end of a short last chunk
+    } else {
+      while (p < ce) {
+        const u32 o = (u32)(p - cs);
+        m[lane][o >> 5] |= 1u << (o & 31u);
+        k++;
+        p += 1 + (u64)raw[p];
+      }
+      if (p >= n) state = p == n ? END : kStInvalid;
+      else state = p - ce < kWin ? (u32)((c + 1) * kWin + (p - ce)) : kStInvalid;
+    }
+    nxt[c * kWin + lane] = state;
+    cnt[c * kWin + lane] = k;
+    __syncwarp();
+    u32* mg = mask + c * (u64)(kWin * kMaskW);
+    for (u32 r = 0; r < kWin; r++) mg[r * kMaskW + lane] = m[r][lane];  // row r = candidate r, coalesced
+    __syncwarp();
+  }
+  if (warp == 0 && lane == 0) {
+    nxt[END] = END;
+    cnt[END] = 0;
+  }
+}
+
+// all doubling levels in one cooperative launch: J_k = J_{k-1} o J_{k-1}
+// over the chunk states (counts summed; INVALID absorbs)
+__global__ void k_state_double_all(u32* nx, u32* ct, u64 S, int K) {
+  cg::grid_group grid = cg::this_grid();
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (int k = 1; k < K; k++) {
+    const u32* a_nx = nx + (u64)(k - 1) * S;
+    const u32* a_ct = ct + (u64)(k - 1) * S;
+    u32* b_nx = nx + (u64)k * S;
+    u32* b_ct = ct + (u64)k * S;
+    for (u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += stride) {
+      const u32 a = __ldcg(a_nx + s);
+      if (a == kStInvalid) {
+        b_nx[s] = kStInvalid;
+        b_ct[s] = 0;
+      } else {
+        b_nx[s] = __ldcg(a_nx + a);
+        b_ct[s] = __ldcg(a_ct + s) + __ldcg(a_ct + a);
+      }
+    }
+    grid.sync();
+  }
+}
+
+// the state of the chain after c chunk steps from (chunk 0, offset 0) and the
+// records started before chunk c; c == nch checks the end of the section
+__global__ void k_chunk_entry(const u32* __restrict__ nx, const u32* __restrict__ ct, u64 S, int K, u64 nch,
+                              u64 R, u32* entry, u32* base, u32* bad) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  const u32 END = (u32)(nch * kWin);
+  for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c <= nch; c += stride) {
+    u32 st = 0;
+    u64 b = 0;
+    for (int k = K - 1; k >= 0 && st != kStInvalid; k--)
+      if ((c >> k) & 1) {
+        b += ct[(u64)k * S + st];
+        st = nx[(u64)k * S + st];
+      }
+    if (c == nch) {
+      if (st != END || b != R - 1) *bad = 1;
+    } else if (st == kStInvalid || (st != END && st / kWin != c)) {
+      *bad = 1;
+    } else {
+      entry[c] = st;
+      base[c] = (u32)b;
+    }
+  }
+}
+
+// rule starts from the true entry's mask: one warp per chunk, lane w expands
+// mask word w at its popcount prefix.  Runs before the host sees the check:
+// indices are bounded by R so that a failed parse only leaves rstart to be
+// overwritten by the fallback.
+__global__ void k_chunk_starts(u64 p1, u64 nch, u64 R, const u32* entry, const u32* base, const u32* mask,
+                               u32* rstart) {
+  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u32 lane = threadIdx.x & 31u;
+  const u32 END = (u32)(nch * kWin);
+  for (u64 c = warp; c < nch; c += nwarps) {
+    const u32 st = entry[c];
+    if (st == END) continue;
+    u32 bits = mask[c * (u64)(kWin * kMaskW) + (u64)(st % kWin) * kMaskW + lane];
+    const u32 pc = __popc(bits);
+    u32 pre = pc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 o = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+      if (lane >= (u32)d) pre += o;
+    }
+    u64 i = 1 + (u64)base[c] + pre - pc;
+    const u64 pos0 = p1 + c * kChunkB + lane * 32u;
+    while (bits) {
+      const u32 b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (i < R) rstart[i] = (u32)(pos0 + b + 1);
+      i++;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) rstart[0] = 1;
+}
+
 __global__ void k_boff(const u32* rstart, u64 R, u64 E, u64* boff) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= R; i += stride)
@@ -382,23 +587,15 @@ __global__ void k_gather3(const u32* idx, u64 n, const u32* a, const u32* b, con
   }
 }
 
-// distinct children / non-root parents counters; root-parent flag
-__global__ void k_degrees(const u64* sub_off, const u64* par_off, const u32* par_ids, u64 R,
-                          u32* rem_bu, u32* rem_td, uint8_t* root_parent) {
+// non-root parent counters; root-parent flag
+__global__ void k_degrees(const u64* par_off, const u32* par_ids, u64 R, u32* rem_td, uint8_t* root_parent) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
-    rem_bu[r] = (u32)(sub_off[r + 1] - sub_off[r]);
     u64 np = par_off[r + 1] - par_off[r];
     bool rp = np && par_ids[par_off[r]] == 0;
     root_parent[r] = rp;
     rem_td[r] = (u32)(np - (rp ? 1 : 0));
   }
-}
-
-__global__ void k_flag_zero(const u32* rem, u64 R, u64 first, uint8_t* flag) {
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride)
-    flag[r] = (r >= first) && rem[r] == 0;
 }
 
 // Warp-aggregated "decrement and detect completion": lanes hitting the same
@@ -417,35 +614,25 @@ __device__ __forceinline__ bool dec_to_zero(u32* rem, u32 key, bool active) {
 }
 
 // ---------------------------------------------------------------------------
-// Persistent Kahn layering: ONE cooperative launch runs every layer, frontier
-// counts live on the device, layers are separated by grid barriers (no host
-// round trip per layer).  Bottom-up (TD = false): frontier = rules whose
-// children all finished, edges = parents (par CSR).  Top-down (TD = true):
-// frontier = rules whose non-root parents all finished, edges = children
-// (sub CSR), reachability from the root carried along.  A rule with more
-// than kLight edges is split into chunk tasks of kChunk edges that every
-// warp of the grid shares after a second barrier (a rule with 10^6 parents
-// is never one warp's serial loop).
+// Persistent top-down Kahn layering: ONE cooperative launch runs every layer,
+// layers separated by grid barriers (no host round trip per layer).  The
+// frontier of layer L is a BITMAP of rules (bit set by the edge that took a
+// rule's counter of non-root parents to zero during layer L-1, with a
+// fire-and-forget atomicOr): warps scan it 1024 rules per step and deal the
+// set bits to lanes, so no frontier queue, no counter atomic with return on
+// the append path.  Reachability from the root is pushed along the edges
+// (reach[child] = 1 from a reached parent, a plain byte store) and is final
+// when the child's counter reaches zero.  A rule with more than kLight
+// children is split into chunk tasks of kChunk edges that every warp of the
+// grid shares after a second barrier (a rule with 10^6 children is never
+// one warp's serial loop).
 // ---------------------------------------------------------------------------
 constexpr u32 kLight = 8, kChunk = 256;
 
-// warp-aggregated append of the lanes with `take` set (one atomic per warp
-// on the shared frontier counter instead of one per completed rule; must be
-// called by every lane of the warp)
-__device__ __forceinline__ void warp_append(bool take, u32 v, u32* q, u64* cnt) {
-  const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
-  if (!m) return;
-  const unsigned lane = threadIdx.x & 31u;
-  const int leader = __ffs(m) - 1;
-  unsigned long long base = 0;
-  if ((int)lane == leader) base = atomicAdd((unsigned long long*)cnt, (unsigned long long)__popc(m));
-  base = __shfl_sync(0xFFFFFFFFu, base, leader);
-  if (take) q[base + __popc(m & ((1u << lane) - 1u))] = v;
-}
-
 struct KahnCtl {
-  u64 cnt[3];    // rotating frontier counts: layer L reads cnt[L%3], appends to cnt[(L+1)%3]
-  u64 ntask[2];  // heavy-task counts, layer L uses ntask[L&1]
+  u32 any[3];    // layer L is non-empty: any[L % 3] (set by the layer that fills it)
+  u32 pad;
+  u64 ntask[2];  // heavy-task counts, layer L uses ntask[L & 1]
   u64 processed;
   u64 layers;
 };
@@ -456,104 +643,141 @@ __device__ __forceinline__ u64 ld_cg64(const u64* p) {
 
 constexpr int kKahnBlock = 1024;  // few, large blocks: cheaper grid barriers
 
-template <bool TD>
-__global__ void __launch_bounds__(kKahnBlock) k_kahn(KahnCtl* ctl, u32* q0, u32* q1, const u64* __restrict__ off,
-                                              const u32* __restrict__ ids, u32* rem, u32* lvl,
-                                              const u64* __restrict__ par_off,
-                                              const u32* __restrict__ par_ids,
-                                              const uint8_t* __restrict__ root_parent, uint8_t* reach,
-                                              uint2* tasks, u64 max_layers) {
+// first frontier: rules (not the root) without non-root parents
+__global__ void k_kahn_first(const u32* rem, u64 R, u32* bm, KahnCtl* ctl) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = 1 + (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride)
+    if (rem[r] == 0) {
+      atomicOr(&bm[r >> 5], 1u << (r & 31u));
+      ctl->any[1] = 1;
+    }
+}
+
+// one edge of a frontier rule: push reachability, take the child's counter
+// down (warp-aggregated) and put it into the next frontier at zero
+__device__ __forceinline__ void kahn_edge(u32 c, bool act, bool reached, u32* rem, uint8_t* reach, u32* nxt,
+                                          u32* any_next) {
+  if (act && reached) reach[c] = 1;
+  if (dec_to_zero(rem, c, act)) {
+    atomicOr(&nxt[c >> 5], 1u << (c & 31u));
+    *any_next = 1;
+  }
+}
+
+__global__ void __launch_bounds__(kKahnBlock) k_kahn(KahnCtl* ctl, u32* bm0, u32* bm1, u64 nwords,
+                                                     const u64* __restrict__ off, const u32* __restrict__ ids,
+                                                     u32* rem, u32* lvl, uint8_t* reach, uint2* tasks,
+                                                     u64 max_layers) {
   cg::grid_group grid = cg::this_grid();
   const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   const u64 nthreads = (u64)gridDim.x * blockDim.x;
+  const u64 warp = gtid >> 5, nwarps = nthreads >> 5;
   const unsigned lane = threadIdx.x & 31u;
-  u64 total = 0, L = 1;
+  const volatile uint8_t* rv = reach;
+  u32 WS = 1;
+  while (WS < 32 && (u64)WS * 2 * nwarps <= nwords) WS *= 2;
+  u64 found = 0, L = 1;
   for (;; L++) {
-    const u64 n = ld_cg64(&ctl->cnt[L % 3]);
-    if (n == 0 || L > max_layers) break;
-    total += n;
+    if (__ldcg(&ctl->any[L % 3]) == 0 || L > max_layers) break;
     if (gtid == 0) {
-      ctl->cnt[(L + 2) % 3] = 0;
+      ctl->any[(L + 2) % 3] = 0;
       ctl->ntask[(L + 1) & 1] = 0;
     }
-    const u32* cur = (L & 1) ? q1 : q0;
-    u32* nxt = (L & 1) ? q0 : q1;
-    u64* ncnt = &ctl->cnt[(L + 1) % 3];
+    u32* cur = (L & 1) ? bm1 : bm0;
+    u32* nxt = (L & 1) ? bm0 : bm1;
+    u32* any_next = &ctl->any[(L + 1) % 3];
     u64* ntask = &ctl->ntask[L & 1];
-    // phase A: light rules inline, heavy rules -> chunk tasks
-    for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += nthreads) {
-      const u64 i = base + threadIdx.x;
-      const bool active = i < n;
-      u32 r = 0;
-      u64 e0 = 0, len = 0;
-      if (active) {
-        r = __ldcg(cur + i);
-        lvl[r] = (u32)L;
-        if (TD) {
-          bool rc = root_parent[r];
-          const volatile uint8_t* rv = reach;
-          for (u64 e = par_off[r]; e < par_off[r + 1] && !rc; e++) {
-            const u32 p = par_ids[e];
-            if (p != 0 && rv[p]) rc = true;
-          }
-          reach[r] = rc;
-        }
-        e0 = off[r];
-        len = off[r + 1] - e0;
-        if (len > kLight) {
-          const u64 nch = (len + kChunk - 1) / kChunk;
-          const u64 t0 = atomicAdd((unsigned long long*)ntask, (unsigned long long)nch);
-          for (u64 k = 0; k < nch; k++) tasks[t0 + k] = make_uint2(r, (u32)(k * kChunk));
-          len = 0;
-        }
-      }
-      // the warp's light edges dealt round-robin over its lanes: exclusive
-      // scan of the per-lane counts, then lane j takes edge k*32 + j and finds
-      // its owning lane by a shuffle binary search (no lane walks a long list)
-      u32 inc = (u32)len;
+    // phase A: WS bitmap words (32 * WS rules) per warp step, WS <= 32 sized
+    // so that a small grammar still spreads over every warp
+    for (u64 w0 = warp * WS; w0 < nwords; w0 += nwarps * WS) {
+      const u64 wi = w0 + lane;
+      const u32 bits = lane < WS && wi < nwords ? __ldcg(cur + wi) : 0u;
+      if (bits) cur[wi] = 0;  // cleared for layer L + 2
+      const u32 pc = __popc(bits);
+      u32 incl = pc;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-        if (lane >= (unsigned)d) inc += t;
+        const u32 t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= (unsigned)d) incl += t;
       }
-      const u32 excl = inc - (u32)len;
-      const u32 tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
-      for (u32 k0 = 0; k0 < tot; k0 += 32) {
-        const u32 q = k0 + lane;
-        // owner = last lane whose exclusive start <= q
+      const u32 excl_b = incl - pc;
+      const u32 T = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      for (u32 q0 = 0; q0 < T; q0 += 32) {
+        // rule q0 + lane of the step: owning lane by a shuffle binary search,
+        // then the matching set bit of that lane's word
+        const u32 q = q0 + lane;
         int lo = 0;
 #pragma unroll
         for (int step = 16; step; step >>= 1) {
-          const u32 st_ex = __shfl_sync(0xFFFFFFFFu, excl, lo + step);
-          if (st_ex <= q) lo += step;
+          const u32 se = __shfl_sync(0xFFFFFFFFu, excl_b, lo + step);
+          if (se <= q) lo += step;
         }
-        const u32 own_start = __shfl_sync(0xFFFFFFFFu, excl, lo);
-        const u64 own_e0 = __shfl_sync(0xFFFFFFFFu, e0, lo);
-        const bool a = q < tot;
-        const u32 c = a ? ids[own_e0 + (q - own_start)] : 0u;
-        warp_append(dec_to_zero(rem, c, a), c, nxt, ncnt);
+        const u32 ow_bits = __shfl_sync(0xFFFFFFFFu, bits, lo);
+        const u32 ow_ex = __shfl_sync(0xFFFFFFFFu, excl_b, lo);
+        const bool active = q < T;
+        u32 r = 0;
+        u64 e0 = 0, len = 0;
+        bool rc = false;
+        if (active) {
+          const u32 bp = __fns(ow_bits, 0, (int)(q - ow_ex) + 1);
+          r = (u32)((w0 + (u64)lo) * 32 + bp);
+          lvl[r] = (u32)L;
+          found++;
+          rc = rv[r] != 0;
+          e0 = off[r];
+          len = off[r + 1] - e0;
+          if (len > kLight) {
+            const u64 nch = (len + kChunk - 1) / kChunk;
+            const u64 t0 = atomicAdd((unsigned long long*)ntask, (unsigned long long)nch);
+            for (u64 k = 0; k < nch; k++) tasks[t0 + k] = make_uint2(r, (u32)(k * kChunk));
+            len = 0;
+          }
+        }
+        // the light edges of the step's rules dealt round-robin over the lanes
+        u32 inc = (u32)len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+          if (lane >= (unsigned)d) inc += t;
+        }
+        const u32 excl = inc - (u32)len;
+        const u32 tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
+        for (u32 k0 = 0; k0 < tot; k0 += 32) {
+          const u32 qe = k0 + lane;
+          int le = 0;
+#pragma unroll
+          for (int step = 16; step; step >>= 1) {
+            const u32 st_ex = __shfl_sync(0xFFFFFFFFu, excl, le + step);
+            if (st_ex <= qe) le += step;
+          }
+          const u32 own_start = __shfl_sync(0xFFFFFFFFu, excl, le);
+          const u64 own_e0 = __shfl_sync(0xFFFFFFFFu, e0, le);
+          const bool own_rc = __shfl_sync(0xFFFFFFFFu, rc, le);
+          const bool a = qe < tot;
+          const u32 c = a ? ids[own_e0 + (qe - own_start)] : 0u;
+          kahn_edge(c, a, own_rc, rem, reach, nxt, any_next);
+        }
       }
     }
     grid.sync();
-    // phase B: chunk tasks, one warp per task (most top-down layers have none:
-    // then the second barrier is skipped, uniformly across the grid)
+    // phase B: chunk tasks, one warp per task (most layers have none: then
+    // the second barrier is skipped, uniformly across the grid)
     const u64 nt = ld_cg64(ntask);
     if (nt == 0) continue;
-    for (u64 t = gtid >> 5; t < nt; t += nthreads >> 5) {
+    for (u64 t = warp; t < nt; t += nwarps) {
       const uint2 tk = __ldcg(tasks + t);
+      const bool trc = rv[tk.x] != 0;
       const u64 a = off[tk.x] + tk.y, b = min(off[tk.x + 1], a + kChunk);
       for (u64 e = a; e < b; e += 32) {
         const bool act = e + lane < b;
         const u32 c = act ? ids[e + lane] : 0u;
-        warp_append(dec_to_zero(rem, c, act), c, nxt, ncnt);
+        kahn_edge(c, act, trc, rem, reach, nxt, any_next);
       }
     }
     grid.sync();
   }
-  if (gtid == 0) {
-    ctl->processed = total;
-    ctl->layers = L - 1;
-  }
+  if (found) atomicAdd((unsigned long long*)&ctl->processed, (unsigned long long)found);
+  if (gtid == 0) ctl->layers = L - 1;
 }
 
 // Bottom-up sums in ONE persistent reverse-level pass over the child edges
@@ -734,7 +958,7 @@ struct ValRootLen {
 template <class T>
 static void d2h(T* dst, const void* src, size_t n, cudaStream_t s) {
   GT_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
-  GT_CUDA(cudaStreamSynchronize(s));
+  stream_sync(s);
 }
 
 #define LAUNCH(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
@@ -791,7 +1015,7 @@ static void reserve_pool(int device, cudaStream_t st) {
   void* p = nullptr;
   if (cudaMallocAsync(&p, want, st) == cudaSuccess) {
     GT_CUDA(cudaFreeAsync(p, st));
-    GT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
   } else {
     cudaGetLastError();  // best effort: the pool then grows on demand
   }
@@ -848,9 +1072,9 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   if (nbytes < 4 || memcmp(blob, "GTDC", 4) != 0) fail(GT_E_FORMAT, "bad magic: not a GTDC file");
   GT_CUDA(cudaSetDevice(device));
   d->device = device;
-  if (!d->stream) GT_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  if (!d->stream) d->stream = stream_acquire(device);
   cudaStream_t st = d->stream;
-  ph.st = st;
+  ph.bind(st);
   reserve_pool(device, st);
   ph.mark("stream");
   // the whole blob streams to the device while the host validates the
@@ -871,7 +1095,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   bool host_chain = false;
   auto need_host_chain = [&]() {
     if (host_chain) return;
-    GT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     P.rstart = rstart_host.get(P.R);
     parse_rules(blob, nbytes, &P);
     host_chain = true;
@@ -881,7 +1105,45 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     const u64 n = nsec;
     const int K = bitlen(P.R - 1);  // J_0 .. J_{K-1}
     bool ok = n >= 1 && n < 0xFFFFFFFFull && (nbytes - P.rules_pos) % 4 == 0;
-    if (ok) {
+    bool done = false;
+    static const bool words_only = getenv("GT_CHAIN_WORDS") != nullptr;  // diagnostics: skip the chunked form
+    const u64 p1 = ok ? 1 + (u64)rd32(blob + P.rules_pos) : 0;  // the first record after the root
+    if (ok && !words_only && P.R >= 2 && p1 < n) {
+      const u64 nch = (n - p1 + kChunkB - 1) / kChunkB, S = nch * kWin + 1;
+      const int K2 = bitlen(nch);  // J_0 .. J_{K2-1} cover c <= nch chunk steps
+      DBuf nx((u64)K2 * S * 4, st), ct((u64)K2 * S * 4, st), entry(nch * 4, st), base(nch * 4, st), bad(4, st);
+      DBuf mask(nch * kWin * kMaskW * 4, st);
+      GT_KLAUNCH("k_chunk_tables", k_chunk_tables, grid_for(nch * 32, kTabWarps * 32), kTabWarps * 32, st,
+                 raw.as<u32>(), n, p1, nch, nx.as<u32>(), ct.as<u32>(), mask.as<u32>());
+      if (K2 > 1) {
+        static int per_sm = -1;
+        if (per_sm < 0) {
+          GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_state_double_all, 256, 0));
+          per_sm = std::max(1, std::min(per_sm, 4));
+        }
+        int nsm = 148;
+        GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+        const unsigned blocks = (unsigned)std::max<u64>(1, std::min<u64>((u64)nsm * per_sm, (S + 255) / 256));
+        u32* nxp = nx.as<u32>();
+        u32* ctp = ct.as<u32>();
+        u64 Sv = S;
+        int Kv = K2;
+        void* args[] = {(void*)&nxp, (void*)&ctp, (void*)&Sv, (void*)&Kv};
+        ProfScope ps("k_state_double_all", st);
+        GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_state_double_all, dim3(blocks), dim3(256), args, 0, st));
+        g_launches++;
+      }
+      GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+      LAUNCH(k_chunk_entry, nch + 1, nx.as<u32>(), ct.as<u32>(), S, K2, nch, P.R, entry.as<u32>(), base.as<u32>(),
+             bad.as<u32>());
+      LAUNCH(k_chunk_starts, nch * 32, p1, nch, P.R, entry.as<u32>(), base.as<u32>(), mask.as<u32>(),
+             rstart.as<u32>());
+      u32 b = 0;
+      d2h(&b, bad.p, 1, st);
+      done = b == 0;
+      if (done) d->load_flags |= 1;
+    }
+    if (ok && !done) {
       DBuf J((u64)std::max(K, 1) * (n + 1) * 4, st), pos(P.R * 4, st), bad(4, st);
       u32* Jb = J.as<u32>();
       LAUNCH(k_jump0, n + 1, raw.as<u32>(), n, Jb);
@@ -958,8 +1220,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   GT_CUDA(cudaEventCreateWithFlags(&ev_body, cudaEventDisableTiming));
   GT_CUDA(cudaEventRecord(ev_body, st));
   Error root_err{GT_OK, ""};
-  cudaStream_t s_root = nullptr;
-  GT_CUDA(cudaStreamCreateWithFlags(&s_root, cudaStreamNonBlocking));
+  cudaStream_t s_root = stream_acquire(device);
   auto root_side = [&]() {
     try {
       GT_CUDA(cudaSetDevice(device));
@@ -1045,7 +1306,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     cudaEventDestroy(ev_body);
     rebind_stream(st, {&d->seg_lo, &d->seg_hi, &d->root_seg, &d->rs_rule, &d->rs_seg, &d->rs_cnt, &d->rs_off,
                        &d->rw_word, &d->rw_seg, &d->rw_cnt});
-    cudaStreamDestroy(s_root);
+    stream_release(device, s_root);
     if (root_err.code != GT_OK) throw root_err;
   };
   struct JoinGuard {
@@ -1064,93 +1325,102 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
       cudaEventDestroy(ev_body);
       rebind_stream(st, {&d->seg_lo, &d->seg_hi, &d->root_seg, &d->rs_rule, &d->rs_seg, &d->rs_cnt,
                          &d->rs_off, &d->rw_word, &d->rw_seg, &d->rw_cnt});
-      cudaStreamDestroy(s_root);
+      stream_release(device, s_root);
     }
   }};
 
 
-  // ---- (rule, symbol) sort + RLE -> own / sub CSR ----------------------
-  // bodies are contiguous per rule, so the (rule, symbol) order is a
-  // segmented sort of the body by symbol (one pass for the short bodies);
-  // a 64-bit global radix sort of (rule << SB | symbol) beyond 2^31 symbols
+  // ---- own / sub CSR: per-rule sort + RLE (csr_build.cu); the global
+  // (rule, symbol) sort below remains for sections beyond 2^31 symbols
   const int SB = std::max(1, bitlen(limit - 1));
-  DBuf head(E + 1, st), hidx(E * 4 + 4, st), cnt(16, st);
-  DBuf sbody, skeys;
-  // (measured: the global sort wins on C2-sized grammars, the segmented one from ~10^7 symbols)
-  const bool segmented = E >= (8ull << 20) && E < (1ull << 31) && R < (1ull << 31);
-  if (segmented) {
-    sbody.alloc(E * 4 + 4, st);
-    sort_segments_u32(d->body.as<u32>(), sbody.as<u32>(), E, R, d->boff.as<u64>(), st);
-    LAUNCH(k_heads_seg, E, sbody.as<u32>(), owner.as<u32>(), E, head.as<uint8_t>());
+  DBuf own_rule, sub_rule;
+  static const bool csr_sort = getenv("GT_CSR_SORT") != nullptr;  // diagnostics: the global-sort form
+  const bool fused = !csr_sort && E < (1ull << 31) && SB + std::max(1, bitlen(R - 1)) <= 64;
+  if (fused) {
+    build_rule_pairs(d, owner.as<u32>(), own_rule, sub_rule, st);
   } else {
-    const int KB = SB + std::max(1, bitlen(R - 1));
-    DBuf keys(E * 8 + 8, st);
-    skeys.alloc(E * 8 + 8, st);
-    LAUNCH(k_make_keys, E, d->body.as<u32>(), owner.as<u32>(), E, SB, keys.as<u64>());
-    sort_keys_u64(keys.as<u64>(), skeys.as<u64>(), E, KB, st);
-    LAUNCH(k_heads, E, skeys.as<u64>(), E, head.as<uint8_t>());
-  }
-  // runs of equal (rule, symbol), sized by the worst case E so the only host
-  // round trip of this phase is the one for the own / sub pair counts
-  DBuf cnt3(32, st);
-  select_flagged_index(head.as<uint8_t>(), hidx.as<u32>(), cnt3.as<u64>(), E, st);
-  DBuf pr_rule(E * 4 + 4, st), pr_sym(E * 4 + 4, st), pr_cnt(E * 4 + 4, st);
-  DBuf is_own(E + 1, st), is_sub(E + 1, st);
-  GT_CUDA(cudaMemsetAsync(is_own.p, 0, E + 1, st));
-  GT_CUDA(cudaMemsetAsync(is_sub.p, 0, E + 1, st));
-  if (segmented)
-    LAUNCH(k_rle_seg, E, sbody.as<u32>(), owner.as<u32>(), hidx.as<u32>(), cnt3.as<u64>(), E, nw, base,
-           pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
-  else
-    LAUNCH(k_rle, E, skeys.as<u64>(), hidx.as<u32>(), cnt3.as<u64>(), E, SB, nw, base, pr_rule.as<u32>(),
-           pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
-  sbody.release();
-  skeys.release();
-  head.release();
-  DBuf selO(E * 4 + 4, st), selS(E * 4 + 4, st);
-  select_flagged_index(is_own.as<uint8_t>(), selO.as<u32>(), cnt3.as<u64>() + 1, E, st);
-  select_flagged_index(is_sub.as<uint8_t>(), selS.as<u32>(), cnt3.as<u64>() + 2, E, st);
-  {
-    u64 h[2];
-    d2h(h, cnt3.as<u64>() + 1, 2, st);
-    d->E_own = h[0];
-    d->E_sub = h[1];
+    // ---- (rule, symbol) sort + RLE -> own / sub CSR ----------------------
+    // bodies are contiguous per rule, so the (rule, symbol) order is a
+    // segmented sort of the body by symbol (one pass for the short bodies);
+    // a 64-bit global radix sort of (rule << SB | symbol) beyond 2^31 symbols
+    DBuf head(E + 1, st), hidx(E * 4 + 4, st), cnt(16, st);
+    DBuf sbody, skeys;
+    // (measured: the global sort wins on C2-sized grammars, the segmented one from ~10^7 symbols)
+    const bool segmented = E >= (8ull << 20) && E < (1ull << 31) && R < (1ull << 31);
+    if (segmented) {
+      sbody.alloc(E * 4 + 4, st);
+      sort_segments_u32(d->body.as<u32>(), sbody.as<u32>(), E, R, d->boff.as<u64>(), st);
+      LAUNCH(k_heads_seg, E, sbody.as<u32>(), owner.as<u32>(), E, head.as<uint8_t>());
+    } else {
+      const int KB = SB + std::max(1, bitlen(R - 1));
+      DBuf keys(E * 8 + 8, st);
+      skeys.alloc(E * 8 + 8, st);
+      LAUNCH(k_make_keys, E, d->body.as<u32>(), owner.as<u32>(), E, SB, keys.as<u64>());
+      sort_keys_u64(keys.as<u64>(), skeys.as<u64>(), E, KB, st);
+      LAUNCH(k_heads, E, skeys.as<u64>(), E, head.as<uint8_t>());
+    }
+    // runs of equal (rule, symbol), sized by the worst case E so the only host
+    // round trip of this phase is the one for the own / sub pair counts
+    DBuf cnt3(32, st);
+    select_flagged_index(head.as<uint8_t>(), hidx.as<u32>(), cnt3.as<u64>(), E, st);
+    DBuf pr_rule(E * 4 + 4, st), pr_sym(E * 4 + 4, st), pr_cnt(E * 4 + 4, st);
+    DBuf is_own(E + 1, st), is_sub(E + 1, st);
+    GT_CUDA(cudaMemsetAsync(is_own.p, 0, E + 1, st));
+    GT_CUDA(cudaMemsetAsync(is_sub.p, 0, E + 1, st));
+    if (segmented)
+      LAUNCH(k_rle_seg, E, sbody.as<u32>(), owner.as<u32>(), hidx.as<u32>(), cnt3.as<u64>(), E, nw, base,
+             pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
+    else
+      LAUNCH(k_rle, E, skeys.as<u64>(), hidx.as<u32>(), cnt3.as<u64>(), E, SB, nw, base, pr_rule.as<u32>(),
+             pr_sym.as<u32>(), pr_cnt.as<u32>(), is_own.as<uint8_t>(), is_sub.as<uint8_t>());
+    sbody.release();
+    skeys.release();
+    head.release();
+    DBuf selO(E * 4 + 4, st), selS(E * 4 + 4, st);
+    select_flagged_index(is_own.as<uint8_t>(), selO.as<u32>(), cnt3.as<u64>() + 1, E, st);
+    select_flagged_index(is_sub.as<uint8_t>(), selS.as<u32>(), cnt3.as<u64>() + 2, E, st);
+    {
+      u64 h[2];
+      d2h(h, cnt3.as<u64>() + 1, 2, st);
+      d->E_own = h[0];
+      d->E_sub = h[1];
+    }
+    const u64 Eo = d->E_own, Es = d->E_sub;
+    own_rule.alloc(Eo * 4 + 4, st);
+    d->own_ids.alloc(Eo * 4 + 4, st);
+    d->own_freqs.alloc(Eo * 4 + 4, st);
+    LAUNCH(k_gather3, Eo, selO.as<u32>(), Eo, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
+           own_rule.as<u32>(), d->own_ids.as<u32>(), d->own_freqs.as<u32>());
+    sub_rule.alloc(Es * 4 + 4, st);
+    d->sub_ids.alloc(Es * 4 + 4, st);
+    d->sub_freqs.alloc(Es * 4 + 4, st);
+    LAUNCH(k_gather3, Es, selS.as<u32>(), Es, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
+           sub_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>());
+    selO.release();
+    selS.release();
+    pr_rule.release();
+    pr_sym.release();
+    pr_cnt.release();
+    is_own.release();
+    is_sub.release();
+    hidx.release();
+    d->own_off.alloc((R + 1) * 8, st);
+    d->sub_off.alloc((R + 1) * 8, st);
+    LAUNCH(k_csr_offsets, R + 1, own_rule.as<u32>(), Eo, R, d->own_off.as<u64>());
+    LAUNCH(k_csr_offsets, R + 1, sub_rule.as<u32>(), Es, R, d->sub_off.as<u64>());
   }
   const u64 Eo = d->E_own, Es = d->E_sub;
-  DBuf own_rule(Eo * 4 + 4, st);
-  d->own_ids.alloc(Eo * 4 + 4, st);
-  d->own_freqs.alloc(Eo * 4 + 4, st);
-  LAUNCH(k_gather3, Eo, selO.as<u32>(), Eo, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
-         own_rule.as<u32>(), d->own_ids.as<u32>(), d->own_freqs.as<u32>());
-  DBuf sub_rule(Es * 4 + 4, st);
-  d->sub_ids.alloc(Es * 4 + 4, st);
-  d->sub_freqs.alloc(Es * 4 + 4, st);
-  LAUNCH(k_gather3, Es, selS.as<u32>(), Es, pr_rule.as<u32>(), pr_sym.as<u32>(), pr_cnt.as<u32>(),
-         sub_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>());
-  selO.release();
-  selS.release();
-  pr_rule.release();
-  pr_sym.release();
-  pr_cnt.release();
-  is_own.release();
-  is_sub.release();
-  hidx.release();
-  d->own_off.alloc((R + 1) * 8, st);
-  d->sub_off.alloc((R + 1) * 8, st);
-  LAUNCH(k_csr_offsets, R + 1, own_rule.as<u32>(), Eo, R, d->own_off.as<u64>());
-  LAUNCH(k_csr_offsets, R + 1, sub_rule.as<u32>(), Es, R, d->sub_off.as<u64>());
   ph.mark("own/sub CSR");
 
   // ---- word-major transpose of the own pairs (no host sync: side stream) ----
-  cudaStream_t s_own = nullptr;
-  GT_CUDA(cudaStreamCreateWithFlags(&s_own, cudaStreamNonBlocking));
+  cudaStream_t s_own = stream_acquire(device);
   struct StreamGuard {
     cudaStream_t s, main;
     DeviceDag* d;
     ~StreamGuard() {
       cudaStreamSynchronize(s);
       rebind_stream(main, {&d->ow_word, &d->ow_rule, &d->ow_freq, &d->ow_off});
-      cudaStreamDestroy(s);
+      stream_release(d->device, s);
     }
   } own_guard{s_own, st, d};
   {
@@ -1162,81 +1432,79 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   }
     {
     cudaStream_t st = s_own;
-    DBuf id2(Eo * 4 + 4, st), sid(Eo * 4 + 4, st);
+    // (rule, freq) travel with the word keys through the radix sort: no
+    // permutation gather afterwards
+    DBuf v1(Eo * 8 + 8, st), v2(Eo * 8 + 8, st);
     d->ow_word.alloc(Eo * 4 + 4, st);
     d->ow_rule.alloc(Eo * 4 + 4, st);
     d->ow_freq.alloc(Eo * 4 + 4, st);
     d->ow_off.alloc((nw + 1) * 8, st);
-    LAUNCH(k_iota_u32, Eo, id2.as<u32>(), Eo);
-    sort_pairs_u32_u32(d->own_ids.as<u32>(), d->ow_word.as<u32>(), id2.as<u32>(), sid.as<u32>(), Eo,
+    LAUNCH(k_pack2, Eo, own_rule.as<u32>(), d->own_freqs.as<u32>(), Eo, v1.as<u64>());
+    sort_pairs_u32_u64(d->own_ids.as<u32>(), d->ow_word.as<u32>(), v1.as<u64>(), v2.as<u64>(), Eo,
                        std::max(1, bitlen(nw ? nw - 1 : 0)), st);
-    LAUNCH(k_gather3, Eo, sid.as<u32>(), Eo, own_rule.as<u32>(), d->own_freqs.as<u32>(),
-           (const u32*)nullptr, d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), (u32*)nullptr);
-    LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
+    LAUNCH(k_unpack2, Eo, v2.as<u64>(), Eo, d->ow_rule.as<u32>(), d->ow_freq.as<u32>());
+    LAUNCH(k_csr_offsets_lin, Eo + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
   }
 
   // ---- parents: stable sort of sub pairs by child -------------------------
-  DBuf idx(Es * 4 + 4, st), sidx(Es * 4 + 4, st), child_sorted(Es * 4 + 4, st);
-  LAUNCH(k_iota_u32, Es, idx.as<u32>(), Es);
-  sort_pairs_u32_u32(d->sub_ids.as<u32>(), child_sorted.as<u32>(), idx.as<u32>(), sidx.as<u32>(), Es,
-                     std::max(1, bitlen(R - 1)), st);
-  d->par_ids.alloc(Es * 4 + 4, st);
-  d->par_freqs.alloc(Es * 4 + 4, st);
-  d->par_off.alloc((R + 1) * 8, st);
-  LAUNCH(k_gather3, Es, sidx.as<u32>(), Es, sub_rule.as<u32>(), d->sub_freqs.as<u32>(),
-         (const u32*)nullptr, d->par_ids.as<u32>(), d->par_freqs.as<u32>(), (u32*)nullptr);
-  LAUNCH(k_csr_offsets, R + 1, child_sorted.as<u32>(), Es, R, d->par_off.as<u64>());
-  idx.release();
-  sidx.release();
+  DBuf child_sorted(Es * 4 + 4, st);
+  {
+    DBuf v1(Es * 8 + 8, st), v2(Es * 8 + 8, st);
+    LAUNCH(k_pack2, Es, sub_rule.as<u32>(), d->sub_freqs.as<u32>(), Es, v1.as<u64>());
+    sort_pairs_u32_u64(d->sub_ids.as<u32>(), child_sorted.as<u32>(), v1.as<u64>(), v2.as<u64>(), Es,
+                       std::max(1, bitlen(R - 1)), st);
+    d->par_ids.alloc(Es * 4 + 4, st);
+    d->par_freqs.alloc(Es * 4 + 4, st);
+    d->par_off.alloc((R + 1) * 8, st);
+    LAUNCH(k_unpack2, Es, v2.as<u64>(), Es, d->par_ids.as<u32>(), d->par_freqs.as<u32>());
+    LAUNCH(k_csr_offsets_lin, Es + 1, child_sorted.as<u32>(), Es, R, d->par_off.as<u64>());
+  }
   ph.mark("parent CSR");
 
   // ---- per-rule sums -------------------------------------------------------
-  d->own_tok.alloc(R * 8, st);
-  d->num_out.alloc(R * 8, st);
   d->num_in.alloc(R * 8, st);
-  GT_CUDA(cudaMemsetAsync(d->own_tok.p, 0, R * 8, st));
-  GT_CUDA(cudaMemsetAsync(d->num_out.p, 0, R * 8, st));
   GT_CUDA(cudaMemsetAsync(d->num_in.p, 0, R * 8, st));
-  LAUNCH(k_seg_sum_sorted, Eo, own_rule.as<u32>(), Eo, ValU32{d->own_freqs.as<u32>()}, d->own_tok.as<u64>());
-  LAUNCH(k_seg_sum_sorted, Es, sub_rule.as<u32>(), Es, ValU32{d->sub_freqs.as<u32>()}, d->num_out.as<u64>());
+  if (!fused) {  // (the per-rule pass produced them)
+    d->own_tok.alloc(R * 8, st);
+    d->num_out.alloc(R * 8, st);
+    GT_CUDA(cudaMemsetAsync(d->own_tok.p, 0, R * 8, st));
+    GT_CUDA(cudaMemsetAsync(d->num_out.p, 0, R * 8, st));
+    LAUNCH(k_seg_sum_sorted, Eo, own_rule.as<u32>(), Eo, ValU32{d->own_freqs.as<u32>()}, d->own_tok.as<u64>());
+    LAUNCH(k_seg_sum_sorted, Es, sub_rule.as<u32>(), Es, ValU32{d->sub_freqs.as<u32>()}, d->num_out.as<u64>());
+  }
   LAUNCH(k_seg_sum_sorted, Es, child_sorted.as<u32>(), Es,
          (ValU32NonRoot{d->par_freqs.as<u32>(), d->par_ids.as<u32>()}), d->num_in.as<u64>());
 
   // ---- bottom-up layering (cycle check) then top-down layering -----------
-  DBuf rem_bu(R * 4, st), rem_td(R * 4, st), rootp(R, st), flag(R, st);
-  DBuf fr(R * 4 + 4, st), nx(R * 4 + 4, st), fcnt(16, st);
+  DBuf rem_td(R * 4, st), rootp(R, st);
+  DBuf bm(((R + 31) / 32) * 8 + 8, st);  // two frontier bitmaps
   d->bu_level.alloc(R * 4, st);
   d->td_level.alloc(R * 4, st);
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, R * 4, st));
   GT_CUDA(cudaMemsetAsync(d->td_level.p, 0, R * 4, st));
-  LAUNCH(k_degrees, R, d->sub_off.as<u64>(), d->par_off.as<u64>(), d->par_ids.as<u32>(), R,
-         rem_bu.as<u32>(), rem_td.as<u32>(), rootp.as<uint8_t>());
-  // persistent Kahn layering, bottom-up (doubles as the cycle check), then
-  // top-down (carries reachability): one cooperative launch each
+  LAUNCH(k_degrees, R, d->par_off.as<u64>(), d->par_ids.as<u32>(), R, rem_td.as<u32>(), rootp.as<uint8_t>());
+  // persistent top-down Kahn layering (doubles as the cycle check, carries
+  // reachability): one cooperative launch
   const u64 ntask_max = Es / kChunk + R + 1;
   DBuf tasks(ntask_max * 8, st), ctl_b(sizeof(KahnCtl), st);
   KahnCtl* ctl = ctl_b.as<KahnCtl>();
-  DBuf reach(R, st), firstu(4, st);
-  GT_CUDA(cudaMemsetAsync(reach.p, 0, R, st));
-  auto kahn = [&](bool td, DBuf& rem, const DBuf& off, const DBuf& ids, DBuf& lvl) {
+  DBuf reach(R, st);
+  auto kahn = [&](DBuf& rem, const DBuf& off, const DBuf& ids, DBuf& lvl) {
+    const u64 nwords = (R + 31) / 32;
     GT_CUDA(cudaMemsetAsync(ctl, 0, sizeof(KahnCtl), st));
-    LAUNCH(k_flag_zero, R, rem.as<u32>(), R, td ? 1 : 0, flag.as<uint8_t>());
-    // first frontier -> q1 (layer 1 reads q1), its count -> cnt[1]
-    select_flagged_index(flag.as<uint8_t>(), nx.as<u32>(), &ctl->cnt[1], R, st);
-    const void* kern = td ? (const void*)k_kahn<true> : (const void*)k_kahn<false>;
-    static int per_sm[2] = {-1, -1};
-    int& ps = per_sm[td ? 1 : 0];
-    if (ps < 0) {
-      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, kKahnBlock, 0));
-      ps = std::max(ps, 1);
+    GT_CUDA(cudaMemsetAsync(bm.p, 0, 2 * nwords * 4, st));
+    // reachability starts at the rules the root references
+    GT_CUDA(cudaMemcpyAsync(reach.p, rootp.p, R, cudaMemcpyDeviceToDevice, st));
+    u32* b0 = bm.as<u32>();
+    u32* b1 = b0 + nwords;
+    LAUNCH(k_kahn_first, R, rem.as<u32>(), R, b1, ctl);  // layer 1 reads b1
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kahn, kKahnBlock, 0));
+      per_sm = std::max(per_sm, 1);
     }
     int nsm = 148;
     GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-    u32* q0 = fr.as<u32>();
-    u32* q1 = nx.as<u32>();
-    const u64* po = d->par_off.as<u64>();
-    const u32* pi = d->par_ids.as<u32>();
-    const uint8_t* rp = rootp.as<uint8_t>();
     uint8_t* rc = reach.as<uint8_t>();
     uint2* tk = tasks.as<uint2>();
     const u64* o = off.as<u64>();
@@ -1244,11 +1512,13 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     u32* rm = rem.as<u32>();
     u32* lv = lvl.as<u32>();
     u64 maxl = R + 2;
-    void* args[] = {(void*)&ctl, (void*)&q0, (void*)&q1, (void*)&o, (void*)&ii, (void*)&rm, (void*)&lv,
-                    (void*)&po, (void*)&pi, (void*)&rp, (void*)&rc, (void*)&tk, (void*)&maxl};
+    u64 nw_ = nwords;
+    void* args[] = {(void*)&ctl, (void*)&b0, (void*)&b1, (void*)&nw_, (void*)&o, (void*)&ii, (void*)&rm,
+                    (void*)&lv, (void*)&rc, (void*)&tk, (void*)&maxl};
     {
-      ProfScope ps_(td ? "k_kahn<td>" : "k_kahn<bu>", st);
-      GT_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)(nsm * ps)), dim3(kKahnBlock), args, 0, st));
+      ProfScope ps_("k_kahn<td>", st);
+      GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_kahn, dim3((unsigned)(nsm * per_sm)), dim3(kKahnBlock),
+                                          args, 0, st));
       g_launches++;
     }
   };
@@ -1256,7 +1526,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // a reference cycle, so an incomplete layering is the cycle check
   // (grammar.py:127-161 order: cycles before unreachable rules, dag.py:173-184)
   u64 processed = 0;
-  kahn(true, rem_td, d->sub_off, d->sub_ids, d->td_level);
+  kahn(rem_td, d->sub_off, d->sub_ids, d->td_level);
   // every rule but the root must be layered, and no reachable rule (nor the
   // root itself) may reference the root: either way there is a cycle; then
   // the first unreachable rule.  One host round trip for all three checks.
@@ -1270,7 +1540,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, cd.as<u32>() + 1);
     GT_CUDA(cudaMemcpyAsync(&h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
     GT_CUDA(cudaMemcpyAsync(chk, cd.p, 8, cudaMemcpyDeviceToHost, st));
-    GT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
   }
   processed = h.processed;
   const int ntd = (int)h.layers;
@@ -1280,10 +1550,8 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   }
   if (chk[1] != 0xFFFFFFFFu) fail(GT_E_CORRUPTION, "rule %u is not reachable from the root", chk[1]);
   ph.mark("top-down layering");
-  rem_bu.release();
   rem_td.release();
-  fr.release();
-  nx.release();
+  bm.release();
 
   // ---- level-ordered edge lists (radix sort is stable: within a level the
   // edges keep (child, parent) resp. (rule, child) order) -------------------
@@ -1296,15 +1564,16 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
                          DBuf& of, u64* off_stage, DBuf& off_dev) {
     // every edge is sorted (dropped ones under key nl + 1, after all levels),
     // so no count has to come back to the host first
-    DBuf idx(Es * 4 + 4, st), key(Es * 4 + 4, st), key2(Es * 4 + 4, st), idx2(Es * 4 + 4, st);
-    LAUNCH(k_iota_u32, Es, idx.as<u32>(), Es);
+    // the edge triples travel with the level keys (one radix pass for <= 255 levels)
+    DBuf key(Es * 4 + 4, st), key2(Es * 4 + 4, st), v1(Es * 12 + 12, st), v2(Es * 12 + 12, st);
     LAUNCH(k_edge_level_keys2, Es, group_of, keep, lvl, (u32)nl + 1, Es, key.as<u32>());
-    sort_pairs_u32_u32(key.as<u32>(), key2.as<u32>(), idx.as<u32>(), idx2.as<u32>(), Es,
-                       std::max(1, bitlen((u64)nl + 1)), st);
+    LAUNCH(k_pack3, Es, a_src, b_src, f_src, Es, v1.as<U3>());
+    sort_pairs_u32_u3(key.as<u32>(), key2.as<u32>(), v1.as<U3>(), v2.as<U3>(), Es,
+                      std::max(1, bitlen((u64)nl + 1)), st);
     oa.alloc(Es * 4 + 16, st);  // + 16: the TMA-staged level loop copies whole 16-byte words
     ob.alloc(Es * 4 + 16, st);
     of.alloc(Es * 4 + 16, st);
-    LAUNCH(k_gather3, Es, idx2.as<u32>(), Es, a_src, b_src, f_src, oa.as<u32>(), ob.as<u32>(), of.as<u32>());
+    LAUNCH(k_unpack3, Es, v2.as<U3>(), Es, oa.as<u32>(), ob.as<u32>(), of.as<u32>());
     DBuf koff(((u64)nl + 3) * 8, st);
     LAUNCH(k_csr_offsets, (u64)nl + 3, key2.as<u32>(), Es, (u64)nl + 2, koff.as<u64>());
     GT_CUDA(cudaMemcpyAsync(off_stage, koff.p, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
@@ -1386,8 +1655,8 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   }
   ph.mark("root side joined");
 
-  GT_CUDA(cudaStreamSynchronize(st));
-  GT_CUDA(cudaStreamSynchronize(s_own));
+  stream_sync(st);
+  stream_sync(s_own);
   own_rule.release();
   {
     d->te_off.assign(stage, stage + ntd + 3);
@@ -1400,6 +1669,30 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   }
   ph.mark("finish");
   d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+static std::mutex g_stream_mu;
+static std::vector<cudaStream_t> g_stream_pool[64];
+
+cudaStream_t stream_acquire(int device) {
+  {
+    std::lock_guard<std::mutex> lock(g_stream_mu);
+    auto& v = g_stream_pool[device & 63];
+    if (!v.empty()) {
+      cudaStream_t s = v.back();
+      v.pop_back();
+      return s;
+    }
+  }
+  cudaStream_t s = nullptr;
+  GT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+void stream_release(int device, cudaStream_t s) {
+  if (!s) return;
+  std::lock_guard<std::mutex> lock(g_stream_mu);
+  g_stream_pool[device & 63].push_back(s);
 }
 
 }  // namespace gt

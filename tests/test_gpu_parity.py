@@ -47,6 +47,7 @@ def test_composed_all_tasks_match_oracle(name, scale, seed):
     dag = gt.DeviceDag(blob)
     ref = OracleDag(blob)
     assert dag.info["words"] == ref.info["words"] == stats["W"]
+    assert dag.info["load_flags"] & 1  # short rules: the chunked rule-chain parse ran
     for task in TASKS:
         lens = (2, 3, 4) if task in ("seqcount", "rankedinvertedindex") else (3,)
         for l in lens:
@@ -57,6 +58,54 @@ def test_composed_all_tasks_match_oracle(name, scale, seed):
                 assert_same(got, exp, (name, scale, task, l, strategy))
                 if strategy == "bottomup" and task in ("wordcount", "sort", "invertedindex", "termvector"):
                     assert got.strategy == "bottomup"  # the pooled hash-table path ran
+    dag.close()
+
+
+def _rule_lengths(blob):
+    import struct
+    pos = 5
+    nw, ns, R = struct.unpack_from("<III", blob, pos)
+    pos += 12
+    for _ in range(nw):
+        pos += 4 + struct.unpack_from("<I", blob, pos)[0]
+    raw = np.frombuffer(blob[pos:], dtype="<u4")
+    p, lens = 0, []
+    for _ in range(R):
+        lens.append(int(raw[p]))
+        p += 1 + int(raw[p])
+    return lens
+
+
+# Phrases repeated verbatim become single Sequitur rules of about the phrase
+# length (rule utility inlines the inner digram rules), so these grammars hold
+# non-root records of 31..5000 words: the chunked rule-chain parse (loader.cu
+# k_chunk_tables, 32-word entry window) must fall back to word-level doubling
+# on the ones >= 32 and stay exact on the others.
+@pytest.mark.parametrize("phrase_lens", [(2, 3, 5), (31, 30, 29), (32, 33, 40), (1000, 31), (5000,),
+                                         (1030, 2100, 7)])
+def test_rule_chain_parse_long_records(phrase_lens):
+    import paper_2106_06889_b200 as gt
+    from oracle.oracle import OracleDag
+    rng = np.random.default_rng(sum(phrase_lens))
+    files = []
+    for k, L in enumerate(phrase_lens):
+        phrase = [f"p{k}_{i}" for i in range(L)]
+        for rep in range(3):
+            filler = [f"w{int(x)}" for x in np.minimum(rng.zipf(1.3, size=int(rng.integers(50, 3000))), 400)]
+            cut = int(rng.integers(0, len(filler) + 1))
+            files.append((f"f{k}_{rep}", " ".join(filler[:cut] + phrase + filler[cut:]).encode()))
+    from paper_2106_06889_b200.compress import compress_files
+    blob, _ = compress_files(files)
+    lens = _rule_lengths(blob)
+    assert max(lens[1:]) >= max(phrase_lens) - 2  # the long rule exists
+    dag = gt.DeviceDag(blob)
+    if max(lens[1:]) < 32:
+        assert dag.info["load_flags"] & 1
+    ref = OracleDag(blob)
+    for task in TASKS:
+        got = gt.run_compact(dag, task, gt.TraversalConfig(), 3)
+        exp = gt.run_compact(ref, task, gt.TraversalConfig(), 3)
+        assert_same(got, exp, (phrase_lens, task))
     dag.close()
 
 
