@@ -17,7 +17,7 @@ timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_atom.sum,lts__t_sectors_op_red.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__warps_active.avg.pct_of_peak_sustained_active \
   --clock-control none -k regex:"k_segred|k_seed|k_root_words|k_expand_rows|k_popc_rows|k_records|k_ii_groups" --csv \
   --log-file "$OUT/metrics.csv" python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_segred_levels" -s 8 -c 2 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_segred1?_levels" -s 8 -c 2 \
   -o "$OUT/full" python bench.py --steps 1 --warmup 3 --no-cpu-baseline > "$OUT/full.log" 2>&1
 timeout 900 python tools/gpu_probe.py c2 c3 c4 c5 --pinned --reps 2 > "$OUT/probe.txt" 2>&1
 echo done
