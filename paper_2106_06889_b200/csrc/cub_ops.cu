@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/tabulate_output_iterator.h>
 
 #include "gt_internal.cuh"
 
@@ -77,6 +78,50 @@ void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 
   thrust::counting_iterator<u32> it(0);
   with_temp("cub::SelectFlagged", [&](void* t, size_t& b) {
     GT_CUDA(cub::DeviceSelect::Flagged(t, b, it, flags, out_idx, d_count, (int64_t)n, s));
+  }, s);
+}
+
+struct NonzeroAt {
+  const u64* v;
+  __device__ __forceinline__ bool operator()(const u32& i) const { return v[i] != 0; }
+};
+
+// indices i < n with v[i] != 0, ascending (one select pass, no flag array)
+void select_nonzero_index(const u64* v, u32* out_idx, u64* d_count, u64 n, cudaStream_t s) {
+  if (!n) {
+    GT_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u64), s));
+    return;
+  }
+  thrust::counting_iterator<u32> it(0);
+  with_temp("cub::SelectIf", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceSelect::If(t, b, it, out_idx, d_count, (int64_t)n, NonzeroAt{v}, s));
+  }, s);
+}
+
+// the k-th selected index i becomes record k: (i % V, v[i], i / V)
+struct RecordWriter {
+  const u64* v;
+  u64 V;
+  u32* id;
+  u64* cnt;
+  u32* file;
+  __device__ __forceinline__ void operator()(int64_t k, u32 i) const {
+    id[k] = (u32)(i % V);
+    cnt[k] = v[i];
+    if (file) file[k] = (u32)(i / V);
+  }
+};
+
+void select_nonzero_records(const u64* v, u64 V, u64 n, u32* id, u64* cnt, u32* file, u64* d_count,
+                            cudaStream_t s) {
+  if (!n) {
+    GT_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u64), s));
+    return;
+  }
+  thrust::counting_iterator<u32> it(0);
+  auto out = thrust::make_tabulate_output_iterator(RecordWriter{v, V, id, cnt, file});
+  with_temp("cub::SelectIf", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceSelect::If(t, b, it, out, d_count, (int64_t)n, NonzeroAt{v}, s));
   }, s);
 }
 

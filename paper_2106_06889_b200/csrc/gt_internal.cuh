@@ -161,6 +161,9 @@ void exclusive_scan_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
 void inclusive_scan_u32(const u32* in, u32* out, u64 n, cudaStream_t s);
 // ordered compaction of indices i in [0,n) with flags[i] != 0; count -> d_count
 void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 n, cudaStream_t s);
+void select_nonzero_index(const u64* v, u32* out_idx, u64* d_count, u64 n, cudaStream_t s);
+void select_nonzero_records(const u64* v, u64 V, u64 n, u32* id, u64* cnt, u32* file, u64* d_count,
+                            cudaStream_t s);
 void reduce_max_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
 // sort the keys of each segment [off[i], off[i+1]) independently (n < 2^31)
 void sort_segments_u32(const u32* keys_in, u32* keys_out, u64 n, u64 nseg, const u64* off, cudaStream_t s);

@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "kernels_common.cuh"
 
@@ -332,6 +333,62 @@ __global__ void __launch_bounds__(256) k_segredG(const u32* __restrict__ dst,
 }
 
 // ---------------------------------------------------------------------------
+// Top-down seeds (init_top_down_masks, engine.py:178-193): the root's direct
+// references per owned segment (rs lists sorted by (rule, segment)).  Global
+// mode adds every owned segment's count into row[rule]; per-file mode into
+// row[rule*C + segment]; presence (OrMode) sets bit segment%64 of
+// row[rule*C + segment/64].  Lanes of a warp hitting the same cell are
+// combined with a segmented shuffle scan (keys ascend along the list), one
+// reduction per run.  zero_n: rows to clear first (persistent phase 0 only).
+// ---------------------------------------------------------------------------
+struct SeedArgs {
+  const u32* rule;
+  const u32* seg;
+  const u32* cnt;
+  u64 n;
+  u32 file_lo, nseg;
+  int per_file;
+  u32 C;
+  u64* row;
+  u64 zero_n;
+};
+
+template <class Mode>
+__device__ __forceinline__ void seed_rows_body(const SeedArgs& a) {
+  const unsigned lane = threadIdx.x & 31u;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const bool is_or = std::is_same<Mode, OrMode>::value;
+  for (u64 base = (u64)blockIdx.x * blockDim.x; base < a.n; base += stride) {
+    const u64 i = base + threadIdx.x;
+    u64 key = ~0ull, v = 0;
+    if (i < a.n) {
+      const u32 sg = a.seg[i] - a.file_lo;
+      if (sg < a.nseg) {
+        const u64 r = a.rule[i];
+        if (!a.per_file) {
+          key = r;
+          v = a.cnt[i];
+        } else if (is_or) {
+          key = r * a.C + (sg >> 6);
+          v = 1ull << (sg & 63u);
+        } else {
+          key = r * a.C + sg;
+          v = a.cnt[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, d);
+      const u64 ok = __shfl_up_sync(0xFFFFFFFFu, key, d);
+      if (lane >= (unsigned)d && ok == key) v = Mode::merge(v, ov);
+    }
+    const u64 nk = __shfl_down_sync(0xFFFFFFFFu, key, 1);
+    if (key != ~0ull && (lane == 31 || nk != key)) Mode::atomic(&a.row[key], v);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Persistent level loop: ONE cooperative launch runs levels [L0, L1] of a
 // level-ordered item list (lvl_off on the device), the whole grid resident
 // and separated by grid-wide barriers instead of kernel boundaries.  Level
@@ -384,8 +441,16 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
                                                           const u32* __restrict__ src,
                                                           const u32* __restrict__ freq,
                                                           const u64* __restrict__ lvl_off, int L0, int L1,
-                                                          int reverse, int prefetch, Src in, Out out) {
+                                                          int reverse, int prefetch, SeedArgs seed, Src in,
+                                                          Out out) {
   cg::grid_group grid = cg::this_grid();
+  if (seed.row) {  // phase 0: clear the rows, then the root seeds
+    const u64 gt0 = (u64)blockIdx.x * blockDim.x + threadIdx.x, nt0 = (u64)gridDim.x * blockDim.x;
+    for (u64 i = gt0; i < seed.zero_n; i += nt0) seed.row[i] = 0;
+    grid.sync();
+    seed_rows_body<Mode>(seed);
+    grid.sync();
+  }
   const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   const u64 nthreads = (u64)gridDim.x * blockDim.x;
   // warps numbered round-robin over the blocks: a level smaller than the
@@ -707,14 +772,15 @@ void seg_reduce_levels_tma(const char* name, const u32* dst, const u32* src, con
 
 template <int BLOCK, int PRE, class Mode, class Src, class Out>
 void seg_reduce_levels1_b(const char* name, const u32* dst, const u32* src, const u32* freq,
-                          const u64* lvl_off_dev, int L0, int L1, int reverse, int prefetch, Src in, Out out,
-                          cudaStream_t st) {
+                          const u64* lvl_off_dev, int L0, int L1, int reverse, int prefetch, const SeedArgs* seed,
+                          Src in, Out out, cudaStream_t st) {
   auto kern = k_segred1_levels<BLOCK, PRE, Mode, Src, Out>;
   int dev = 0, nsm = 148;
   GT_CUDA(cudaGetDevice(&dev));
   GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  SeedArgs sa = seed ? *seed : SeedArgs{};
   void* args[] = {(void*)&dst, (void*)&src, (void*)&freq, (void*)&lvl_off_dev, (void*)&L0, (void*)&L1,
-                  (void*)&reverse, (void*)&prefetch, (void*)&in, (void*)&out};
+                  (void*)&reverse, (void*)&prefetch, (void*)&sa, (void*)&in, (void*)&out};
   ProfScope ps(name, st);
   GT_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)nsm), dim3(BLOCK), args, 0, st));
   g_launches++;
@@ -727,34 +793,36 @@ void seg_reduce_levels1_b(const char* name, const u32* dst, const u32* src, cons
 // Measured per pass: C2 94 -> 70 us, C4 0.39 -> 0.36 ms, C5 0.70 -> 0.68 ms.
 template <class Mode, class Src, class Out>
 void seg_reduce_levels1(const char* name, const u32* dst, const u32* src, const u32* freq,
-                        const u64* lvl_off_dev, int L0, int L1, int reverse, u64 avg_items, Src in, Out out,
-                        cudaStream_t st) {
+                        const u64* lvl_off_dev, int L0, int L1, int reverse, u64 avg_items, const SeedArgs* seed,
+                        Src in, Out out, cudaStream_t st) {
   static const int prefetch = getenv("GT_LEVEL_PREFETCH") ? atoi(getenv("GT_LEVEL_PREFETCH")) : 1;
   static const int force_pre = getenv("GT_LEVEL_PRE") ? atoi(getenv("GT_LEVEL_PRE")) : 0;
   const int pre = force_pre ? force_pre : (avg_items > 148ull * kLevelBlock ? 4 : 1);
   if (pre == 4)
-    seg_reduce_levels1_b<kLevelBlock, 4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, reverse, prefetch, in,
-                                               out, st);
+    seg_reduce_levels1_b<kLevelBlock, 4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, reverse, prefetch, seed,
+                                               in, out, st);
   else
-    seg_reduce_levels1_b<kLevelBlock, 1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, reverse, prefetch, in,
-                                               out, st);
+    seg_reduce_levels1_b<kLevelBlock, 1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, reverse, prefetch, seed,
+                                               in, out, st);
 }
 
 // levels [L0, L1] in increasing order, or decreasing with reverse = true
 template <class Mode, class Src, class Out>
 void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u32* freq,
                        const u64* lvl_off_dev, int L0, int L1, u32 C, Src in, Out out, cudaStream_t st,
-                       bool reverse = false, u64 avg_items = 0) {
-  if (L1 < L0 || !C) return;
+                       bool reverse = false, u64 avg_items = 0, const SeedArgs* seed = nullptr) {
+  // seed (C == 1 only): zero + seed the rows as phase 0 of the same launch
+  if (!C) return;
+  if (L1 < L0 && !seed) return;
   const int rv = reverse ? 1 : 0;
   // the TMA-staged variant is opt-in: measured slower on every config (C2 top-
   // down pass 0.223 vs 0.188 ms per step, C5 0.73 vs 0.68 ms) — the item
   // loads it hides are not on the critical path; the row gathers and the
   // grid barrier are
   static const bool use_tma = getenv("GT_LEVELS_TMA") != nullptr;
-  if (C == 1 && use_tma)
+  if (C == 1 && use_tma && !seed)
     seg_reduce_levels_tma<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, in, out, st, reverse);
-  else if (C == 1) seg_reduce_levels1<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, avg_items, in, out, st);
+  else if (C == 1) seg_reduce_levels1<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, avg_items, seed, in, out, st);
   else if (C <= 2) seg_reduce_levels_G<2, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 4) seg_reduce_levels_G<4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 8) seg_reduce_levels_G<8, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);

@@ -29,47 +29,12 @@
 
 namespace gt {
 
-// Seeds of the top-down pass: the root's direct references, per owned
-// segment (rs lists sorted by (rule, segment)).  Global mode adds every owned
-// segment's count into row[rule]; per-file mode into row[rule*C + segment];
-// presence (OrMode) sets bit segment%64 of row[rule*C + segment/64].  Lanes
-// of a warp hitting the same cell are combined with a segmented shuffle scan
-// (keys ascend along the list), one atomic per run.
+// Seeds of the top-down pass (segreduce.cuh seed_rows_body): the root's
+// direct references per owned segment; also run as phase 0 of the C = 1
+// persistent level loop.
 template <class Mode>
-__global__ void __launch_bounds__(256) k_seed(const u32* __restrict__ rs_rule, const u32* __restrict__ rs_seg,
-                                              const u32* __restrict__ rs_cnt, u64 n, u32 file_lo,
-                                              u32 nseg, int per_file, u32 C, u64* __restrict__ row) {
-  const unsigned lane = threadIdx.x & 31u;
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  const bool is_or = std::is_same<Mode, OrMode>::value;
-  for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const u64 i = base + threadIdx.x;
-    u64 key = ~0ull, v = 0;
-    if (i < n) {
-      const u32 sg = rs_seg[i] - file_lo;
-      if (sg < nseg) {
-        const u64 r = rs_rule[i];
-        if (!per_file) {
-          key = r;
-          v = rs_cnt[i];
-        } else if (is_or) {
-          key = r * C + (sg >> 6);
-          v = 1ull << (sg & 63u);
-        } else {
-          key = r * C + sg;
-          v = rs_cnt[i];
-        }
-      }
-    }
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, d);
-      const u64 ok = __shfl_up_sync(0xFFFFFFFFu, key, d);
-      if (lane >= (unsigned)d && ok == key) v = Mode::merge(v, ov);
-    }
-    const u64 nk = __shfl_down_sync(0xFFFFFFFFu, key, 1);
-    if (key != ~0ull && (lane == 31 || nk != key)) Mode::atomic(&row[key], v);
-  }
+__global__ void __launch_bounds__(256) k_seed(SeedArgs a) {
+  seed_rows_body<Mode>(a);
 }
 
 // root words of owned segments: (word, seg, cnt) sorted by word
@@ -148,6 +113,40 @@ __global__ void k_ii_groups(const u32* words, const u64* ngroups, const u64* off
   }
 }
 
+// inverted index with at most 64 owned files (one presence word per vocab
+// word): ONE scan over packed (has-files << 32 | popcount) gives both the
+// group index and the record offset of every word, so groups and records
+// come out of one emit pass (no select, no second scan)
+__global__ void k_ii_keys(const u64* __restrict__ pres, u64 V, u64* key) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 w = (u64)blockIdx.x * blockDim.x + threadIdx.x; w <= V; w += stride) {
+    const u64 pc = w < V ? (u64)__popcll(pres[w]) : 0;
+    key[w] = (pc ? (1ull << 32) : 0ull) | pc;
+  }
+}
+
+__global__ void k_ii_emit(const u64* __restrict__ pres, u64 V, const u64* __restrict__ pref, u32 file_lo,
+                          u32* files, u32* gid, u64* goff) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 w = (u64)blockIdx.x * blockDim.x + threadIdx.x; w <= V; w += stride) {
+    const u64 k = pref[w];
+    const u64 g = k >> 32, o = k & 0xFFFFFFFFull;
+    if (w == V) {
+      goff[g] = o;
+      continue;
+    }
+    u64 b = pres[w];
+    if (!b) continue;
+    gid[g] = (u32)w;
+    goff[g] = o;
+    u64 q = o;
+    while (b) {
+      files[q++] = file_lo + (u32)(__ffsll((long long)b) - 1);
+      b &= b - 1;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host drivers
 // ---------------------------------------------------------------------------
@@ -160,14 +159,18 @@ __global__ void k_ii_groups(const u32* words, const u64* ngroups, const u64* off
 template <class Mode>
 static void td_levels(const DeviceDag* d, u32 C, u64* row, u32 per_file = 1) {
   cudaStream_t st = d->stream;
-  GT_CUDA(cudaMemsetAsync(row, 0, sizeof(u64) * C * d->R, st));
-  if (d->n_rs)
-    KL(k_seed<Mode>, grid_for(d->n_rs, 256), d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(),
-       d->n_rs, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row);
-  // all levels in one persistent launch, grid barriers between levels
+  const SeedArgs seed{d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
+                      (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row, (u64)C * d->R};
+  if (C != 1) {
+    GT_CUDA(cudaMemsetAsync(row, 0, sizeof(u64) * C * d->R, st));
+    if (d->n_rs) KL(k_seed<Mode>, grid_for(d->n_rs, 256), seed);
+  }
+  // all levels in one persistent launch, grid barriers between levels (C = 1:
+  // the zeroing and the seeds run as its phase 0)
   seg_reduce_levels<Mode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
                           d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrc{row, C}, TdRows{row, C}, st, false,
-                          d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0);
+                          d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0,
+                          C == 1 ? &seed : nullptr);
 }
 
 // Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
@@ -197,8 +200,9 @@ void td_root_seeds(DeviceDag* d, u64* row) {
   cudaStream_t st = d->stream;
   GT_CUDA(cudaMemsetAsync(row, 0, sizeof(u64) * d->R, st));
   if (d->n_rs)
-    KL(k_seed<SumMode>, grid_for(d->n_rs, 256), d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(),
-       d->n_rs, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), 0, 1u, row);
+    KL(k_seed<SumMode>, grid_for(d->n_rs, 256),
+       SeedArgs{d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
+                (u32)(d->file_hi - d->file_lo), 0, 1u, row, 0});
 }
 
 u64 scratch_budget(const DeviceDag* d) {
@@ -261,19 +265,30 @@ void assemble_counts(DeviceDag* d, const u64* dense, u64 V, u32 ncols, bool by_c
   const bool pf = ncols > 0;
   const u64 N = V * (u64)(pf ? ncols : 1);
   if (N >= (1ull << 32)) fail(GT_E_RESOURCE, "dense per-file table of %lu entries exceeds 2^32; use the bottom-up strategy", (unsigned long)N);
-  DBuf flags(N + 1, st), sel(N * 4 + 4, st), cnt(8, st);
-  KL(k_nonzero_flags, grid_for(N, 256), dense, N, flags.as<uint8_t>());
-  select_flagged_index(flags.as<uint8_t>(), sel.as<u32>(), cnt.as<u64>(), N, st);
+  DBuf cnt(8, st), file;
   u64 n;
-  GT_CUDA(cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, st));
-  GT_CUDA(cudaStreamSynchronize(st));
+  if (N <= (1ull << 26)) {
+    // the select writes the records itself (worst-case sized outputs, no
+    // index list and no second pass)
+    R->id.alloc(N * 4 + 4, st);
+    R->count.alloc(N * 8 + 8, st);
+    if (pf) file.alloc(N * 4 + 4, st);
+    select_nonzero_records(dense, V, N, R->id.as<u32>(), R->count.as<u64>(), pf ? file.as<u32>() : nullptr,
+                           cnt.as<u64>(), st);
+    GT_CUDA(cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+  } else {
+    DBuf sel(N * 4 + 4, st);
+    select_nonzero_index(dense, sel.as<u32>(), cnt.as<u64>(), N, st);
+    GT_CUDA(cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+    R->id.alloc(n * 4 + 4, st);
+    R->count.alloc(n * 8 + 8, st);
+    if (pf) file.alloc(n * 4 + 4, st);
+    KL(k_records, grid_for(n, 256), sel.as<u32>(), cnt.as<u64>(), dense, V, R->id.as<u32>(),
+       R->count.as<u64>(), pf ? file.as<u32>() : nullptr);
+  }
   R->n = n;
-  R->id.alloc(n * 4 + 4, st);
-  R->count.alloc(n * 8 + 8, st);
-  DBuf file;
-  if (pf) file.alloc(n * 4 + 4, st);
-  KL(k_records, grid_for(n, 256), sel.as<u32>(), cnt.as<u64>(), dense, V, R->id.as<u32>(),
-     R->count.as<u64>(), pf ? file.as<u32>() : nullptr);
   if (pf) {
     R->group_off.alloc((ncols + 1) * 8, st);
     KL(k_csr_offsets, grid_for(ncols + 1, 256), file.as<u32>(), n, (u64)ncols, R->group_off.as<u64>());
@@ -297,6 +312,23 @@ void assemble_counts(DeviceDag* d, const u64* dense, u64 V, u32 ncols, bool by_c
 void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R) {
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
+  if (FW == 1 && V < (1ull << 32)) {
+    DBuf key((V + 1) * 8, st), pref((V + 1) * 8, st);
+    KL(k_ii_keys, grid_for(V + 1, 256), pres, V, key.as<u64>());
+    exclusive_scan_u64(key.as<u64>(), pref.as<u64>(), V + 1, st);
+    u64 h;
+    GT_CUDA(cudaMemcpyAsync(&h, pref.as<u64>() + V, 8, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+    const u64 ng = h >> 32, n = h & 0xFFFFFFFFull;
+    R->n = n;
+    R->n_groups = ng;
+    R->id.alloc(n * 4 + 4, st);
+    R->group_id.alloc(ng * 4 + 4, st);
+    R->group_off.alloc((ng + 1) * 8, st);
+    KL(k_ii_emit, grid_for(V + 1, 256), pres, V, pref.as<u64>(), (u32)d->file_lo, R->id.as<u32>(),
+       R->group_id.as<u32>(), R->group_off.as<u64>());
+    return;
+  }
   DBuf off, files, pc;
   bits_count(pres, V, FW, 1, V, off, pc, st);
   DBuf nz(V + 1, st), words(V * 4 + 4, st), cnt(16, st);
