@@ -88,7 +88,8 @@ typedef struct gt_info {
   uint64_t device_bytes;   /* device memory held by the context               */
   double init_ms;          /* gt_open wall time (the "initialization" phase)  */
   uint64_t td_edges;       /* non-root parent edges (top-down pass items)     */
-  uint64_t load_flags;     /* bit 0: rule chain parsed in the chunked form    */
+  uint64_t load_flags;     /* bit 0: rule chain parsed in the chunked form;   */
+                           /* bit 1: per-file cells held in u32 (files < 2^32 words) */
 } gt_info;
 
 /*

@@ -304,8 +304,9 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
           strat = GT_TOPDOWN_SPARSE;
         } else {
           DBuf cnt;
-          td_file_counts(&d, cnt);
-          assemble_counts(&d, cnt.as<u64>(), d.nw, Fo, true, &R);
+          bool c32 = false;
+          td_file_counts(&d, cnt, &c32);
+          assemble_counts(&d, cnt.p, d.nw, Fo, true, &R, c32);
           strat = GT_TOPDOWN;
         }
         break;

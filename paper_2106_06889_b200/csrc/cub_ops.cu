@@ -81,26 +81,31 @@ void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 
   }, s);
 }
 
+template <class T>
 struct NonzeroAt {
-  const u64* v;
+  const T* v;
   __device__ __forceinline__ bool operator()(const u32& i) const { return v[i] != 0; }
 };
 
 // indices i < n with v[i] != 0, ascending (one select pass, no flag array)
-void select_nonzero_index(const u64* v, u32* out_idx, u64* d_count, u64 n, cudaStream_t s) {
+void select_nonzero_index(const void* v, bool v32, u32* out_idx, u64* d_count, u64 n, cudaStream_t s) {
   if (!n) {
     GT_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u64), s));
     return;
   }
   thrust::counting_iterator<u32> it(0);
   with_temp("cub::SelectIf", [&](void* t, size_t& b) {
-    GT_CUDA(cub::DeviceSelect::If(t, b, it, out_idx, d_count, (int64_t)n, NonzeroAt{v}, s));
+    if (v32)
+      GT_CUDA(cub::DeviceSelect::If(t, b, it, out_idx, d_count, (int64_t)n, NonzeroAt<u32>{(const u32*)v}, s));
+    else
+      GT_CUDA(cub::DeviceSelect::If(t, b, it, out_idx, d_count, (int64_t)n, NonzeroAt<u64>{(const u64*)v}, s));
   }, s);
 }
 
 // the k-th selected index i becomes record k: (i % V, v[i], i / V)
+template <class T>
 struct RecordWriter {
-  const u64* v;
+  const T* v;
   u64 V;
   u32* id;
   u64* cnt;
@@ -112,16 +117,23 @@ struct RecordWriter {
   }
 };
 
-void select_nonzero_records(const u64* v, u64 V, u64 n, u32* id, u64* cnt, u32* file, u64* d_count,
+void select_nonzero_records(const void* v, bool v32, u64 V, u64 n, u32* id, u64* cnt, u32* file, u64* d_count,
                             cudaStream_t s) {
   if (!n) {
     GT_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u64), s));
     return;
   }
   thrust::counting_iterator<u32> it(0);
-  auto out = thrust::make_tabulate_output_iterator(RecordWriter{v, V, id, cnt, file});
   with_temp("cub::SelectIf", [&](void* t, size_t& b) {
-    GT_CUDA(cub::DeviceSelect::If(t, b, it, out, d_count, (int64_t)n, NonzeroAt{v}, s));
+    if (v32) {
+      const u32* p = (const u32*)v;
+      auto out = thrust::make_tabulate_output_iterator(RecordWriter<u32>{p, V, id, cnt, file});
+      GT_CUDA(cub::DeviceSelect::If(t, b, it, out, d_count, (int64_t)n, NonzeroAt<u32>{p}, s));
+    } else {
+      const u64* p = (const u64*)v;
+      auto out = thrust::make_tabulate_output_iterator(RecordWriter<u64>{p, V, id, cnt, file});
+      GT_CUDA(cub::DeviceSelect::If(t, b, it, out, d_count, (int64_t)n, NonzeroAt<u64>{p}, s));
+    }
   }, s);
 }
 

@@ -90,6 +90,7 @@ struct Levels {
   DBuf order;                  // u32[n]
   std::vector<u64> off;        // host: level L occupies [off[L], off[L+1]) (L=0..nl-1)
   std::vector<u64> heavy_off;  // host: first heavy rule of level L
+  DBuf off_dev;                // device copy of off (persistent level loops)
   int nl = 0;
 };
 
@@ -126,6 +127,8 @@ struct DeviceDag {
   std::vector<u64> be_off;  // host: bu level L items [be_off[L], be_off[L+1])
   DBuf be_off_dev;
   u64 load_flags = 0;  // gt_info.load_flags
+  u64 max_file_tokens = 0;
+  bool cnt32 = false;  // every file < 2^32 words: per-file rows / counts in u32 (GT_ROWS64=1: never)
   double init_ms = 0;
   // scratch kept across runs
   DBuf word_counts;  // u64[V] of the last global run
@@ -161,8 +164,8 @@ void exclusive_scan_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
 void inclusive_scan_u32(const u32* in, u32* out, u64 n, cudaStream_t s);
 // ordered compaction of indices i in [0,n) with flags[i] != 0; count -> d_count
 void select_flagged_index(const uint8_t* flags, u32* out_idx, u64* d_count, u64 n, cudaStream_t s);
-void select_nonzero_index(const u64* v, u32* out_idx, u64* d_count, u64 n, cudaStream_t s);
-void select_nonzero_records(const u64* v, u64 V, u64 n, u32* id, u64* cnt, u32* file, u64* d_count,
+void select_nonzero_index(const void* v, bool v32, u32* out_idx, u64* d_count, u64 n, cudaStream_t s);
+void select_nonzero_records(const void* v, bool v32, u64 V, u64 n, u32* id, u64* cnt, u32* file, u64* d_count,
                             cudaStream_t s);
 void reduce_max_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
 // sort the keys of each segment [off[i], off[i+1]) independently (n < 2^31)

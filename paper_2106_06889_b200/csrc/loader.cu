@@ -986,6 +986,9 @@ static void build_levels(DeviceDag* d, const DBuf& lvl, const DBuf& off, u64 th,
     out->heavy_off[L] = h[2 * L + 1];
   }
   out->off[nl + 1] = R;
+  out->off_dev.alloc((nl + 2) * 8, st);
+  GT_CUDA(cudaMemcpyAsync(out->off_dev.p, out->off.data(), (nl + 2) * 8, cudaMemcpyHostToDevice, st));
+  stream_sync(st);  // the host vector is the copy's source
 }
 
 // The stream-ordered pool keeps freed memory (release threshold = inf) and,
@@ -1558,7 +1561,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // host values read back once at the end of gt_open (one pinned staging
   // buffer: te and be level offsets, root height, W)
   static thread_local PinnedU64 stage_host;
-  u64* stage = stage_host.get(2 * ((u64)ntd + 3) + 2);
+  u64* stage = stage_host.get(2 * ((u64)ntd + 3) + 3);
   auto level_edges = [&](const u32* group_of, const uint8_t* keep, const u32* lvl, int nl,
                          const u32* a_src, const u32* b_src, const u32* f_src, DBuf& oa, DBuf& ob,
                          DBuf& of, u64* off_stage, DBuf& off_dev) {
@@ -1652,6 +1655,10 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     GT_CUDA(cudaMemsetAsync(d->seg_tokens.p, 0, d->F * 8, st));
     LAUNCH(k_seg_sum_sorted, d->L0, segof.as<u32>(), d->L0,
            (ValRootLen{d->body.as<u32>(), d->exp_len.as<u64>(), nw, base}), d->seg_tokens.as<u64>());
+    // the longest file, read back with the staging buffer below
+    DBuf mx(8, st);
+    reduce_max_u64(d->seg_tokens.as<u64>(), mx.as<u64>(), d->F, st);
+    GT_CUDA(cudaMemcpyAsync(stage + 2 * ((u64)ntd + 3) + 2, mx.p, 8, cudaMemcpyDeviceToHost, st));
   }
   ph.mark("root side joined");
 
@@ -1665,6 +1672,10 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     nbu = (int)hw[0];
     d->depth = (i64)hw[0] - 1;
     d->W = hw[1];
+    d->max_file_tokens = hw[2];
+    static const bool rows64 = getenv("GT_ROWS64") != nullptr;
+    d->cnt32 = !rows64 && hw[2] < (1ull << 32);
+    if (d->cnt32) d->load_flags |= 2;
     d->bu.nl = nbu;
   }
   ph.mark("finish");

@@ -34,11 +34,18 @@ namespace cg = cooperative_groups;
 
 namespace gt {
 
+// Values are combined in u64 registers; rows / outputs are u64, or u32 for
+// per-file counts when every file has < 2^32 words (DeviceDag::cnt32: a
+// per-file cell never exceeds its file's word count), halving the row bytes
+// of the 64-column passes.
 struct SumMode {
   __device__ static __forceinline__ u64 combine(u32 f, u64 x) { return (u64)f * x; }
   __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a + b; }
   __device__ static __forceinline__ void atomic(u64* p, u64 v) {
     if (v) atomicAdd((unsigned long long*)p, (unsigned long long)v);
+  }
+  __device__ static __forceinline__ void atomic(u32* p, u64 v) {
+    if (v) atomicAdd((unsigned*)p, (unsigned)v);
   }
 };
 
@@ -47,6 +54,9 @@ struct OrMode {
   __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a | b; }
   __device__ static __forceinline__ void atomic(u64* p, u64 v) {
     if (v) atomicOr((unsigned long long*)p, (unsigned long long)v);
+  }
+  __device__ static __forceinline__ void atomic(u32* p, u64 v) {
+    if (v) atomicOr((unsigned*)p, (unsigned)v);
   }
 };
 
@@ -68,41 +78,56 @@ __device__ __forceinline__ u64 ldcg(const u64* p) {
   return (u64)__ldcg(reinterpret_cast<const unsigned long long*>(p));
 }
 
-struct RowSrc {  // in[src*C + col]
-  const u64* in;
+__device__ __forceinline__ u64 ldcg(const u32* p) { return (u64)__ldcg(reinterpret_cast<const unsigned*>(p)); }
+
+template <class T>
+struct RowSrcT {  // in[src*C + col]
+  const T* in;
   u32 C;
   __device__ __forceinline__ u64 operator()(u32 s, u32 col) const { return ldcg(in + (u64)s * C + col); }
 };
+using RowSrc = RowSrcT<u64>;
 
-// two adjacent columns of a source row (col even): one 16-byte load for
-// RowSrc, two scalar reads otherwise
+// two adjacent columns of a source row (col even): one 16-byte (u64 rows) or
+// 8-byte (u32 rows) load for RowSrcT, two scalar reads otherwise
 template <class Src>
 __device__ __forceinline__ void load_pair(const Src& in, u32 s, u32 col, u64* a, u64* b) {
   *a = in(s, col);
   *b = in(s, col + 1);
 }
-__device__ __forceinline__ void load_pair(const RowSrc& in, u32 s, u32 col, u64* a, u64* b) {
+__device__ __forceinline__ void load_pair(const RowSrcT<u64>& in, u32 s, u32 col, u64* a, u64* b) {
   const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(in.in + (u64)s * in.C + col));
+  *a = v.x;
+  *b = v.y;
+}
+__device__ __forceinline__ void load_pair(const RowSrcT<u32>& in, u32 s, u32 col, u64* a, u64* b) {
+  const uint2 v = __ldcg(reinterpret_cast<const uint2*>(in.in + (u64)s * in.C + col));
   *a = v.x;
   *b = v.y;
 }
 
 // ---- output address functors --------------------------------------------------
-struct OutRowMajor {  // out[dst*C + col]
-  u64* out;
+template <class T>
+struct OutRowMajorT {  // out[dst*C + col]
+  T* out;
   u32 C;
-  __device__ __forceinline__ u64* operator()(u32 d, u32 col) const { return out + (u64)d * C + col; }
+  __device__ __forceinline__ T* operator()(u32 d, u32 col) const { return out + (u64)d * C + col; }
 };
-struct TdRows {  // out[dst*C + col] for the top-down pass (a distinct kernel name in ncu)
-  u64* out;
+using OutRowMajor = OutRowMajorT<u64>;
+template <class T>
+struct TdRowsT {  // out[dst*C + col] for the top-down pass (a distinct kernel name in ncu)
+  T* out;
   u32 C;
-  __device__ __forceinline__ u64* operator()(u32 d, u32 col) const { return out + (u64)d * C + col; }
+  __device__ __forceinline__ T* operator()(u32 d, u32 col) const { return out + (u64)d * C + col; }
 };
-struct OutColMajor {  // out[col*V + dst]
-  u64* out;
+using TdRows = TdRowsT<u64>;
+template <class T>
+struct OutColMajorT {  // out[col*V + dst]
+  T* out;
   u64 V;
-  __device__ __forceinline__ u64* operator()(u32 d, u32 col) const { return out + (u64)col * V + d; }
+  __device__ __forceinline__ T* operator()(u32 d, u32 col) const { return out + (u64)col * V + d; }
 };
+using OutColMajor = OutColMajorT<u64>;
 
 __device__ __forceinline__ u32 item_freq(const u32* freq, u64 i) { return freq ? freq[i] : 1u; }
 
@@ -144,7 +169,7 @@ __device__ __forceinline__ void segred1_body(const u32* __restrict__ dst, const 
         const u32 d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
         if (carry_d != 0xFFFFFFFFu && d0 != carry_d) {  // the carried run ended at the last step
           if (lane == 0) {
-            u64* p = out(carry_d, 0);
+            auto* p = out(carry_d, 0);
             Mode::atomic(p, carry_v);
           }
           carry_d = 0xFFFFFFFFu;
@@ -159,7 +184,7 @@ __device__ __forceinline__ void segred1_body(const u32* __restrict__ dst, const 
         if (d == carry_d) v = Mode::merge(v, carry_v);
         const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
         if (ok && lane != 31 && dn != d) {  // run ends inside this step
-          u64* p = out(d, 0);
+          auto* p = out(d, 0);
           Mode::atomic(p, v);
         }
         carry_d = __shfl_sync(0xFFFFFFFFu, d, 31);
@@ -167,7 +192,7 @@ __device__ __forceinline__ void segred1_body(const u32* __restrict__ dst, const 
       }
     }
     if (lane == 0 && carry_d != 0xFFFFFFFFu) {
-      u64* p = out(carry_d, 0);
+      auto* p = out(carry_d, 0);
       Mode::atomic(p, carry_v);
     }
   }
@@ -309,7 +334,7 @@ __device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const 
         for (int j = 0; j < B; j++) {
           if (dd[j] == 0xFFFFFFFFu) break;
           if (dd[j] != cd) {
-            u64* p = out(cd, col);
+            auto* p = out(cd, col);
             Mode::atomic(p, acc);
             cd = dd[j];
             acc = 0;
@@ -317,7 +342,7 @@ __device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const 
           acc = Mode::merge(acc, v[j]);
         }
       }
-      u64* p = out(cd, col);
+      auto* p = out(cd, col);
       Mode::atomic(p, acc);
     }
   }
@@ -349,12 +374,13 @@ struct SeedArgs {
   u32 file_lo, nseg;
   int per_file;
   u32 C;
-  u64* row;
+  void* row;  // u64 rows, or u32 (per-file counts under DeviceDag::cnt32)
   u64 zero_n;
 };
 
-template <class Mode>
+template <class Mode, class T = u64>
 __device__ __forceinline__ void seed_rows_body(const SeedArgs& a) {
+  T* row = reinterpret_cast<T*>(a.row);
   const unsigned lane = threadIdx.x & 31u;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const bool is_or = std::is_same<Mode, OrMode>::value;
@@ -384,7 +410,7 @@ __device__ __forceinline__ void seed_rows_body(const SeedArgs& a) {
       if (lane >= (unsigned)d && ok == key) v = Mode::merge(v, ov);
     }
     const u64 nk = __shfl_down_sync(0xFFFFFFFFu, key, 1);
-    if (key != ~0ull && (lane == 31 || nk != key)) Mode::atomic(&a.row[key], v);
+    if (key != ~0ull && (lane == 31 || nk != key)) Mode::atomic(&row[key], v);
   }
 }
 
@@ -446,7 +472,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
   cg::grid_group grid = cg::this_grid();
   if (seed.row) {  // phase 0: clear the rows, then the root seeds
     const u64 gt0 = (u64)blockIdx.x * blockDim.x + threadIdx.x, nt0 = (u64)gridDim.x * blockDim.x;
-    for (u64 i = gt0; i < seed.zero_n; i += nt0) seed.row[i] = 0;
+    u64* zr = reinterpret_cast<u64*>(seed.row);
+    for (u64 i = gt0; i < seed.zero_n; i += nt0) zr[i] = 0;
     grid.sync();
     seed_rows_body<Mode>(seed);
     grid.sync();

@@ -18,6 +18,8 @@
 // is reduced against the per-file weight rows (F columns, from the same
 // top-down level pull as term vectors), and the nonzero (gram, file, count)
 // records are ordered for render with two stable radix sorts.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "kernels_common.cuh"
@@ -29,37 +31,58 @@ namespace gt {
 
 namespace {
 
-// heads/tails for the rules of one bottom-up level (children are finished)
-__global__ void k_head_tail(const u32* order, u64 lo, u64 hi, const u32* __restrict__ body,
-                            const u64* __restrict__ boff, u64 nw, u64 base,
-                            const u64* __restrict__ exp_len, u32 m, u32* H, u32* T, u32* hl,
-                            u32* tl) {
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = lo + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
-    const u32 r = order[i];
-    if (r == 0) continue;
-    const u64 el = exp_len[r];
-    const u32 target = (u32)(el < m ? el : m);
-    u32 n = 0;
-    for (u64 q = boff[r]; q < boff[r + 1] && n < target; q++) {
-      u32 s = body[q];
-      if (s < nw) H[(u64)r * m + n++] = s;
-      else if (s >= base) {
-        u32 c = s - (u32)base;
-        for (u32 j = 0; j < hl[c] && n < target; j++) H[(u64)r * m + n++] = H[(u64)c * m + j];
-      }
+// heads/tails (sequence.py:110-140): the first / last min(l-1, exp_len)
+// words of a rule's expansion, from its body and its children's (finished:
+// lower bottom-up level).  Children's buffers are read through L2 (ld.cg):
+// they were written by other SMs before the last grid barrier.
+__device__ __forceinline__ void head_tail_rule(u32 r, const u32* __restrict__ body, const u64* __restrict__ boff,
+                                               u64 nw, u64 base, const u64* __restrict__ exp_len, u32 m, u32* H,
+                                               u32* T, u32* hl, u32* tl) {
+  const u64 el = exp_len[r];
+  const u32 target = (u32)(el < m ? el : m);
+  const u64 b0 = boff[r], b1 = boff[r + 1];
+  u32 n = 0;
+  for (u64 q = b0; q < b1 && n < target; q++) {
+    const u32 s = body[q];
+    if (s < nw) {
+      H[(u64)r * m + n++] = s;
+    } else if (s >= base) {
+      const u32 c = s - (u32)base;
+      const u32 hc = __ldcg(hl + c);
+      for (u32 j = 0; j < hc && n < target; j++) H[(u64)r * m + n++] = __ldcg(H + (u64)c * m + j);
     }
-    hl[r] = target;
-    n = 0;
-    for (u64 q = boff[r + 1]; q > boff[r] && n < target; q--) {
-      u32 s = body[q - 1];
-      if (s < nw) T[(u64)r * m + (target - 1 - n++)] = s;
-      else if (s >= base) {
-        u32 c = s - (u32)base;
-        for (u32 j = tl[c]; j > 0 && n < target; j--) T[(u64)r * m + (target - 1 - n++)] = T[(u64)c * m + j - 1];
-      }
+  }
+  hl[r] = target;
+  n = 0;
+  for (u64 q = b1; q > b0 && n < target; q--) {
+    const u32 s = body[q - 1];
+    if (s < nw) {
+      T[(u64)r * m + (target - 1 - n++)] = s;
+    } else if (s >= base) {
+      const u32 c = s - (u32)base;
+      for (u32 j = __ldcg(tl + c); j > 0 && n < target; j--)
+        T[(u64)r * m + (target - 1 - n++)] = __ldcg(T + (u64)c * m + j - 1);
     }
-    tl[r] = target;
+  }
+  tl[r] = target;
+}
+
+// every bottom-up level in ONE cooperative launch (grid barrier between
+// levels instead of a launch per level)
+__global__ void __launch_bounds__(1024) k_head_tail_levels(const u32* __restrict__ order, const u64* __restrict__ off,
+                                                           int nl, const u32* __restrict__ body,
+                                                           const u64* __restrict__ boff, u64 nw, u64 base,
+                                                           const u64* __restrict__ exp_len, u32 m, u32* H, u32* T,
+                                                           u32* hl, u32* tl) {
+  cg::grid_group grid = cg::this_grid();
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (int L = 1; L <= nl; L++) {
+    const u64 lo = off[L], hi = off[L + 1];
+    for (u64 i = lo + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
+      const u32 r = order[i];
+      if (r != 0) head_tail_rule(r, body, boff, nw, base, exp_len, m, H, T, hl, tl);
+    }
+    if (L < nl) grid.sync();
   }
 }
 
@@ -189,13 +212,36 @@ __global__ void k_run_heads(const u64* key, const u32* gram, u64 n, u32 l, int p
 // gram-run rows: an occurrence from rule s < R adds that rule's per-file
 // weight row; an occurrence counted directly in root segment s-R adds 1 to
 // that file's column
+template <class T>
 struct SeqSrc {
-  const u64* w;
+  const T* w;
   u32 R, C;
   __device__ __forceinline__ u64 operator()(u32 s, u32 col) const {
     return s < R ? w[(u64)s * C + col] : (s - R == col ? 1ull : 0ull);
   }
 };
+
+// two adjacent columns in one vector load (segreduce.cuh paired path)
+__device__ __forceinline__ void load_pair(const SeqSrc<u32>& in, u32 s, u32 col, u64* a, u64* b) {
+  if (s < in.R) {
+    const uint2 v = *reinterpret_cast<const uint2*>(in.w + (u64)s * in.C + col);
+    *a = v.x;
+    *b = v.y;
+  } else {
+    *a = s - in.R == col ? 1ull : 0ull;
+    *b = s - in.R == col + 1 ? 1ull : 0ull;
+  }
+}
+__device__ __forceinline__ void load_pair(const SeqSrc<u64>& in, u32 s, u32 col, u64* a, u64* b) {
+  if (s < in.R) {
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(in.w + (u64)s * in.C + col);
+    *a = v.x;
+    *b = v.y;
+  } else {
+    *a = s - in.R == col ? 1ull : 0ull;
+    *b = s - in.R == col + 1 ? 1ull : 0ull;
+  }
+}
 
 __global__ void k_heads_u32(const uint8_t* h, u64 n, u32* o) {
   u64 stride = (u64)gridDim.x * blockDim.x;
@@ -207,13 +253,9 @@ __global__ void k_dec_u32(u32* v, u64 n) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) v[i] -= 1;
 }
 
-__global__ void k_nz(const u64* v, u64 n, uint8_t* f) {
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f[i] = v[i] != 0;
-}
-
 // dense rows -> cells: selected index j = run*C + col
-__global__ void k_cells_dense(const u32* sel, const u64* nsel, const u64* rows, u32 C, u32* crun,
+template <class T>
+__global__ void k_cells_dense(const u32* sel, const u64* nsel, const T* rows, u32 C, u32* crun,
                               u32* ccol, u64* ccnt) {
   u64 n = *nsel;
   u64 stride = (u64)gridDim.x * blockDim.x;
@@ -245,11 +287,14 @@ __global__ void k_rec_keys(const u32* crun, const u32* ccol, const u64* ccnt, u6
 }
 
 // payload-carrying record sort (packed grams)
+// record sort keys (major << CB | W - count); K = u32 when CB + MB <= 32
+// (C2: 28 + 4 bits — a quarter less radix traffic than u64 keys)
+template <class K>
 __global__ void k_rec_keys2(const u32* crun, const u32* ccol, const u64* ccnt, u64 n, u64 W, int CB, int by_file,
-                            u64* skey) {
+                            K* skey) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    skey[i] = ((u64)(by_file ? ccol[i] : crun[i]) << CB) | (W - ccnt[i]);
+    skey[i] = (K)(((u64)(by_file ? ccol[i] : crun[i]) << CB) | (W - ccnt[i]));
 }
 
 __global__ void k_cell_grams(const u32* crun, u64 n, const u32* run_start, const u64* skey_sorted, u64* gk) {
@@ -258,12 +303,14 @@ __global__ void k_cell_grams(const u32* crun, u64 n, const u32* run_start, const
 }
 
 // sorted (major << CB | W - count) -> count, major
-__global__ void k_unkey2(const u64* key, u64 n, u64 W, int CB, u64* cnt, u32* major, u32) {
+template <class K>
+__global__ void k_unkey2(const K* key, u64 n, u64 W, int CB, u64* cnt, u32* major, u32) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   const u64 m = (1ull << CB) - 1;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    cnt[i] = W - (key[i] & m);
-    major[i] = (u32)(key[i] >> CB);
+    const u64 k = key[i];
+    cnt[i] = W - (k & m);
+    major[i] = (u32)(k >> CB);
   }
 }
 
@@ -364,24 +411,39 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   GT_CUDA(cudaMemsetAsync(tl.p, 0, R * 4, st));
   if (m) {
     ensure_bu_levels(d);
-    for (int L = 1; L <= d->bu.nl; L++) {
-      u64 lo = d->bu.off[L], hi = d->bu.off[L + 1];
-      if (hi > lo)
-        SL(k_head_tail, hi - lo, d->bu.order.as<u32>(), lo, hi, d->body.as<u32>(), d->boff.as<u64>(),
-           nw, base, d->exp_len.as<u64>(), m, H.as<u32>(), T.as<u32>(), hl.as<u32>(), tl.as<u32>());
+    if (d->bu.nl >= 1) {
+      int dev = 0, nsm = 148;
+      GT_CUDA(cudaGetDevice(&dev));
+      GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      const u32* ord = d->bu.order.as<u32>();
+      const u64* lo = d->bu.off_dev.as<u64>();
+      int nl = d->bu.nl;
+      const u32* bd = d->body.as<u32>();
+      const u64* bo = d->boff.as<u64>();
+      const u64* el = d->exp_len.as<u64>();
+      u32 *Hp = H.as<u32>(), *Tp = T.as<u32>(), *hlp = hl.as<u32>(), *tlp = tl.as<u32>();
+      u64 nw_ = nw, base_ = base;
+      u32 m_ = m;
+      void* args[] = {(void*)&ord, (void*)&lo, (void*)&nl, (void*)&bd, (void*)&bo, (void*)&nw_, (void*)&base_,
+                      (void*)&el, (void*)&m_, (void*)&Hp, (void*)&Tp, (void*)&hlp, (void*)&tlp};
+      ProfScope ps("k_head_tail_levels", st);
+      GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_head_tail_levels, dim3((unsigned)nsm), dim3(1024), args,
+                                          0, st));
+      g_launches++;
     }
   }
   ph.mark("heads/tails");
   // per-file rule weights: dense top-down rows (F columns) or, for many
   // files, the presence-guided sparse (rule, file) weights (sparse.cu)
   DBuf w;
+  bool w32 = false;
   SparseW sw;
   if (sparse) {
     u32 FW;
     sparse_file_weights(d, &sw, nullptr, &FW);
   } else {
     u32 Cw;
-    td_file_weights(d, w, &Cw);
+    td_file_weights(d, w, &Cw, &w32);
   }
 
   ph.mark("weights");
@@ -452,21 +514,37 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   } else {
     const u64 NR = nruns * C;
     if (NR >= (1ull << 32)) fail(GT_E_RESOURCE, "%lu gram x file cells exceed the 2^32 limit", (unsigned long)NR);
-    DBuf rows(NR * 8 + 8, st);
-    GT_CUDA(cudaMemsetAsync(rows.p, 0, NR * 8, st));
-    if (nruns)
-      seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
-                          SeqSrc{w.as<u64>(), (u32)R, C}, OutRowMajor{rows.as<u64>(), C}, st);
+    // per-file weights fit u32 (w32) -> so do the (gram, file) cells
+    // (GT_SEQ_ROWS=64: u64 cell rows over u32 weights, diagnostics)
+    static const bool rows64_env = getenv("GT_SEQ_ROWS") && atoi(getenv("GT_SEQ_ROWS")) == 64;
+    const bool r32 = w32 && !rows64_env;
+    const u64 eb = r32 ? 4 : 8;
+    DBuf rows(NR * eb + 8, st);
+    GT_CUDA(cudaMemsetAsync(rows.p, 0, NR * eb, st));
+    if (nruns) {
+      if (w32 && r32)
+        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
+                            SeqSrc<u32>{w.as<u32>(), (u32)R, C}, OutRowMajorT<u32>{rows.as<u32>(), C}, st);
+      else if (w32)
+        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
+                            SeqSrc<u32>{w.as<u32>(), (u32)R, C}, OutRowMajor{rows.as<u64>(), C}, st);
+      else
+        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
+                            SeqSrc<u64>{w.as<u64>(), (u32)R, C}, OutRowMajor{rows.as<u64>(), C}, st);
+    }
     w.release();
-    DBuf nzf(NR + 1, st), sel(NR * 4 + 4, st);
-    SL(k_nz, NR, rows.as<u64>(), NR, nzf.as<uint8_t>());
-    select_flagged_index(nzf.as<uint8_t>(), sel.as<u32>(), dcnt.as<u64>(), NR, st);
+    DBuf sel(NR * 4 + 4, st);
+    select_nonzero_index(rows.p, r32, sel.as<u32>(), dcnt.as<u64>(), NR, st);
     n = d2h1<u64>(dcnt.p, st);
     crun.alloc(n * 4 + 4, st);
     ccol.alloc(n * 4 + 4, st);
     ccnt.alloc(n * 8 + 8, st);
-    SL(k_cells_dense, n, sel.as<u32>(), dcnt.as<u64>(), rows.as<u64>(), C, crun.as<u32>(),
-       ccol.as<u32>(), ccnt.as<u64>());
+    if (r32)
+      SL(k_cells_dense<u32>, n, sel.as<u32>(), dcnt.as<u64>(), rows.as<u32>(), C, crun.as<u32>(),
+         ccol.as<u32>(), ccnt.as<u64>());
+    else
+      SL(k_cells_dense<u64>, n, sel.as<u32>(), dcnt.as<u64>(), rows.as<u64>(), C, crun.as<u32>(),
+         ccol.as<u32>(), ccnt.as<u64>());
   }
   ssrc.release();
   rid.release();
@@ -480,26 +558,41 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
     // the sort carries its payload: SEQCOUNT sorts (file | W - count) with the
     // packed gram as the value, RII (run | W - count) with the file — every
     // output field comes out of the sorted arrays, no permutation gathers
+    const bool k32 = CB + MB <= 32;
     DBuf sk(n * 8 + 8, st), sk2(n * 8 + 8, st);
-    SL(k_rec_keys2, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
-       sk.as<u64>());
+    if (k32)
+      SL(k_rec_keys2<u32>, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
+         sk.as<u32>());
+    else
+      SL(k_rec_keys2<u64>, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
+         sk.as<u64>());
     Rr->n = n;
     Rr->count.alloc(n * 8 + 8, st);
     if (by_file) {
       DBuf gk(n * 8 + 8, st);
       Rr->key.alloc(n * 8 + 8, st);
       SL(k_cell_grams, n, crun.as<u32>(), n, runs.as<u32>(), skey.as<u64>(), gk.as<u64>());
-      sort_pairs_u64_u64(sk.as<u64>(), sk2.as<u64>(), gk.as<u64>(), Rr->key.as<u64>(), n, CB + MB, st);
       DBuf major(n * 4 + 4, st);
-      SL(k_unkey2, n, sk2.as<u64>(), n, Wt, CB, Rr->count.as<u64>(), major.as<u32>(), 0u);
+      if (k32) {
+        sort_pairs_u32_u64(sk.as<u32>(), sk2.as<u32>(), gk.as<u64>(), Rr->key.as<u64>(), n, CB + MB, st);
+        SL(k_unkey2<u32>, n, sk2.as<u32>(), n, Wt, CB, Rr->count.as<u64>(), major.as<u32>(), 0u);
+      } else {
+        sort_pairs_u64_u64(sk.as<u64>(), sk2.as<u64>(), gk.as<u64>(), Rr->key.as<u64>(), n, CB + MB, st);
+        SL(k_unkey2<u64>, n, sk2.as<u64>(), n, Wt, CB, Rr->count.as<u64>(), major.as<u32>(), 0u);
+      }
       Rr->n_groups = Fo;
       Rr->group_off.alloc((Fo + 1) * 8, st);
       SL(k_csr_offsets, Fo + 1, major.as<u32>(), n, (u64)Fo, Rr->group_off.as<u64>());
     } else {
       Rr->id.alloc(n * 4 + 4, st);
-      sort_pairs_u64_u32(sk.as<u64>(), sk2.as<u64>(), ccol.as<u32>(), Rr->id.as<u32>(), n, CB + MB, st);
       DBuf rn(n * 4 + 4, st), gh(n + 1, st), gsel(n * 4 + 4, st);
-      SL(k_unkey2, n, sk2.as<u64>(), n, Wt, CB, Rr->count.as<u64>(), rn.as<u32>(), (u32)d->file_lo);
+      if (k32) {
+        sort_pairs_u32_u32(sk.as<u32>(), sk2.as<u32>(), ccol.as<u32>(), Rr->id.as<u32>(), n, CB + MB, st);
+        SL(k_unkey2<u32>, n, sk2.as<u32>(), n, Wt, CB, Rr->count.as<u64>(), rn.as<u32>(), (u32)d->file_lo);
+      } else {
+        sort_pairs_u64_u32(sk.as<u64>(), sk2.as<u64>(), ccol.as<u32>(), Rr->id.as<u32>(), n, CB + MB, st);
+        SL(k_unkey2<u64>, n, sk2.as<u64>(), n, Wt, CB, Rr->count.as<u64>(), rn.as<u32>(), (u32)d->file_lo);
+      }
       SL(k_add_u32_base, n, Rr->id.as<u32>(), n, (u32)d->file_lo);
       SL(k_heads_u32v, n, rn.as<u32>(), n, gh.as<uint8_t>());
       select_flagged_index(gh.as<uint8_t>(), gsel.as<u32>(), dcnt.as<u64>(), n, st);

@@ -32,16 +32,16 @@ namespace gt {
 // Seeds of the top-down pass (segreduce.cuh seed_rows_body): the root's
 // direct references per owned segment; also run as phase 0 of the C = 1
 // persistent level loop.
-template <class Mode>
+template <class Mode, class T = u64>
 __global__ void __launch_bounds__(256) k_seed(SeedArgs a) {
-  seed_rows_body<Mode>(a);
+  seed_rows_body<Mode, T>(a);
 }
 
 // root words of owned segments: (word, seg, cnt) sorted by word
-template <class Mode>
+template <class Mode, class T = u64>
 __global__ void k_root_words(const u32* __restrict__ rw_word, const u32* __restrict__ rw_seg,
                              const u32* __restrict__ rw_cnt, u64 n, u32 file_lo, u32 nseg,
-                             int per_file, u32 C, u64 V, u64* __restrict__ out) {
+                             int per_file, u32 C, u64 V, T* __restrict__ out) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     u32 sg = rw_seg[i] - file_lo;
@@ -67,7 +67,8 @@ __global__ void k_nonzero_flags(const u64* v, u64 n, uint8_t* f) {
 }
 
 // records from selected indices: id = idx % V (word), count, file = idx / V
-__global__ void k_records(const u32* sel, const u64* nsel, const u64* vals, u64 V, u32* id,
+template <class T>
+__global__ void k_records(const u32* sel, const u64* nsel, const T* vals, u64 V, u32* id,
                           u64* cnt, u32* file) {
   u64 n = *nsel;
   u64 stride = (u64)gridDim.x * blockDim.x;
@@ -156,35 +157,37 @@ __global__ void k_ii_emit(const u64* __restrict__ pres, u64 V, const u64* __rest
 // Top-down weights (Alg. 1, engine.py:196-227): rows of C columns per rule,
 // seeded from the root references, then one segmented gather-reduce launch
 // per top-down level over that level's non-root parent edges.
-template <class Mode>
-static void td_levels(const DeviceDag* d, u32 C, u64* row, u32 per_file = 1) {
+template <class Mode, class T = u64>
+static void td_levels(const DeviceDag* d, u32 C, T* row, u32 per_file = 1) {
   cudaStream_t st = d->stream;
   const SeedArgs seed{d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
                       (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row, (u64)C * d->R};
-  if (C != 1) {
-    GT_CUDA(cudaMemsetAsync(row, 0, sizeof(u64) * C * d->R, st));
-    if (d->n_rs) KL(k_seed<Mode>, grid_for(d->n_rs, 256), seed);
+  // C = 1 with u64 rows: the zeroing and the seeds run as phase 0 of the
+  // persistent launch
+  const bool fused_seed = C == 1 && sizeof(T) == 8;
+  if (!fused_seed) {
+    GT_CUDA(cudaMemsetAsync(row, 0, sizeof(T) * C * d->R, st));
+    if (d->n_rs) KL((k_seed<Mode, T>), grid_for(d->n_rs, 256), seed);
   }
-  // all levels in one persistent launch, grid barriers between levels (C = 1:
-  // the zeroing and the seeds run as its phase 0)
+  // all levels in one persistent launch, grid barriers between levels
   seg_reduce_levels<Mode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
-                          d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrc{row, C}, TdRows{row, C}, st, false,
-                          d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0,
-                          C == 1 ? &seed : nullptr);
+                          d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrcT<T>{row, C}, TdRowsT<T>{row, C}, st,
+                          false, d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0,
+                          fused_seed ? &seed : nullptr);
 }
 
 // Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
 // as a gather-reduce over the word-major own pairs, then the root's plain
 // words per owned segment (root_words_round, _kernels.py:175-188).
-template <class Mode>
-static void reduce_words(const DeviceDag* d, u32 C, const u64* row, u64* out, bool per_file) {
+template <class Mode, class T = u64>
+static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool per_file) {
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
-  GT_CUDA(cudaMemsetAsync(out, 0, sizeof(u64) * V * C, st));
+  GT_CUDA(cudaMemsetAsync(out, 0, sizeof(T) * V * C, st));
   seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(),
-                   d->E_own, C, RowSrc{row, C}, OutColMajor{out, V}, st);
+                   d->E_own, C, RowSrcT<T>{row, C}, OutColMajorT<T>{out, V}, st);
   if (d->n_rw)
-    KL(k_root_words<Mode>, grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
+    KL((k_root_words<Mode, T>), grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
        d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo),
        per_file ? 1 : 0, C, V, out);
 }
@@ -225,21 +228,41 @@ void td_word_counts(DeviceDag* d, DBuf& counts) {
   reduce_words<SumMode>(d, 1, w.as<u64>(), counts.as<u64>(), false);
 }
 
-// per-file counts -> dense u64[Fo][V]
-void td_file_counts(DeviceDag* d, DBuf& counts) {
+// per-file cells fit u32 when every owned file has < 2^32 words (a weight or
+// count of one file never exceeds its word count); C = 1 keeps u64 rows (the
+// fused phase-0 seed of the C = 1 level loop writes u64)
+static bool rows32(const DeviceDag* d, u32 C) { return d->cnt32 && C >= 2; }
+
+// per-file counts -> dense [Fo][V] of u64, or u32 (*is32)
+void td_file_counts(DeviceDag* d, DBuf& counts, bool* is32) {
   cudaStream_t st = d->stream;
   const u32 C = (u32)(d->file_hi - d->file_lo);
-  DBuf w(d->R * 8 * (u64)std::max<u32>(C, 1), st);
+  const u64 Cm = std::max<u32>(C, 1);
+  *is32 = rows32(d, C);
+  if (*is32) {
+    DBuf w(d->R * 4 * Cm, st);
+    td_levels<SumMode, u32>(d, C, w.as<u32>());
+    counts.alloc(d->nw * 4 * Cm + 8, st);
+    reduce_words<SumMode, u32>(d, C, w.as<u32>(), counts.as<u32>(), true);
+    return;
+  }
+  DBuf w(d->R * 8 * Cm, st);
   td_levels<SumMode>(d, C, w.as<u64>());
-  counts.alloc(d->nw * 8 * (u64)std::max<u32>(C, 1) + 8, st);
+  counts.alloc(d->nw * 8 * Cm + 8, st);
   reduce_words<SumMode>(d, C, w.as<u64>(), counts.as<u64>(), true);
 }
 
-// per-file weights only -> u64[R][Fo]
-void td_file_weights(DeviceDag* d, DBuf& w, u32* C_out) {
+// per-file weights only -> [R][Fo] of u64, or u32 (*is32)
+void td_file_weights(DeviceDag* d, DBuf& w, u32* C_out, bool* is32) {
   const u32 C = std::max<u32>(1, (u32)(d->file_hi - d->file_lo));
-  w.alloc(d->R * 8 * (u64)C, d->stream);
-  td_levels<SumMode>(d, C, w.as<u64>());
+  *is32 = rows32(d, C);
+  if (*is32) {
+    w.alloc(d->R * 4 * (u64)C, d->stream);
+    td_levels<SumMode, u32>(d, C, w.as<u32>());
+  } else {
+    w.alloc(d->R * 8 * (u64)C, d->stream);
+    td_levels<SumMode>(d, C, w.as<u64>());
+  }
   *C_out = C;
 }
 
@@ -259,7 +282,7 @@ void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out, DBuf* rows_out) {
 
 // ---- assembly -------------------------------------------------------------
 
-void assemble_counts(DeviceDag* d, const u64* dense, u64 V, u32 ncols, bool by_count, DevRecords* R) {
+void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_count, DevRecords* R, bool dense32) {
   // ncols == 0: one global table; ncols >= 1: per-file tables (file-major)
   cudaStream_t st = d->stream;
   const bool pf = ncols > 0;
@@ -273,20 +296,24 @@ void assemble_counts(DeviceDag* d, const u64* dense, u64 V, u32 ncols, bool by_c
     R->id.alloc(N * 4 + 4, st);
     R->count.alloc(N * 8 + 8, st);
     if (pf) file.alloc(N * 4 + 4, st);
-    select_nonzero_records(dense, V, N, R->id.as<u32>(), R->count.as<u64>(), pf ? file.as<u32>() : nullptr,
-                           cnt.as<u64>(), st);
+    select_nonzero_records(dense, dense32, V, N, R->id.as<u32>(), R->count.as<u64>(),
+                           pf ? file.as<u32>() : nullptr, cnt.as<u64>(), st);
     GT_CUDA(cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, st));
     GT_CUDA(cudaStreamSynchronize(st));
   } else {
     DBuf sel(N * 4 + 4, st);
-    select_nonzero_index(dense, sel.as<u32>(), cnt.as<u64>(), N, st);
+    select_nonzero_index(dense, dense32, sel.as<u32>(), cnt.as<u64>(), N, st);
     GT_CUDA(cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, st));
     GT_CUDA(cudaStreamSynchronize(st));
     R->id.alloc(n * 4 + 4, st);
     R->count.alloc(n * 8 + 8, st);
     if (pf) file.alloc(n * 4 + 4, st);
-    KL(k_records, grid_for(n, 256), sel.as<u32>(), cnt.as<u64>(), dense, V, R->id.as<u32>(),
-       R->count.as<u64>(), pf ? file.as<u32>() : nullptr);
+    if (dense32)
+      KL(k_records<u32>, grid_for(n, 256), sel.as<u32>(), cnt.as<u64>(), (const u32*)dense, V, R->id.as<u32>(),
+         R->count.as<u64>(), pf ? file.as<u32>() : nullptr);
+    else
+      KL(k_records<u64>, grid_for(n, 256), sel.as<u32>(), cnt.as<u64>(), (const u64*)dense, V, R->id.as<u32>(),
+         R->count.as<u64>(), pf ? file.as<u32>() : nullptr);
   }
   R->n = n;
   if (pf) {

@@ -12,10 +12,11 @@ struct DevRecords {
 };
 
 void td_word_counts(DeviceDag* d, DBuf& counts);
-void td_file_counts(DeviceDag* d, DBuf& counts);
+void td_file_counts(DeviceDag* d, DBuf& counts, bool* is32);
 void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW, DBuf* rows_out = nullptr);
-void td_file_weights(DeviceDag* d, DBuf& w, u32* C);
-void assemble_counts(DeviceDag* d, const u64* dense, u64 V, u32 ncols, bool by_count, DevRecords* R);
+void td_file_weights(DeviceDag* d, DBuf& w, u32* C, bool* is32);
+void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_count, DevRecords* R,
+                     bool dense32 = false);
 void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R);
 
 }  // namespace gt

@@ -48,6 +48,8 @@ def test_composed_all_tasks_match_oracle(name, scale, seed):
     ref = OracleDag(blob)
     assert dag.info["words"] == ref.info["words"] == stats["W"]
     assert dag.info["load_flags"] & 1  # short rules: the chunked rule-chain parse ran
+    import os
+    assert bool(dag.info["load_flags"] & 2) == ("GT_ROWS64" not in os.environ)  # u32 per-file cells
     for task in TASKS:
         lens = (2, 3, 4) if task in ("seqcount", "rankedinvertedindex") else (3,)
         for l in lens:
@@ -59,6 +61,19 @@ def test_composed_all_tasks_match_oracle(name, scale, seed):
                 if strategy == "bottomup" and task in ("wordcount", "sort", "invertedindex", "termvector"):
                     assert got.strategy == "bottomup"  # the pooled hash-table path ran
     dag.close()
+
+
+def test_u64_row_path_matches_oracle():
+    """The per-file rows / cells fall back to u64 when a file has >= 2^32 words;
+    GT_ROWS64=1 forces that path (read once per process: run in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, GT_ROWS64="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-x", "-q", "-p", "no:cacheprovider",
+                        "-k", "composed_all_tasks and (c4-0.0005 or c2-0.002)"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
 def _rule_lengths(blob):

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--strategy", default="auto", choices=["auto", "topdown", "bottomup"])
     ap.add_argument("--pinned", action="store_true", help="open from a pinned host copy (as bench e2e)")
+    ap.add_argument("--top", type=int, default=6, help="kernels listed per task")
     a = ap.parse_args()
     import paper_2106_06889_b200 as gt
     from paper_2106_06889_b200 import device
@@ -76,7 +77,7 @@ def main():
                 print(line, flush=True)
                 rp = dag.profile_report()
                 dag.profile(False)
-                for k, (n, ms) in sorted(rp.items(), key=lambda kv: -kv[1][1])[:6]:
+                for k, (n, ms) in sorted(rp.items(), key=lambda kv: -kv[1][1])[:a.top]:
                     print(f"      {ms:9.3f} ms {n:5d}x  {k}")
             except Exception as e:  # noqa: BLE001
                 dag.profile(False)
