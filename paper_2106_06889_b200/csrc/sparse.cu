@@ -354,7 +354,7 @@ void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
   ph.mark("weights");
   // (word, file) cells = word presence bits; word-major, files ascending
   DBuf woff, wfile, wword;
-  const u64 O = bits_to_csr(pres.as<u64>(), V, FW, 1, V, woff, wfile, &wword, st);
+  const u64 O = bits_to_csr(pres.as<u64>(), V, FW, FW, 1, woff, wfile, &wword, st);
   pres.release();
   DBuf cnt(O * 8 + 8, st);
   GT_CUDA(cudaMemsetAsync(cnt.p, 0, O * 8 + 8, st));

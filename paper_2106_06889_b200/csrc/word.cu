@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) k_seed(SeedArgs a) {
 template <class Mode, class T = u64>
 __global__ void k_root_words(const u32* __restrict__ rw_word, const u32* __restrict__ rw_seg,
                              const u32* __restrict__ rw_cnt, u64 n, u32 file_lo, u32 nseg,
-                             int per_file, u32 C, u64 V, T* __restrict__ out) {
+                             int per_file, u32 C, u64 V, int row_major, T* __restrict__ out) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     u32 sg = rw_seg[i] - file_lo;
@@ -53,7 +53,7 @@ __global__ void k_root_words(const u32* __restrict__ rw_word, const u32* __restr
       const bool is_or = std::is_same<Mode, OrMode>::value;
       const u32 col = is_or ? (sg >> 6) : sg;
       const u64 v = is_or ? (1ull << (sg & 63u)) : (u64)rw_cnt[i];
-      Mode::atomic(&out[(u64)col * V + w], v);
+      Mode::atomic(&out[row_major ? (u64)w * C + col : (u64)col * V + w], v);
     }
   }
 }
@@ -179,24 +179,31 @@ static void td_levels(const DeviceDag* d, u32 C, T* row, u32 per_file = 1) {
 // Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
 // as a gather-reduce over the word-major own pairs, then the root's plain
 // words per owned segment (root_words_round, _kernels.py:175-188).
+// out: [C][V] (file-major: the per-file count tables in render order), or
+// [V][C] with row_major (presence bitsets: a word's FW words contiguous, so
+// the team's reductions and the later bit expansion are coalesced)
 template <class Mode, class T = u64>
-static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool per_file) {
+static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool per_file, bool row_major = false) {
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
   GT_CUDA(cudaMemsetAsync(out, 0, sizeof(T) * V * C, st));
-  seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(),
-                   d->E_own, C, RowSrcT<T>{row, C}, OutColMajorT<T>{out, V}, st);
+  if (row_major)
+    seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(),
+                     d->E_own, C, RowSrcT<T>{row, C}, OutRowMajorT<T>{out, C}, st);
+  else
+    seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(),
+                     d->E_own, C, RowSrcT<T>{row, C}, OutColMajorT<T>{out, V}, st);
   if (d->n_rw)
     KL((k_root_words<Mode, T>), grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
        d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo),
-       per_file ? 1 : 0, C, V, out);
+       per_file ? 1 : 0, C, V, row_major ? 1 : 0, out);
 }
 
 void bu_root_words_dense(DeviceDag* d, u64* out) {
   cudaStream_t st = d->stream;
   if (d->n_rw)
     KL(k_root_words<SumMode>, grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
-       d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), 0, 1u, d->nw, out);
+       d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), 0, 1u, d->nw, 0, out);
 }
 
 void td_root_seeds(DeviceDag* d, u64* row) {
@@ -266,8 +273,8 @@ void td_file_weights(DeviceDag* d, DBuf& w, u32* C_out, bool* is32) {
   *C_out = C;
 }
 
-// per-file presence bitsets -> dense u64[FW][V]; the rule rows (u64[R][FW])
-// are handed back in *rows_out when requested (sparse per-file path)
+// per-file presence bitsets -> dense u64[V][FW] (row-major); the rule rows
+// (u64[R][FW]) are handed back in *rows_out when requested (sparse path)
 void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out, DBuf* rows_out) {
   cudaStream_t st = d->stream;
   const u32 Fo = (u32)(d->file_hi - d->file_lo);
@@ -275,7 +282,7 @@ void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out, DBuf* rows_out) {
   DBuf m(d->R * 8 * (u64)FW, st);
   td_levels<OrMode>(d, FW, m.as<u64>());
   pres.alloc(d->nw * 8 * (u64)FW + 8, st);
-  reduce_words<OrMode>(d, FW, m.as<u64>(), pres.as<u64>(), true);
+  reduce_words<OrMode>(d, FW, m.as<u64>(), pres.as<u64>(), true, true);
   *FW_out = FW;
   if (rows_out) *rows_out = std::move(m);
 }
@@ -357,7 +364,7 @@ void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R) {
     return;
   }
   DBuf off, files, pc;
-  bits_count(pres, V, FW, 1, V, off, pc, st);
+  bits_count(pres, V, FW, FW, 1, off, pc, st);
   DBuf nz(V + 1, st), words(V * 4 + 4, st), cnt(16, st);
   KL(k_nz_u64, grid_for(V, 256), pc.as<u64>(), V, nz.as<uint8_t>());
   select_flagged_index(nz.as<uint8_t>(), words.as<u32>(), cnt.as<u64>(), V, st);
@@ -367,7 +374,7 @@ void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R) {
   GT_CUDA(cudaMemcpyAsync(h, cnt.p, 16, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
   const u64 ng = h[0], n = h[1];
-  bits_expand(pres, V, FW, 1, V, off, n, files, nullptr, st, (u32)d->file_lo);
+  bits_expand(pres, V, FW, FW, 1, off, n, files, nullptr, st, (u32)d->file_lo);
   R->n = n;
   R->n_groups = ng;
   R->group_id.alloc(ng * 4 + 4, st);
