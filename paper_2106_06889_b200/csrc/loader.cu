@@ -791,7 +791,7 @@ __global__ void __launch_bounds__(1024) k_bu_pair(const u32* __restrict__ rule, 
                                                   int L1, u64* hgt, u64* elen) {
   cg::grid_group grid = cg::this_grid();
   const unsigned lane = threadIdx.x & 31u;
-  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 warp = (u64)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;  // round-robin over the SMs
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   for (int L = L1; L >= 0; L--) {
     const u64 a = lvl_off[L], n = lvl_off[L + 1] - a;

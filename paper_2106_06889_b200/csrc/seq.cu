@@ -76,9 +76,12 @@ __global__ void __launch_bounds__(1024) k_head_tail_levels(const u32* __restrict
                                                            u32* hl, u32* tl) {
   cg::grid_group grid = cg::this_grid();
   const u64 stride = (u64)gridDim.x * blockDim.x;
+  // 32 consecutive rules per warp, warps round-robin over the SMs (a small
+  // level reaches every SM instead of the first blocks)
+  const u64 t0 = ((u64)(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32 + (threadIdx.x & 31u);
   for (int L = 1; L <= nl; L++) {
     const u64 lo = off[L], hi = off[L + 1];
-    for (u64 i = lo + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
+    for (u64 i = lo + t0; i < hi; i += stride) {
       const u32 r = order[i];
       if (r != 0) head_tail_rule(r, body, boff, nw, base, exp_len, m, H, T, hl, tl);
     }
