@@ -148,6 +148,33 @@ __global__ void k_list_len(const u32* __restrict__ key, u64 n, const u64* __rest
     deg[i] = off[key[i] + 1] - off[key[i]];
 }
 
+// Expansion of a group list (group e = one edge or own pair, owning the
+// files of its source rule, pos = exclusive scan of the group sizes): each
+// thread takes kExp consecutive items, locates its first group once (binary
+// search over pos) and then walks: within a group the source files ascend,
+// so the target slot advances by a linear merge through the target's
+// (ascending, superset) file list instead of a binary search per item.
+constexpr u64 kExp = 16;
+
+// first index in [lo, hi) with a[idx] >= x (a ascending), galloping from lo:
+// O(log distance), so a sparse source list walking a dense target list
+// costs no more than the binary searches it replaces
+__device__ __forceinline__ u64 gallop_u32(const u32* a, u64 lo, u64 hi, u32 x) {
+  if (lo >= hi || a[lo] >= x) return lo;
+  u64 step = 1, prev = lo;
+  while (lo + step < hi && a[lo + step] < x) {
+    prev = lo + step;
+    step <<= 1;
+  }
+  u64 l = prev + 1, h = lo + step < hi ? lo + step : hi;
+  while (l < h) {
+    const u64 m = (l + h) >> 1;
+    if (a[m] < x) l = m + 1;
+    else h = m;
+  }
+  return l;
+}
+
 // one top-down level: for every edge (c, p, f) and every file of p:
 //   w(c, file) += f · w(p, file)
 __global__ void k_sparse_level(const u32* __restrict__ child, const u32* __restrict__ par,
@@ -156,20 +183,37 @@ __global__ void k_sparse_level(const u32* __restrict__ child, const u32* __restr
                                const u32* __restrict__ file, u64* __restrict__ wt) {
   if (!n) return;
   const u64 T = pos[n - 1] + deg[n - 1];
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += stride) {
-    const u64 e = find_group(pos, n, i);
-    const u32 p = par[e], c = child[e];
-    const u64 k = off[p] + (i - pos[e]);
-    const u64 v = (u64)freq[e] * wt[k];
-    const u64 a = off[c];
-    const u64 q = a + lower_bound_u32(file + a, off[c + 1] - a, file[k]);
-    atomicAdd((unsigned long long*)&wt[q], (unsigned long long)v);
+  const u64 stride = (u64)gridDim.x * blockDim.x * kExp;
+  for (u64 i0 = ((u64)blockIdx.x * blockDim.x + threadIdx.x) * kExp; i0 < T; i0 += stride) {
+    const u64 i1 = i0 + kExp < T ? i0 + kExp : T;
+    u64 e = find_group(pos, n, i0);
+    u64 gend = pos[e] + deg[e];
+    u32 p = par[e], c = child[e];
+    u64 f = freq[e];
+    u64 k = off[p] + (i0 - pos[e]);
+    u64 q = off[c] + lower_bound_u32(file + off[c], off[c + 1] - off[c], file[k]);
+    for (u64 i = i0; i < i1; i++) {
+      if (i == gend) {  // next non-empty group
+        do e++;
+        while (deg[e] == 0);
+        gend = pos[e] + deg[e];
+        p = par[e];
+        c = child[e];
+        f = freq[e];
+        k = off[p];
+        q = off[c] + lower_bound_u32(file + off[c], off[c + 1] - off[c], file[k]);
+      } else if (i != i0) {
+        k++;
+        q = gallop_u32(file, q, off[c + 1], file[k]);
+      }
+      atomicAdd((unsigned long long*)&wt[q], (unsigned long long)(f * wt[k]));
+    }
   }
 }
 
 // term-vector cells: every own pair (w, r, f) adds f · w(r, file) to cell
-// (w, file) for every file of r
+// (w, file) for every file of r (chunked walk as k_sparse_level; the word's
+// file list is a superset of the rule's)
 __global__ void k_tv_own(const u32* __restrict__ ow_word, const u32* __restrict__ ow_rule,
                          const u32* __restrict__ ow_freq, u64 n, const u64* __restrict__ pos,
                          const u64* __restrict__ deg, const u64* __restrict__ off,
@@ -178,14 +222,31 @@ __global__ void k_tv_own(const u32* __restrict__ ow_word, const u32* __restrict_
                          u64* __restrict__ cnt) {
   if (!n) return;
   const u64 T = pos[n - 1] + deg[n - 1];
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += stride) {
-    const u64 e = find_group(pos, n, i);
-    const u32 r = ow_rule[e], w = ow_word[e];
-    const u64 k = off[r] + (i - pos[e]);
-    const u64 a = woff[w];
-    const u64 q = a + lower_bound_u32(wfile + a, woff[w + 1] - a, file[k]);
-    atomicAdd((unsigned long long*)&cnt[q], (unsigned long long)((u64)ow_freq[e] * wt[k]));
+  const u64 stride = (u64)gridDim.x * blockDim.x * kExp;
+  for (u64 i0 = ((u64)blockIdx.x * blockDim.x + threadIdx.x) * kExp; i0 < T; i0 += stride) {
+    const u64 i1 = i0 + kExp < T ? i0 + kExp : T;
+    u64 e = find_group(pos, n, i0);
+    u64 gend = pos[e] + deg[e];
+    u32 r = ow_rule[e], w = ow_word[e];
+    u64 f = ow_freq[e];
+    u64 k = off[r] + (i0 - pos[e]);
+    u64 q = woff[w] + lower_bound_u32(wfile + woff[w], woff[w + 1] - woff[w], file[k]);
+    for (u64 i = i0; i < i1; i++) {
+      if (i == gend) {
+        do e++;
+        while (deg[e] == 0);
+        gend = pos[e] + deg[e];
+        r = ow_rule[e];
+        w = ow_word[e];
+        f = ow_freq[e];
+        k = off[r];
+        q = woff[w] + lower_bound_u32(wfile + woff[w], woff[w + 1] - woff[w], file[k]);
+      } else if (i != i0) {
+        k++;
+        q = gallop_u32(wfile, q, woff[w + 1], file[k]);
+      }
+      atomicAdd((unsigned long long*)&cnt[q], (unsigned long long)(f * wt[k]));
+    }
   }
 }
 
