@@ -552,7 +552,8 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   ssrc.release();
   rid.release();
   ph.mark("cells");
-  const u64 Wt = d->W;
+  // (gram, file) counts never exceed the file's words: fewer sort-key bits
+  const u64 Wt = d->max_file_tokens ? d->max_file_tokens : d->W;
   const int CB = std::max(1, bitlen(Wt));
   const bool by_file = task == GT_SEQCOUNT;
   const int MB = by_file ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns));

@@ -434,8 +434,8 @@ void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
   ph.mark("cells");
   s = SparseW();
   // file-major, (-count, word) within a file: one stable radix sort of the
-  // word-major cells on (file, W - count)
-  const u64 W = d->W;
+  // word-major cells on (file, W - count); W = the longest file's words
+  const u64 W = d->max_file_tokens ? d->max_file_tokens : d->W;
   const int CB = std::max(1, bitlen(W));
   const int FB = std::max(1, bitlen(Fo ? Fo - 1 : 0));
   DBuf k1(O * 8 + 8, st), k2(O * 8 + 8, st);

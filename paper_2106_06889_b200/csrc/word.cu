@@ -329,7 +329,8 @@ void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_
     R->n_groups = ncols;
   }
   if (by_count && n) {
-    const u64 W = d->W;
+    // a per-file count never exceeds its file's words: fewer key bits
+    const u64 W = pf && d->max_file_tokens ? d->max_file_tokens : d->W;
     const int CB = std::max(1, bitlen(W));
     const int FB = pf ? bitlen(ncols - 1) : 0;
     DBuf k1(n * 8, st), k2(n * 8, st), id2(n * 4, st);
