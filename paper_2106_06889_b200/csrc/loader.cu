@@ -87,8 +87,9 @@ __global__ void k_csr_offsets(const u32* key, u64 n, u64 R, u64* off) {
 }
 
 // CSR row offsets of a sorted key list in one coalesced pass: element i
-// writes the offsets of the rows (key[i-1], key[i]] (O(n + R); the binary
-// search above is kept for a handful of rows over long lists)
+// writes the offsets of the rows (key[i-1], key[i]] (O(n + R), for keys
+// dense in [0, R): a gap is filled by one thread; sparse keys use the
+// per-row binary search above)
 __global__ void k_csr_offsets_lin(const u32* __restrict__ key, u64 n, u64 R, u64* off) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) {
@@ -1292,7 +1293,10 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     occ_list(rkey, isr, std::max(1, bitlen(R - 1)), d->rs_rule, d->rs_seg, d->rs_cnt, &d->n_rs);
     occ_list(wkey, isw, std::max(1, bitlen(nw ? nw - 1 : 0)), d->rw_word, d->rw_seg, d->rw_cnt, &d->n_rw);
     d->rs_off.alloc((R + 1) * 8, st);
-    LAUNCH(k_csr_offsets, R + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
+    if (d->n_rs * 4 >= R)  // dense keys: one coalesced pass; sparse: a search per row
+      LAUNCH(k_csr_offsets_lin, d->n_rs + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
+    else
+      LAUNCH(k_csr_offsets, R + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
       GT_CUDA(cudaStreamSynchronize(st));
     } catch (const Error& e) {
       root_err = e;
@@ -1446,7 +1450,10 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     sort_pairs_u32_u64(d->own_ids.as<u32>(), d->ow_word.as<u32>(), v1.as<u64>(), v2.as<u64>(), Eo,
                        std::max(1, bitlen(nw ? nw - 1 : 0)), st);
     LAUNCH(k_unpack2, Eo, v2.as<u64>(), Eo, d->ow_rule.as<u32>(), d->ow_freq.as<u32>());
-    LAUNCH(k_csr_offsets_lin, Eo + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
+    if (Eo * 4 >= nw)  // dense keys: one coalesced pass; sparse: a search per row
+      LAUNCH(k_csr_offsets_lin, Eo + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
+    else
+      LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
   }
 
   // ---- parents: stable sort of sub pairs by child -------------------------
