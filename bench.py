@@ -388,7 +388,8 @@ def main():
         n_l, ms_l = named[k_dom]
         b = alg_bytes(k_dom, info, Fo)  # per step
         ach = b * K / (ms_l / 1e3) / 1e9
-        traffic, traffic_src = ncu_traffic(k_dom)
+        # the committed ncu capture is of the default workload only
+        traffic, traffic_src = ncu_traffic(k_dom) if args.config == "c2" and args.scale == 1.0 else (None, None)
         roof = {"bound": "hbm", "kernel": k_dom, "launches_per_step": n_l / K,
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "traffic_unit": "bytes per step (ncu dram read+write)",
