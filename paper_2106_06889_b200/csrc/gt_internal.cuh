@@ -120,6 +120,12 @@ struct DeviceDag {
   // level-ordered edge lists for the segmented gather-reduce (segreduce.cuh)
   //   te_*: non-root parent edges (child, parent, freq) by (td level, child, parent)
   //   be_*: child edges (rule, child, freq) by (bu level, rule, child)
+  // top-down rows are indexed by `tid` (rules numbered by top-down level,
+  // ascending rule id within a level: a level's rows are contiguous, so the
+  // reductions of a level and the parent gathers of the next stay in L2);
+  // te_child / te_par, rs_rule_t and ow_rule_t hold tids
+  DBuf tid;                 // u32[R]: rule -> tid
+  DBuf rs_rule_t, ow_rule_t;
   DBuf te_child, te_par, te_freq;
   std::vector<u64> te_off;  // host: td level L items [te_off[L], te_off[L+1])
   DBuf te_off_dev;          // device copy (persistent level loops)
@@ -139,7 +145,7 @@ struct DeviceDag {
                          &num_in, &num_out, &exp_len, &td_level, &bu_level, &seg_lo, &seg_hi,
                          &seg_tokens, &ow_word, &ow_rule, &ow_freq, &ow_off, &rs_rule, &rs_seg,
                          &rs_cnt, &rs_off, &rw_word, &rw_seg, &rw_cnt, &td.order, &bu.order,
-                         &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts,
+                         &tid, &rs_rule_t, &ow_rule_t, &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts,
                          &te_off_dev, &be_off_dev};
     u64 t = 0;
     for (const DBuf* b : all) t += b->bytes;

@@ -119,6 +119,24 @@ __global__ void k_pack3(const u32* __restrict__ a, const u32* __restrict__ b, co
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = U3{a[i], b[i], c[i]};
 }
 
+// (map[a], map[b], c) triples (map = the tid numbering; nullptr: identity)
+__global__ void k_pack3_map(const u32* __restrict__ a, const u32* __restrict__ b, const u32* __restrict__ c, u64 n,
+                            const u32* __restrict__ map, U3* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = U3{map[a[i]], map[b[i]], c[i]};
+}
+
+__global__ void k_map_u32(const u32* __restrict__ in, u64 n, const u32* __restrict__ map, u32* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = map[in[i]];
+}
+
+__global__ void k_rank_of(const u32* __restrict__ order, u64 n, u32* rank) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) rank[order[i]] = (u32)i;
+}
+
 __global__ void k_unpack3(const U3* __restrict__ in, u64 n, u32* a, u32* b, u32* c) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -1571,13 +1589,14 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   u64* stage = stage_host.get(2 * ((u64)ntd + 3) + 3);
   auto level_edges = [&](const u32* group_of, const uint8_t* keep, const u32* lvl, int nl,
                          const u32* a_src, const u32* b_src, const u32* f_src, DBuf& oa, DBuf& ob,
-                         DBuf& of, u64* off_stage, DBuf& off_dev) {
+                         DBuf& of, u64* off_stage, DBuf& off_dev, const u32* map) {
     // every edge is sorted (dropped ones under key nl + 1, after all levels),
     // so no count has to come back to the host first
     // the edge triples travel with the level keys (one radix pass for <= 255 levels)
     DBuf key(Es * 4 + 4, st), key2(Es * 4 + 4, st), v1(Es * 12 + 12, st), v2(Es * 12 + 12, st);
     LAUNCH(k_edge_level_keys2, Es, group_of, keep, lvl, (u32)nl + 1, Es, key.as<u32>());
-    LAUNCH(k_pack3, Es, a_src, b_src, f_src, Es, v1.as<U3>());
+    if (map) LAUNCH(k_pack3_map, Es, a_src, b_src, f_src, Es, map, v1.as<U3>());
+    else LAUNCH(k_pack3, Es, a_src, b_src, f_src, Es, v1.as<U3>());
     sort_pairs_u32_u3(key.as<u32>(), key2.as<u32>(), v1.as<U3>(), v2.as<U3>(), Es,
                       std::max(1, bitlen((u64)nl + 1)), st);
     oa.alloc(Es * 4 + 16, st);  // + 16: the TMA-staged level loop copies whole 16-byte words
@@ -1589,20 +1608,30 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     GT_CUDA(cudaMemcpyAsync(off_stage, koff.p, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
     off_dev = std::move(koff);
   };
+  // tid: rules numbered by top-down level (stable: ascending rule id within
+  // a level, so the td edge lists stay sorted by destination)
+  {
+    DBuf iota(R * 4, st), k2(R * 4, st), ord(R * 4, st);
+    LAUNCH(k_iota_u32, R, iota.as<u32>(), R);
+    sort_pairs_u32_u32(d->td_level.as<u32>(), k2.as<u32>(), iota.as<u32>(), ord.as<u32>(), R,
+                       std::max(1, bitlen((u64)ntd)), st);
+    d->tid.alloc(R * 4, st);
+    LAUNCH(k_rank_of, R, ord.as<u32>(), R, d->tid.as<u32>());
+  }
   {
     // td: par entries (grouped by child) whose parent is not the root
     DBuf keep(Es + 1, st);
     LAUNCH(k_flag_nonzero_u32, Es, d->par_ids.as<u32>(), Es, keep.as<uint8_t>());
     level_edges(child_sorted.as<u32>(), keep.as<uint8_t>(), d->td_level.as<u32>(), ntd,
                 child_sorted.as<u32>(), d->par_ids.as<u32>(), d->par_freqs.as<u32>(), d->te_child,
-                d->te_par, d->te_freq, stage, d->te_off_dev);
+                d->te_par, d->te_freq, stage, d->te_off_dev, d->tid.as<u32>());
     // be: sub entries (grouped by rule) by the rule's TOP-DOWN level; walked
     // in decreasing level order every child is finished before its parents
     // (a child's td level exceeds each parent's), which is all the bottom-up
     // sums need.  The root (td level 0) comes last.
     level_edges(sub_rule.as<u32>(), nullptr, d->td_level.as<u32>(), ntd, sub_rule.as<u32>(),
                 d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), d->be_rule, d->be_child, d->be_freq,
-                stage + (ntd + 3), d->be_off_dev);
+                stage + (ntd + 3), d->be_off_dev, nullptr);
   }
   sub_rule.release();
   child_sorted.release();
@@ -1668,6 +1697,20 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     GT_CUDA(cudaMemcpyAsync(stage + 2 * ((u64)ntd + 3) + 2, mx.p, 8, cudaMemcpyDeviceToHost, st));
   }
   ph.mark("root side joined");
+
+  // the seeds' and the reduce's rule ids in tid numbering (after the own
+  // transpose on the side stream)
+  {
+    cudaEvent_t ev;
+    GT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    GT_CUDA(cudaEventRecord(ev, s_own));
+    GT_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    cudaEventDestroy(ev);
+    d->rs_rule_t.alloc(d->n_rs * 4 + 4, st);
+    d->ow_rule_t.alloc(Eo * 4 + 4, st);
+    if (d->n_rs) LAUNCH(k_map_u32, d->n_rs, d->rs_rule.as<u32>(), d->n_rs, d->tid.as<u32>(), d->rs_rule_t.as<u32>());
+    if (Eo) LAUNCH(k_map_u32, Eo, d->ow_rule.as<u32>(), Eo, d->tid.as<u32>(), d->ow_rule_t.as<u32>());
+  }
 
   stream_sync(st);
   stream_sync(s_own);

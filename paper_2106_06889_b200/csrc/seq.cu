@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(1024) k_head_tail_levels(const u32* __restrict
 struct WinCtx {
   const u32* body;
   const u32* owner;
+  const u32* tid;  // rule -> tid (the weight rows' numbering)
   const u64* boff;
   const u32* root_seg;
   const u32 *H, *T, *hl, *tl;
@@ -108,7 +109,7 @@ __device__ __forceinline__ u32 windows_at(const WinCtx& c, u64 p, u32* src, u32*
     if (sg >= c.nseg) return 0;
     *src = c.R + sg;
   } else {
-    *src = r;
+    *src = c.tid[r];
   }
   const u32 s = c.body[p];
   u32 tlen;
@@ -451,7 +452,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
 
   ph.mark("weights");
   // phase 2: windows attributed per body position (two passes + scan)
-  WinCtx c{d->body.as<u32>(), d->pos_owner.as<u32>(), d->boff.as<u64>(), d->root_seg.as<u32>(),
+  WinCtx c{d->body.as<u32>(), d->pos_owner.as<u32>(), d->tid.as<u32>(), d->boff.as<u64>(), d->root_seg.as<u32>(),
            H.as<u32>(), T.as<u32>(), hl.as<u32>(), tl.as<u32>(), nw, base, l, m, (u32)wbits,
            (u32)R, (u32)d->file_lo, Fo};
   DBuf cnt(E * 8 + 8, st), off(E * 8 + 8, st);

@@ -387,7 +387,7 @@ void sparse_file_weights(DeviceDag* d, SparseW* s, DBuf* word_pres, u32* FW_out)
   GT_CUDA(cudaMemsetAsync(s->wt.p, 0, s->P * 8 + 8, st));
   const u32 nseg = (u32)(d->file_hi - d->file_lo);
   if (d->n_rs)
-    SK(k_sparse_seed, d->n_rs, d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs,
+    SK(k_sparse_seed, d->n_rs, d->rs_rule_t.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs,
        (u32)d->file_lo, nseg, s->off.as<u64>(), s->file.as<u32>(), s->wt.as<u64>());
   ph.mark("pairs+seeds");
   const u64 Etd = d->te_off.empty() ? 0 : d->te_off.back();
@@ -422,9 +422,9 @@ void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
   const u64 Eo = d->E_own;
   if (Eo) {
     DBuf deg(Eo * 8 + 8, st), pos(Eo * 8 + 8, st);
-    SK(k_list_len, Eo, d->ow_rule.as<u32>(), Eo, s.off.as<u64>(), deg.as<u64>());
+    SK(k_list_len, Eo, d->ow_rule_t.as<u32>(), Eo, s.off.as<u64>(), deg.as<u64>());
     exclusive_scan_u64(deg.as<u64>(), pos.as<u64>(), Eo, st);
-    SKE(k_tv_own, d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), Eo, pos.as<u64>(),
+    SKE(k_tv_own, d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), Eo, pos.as<u64>(),
         deg.as<u64>(), s.off.as<u64>(), s.file.as<u32>(), s.wt.as<u64>(), woff.as<u64>(),
         wfile.as<u32>(), cnt.as<u64>());
   }

@@ -160,7 +160,8 @@ __global__ void k_ii_emit(const u64* __restrict__ pres, u64 V, const u64* __rest
 template <class Mode, class T = u64>
 static void td_levels(const DeviceDag* d, u32 C, T* row, u32 per_file = 1) {
   cudaStream_t st = d->stream;
-  const SeedArgs seed{d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
+  // rows indexed by tid (DeviceDag::tid): seeds and edges carry tids
+  const SeedArgs seed{d->rs_rule_t.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
                       (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row, (u64)C * d->R};
   // C = 1 with u64 rows: the zeroing and the seeds run as phase 0 of the
   // persistent launch
@@ -188,10 +189,10 @@ static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool p
   const u64 V = d->nw;
   GT_CUDA(cudaMemsetAsync(out, 0, sizeof(T) * V * C, st));
   if (row_major)
-    seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(),
+    seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
                      d->E_own, C, RowSrcT<T>{row, C}, OutRowMajorT<T>{out, C}, st);
   else
-    seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(),
+    seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
                      d->E_own, C, RowSrcT<T>{row, C}, OutColMajorT<T>{out, V}, st);
   if (d->n_rw)
     KL((k_root_words<Mode, T>), grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
