@@ -106,6 +106,16 @@ __device__ __forceinline__ void load_pair(const RowSrcT<u32>& in, u32 s, u32 col
   *b = v.y;
 }
 
+// row sources whose paired path loads the items' metadata one per lane
+template <class Src>
+struct LaneMeta {
+  static constexpr bool value = false;
+};
+template <class T>
+struct LaneMeta<RowSrcT<T>> {
+  static constexpr bool value = true;
+};
+
 // ---- output address functors --------------------------------------------------
 template <class T>
 struct OutRowMajorT {  // out[dst*C + col]
@@ -219,9 +229,9 @@ __device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const 
   constexpr int B = 8;
   const u64 teams = nthreads / G;
   const u32 tl = threadIdx.x % G;
-  if (C == 2u * G) {
-    // two ADJACENT columns per lane: the team reads a whole row with 16-byte
-    // loads (C = 64: one 512-byte access per item), 8 items in flight
+  if (C == 2u * G && !LaneMeta<Src>::value) {
+    // (gram-run rows: the per-item metadata loads are broadcast; measured
+    // faster there than the lane-loaded form below)
     constexpr int BB = 8;
     const u32 c0 = 2 * tl;
     for (u64 t = gtid / G; t * K < n; t += teams) {
@@ -257,6 +267,64 @@ __device__ __forceinline__ void segredG_body(const u32* __restrict__ dst, const 
           }
           acc0 = Mode::merge(acc0, v0[j]);
           acc1 = Mode::merge(acc1, v1[j]);
+        }
+      }
+      Mode::atomic(out(cd, c0), acc0);
+      Mode::atomic(out(cd, c0 + 1), acc1);
+    }
+    return;
+  }
+  if (C == 2u * G) {
+    // two ADJACENT columns per lane: the team reads a whole row with one
+    // vector load per lane (C = 64: one 512 / 256-byte access per item).  The
+    // items' (dst, src, freq) are loaded G at a time, one per lane, and
+    // broadcast by shuffles, so only the row gathers (BB in flight) remain
+    // on each group's dependent path.
+    constexpr int BB = 8;
+    const u32 c0 = 2 * tl;
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned tmask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << (lane & ~(unsigned)(G - 1));
+    for (u64 t = gtid / G; t * K < n; t += teams) {
+      const u64 a = t * K, b = a + K < n ? a + K : n;
+      u32 cd = dst[a];
+      u64 acc0 = 0, acc1 = 0;
+      for (u64 i0 = a; i0 < b; i0 += G) {
+        const u64 im = i0 + tl;
+        const bool okm = im < b;
+        const u32 md = okm ? dst[im] : 0xFFFFFFFFu;
+        const u32 ms = okm ? src[im] : 0u;
+        const u32 mf = okm ? item_freq(freq, im) : 0u;
+#pragma unroll 1
+        for (int g = 0; g < G; g += BB) {
+          u32 dd[BB];
+          u64 v0[BB], v1[BB];
+#pragma unroll
+          for (int j = 0; j < BB; j++) {
+            dd[j] = __shfl_sync(tmask, md, g + j, G);
+            const u32 sj = __shfl_sync(tmask, ms, g + j, G);
+            const u32 fj = __shfl_sync(tmask, mf, g + j, G);
+            u64 x = 0, y = 0;
+            if (dd[j] != 0xFFFFFFFFu) {
+              load_pair(in, sj, c0, &x, &y);
+              x = Mode::combine(fj, x);
+              y = Mode::combine(fj, y);
+            }
+            v0[j] = x;
+            v1[j] = y;
+          }
+#pragma unroll
+          for (int j = 0; j < BB; j++) {
+            if (dd[j] == 0xFFFFFFFFu) break;
+            if (dd[j] != cd) {
+              Mode::atomic(out(cd, c0), acc0);
+              Mode::atomic(out(cd, c0 + 1), acc1);
+              acc0 = acc1 = 0;
+              cd = dd[j];
+            }
+            acc0 = Mode::merge(acc0, v0[j]);
+            acc1 = Mode::merge(acc1, v1[j]);
+          }
+          if (dd[BB - 1] == 0xFFFFFFFFu) break;  // past the chunk end (team-uniform)
         }
       }
       Mode::atomic(out(cd, c0), acc0);
