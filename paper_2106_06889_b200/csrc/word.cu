@@ -61,11 +61,6 @@ __global__ void k_root_words(const u32* __restrict__ rw_word, const u32* __restr
 // ---------------------------------------------------------------------------
 // assembly
 // ---------------------------------------------------------------------------
-__global__ void k_nonzero_flags(const u64* v, u64 n, uint8_t* f) {
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f[i] = v[i] != 0;
-}
-
 // records from selected indices: id = idx % V (word), count, file = idx / V
 template <class T>
 __global__ void k_records(const u32* sel, const u64* nsel, const T* vals, u64 V, u32* id,
