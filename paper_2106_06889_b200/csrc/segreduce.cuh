@@ -539,14 +539,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
                                                           Out out) {
   cg::grid_group grid = cg::this_grid();
   if (seed.row) {  // phase 0: clear the rows, then the root seeds
-    const u64 gt0 = (u64)blockIdx.x * blockDim.x + threadIdx.x, nt0 = (u64)gridDim.x * blockDim.x;
     u64* zr = reinterpret_cast<u64*>(seed.row);
-    for (u64 i = gt0; i < seed.zero_n; i += nt0) zr[i] = 0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < seed.zero_n; i += (u64)gridDim.x * blockDim.x)
+      zr[i] = 0;
     grid.sync();
     seed_rows_body<Mode>(seed);
     grid.sync();
   }
-  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   const u64 nthreads = (u64)gridDim.x * blockDim.x;
   // warps numbered round-robin over the blocks: a level smaller than the
   // grid is spread over every SM instead of filling the first blocks
