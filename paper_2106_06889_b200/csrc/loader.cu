@@ -1068,11 +1068,14 @@ struct PinnedU64 {  // grow-only pinned host buffer (deferred read-backs)
 // pinned 64 MB staging buffers by several host threads while the copy engine
 // drains the other buffer (C4, 227 MB: pageable gt_open 31 -> 20 ms).
 static void h2d_blob(void* dst, const uint8_t* src, size_t n, cudaStream_t st) {
-  cudaPointerAttributes at{};
-  const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
-  if (!pinned) cudaGetLastError();
   constexpr size_t kCh = 64ull << 20;
-  if (pinned || n < (32ull << 20)) {
+  bool direct = n < (32ull << 20);
+  if (!direct) {
+    cudaPointerAttributes at{};
+    direct = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    if (!direct) cudaGetLastError();
+  }
+  if (direct) {
     GT_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
     return;
   }
