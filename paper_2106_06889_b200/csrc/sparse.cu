@@ -89,15 +89,39 @@ __global__ void k_expand_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u
         const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
         if (lane >= (unsigned)d) inc += t;
       }
-      u64 q = o + inc - c;
-      while (b) {
-        const int t = __ffsll((long long)b) - 1;
-        col[q] = col_base + j * 64u + (u32)t;
-        if (row_of) row_of[q] = (u32)r;
-        q++;
-        b &= b - 1;
+      const u32 tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
+      if (tot >= 256) {
+        // dense step: the warp writes one word's set bits at a time, lane l
+        // owning bits l and l + 32, so consecutive outputs come from
+        // consecutive lanes (a lane walking its own dense word would spread
+        // each store instruction over 32 sectors)
+        const u32 ex = inc - c;
+        for (int w = 0; w < 32; w++) {
+          const u64 bw = __shfl_sync(0xFFFFFFFFu, b, w);
+          if (!bw) continue;
+          const u64 ow = o + __shfl_sync(0xFFFFFFFFu, ex, w);
+          const u32 jw = j0 + (u32)w;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const u32 t = lane + 32u * h;
+            if ((bw >> t) & 1ull) {
+              const u64 q = ow + (u64)__popcll(bw & ((1ull << t) - 1ull));
+              col[q] = col_base + jw * 64u + t;
+              if (row_of) row_of[q] = (u32)r;
+            }
+          }
+        }
+      } else {
+        u64 q = o + inc - c;
+        while (b) {
+          const int t = __ffsll((long long)b) - 1;
+          col[q] = col_base + j * 64u + (u32)t;
+          if (row_of) row_of[q] = (u32)r;
+          q++;
+          b &= b - 1;
+        }
       }
-      o += __shfl_sync(0xFFFFFFFFu, inc, 31);
+      o += tot;
     }
   }
 }
