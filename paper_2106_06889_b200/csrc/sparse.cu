@@ -290,20 +290,23 @@ __global__ void k_tv_root(const u32* __restrict__ rw_word, const u32* __restrict
 }
 
 // (file, W - count) sort keys of the word-major cells
+template <class K>
 __global__ void k_tv_keys(const u32* __restrict__ wfile, const u64* __restrict__ cnt, u64 n, u64 W,
-                          int CB, u64* __restrict__ key) {
+                          int CB, K* __restrict__ key) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    key[i] = ((u64)wfile[i] << CB) | (W - cnt[i]);
+    key[i] = (K)(((u64)wfile[i] << CB) | (W - cnt[i]));
 }
 
-__global__ void k_tv_unkey(const u64* __restrict__ key, u64 n, u64 W, int CB, u64* __restrict__ cnt,
+template <class K>
+__global__ void k_tv_unkey(const K* __restrict__ key, u64 n, u64 W, int CB, u64* __restrict__ cnt,
                            u32* __restrict__ file) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const u64 m = (1ull << CB) - 1;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    cnt[i] = W - (key[i] & m);
-    file[i] = (u32)(key[i] >> CB);
+    const u64 k = key[i];
+    cnt[i] = W - (k & m);
+    file[i] = (u32)(k >> CB);
   }
 }
 
@@ -463,12 +466,19 @@ void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
   const int CB = std::max(1, bitlen(W));
   const int FB = std::max(1, bitlen(Fo ? Fo - 1 : 0));
   DBuf k1(O * 8 + 8, st), k2(O * 8 + 8, st);
-  SK(k_tv_keys, O, wfile.as<u32>(), cnt.as<u64>(), O, W, CB, k1.as<u64>());
   Rr->n = O;
   Rr->id.alloc(O * 4 + 4, st);
-  sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), wword.as<u32>(), Rr->id.as<u32>(), O, CB + FB, st);
-  Rr->count = std::move(cnt);
-  SK(k_tv_unkey, O, k2.as<u64>(), O, W, CB, Rr->count.as<u64>(), wfile.as<u32>());
+  if (CB + FB <= 32) {  // u32 keys (C3: 13 + 17 bits)
+    SK(k_tv_keys<u32>, O, wfile.as<u32>(), cnt.as<u64>(), O, W, CB, k1.as<u32>());
+    sort_pairs_u32_u32(k1.as<u32>(), k2.as<u32>(), wword.as<u32>(), Rr->id.as<u32>(), O, CB + FB, st);
+    Rr->count = std::move(cnt);
+    SK(k_tv_unkey<u32>, O, k2.as<u32>(), O, W, CB, Rr->count.as<u64>(), wfile.as<u32>());
+  } else {
+    SK(k_tv_keys<u64>, O, wfile.as<u32>(), cnt.as<u64>(), O, W, CB, k1.as<u64>());
+    sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), wword.as<u32>(), Rr->id.as<u32>(), O, CB + FB, st);
+    Rr->count = std::move(cnt);
+    SK(k_tv_unkey<u64>, O, k2.as<u64>(), O, W, CB, Rr->count.as<u64>(), wfile.as<u32>());
+  }
   Rr->n_groups = Fo;
   Rr->group_off.alloc(((u64)Fo + 1) * 8, st);
   SK(k_csr_offsets, (u64)Fo + 1, wfile.as<u32>(), O, (u64)Fo, Rr->group_off.as<u64>());

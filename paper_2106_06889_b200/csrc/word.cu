@@ -76,17 +76,20 @@ __global__ void k_records(const u32* sel, const u64* nsel, const T* vals, u64 V,
 }
 
 // sort keys: (file << CB) | (W - count)  -> (file asc, count desc), stable on word
-__global__ void k_sort_keys(const u64* cnt, const u32* file, u64 n, u64 W, int CB, u64* key) {
+// sort keys (file << CB) | (W - count): K = u32 when they fit 32 bits
+template <class K>
+__global__ void k_sort_keys(const u64* cnt, const u32* file, u64 n, u64 W, int CB, K* key) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    key[i] = ((file ? (u64)file[i] : 0ull) << CB) | (W - cnt[i]);
+    key[i] = (K)(((file ? (u64)file[i] : 0ull) << CB) | (W - cnt[i]));
 }
 
-__global__ void k_unkey(const u64* key, u64 n, u64 W, int CB, u64* cnt) {
+template <class K>
+__global__ void k_unkey(const K* key, u64 n, u64 W, int CB, u64* cnt) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   u64 m = (CB >= 64) ? ~0ull : ((1ull << CB) - 1);
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    cnt[i] = W - (key[i] & m);
+    cnt[i] = W - ((u64)key[i] & m);
 }
 
 __global__ void k_nz_u64(const u64* v, u64 n, uint8_t* f) {
@@ -330,9 +333,17 @@ void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_
     const int CB = std::max(1, bitlen(W));
     const int FB = pf ? bitlen(ncols - 1) : 0;
     DBuf k1(n * 8, st), k2(n * 8, st), id2(n * 4, st);
-    KL(k_sort_keys, grid_for(n, 256), R->count.as<u64>(), pf ? file.as<u32>() : nullptr, n, W, CB, k1.as<u64>());
-    sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), R->id.as<u32>(), id2.as<u32>(), n, CB + FB, st);
-    KL(k_unkey, grid_for(n, 256), k2.as<u64>(), n, W, CB, R->count.as<u64>());
+    if (CB + FB <= 32) {  // u32 keys: half the radix key traffic
+      KL(k_sort_keys<u32>, grid_for(n, 256), R->count.as<u64>(), pf ? file.as<u32>() : nullptr, n, W, CB,
+         k1.as<u32>());
+      sort_pairs_u32_u32(k1.as<u32>(), k2.as<u32>(), R->id.as<u32>(), id2.as<u32>(), n, CB + FB, st);
+      KL(k_unkey<u32>, grid_for(n, 256), k2.as<u32>(), n, W, CB, R->count.as<u64>());
+    } else {
+      KL(k_sort_keys<u64>, grid_for(n, 256), R->count.as<u64>(), pf ? file.as<u32>() : nullptr, n, W, CB,
+         k1.as<u64>());
+      sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), R->id.as<u32>(), id2.as<u32>(), n, CB + FB, st);
+      KL(k_unkey<u64>, grid_for(n, 256), k2.as<u64>(), n, W, CB, R->count.as<u64>());
+    }
     R->id = std::move(id2);
   }
 }
