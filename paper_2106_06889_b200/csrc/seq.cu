@@ -553,8 +553,14 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   ssrc.release();
   rid.release();
   ph.mark("cells");
-  // (gram, file) counts never exceed the file's words: fewer sort-key bits
-  const u64 Wt = d->max_file_tokens ? d->max_file_tokens : d->W;
+  // the count field of the record sort key spans the largest cell count (one
+  // reduction + read-back): C4 39 -> 32-bit keys, one radix pass fewer
+  u64 Wt = d->max_file_tokens ? d->max_file_tokens : d->W;
+  if (n) {
+    DBuf mx(8, st);
+    reduce_max_u64(ccnt.as<u64>(), mx.as<u64>(), n, st);
+    Wt = std::max<u64>(1, d2h1<u64>(mx.p, st));
+  }
   const int CB = std::max(1, bitlen(Wt));
   const bool by_file = task == GT_SEQCOUNT;
   const int MB = by_file ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns));
