@@ -556,7 +556,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   // the count field of the record sort key spans the largest cell count (one
   // reduction + read-back): C4 39 -> 32-bit keys, one radix pass fewer
   u64 Wt = d->max_file_tokens ? d->max_file_tokens : d->W;
-  if (n) {
+  if (n && bitlen(Wt) + (task == GT_SEQCOUNT ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns))) > 32) {
     DBuf mx(8, st);
     reduce_max_u64(ccnt.as<u64>(), mx.as<u64>(), n, st);
     Wt = std::max<u64>(1, d2h1<u64>(mx.p, st));

@@ -461,8 +461,14 @@ void sparse_term_vector(DeviceDag* d, DevRecords* Rr) {
   ph.mark("cells");
   s = SparseW();
   // file-major, (-count, word) within a file: one stable radix sort of the
-  // word-major cells on (file, W - count); W = the longest file's words
-  const u64 W = d->max_file_tokens ? d->max_file_tokens : d->W;
+  // word-major cells on (file, W - count); W = the longest file's words, or
+  // the largest cell count when that bound needs a u64 key
+  u64 W = d->max_file_tokens ? d->max_file_tokens : d->W;
+  if (O && bitlen(W) + std::max(1, bitlen(Fo ? Fo - 1 : 0)) > 32) {
+    DBuf mx(8, st);
+    reduce_max_u64(cnt.as<u64>(), mx.as<u64>(), O, st);
+    W = std::max<u64>(1, d2h1<u64>(mx.p, st));
+  }
   const int CB = std::max(1, bitlen(W));
   const int FB = std::max(1, bitlen(Fo ? Fo - 1 : 0));
   DBuf k1(O * 8 + 8, st), k2(O * 8 + 8, st);

@@ -328,8 +328,17 @@ void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_
     R->n_groups = ncols;
   }
   if (by_count && n) {
-    // a per-file count never exceeds its file's words: fewer key bits
-    const u64 W = pf && d->max_file_tokens ? d->max_file_tokens : d->W;
+    // a per-file count never exceeds its file's words; when that bound still
+    // needs a u64 key, the count field spans the largest count instead (one
+    // reduction + read-back) — often a u32 key
+    u64 W = pf && d->max_file_tokens ? d->max_file_tokens : d->W;
+    if (bitlen(W) + (pf ? bitlen(ncols - 1) : 0) > 32) {
+      DBuf mx(8, st);
+      reduce_max_u64(R->count.as<u64>(), mx.as<u64>(), n, st);
+      GT_CUDA(cudaMemcpyAsync(&W, mx.p, 8, cudaMemcpyDeviceToHost, st));
+      GT_CUDA(cudaStreamSynchronize(st));
+      W = std::max<u64>(W, 1);
+    }
     const int CB = std::max(1, bitlen(W));
     const int FB = pf ? bitlen(ncols - 1) : 0;
     DBuf k1(n * 8, st), k2(n * 8, st), id2(n * 4, st);
