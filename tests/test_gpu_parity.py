@@ -76,6 +76,19 @@ def test_u64_row_path_matches_oracle():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+def test_forced_sparse_path_matches_oracle():
+    """The presence-guided sparse per-file path (auto only for > 64 files) on
+    few-file grammars too: GT_FORCE_SPARSE=1 in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, GT_FORCE_SPARSE="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-x", "-q", "-p", "no:cacheprovider",
+                        "-k", "composed_all_tasks and (c2-0.002 or c4-0.0005 or c5-0.0002)"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def _rule_lengths(blob):
     import struct
     pos = 5
