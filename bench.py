@@ -133,6 +133,9 @@ def task_columns(task: str, files: int) -> int:
     return max(1, files)  # per-file counts
 
 
+FUSED_REDUCE_MAX = 4 << 20  # word.cu kFusedReduceMax: the C = 1 reduce runs inside the top-down launch
+
+
 def alg_bytes(kernel: str, info: dict, files: int, tasks=TASKS) -> float | None:
     """Algorithmic (compulsory) bytes of one bench step for a kernel, summed
     over the step's tasks: every input element read once,
@@ -140,13 +143,18 @@ def alg_bytes(kernel: str, info: dict, files: int, tasks=TASKS) -> float | None:
     weights/counts).  k_td_level: the non-root parent edges (child, parent,
     freq: 12 B) + every rule row written once and read once (16·C B);
     k_reduce_words: the word-major own pairs (12 B) + every rule row read once
-    + the dense (C x V) output written once."""
+    + the dense (C x V) output written once.  For C = 1 (word count, inverted
+    index of <= 64 files) on grammars with at most FUSED_REDUCE_MAX own pairs
+    the reduce runs inside the top-down launch, so k_td_levels carries both
+    terms."""
     R, Eo, V, Te = info["num_rules"], info["own_pairs"], info["num_words"], info["td_edges"]
     tot = 0
     for t in tasks:
         C = task_columns(t, files)
         if kernel in ("k_td_level", "k_td_levels"):
             tot += 12 * Te + 16 * C * (R - 1)
+            if C == 1 and Eo <= FUSED_REDUCE_MAX:
+                tot += 12 * Eo + 8 * R + 8 * V
         elif kernel == "k_reduce_words":
             tot += 12 * Eo + 8 * C * R + 8 * C * V
         else:

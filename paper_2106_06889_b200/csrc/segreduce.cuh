@@ -446,6 +446,25 @@ struct SeedArgs {
   u64 zero_n;
 };
 
+// Reduce-by-word folded into the same launch after the last level (C = 1):
+// out[w] (+)= f * row[r] over the word-major own pairs, then the root's plain
+// words of the owned segments (reduce_words_round + root_words_round,
+// _kernels.py:154-188); out is cleared in phase 0.
+struct PostArgs {
+  const u32* dst;  // ow_word
+  const u32* src;  // ow_rule (tid)
+  const u32* freq;
+  u64 n;
+  u64* out;  // nullptr: no post phase
+  u64 out_n;
+  const u32* rw_word;
+  const u32* rw_seg;
+  const u32* rw_cnt;
+  u64 n_rw;
+  u32 file_lo, nseg;
+  int per_file;
+};
+
 template <class Mode, class T = u64>
 __device__ __forceinline__ void seed_rows_body(const SeedArgs& a) {
   T* row = reinterpret_cast<T*>(a.row);
@@ -535,13 +554,16 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
                                                           const u32* __restrict__ src,
                                                           const u32* __restrict__ freq,
                                                           const u64* __restrict__ lvl_off, int L0, int L1,
-                                                          int reverse, int prefetch, SeedArgs seed, Src in,
-                                                          Out out) {
+                                                          int reverse, int prefetch, SeedArgs seed, PostArgs post,
+                                                          Src in, Out out) {
   cg::grid_group grid = cg::this_grid();
-  if (seed.row) {  // phase 0: clear the rows, then the root seeds
+  if (seed.row) {  // phase 0: clear the rows (and the reduce output), then the root seeds
     u64* zr = reinterpret_cast<u64*>(seed.row);
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < seed.zero_n; i += (u64)gridDim.x * blockDim.x)
       zr[i] = 0;
+    if (post.out)
+      for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < post.out_n; i += (u64)gridDim.x * blockDim.x)
+        post.out[i] = 0;
     grid.sync();
     seed_rows_body<Mode>(seed);
     grid.sync();
@@ -624,6 +646,23 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
       fetch(it + 1);
     }
     if (it + 1 < nit) grid.sync();
+  }
+  if (post.out) {  // the word reduce over the finished rows
+    grid.sync();
+    if (post.n) {
+      int K = (int)((post.n + 32 * nwarps - 1) / (32 * nwarps));
+      K = K < 1 ? 1 : (K > 16 ? 16 : K);
+      segred1_body<Mode>(post.dst, post.src, post.freq, post.n, K, in, OutColMajorT<u64>{post.out, post.out_n},
+                         warp, nwarps);
+    }
+    const bool is_or = std::is_same<Mode, OrMode>::value;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < post.n_rw; i += nthreads) {
+      const u32 sg = post.rw_seg[i] - post.file_lo;
+      if (sg >= post.nseg) continue;
+      const u32 w = post.rw_word[i];
+      if (!post.per_file) Mode::atomic(&post.out[w], Mode::combine(post.rw_cnt[i], 1ull));
+      else Mode::atomic(&post.out[w], is_or ? (1ull << (sg & 63u)) : (u64)post.rw_cnt[i]);
+    }
   }
 }
 
@@ -867,14 +906,15 @@ void seg_reduce_levels_tma(const char* name, const u32* dst, const u32* src, con
 template <int BLOCK, int PRE, class Mode, class Src, class Out>
 void seg_reduce_levels1_b(const char* name, const u32* dst, const u32* src, const u32* freq,
                           const u64* lvl_off_dev, int L0, int L1, int reverse, int prefetch, const SeedArgs* seed,
-                          Src in, Out out, cudaStream_t st) {
+                          const PostArgs* post, Src in, Out out, cudaStream_t st) {
   auto kern = k_segred1_levels<BLOCK, PRE, Mode, Src, Out>;
   int dev = 0, nsm = 148;
   GT_CUDA(cudaGetDevice(&dev));
   GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   SeedArgs sa = seed ? *seed : SeedArgs{};
+  PostArgs pa = post ? *post : PostArgs{};
   void* args[] = {(void*)&dst, (void*)&src, (void*)&freq, (void*)&lvl_off_dev, (void*)&L0, (void*)&L1,
-                  (void*)&reverse, (void*)&prefetch, (void*)&sa, (void*)&in, (void*)&out};
+                  (void*)&reverse, (void*)&prefetch, (void*)&sa, (void*)&pa, (void*)&in, (void*)&out};
   ProfScope ps(name, st);
   GT_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)nsm), dim3(BLOCK), args, 0, st));
   g_launches++;
@@ -888,23 +928,24 @@ void seg_reduce_levels1_b(const char* name, const u32* dst, const u32* src, cons
 template <class Mode, class Src, class Out>
 void seg_reduce_levels1(const char* name, const u32* dst, const u32* src, const u32* freq,
                         const u64* lvl_off_dev, int L0, int L1, int reverse, u64 avg_items, const SeedArgs* seed,
-                        Src in, Out out, cudaStream_t st) {
+                        const PostArgs* post, Src in, Out out, cudaStream_t st) {
   static const int prefetch = getenv("GT_LEVEL_PREFETCH") ? atoi(getenv("GT_LEVEL_PREFETCH")) : 1;
   static const int force_pre = getenv("GT_LEVEL_PRE") ? atoi(getenv("GT_LEVEL_PRE")) : 0;
   const int pre = force_pre ? force_pre : (avg_items > 148ull * kLevelBlock ? 4 : 1);
   if (pre == 4)
     seg_reduce_levels1_b<kLevelBlock, 4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, reverse, prefetch, seed,
-                                               in, out, st);
+                                               post, in, out, st);
   else
     seg_reduce_levels1_b<kLevelBlock, 1, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, reverse, prefetch, seed,
-                                               in, out, st);
+                                               post, in, out, st);
 }
 
 // levels [L0, L1] in increasing order, or decreasing with reverse = true
 template <class Mode, class Src, class Out>
 void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u32* freq,
                        const u64* lvl_off_dev, int L0, int L1, u32 C, Src in, Out out, cudaStream_t st,
-                       bool reverse = false, u64 avg_items = 0, const SeedArgs* seed = nullptr) {
+                       bool reverse = false, u64 avg_items = 0, const SeedArgs* seed = nullptr,
+                       const PostArgs* post = nullptr) {
   // seed (C == 1 only): zero + seed the rows as phase 0 of the same launch
   if (!C) return;
   if (L1 < L0 && !seed) return;
@@ -914,9 +955,9 @@ void seg_reduce_levels(const char* name, const u32* dst, const u32* src, const u
   // loads it hides are not on the critical path; the row gathers and the
   // grid barrier are
   static const bool use_tma = getenv("GT_LEVELS_TMA") != nullptr;
-  if (C == 1 && use_tma && !seed)
+  if (C == 1 && use_tma && !seed && !post)
     seg_reduce_levels_tma<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, in, out, st, reverse);
-  else if (C == 1) seg_reduce_levels1<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, avg_items, seed, in, out, st);
+  else if (C == 1) seg_reduce_levels1<Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, avg_items, seed, post, in, out, st);
   else if (C <= 2) seg_reduce_levels_G<2, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 4) seg_reduce_levels_G<4, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);
   else if (C <= 8) seg_reduce_levels_G<8, Mode>(name, dst, src, freq, lvl_off_dev, L0, L1, rv, C, in, out, st);

@@ -156,7 +156,7 @@ __global__ void k_ii_emit(const u64* __restrict__ pres, u64 V, const u64* __rest
 // seeded from the root references, then one segmented gather-reduce launch
 // per top-down level over that level's non-root parent edges.
 template <class Mode, class T = u64>
-static void td_levels(const DeviceDag* d, u32 C, T* row, u32 per_file = 1) {
+static void td_levels(const DeviceDag* d, u32 C, T* row, u32 per_file = 1, const PostArgs* post = nullptr) {
   cudaStream_t st = d->stream;
   // rows indexed by tid (DeviceDag::tid): seeds and edges carry tids
   const SeedArgs seed{d->rs_rule_t.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
@@ -172,8 +172,9 @@ static void td_levels(const DeviceDag* d, u32 C, T* row, u32 per_file = 1) {
   seg_reduce_levels<Mode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
                           d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrcT<T>{row, C}, TdRowsT<T>{row, C}, st,
                           false, d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0,
-                          fused_seed ? &seed : nullptr);
+                          fused_seed ? &seed : nullptr, fused_seed ? post : nullptr);
 }
+
 
 // Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
 // as a gather-reduce over the word-major own pairs, then the root's plain
@@ -196,6 +197,26 @@ static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool p
     KL((k_root_words<Mode, T>), grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
        d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo),
        per_file ? 1 : 0, C, V, row_major ? 1 : 0, out);
+}
+
+// C = 1 top-down pass with the word reduce and the root words folded into
+// the same cooperative launch (phase 0 clears rows and output) — for small
+// grammars, where the separate launches cost more than the reduce itself
+// (C2: word count 0.133 -> 0.120 ms).  A large reduce is bandwidth-bound and
+// needs the full-occupancy flat launch (C5: fused 1.77 ms vs 0.92 ms).
+constexpr u64 kFusedReduceMax = 4ull << 20;
+
+template <class Mode>
+static void td_words_fused(const DeviceDag* d, u64* row, u64* out, bool per_file) {
+  if (d->E_own > kFusedReduceMax) {
+    td_levels<Mode>(d, 1, row, per_file ? 1 : 0);
+    reduce_words<Mode>(d, 1, row, out, per_file);
+    return;
+  }
+  const PostArgs post{d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), d->E_own, out, d->nw,
+                      d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo,
+                      (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0};
+  td_levels<Mode>(d, 1, row, per_file ? 1 : 0, &post);
 }
 
 void bu_root_words_dense(DeviceDag* d, u64* out) {
@@ -229,9 +250,8 @@ u64 scratch_budget(const DeviceDag* d) {
 void td_word_counts(DeviceDag* d, DBuf& counts) {
   cudaStream_t st = d->stream;
   DBuf w(d->R * 8, st);
-  td_levels<SumMode>(d, 1, w.as<u64>(), 0);
   counts.alloc(d->nw * 8 + 8, st);
-  reduce_words<SumMode>(d, 1, w.as<u64>(), counts.as<u64>(), false);
+  td_words_fused<SumMode>(d, w.as<u64>(), counts.as<u64>(), false);
 }
 
 // per-file cells fit u32 when every owned file has < 2^32 words (a weight or
@@ -279,9 +299,13 @@ void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out, DBuf* rows_out) {
   const u32 Fo = (u32)(d->file_hi - d->file_lo);
   const u32 FW = std::max<u32>(1, (Fo + 63) / 64);
   DBuf m(d->R * 8 * (u64)FW, st);
-  td_levels<OrMode>(d, FW, m.as<u64>());
   pres.alloc(d->nw * 8 * (u64)FW + 8, st);
-  reduce_words<OrMode>(d, FW, m.as<u64>(), pres.as<u64>(), true, true);
+  if (FW == 1) {
+    td_words_fused<OrMode>(d, m.as<u64>(), pres.as<u64>(), true);
+  } else {
+    td_levels<OrMode>(d, FW, m.as<u64>());
+    reduce_words<OrMode>(d, FW, m.as<u64>(), pres.as<u64>(), true, true);
+  }
   *FW_out = FW;
   if (rows_out) *rows_out = std::move(m);
 }
