@@ -287,11 +287,15 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
         // and top-down run Alg. 1 (engine.py:63-71 picks top-down here)
         if (strat == GT_BOTTOMUP && strategy == GT_BOTTOMUP && bu_word_counts(&d, d.word_counts, scratch_budget(&d))) {
           strat = GT_BOTTOMUP;
+          assemble_counts(&d, d.word_counts.as<u64>(), d.nw, 0, task == GT_SORT, &R);
+        } else if (td_word_records(&d, &R)) {  // small grammar: one launch
+          strat = GT_TOPDOWN;
+          if (task == GT_SORT) order_by_count(&d, &R, 0, nullptr);
         } else {
           td_word_counts(&d, d.word_counts);
           strat = GT_TOPDOWN;
+          assemble_counts(&d, d.word_counts.as<u64>(), d.nw, 0, task == GT_SORT, &R);
         }
-        assemble_counts(&d, d.word_counts.as<u64>(), d.nw, 0, task == GT_SORT, &R);
         break;
       }
       case GT_TERMVECTOR: {
@@ -314,6 +318,8 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
       case GT_INVERTEDINDEX: {
         if (strategy == GT_BOTTOMUP && bu_file_tables(&d, GT_INVERTEDINDEX, &R, scratch_budget(&d))) {
           strat = GT_BOTTOMUP;
+        } else if (td_presence_records(&d, &R)) {  // small grammar, <= 64 files: one launch
+          strat = GT_TOPDOWN;
         } else {
           DBuf pres;
           u32 FW;

@@ -463,7 +463,146 @@ struct PostArgs {
   u64 n_rw;
   u32 file_lo, nseg;
   int per_file;
+  // compaction of out (after one more barrier) into render-order records:
+  // 1 = nonzero counts -> (word, count) records (word count); 2 = presence
+  // words -> (word groups, ascending files) (inverted index, <= 64 files).
+  // Outputs sized for the worst case; tot = {records, groups}; bsum =
+  // 2 * gridDim scratch.
+  int compact;
+  u32* rid;
+  u64* rcnt;
+  u32* gid;
+  u64* goff;
+  u64* tot;
+  u64* bsum;
 };
+
+// block-wide exclusive scan of two counters (1024 threads); returns the
+// block totals through *ta / *tb
+__device__ __forceinline__ void block_scan2(u32 a, u32 b, u32* ea, u32* eb, u32* ta, u32* tb) {
+  __shared__ u32 wa[32], wb[32];
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  u32 ia = a, ib = b;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u32 xa = __shfl_up_sync(0xFFFFFFFFu, ia, d), xb = __shfl_up_sync(0xFFFFFFFFu, ib, d);
+    if (lane >= (unsigned)d) {
+      ia += xa;
+      ib += xb;
+    }
+  }
+  if (lane == 31) {
+    wa[wid] = ia;
+    wb[wid] = ib;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const unsigned nw = blockDim.x >> 5;
+    u32 va = lane < nw ? wa[lane] : 0u, vb = lane < nw ? wb[lane] : 0u;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 xa = __shfl_up_sync(0xFFFFFFFFu, va, d), xb = __shfl_up_sync(0xFFFFFFFFu, vb, d);
+      if (lane >= (unsigned)d) {
+        va += xa;
+        vb += xb;
+      }
+    }
+    if (lane < nw) {
+      wa[lane] = va;
+      wb[lane] = vb;
+    }
+  }
+  __syncthreads();
+  const u32 pa = wid ? wa[wid - 1] : 0u, pb = wid ? wb[wid - 1] : 0u;
+  *ea = pa + ia - a;
+  *eb = pb + ib - b;
+  *ta = wa[(blockDim.x >> 5) - 1];
+  *tb = wb[(blockDim.x >> 5) - 1];
+  __syncthreads();
+}
+
+// the compaction of the post phase: blocks own contiguous word ranges, count
+// them, learn their offsets after a grid barrier, and write in order
+template <class Mode>
+__device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& grid) {
+  const u64 V = p.out_n, nb = gridDim.x;
+  const u64 CH = (V + nb - 1) / nb, lo = blockIdx.x * CH, hi = lo + CH < V ? lo + CH : V;
+  const bool pres = p.compact == 2;
+  __shared__ unsigned long long sa, sb;
+  if (threadIdx.x == 0) sa = sb = 0;
+  __syncthreads();
+  unsigned long long la = 0, lb = 0;
+  for (u64 w = lo + threadIdx.x; w < hi; w += blockDim.x) {
+    const u64 v = __ldcg(reinterpret_cast<const unsigned long long*>(p.out + w));
+    if (v) {
+      la += pres ? (unsigned long long)__popcll(v) : 1ull;
+      lb += 1;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    la += __shfl_xor_sync(0xFFFFFFFFu, la, d);
+    lb += __shfl_xor_sync(0xFFFFFFFFu, lb, d);
+  }
+  if ((threadIdx.x & 31u) == 0 && (la || lb)) {  // one shared atomic per warp
+    atomicAdd(&sa, la);
+    if (pres) atomicAdd(&sb, lb);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    p.bsum[blockIdx.x] = sa;
+    p.bsum[nb + blockIdx.x] = sb;
+  }
+  grid.sync();
+  // this block's offsets: sums over the blocks before it (one warp)
+  __shared__ unsigned long long oa, ob;
+  if (threadIdx.x < 32) {
+    unsigned long long xa = 0, xb = 0;
+    for (u64 j = threadIdx.x; j < blockIdx.x; j += 32) {
+      xa += __ldcg(reinterpret_cast<const unsigned long long*>(p.bsum + j));
+      xb += __ldcg(reinterpret_cast<const unsigned long long*>(p.bsum + nb + j));
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      xa += __shfl_xor_sync(0xFFFFFFFFu, xa, d);
+      xb += __shfl_xor_sync(0xFFFFFFFFu, xb, d);
+    }
+    if (threadIdx.x == 0) {
+      oa = xa;
+      ob = xb;
+      if (blockIdx.x == nb - 1) {
+        p.tot[0] = xa + __ldcg(reinterpret_cast<const unsigned long long*>(p.bsum + blockIdx.x));
+        p.tot[1] = xb + __ldcg(reinterpret_cast<const unsigned long long*>(p.bsum + nb + blockIdx.x));
+        if (pres) p.goff[p.tot[1]] = p.tot[0];
+      }
+    }
+  }
+  __syncthreads();
+  u64 ba = oa, bb = ob;
+  for (u64 t0 = lo; t0 < hi; t0 += blockDim.x) {  // block-uniform trip count
+    const u64 w = t0 + threadIdx.x;
+    const u64 v = w < hi ? __ldcg(reinterpret_cast<const unsigned long long*>(p.out + w)) : 0ull;
+    const u32 a = v ? (pres ? (u32)__popcll(v) : 1u) : 0u, b = (pres && v) ? 1u : 0u;
+    u32 ea, eb, ta, tb;
+    block_scan2(a, b, &ea, &eb, &ta, &tb);
+    if (v) {
+      if (!pres) {
+        p.rid[ba + ea] = (u32)w;
+        p.rcnt[ba + ea] = v;
+      } else {
+        p.gid[bb + eb] = (u32)w;
+        p.goff[bb + eb] = ba + ea;
+        u64 q = ba + ea, x = v;
+        while (x) {
+          p.rid[q++] = p.file_lo + (u32)(__ffsll((long long)x) - 1);
+          x &= x - 1;
+        }
+      }
+    }
+    ba += ta;
+    bb += tb;
+  }
+}
 
 template <class Mode, class T = u64>
 __device__ __forceinline__ void seed_rows_body(const SeedArgs& a) {
@@ -662,6 +801,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
       const u32 w = post.rw_word[i];
       if (!post.per_file) Mode::atomic(&post.out[w], Mode::combine(post.rw_cnt[i], 1ull));
       else Mode::atomic(&post.out[w], is_or ? (1ull << (sg & 63u)) : (u64)post.rw_cnt[i]);
+    }
+    if (post.compact) {
+      grid.sync();
+      post_compact<Mode>(post, grid);
     }
   }
 }

@@ -207,16 +207,77 @@ static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool p
 constexpr u64 kFusedReduceMax = 4ull << 20;
 
 template <class Mode>
-static void td_words_fused(const DeviceDag* d, u64* row, u64* out, bool per_file) {
+static void td_words_fused(const DeviceDag* d, u64* row, u64* out, bool per_file, PostArgs* compact = nullptr) {
   if (d->E_own > kFusedReduceMax) {
     td_levels<Mode>(d, 1, row, per_file ? 1 : 0);
     reduce_words<Mode>(d, 1, row, out, per_file);
     return;
   }
-  const PostArgs post{d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), d->E_own, out, d->nw,
-                      d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo,
-                      (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0};
+  PostArgs post{d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), d->E_own, out, d->nw,
+                d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo,
+                (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0};
+  if (compact) {
+    post.compact = compact->compact;
+    post.rid = compact->rid;
+    post.rcnt = compact->rcnt;
+    post.gid = compact->gid;
+    post.goff = compact->goff;
+    post.tot = compact->tot;
+    post.bsum = compact->bsum;
+  }
   td_levels<Mode>(d, 1, row, per_file ? 1 : 0, &post);
+}
+
+// small grammars, one launch per task: top-down pass + word reduce + root
+// words + the render-order compaction (word count records / inverted-index
+// groups); false when the grammar takes the multi-launch path
+static bool small_task(const DeviceDag* d) { return d->E_own <= kFusedReduceMax && d->nw < (1ull << 32); }
+
+bool td_word_records(DeviceDag* d, DevRecords* R) {
+  if (!small_task(d)) return false;
+  cudaStream_t st = d->stream;
+  const u64 V = d->nw;
+  DBuf w(d->R * 8, st), bsum(2 * 1024 * 8, st), tot(16, st);
+  d->word_counts.alloc(V * 8 + 8, st);
+  R->id.alloc(V * 4 + 4, st);
+  R->count.alloc(V * 8 + 8, st);
+  PostArgs c{};
+  c.compact = 1;
+  c.rid = R->id.as<u32>();
+  c.rcnt = R->count.as<u64>();
+  c.tot = tot.as<u64>();
+  c.bsum = bsum.as<u64>();
+  td_words_fused<SumMode>(d, w.as<u64>(), d->word_counts.as<u64>(), false, &c);
+  u64 h[2];
+  GT_CUDA(cudaMemcpyAsync(h, tot.p, 16, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  R->n = h[0];
+  return true;
+}
+
+bool td_presence_records(DeviceDag* d, DevRecords* R) {
+  const u32 Fo = (u32)(d->file_hi - d->file_lo);
+  if (!small_task(d) || Fo > 64) return false;
+  cudaStream_t st = d->stream;
+  const u64 V = d->nw;
+  DBuf m(d->R * 8, st), pres(V * 8 + 8, st), bsum(2 * 1024 * 8, st), tot(16, st);
+  R->id.alloc(V * (u64)std::max<u32>(Fo, 1) * 4 + 4, st);
+  R->group_id.alloc(V * 4 + 4, st);
+  R->group_off.alloc((V + 1) * 8, st);
+  PostArgs c{};
+  c.compact = 2;
+  c.rid = R->id.as<u32>();
+  c.gid = R->group_id.as<u32>();
+  c.goff = R->group_off.as<u64>();
+  c.tot = tot.as<u64>();
+  c.bsum = bsum.as<u64>();
+  td_words_fused<OrMode>(d, m.as<u64>(), pres.as<u64>(), true, &c);
+  u64 h[2];
+  GT_CUDA(cudaMemcpyAsync(h, tot.p, 16, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  R->n = h[0];
+  R->n_groups = h[1];
+  return true;
 }
 
 void bu_root_words_dense(DeviceDag* d, u64* out) {
@@ -312,6 +373,39 @@ void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out, DBuf* rows_out) {
 
 // ---- assembly -------------------------------------------------------------
 
+// records in (file, -count, id) order (sort / term vector, tasks.py:122-168):
+// one stable radix sort on (file << CB) | (W - count) carrying the id
+void order_by_count(DeviceDag* d, DevRecords* R, u32 ncols, const u32* file) {
+  cudaStream_t st = d->stream;
+  const u64 n = R->n;
+  const bool pf = ncols > 0;
+  if (!n) return;
+  // a per-file count never exceeds its file's words; when that bound still
+  // needs a u64 key, the count field spans the largest count instead (one
+  // reduction + read-back) — often a u32 key
+  u64 W = pf && d->max_file_tokens ? d->max_file_tokens : d->W;
+  if (bitlen(W) + (pf ? bitlen(ncols - 1) : 0) > 32) {
+    DBuf mx(8, st);
+    reduce_max_u64(R->count.as<u64>(), mx.as<u64>(), n, st);
+    GT_CUDA(cudaMemcpyAsync(&W, mx.p, 8, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+    W = std::max<u64>(W, 1);
+  }
+  const int CB = std::max(1, bitlen(W));
+  const int FB = pf ? bitlen(ncols - 1) : 0;
+  DBuf k1(n * 8, st), k2(n * 8, st), id2(n * 4, st);
+  if (CB + FB <= 32) {  // u32 keys: half the radix key traffic
+    KL(k_sort_keys<u32>, grid_for(n, 256), R->count.as<u64>(), file, n, W, CB, k1.as<u32>());
+    sort_pairs_u32_u32(k1.as<u32>(), k2.as<u32>(), R->id.as<u32>(), id2.as<u32>(), n, CB + FB, st);
+    KL(k_unkey<u32>, grid_for(n, 256), k2.as<u32>(), n, W, CB, R->count.as<u64>());
+  } else {
+    KL(k_sort_keys<u64>, grid_for(n, 256), R->count.as<u64>(), file, n, W, CB, k1.as<u64>());
+    sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), R->id.as<u32>(), id2.as<u32>(), n, CB + FB, st);
+    KL(k_unkey<u64>, grid_for(n, 256), k2.as<u64>(), n, W, CB, R->count.as<u64>());
+  }
+  R->id = std::move(id2);
+}
+
 void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_count, DevRecords* R, bool dense32) {
   // ncols == 0: one global table; ncols >= 1: per-file tables (file-major)
   cudaStream_t st = d->stream;
@@ -351,34 +445,7 @@ void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_
     KL(k_csr_offsets, grid_for(ncols + 1, 256), file.as<u32>(), n, (u64)ncols, R->group_off.as<u64>());
     R->n_groups = ncols;
   }
-  if (by_count && n) {
-    // a per-file count never exceeds its file's words; when that bound still
-    // needs a u64 key, the count field spans the largest count instead (one
-    // reduction + read-back) — often a u32 key
-    u64 W = pf && d->max_file_tokens ? d->max_file_tokens : d->W;
-    if (bitlen(W) + (pf ? bitlen(ncols - 1) : 0) > 32) {
-      DBuf mx(8, st);
-      reduce_max_u64(R->count.as<u64>(), mx.as<u64>(), n, st);
-      GT_CUDA(cudaMemcpyAsync(&W, mx.p, 8, cudaMemcpyDeviceToHost, st));
-      GT_CUDA(cudaStreamSynchronize(st));
-      W = std::max<u64>(W, 1);
-    }
-    const int CB = std::max(1, bitlen(W));
-    const int FB = pf ? bitlen(ncols - 1) : 0;
-    DBuf k1(n * 8, st), k2(n * 8, st), id2(n * 4, st);
-    if (CB + FB <= 32) {  // u32 keys: half the radix key traffic
-      KL(k_sort_keys<u32>, grid_for(n, 256), R->count.as<u64>(), pf ? file.as<u32>() : nullptr, n, W, CB,
-         k1.as<u32>());
-      sort_pairs_u32_u32(k1.as<u32>(), k2.as<u32>(), R->id.as<u32>(), id2.as<u32>(), n, CB + FB, st);
-      KL(k_unkey<u32>, grid_for(n, 256), k2.as<u32>(), n, W, CB, R->count.as<u64>());
-    } else {
-      KL(k_sort_keys<u64>, grid_for(n, 256), R->count.as<u64>(), pf ? file.as<u32>() : nullptr, n, W, CB,
-         k1.as<u64>());
-      sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), R->id.as<u32>(), id2.as<u32>(), n, CB + FB, st);
-      KL(k_unkey<u64>, grid_for(n, 256), k2.as<u64>(), n, W, CB, R->count.as<u64>());
-    }
-    R->id = std::move(id2);
-  }
+  if (by_count && n) order_by_count(d, R, ncols, pf ? file.as<u32>() : nullptr);
 }
 
 // inverted index from the word presence bitsets u64[FW][V]: per word, the

@@ -13,6 +13,9 @@ struct DevRecords {
 
 void td_word_counts(DeviceDag* d, DBuf& counts);
 void td_file_counts(DeviceDag* d, DBuf& counts, bool* is32);
+bool td_word_records(DeviceDag* d, DevRecords* R);
+bool td_presence_records(DeviceDag* d, DevRecords* R);
+void order_by_count(DeviceDag* d, DevRecords* R, u32 ncols, const u32* file);
 void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW, DBuf* rows_out = nullptr);
 void td_file_weights(DeviceDag* d, DBuf& w, u32* C, bool* is32);
 void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_count, DevRecords* R,
