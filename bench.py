@@ -411,7 +411,7 @@ def main():
 
     # ---- e2e through the public C-ABI from pinned host bytes: gt_open (H2D +
     # device DAG build) + the step (+ collective) + D2H of results + gt_close
-    e2e_times, d2h_bytes = [], 0
+    e2e_times, d2h_bytes, parts = [], 0, []
     for i in range(max(2, min(args.steps, 5)) + 1):
         if dist:
             dist.barrier()
@@ -420,11 +420,14 @@ def main():
         d = DeviceDag(src, device=local)
         if not corpus_mode:
             d.set_files(lo, hi)
+        t1 = time.perf_counter()
         _, _, nb = step(d)
+        t2 = time.perf_counter()
         d.close()
         el = time.perf_counter() - t0
         if i:
             e2e_times.append(el)
+            parts.append((t1 - t0, t2 - t1, el - (t2 - t0)))
             d2h_bytes = nb
     e2e_s = statistics.mean(e2e_times)
     if dist:
@@ -460,7 +463,9 @@ def main():
                        "parallelism": par},
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": W_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_s * 1e3},
+                    "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_s * 1e3,
+                    "breakdown_ms": {k: round(statistics.mean(p[j] for p in parts) * 1e3, 4)
+                                     for j, k in enumerate(("gt_open", "tasks_incl_d2h", "gt_close"))}},
             "gpu_launches": launches, "clocks": clk.summary(), "wall_s_timed_region": wall,
             "init_ms": info["init_ms"], "kernels": kernel_table,
         }
