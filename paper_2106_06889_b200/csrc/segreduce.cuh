@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kLevelBlock) k_segred_levels(const u32* __rest
       } else {
         const u64 teams = nthreads / G;
         u32 K = (u32)((n + teams - 1) / teams);
-        K = K < 8 ? 8 : (K > 64 ? 64 : K);
+        K = K < 2 ? 2 : (K > 64 ? 64 : K);
         segredG_body<G, Mode, true>(dst + a, src + a, freq ? freq + a : nullptr, n, K, C, in, out, gtid, nthreads);
       }
     }
