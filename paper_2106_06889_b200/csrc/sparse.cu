@@ -57,7 +57,7 @@ __device__ __forceinline__ u64 find_group(const u64* pos, u64 G, u64 i) {
 // popcount of each bitset row (warp per row): row r has FW words at stride
 // `rs` words, word j at r*rs_row + j*rs_col
 __global__ void k_popc_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col,
-                            u64* __restrict__ cnt) {
+                            u64* __restrict__ cnt, int packed) {
   const unsigned lane = threadIdx.x & 31u;
   const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
   for (u64 r = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows; r += nw) {
@@ -65,20 +65,30 @@ __global__ void k_popc_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u64
     for (u32 j = lane; j < FW; j += 32) c += __popcll(bits[r * rs_row + (u64)j * rs_col]);
 #pragma unroll
     for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
-    if (lane == 0) cnt[r] = c;
+    if (lane == 0) cnt[r] = packed ? ((c ? (1ull << 40) : 0ull) | c) : c;
   }
 }
 
 // set bits of each row -> ascending column indices at off[r] (warp per row,
 // 32 words per step, ballot-free: popcount prefix by shuffle scan)
+// (packed: off[r] = (nonempty rows before r) << 40 | (bits before r), the
+// group index and record offset from ONE scan; the nonempty rows' ids and
+// record offsets are written to gid / goff — the inverted-index groups)
 __global__ void k_expand_rows(const u64* __restrict__ bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col,
                               const u64* __restrict__ off, u32 col_base, u32* __restrict__ col,
-                              u32* __restrict__ row_of) {
+                              u32* __restrict__ row_of, int packed, u32* __restrict__ gid,
+                              u64* __restrict__ goff) {
   const unsigned lane = threadIdx.x & 31u;
   const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u64 M = (1ull << 40) - 1;
   for (u64 r = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows; r += nw) {
-    u64 o = off[r];
-    if (off[r + 1] == o) continue;
+    u64 o = packed ? (off[r] & M) : off[r];
+    if ((packed ? (off[r + 1] & M) : off[r + 1]) == o) continue;
+    if (packed && lane == 0) {
+      const u64 g = off[r] >> 40;
+      gid[g] = (u32)r;
+      goff[g] = o;
+    }
     for (u32 j0 = 0; j0 < FW; j0 += 32) {
       const u32 j = j0 + lane;
       u64 b = j < FW ? bits[r * rs_row + (u64)j * rs_col] : 0ull;
@@ -371,7 +381,7 @@ void bits_count(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf
   cnt.alloc(nrows * 8 + 8, st);
   off.alloc((nrows + 1) * 8, st);
   if (FW == 1) SK(k_popc_rows1, nrows, bits, nrows, rs_row, cnt.as<u64>());
-  else SKW(k_popc_rows, nrows, bits, nrows, FW, rs_row, rs_col, cnt.as<u64>());
+  else SKW(k_popc_rows, nrows, bits, nrows, FW, rs_row, rs_col, cnt.as<u64>(), 0);
   GT_CUDA(cudaMemsetAsync(cnt.as<u64>() + nrows, 0, 8, st));
   exclusive_scan_u64(cnt.as<u64>(), off.as<u64>(), nrows + 1, st);
 }
@@ -385,7 +395,33 @@ void bits_expand(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, con
        row_of ? row_of->as<u32>() : (u32*)nullptr);
   else
     SKW(k_expand_rows, nrows, bits, nrows, FW, rs_row, rs_col, off.as<u64>(), col_base, col.as<u32>(),
-        row_of ? row_of->as<u32>() : (u32*)nullptr);
+        row_of ? row_of->as<u32>() : (u32*)nullptr, 0, (u32*)nullptr, (u64*)nullptr);
+}
+
+__global__ void k_set_u64(u64* p, u64 v) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p = v;
+}
+
+// inverted-index groups from word-major bitsets (FW words per row): one
+// packed scan (group index << 40 | record offset; rows < 2^24) gives each
+// row's group index and record offset; returns
+// (records, groups) and fills files / gid / goff (goff[groups] = records)
+void bits_groups(const u64* bits, u64 nrows, u32 FW, u32 col_base, DBuf& files, DBuf& gid, DBuf& goff, u64* n_out,
+                 u64* ng_out, cudaStream_t st) {
+  DBuf key((nrows + 1) * 8, st), pref((nrows + 1) * 8, st);
+  GT_CUDA(cudaMemsetAsync(key.as<u64>() + nrows, 0, 8, st));
+  SKW(k_popc_rows, nrows, bits, nrows, FW, (u64)FW, 1ull, key.as<u64>(), 1);
+  exclusive_scan_u64(key.as<u64>(), pref.as<u64>(), nrows + 1, st);
+  const u64 h = d2h1<u64>(pref.as<u64>() + nrows, st);
+  const u64 ng = h >> 40, n = h & ((1ull << 40) - 1);
+  files.alloc(n * 4 + 4, st);
+  gid.alloc(ng * 4 + 4, st);
+  goff.alloc((ng + 1) * 8, st);
+  SK(k_set_u64, 1, goff.as<u64>() + ng, n);
+  SKW(k_expand_rows, nrows, bits, nrows, FW, (u64)FW, 1ull, pref.as<u64>(), col_base, files.as<u32>(),
+      (u32*)nullptr, 1, gid.as<u32>(), goff.as<u64>());
+  *n_out = n;
+  *ng_out = ng;
 }
 
 u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& col,

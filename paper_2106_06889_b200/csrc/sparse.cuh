@@ -23,6 +23,8 @@ u64 bits_to_csr(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf
 // caller knows P = off[nrows]) for callers that batch their host syncs
 void bits_count(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, DBuf& off, DBuf& cnt,
                 cudaStream_t st);
+void bits_groups(const u64* bits, u64 nrows, u32 FW, u32 col_base, DBuf& files, DBuf& gid, DBuf& goff, u64* n_out,
+                 u64* ng_out, cudaStream_t st);
 void bits_expand(const u64* bits, u64 nrows, u32 FW, u64 rs_row, u64 rs_col, const DBuf& off, u64 P,
                  DBuf& col, DBuf* row_of, cudaStream_t st, u32 col_base = 0);
 

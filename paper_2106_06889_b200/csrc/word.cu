@@ -471,6 +471,18 @@ void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R) {
        R->group_id.as<u32>(), R->group_off.as<u64>());
     return;
   }
+  if (V < (1ull << 24)) {
+    // one packed scan for the group indices and record offsets
+    DBuf files, gid, goff;
+    u64 n = 0, ng = 0;
+    bits_groups(pres, V, FW, (u32)d->file_lo, files, gid, goff, &n, &ng, st);
+    R->n = n;
+    R->n_groups = ng;
+    R->id = std::move(files);
+    R->group_id = std::move(gid);
+    R->group_off = std::move(goff);
+    return;
+  }
   DBuf off, files, pc;
   bits_count(pres, V, FW, FW, 1, off, pc, st);
   DBuf nz(V + 1, st), words(V * 4 + 4, st), cnt(16, st);
