@@ -294,70 +294,61 @@ void build_rule_pairs(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_
   const u64 R = d->R, E = d->E, nw = d->nw, base = d->nw + d->ns;
   const u32* body = d->body.as<u32>();
   const u64* boff = d->boff.as<u64>();
-  DBuf tsym(E * 4 + 4, st), tcnt(E * 4 + 4, st), n_own(R * 4 + 4, st), n_sub(R * 4 + 4, st), lflag(R + 1, st);
+  // this phase's temporaries in one allocation
+  enum { TSYM, TCNT, NOWN, NSUB, LFLAG, GFLAG, LIDS, GIDS, GPOS, CNT, MEDF, WIDE };
+  const Carve a(st, {E * 4 + 4, E * 4 + 4, R * 4 + 4, R * 4 + 4, R + 1, E + 1, R * 4 + 4, R * 4 + 4, E * 4 + 4, 32,
+                     R + 1, (R + 1) * 8});
+  u32 *tsym = a.at<u32>(TSYM), *tcnt = a.at<u32>(TCNT), *n_own = a.at<u32>(NOWN), *n_sub = a.at<u32>(NSUB);
+  uint8_t* lflag = a.at<uint8_t>(LFLAG);
+  u64* cnt = a.at<u64>(CNT);
   d->own_tok.alloc(R * 8, st);
   d->num_out.alloc(R * 8, st);
-  CK(k_rules_short, R, body, boff, R, nw, base, tsym.as<u32>(), tcnt.as<u32>(), n_own.as<u32>(), n_sub.as<u32>(),
-     d->own_tok.as<u64>(), d->num_out.as<u64>(), lflag.as<uint8_t>());
+  CK(k_rules_short, R, body, boff, R, nw, base, tsym, tcnt, n_own, n_sub, d->own_tok.as<u64>(),
+     d->num_out.as<u64>(), lflag);
   // the longer bodies: one host round trip for their number and size
-  DBuf gflag(E + 1, st), lids(R * 4 + 4, st), gids(R * 4 + 4, st), gpos(E * 4 + 4, st), cnt(32, st);
-  {
-    DBuf medf(R + 1, st);
-    CK(k_eq_u8, R, lflag.as<uint8_t>(), R, (uint8_t)1, medf.as<uint8_t>());
-    select_flagged_index(medf.as<uint8_t>(), lids.as<u32>(), cnt.as<u64>(), R, st);
-    CK(k_eq_u8, R, lflag.as<uint8_t>(), R, (uint8_t)2, medf.as<uint8_t>());
-    select_flagged_index(medf.as<uint8_t>(), gids.as<u32>(), cnt.as<u64>() + 3, R, st);
-  }
-  CK(k_giant_elems, E, owner, lflag.as<uint8_t>(), E, gflag.as<uint8_t>());
-  select_flagged_index(gflag.as<uint8_t>(), gpos.as<u32>(), cnt.as<u64>() + 1, E, st);
-  gflag.release();
+  CK(k_eq_u8, R, lflag, R, (uint8_t)1, a.at<uint8_t>(MEDF));
+  select_flagged_index(a.at<uint8_t>(MEDF), a.at<u32>(LIDS), cnt, R, st);
+  CK(k_eq_u8, R, lflag, R, (uint8_t)2, a.at<uint8_t>(MEDF));
+  select_flagged_index(a.at<uint8_t>(MEDF), a.at<u32>(GIDS), cnt + 3, R, st);
+  CK(k_giant_elems, E, owner, lflag, E, a.at<uint8_t>(GFLAG));
+  select_flagged_index(a.at<uint8_t>(GFLAG), a.at<u32>(GPOS), cnt + 1, E, st);
   u64 h[4];
-  GT_CUDA(cudaMemcpyAsync(h, cnt.p, 32, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(h, cnt, 32, cudaMemcpyDeviceToHost, st));
   stream_sync(st);
   const u64 nmed = h[0], ngel = h[1], ngiant = h[3];
-  DBuf n_spl, rfirst;
   if (nmed || ngel) {
-    DBuf sbody(E * 4 + 4, st);
+    enum { SBODY, BEG, END, K1, K2, GRANK, HEAD, HIDX, NSPL, RFIRST };
+    const Carve b(st, {E * 4 + 4, nmed * 4 + 4, nmed * 4 + 4, ngel * 8 + 8, ngel * 8 + 8, R * 4 + 4, E + 1,
+                       E * 4 + 4, R * 4 + 4, R * 4 + 4});
+    u32* sbody = b.at<u32>(SBODY);
     if (nmed) {
-      DBuf beg(nmed * 4, st), end(nmed * 4, st);
-      CK(k_seg_bounds, nmed, lids.as<u32>(), nmed, boff, beg.as<int>(), end.as<int>());
-      sort_segments_listed_u32(body, sbody.as<u32>(), E, nmed, beg.as<int>(), end.as<int>(), st);
+      CK(k_seg_bounds, nmed, a.at<u32>(LIDS), nmed, boff, b.at<int>(BEG), b.at<int>(END));
+      sort_segments_listed_u32(body, sbody, E, nmed, b.at<int>(BEG), b.at<int>(END), st);
     }
     if (ngel) {
       const int SB = std::max(1, bitlen(d->nw + d->ns + R - 1));
       const int KB = SB + bitlen(ngiant - 1);
-      DBuf k1(ngel * 8, st), k2(ngel * 8, st), grank(R * 4 + 4, st);
-      CK(k_scatter_rank, ngiant, gids.as<u32>(), ngiant, grank.as<u32>());
-      CK(k_giant_keys, ngel, gpos.as<u32>(), ngel, owner, grank.as<u32>(), body, SB, k1.as<u64>());
-      sort_keys_u64(k1.as<u64>(), k2.as<u64>(), ngel, KB, st);
-      CK(k_giant_scatter, ngel, k2.as<u64>(), gpos.as<u32>(), ngel, SB, sbody.as<u32>());
+      CK(k_scatter_rank, ngiant, a.at<u32>(GIDS), ngiant, b.at<u32>(GRANK));
+      CK(k_giant_keys, ngel, a.at<u32>(GPOS), ngel, owner, b.at<u32>(GRANK), body, SB, b.at<u64>(K1));
+      sort_keys_u64(b.at<u64>(K1), b.at<u64>(K2), ngel, KB, st);
+      CK(k_giant_scatter, ngel, b.at<u64>(K2), a.at<u32>(GPOS), ngel, SB, sbody);
     }
-    DBuf head(E + 1, st), hidx(E * 4 + 4, st);
-    CK(k_long_heads, E, owner, lflag.as<uint8_t>(), boff, sbody.as<u32>(), E, head.as<uint8_t>());
-    select_flagged_index(head.as<uint8_t>(), hidx.as<u32>(), cnt.as<u64>() + 2, E, st);
-    head.release();
-    n_spl.alloc(R * 4 + 4, st);
-    rfirst.alloc(R * 4 + 4, st);
-    GT_CUDA(cudaMemsetAsync(n_spl.p, 0, R * 4 + 4, st));
-    CK(k_long_count, E, hidx.as<u32>(), cnt.as<u64>() + 2, owner, boff, sbody.as<u32>(), nw, base,
-       n_own.as<u32>(), n_sub.as<u32>(), n_spl.as<u32>(), d->own_tok.as<u64>(), d->num_out.as<u64>(),
-       rfirst.as<u32>());
-    CK(k_long_write, E, hidx.as<u32>(), cnt.as<u64>() + 2, owner, boff, sbody.as<u32>(), nw, base,
-       n_spl.as<u32>(), rfirst.as<u32>(), tsym.as<u32>(), tcnt.as<u32>());
+    CK(k_long_heads, E, owner, lflag, boff, sbody, E, b.at<uint8_t>(HEAD));
+    select_flagged_index(b.at<uint8_t>(HEAD), b.at<u32>(HIDX), cnt + 2, E, st);
+    GT_CUDA(cudaMemsetAsync(b.at<u32>(NSPL), 0, R * 4 + 4, st));
+    CK(k_long_count, E, b.at<u32>(HIDX), cnt + 2, owner, boff, sbody, nw, base, n_own, n_sub, b.at<u32>(NSPL),
+       d->own_tok.as<u64>(), d->num_out.as<u64>(), b.at<u32>(RFIRST));
+    CK(k_long_write, E, b.at<u32>(HIDX), cnt + 2, owner, boff, sbody, nw, base, b.at<u32>(NSPL),
+       b.at<u32>(RFIRST), tsym, tcnt);
   }
-  lids.release();
-  gids.release();
-  gpos.release();
   // per-rule counts -> CSR offsets (no search: the scan IS the offsets)
-  {
-    DBuf wide((R + 1) * 8, st);
-    d->own_off.alloc((R + 1) * 8, st);
-    d->sub_off.alloc((R + 1) * 8, st);
-    CK(k_widen_u32, R + 1, n_own.as<u32>(), R, wide.as<u64>());
-    exclusive_scan_u64(wide.as<u64>(), d->own_off.as<u64>(), R + 1, st);
-    CK(k_widen_u32, R + 1, n_sub.as<u32>(), R, wide.as<u64>());
-    exclusive_scan_u64(wide.as<u64>(), d->sub_off.as<u64>(), R + 1, st);
-  }
+  d->own_off.alloc((R + 1) * 8, st);
+  d->sub_off.alloc((R + 1) * 8, st);
+  u64* wide = a.at<u64>(WIDE);
+  CK(k_widen_u32, R + 1, n_own, R, wide);
+  exclusive_scan_u64(wide, d->own_off.as<u64>(), R + 1, st);
+  CK(k_widen_u32, R + 1, n_sub, R, wide);
+  exclusive_scan_u64(wide, d->sub_off.as<u64>(), R + 1, st);
   u64 tot[2];
   GT_CUDA(cudaMemcpyAsync(&tot[0], d->own_off.as<u64>() + R, 8, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaMemcpyAsync(&tot[1], d->sub_off.as<u64>() + R, 8, cudaMemcpyDeviceToHost, st));
@@ -371,9 +362,9 @@ void build_rule_pairs(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_
   d->sub_ids.alloc(Es * 4 + 4, st);
   d->sub_freqs.alloc(Es * 4 + 4, st);
   sub_rule.alloc(Es * 4 + 4, st);
-  CK(k_rules_compact, E, owner, boff, E, n_own.as<u32>(), n_sub.as<u32>(), d->own_off.as<u64>(),
-     d->sub_off.as<u64>(), tsym.as<u32>(), tcnt.as<u32>(), d->own_ids.as<u32>(), d->own_freqs.as<u32>(),
-     own_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), sub_rule.as<u32>());
+  CK(k_rules_compact, E, owner, boff, E, n_own, n_sub, d->own_off.as<u64>(), d->sub_off.as<u64>(), tsym, tcnt,
+     d->own_ids.as<u32>(), d->own_freqs.as<u32>(), own_rule.as<u32>(), d->sub_ids.as<u32>(),
+     d->sub_freqs.as<u32>(), sub_rule.as<u32>());
 }
 
 }  // namespace gt

@@ -1,6 +1,8 @@
 // cub_ops.cu — device-wide sort/scan/select plumbing (CUB, CUDA 12.9 toolkit
 // headers, instantiated into this library).  Used by the DAG loader and by
 // the result-assembly steps; the analytics kernels themselves are ours.
+#include <algorithm>
+
 #include <cub/cub.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -10,13 +12,49 @@
 
 namespace gt {
 
+// CUB temporary storage: a per-thread, per-stream buffer reused across calls
+// (stream order makes the reuse safe) for requests up to kTempCache bytes —
+// an allocation + free per CUB call is ~4 us of host time, and a small
+// grammar's gt_open makes a dozen CUB calls.  Never freed (process lifetime;
+// freeing from a thread_local destructor would run after the CUDA teardown).
+constexpr size_t kTempCache = 64ull << 20;
+struct TempSlot {
+  cudaStream_t s = nullptr;
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+static void* temp_for(cudaStream_t s, size_t bytes) {
+  static thread_local TempSlot slots[4];
+  TempSlot* t = nullptr;
+  for (auto& x : slots)
+    if (x.s == s) t = &x;
+  if (!t)
+    for (auto& x : slots)
+      if (!x.s) {
+        t = &x;
+        t->s = s;
+        break;
+      }
+  if (!t) return nullptr;
+  if (t->bytes < bytes) {
+    if (t->p) cudaFreeAsync(t->p, s);
+    t->p = nullptr;
+    t->bytes = 0;
+    GT_CUDA(cudaMallocAsync(&t->p, bytes, s));
+    t->bytes = bytes;
+  }
+  return t->p;
+}
+
 template <class F>
 static void with_temp(const char* name, F f, cudaStream_t s) {
   size_t bytes = 0;
   f(nullptr, bytes);
-  DBuf tmp(bytes ? bytes : 16, s);
+  void* cached = bytes && bytes <= kTempCache ? temp_for(s, std::max<size_t>(bytes, 4096)) : nullptr;
+  DBuf tmp;
+  if (!cached) tmp.alloc(bytes ? bytes : 16, s);
   ProfScope ps(name, s);
-  f(tmp.p, bytes);
+  f(cached ? cached : tmp.p, bytes);
   g_launches += 4;  // CUB device-wide primitives launch a small fixed set of kernels
 }
 
