@@ -106,6 +106,15 @@ struct Carve {
   }
 };
 
+// a non-owning view with DBuf's accessor (a carved piece used where a DBuf was)
+struct DPtr {
+  void* p;
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
 // ---- the device DAG ---------------------------------------------------------
 
 struct Levels {

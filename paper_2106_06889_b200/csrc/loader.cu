@@ -1181,8 +1181,9 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     if (ok && !words_only && P.R >= 2 && p1 < n) {
       const u64 nch = (n - p1 + kChunkB - 1) / kChunkB, S = nch * kWin + 1;
       const int K2 = bitlen(nch);  // J_0 .. J_{K2-1} cover c <= nch chunk steps
-      DBuf nx((u64)K2 * S * 4, st), ct((u64)K2 * S * 4, st), entry(nch * 4, st), base(nch * 4, st), bad(4, st);
-      DBuf mask(nch * kWin * kMaskW * 4, st);
+      const Carve cv(st, {(u64)K2 * S * 4, (u64)K2 * S * 4, nch * 4, nch * 4, 4, nch * kWin * kMaskW * 4});
+      const DPtr nx{cv.at<void>(0)}, ct{cv.at<void>(1)}, entry{cv.at<void>(2)}, base{cv.at<void>(3)},
+          bad{cv.at<void>(4)}, mask{cv.at<void>(5)};
       GT_KLAUNCH("k_chunk_tables", k_chunk_tables, grid_for(nch * 32, kTabWarps * 32), kTabWarps * 32, st,
                  raw.as<u32>(), n, p1, nch, nx.as<u32>(), ct.as<u32>(), mask.as<u32>());
       if (K2 > 1) {
@@ -1641,7 +1642,8 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     // every edge is sorted (dropped ones under key nl + 1, after all levels),
     // so no count has to come back to the host first
     // the edge triples travel with the level keys (one radix pass for <= 255 levels)
-    DBuf key(Es * 4 + 4, st), key2(Es * 4 + 4, st), v1(Es * 12 + 12, st), v2(Es * 12 + 12, st);
+    const Carve cv(st, {Es * 4 + 4, Es * 4 + 4, Es * 12 + 12, Es * 12 + 12});
+    const DPtr key{cv.at<void>(0)}, key2{cv.at<void>(1)}, v1{cv.at<void>(2)}, v2{cv.at<void>(3)};
     LAUNCH(k_edge_level_keys2, Es, group_of, keep, lvl, (u32)nl + 1, Es, key.as<u32>());
     if (map) LAUNCH(k_pack3_map, Es, a_src, b_src, f_src, Es, map, v1.as<U3>());
     else LAUNCH(k_pack3, Es, a_src, b_src, f_src, Es, v1.as<U3>());
@@ -1659,12 +1661,12 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // tid: rules numbered by top-down level (stable: ascending rule id within
   // a level, so the td edge lists stay sorted by destination)
   {
-    DBuf iota(R * 4, st), k2(R * 4, st), ord(R * 4, st);
-    LAUNCH(k_iota_u32, R, iota.as<u32>(), R);
-    sort_pairs_u32_u32(d->td_level.as<u32>(), k2.as<u32>(), iota.as<u32>(), ord.as<u32>(), R,
+    const Carve cv(st, {R * 4, R * 4, R * 4});
+    LAUNCH(k_iota_u32, R, cv.at<u32>(0), R);
+    sort_pairs_u32_u32(d->td_level.as<u32>(), cv.at<u32>(1), cv.at<u32>(0), cv.at<u32>(2), R,
                        std::max(1, bitlen((u64)ntd)), st);
     d->tid.alloc(R * 4, st);
-    LAUNCH(k_rank_of, R, ord.as<u32>(), R, d->tid.as<u32>());
+    LAUNCH(k_rank_of, R, cv.at<u32>(2), R, d->tid.as<u32>());
   }
   {
     // td: par entries (grouped by child) whose parent is not the root
