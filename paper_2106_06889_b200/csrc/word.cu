@@ -237,7 +237,7 @@ bool td_word_records(DeviceDag* d, DevRecords* R) {
   if (!small_task(d)) return false;
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
-  DBuf w(d->R * 8, st), bsum(2 * 1024 * 8, st), tot(16, st);
+  const Carve cv(st, {d->R * 8, 2 * 1024 * 8, 16});  // rows, block sums, totals
   d->word_counts.alloc(V * 8 + 8, st);
   R->id.alloc(V * 4 + 4, st);
   R->count.alloc(V * 8 + 8, st);
@@ -245,11 +245,11 @@ bool td_word_records(DeviceDag* d, DevRecords* R) {
   c.compact = 1;
   c.rid = R->id.as<u32>();
   c.rcnt = R->count.as<u64>();
-  c.tot = tot.as<u64>();
-  c.bsum = bsum.as<u64>();
-  td_words_fused<SumMode>(d, w.as<u64>(), d->word_counts.as<u64>(), false, &c);
+  c.tot = cv.at<u64>(2);
+  c.bsum = cv.at<u64>(1);
+  td_words_fused<SumMode>(d, cv.at<u64>(0), d->word_counts.as<u64>(), false, &c);
   u64 h[2];
-  GT_CUDA(cudaMemcpyAsync(h, tot.p, 16, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(h, c.tot, 16, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
   R->n = h[0];
   return true;
@@ -260,7 +260,7 @@ bool td_presence_records(DeviceDag* d, DevRecords* R) {
   if (!small_task(d) || Fo > 64) return false;
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
-  DBuf m(d->R * 8, st), pres(V * 8 + 8, st), bsum(2 * 1024 * 8, st), tot(16, st);
+  const Carve cv(st, {d->R * 8, V * 8 + 8, 2 * 1024 * 8, 16});  // rows, presence, block sums, totals
   R->id.alloc(V * (u64)std::max<u32>(Fo, 1) * 4 + 4, st);
   R->group_id.alloc(V * 4 + 4, st);
   R->group_off.alloc((V + 1) * 8, st);
@@ -269,11 +269,11 @@ bool td_presence_records(DeviceDag* d, DevRecords* R) {
   c.rid = R->id.as<u32>();
   c.gid = R->group_id.as<u32>();
   c.goff = R->group_off.as<u64>();
-  c.tot = tot.as<u64>();
-  c.bsum = bsum.as<u64>();
-  td_words_fused<OrMode>(d, m.as<u64>(), pres.as<u64>(), true, &c);
+  c.tot = cv.at<u64>(3);
+  c.bsum = cv.at<u64>(2);
+  td_words_fused<OrMode>(d, cv.at<u64>(0), cv.at<u64>(1), true, &c);
   u64 h[2];
-  GT_CUDA(cudaMemcpyAsync(h, tot.p, 16, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(h, c.tot, 16, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
   R->n = h[0];
   R->n_groups = h[1];
