@@ -693,8 +693,10 @@ __global__ void __launch_bounds__(kKahnBlock) k_kahn(KahnCtl* ctl, u32* bm0, u32
   const u64 warp = gtid >> 5, nwarps = nthreads >> 5;
   const unsigned lane = threadIdx.x & 31u;
   const volatile uint8_t* rv = reach;
+  // words per warp step: the smallest power of two that covers the bitmap in
+  // one step per warp (a second step doubles a layer's dependent chain)
   u32 WS = 1;
-  while (WS < 32 && (u64)WS * 2 * nwarps <= nwords) WS *= 2;
+  while (WS < 32 && (u64)WS * nwarps < nwords) WS *= 2;
   u64 found = 0, L = 1;
   for (;; L++) {
     if (__ldcg(&ctl->any[L % 3]) == 0 || L > max_layers) break;
