@@ -1495,7 +1495,8 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     DeviceDag* d;
     ~StreamGuard() {
       cudaStreamSynchronize(s);
-      rebind_stream(main, {&d->ow_word, &d->ow_rule, &d->ow_freq, &d->ow_off});
+      rebind_stream(main, {&d->ow_word, &d->ow_rule, &d->ow_freq, &d->ow_off, &d->be_rule, &d->be_child,
+                           &d->be_freq, &d->be_off_dev});
       stream_release(d->device, s);
     }
   } own_guard{s_own, st, d};
@@ -1638,7 +1639,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // buffer: te and be level offsets, root height, W)
   static thread_local PinnedU64 stage_host;
   u64* stage = stage_host.get(2 * ((u64)ntd + 3) + 3);
-  auto level_edges = [&](const u32* group_of, const uint8_t* keep, const u32* lvl, int nl,
+  auto level_edges = [&](cudaStream_t st, const u32* group_of, const uint8_t* keep, const u32* lvl, int nl,
                          const u32* a_src, const u32* b_src, const u32* f_src, DBuf& oa, DBuf& ob,
                          DBuf& of, u64* off_stage, DBuf& off_dev, const u32* map) {
     // every edge is sorted (dropped ones under key nl + 1, after all levels),
@@ -1660,6 +1661,20 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     GT_CUDA(cudaMemcpyAsync(off_stage, koff.p, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
     off_dev = std::move(koff);
   };
+  // be: sub entries (grouped by rule) by the rule's TOP-DOWN level; walked in
+  // decreasing level order every child is finished before its parents (a
+  // child's td level exceeds each parent's), which is all the bottom-up sums
+  // need.  The root (td level 0) comes last.  Built on the side stream,
+  // concurrently with the tid numbering and the td lists below.
+  cudaEvent_t ev_lv, ev_be;
+  GT_CUDA(cudaEventCreateWithFlags(&ev_lv, cudaEventDisableTiming));
+  GT_CUDA(cudaEventCreateWithFlags(&ev_be, cudaEventDisableTiming));
+  GT_CUDA(cudaEventRecord(ev_lv, st));
+  GT_CUDA(cudaStreamWaitEvent(s_own, ev_lv, 0));
+  level_edges(s_own, sub_rule.as<u32>(), nullptr, d->td_level.as<u32>(), ntd, sub_rule.as<u32>(),
+              d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), d->be_rule, d->be_child, d->be_freq,
+              stage + (ntd + 3), d->be_off_dev, nullptr);
+  GT_CUDA(cudaEventRecord(ev_be, s_own));
   // tid: rules numbered by top-down level (stable: ascending rule id within
   // a level, so the td edge lists stay sorted by destination)
   {
@@ -1674,17 +1689,13 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     // td: par entries (grouped by child) whose parent is not the root
     DBuf keep(Es + 1, st);
     LAUNCH(k_flag_nonzero_u32, Es, d->par_ids.as<u32>(), Es, keep.as<uint8_t>());
-    level_edges(child_sorted.as<u32>(), keep.as<uint8_t>(), d->td_level.as<u32>(), ntd,
+    level_edges(st, child_sorted.as<u32>(), keep.as<uint8_t>(), d->td_level.as<u32>(), ntd,
                 child_sorted.as<u32>(), d->par_ids.as<u32>(), d->par_freqs.as<u32>(), d->te_child,
                 d->te_par, d->te_freq, stage, d->te_off_dev, d->tid.as<u32>());
-    // be: sub entries (grouped by rule) by the rule's TOP-DOWN level; walked
-    // in decreasing level order every child is finished before its parents
-    // (a child's td level exceeds each parent's), which is all the bottom-up
-    // sums need.  The root (td level 0) comes last.
-    level_edges(sub_rule.as<u32>(), nullptr, d->td_level.as<u32>(), ntd, sub_rule.as<u32>(),
-                d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), d->be_rule, d->be_child, d->be_freq,
-                stage + (ntd + 3), d->be_off_dev, nullptr);
   }
+  GT_CUDA(cudaStreamWaitEvent(st, ev_be, 0));  // the bottom-up pass below reads the be lists
+  cudaEventDestroy(ev_lv);
+  cudaEventDestroy(ev_be);
   sub_rule.release();
   child_sorted.release();
   // bottom-up levels = heights (leaf = 1; the reference's bottom-up rounds,
