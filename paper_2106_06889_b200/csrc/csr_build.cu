@@ -115,7 +115,10 @@ __global__ void k_rules_short(const u32* __restrict__ body, const u64* __restric
     } else if (len <= kShort) {
       short_rule<32>(body, b, (u32)len, o);
     } else {
-      f = len > kGiant ? 2 : 1;
+      // the root (rule 0, body positions [0, L0)) is sorted on its own, in
+      // place and without keys to gather: it is the one long body of a
+      // Sequitur grammar
+      f = r == 0 ? 3 : (len > kGiant ? 2 : 1);
     }
     lflag[r] = f;
     n_own[r] = o.no;
@@ -290,6 +293,9 @@ __global__ void k_rules_compact(const u32* __restrict__ owner, const u64* __rest
 
 #define CK(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
 
+// the root's body length, known on the host before the device DAG is built
+static u64 boff_host_root_len(const DeviceDag* d) { return d->L0; }
+
 void build_rule_pairs(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_rule, cudaStream_t st) {
   const u64 R = d->R, E = d->E, nw = d->nw, base = d->nw + d->ns;
   const u32* body = d->body.as<u32>();
@@ -316,11 +322,14 @@ void build_rule_pairs(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_
   GT_CUDA(cudaMemcpyAsync(h, cnt, 32, cudaMemcpyDeviceToHost, st));
   stream_sync(st);
   const u64 nmed = h[0], ngel = h[1], ngiant = h[3];
-  if (nmed || ngel) {
+  const u64 L0 = boff_host_root_len(d);
+  const bool root_long = L0 > kShort;
+  if (nmed || ngel || root_long) {
     enum { SBODY, BEG, END, K1, K2, GRANK, HEAD, HIDX, NSPL, RFIRST };
     const Carve b(st, {E * 4 + 4, nmed * 4 + 4, nmed * 4 + 4, ngel * 8 + 8, ngel * 8 + 8, R * 4 + 4, E + 1,
                        E * 4 + 4, R * 4 + 4, R * 4 + 4});
     u32* sbody = b.at<u32>(SBODY);
+    if (root_long) sort_keys_u32(body, sbody, L0, std::max(1, bitlen(d->nw + d->ns + R - 1)), st);
     if (nmed) {
       CK(k_seg_bounds, nmed, a.at<u32>(LIDS), nmed, boff, b.at<int>(BEG), b.at<int>(END));
       sort_segments_listed_u32(body, sbody, E, nmed, b.at<int>(BEG), b.at<int>(END), st);

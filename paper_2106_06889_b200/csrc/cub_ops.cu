@@ -86,6 +86,13 @@ void sort_pairs_u32_u3(u32* ki, u32* ko, U3* vi, U3* vo, u64 n, int end_bit, cud
   }, s);
 }
 
+void sort_keys_u32(const u32* ki, u32* ko, u64 n, int end_bit, cudaStream_t s) {
+  if (!n) return;
+  with_temp("cub::SortKeys32", [&](void* t, size_t& b) {
+    GT_CUDA(cub::DeviceRadixSort::SortKeys(t, b, ki, ko, (int64_t)n, 0, end_bit, s));
+  }, s);
+}
+
 void sort_keys_u64(u64* ki, u64* ko, u64 n, int end_bit, cudaStream_t s) {
   if (!n) return;
   with_temp("cub::SortKeys64", [&](void* t, size_t& b) {

@@ -198,6 +198,7 @@ void sort_pairs_u64_u32(u64* keys_in, u64* keys_out, u32* vals_in, u32* vals_out
 void sort_pairs_u32_u32(u32* keys_in, u32* keys_out, u32* vals_in, u32* vals_out, u64 n,
                         int end_bit, cudaStream_t s);
 void sort_keys_u64(u64* keys_in, u64* keys_out, u64 n, int end_bit, cudaStream_t s);
+void sort_keys_u32(const u32* keys_in, u32* keys_out, u64 n, int end_bit, cudaStream_t s);
 void exclusive_scan_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
 void inclusive_scan_u32(const u32* in, u32* out, u64 n, cudaStream_t s);
 // ordered compaction of indices i in [0,n) with flags[i] != 0; count -> d_count
