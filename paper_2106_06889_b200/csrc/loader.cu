@@ -3,16 +3,21 @@
 // Replaces deserialize_grammar (grammar.py:193-228), build_dag
 // (dag.py:131-230) and the round discovery the reference's engine performs
 // every traversal (engine.py:196-227 top-down mask rounds, engine.py:313-335
-// bottom-up readiness rounds).  The host only walks the u32 length words (a
-// sequential chain) and validates the dictionary; everything proportional to
-// E runs on the device:
-//   unpack -> (rule,symbol) radix sort -> run-length encode -> own/sub CSR
-//   -> parent CSR (stable sort by child) -> per-rule sums
-//   -> bottom-up layering (Kahn from the leaves; = reference bottom-up rounds,
-//      doubles as the cycle check) -> top-down layering (Kahn over non-root
-//      in-edges; = reference top-down rounds; carries reachability)
-//   -> exp_len by bottom-up level -> root segments, segment tokens, root
-//      occurrence lists -> word-major transpose of the own pairs.
+// bottom-up readiness rounds).  The host validates the header and the
+// dictionary while the blob uploads; everything proportional to E runs on
+// the device:
+//   rule-chain parse (chunk tables + doubling over chunk states; word-level
+//   doubling / host walk only as fallbacks) -> unpack (body, owner)
+//   -> own/sub CSR (csr_build.cu: per-rule register sorts, the root sorted
+//      in place) -> parent CSR and the word-major own transpose (payload
+//      radix sorts; side stream) -> per-rule sums
+//   -> top-down layering (persistent Kahn over non-root in-edges with a
+//      bitmap frontier; = reference top-down rounds; carries reachability;
+//      an incomplete layering is the cycle check)
+//   -> tid numbering + top-down edge lists, bottom-up edge lists (side
+//      stream) -> heights (= reference bottom-up rounds) and exp_len in one
+//      reverse pass -> root segments, segment tokens, root occurrence lists
+//      (helper thread + stream).
 // Error checks are reported in the reference's order and with its messages;
 // the exact rule named in a cycle message needs the reference's DFS order,
 // so only on that error path the host replays _topo_order (grammar.py:127).
