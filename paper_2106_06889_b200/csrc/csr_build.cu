@@ -9,10 +9,11 @@
 //   * bodies of <= 32 symbols (all but a handful of rules) are sorted in
 //     registers by one thread with a bitonic network and run-length encoded
 //     on the spot;
-//   * bodies of 33..kGiant symbols go through a segmented sort (CUB, only
-//     those segments), bodies above kGiant (typically the root of a
-//     many-file corpus) through one radix sort of their (rule, symbol) keys;
-//     their runs are then found element-parallel (head flags, select).
+//   * the root (rule 0, body positions [0, L0)) is sorted in place with one
+//     32-bit radix sort; other bodies of 33..kGiant symbols go through a
+//     segmented sort (CUB, only those segments), longer ones through one
+//     radix sort of their (giant rank, symbol) keys; the runs of all long
+//     bodies are then found element-parallel (head flags, select).
 // Every rule writes its runs in place at its body offset (own words first,
 // then the child rules: words sort below splitters below rules), the per-rule
 // counts are scanned into own_off / sub_off directly, and one element-
