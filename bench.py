@@ -405,7 +405,14 @@ def main():
                 "share_of_step": (ms_l / K) / (sum(prof_ms) / K), "profiled_step_ms": sum(prof_ms) / K,
                 "peak_source": peak_src,
                 "kernel_timing": "CUDA events per launch on the library stream over K profiled steps "
-                                 "(same workload, run after the unprofiled timed region)"}
+                                 "(same workload, run after the unprofiled timed region)",
+                # the top-down pass is a chain of grid-barrier-separated levels:
+                # its time per level against the measured per-level floor
+                # (grid barrier + item load + L2 gather + RED, tools/barrier_probe.cu)
+                "latency_model": {"levels_per_launch": info["td_levels"],
+                                  "us_per_level_upper": (ms_l / n_l) * 1e3 / max(1, info["td_levels"]),
+                                  "floor_us_per_level": [2.0, 2.7], "barrier_us": 1.26,
+                                  "floor_source": "profiles/r1_barrier_probe.txt"}}
     kernel_table = {k: {"launches_per_step": n / K, "ms_per_step": round(ms / K, 5)} for k, (n, ms) in
                     sorted(rep.items(), key=lambda kv: -kv[1][1])[:12]}
 
