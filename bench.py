@@ -398,7 +398,10 @@ def main():
         ach = b * K / (ms_l / 1e3) / 1e9
         # the committed ncu capture is of the default workload only
         traffic, traffic_src = ncu_traffic(k_dom) if args.config == "c2" and args.scale == 1.0 else (None, None)
-        roof = {"bound": "hbm", "kernel": k_dom, "launches_per_step": n_l / K,
+        roof = {"bound": "hbm", "kernel": k_dom,
+                # phase label -> the CUDA symbol in the ncu launch list
+                "cuda_symbol": {"k_td_levels": "k_segred1_levels"}.get(k_dom, k_dom),
+                "launches_per_step": n_l / K,
                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "traffic_unit": "bytes per step (ncu dram read+write)",
                 "traffic_source": traffic_src, "alg_bytes_per_step": b, "kernel_ms_per_step": ms_l / K,
@@ -419,7 +422,7 @@ def main():
     # ---- e2e through the public C-ABI from pinned host bytes: gt_open (H2D +
     # device DAG build) + the step (+ collective) + D2H of results + gt_close
     e2e_times, d2h_bytes, parts = [], 0, []
-    for i in range(max(2, min(args.steps, 5)) + 1):
+    for i in range(max(3, min(args.steps, 20)) + 1):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
