@@ -150,6 +150,18 @@ int gt_info_get(const gt_ctx* ctx, gt_info* out);
  * seq_len is used by SEQCOUNT / RANKEDINVERTEDINDEX only. */
 int gt_run(gt_ctx* ctx, int task, int seq_len, int strategy, int file_set_width,
            gt_result** out);
+/* Run several tasks over one DAG in one call; outs[i] receives the result of
+ * tasks[i] (the same result gt_run would give).  Tasks that share a traversal
+ * share it on the device: a WORDCOUNT (or SORT) together with an
+ * INVERTEDINDEX whose owned files fit one presence word (<= 64) and that runs
+ * top-down run as ONE top-down pass over {weight, presence} rule pairs — the
+ * level chain, word reduce and compaction of both tasks in one launch (the
+ * bench step: BASELINE.json's word count + inverted index).  The shared pass's
+ * device time is charged to the word-count result (the inverted index's
+ * device_ms is 0); the other tasks run as by gt_run.  On error every outs[i]
+ * is NULL. */
+int gt_run_many(gt_ctx* ctx, const int* tasks, int ntasks, int seq_len, int strategy,
+                int file_set_width, gt_result** outs);
 int gt_result_view(const gt_result* res, gt_view* out);
 void gt_result_free(gt_result* res);
 void gt_close(gt_ctx* ctx);

@@ -12,7 +12,7 @@ from .errors import (CorruptionError, DivergenceError, FormatError, GtadocError,
 from .tasks import (TASK_NAMES, InvertedIndex, RankedInvertedIndex, SequenceCounts,
                     SortedWords, TermVectors, TraversalConfig, WordCounts, first_divergence,
                     inverted_index, output_digest, ranked_inverted_index, render, render_native,
-                    run_compact, run_task, sequence_count, sort_by_frequency, term_vector,
+                    run_compact, run_compact_many, run_task, run_tasks, sequence_count, sort_by_frequency, term_vector,
                     word_count)
 
 __version__ = "0.1.0"
@@ -23,5 +23,5 @@ __all__ = [
     "sequence_count", "ranked_inverted_index", "WordCounts", "SortedWords", "InvertedIndex",
     "TermVectors", "SequenceCounts", "RankedInvertedIndex", "TASK_NAMES", "GtadocError",
     "UsageError", "IngestError", "ResourceError", "FormatError", "CorruptionError",
-    "DivergenceError", "output_digest", "render_native",
+    "DivergenceError", "output_digest", "render_native", "run_compact_many", "run_tasks",
 ]

@@ -218,9 +218,9 @@ static const T* pull(gt_result* r, const DBuf& b, u64 n, cudaStream_t st, u64* b
   return (const T*)h;
 }
 
-static void finish(gt_ctx* c, gt_result* r, DevRecords& R, int task, int seq_len, int wbits,
-                   int strat, std::chrono::steady_clock::time_point t0, u64 launches0) {
-  cudaStream_t st = c->d.stream;
+// enqueue the D2H copies of a result's compact arrays into pinned blocks the
+// gt_result owns; returns the bytes
+static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int wbits, int strat, cudaStream_t st) {
   u64 bytes = 0;
   gt_view& v = r->v;
   v.task = task;
@@ -238,6 +238,15 @@ static void finish(gt_ctx* c, gt_result* r, DevRecords& R, int task, int seq_len
   v.key = pull<uint64_t>(r, R.key, R.n, st, &bytes);
   v.gram = pull<uint32_t>(r, R.gram, R.n * l, st, &bytes);
   v.count = pull<uint64_t>(r, R.count, R.n, st, &bytes);
+  v.d2h_bytes = bytes;
+  return bytes;
+}
+
+static void finish(gt_ctx* c, gt_result* r, DevRecords& R, int task, int seq_len, int wbits,
+                   int strat, std::chrono::steady_clock::time_point t0, u64 launches0) {
+  cudaStream_t st = c->d.stream;
+  pull_records(r, R, task, seq_len, wbits, strat, st);
+  gt_view& v = r->v;
   GT_CUDA(cudaEventRecord(c->ev[2], st));
   GT_CUDA(cudaStreamSynchronize(st));
   float ms = 0, ms2 = 0;
@@ -245,7 +254,6 @@ static void finish(gt_ctx* c, gt_result* r, DevRecords& R, int task, int seq_len
   GT_CUDA(cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]));
   v.device_ms = ms;
   v.d2h_ms = ms2;
-  v.d2h_bytes = bytes;
   v.kernel_launches = g_launches - launches0;
   v.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -344,6 +352,82 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
     return status;
   }
   *out = r;
+  return GT_OK;
+}
+
+int gt_run_many(gt_ctx* c, const int* tasks, int ntasks, int seq_len, int strategy, int file_set_width,
+                gt_result** outs) {
+  for (int i = 0; i < ntasks; i++) outs[i] = nullptr;
+  if (ntasks < 0) {
+    set_last_error("gt_run_many: negative task count");
+    return GT_E_USAGE;
+  }
+  // the fusable group: the first word count / sort with the first inverted
+  // index (one top-down pass of {weight, presence} pairs, word.cu
+  // td_wc_ii_records) when both would run top-down on one launch
+  int iw = -1, ii = -1;
+  for (int i = 0; i < ntasks; i++) {
+    if (iw < 0 && (tasks[i] == GT_WORDCOUNT || tasks[i] == GT_SORT)) iw = i;
+    if (ii < 0 && tasks[i] == GT_INVERTEDINDEX) ii = i;
+  }
+  const int fsw = file_set_width;
+  for (int i = 0; i < ntasks; i++) {
+    if (iw >= 0 && ii >= 0 && (i == iw || i == ii) && strategy != GT_BOTTOMUP &&
+        select_strategy(c->d, GT_INVERTEDINDEX, strategy, fsw) == GT_TOPDOWN) {
+      if (i != std::min(iw, ii)) continue;  // produced with its partner
+      gt_result* rw = new gt_result();
+      gt_result* ri = new gt_result();
+      bool fused = false;
+      int status = guard([&] {
+        DeviceDag& d = c->d;
+        GT_CUDA(cudaSetDevice(d.device));
+        cudaStream_t st = d.stream;
+        auto t0 = std::chrono::steady_clock::now();
+        u64 launches0 = g_launches;
+        GT_CUDA(cudaEventRecord(c->ev[0], st));
+        DevRecords W, I;
+        if (!td_wc_ii_records(&d, &W, &I)) return;
+        fused = true;
+        if (tasks[iw] == GT_SORT) order_by_count(&d, &W, 0, nullptr);
+        GT_CUDA(cudaEventRecord(c->ev[1], st));
+        pull_records(rw, W, tasks[iw], seq_len, 0, GT_TOPDOWN, st);
+        pull_records(ri, I, GT_INVERTEDINDEX, seq_len, 0, GT_TOPDOWN, st);
+        GT_CUDA(cudaEventRecord(c->ev[2], st));
+        GT_CUDA(cudaStreamSynchronize(st));
+        float ms = 0, ms2 = 0;
+        GT_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+        GT_CUDA(cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]));
+        const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        // the shared pass is charged to the word-count result
+        rw->v.device_ms = ms;
+        ri->v.device_ms = 0.0;
+        rw->v.d2h_ms = ri->v.d2h_ms = ms2;
+        rw->v.total_ms = ri->v.total_ms = tot;
+        rw->v.kernel_launches = g_launches - launches0;
+        ri->v.kernel_launches = 0;
+      });
+      if (status != GT_OK) {
+        delete rw;
+        delete ri;
+        for (int j = 0; j < ntasks; j++) gt_result_free(outs[j]), outs[j] = nullptr;
+        return status;
+      }
+      if (fused) {
+        outs[iw] = rw;
+        outs[ii] = ri;
+        continue;
+      }
+      delete rw;
+      delete ri;
+      iw = ii = -1;  // not fusable on this grammar: run them one by one
+    }
+    if (outs[i]) continue;
+    const int st = gt_run(c, tasks[i], seq_len, strategy, file_set_width, &outs[i]);
+    if (st != GT_OK) {
+      for (int j = 0; j < ntasks; j++) gt_result_free(outs[j]), outs[j] = nullptr;
+      return st;
+    }
+  }
   return GT_OK;
 }
 

@@ -39,6 +39,8 @@ namespace gt {
 // per-file cell never exceeds its file's word count), halving the row bytes
 // of the 64-column passes.
 struct SumMode {
+  using V = u64;
+  __device__ static __forceinline__ V zero() { return 0; }
   __device__ static __forceinline__ u64 combine(u32 f, u64 x) { return (u64)f * x; }
   __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a + b; }
   __device__ static __forceinline__ void atomic(u64* p, u64 v) {
@@ -50,6 +52,8 @@ struct SumMode {
 };
 
 struct OrMode {
+  using V = u64;
+  __device__ static __forceinline__ V zero() { return 0; }
   __device__ static __forceinline__ u64 combine(u32, u64 x) { return x; }
   __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a | b; }
   __device__ static __forceinline__ void atomic(u64* p, u64 v) {
@@ -63,12 +67,47 @@ struct OrMode {
 // height pass (bottom-up levels without Kahn): height(r) = max(height(r),
 // 1 + height(child)), combined with u64 atomicMax
 struct HeightMode {
+  using V = u64;
+  __device__ static __forceinline__ V zero() { return 0; }
   __device__ static __forceinline__ u64 combine(u32, u64 x) { return x + 1; }
   __device__ static __forceinline__ u64 merge(u64 a, u64 b) { return a > b ? a : b; }
   __device__ static __forceinline__ void atomic(u64* p, u64 v) {
     atomicMax((unsigned long long*)p, (unsigned long long)v);
   }
 };
+
+// Word count and inverted index in ONE pass (gt_run_many): every rule row is
+// a 16-byte pair {corpus weight (sum), file-presence bitset (or)} — the two
+// tasks share the same edges, levels and barriers, so the step pays one
+// latency-bound level chain instead of two.  A pair is gathered with one
+// 16-byte load (one sector) and flushed with one RED.ADD + one RED.OR.
+struct u64x2 {
+  u64 a, b;
+};
+struct PairPtr {  // where a pair is reduced into: the weight and presence words
+  u64* a;
+  u64* b;
+};
+struct WcPresMode {
+  using V = u64x2;
+  __device__ static __forceinline__ V zero() { return {0, 0}; }
+  __device__ static __forceinline__ V combine(u32 f, V x) { return {(u64)f * x.a, x.b}; }
+  __device__ static __forceinline__ V merge(V x, V y) { return {x.a + y.a, x.b | y.b}; }
+  __device__ static __forceinline__ void atomic(PairPtr p, V v) {
+    if (v.a) atomicAdd((unsigned long long*)p.a, (unsigned long long)v.a);
+    if (v.b) atomicOr((unsigned long long*)p.b, (unsigned long long)v.b);
+  }
+};
+
+// warp shuffles of a mode's value (u64 or a pair)
+__device__ __forceinline__ u64 shfl_up(u64 v, int s) { return __shfl_up_sync(0xFFFFFFFFu, v, s); }
+__device__ __forceinline__ u64 shfl_idx(u64 v, int l) { return __shfl_sync(0xFFFFFFFFu, v, l); }
+__device__ __forceinline__ u64x2 shfl_up(u64x2 v, int s) {
+  return {__shfl_up_sync(0xFFFFFFFFu, v.a, s), __shfl_up_sync(0xFFFFFFFFu, v.b, s)};
+}
+__device__ __forceinline__ u64x2 shfl_idx(u64x2 v, int l) {
+  return {__shfl_sync(0xFFFFFFFFu, v.a, l), __shfl_sync(0xFFFFFFFFu, v.b, l)};
+}
 
 // ---- source row functors ----------------------------------------------------
 // Row and output reads go through L2 (ld.global.cg): the level loops of a
@@ -139,6 +178,25 @@ struct OutColMajorT {  // out[col*V + dst]
 };
 using OutColMajor = OutColMajorT<u64>;
 
+// the fused word count + presence pass: interleaved 16-byte rule rows
+struct RowSrcPair {
+  const u64* in;
+  __device__ __forceinline__ u64x2 operator()(u32 s, u32) const {
+    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(in + 2ull * s));
+    return {v.x, v.y};
+  }
+};
+struct TdRowsPair {
+  u64* out;
+  __device__ __forceinline__ PairPtr operator()(u32 d, u32) const { return {out + 2ull * d, out + 2ull * d + 1}; }
+};
+// per word: the count vector u64[V] and the presence vector u64[V]
+struct OutPair {
+  u64* cnt;
+  u64* pres;
+  __device__ __forceinline__ PairPtr operator()(u32 d, u32) const { return {cnt + d, pres + d}; }
+};
+
 __device__ __forceinline__ u32 item_freq(const u32* freq, u64 i) { return freq ? freq[i] : 1u; }
 
 // ---------------------------------------------------------------------------
@@ -152,59 +210,51 @@ __device__ __forceinline__ void segred1_body(const u32* __restrict__ dst, const 
   // K 32-item steps per tile; the (up to) U steps of a group are
   // loaded together (U independent row gathers in flight per lane), then
   // reduced one after the other with the carried run
+  using V = typename Mode::V;
   constexpr int U = 4;
   const unsigned lane = threadIdx.x & 31u;
   const u64 TILE = 32ull * K;
   for (u64 t0 = warp * TILE; t0 < n; t0 += nwarps * TILE) {
     const u64 tend = t0 + TILE < n ? t0 + TILE : n;
     u32 carry_d = 0xFFFFFFFFu;
-    u64 carry_v = 0;
+    V carry_v = Mode::zero();
 #pragma unroll 1
     for (int k0 = 0; k0 < K; k0 += U) {
       u32 dd[U];
-      u64 vv[U];
+      V vv[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const u64 i = t0 + (u64)(k0 + u) * 32 + lane;
         const bool in_tile = k0 + u < K && i < tend;
         dd[u] = in_tile ? dst[i] : 0xFFFFFFFFu;
-        vv[u] = in_tile ? Mode::combine(item_freq(freq, i), in(src[i], 0)) : 0;
+        vv[u] = in_tile ? Mode::combine(item_freq(freq, i), in(src[i], 0)) : Mode::zero();
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
         if (k0 + u >= K) break;  // warp-uniform
         const u32 d = dd[u];
-        u64 v = vv[u];
+        V v = vv[u];
         const bool ok = d != 0xFFFFFFFFu;
         const u32 d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
         if (carry_d != 0xFFFFFFFFu && d0 != carry_d) {  // the carried run ended at the last step
-          if (lane == 0) {
-            auto* p = out(carry_d, 0);
-            Mode::atomic(p, carry_v);
-          }
+          if (lane == 0) Mode::atomic(out(carry_d, 0), carry_v);
           carry_d = 0xFFFFFFFFu;
-          carry_v = 0;
+          carry_v = Mode::zero();
         }
 #pragma unroll
         for (int s = 1; s < 32; s <<= 1) {
-          const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, s);
+          const V ov = shfl_up(v, s);
           const u32 od = __shfl_up_sync(0xFFFFFFFFu, d, s);
           if (lane >= (unsigned)s && od == d) v = Mode::merge(v, ov);
         }
         if (d == carry_d) v = Mode::merge(v, carry_v);
         const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
-        if (ok && lane != 31 && dn != d) {  // run ends inside this step
-          auto* p = out(d, 0);
-          Mode::atomic(p, v);
-        }
+        if (ok && lane != 31 && dn != d) Mode::atomic(out(d, 0), v);  // run ends inside this step
         carry_d = __shfl_sync(0xFFFFFFFFu, d, 31);
-        carry_v = __shfl_sync(0xFFFFFFFFu, v, 31);
+        carry_v = shfl_idx(v, 31);
       }
     }
-    if (lane == 0 && carry_d != 0xFFFFFFFFu) {
-      auto* p = out(carry_d, 0);
-      Mode::atomic(p, carry_v);
-    }
+    if (lane == 0 && carry_d != 0xFFFFFFFFu) Mode::atomic(out(carry_d, 0), carry_v);
   }
 }
 
@@ -457,6 +507,7 @@ struct PostArgs {
   u64 n;
   u64* out;  // nullptr: no post phase
   u64 out_n;
+  u64* out2;  // WcPresMode: the presence vector u64[V] beside the counts in out
   const u32* rw_word;
   const u32* rw_seg;
   const u32* rw_cnt;
@@ -465,10 +516,13 @@ struct PostArgs {
   int per_file;
   // compaction of out (after one more barrier) into render-order records:
   // 1 = nonzero counts -> (word, count) records (word count); 2 = presence
-  // words -> (word groups, ascending files) (inverted index, <= 64 files).
-  // Outputs sized for the worst case; tot = {records, groups}; bsum =
-  // 2 * gridDim scratch.
+  // words -> (word groups, ascending files) (inverted index, <= 64 files);
+  // 3 = both from the fused pair (WcPresMode): word-count records (wid,
+  // rcnt) and the inverted-index groups / files (gid, goff, rid) share the
+  // word order, so one scan gives both.  Outputs sized for the worst case;
+  // tot = {records, groups}; bsum = 2 * gridDim scratch.
   int compact;
+  u32* wid;
   u32* rid;
   u64* rcnt;
   u32* gid;
@@ -522,20 +576,28 @@ __device__ __forceinline__ void block_scan2(u32 a, u32 b, u32* ea, u32* eb, u32*
 }
 
 // the compaction of the post phase: blocks own contiguous word ranges, count
-// them, learn their offsets after a grid barrier, and write in order
-template <class Mode>
+// them, learn their offsets after a grid barrier, and write in order.  Per
+// word: a = records (1 per nonzero count, or the popcount of the presence
+// word), b = groups (1 per nonempty word; compact 2 and 3 only).
+__device__ __forceinline__ void post_word(const PostArgs& p, u64 w, u64* v, u64* pr) {
+  *v = __ldcg(reinterpret_cast<const unsigned long long*>(p.out + w));
+  *pr = p.compact == 3 ? __ldcg(reinterpret_cast<const unsigned long long*>(p.out2 + w))
+                       : (p.compact == 2 ? *v : 0ull);
+}
+
 __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& grid) {
   const u64 V = p.out_n, nb = gridDim.x;
   const u64 CH = (V + nb - 1) / nb, lo = blockIdx.x * CH, hi = lo + CH < V ? lo + CH : V;
-  const bool pres = p.compact == 2;
+  const bool groups = p.compact >= 2;
   __shared__ unsigned long long sa, sb;
   if (threadIdx.x == 0) sa = sb = 0;
   __syncthreads();
   unsigned long long la = 0, lb = 0;
   for (u64 w = lo + threadIdx.x; w < hi; w += blockDim.x) {
-    const u64 v = __ldcg(reinterpret_cast<const unsigned long long*>(p.out + w));
-    if (v) {
-      la += pres ? (unsigned long long)__popcll(v) : 1ull;
+    u64 v, pr;
+    post_word(p, w, &v, &pr);
+    if (v || pr) {
+      la += groups ? (unsigned long long)__popcll(pr) : 1ull;
       lb += 1;
     }
   }
@@ -546,7 +608,7 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
   }
   if ((threadIdx.x & 31u) == 0 && (la || lb)) {  // one shared atomic per warp
     atomicAdd(&sa, la);
-    if (pres) atomicAdd(&sb, lb);
+    if (groups) atomicAdd(&sb, lb);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -573,7 +635,7 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
       if (blockIdx.x == nb - 1) {
         p.tot[0] = xa + __ldcg(reinterpret_cast<const unsigned long long*>(p.bsum + blockIdx.x));
         p.tot[1] = xb + __ldcg(reinterpret_cast<const unsigned long long*>(p.bsum + nb + blockIdx.x));
-        if (pres) p.goff[p.tot[1]] = p.tot[0];
+        if (groups) p.goff[p.tot[1]] = p.tot[0];
       }
     }
   }
@@ -581,18 +643,24 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
   u64 ba = oa, bb = ob;
   for (u64 t0 = lo; t0 < hi; t0 += blockDim.x) {  // block-uniform trip count
     const u64 w = t0 + threadIdx.x;
-    const u64 v = w < hi ? __ldcg(reinterpret_cast<const unsigned long long*>(p.out + w)) : 0ull;
-    const u32 a = v ? (pres ? (u32)__popcll(v) : 1u) : 0u, b = (pres && v) ? 1u : 0u;
+    u64 v = 0, pr = 0;
+    if (w < hi) post_word(p, w, &v, &pr);
+    const bool nz = v || pr;
+    const u32 a = nz ? (groups ? (u32)__popcll(pr) : 1u) : 0u, b = (groups && nz) ? 1u : 0u;
     u32 ea, eb, ta, tb;
     block_scan2(a, b, &ea, &eb, &ta, &tb);
-    if (v) {
-      if (!pres) {
+    if (nz) {
+      if (!groups) {
         p.rid[ba + ea] = (u32)w;
         p.rcnt[ba + ea] = v;
       } else {
+        if (p.compact == 3) {  // the word-count record of this word
+          p.wid[bb + eb] = (u32)w;
+          p.rcnt[bb + eb] = v;
+        }
         p.gid[bb + eb] = (u32)w;
         p.goff[bb + eb] = ba + ea;
-        u64 q = ba + ea, x = v;
+        u64 q = ba + ea, x = pr;
         while (x) {
           p.rid[q++] = p.file_lo + (u32)(__ffsll((long long)x) - 1);
           x &= x - 1;
@@ -606,18 +674,24 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
 
 template <class Mode, class T = u64>
 __device__ __forceinline__ void seed_rows_body(const SeedArgs& a) {
+  using V = typename Mode::V;
+  constexpr bool pair = std::is_same<Mode, WcPresMode>::value;
   T* row = reinterpret_cast<T*>(a.row);
   const unsigned lane = threadIdx.x & 31u;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const bool is_or = std::is_same<Mode, OrMode>::value;
   for (u64 base = (u64)blockIdx.x * blockDim.x; base < a.n; base += stride) {
     const u64 i = base + threadIdx.x;
-    u64 key = ~0ull, v = 0;
+    u64 key = ~0ull;
+    V v = Mode::zero();
     if (i < a.n) {
       const u32 sg = a.seg[i] - a.file_lo;
       if (sg < a.nseg) {
         const u64 r = a.rule[i];
-        if (!a.per_file) {
+        if constexpr (pair) {  // corpus weight + presence bit of the segment
+          key = r;
+          v = V{(u64)a.cnt[i], 1ull << (sg & 63u)};
+        } else if (!a.per_file) {
           key = r;
           v = a.cnt[i];
         } else if (is_or) {
@@ -631,12 +705,15 @@ __device__ __forceinline__ void seed_rows_body(const SeedArgs& a) {
     }
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, d);
+      const V ov = shfl_up(v, d);
       const u64 ok = __shfl_up_sync(0xFFFFFFFFu, key, d);
       if (lane >= (unsigned)d && ok == key) v = Mode::merge(v, ov);
     }
     const u64 nk = __shfl_down_sync(0xFFFFFFFFu, key, 1);
-    if (key != ~0ull && (lane == 31 || nk != key)) Mode::atomic(&row[key], v);
+    if (key != ~0ull && (lane == 31 || nk != key)) {
+      if constexpr (pair) Mode::atomic(PairPtr{(u64*)row + 2 * key, (u64*)row + 2 * key + 1}, v);
+      else Mode::atomic(&row[key], v);
+    }
   }
 }
 
@@ -695,14 +772,18 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
                                                           const u64* __restrict__ lvl_off, int L0, int L1,
                                                           int reverse, int prefetch, SeedArgs seed, PostArgs post,
                                                           Src in, Out out) {
+  using V = typename Mode::V;
+  constexpr bool pair = std::is_same<Mode, WcPresMode>::value;
   cg::grid_group grid = cg::this_grid();
   if (seed.row) {  // phase 0: clear the rows (and the reduce output), then the root seeds
     u64* zr = reinterpret_cast<u64*>(seed.row);
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < seed.zero_n; i += (u64)gridDim.x * blockDim.x)
       zr[i] = 0;
     if (post.out)
-      for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < post.out_n; i += (u64)gridDim.x * blockDim.x)
+      for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < post.out_n; i += (u64)gridDim.x * blockDim.x) {
         post.out[i] = 0;
+        if (pair) post.out2[i] = 0;
+      }
     grid.sync();
     seed_rows_body<Mode>(seed);
     grid.sync();
@@ -738,31 +819,31 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
   for (int it = 0; it < nit; it++) {
     if (pk) {
       u32 dd[kPre];
-      u64 vv[kPre];
+      V vv[kPre];
       const int K = pk;
 #pragma unroll
       for (int p = 0; p < kPre; p++) {
         dd[p] = pd[p];
-        vv[p] = dd[p] != 0xFFFFFFFFu ? Mode::combine(pf[p], in(ps[p], 0)) : 0;
+        vv[p] = dd[p] != 0xFFFFFFFFu ? Mode::combine(pf[p], in(ps[p], 0)) : Mode::zero();
       }
       fetch(it + 1);  // the next level's items load while these gathers are in flight
       if (__any_sync(0xFFFFFFFFu, dd[0] != 0xFFFFFFFFu)) {
         u32 carry_d = 0xFFFFFFFFu;
-        u64 carry_v = 0;
+        V carry_v = Mode::zero();
 #pragma unroll
         for (int p = 0; p < kPre; p++) {
           if (p >= K) break;  // warp-uniform
           const u32 d = dd[p];
-          u64 v = vv[p];
+          V v = vv[p];
           const u32 d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
           if (carry_d != 0xFFFFFFFFu && d0 != carry_d) {
             if (lane == 0) Mode::atomic(out(carry_d, 0), carry_v);
             carry_d = 0xFFFFFFFFu;
-            carry_v = 0;
+            carry_v = Mode::zero();
           }
 #pragma unroll
           for (int s = 1; s < 32; s <<= 1) {
-            const u64 ov = __shfl_up_sync(0xFFFFFFFFu, v, s);
+            const V ov = shfl_up(v, s);
             const u32 od = __shfl_up_sync(0xFFFFFFFFu, d, s);
             if (lane >= (unsigned)s && od == d) v = Mode::merge(v, ov);
           }
@@ -770,7 +851,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
           const u32 dn = __shfl_down_sync(0xFFFFFFFFu, d, 1);
           if (d != 0xFFFFFFFFu && lane != 31 && dn != d) Mode::atomic(out(d, 0), v);
           carry_d = __shfl_sync(0xFFFFFFFFu, d, 31);
-          carry_v = __shfl_sync(0xFFFFFFFFu, v, 31);
+          carry_v = shfl_idx(v, 31);
         }
         if (lane == 0 && carry_d != 0xFFFFFFFFu) Mode::atomic(out(carry_d, 0), carry_v);
       }
@@ -791,20 +872,28 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
     if (post.n) {
       int K = (int)((post.n + 32 * nwarps - 1) / (32 * nwarps));
       K = K < 1 ? 1 : (K > 16 ? 16 : K);
-      segred1_body<Mode>(post.dst, post.src, post.freq, post.n, K, in, OutColMajorT<u64>{post.out, post.out_n},
-                         warp, nwarps);
+      if constexpr (pair)
+        segred1_body<Mode>(post.dst, post.src, post.freq, post.n, K, in, OutPair{post.out, post.out2}, warp, nwarps);
+      else
+        segred1_body<Mode>(post.dst, post.src, post.freq, post.n, K, in, OutColMajorT<u64>{post.out, post.out_n},
+                           warp, nwarps);
     }
     const bool is_or = std::is_same<Mode, OrMode>::value;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < post.n_rw; i += nthreads) {
       const u32 sg = post.rw_seg[i] - post.file_lo;
       if (sg >= post.nseg) continue;
       const u32 w = post.rw_word[i];
-      if (!post.per_file) Mode::atomic(&post.out[w], Mode::combine(post.rw_cnt[i], 1ull));
-      else Mode::atomic(&post.out[w], is_or ? (1ull << (sg & 63u)) : (u64)post.rw_cnt[i]);
+      if constexpr (pair) {
+        atomicAdd((unsigned long long*)&post.out[w], (unsigned long long)post.rw_cnt[i]);
+        atomicOr((unsigned long long*)&post.out2[w], 1ull << (sg & 63u));
+      } else {
+        if (!post.per_file) Mode::atomic(&post.out[w], Mode::combine(post.rw_cnt[i], 1ull));
+        else Mode::atomic(&post.out[w], is_or ? (1ull << (sg & 63u)) : (u64)post.rw_cnt[i]);
+      }
     }
     if (post.compact) {
       grid.sync();
-      post_compact<Mode>(post, grid);
+      post_compact(post, grid);
     }
   }
 }

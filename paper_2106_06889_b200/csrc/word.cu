@@ -213,7 +213,7 @@ static void td_words_fused(const DeviceDag* d, u64* row, u64* out, bool per_file
     reduce_words<Mode>(d, 1, row, out, per_file);
     return;
   }
-  PostArgs post{d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), d->E_own, out, d->nw,
+  PostArgs post{d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), d->E_own, out, d->nw, nullptr,
                 d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo,
                 (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0};
   if (compact) {
@@ -277,6 +277,53 @@ bool td_presence_records(DeviceDag* d, DevRecords* R) {
   GT_CUDA(cudaStreamSynchronize(st));
   R->n = h[0];
   R->n_groups = h[1];
+  return true;
+}
+
+// Word count AND inverted index (<= 64 owned files) in ONE launch: the
+// rows are {corpus weight, presence bitset} pairs (segreduce.cuh WcPresMode),
+// so both tasks share the top-down level chain — the latency-bound part of a
+// small grammar's pass — and the word reduce, the root words and the
+// compaction (compact 3: the word-count records and the inverted-index
+// groups have the same words in the same order).  Leaves the dense u64[V]
+// counts in d->word_counts like td_word_records.
+bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
+  const u32 Fo = (u32)(d->file_hi - d->file_lo);
+  if (!small_task(d) || Fo > 64) return false;
+  cudaStream_t st = d->stream;
+  const u64 V = d->nw;
+  // rows (pairs), presence, block sums, totals
+  const Carve cv(st, {d->R * 16, V * 8 + 8, 2 * 1024 * 8, 16});
+  d->word_counts.alloc(V * 8 + 8, st);
+  wc->id.alloc(V * 4 + 4, st);
+  wc->count.alloc(V * 8 + 8, st);
+  ii->id.alloc(V * (u64)std::max<u32>(Fo, 1) * 4 + 4, st);
+  ii->group_id.alloc(V * 4 + 4, st);
+  ii->group_off.alloc((V + 1) * 8, st);
+  u64* row = cv.at<u64>(0);
+  const SeedArgs seed{d->rs_rule_t.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
+                      Fo, 1, 1u, row, 2 * d->R};
+  PostArgs post{d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), d->E_own,
+                d->word_counts.as<u64>(), V, cv.at<u64>(1), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
+                d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, Fo, 1};
+  post.compact = 3;
+  post.wid = wc->id.as<u32>();
+  post.rcnt = wc->count.as<u64>();
+  post.rid = ii->id.as<u32>();
+  post.gid = ii->group_id.as<u32>();
+  post.goff = ii->group_off.as<u64>();
+  post.tot = cv.at<u64>(3);
+  post.bsum = cv.at<u64>(2);
+  seg_reduce_levels1<WcPresMode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
+                                 d->te_off_dev.as<u64>(), 1, d->td.nl, 0,
+                                 d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0, &seed, &post,
+                                 RowSrcPair{row}, TdRowsPair{row}, st);
+  u64 h[2];
+  GT_CUDA(cudaMemcpyAsync(h, post.tot, 16, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  ii->n = h[0];
+  ii->n_groups = h[1];
+  wc->n = h[1];
   return true;
 }
 

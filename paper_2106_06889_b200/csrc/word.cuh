@@ -15,6 +15,7 @@ void td_word_counts(DeviceDag* d, DBuf& counts);
 void td_file_counts(DeviceDag* d, DBuf& counts, bool* is32);
 bool td_word_records(DeviceDag* d, DevRecords* R);
 bool td_presence_records(DeviceDag* d, DevRecords* R);
+bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii);
 void order_by_count(DeviceDag* d, DevRecords* R, u32 ncols, const u32* file);
 void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW, DBuf* rows_out = nullptr);
 void td_file_weights(DeviceDag* d, DBuf& w, u32* C, bool* is32);

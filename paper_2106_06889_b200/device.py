@@ -26,7 +26,7 @@ EXPORTS = ("gt_abi_version", "gt_last_error", "gt_open", "gt_info_get", "gt_run"
            "gt_dag_array", "gt_flush_l2", "gt_sync", "gt_profile", "gt_profile_report",
            "gt_set_files", "gt_assemble_counts", "gt_dict_open", "gt_dict_close", "gt_render_view",
            "gt_free_text", "gt_digest_view", "gt_sha256", "gt_table_add_batch", "gt_run_naive",
-           "gt_compress", "gt_compress_free", "gt_compress_last_error")
+           "gt_compress", "gt_compress_free", "gt_compress_last_error", "gt_run_many")
 _lib = None
 
 
@@ -45,6 +45,9 @@ def lib():
         L.gt_info_get.argtypes = [C.c_void_p, C.POINTER(GtInfo)]
         L.gt_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.gt_run.restype = C.c_int
+        L.gt_run_many.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.POINTER(C.c_void_p)]
+        L.gt_run_many.restype = C.c_int
         L.gt_result_view.argtypes = [C.c_void_p, C.POINTER(GtView)]
         L.gt_result_free.argtypes = [C.c_void_p]
         L.gt_close.argtypes = [C.c_void_p]
@@ -125,6 +128,31 @@ class DeviceDag:
             return compact_from_view(v)
         finally:
             L.gt_result_free(r)
+
+    def run_many(self, tasks, seq_len: int, strategy: int, file_set_width: int):
+        """gt_run_many: several tasks in one call (word count + inverted index
+        share one device pass); returns one Compact per task."""
+        rs = self.run_many_raw(tasks, seq_len, strategy, file_set_width)
+        try:
+            return [compact_from_view(v) for _, v in rs]
+        finally:
+            for r, _ in rs:
+                self.free_raw(r)
+
+    def run_many_raw(self, tasks, seq_len: int = 3, strategy: int = 0, file_set_width: int = 64):
+        """gt_run_many returning [(result handle, view)] without copying."""
+        L = lib()
+        n = len(tasks)
+        ids = (C.c_int * n)(*tasks)
+        outs = (C.c_void_p * n)()
+        st = L.gt_run_many(self._h, ids, n, seq_len, strategy, file_set_width, outs)
+        raise_for_status(st, _err())
+        res = []
+        for i in range(n):
+            v = GtView()
+            L.gt_result_view(outs[i], C.byref(v))
+            res.append((C.c_void_p(outs[i]), v))
+        return res
 
     def run_raw(self, task: int, seq_len: int = 3, strategy: int = 0, file_set_width: int = 64):
         """gt_run returning (result handle, view) without copying the arrays;

@@ -84,6 +84,29 @@ def run_compact(dag, task: str, cfg: TraversalConfig | None = None,
     return dag.run(TASK_IDS[task], seq_len, STRATEGY_IDS[cfg.strategy], cfg.file_set_width)
 
 
+def run_compact_many(dag, tasks, cfg: TraversalConfig | None = None,
+                     seq_len: int = DEFAULT_SEQ_LEN) -> list[Compact]:
+    """Several tasks in one call, one Compact per task (same results as
+    run_compact each).  On the device, word count / sort together with the
+    inverted index share ONE top-down pass (gt_run_many)."""
+    cfg = cfg or TraversalConfig()
+    for task in tasks:
+        if task not in TASK_IDS:
+            raise UsageError(f"unknown task {task!r}; expected one of {', '.join(TASK_NAMES)}")
+    if any(t in ("seqcount", "rankedinvertedindex") for t in tasks) and seq_len < 1:
+        raise UsageError("sequence length must be >= 1")
+    if hasattr(dag, "run_many"):
+        return dag.run_many([TASK_IDS[t] for t in tasks], seq_len, STRATEGY_IDS[cfg.strategy],
+                            cfg.file_set_width)
+    return [run_compact(dag, t, cfg, seq_len) for t in tasks]
+
+
+def run_tasks(dag, tasks, cfg: TraversalConfig, seq_len: int = DEFAULT_SEQ_LEN) -> list:
+    """run_task (tasks.py:171-185) for several tasks at once: the reference's
+    output containers, in the order of `tasks`."""
+    return [to_container(c) for c in run_compact_many(dag, tasks, cfg, seq_len)]
+
+
 def output_digest(dag, task: str, cfg: TraversalConfig | None = None,
                   seq_len: int = DEFAULT_SEQ_LEN) -> tuple[str, int]:
     """sha256 hex + byte length of `render(run_task(...))` — the reference

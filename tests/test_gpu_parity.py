@@ -153,6 +153,83 @@ def test_c2_full_wordcount_and_invertedindex_match_oracle():
     dag.close()
 
 
+def test_c2_full_sequence_tasks_match_oracle():
+    """BASELINE configs[1] at full size, sequence tasks (l = 3) against the
+    oracle (sequence.py:292-417; the oracle sizes its per-file gram tables by
+    tokens like the reference: ~9 GB of host RAM here)."""
+    import paper_2106_06889_b200 as gt
+    from oracle.oracle import OracleDag
+    blob, _ = composed("c2", 1.0)
+    dag = gt.DeviceDag(blob)
+    ref = OracleDag(blob)
+    for task in ("seqcount", "rankedinvertedindex"):
+        got = gt.run_compact(dag, task, gt.TraversalConfig(), 3)
+        exp = gt.run_compact(ref, task, gt.TraversalConfig(), 3)
+        assert_same(got, exp, task)
+    dag.close()
+
+
+@pytest.mark.parametrize("scale", [0.1, 1.0])
+def test_c3_many_files_match_oracle(scale, tmp_path):
+    """BASELINE configs[2] (100k small files) at 10k files and at full size:
+    the tasks against the oracle.  The oracle follows the reference's
+    bottom-up per-file path, whose dense segment_rule_counts alone is
+    8*R*F bytes (dag.py:75-86, 38 GB at full size); it runs in a child
+    process under an address-space limit (tests/oracle_worker.py), and the
+    full size is skipped when the host cannot give it that much (logged)."""
+    import os
+    import oracle_worker
+    import paper_2106_06889_b200 as gt
+    blob, stats = composed("c3", scale)
+    need_gb = 2.2 * 8 * stats["R"] * stats["F"] / 2**30 + 8  # dense counts + per-file tables
+    avail_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_AVPHYS_PAGES") / 2**30
+    print(f"c3 scale {scale}: R={stats['R']} F={stats['F']} W={stats['W']}; oracle limit ~{need_gb:.0f} GiB,"
+          f" host has {avail_gb:.0f} GiB available")
+    if need_gb > 0.75 * avail_gb:
+        pytest.skip(f"oracle needs ~{need_gb:.0f} GiB of host RAM, {avail_gb:.0f} GiB available")
+    tasks = TASKS if scale < 1.0 else ["wordcount", "invertedindex", "termvector"]
+    exp = oracle_worker.run(blob, tasks, 3, min(need_gb * 1.5, 0.8 * avail_gb), tmp_path)
+    dag = gt.DeviceDag(blob)
+    for task in tasks:
+        got = gt.run_compact(dag, task, gt.TraversalConfig(), 3)
+        assert_same(got, exp[task], (scale, task))
+        if task == "termvector":
+            assert got.strategy == "topdown-sparse"  # F > file_set_width: the many-file path
+        if task == "invertedindex":
+            assert got.strategy == "topdown"  # presence bitsets (ceil(F/64) words per rule) at any F
+    dag.close()
+
+
+MANY_CASES = [("c2", 0.002, None), ("c3", 0.002, None), ("c4", 0.0005, None), ("c2", 1.0, None)]
+
+
+@pytest.mark.parametrize("name,scale,seed", MANY_CASES)
+def test_run_many_matches_single_runs(name, scale, seed):
+    """gt_run_many (word count / sort + inverted index in ONE device pass when
+    the files fit one presence word) returns exactly what the single-task runs
+    and the oracle return, in the order of the request."""
+    import paper_2106_06889_b200 as gt
+    from oracle.oracle import OracleDag
+    blob, _ = composed(name, scale, seed)
+    dag = gt.DeviceDag(blob)
+    ref = OracleDag(blob)
+    cfg = gt.TraversalConfig()
+    fusable = dag.num_files <= 64
+    for tasks in (["wordcount", "invertedindex"], ["invertedindex", "sort"],
+                  ["termvector", "wordcount", "seqcount", "invertedindex"], ["invertedindex"], ["wordcount"]):
+        got = gt.run_compact_many(dag, tasks, cfg, 3)
+        assert [c.task for c in got] == tasks
+        for task, g in zip(tasks, got):
+            assert_same(g, gt.run_compact(dag, task, cfg, 3), (name, tasks, task, "single"))
+            if scale < 1.0:
+                assert_same(g, gt.run_compact(ref, task, cfg, 3), (name, tasks, task, "oracle"))
+        kinds = {t for t in tasks if t in ("wordcount", "sort", "invertedindex")}
+        if fusable and "invertedindex" in kinds and len(kinds) == 2:
+            ii = got[tasks.index("invertedindex")]
+            assert ii.timings["kernel_launches"] == 0  # produced by the shared pass
+    dag.close()
+
+
 def test_c2_full_sequence_properties():
     """Size-independent properties at full C2 size: per-file window totals equal
     tokens_f - (l-1); every gram's file list is sorted by (-count, file)."""
