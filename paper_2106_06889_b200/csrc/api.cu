@@ -338,9 +338,11 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
         break;
       }
       default: {
-        const bool sparse = strat == GT_BOTTOMUP || force_sparse();
-        run_sequences(&d, task, seq_len, sparse, &R, &wbits);
-        strat = sparse ? GT_TOPDOWN_SPARSE : GT_TOPDOWN;
+        // a forced bottom-up runs Alg. 2 for grams (pooled window tables);
+        // auto for F > file_set_width takes the sparse top-down path
+        const int mode = strategy == GT_BOTTOMUP ? GT_BOTTOMUP
+                         : (strat == GT_BOTTOMUP || force_sparse()) ? GT_TOPDOWN_SPARSE : GT_TOPDOWN;
+        strat = run_sequences(&d, task, seq_len, mode, &R, &wbits);
         break;
       }
     }

@@ -102,22 +102,29 @@ __global__ void k_own_distinct(const u64* own_off, u64 R, u64* bound) {
     bound[r] = own_off[r + 1] - own_off[r];
 }
 
-struct CappedBound {  // min(bound[c], exp_len[c], V)
+// the table-size cap of a rule: min(exp_len, V) for words (local_table_bounds
+// caps, engine.py:338-367), max(exp_len - (l-1), 0) for l-grams (exp_windows,
+// sequence.py:319-321; V = ~0 there)
+__device__ __forceinline__ u64 table_cap(u64 exp_len, u64 sub, u64 V) {
+  const u64 e = exp_len > sub ? exp_len - sub : 0;
+  return e < V ? e : V;
+}
+
+struct CappedBound {  // min(bound[c], cap(c))
   const u64* bound;
   const u64* exp_len;
-  u64 V;
+  u64 V, sub;
   __device__ __forceinline__ u64 operator()(u32 c, u32) const {
-    const u64 b = ldcg(bound + c), e = exp_len[c];
-    const u64 cap = e < V ? e : V;
+    const u64 b = ldcg(bound + c), cap = table_cap(exp_len[c], sub, V);
     return b < cap ? b : cap;
   }
 };
 
-__global__ void k_table_caps(const u64* bound, const u64* exp_len, u64 V, u64 R, u32* tcap, u64* tcap64) {
+__global__ void k_table_caps(const u64* bound, const u64* exp_len, u64 V, u64 sub, u64 R, u32* tcap, u64* tcap64) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
     u64 b = bound[r];
-    const u64 cap = exp_len[r] < V ? exp_len[r] : V;
+    const u64 cap = table_cap(exp_len[r], sub, V);
     if (b > cap) b = cap;
     u32 c = 0;
     if (b) {
@@ -129,14 +136,17 @@ __global__ void k_table_caps(const u64* bound, const u64* exp_len, u64 V, u64 R,
   }
 }
 
-// own words of every non-root rule
-__global__ void k_own_insert(const u32* ow_word, const u32* ow_rule, const u32* ow_freq, u64 n, u32* keys,
-                             u64* vals, const u64* toff, const u32* tcap, u32* full) {
+// own items of every non-root rule: (key, rule, freq) — the own words
+// (ow_word, ow_rule, ow_freq) or the attributed gram windows (run id, rule,
+// 1); rules >= rule_limit (root segments of the gram windows) are skipped
+__global__ void k_own_insert(const u32* ow_word, const u32* ow_rule, const u32* ow_freq, u64 n, u32 rule_limit,
+                             u32* keys, u64* vals, const u64* toff, const u32* tcap, u32* full) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
     const u64 i = base + threadIdx.x;
-    const bool a = i < n && ow_rule[i] != 0;
-    ht_add_warp(keys, vals, toff, tcap, a ? ow_rule[i] : 0, a ? ow_word[i] : 0, a ? ow_freq[i] : 0, a,
+    const u32 r = i < n ? ow_rule[i] : 0u;
+    const bool a = r != 0 && r < rule_limit;
+    ht_add_warp(keys, vals, toff, tcap, a ? r : 0, a ? ow_word[i] : 0, a ? (ow_freq ? ow_freq[i] : 1u) : 0, a,
                 full);
   }
 }
@@ -209,14 +219,14 @@ __global__ void k_file_bounds(const u32* rs_rule, const u32* rs_seg, u64 nrs, co
   }
 }
 
-__global__ void k_file_caps(const u64* fb, const u64* seg_tokens, u32 file_lo, u64 V, u32 nseg, u32* fcap,
+// per-file table caps: min(bound, tokens_f - sub, V)
+__global__ void k_file_caps(const u64* fb, const u64* seg_tokens, u32 file_lo, u64 V, u64 sub, u32 nseg, u32* fcap,
                             u64* fcap64) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 f = (u64)blockIdx.x * blockDim.x + threadIdx.x; f < nseg; f += stride) {
     u64 b = fb[f];
-    const u64 tk = seg_tokens[file_lo + f];
-    if (b > V) b = V;
-    if (b > tk) b = tk;
+    const u64 cap = table_cap(seg_tokens[file_lo + f], sub, V);
+    if (b > cap) b = cap;
     u32 c = 0;
     if (b) {
       c = 2;
@@ -268,6 +278,45 @@ __global__ void k_level2_files(const u32* rs_rule, const u32* rs_seg, const u32*
       }
     }
     ht_add_warp(fkeys, fvals, foff, fcap, f, w, v, a, full);
+  }
+}
+
+// l-gram windows (bottom-up gram strategy): own window count per rule
+// (own_candidates, sequence.py:319-321), root-segment windows per file (the
+// file-table bounds) and their inserts into the per-file tables
+__global__ void k_gram_counts(const u32* src, u64 n, u32 R, u64* own_c, u64* fb) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 s = src[i];
+    atomicAdd((unsigned long long*)(s < R ? own_c + s : fb + (s - R)), 1ull);
+  }
+}
+
+__global__ void k_file_root_grams(const u32* run, const u32* src, u64 n, u32 R, u32* keys, u64* vals,
+                                  const u64* foff, const u32* fcap, u32* full) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 base = (u64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const u64 i = base + threadIdx.x;
+    const u32 s = i < n ? src[i] : 0u;
+    const bool a = i < n && s >= R;
+    ht_add_warp(keys, vals, foff, fcap, a ? s - R : 0, a ? run[i] : 0, 1ull, a, full);
+  }
+}
+
+// (run << FB | file) keys of the occupied per-file slots
+__global__ void k_key_rf(const u32* file, const u32* run, u64 n, int FB, u64* key) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    key[i] = ((u64)run[i] << FB) | file[i];
+}
+
+__global__ void k_split_rf(const u64* key, const u32* idx, const u64* cnt, u64 n, int FB, u32* crun, u32* ccol,
+                           u64* ccnt) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    crun[i] = (u32)(key[i] >> FB);
+    ccol[i] = (u32)(key[i] & ((1ull << FB) - 1));
+    ccnt[i] = cnt[idx[i]];
   }
 }
 
@@ -366,20 +415,32 @@ struct RuleTables {
   u64 S = 0;
 };
 
-bool build_rule_tables(DeviceDag* d, RuleTables* T, u64 budget) {
+// the own items of a table arena (see k_own_insert)
+struct OwnItems {
+  const u32* key;
+  const u32* rule;
+  const u32* freq;  // nullable: 1 per item
+  u64 n;
+  u32 rule_limit;
+};
+
+// Per-rule tables built children-first (bottom_up_traverse, engine.py:409-446).
+// own_bound: u64[R] own table sizes (consumed as the bound array); V / sub:
+// the table caps (table_cap).  false = the arena would exceed `budget`.
+bool build_rule_tables(DeviceDag* d, RuleTables* T, u64 budget, const OwnItems& own, DBuf&& own_bound, u64 V,
+                       u64 sub) {
   cudaStream_t st = d->stream;
-  const u64 R = d->R, V = d->nw;
+  const u64 R = d->R;
   // bounds (local_table_bounds, engine.py:338-367)
-  T->bound.alloc(R * 8, st);
-  BK(k_own_distinct, R, d->own_off.as<u64>(), R, T->bound.as<u64>());
+  T->bound = std::move(own_bound);
   seg_reduce_levels<SumMode>("k_bu_bounds", d->be_rule.as<u32>(), d->be_child.as<u32>(), nullptr,
                              d->be_off_dev.as<u64>(), 0, d->td.nl, 1,
-                             CappedBound{T->bound.as<u64>(), d->exp_len.as<u64>(), V},
+                             CappedBound{T->bound.as<u64>(), d->exp_len.as<u64>(), V, sub},
                              OutRowMajor{T->bound.as<u64>(), 1}, st, true);
   // arena (plan_pool, engine.py:370-377)
   DBuf cap64(R * 8 + 8, st);
   T->tcap.alloc(R * 4, st);
-  BK(k_table_caps, R, T->bound.as<u64>(), d->exp_len.as<u64>(), V, R, T->tcap.as<u32>(), cap64.as<u64>());
+  BK(k_table_caps, R, T->bound.as<u64>(), d->exp_len.as<u64>(), V, sub, R, T->tcap.as<u32>(), cap64.as<u64>());
   GT_CUDA(cudaMemsetAsync(cap64.as<u64>() + R, 0, 8, st));
   T->toff.alloc((R + 1) * 8, st);
   exclusive_scan_u64(cap64.as<u64>(), T->toff.as<u64>(), R + 1, st);
@@ -391,10 +452,10 @@ bool build_rule_tables(DeviceDag* d, RuleTables* T, u64 budget) {
   GT_CUDA(cudaMemsetAsync(T->vals.p, 0, T->S * 8 + 8, st));
   DBuf full(4, st);
   GT_CUDA(cudaMemsetAsync(full.p, 0, 4, st));
-  // own words (own_insert_round, _kernels.py:219-233)
-  if (d->E_own)
-    BK(k_own_insert, d->E_own, d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(), d->E_own,
-       T->keys.as<u32>(), T->vals.as<u64>(), T->toff.as<u64>(), T->tcap.as<u32>(), full.as<u32>());
+  // own items (own_insert_round _kernels.py:219-233 / window_count_round :279-309)
+  if (own.n)
+    BK(k_own_insert, own.n, own.key, own.rule, own.freq, own.n, own.rule_limit, T->keys.as<u32>(),
+       T->vals.as<u64>(), T->toff.as<u64>(), T->tcap.as<u32>(), full.as<u32>());
   // children first: decreasing top-down level, root (level 0) excluded
   // (merge_round, _kernels.py:236-250)
   const u64 Eb = d->be_off.empty() ? 0 : d->be_off.back();
@@ -408,8 +469,18 @@ bool build_rule_tables(DeviceDag* d, RuleTables* T, u64 budget) {
         pos.as<u64>(), deg.as<u64>(), T->keys.as<u32>(), T->vals.as<u64>(), T->toff.as<u64>(),
         T->tcap.as<u32>(), full.as<u32>());
   }
-  if (rd1<u32>(full.p, st)) fail(GT_E_RESOURCE, "local word table full (bound violated)");
+  if (rd1<u32>(full.p, st)) fail(GT_E_RESOURCE, "local table full (bound violated)");
   return true;
+}
+
+// the word tables: own distinct words, caps min(exp_len, V)
+bool build_word_tables(DeviceDag* d, RuleTables* T, u64 budget) {
+  cudaStream_t st = d->stream;
+  DBuf own(d->R * 8, st);
+  BK(k_own_distinct, d->R, d->own_off.as<u64>(), d->R, own.as<u64>());
+  return build_rule_tables(d, T, budget, OwnItems{d->ow_word.as<u32>(), d->ow_rule.as<u32>(), d->ow_freq.as<u32>(),
+                                                  d->E_own, (u32)d->R},
+                           std::move(own), d->nw, 0);
 }
 
 __global__ void k_table_batch(const u32* keys_in, const u64* deltas, u64 n, u32* keys, u64* vals, const u64* toff,
@@ -465,7 +536,7 @@ bool bu_word_counts(DeviceDag* d, DBuf& counts, u64 budget) {
   cudaStream_t st = d->stream;
   const u64 R = d->R, V = d->nw;
   RuleTables T;
-  if (!build_rule_tables(d, &T, budget)) return false;
+  if (!build_word_tables(d, &T, budget)) return false;
   counts.alloc(V * 8 + 8, st);
   GT_CUDA(cudaMemsetAsync(counts.p, 0, V * 8 + 8, st));
   // root words of the owned segments (root_words_round) ...
@@ -485,7 +556,7 @@ bool bu_file_tables(DeviceDag* d, int task, DevRecords* Rr, u64 budget) {
   const u64 V = d->nw;
   const u32 file_lo = (u32)d->file_lo, nseg = (u32)(d->file_hi - d->file_lo);
   RuleTables T;
-  if (!build_rule_tables(d, &T, budget)) return false;
+  if (!build_word_tables(d, &T, budget)) return false;
   // per-file output tables appended to the plan (extra_bounds of plan_pool)
   DBuf fb((u64)nseg * 8 + 8, st), fcap((u64)nseg * 4 + 4, st), fcap64((u64)nseg * 8 + 8, st),
       foff((u64)nseg * 8 + 8, st);
@@ -493,7 +564,8 @@ bool bu_file_tables(DeviceDag* d, int task, DevRecords* Rr, u64 budget) {
   if (d->n_rs + d->n_rw)
     BK(k_file_bounds, d->n_rs + d->n_rw, d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->n_rs, d->rw_seg.as<u32>(),
        d->n_rw, file_lo, nseg, T.bound.as<u64>(), fb.as<u64>());
-  BK(k_file_caps, nseg, fb.as<u64>(), d->seg_tokens.as<u64>(), file_lo, V, nseg, fcap.as<u32>(), fcap64.as<u64>());
+  BK(k_file_caps, nseg, fb.as<u64>(), d->seg_tokens.as<u64>(), file_lo, V, 0ull, nseg, fcap.as<u32>(),
+     fcap64.as<u64>());
   GT_CUDA(cudaMemsetAsync(fcap64.as<u64>() + nseg, 0, 8, st));
   exclusive_scan_u64(fcap64.as<u64>(), foff.as<u64>(), (u64)nseg + 1, st);
   const u64 FS = rd1<u64>(foff.as<u64>() + nseg, st);
@@ -537,8 +609,11 @@ bool bu_file_tables(DeviceDag* d, int task, DevRecords* Rr, u64 budget) {
     DBuf f2(n * 4 + 4, st), c2(n * 8 + 8, st);
     BK(k_gather_u32, n, idx2.as<u32>(), n, file.as<u32>(), f2.as<u32>());
     BK(k_gather_u64b, n, idx2.as<u32>(), n, cnt.as<u64>(), c2.as<u64>());
-    const u64 W = d->W;
+    // count field sized by the largest file (a per-file count never exceeds
+    // its file's words), as sparse.cu; the key must hold file and count bits
+    const u64 W = d->max_file_tokens ? d->max_file_tokens : d->W;
     const int CB = std::max(1, bitlen(W));
+    if (CB + FB > 64) fail(GT_E_RESOURCE, "term-vector sort key of %d bits exceeds 64", CB + FB);
     BK(k_tv_key, n, f2.as<u32>(), c2.as<u64>(), n, W, CB, k1.as<u64>());
     sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), idx2.as<u32>(), idx.as<u32>(), n, CB + FB, st);
     Rr->n = n;
@@ -569,6 +644,84 @@ bool bu_file_tables(DeviceDag* d, int task, DevRecords* Rr, u64 budget) {
        Rr->group_off.as<u64>());
   }
   GT_CUDA(cudaStreamSynchronize(st));
+  return true;
+}
+
+// Bottom-up l-gram counting (count_sequences strategy="bottomup",
+// sequence.py:369-415): per-rule window tables sized by local_table_bounds
+// over the own window counts capped by exp_windows, filled with each rule's
+// attributed windows (keys = gram run ids of the sorted windows: packed or
+// gram-mode grams share one u32 key space) and merged children-first scaled
+// by body frequency; then the root: every file's segment windows plus
+// seg_count(c, f) x table(c) for the root's children (level 2) into per-file
+// tables.  Out: nonzero (run, file, count) cells in (run, file) order —
+// the input of seq.cu's render-order record assembly.  src: rule id (< R)
+// or R + owned segment per window occurrence; false = over budget.
+bool bu_seq_cells(DeviceDag* d, u32 l, const u32* run, const u32* src, u64 N, u64 nruns, DBuf& crun, DBuf& ccol,
+                  DBuf& ccnt, u64* n_out, u64 budget) {
+  cudaStream_t st = d->stream;
+  const u64 R = d->R, m = l - 1;
+  const u32 file_lo = (u32)d->file_lo, nseg = (u32)(d->file_hi - d->file_lo);
+  DBuf own(R * 8, st), fb((u64)nseg * 8 + 8, st);
+  GT_CUDA(cudaMemsetAsync(own.p, 0, R * 8, st));
+  GT_CUDA(cudaMemsetAsync(fb.p, 0, (u64)nseg * 8 + 8, st));
+  if (N) BK(k_gram_counts, N, src, N, (u32)R, own.as<u64>(), fb.as<u64>());
+  RuleTables T;
+  if (!build_rule_tables(d, &T, budget, OwnItems{run, src, nullptr, N, (u32)R}, std::move(own), ~0ull, m))
+    return false;
+  // per-file tables: bound = segment windows + the root references' bounds,
+  // cap = min(tokens_f - (l-1), distinct grams)
+  DBuf fcap((u64)nseg * 4 + 4, st), fcap64((u64)nseg * 8 + 8, st), foff((u64)nseg * 8 + 8, st);
+  if (d->n_rs)
+    BK(k_file_bounds, d->n_rs, d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->n_rs, (const u32*)nullptr, 0ull,
+       file_lo, nseg, T.bound.as<u64>(), fb.as<u64>());
+  BK(k_file_caps, nseg, fb.as<u64>(), d->seg_tokens.as<u64>(), file_lo, nruns, m, nseg, fcap.as<u32>(),
+     fcap64.as<u64>());
+  GT_CUDA(cudaMemsetAsync(fcap64.as<u64>() + nseg, 0, 8, st));
+  exclusive_scan_u64(fcap64.as<u64>(), foff.as<u64>(), (u64)nseg + 1, st);
+  const u64 FS = rd1<u64>(foff.as<u64>() + nseg, st);
+  if ((T.S + FS) * 12 > budget) return false;
+  DBuf fkeys(FS * 4 + 4, st), fvals(FS * 8 + 8, st), full(4, st);
+  GT_CUDA(cudaMemsetAsync(fkeys.p, 0xFF, FS * 4 + 4, st));
+  GT_CUDA(cudaMemsetAsync(fvals.p, 0, FS * 8 + 8, st));
+  GT_CUDA(cudaMemsetAsync(full.p, 0, 4, st));
+  if (N)  // _count_segments: the root segments' own windows
+    BK(k_file_root_grams, N, run, src, N, (u32)R, fkeys.as<u32>(), fvals.as<u64>(), foff.as<u64>(),
+       fcap.as<u32>(), full.as<u32>());
+  if (d->n_rs) {  // level 2: seg_count(c, f) x table(c) (merge_with_retries over the root's children)
+    DBuf deg(d->n_rs * 8 + 8, st), pos(d->n_rs * 8 + 8, st);
+    BK(k_rs_slots, d->n_rs, d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->n_rs, file_lo, nseg,
+       T.tcap.as<u32>(), deg.as<u64>());
+    exclusive_scan_u64(deg.as<u64>(), pos.as<u64>(), d->n_rs, st);
+    BKE(k_level2_files, d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, file_lo,
+        pos.as<u64>(), deg.as<u64>(), T.keys.as<u32>(), T.vals.as<u64>(), T.toff.as<u64>(), fkeys.as<u32>(),
+        fvals.as<u64>(), foff.as<u64>(), fcap.as<u32>(), full.as<u32>());
+  }
+  if (rd1<u32>(full.p, st)) fail(GT_E_RESOURCE, "per-file gram table full (bound violated)");
+  T = RuleTables();
+  // occupied slots -> (file, run, count) -> (run, file) order
+  DBuf occ(FS + 1, st), sel(FS * 4 + 4, st), nsel(8, st);
+  BK(k_occupied, FS, fkeys.as<u32>(), FS, occ.as<uint8_t>());
+  select_flagged_index(occ.as<uint8_t>(), sel.as<u32>(), nsel.as<u64>(), FS, st);
+  const u64 n = rd1<u64>(nsel.p, st);
+  DBuf file(n * 4 + 4, st), key(n * 4 + 4, st), cnt(n * 8 + 8, st);
+  BK(k_slot_records, n, sel.as<u32>(), nsel.as<u64>(), fkeys.as<u32>(), fvals.as<u64>(), foff.as<u64>(), nseg,
+     file.as<u32>(), key.as<u32>(), cnt.as<u64>());
+  fkeys.release();
+  fvals.release();
+  const int FB = std::max(1, bitlen(nseg ? nseg - 1 : 0));
+  const int KB = std::max(1, bitlen(nruns ? nruns - 1 : 0));
+  if (KB + FB > 64) fail(GT_E_RESOURCE, "gram x file key of %d bits exceeds 64", KB + FB);
+  DBuf k1(n * 8 + 8, st), k2(n * 8 + 8, st), idx(n * 4 + 4, st), idx2(n * 4 + 4, st);
+  BK(k_iota_u32, n, idx.as<u32>(), n);
+  BK(k_key_rf, n, file.as<u32>(), key.as<u32>(), n, FB, k1.as<u64>());
+  sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), idx.as<u32>(), idx2.as<u32>(), n, KB + FB, st);
+  crun.alloc(n * 4 + 4, st);
+  ccol.alloc(n * 4 + 4, st);
+  ccnt.alloc(n * 8 + 8, st);
+  BK(k_split_rf, n, k2.as<u64>(), idx2.as<u32>(), cnt.as<u64>(), n, FB, crun.as<u32>(), ccol.as<u32>(),
+     ccnt.as<u64>());
+  *n_out = n;
   return true;
 }
 

@@ -1162,6 +1162,12 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   parse_dict(blob, nbytes, &P);
   ph.mark("host parse: dictionary");
   const u64 nsec = (nbytes - P.rules_pos) / 4;
+  // device ids and body offsets of the rule-chain parse and the CSR build are
+  // u32: a rules section of 2^32 - 1 or more words cannot be represented
+  // (fail loudly instead of truncating rule starts)
+  if (nsec >= 0xFFFFFFFFull)
+    fail(GT_E_RESOURCE, "grammar too large: rules section of %lu words exceeds the 2^32 - 2 word limit",
+         (unsigned long)nsec);
   DBuf raw(nsec * 4 + 4, st);
   if (nsec) GT_CUDA(cudaMemcpyAsync(raw.p, dblob.as<uint8_t>() + P.rules_pos, nsec * 4, cudaMemcpyDeviceToDevice, st));
   dblob.release();

@@ -24,6 +24,7 @@
 
 #include "kernels_common.cuh"
 #include "segreduce.cuh"
+#include "bottomup.cuh"
 #include "seq.cuh"
 #include "sparse.cuh"
 
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(1024) k_head_tail_levels(const u32* __restrict
 struct WinCtx {
   const u32* body;
   const u32* owner;
-  const u32* tid;  // rule -> tid (the weight rows' numbering)
+  const u32* tid;  // rule -> tid (the weight rows' numbering); nullptr: rule ids
   const u64* boff;
   const u32* root_seg;
   const u32 *H, *T, *hl, *tl;
@@ -109,7 +110,7 @@ __device__ __forceinline__ u32 windows_at(const WinCtx& c, u64 p, u32* src, u32*
     if (sg >= c.nseg) return 0;
     *src = c.R + sg;
   } else {
-    *src = c.tid[r];
+    *src = c.tid ? c.tid[r] : r;  // weight-row numbering (top-down) or rule id (bottom-up tables)
   }
   const u32 s = c.body[p];
   u32 tlen;
@@ -384,6 +385,14 @@ __global__ void k_group_out(const u32* gsel, const u64* ng_p, const u32* rec, co
   }
 }
 
+// window sources from rule ids to weight-row ids (tid) after a bottom-up
+// attempt fell back to the top-down path
+__global__ void k_src_tid(u32* src, u64 n, const u32* tid, u32 R) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    if (src[i] < R) src[i] = tid[src[i]];
+}
+
 #define SL(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
 
 template <class T>
@@ -396,7 +405,7 @@ static T d2h1(const void* p, cudaStream_t st) {
 
 }  // namespace
 
-void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, int* wbits_out) {
+int run_sequences(DeviceDag* d, int task, int l_, int mode, DevRecords* Rr, int* wbits_out) {
   cudaStream_t st = d->stream;
   Phases ph("seq", st);
   const u32 l = (u32)l_, m = l - 1;
@@ -438,21 +447,27 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   }
   ph.mark("heads/tails");
   // per-file rule weights: dense top-down rows (F columns) or, for many
-  // files, the presence-guided sparse (rule, file) weights (sparse.cu)
+  // files, the presence-guided sparse (rule, file) weights (sparse.cu);
+  // none for the bottom-up tables
+  bool bottomup = mode == GT_BOTTOMUP;
+  bool sparse = mode == GT_TOPDOWN_SPARSE;
   DBuf w;
   bool w32 = false;
   SparseW sw;
-  if (sparse) {
-    u32 FW;
-    sparse_file_weights(d, &sw, nullptr, &FW);
-  } else {
-    u32 Cw;
-    td_file_weights(d, w, &Cw, &w32);
-  }
-
+  auto weights = [&] {
+    if (sparse) {
+      u32 FW;
+      sparse_file_weights(d, &sw, nullptr, &FW);
+    } else {
+      u32 Cw;
+      td_file_weights(d, w, &Cw, &w32);
+    }
+  };
+  if (!bottomup) weights();
   ph.mark("weights");
   // phase 2: windows attributed per body position (two passes + scan)
-  WinCtx c{d->body.as<u32>(), d->pos_owner.as<u32>(), d->tid.as<u32>(), d->boff.as<u64>(), d->root_seg.as<u32>(),
+  WinCtx c{d->body.as<u32>(), d->pos_owner.as<u32>(), bottomup ? nullptr : d->tid.as<u32>(), d->boff.as<u64>(),
+           d->root_seg.as<u32>(),
            H.as<u32>(), T.as<u32>(), hl.as<u32>(), tl.as<u32>(), nw, base, l, m, (u32)wbits,
            (u32)R, (u32)d->file_lo, Fo};
   DBuf cnt(E * 8 + 8, st), off(E * 8 + 8, st);
@@ -507,7 +522,17 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   // nonzero (run, file) cells in (gram asc, file asc) order
   DBuf crun, ccol, ccnt;
   u64 n = 0;
-  if (sparse) {
+  if (bottomup && !bu_seq_cells(d, l, rid.as<u32>(), ssrc.as<u32>(), nruns ? N : 0, nruns, crun, ccol, ccnt, &n,
+                                scratch_budget(d))) {
+    // the table arena exceeds the memory budget: the top-down sparse path
+    bottomup = false;
+    sparse = true;
+    SL(k_src_tid, N, ssrc.as<u32>(), N, d->tid.as<u32>(), (u32)R);
+    weights();
+  }
+  if (bottomup) {
+    // cells come from the tables
+  } else if (sparse) {
     const int FB = std::max(1, bitlen(C - 1));
     DBuf ckey;
     n = sparse_run_cells(d, sw, rid.as<u32>(), ssrc.as<u32>(), nruns ? N : 0, FB, ckey, ccnt);
@@ -658,6 +683,7 @@ void run_sequences(DeviceDag* d, int task, int l_, bool sparse, DevRecords* Rr, 
   }
   GT_CUDA(cudaStreamSynchronize(st));
   ph.mark("records");
+  return bottomup ? GT_BOTTOMUP : (sparse ? GT_TOPDOWN_SPARSE : GT_TOPDOWN);
 }
 
 }  // namespace gt

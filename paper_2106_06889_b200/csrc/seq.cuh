@@ -3,5 +3,9 @@
 #include "word.cuh"
 
 namespace gt {
-void run_sequences(DeviceDag* d, int task, int seq_len, bool sparse, DevRecords* R, int* wbits_out);
+// mode: GT_TOPDOWN (dense per-file weights), GT_TOPDOWN_SPARSE (presence-
+// guided sparse weights) or GT_BOTTOMUP (pooled per-rule window tables,
+// bottomup.cu; top-down sparse when over the memory budget).  Returns the
+// strategy that ran.
+int run_sequences(DeviceDag* d, int task, int seq_len, int mode, DevRecords* R, int* wbits_out);
 }

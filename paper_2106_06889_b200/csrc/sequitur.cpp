@@ -26,6 +26,7 @@
 #include <string>
 #include <string_view>
 #include <unordered_map>
+#include <stdexcept>
 #include <vector>
 
 #include "../../include/gtadoc_b200.h"
@@ -127,6 +128,9 @@ struct Builder {
   }
 
   uint32_t make(int32_t sym, int32_t rule_id = -1) {
+    // node ids are u32 with NIL = 2^32 - 1; dead nodes are not reused, so a
+    // corpus of ~10^9+ tokens could run out of ids: fail, never wrap
+    if (nodes.size() >= (size_t)NIL - 1) throw std::length_error("grammar node pool exceeds 2^32 - 2 nodes");
     nodes.push_back(Node{sym, rule_id, NIL, NIL, NIL, NIL, false, false});
     return (uint32_t)nodes.size() - 1;
   }
@@ -394,12 +398,24 @@ int gt_compress(const uint8_t* const* files, const uint64_t* lens, uint64_t nfil
     }
     stream.push_back(-1);
   }
+  if ((uint64_t)words.size() + nfiles >= (1ull << 31)) {
+    t_seq_err = "vocabulary + files exceed the 2^31 symbol ids of the compressor";
+    return GT_E_RESOURCE;
+  }
   const int32_t nw = (int32_t)words.size();
   for (uint64_t i = 0, f = 0; i < stream.size(); i++)
     if (stream[i] < 0) stream[i] = nw + (int32_t)(f++);
   // grammar inference
   Builder b;
-  for (int32_t s : stream) b.append(s);
+  try {
+    for (int32_t s : stream) b.append(s);
+  } catch (const std::length_error& e) {
+    t_seq_err = e.what();
+    return GT_E_RESOURCE;
+  } catch (const std::bad_alloc&) {
+    t_seq_err = "out of host memory";
+    return GT_E_RESOURCE;
+  }
   // finalize: live rules in id order, compacted
   std::vector<int32_t> compact(b.guard.size(), -1);
   std::vector<int32_t> live;

@@ -231,7 +231,9 @@ static void td_words_fused(const DeviceDag* d, u64* row, u64* out, bool per_file
 // small grammars, one launch per task: top-down pass + word reduce + root
 // words + the render-order compaction (word count records / inverted-index
 // groups); false when the grammar takes the multi-launch path
-static bool small_task(const DeviceDag* d) { return d->E_own <= kFusedReduceMax && d->nw < (1ull << 32); }
+// (the fused compaction's block scans count records in u32 and its packed
+// offsets must stay below 2^32: V * 64 records at most)
+static bool small_task(const DeviceDag* d) { return d->E_own <= kFusedReduceMax && d->nw * 64 < (1ull << 32); }
 
 bool td_word_records(DeviceDag* d, DevRecords* R) {
   if (!small_task(d)) return false;
@@ -501,7 +503,10 @@ void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_
 void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R) {
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
-  if (FW == 1 && V < (1ull << 32)) {
+  // the packed (has-files << 32 | popcount) scan needs every record offset
+  // below 2^32: at most min(Fo, 64) records per word
+  const u64 Fo = d->file_hi - d->file_lo;
+  if (FW == 1 && V * std::min<u64>(std::max<u64>(Fo, 1), 64) < (1ull << 32)) {
     DBuf key((V + 1) * 8, st), pref((V + 1) * 8, st);
     KL(k_ii_keys, grid_for(V + 1, 256), pres, V, key.as<u64>());
     exclusive_scan_u64(key.as<u64>(), pref.as<u64>(), V + 1, st);

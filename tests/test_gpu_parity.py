@@ -58,8 +58,8 @@ def test_composed_all_tasks_match_oracle(name, scale, seed):
                 got = gt.run_compact(dag, task, cfg, l)
                 exp = gt.run_compact(ref, task, gt.TraversalConfig(strategy="topdown"), l)
                 assert_same(got, exp, (name, scale, task, l, strategy))
-                if strategy == "bottomup" and task in ("wordcount", "sort", "invertedindex", "termvector"):
-                    assert got.strategy == "bottomup"  # the pooled hash-table path ran
+                if strategy == "bottomup":
+                    assert got.strategy == "bottomup"  # the pooled hash-table path ran (words and grams)
     dag.close()
 
 
@@ -163,9 +163,13 @@ def test_c2_full_sequence_tasks_match_oracle():
     dag = gt.DeviceDag(blob)
     ref = OracleDag(blob)
     for task in ("seqcount", "rankedinvertedindex"):
-        got = gt.run_compact(dag, task, gt.TraversalConfig(), 3)
         exp = gt.run_compact(ref, task, gt.TraversalConfig(), 3)
+        got = gt.run_compact(dag, task, gt.TraversalConfig(), 3)
         assert_same(got, exp, task)
+        # Alg. 2 for grams: pooled per-rule window tables (sequence.py:369-415)
+        got = gt.run_compact(dag, task, gt.TraversalConfig(strategy="bottomup"), 3)
+        assert got.strategy == "bottomup"
+        assert_same(got, exp, (task, "bottomup"))
     dag.close()
 
 
