@@ -659,7 +659,29 @@ struct KahnCtl {
   u64 ntask[2];  // heavy-task counts, layer L uses ntask[L & 1]
   u64 processed;
   u64 layers;
+  u64 t[64];     // %globaltimer at the start of layers 1..63 (GT_TRACE=2 prints them)
+  u64 bar;       // k_kahn3's layer barrier: arrivals (bits 0-31), active blocks of even / odd layers (32-47 / 48-63)
 };
+
+__device__ __forceinline__ u64 globaltimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Sum of a per-thread count into *dst with ONE atomic per block (every
+// thread of a full grid adding to one address serialises ~10^5 atomics in
+// one L2 slice: ~65 us at 148 x 1024 threads).  Called by every thread.
+__device__ __forceinline__ void block_add_u64(u64 v, u64* dst) {
+  __shared__ unsigned long long s_sum;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+  if (threadIdx.x == 0) s_sum = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31u) == 0 && v) atomicAdd(&s_sum, (unsigned long long)v);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_sum) atomicAdd((unsigned long long*)dst, s_sum);
+}
 
 __device__ __forceinline__ u64 ld_cg64(const u64* p) {
   return (u64)__ldcg(reinterpret_cast<const unsigned long long*>(p));
@@ -802,8 +824,446 @@ __global__ void __launch_bounds__(kKahnBlock) k_kahn(KahnCtl* ctl, u32* bm0, u32
     }
     grid.sync();
   }
-  if (found) atomicAdd((unsigned long long*)&ctl->processed, (unsigned long long)found);
+  block_add_u64(found, &ctl->processed);
   if (gtid == 0) ctl->layers = L - 1;
+}
+
+// ---------------------------------------------------------------------------
+// Batched Kahn layering (the default): same layers, reachability and heavy-
+// rule chunk tasks as k_kahn, but every warp owns ONE contiguous range of
+// bitmap words for all layers and runs each layer as four memory waves with
+// every load of a wave in flight at once:
+//   bitmap words (4 per lane) -> the frontier rules' CSR bounds and reach
+//   (8 rules per lane, staged in shared memory) -> the child ids (4 edges per
+//   lane, owner found by a binary search over the staged edge prefix) -> the
+//   warp-aggregated counter decrements (4 atomics per lane in flight).
+// k_kahn issues the same accesses as dependent chains (one rule / one edge
+// per lane per round trip): ncu on C5 showed 33 % of its stall samples on
+// the atomic results and 21 % on the offset and id loads.
+// ---------------------------------------------------------------------------
+constexpr int kK2Words = 4;            // bitmap words per lane per batch
+constexpr u32 kK2Cap = 128;            // frontier rules staged per warp per round
+constexpr int kK2PerLane = kK2Cap / 32;
+constexpr int kK2Edges = 4;            // child edges per lane in flight
+constexpr size_t kK2SmemPerWarp = kK2Cap * 8 + (kK2Cap + 1) * 4 + kK2Cap * 4 + kK2Cap;
+constexpr size_t kK2Smem = 32 * ((kK2SmemPerWarp + 15) / 16 * 16);
+
+__global__ void __launch_bounds__(kKahnBlock) k_kahn2(KahnCtl* ctl, u32* bm0, u32* bm1, u64 nwords,
+                                                      const u64* __restrict__ off, const u32* __restrict__ ids,
+                                                      u32* rem, u32* lvl, uint8_t* reach, uint2* tasks,
+                                                      u64 max_layers) {
+  extern __shared__ __align__(16) unsigned char k2_smem[];
+  cg::grid_group grid = cg::this_grid();
+  const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  unsigned char* base = k2_smem + (size_t)wib * ((kK2SmemPerWarp + 15) / 16 * 16);
+  u64* s_e0 = reinterpret_cast<u64*>(base);
+  u32* s_pre = reinterpret_cast<u32*>(base + kK2Cap * 8);
+  u32* s_rule = reinterpret_cast<u32*>(base + kK2Cap * 8 + (kK2Cap + 1) * 4);
+  uint8_t* s_rc = base + kK2Cap * 8 + (kK2Cap + 1) * 4 + kK2Cap * 4;
+  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 warp = gtid >> 5, nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u64 M = (nwords + nwarps - 1) / nwarps;
+  const u64 wlo = min(warp * M, nwords), whi = min(wlo + M, nwords);
+  const volatile uint8_t* rv = reach;
+  u64 found = 0, L = 1;
+  for (;; L++) {
+    if (__ldcg(&ctl->any[L % 3]) == 0 || L > max_layers) break;
+    if (gtid == 0) {
+      ctl->any[(L + 2) % 3] = 0;
+      ctl->ntask[(L + 1) & 1] = 0;
+      if (L < 64) ctl->t[L] = globaltimer();
+    }
+    u32* cur = (L & 1) ? bm1 : bm0;
+    u32* nxt = (L & 1) ? bm0 : bm1;
+    u64* ntask = &ctl->ntask[L & 1];
+    bool set_any = false;
+    for (u64 b0 = wlo; b0 < whi; b0 += 32 * kK2Words) {
+      u32 bits[kK2Words];
+      u32 cnt = 0;
+#pragma unroll
+      for (int k = 0; k < kK2Words; k++) {
+        const u64 wi = b0 + (u64)k * 32 + lane;
+        bits[k] = wi < whi ? __ldcg(cur + wi) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kK2Words; k++) {
+        if (bits[k]) cur[b0 + (u64)k * 32 + lane] = 0;  // cleared for layer L + 2
+        cnt += __popc(bits[k]);
+      }
+      u32 incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= (unsigned)d) incl += t;
+      }
+      const u32 T = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const u32 excl = incl - cnt;
+      found += cnt;
+      for (u32 q0 = 0; q0 < T; q0 += kK2Cap) {
+        const u32 n = min(T - q0, kK2Cap);
+        // stage this round's frontier rules (ascending rule order)
+        __syncwarp();
+        if (excl < q0 + kK2Cap && excl + cnt > q0) {
+          u32 q = excl;
+#pragma unroll
+          for (int k = 0; k < kK2Words; k++) {
+            u32 b = bits[k];
+            while (b && q < q0 + kK2Cap) {
+              const u32 bp = __ffs(b) - 1;
+              b &= b - 1;
+              if (q >= q0) s_rule[q - q0] = (u32)((b0 + (u64)k * 32 + lane) * 32 + bp);
+              q++;
+            }
+          }
+        }
+        __syncwarp();
+        // wave 2: CSR bounds and reach of the staged rules (contiguous 8 per lane)
+        u64 e0v[kK2PerLane], e1v[kK2PerLane];
+        uint8_t rcv[kK2PerLane];
+#pragma unroll
+        for (int j = 0; j < kK2PerLane; j++) {
+          const u32 i = lane * kK2PerLane + j;
+          e0v[j] = e1v[j] = 0;
+          rcv[j] = 0;
+          if (i < n) {
+            const u32 r = s_rule[i];
+            e0v[j] = off[r];
+            e1v[j] = off[r + 1];
+            rcv[j] = rv[r];
+            lvl[r] = (u32)L;
+          }
+        }
+        u32 lsum = 0;
+#pragma unroll
+        for (int j = 0; j < kK2PerLane; j++) {
+          const u32 i = lane * kK2PerLane + j;
+          u64 len = e1v[j] - e0v[j];
+          if (i < n && len > kLight) {  // heavy rule: chunk tasks for phase B
+            const u32 r = s_rule[i];
+            const u64 nch = (len + kChunk - 1) / kChunk;
+            const u64 t0 = atomicAdd((unsigned long long*)ntask, (unsigned long long)nch);
+            for (u64 k = 0; k < nch; k++) tasks[t0 + k] = make_uint2(r, (u32)(k * kChunk));
+            len = 0;
+          }
+          if (i < n) {
+            s_e0[i] = e0v[j];
+            s_rc[i] = rcv[j];
+            s_pre[i] = lsum;  // in-lane prefix, the lane's base added below
+          }
+          lsum += (u32)len;
+        }
+        u32 linc = lsum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const u32 t = __shfl_up_sync(0xFFFFFFFFu, linc, d);
+          if (lane >= (unsigned)d) linc += t;
+        }
+        const u32 NE = __shfl_sync(0xFFFFFFFFu, linc, 31);
+        const u32 lbase = linc - lsum;
+#pragma unroll
+        for (int j = 0; j < kK2PerLane; j++) {
+          const u32 i = lane * kK2PerLane + j;
+          if (i < n) s_pre[i] += lbase;
+        }
+        if (lane == 0) s_pre[n] = NE;
+        __syncwarp();
+        // waves 3 + 4: child ids, then the decrements, kK2Edges per lane in flight
+        for (u32 k0 = 0; k0 < NE; k0 += 32 * kK2Edges) {
+          u32 c[kK2Edges];
+          bool act[kK2Edges], rch[kK2Edges];
+#pragma unroll
+          for (int j = 0; j < kK2Edges; j++) {
+            const u32 qe = k0 + (u32)j * 32 + lane;
+            act[j] = qe < NE;
+            c[j] = 0;
+            rch[j] = false;
+            if (act[j]) {
+              u32 lo = 0, hi = n;  // s_pre[lo] <= qe < s_pre[hi]
+              while (hi - lo > 1) {
+                const u32 mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= qe) lo = mid;
+                else hi = mid;
+              }
+              c[j] = ids[s_e0[lo] + (qe - s_pre[lo])];
+              rch[j] = s_rc[lo] != 0;
+            }
+          }
+          u32 old[kK2Edges], kk[kK2Edges];
+#pragma unroll
+          for (int j = 0; j < kK2Edges; j++) {
+            if (act[j] && rch[j]) reach[c[j]] = 1;
+            const unsigned am = __ballot_sync(0xFFFFFFFFu, act[j]);
+            kk[j] = 0;
+            old[j] = 1;
+            if (act[j]) {
+              const unsigned peers = __match_any_sync(am, c[j]);
+              if ((int)lane == __ffs(peers) - 1) {
+                kk[j] = (u32)__popc(peers);
+                old[j] = atomicSub(&rem[c[j]], kk[j]);
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < kK2Edges; j++)
+            if (kk[j] && old[j] == kk[j]) {
+              atomicOr(&nxt[c[j] >> 5], 1u << (c[j] & 31u));
+              set_any = true;
+            }
+        }
+      }
+    }
+    if (__any_sync(0xFFFFFFFFu, set_any) && lane == 0) ctl->any[(L + 1) % 3] = 1;
+    grid.sync();
+    // phase B: heavy-rule chunk tasks, one warp per task
+    const u64 nt = ld_cg64(ntask);
+    if (nt == 0) continue;
+    u32* any_next = &ctl->any[(L + 1) % 3];
+    for (u64 t = warp; t < nt; t += nwarps) {
+      const uint2 tk = __ldcg(tasks + t);
+      const bool trc = rv[tk.x] != 0;
+      const u64 a = off[tk.x] + tk.y, b = min(off[tk.x + 1], a + kChunk);
+      for (u64 e = a; e < b; e += 32) {
+        const bool act = e + lane < b;
+        const u32 c = act ? ids[e + lane] : 0u;
+        kahn_edge(c, act, trc, rem, reach, nxt, any_next);
+      }
+    }
+    grid.sync();
+  }
+  block_add_u64(found, &ctl->processed);
+  if (gtid == 0) {
+    ctl->layers = L - 1;
+    if (L < 64) ctl->t[L] = globaltimer();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Owner-scan Kahn layering for grammars whose sub CSR fits in shared memory
+// (C1-C3): every warp owns a fixed range of rules for all layers and keeps
+// that range's child lists AND its rules' remaining-parent counts in shared
+// memory.  Decrements never touch those counts directly: a parent processed
+// in layer L adds (fire-and-forget, warp-aggregated RED) to delta[L & 1] of
+// the child; at the start of layer L + 1 the owner reads delta[L & 1] for
+// its range (one coalesced wave, together with the reach bytes and the
+// previous layer's activity flag), subtracts, clears it for layer L + 2 and
+// finds its ready rules (count zero).  So a layer is: one load wave, the
+// ready rules' REDs and reach pushes straight from shared memory, one grid
+// barrier — no frontier bitmap, no atomic with return (k_kahn/k_kahn2 wait on
+// atomic results, and same-address atomics on Zipf-popular children
+// serialise).  Decrements of layer L are invisible to layer L's readiness by
+// construction (they land in the other delta array).  The layering ends one
+// (empty) layer after the last non-empty one.  Same layers, reachability and
+// processed count as k_kahn / k_kahn2.
+// ---------------------------------------------------------------------------
+constexpr u32 kK3WarpWords = 1536;  // per-warp shared memory (u32 words)
+constexpr int kK3Batch = 8;         // delta words loaded per lane per wave
+constexpr u32 kK3List = 32 * kK3Batch;
+constexpr u32 kK3Done = 0xFFFFFFFFu;
+
+__global__ void __launch_bounds__(kKahnBlock) k_kahn3(KahnCtl* ctl, const u64* __restrict__ off,
+                                                      const u32* __restrict__ ids, u64 R, u32* rem, u32* delta1,
+                                                      u32* gdelta0, u32* lvl, uint8_t* reach, u64 max_layers) {
+  extern __shared__ __align__(16) u32 k3_smem[];
+  __shared__ u32 s_go, s_prev[2];
+  cg::grid_group grid = cg::this_grid();
+  const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  u32* sw = k3_smem + (size_t)wib * kK3WarpWords;
+  const u64 gtid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 warp = gtid >> 5, nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u64 nwords = (R + 31) / 32;
+  const u64 M = (nwords + nwarps - 1) / nwarps;
+  const u64 wlo = min(warp * M, nwords), whi = min(wlo + M, nwords);
+  const u64 m = whi - wlo, r0 = wlo * 32, r1 = min(whi * 32, R);
+  const u64 nr = r1 > r0 ? r1 - r0 : 0;
+  const u64 eb = nr ? off[r0] : 0, ee = nr ? off[r1] : 0;
+  u32* s_list = sw;                 // this batch's ready rules: slot | reach << 31
+  u32* s_cnt = sw + kK3List;        // nr remaining-parent counts (kK3Done once layered)
+  u32* s_off = s_cnt + nr;          // nr + 1 offsets relative to eb
+  u32* s_ids = s_off + nr + 1;
+  // global-count mode (gdelta0 given: the grammar is too large for shared
+  // memory): the counts stay in rem, both delta arrays come zeroed
+  const bool gmode = gdelta0 != nullptr;
+  const bool resident = !gmode && kK3List + 2 * nr + 1 + (ee - eb) <= kK3WarpWords;
+  u32* cnt = gmode ? rem + r0 : s_cnt;
+  u32* delta[2] = {gmode ? gdelta0 : rem, delta1};  // smem mode: rem doubles as delta[0]
+  if (gtid == 0) ctl->t[0] = globaltimer();
+  // prologue: 8 loads per lane in flight per step (the copies are tiny but
+  // each dependent load -> store step costs a full L2 round trip)
+  const u32 nr32 = (u32)nr, ne32 = (u32)(ee - eb);
+  if (gmode && gtid == 0) rem[0] = kK3Done;  // the root is layer 0
+  for (u32 i0 = 0; !gmode && i0 < nr32; i0 += 256) {
+    u32 t[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const u32 i = i0 + k * 32 + lane;
+      t[k] = i < nr32 ? __ldcg(rem + r0 + i) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const u32 i = i0 + k * 32 + lane;
+      if (i < nr32) {
+        s_cnt[i] = r0 + i == 0 ? kK3Done : t[k];  // the root is layer 0
+        rem[r0 + i] = 0;
+        delta1[r0 + i] = 0;
+      }
+    }
+  }
+  if (resident) {
+    for (u32 i0 = 0; i0 <= nr32; i0 += 256) {
+      u64 t[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const u32 i = i0 + k * 32 + lane;
+        t[k] = i <= nr32 ? off[r0 + i] : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const u32 i = i0 + k * 32 + lane;
+        if (i <= nr32) s_off[i] = (u32)(t[k] - eb);
+      }
+    }
+    for (u32 i0 = 0; i0 < ne32; i0 += 256) {
+      u32 t[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const u32 i = i0 + k * 32 + lane;
+        t[k] = i < ne32 ? ids[eb + i] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const u32 i = i0 + k * 32 + lane;
+        if (i < ne32) s_ids[i] = t[k];
+      }
+    }
+  }
+  if (threadIdx.x == 0) s_prev[0] = s_prev[1] = 0;
+  grid.sync();
+  const volatile uint8_t* rv = reach;
+  u64 found = 0, L = 1;
+  for (;; L++) {
+    u32* din = delta[(L - 1) & 1];  // decrements made in layer L - 1
+    u32* dout = delta[L & 1];
+    const volatile uint8_t* rvw = rv + r0;
+    u32 v[kK3Batch], rcb = 0;
+#pragma unroll
+    for (int k = 0; k < kK3Batch; k++) {
+      const u32 slot = k * 32 + lane;
+      const bool ok = slot < nr32;
+      v[k] = ok && L > 1 ? __ldcg(din + r0 + slot) : 0u;
+      rcb |= (ok && rvw[slot]) ? 1u << k : 0u;
+    }
+    if (L > 1 && s_go == 0) break;  // layer L - 1 was empty (s_go set by the barrier below)
+    if (L > max_layers) break;
+    if (gtid == 0 && L < 64) ctl->t[L] = globaltimer();
+    bool active = false;
+    for (u64 i0 = 0; i0 < m; i0 += kK3Batch) {
+      if (i0) {
+        rcb = 0;
+#pragma unroll
+        for (int k = 0; k < kK3Batch; k++) {
+          const u32 slot = (u32)i0 * 32 + k * 32 + lane;
+          const bool ok = slot < nr32;
+          v[k] = ok && L > 1 ? __ldcg(din + r0 + slot) : 0u;
+          rcb |= (ok && rvw[slot]) ? 1u << k : 0u;
+        }
+      }
+      // counters -> ready rules, compacted into the warp's list
+      u32 nready = 0;
+      u32* dinw = din + r0;
+#pragma unroll
+      for (int k = 0; k < kK3Batch; k++) {
+        if ((u32)i0 + k >= (u32)m) break;
+        const u32 slot = (u32)i0 * 32 + k * 32 + lane;
+        bool ready = false;
+        if (slot < nr32 && (!gmode || L == 1 || v[k])) {
+          u32 c = gmode ? __ldcg(cnt + slot) : cnt[slot];
+          if (v[k]) {
+            dinw[slot] = 0;  // cleared for layer L + 1's decrements
+            c -= v[k];
+          }
+          ready = c == 0;
+          if (ready) c = kK3Done;
+          if (v[k] || ready) cnt[slot] = c;
+        }
+        const unsigned mask = __ballot_sync(0xFFFFFFFFu, ready);
+        if (ready) s_list[nready + __popc(mask & lt_mask)] = slot | (((rcb >> k) & 1u) << 31);
+        nready += __popc(mask);
+      }
+      if (!nready) continue;
+      active = true;
+      __syncwarp();
+      // the ready rules, one per lane: each walks its own children (fire-
+      // and-forget REDs; most rules have < 8 children)
+      for (u32 q0 = 0; q0 < nready; q0 += 32) {
+        const bool act = q0 + lane < nready;
+        u32 slot = 0, rc = 0, e0 = 0, deg = 0;
+        u64 g0 = 0;
+        if (act) {
+          const u32 e = s_list[q0 + lane];
+          slot = e & 0x7FFFFFFFu;
+          rc = e >> 31;
+          const u64 r = r0 + slot;
+          lvl[r] = (u32)L;
+          found++;
+          if (resident) {
+            e0 = s_off[slot];
+            deg = s_off[slot + 1] - e0;
+          } else {
+            g0 = off[r];
+            deg = (u32)(off[r + 1] - g0);
+          }
+        }
+        const bool light = act && deg <= 32;
+        for (u32 j = 0;; j++) {
+          const bool go = light && j < deg;
+          if (!__any_sync(0xFFFFFFFFu, go)) break;
+          if (go) {
+            const u32 c = resident ? s_ids[e0 + j] : ids[g0 + j];
+            if (rc) reach[c] = 1;
+            atomicAdd(&dout[c], 1u);
+          }
+        }
+        // heavy rules (> 32 children): the whole warp walks each one
+        unsigned hm = __ballot_sync(0xFFFFFFFFu, act && deg > 32);
+        while (hm) {
+          const int src = __ffs(hm) - 1;
+          hm &= hm - 1;
+          const u32 he0 = __shfl_sync(0xFFFFFFFFu, e0, src), hdeg = __shfl_sync(0xFFFFFFFFu, deg, src);
+          const u64 hg0 = __shfl_sync(0xFFFFFFFFu, g0, src);
+          const u32 hrc = __shfl_sync(0xFFFFFFFFu, rc, src);
+          for (u32 q = lane; q < hdeg; q += 32) {
+            const u32 c = resident ? s_ids[he0 + q] : ids[hg0 + q];
+            if (hrc) reach[c] = 1;
+            atomicAdd(&dout[c], 1u);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // layer barrier carrying the layer's activity: one release-add per
+    // block of (1 arrival + the block's activity in this layer's parity
+    // field), thread 0 spins until every block arrived, and the field's
+    // growth since the same-parity layer before tells whether ANY block was
+    // active (a fast block's next-layer add can only touch the other field)
+    const int blk_active = __syncthreads_or(active);
+    if (threadIdx.x == 0) {
+      const int sh = 32 + 16 * (int)(L & 1);
+      const u64 add = 1ull + (blk_active ? (1ull << sh) : 0ull);
+      asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&ctl->bar), "l"(add) : "memory");
+      const u64 target = (u64)gridDim.x * L;
+      u64 v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&ctl->bar) : "memory");
+      } while ((v & 0xFFFFFFFFull) < target);
+      const u32 f = (u32)(v >> sh) & 0xFFFFu;
+      s_go = (f - s_prev[L & 1]) & 0xFFFFu;
+      s_prev[L & 1] = f;
+    }
+    __syncthreads();
+  }
+  block_add_u64(found, &ctl->processed);
+  if (gtid == 0) ctl->layers = L - 2;  // L - 1 was the first empty layer
 }
 
 // Bottom-up sums in ONE persistent reverse-level pass over the child edges
@@ -1568,7 +2028,8 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
 
   // ---- bottom-up layering (cycle check) then top-down layering -----------
   DBuf rem_td(R * 4, st), rootp(R, st);
-  DBuf bm(((R + 31) / 32) * 8 + 8, st);  // two frontier bitmaps
+  DBuf bm(std::max<u64>(((R + 31) / 32) * 8 + 8, R * 4 + 4), st);  // two frontier bitmaps, or delta[1] of k_kahn3
+  DBuf kdelta;  // k_kahn3's delta arrays in the global-count mode
   d->bu_level.alloc(R * 4, st);
   d->td_level.alloc(R * 4, st);
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, R * 4, st));
@@ -1582,36 +2043,71 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   DBuf reach(R, st);
   auto kahn = [&](DBuf& rem, const DBuf& off, const DBuf& ids, DBuf& lvl) {
     const u64 nwords = (R + 31) / 32;
-    GT_CUDA(cudaMemsetAsync(ctl, 0, sizeof(KahnCtl), st));
-    GT_CUDA(cudaMemsetAsync(bm.p, 0, 2 * nwords * 4, st));
-    // reachability starts at the rules the root references
-    GT_CUDA(cudaMemcpyAsync(reach.p, rootp.p, R, cudaMemcpyDeviceToDevice, st));
-    u32* b0 = bm.as<u32>();
-    u32* b1 = b0 + nwords;
-    LAUNCH(k_kahn_first, R, rem.as<u32>(), R, b1, ctl);  // layer 1 reads b1
-    static int per_sm = -1;
-    if (per_sm < 0) {
-      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kahn, kKahnBlock, 0));
-      per_sm = std::max(per_sm, 1);
-    }
     int nsm = 148;
     GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    // GT_KAHN=1|2|3 (diagnostics) forces the dependent-chain, batched-bitmap
+    // or owner-scan kernel; by default owner-scan when a warp's share of the
+    // sub CSR fits its shared memory, else batched-bitmap
+    static const int forced = getenv("GT_KAHN") ? atoi(getenv("GT_KAHN")) : 0;
+    const u64 nwarps3 = (u64)nsm * (kKahnBlock / 32), M3 = (nwords + nwarps3 - 1) / nwarps3;
+    const bool fits3 = kK3List + 64 * M3 + 1 + 2 * ((Es + nwarps3 - 1) / nwarps3) <= kK3WarpWords;
+    // mode 4 (diagnostics): owner-scan with the counts in global memory —
+    // measured slower than the batched bitmap on C5 (235 vs 138 us per
+    // layer: each warp scans ~120 counter words per layer in dependent waves)
+    const int mode = forced >= 1 && forced <= 4 ? forced : (fits3 ? 3 : 2);
+    GT_CUDA(cudaMemsetAsync(ctl, 0, sizeof(KahnCtl), st));
+    // reachability starts at the rules the root references
+    GT_CUDA(cudaMemcpyAsync(reach.p, rootp.p, R, cudaMemcpyDeviceToDevice, st));
     uint8_t* rc = reach.as<uint8_t>();
-    uint2* tk = tasks.as<uint2>();
     const u64* o = off.as<u64>();
     const u32* ii = ids.as<u32>();
     u32* rm = rem.as<u32>();
     u32* lv = lvl.as<u32>();
     u64 maxl = R + 2;
+    if (mode >= 3) {
+      static bool attr = false;
+      const size_t smem = (size_t)32 * kK3WarpWords * 4;
+      u32* gd0 = nullptr;
+      if (mode == 4 || !fits3) {
+        kdelta.alloc(R * 8 + 8, st);
+        GT_CUDA(cudaMemsetAsync(kdelta.p, 0, R * 8 + 8, st));
+        gd0 = kdelta.as<u32>();
+      }
+      if (!attr) {
+        GT_CUDA(cudaFuncSetAttribute(k_kahn3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+      }
+      u64 Rv = R;
+      // delta[1]: the frontier bitmaps' space (R words, see bm) or, in the
+      // global-count mode, the second half of kdelta
+      u32* d1 = gd0 ? gd0 + R + 1 : bm.as<u32>();
+      void* args[] = {(void*)&ctl, (void*)&o,  (void*)&ii, (void*)&Rv,  (void*)&rm,
+                      (void*)&d1,  (void*)&gd0, (void*)&lv, (void*)&rc, (void*)&maxl};
+      ProfScope ps_("k_kahn<td>", st);
+      GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_kahn3, dim3((unsigned)nsm), dim3(kKahnBlock), args, smem, st));
+      g_launches++;
+      return;
+    }
+    GT_CUDA(cudaMemsetAsync(bm.p, 0, 2 * nwords * 4, st));
+    u32* b0 = bm.as<u32>();
+    u32* b1 = b0 + nwords;
+    LAUNCH(k_kahn_first, R, rem.as<u32>(), R, b1, ctl);  // layer 1 reads b1
+    const bool v1 = mode == 1;
+    const void* kfn = v1 ? (const void*)k_kahn : (const void*)k_kahn2;
+    const size_t smem = v1 ? 0 : kK2Smem;
+    static int per_sm[2] = {-1, -1};
+    if (per_sm[v1] < 0) {
+      if (!v1) GT_CUDA(cudaFuncSetAttribute(k_kahn2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK2Smem));
+      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[v1], kfn, kKahnBlock, smem));
+      per_sm[v1] = std::max(per_sm[v1], 1);
+    }
+    uint2* tk = tasks.as<uint2>();
     u64 nw_ = nwords;
     void* args[] = {(void*)&ctl, (void*)&b0, (void*)&b1, (void*)&nw_, (void*)&o, (void*)&ii, (void*)&rm,
                     (void*)&lv, (void*)&rc, (void*)&tk, (void*)&maxl};
-    {
-      ProfScope ps_("k_kahn<td>", st);
-      GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_kahn, dim3((unsigned)(nsm * per_sm)), dim3(kKahnBlock),
-                                          args, 0, st));
-      g_launches++;
-    }
+    ProfScope ps_("k_kahn<td>", st);
+    GT_CUDA(cudaLaunchCooperativeKernel(kfn, dim3((unsigned)(nsm * per_sm[v1])), dim3(kKahnBlock), args, smem, st));
+    g_launches++;
   };
   // top-down Kahn layering: the frontier never reaches a rule on (or below)
   // a reference cycle, so an incomplete layering is the cycle check
@@ -1635,6 +2131,12 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   }
   processed = h.processed;
   const int ntd = (int)h.layers;
+  if (trace2() && ntd > 0 && h.t[1]) {
+    if (h.t[0]) fprintf(stderr, "[gt_open] kahn prologue %.1f us\n", (h.t[1] - h.t[0]) / 1e3);
+    fprintf(stderr, "[gt_open] kahn layers (us):");
+    for (int L = 1; L <= ntd && L + 1 < 64; L++) fprintf(stderr, " %.1f", (h.t[L + 1] - h.t[L]) / 1e3);
+    fprintf(stderr, "\n");
+  }
   if (processed + 1 < R || chk[0]) {
     need_host_chain();
     cycle_message(blob, P);
@@ -1643,6 +2145,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   ph.mark("top-down layering");
   rem_td.release();
   bm.release();
+  kdelta.release();
 
   // ---- level-ordered edge lists (radix sort is stable: within a level the
   // edges keep (child, parent) resp. (rule, child) order) -------------------
