@@ -156,6 +156,8 @@ int gt_open(const uint8_t* gtdc, size_t nbytes, int device, uint64_t file_lo, ui
 
 int gt_info_get(const gt_ctx* c, gt_info* o) {
   memset(o, 0, sizeof *o);
+  const int st = guard([&] { ensure_derived(const_cast<DeviceDag*>(&c->d)); });
+  if (st != GT_OK) return st;
   const DeviceDag& d = c->d;
   o->num_words = d.nw;
   o->num_splitters = d.ns;
@@ -270,6 +272,8 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
     DeviceDag& d = c->d;
     GT_CUDA(cudaSetDevice(d.device));
     cudaStream_t st = d.stream;
+    // a top-down word count / inverted index reads no derived array
+    if (!((task == GT_WORDCOUNT || task == GT_INVERTEDINDEX) && strategy != GT_BOTTOMUP)) ensure_derived(&d);
     auto t0 = std::chrono::steady_clock::now();
     u64 launches0 = g_launches;
     int strat = select_strategy(d, task, strategy, file_set_width);
@@ -390,7 +394,10 @@ int gt_run_many(gt_ctx* c, const int* tasks, int ntasks, int seq_len, int strate
         DevRecords W, I;
         if (!td_wc_ii_records(&d, &W, &I)) return;
         fused = true;
-        if (tasks[iw] == GT_SORT) order_by_count(&d, &W, 0, nullptr);
+        if (tasks[iw] == GT_SORT) {
+          ensure_derived(&d);
+          order_by_count(&d, &W, 0, nullptr);
+        }
         GT_CUDA(cudaEventRecord(c->ev[1], st));
         pull_records(rw, W, tasks[iw], seq_len, 0, GT_TOPDOWN, st);
         pull_records(ri, I, GT_INVERTEDINDEX, seq_len, 0, GT_TOPDOWN, st);
@@ -441,6 +448,7 @@ int gt_run_naive(gt_ctx* c, int task, int seq_len, gt_result** out) {
     if (task >= GT_SEQCOUNT && seq_len < 1) fail(GT_E_USAGE, "sequence length must be >= 1");
     DeviceDag& d = c->d;
     GT_CUDA(cudaSetDevice(d.device));
+    ensure_derived(&d);
     auto t0 = std::chrono::steady_clock::now();
     u64 launches0 = g_launches;
     GT_CUDA(cudaEventRecord(c->ev[0], d.stream));
@@ -474,6 +482,7 @@ int gt_assemble_counts(gt_ctx* c, int task, const uint64_t* dev_counts, gt_resul
     if (task != GT_WORDCOUNT && task != GT_SORT) fail(GT_E_USAGE, "gt_assemble_counts: task %d is not wordcount/sort", task);
     DeviceDag& d = c->d;
     GT_CUDA(cudaSetDevice(d.device));
+    if (task == GT_SORT) ensure_derived(&d);
     auto t0 = std::chrono::steady_clock::now();
     u64 launches0 = g_launches;
     GT_CUDA(cudaEventRecord(c->ev[0], d.stream));
@@ -589,6 +598,8 @@ int64_t gt_dag_array(gt_ctx* c, const char* name, int64_t* out, int64_t cap) {
       return v;
     };
     std::vector<int64_t> v;
+    ensure_derived(&c->d);
+    if (nm == "par_ids" || nm == "par_freqs" || nm == "par_off" || nm == "num_in_edge") ensure_parents(&c->d);
     if (nm == "own_ids") v = fetch32(d.own_ids, d.E_own);
     else if (nm == "own_freqs") v = fetch32(d.own_freqs, d.E_own);
     else if (nm == "own_off") v = fetch64(d.own_off, d.R + 1);

@@ -164,6 +164,12 @@ struct DeviceDag {
   DBuf be_rule, be_child, be_freq;
   std::vector<u64> be_off;  // host: bu level L items [be_off[L], be_off[L+1])
   DBuf be_off_dev;
+  DBuf sub_rule;       // u32[E_sub]: the rule of every sub pair (lazy builds)
+  // derived arrays (ensure_derived): no top-down word count / inverted
+  // index reads them, so gt_open leaves them to the first task that does
+  // (be lists, heights = bu_level, depth, exp_len, W, seg_tokens,
+  // max_file_tokens, cnt32)
+  bool derived = false;
   u64 load_flags = 0;  // gt_info.load_flags
   u64 max_file_tokens = 0;
   bool cnt32 = false;  // every file < 2^32 words: per-file rows / counts in u32 (GT_ROWS64=1: never)
@@ -178,7 +184,7 @@ struct DeviceDag {
                          &seg_tokens, &ow_word, &ow_rule, &ow_freq, &ow_off, &rs_rule, &rs_seg,
                          &rs_cnt, &rs_off, &rw_word, &rw_seg, &rw_cnt, &td.order, &bu.order,
                          &tid, &rs_rule_t, &ow_rule_t, &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts,
-                         &te_off_dev, &be_off_dev};
+                         &te_off_dev, &be_off_dev, &sub_rule};
     u64 t = 0;
     for (const DBuf* b : all) t += b->bytes;
     return t;
@@ -191,6 +197,8 @@ void build_device_dag(const uint8_t* blob, size_t n, int device, u64 file_lo, u6
 
 // bottom-up rule lists by level (built on first use)
 void ensure_bu_levels(DeviceDag* d);
+void ensure_parents(DeviceDag* d);  // par_* and num_in (built on first request)
+void ensure_derived(DeviceDag* d);  // see DeviceDag::derived
 
 // cub_ops.cu (plumbing around CUB device-wide primitives)
 void sort_pairs_u64_u32(u64* keys_in, u64* keys_out, u32* vals_in, u32* vals_out, u64 n,

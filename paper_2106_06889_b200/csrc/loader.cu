@@ -611,17 +611,6 @@ __global__ void k_gather3(const u32* idx, u64 n, const u32* a, const u32* b, con
   }
 }
 
-// non-root parent counters; root-parent flag
-__global__ void k_degrees(const u64* par_off, const u32* par_ids, u64 R, u32* rem_td, uint8_t* root_parent) {
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
-    u64 np = par_off[r + 1] - par_off[r];
-    bool rp = np && par_ids[par_off[r]] == 0;
-    root_parent[r] = rp;
-    rem_td[r] = (u32)(np - (rp ? 1 : 0));
-  }
-}
-
 // Warp-aggregated "decrement and detect completion": lanes hitting the same
 // counter subtract together (one atomic per distinct counter per warp, so a
 // rule with 10^5 parents finishing in one layer does not serialise 10^5
@@ -1320,17 +1309,74 @@ __global__ void k_edge_level_keys2(const u32* group_of, const uint8_t* keep, con
     key[i] = (keep && !keep[i]) ? drop_key : lvl[group_of[i]];
 }
 
-__global__ void k_flag_nonzero_u32(const u32* v, u64 n, uint8_t* f) {
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f[i] = v[i] != 0;
-}
 
-__global__ void k_root_cycle(const u64* par_off, const u32* par_ids, const uint8_t* reach, u32* bad) {
-  for (u64 e = par_off[0] + threadIdx.x; e < par_off[1]; e += blockDim.x) {
-    const u32 p = par_ids[e];
-    if (p == 0 || reach[p]) *bad = 1;
+// in-degrees straight from the (parent-major) sub pairs, no parent sort:
+// rem[c] = distinct non-root parents of c (the top-down Kahn counters),
+// rootp[c] = c is referenced by the root
+__global__ void k_in_degrees(const u32* __restrict__ prule, const u32* __restrict__ child, u64 n, u32* rem,
+                             uint8_t* rootp) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 p = prule[i], c = child[i];
+    if (p == 0) rootp[c] = 1;
+    else atomicAdd(&rem[c], 1u);
   }
 }
+
+// a reachable rule (or the root itself) referencing the root is a cycle
+__global__ void k_root_cycle2(const u32* __restrict__ prule, const u32* __restrict__ child, u64 n,
+                              const uint8_t* __restrict__ reach, u32* bad) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    if (child[i] == 0) {
+      const u32 p = prule[i];
+      if (p == 0 || reach[p]) *bad = 1;
+    }
+}
+
+// top-down edge lists by scatter: every child's non-root parent edges get a
+// contiguous slot range in (td level, child) = tid order (exclusive scan of
+// the in-degrees in tid order); within a child the slot order is the order
+// the atomics land in — the segmented reduce only needs each child's items
+// contiguous, and its sums are exact integers
+__global__ void k_cursor(const u32* __restrict__ degt, const u32* __restrict__ incl, u64 n, u32* cur) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) cur[t] = incl[t] - degt[t];
+}
+
+__global__ void k_te_scatter(const u32* __restrict__ prule, const u32* __restrict__ child,
+                             const u32* __restrict__ freq, u64 n, const u32* __restrict__ tid, u32* cur,
+                             u32* te_child, u32* te_par, u32* te_freq) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 p = prule[i];
+    if (p == 0) continue;
+    const u32 tc = tid[child[i]];
+    const u32 slot = atomicAdd(&cur[tc], 1u);
+    te_child[slot] = tc;
+    te_par[slot] = tid[p];
+    te_freq[slot] = freq[i];
+  }
+}
+
+// level offsets of the td edge lists: off[L] = first edge whose child is in
+// level >= L (ls[L] = first tid of level >= L, L = 0..nl+1), off[nl+2] = all
+__global__ void k_te_level_off(const u64* __restrict__ ls, const u32* __restrict__ incl,
+                               const u32* __restrict__ degt, u64 R, u64 nl, u64* off) {
+  const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > nl + 2) return;
+  const u64 tot = R ? incl[R - 1] : 0;
+  const u64 t = k <= nl + 1 ? ls[k] : R;
+  off[k] = t < R ? incl[t] - degt[t] : tot;
+}
+
+// rule id of every sub pair (expanding sub_off), for the lazily built parent CSR
+__global__ void k_expand_owner(const u64* __restrict__ off, u64 R, u32* owner) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride)
+    for (u64 e = off[r]; e < off[r + 1]; e++) owner[e] = (u32)r;
+}
+
 
 __global__ void k_fill_u64(u64* a, u64 n, u64 v) {
   u64 stride = (u64)gridDim.x * blockDim.x;
@@ -1599,6 +1645,119 @@ void ensure_bu_levels(DeviceDag* d) {
   GT_CUDA(cudaSetDevice(d->device));
   const int nl = d->bu.nl;
   build_levels(d, d->bu_level, d->sub_off, 16, nl, &d->bu);
+}
+
+// dag.py's parent CSR (par_ids / par_freqs / par_off, parents ascending per
+// child) and num_in_edge: no task reads them (the top-down edge lists are
+// scattered from the sub pairs at load), so they are built on first request
+// (gt_dag_array) with one stable sort of the sub pairs by child
+void ensure_parents(DeviceDag* d) {
+  if (d->par_off.p || d->R == 0) return;
+  GT_CUDA(cudaSetDevice(d->device));
+  cudaStream_t st = d->stream;
+  const u64 R = d->R, Es = d->E_sub;
+  DBuf prule(Es * 4 + 4, st), child_sorted(Es * 4 + 4, st), v1(Es * 8 + 8, st), v2(Es * 8 + 8, st);
+  LAUNCH(k_expand_owner, R, d->sub_off.as<u64>(), R, prule.as<u32>());
+  LAUNCH(k_pack2, Es, prule.as<u32>(), d->sub_freqs.as<u32>(), Es, v1.as<u64>());
+  sort_pairs_u32_u64(d->sub_ids.as<u32>(), child_sorted.as<u32>(), v1.as<u64>(), v2.as<u64>(), Es,
+                     std::max(1, bitlen(R - 1)), st);
+  d->par_ids.alloc(Es * 4 + 4, st);
+  d->par_freqs.alloc(Es * 4 + 4, st);
+  d->par_off.alloc((R + 1) * 8, st);
+  LAUNCH(k_unpack2, Es, v2.as<u64>(), Es, d->par_ids.as<u32>(), d->par_freqs.as<u32>());
+  LAUNCH(k_csr_offsets_lin, Es + 1, child_sorted.as<u32>(), Es, R, d->par_off.as<u64>());
+  d->num_in.alloc(R * 8, st);
+  GT_CUDA(cudaMemsetAsync(d->num_in.p, 0, R * 8, st));
+  LAUNCH(k_seg_sum_sorted, Es, child_sorted.as<u32>(), Es,
+         (ValU32NonRoot{d->par_freqs.as<u32>(), d->par_ids.as<u32>()}), d->num_in.as<u64>());
+  GT_CUDA(cudaStreamSynchronize(st));
+}
+
+// The derived arrays (DeviceDag::derived), on first use:
+//   be lists — sub entries (grouped by rule) by the rule's TOP-DOWN level;
+//     walked in decreasing level order every child is finished before its
+//     parents (a child's td level exceeds each parent's), which is all the
+//     bottom-up sums need; the root (td level 0) comes last;
+//   heights (= the reference's bottom-up rounds, engine.py:313-335; leaf = 1)
+//     and exp_len (grammar.py:109-124) in ONE persistent reverse pass;
+//   segment_token_counts (dag.py:88-104), the longest file, W, depth.
+void ensure_derived(DeviceDag* d) {
+  if (d->derived) return;
+  GT_CUDA(cudaSetDevice(d->device));
+  cudaStream_t st = d->stream;
+  const u64 R = d->R, Es = d->E_sub, nw = d->nw, base = d->nw + d->ns;
+  const int ntd = d->td.nl;
+  static thread_local PinnedU64 stage_host;
+  u64* stage = stage_host.get((u64)ntd + 3 + 3);
+  {
+    const Carve cv(st, {Es * 4 + 4, Es * 4 + 4, Es * 12 + 12, Es * 12 + 12});
+    const DPtr key{cv.at<void>(0)}, key2{cv.at<void>(1)}, v1{cv.at<void>(2)}, v2{cv.at<void>(3)};
+    const u32* sr = d->sub_rule.as<u32>();
+    LAUNCH(k_edge_level_keys2, Es, sr, nullptr, d->td_level.as<u32>(), (u32)ntd + 1, Es, key.as<u32>());
+    LAUNCH(k_pack3, Es, sr, d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), Es, v1.as<U3>());
+    sort_pairs_u32_u3(key.as<u32>(), key2.as<u32>(), v1.as<U3>(), v2.as<U3>(), Es,
+                      std::max(1, bitlen((u64)ntd + 1)), st);
+    d->be_rule.alloc(Es * 4 + 16, st);
+    d->be_child.alloc(Es * 4 + 16, st);
+    d->be_freq.alloc(Es * 4 + 16, st);
+    LAUNCH(k_unpack3, Es, v2.as<U3>(), Es, d->be_rule.as<u32>(), d->be_child.as<u32>(), d->be_freq.as<u32>());
+    d->be_off_dev.alloc(((u64)ntd + 3) * 8, st);
+    LAUNCH(k_csr_offsets, (u64)ntd + 3, key2.as<u32>(), Es, (u64)ntd + 2, d->be_off_dev.as<u64>());
+    GT_CUDA(cudaMemcpyAsync(stage, d->be_off_dev.p, ((u64)ntd + 3) * 8, cudaMemcpyDeviceToHost, st));
+  }
+  d->exp_len.alloc(R * 8, st);
+  {
+    DBuf hgt(R * 8, st);
+    LAUNCH(k_fill_u64, R, hgt.as<u64>(), R, 1ull);
+    GT_CUDA(cudaMemcpyAsync(d->exp_len.p, d->own_tok.p, R * 8, cudaMemcpyDeviceToDevice, st));
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bu_pair, 1024, 0));
+      per_sm = std::max(per_sm, 1);
+    }
+    int nsm = 148;
+    GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d->device));
+    const u32* br = d->be_rule.as<u32>();
+    const u32* bc = d->be_child.as<u32>();
+    const u32* bf = d->be_freq.as<u32>();
+    const u64* bo = d->be_off_dev.as<u64>();
+    int L1 = ntd;
+    u64* hg = hgt.as<u64>();
+    u64* el = d->exp_len.as<u64>();
+    void* args[] = {(void*)&br, (void*)&bc, (void*)&bf, (void*)&bo, (void*)&L1, (void*)&hg, (void*)&el};
+    {
+      ProfScope ps_("k_bu_pair", st);
+      GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_bu_pair, dim3((unsigned)(nsm * per_sm)), dim3(1024), args,
+                                          0, st));
+      g_launches++;
+    }
+    LAUNCH(k_u64_to_u32, R, hgt.as<u64>(), R, d->bu_level.as<u32>());
+    // the reference's bottom-up rounds exclude the root (engine.py:305-310)
+    GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
+    u64* hw = stage + (ntd + 3);
+    GT_CUDA(cudaMemcpyAsync(&hw[0], hgt.p, 8, cudaMemcpyDeviceToHost, st));          // root height
+    GT_CUDA(cudaMemcpyAsync(&hw[1], d->exp_len.p, 8, cudaMemcpyDeviceToHost, st));  // W
+  }
+  {
+    d->seg_tokens.alloc(d->F * 8, st);
+    GT_CUDA(cudaMemsetAsync(d->seg_tokens.p, 0, d->F * 8, st));
+    LAUNCH(k_seg_sum_sorted, d->L0, d->root_seg.as<u32>(), d->L0,
+           (ValRootLen{d->body.as<u32>(), d->exp_len.as<u64>(), nw, base}), d->seg_tokens.as<u64>());
+    DBuf mx(8, st);
+    reduce_max_u64(d->seg_tokens.as<u64>(), mx.as<u64>(), d->F, st);
+    GT_CUDA(cudaMemcpyAsync(stage + (ntd + 3) + 2, mx.p, 8, cudaMemcpyDeviceToHost, st));  // longest file
+  }
+  stream_sync(st);
+  d->be_off.assign(stage, stage + ntd + 3);
+  const u64* hw = stage + (ntd + 3);
+  d->bu.nl = (int)hw[0];
+  d->depth = (i64)hw[0] - 1;
+  d->W = hw[1];
+  d->max_file_tokens = hw[2];
+  static const bool rows64 = getenv("GT_ROWS64") != nullptr;
+  d->cnt32 = !rows64 && hw[2] < (1ull << 32);
+  if (d->cnt32) d->load_flags |= 2;
+  d->derived = true;
 }
 
 void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_lo, u64 file_hi,
@@ -1997,24 +2156,10 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
       LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
   }
 
-  // ---- parents: stable sort of sub pairs by child -------------------------
-  DBuf child_sorted(Es * 4 + 4, st);
-  {
-    DBuf v1(Es * 8 + 8, st), v2(Es * 8 + 8, st);
-    LAUNCH(k_pack2, Es, sub_rule.as<u32>(), d->sub_freqs.as<u32>(), Es, v1.as<u64>());
-    sort_pairs_u32_u64(d->sub_ids.as<u32>(), child_sorted.as<u32>(), v1.as<u64>(), v2.as<u64>(), Es,
-                       std::max(1, bitlen(R - 1)), st);
-    d->par_ids.alloc(Es * 4 + 4, st);
-    d->par_freqs.alloc(Es * 4 + 4, st);
-    d->par_off.alloc((R + 1) * 8, st);
-    LAUNCH(k_unpack2, Es, v2.as<u64>(), Es, d->par_ids.as<u32>(), d->par_freqs.as<u32>());
-    LAUNCH(k_csr_offsets_lin, Es + 1, child_sorted.as<u32>(), Es, R, d->par_off.as<u64>());
-  }
-  ph.mark("parent CSR");
-
-  // ---- per-rule sums -------------------------------------------------------
-  d->num_in.alloc(R * 8, st);
-  GT_CUDA(cudaMemsetAsync(d->num_in.p, 0, R * 8, st));
+  // ---- in-degrees straight from the sub pairs ------------------------------
+  // (no parent sort on the critical path: the top-down edge lists are
+  // scattered from the sub pairs below, and dag.py's parent CSR and
+  // num_in_edge are built on first use, ensure_parents)
   if (!fused) {  // (the per-rule pass produced them)
     d->own_tok.alloc(R * 8, st);
     d->num_out.alloc(R * 8, st);
@@ -2023,18 +2168,20 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     LAUNCH(k_seg_sum_sorted, Eo, own_rule.as<u32>(), Eo, ValU32{d->own_freqs.as<u32>()}, d->own_tok.as<u64>());
     LAUNCH(k_seg_sum_sorted, Es, sub_rule.as<u32>(), Es, ValU32{d->sub_freqs.as<u32>()}, d->num_out.as<u64>());
   }
-  LAUNCH(k_seg_sum_sorted, Es, child_sorted.as<u32>(), Es,
-         (ValU32NonRoot{d->par_freqs.as<u32>(), d->par_ids.as<u32>()}), d->num_in.as<u64>());
+  DBuf rem_td(R * 4 + 4, st), rootp(R + 1, st), indeg(R * 4 + 4, st);
+  GT_CUDA(cudaMemsetAsync(rem_td.p, 0, R * 4, st));
+  GT_CUDA(cudaMemsetAsync(rootp.p, 0, R, st));
+  LAUNCH(k_in_degrees, Es, sub_rule.as<u32>(), d->sub_ids.as<u32>(), Es, rem_td.as<u32>(), rootp.as<uint8_t>());
+  GT_CUDA(cudaMemcpyAsync(indeg.p, rem_td.p, R * 4, cudaMemcpyDeviceToDevice, st));  // the layering consumes rem_td
+  ph.mark("in-degrees");
 
-  // ---- bottom-up layering (cycle check) then top-down layering -----------
-  DBuf rem_td(R * 4, st), rootp(R, st);
+  // ---- top-down layering ---------------------------------------------------
   DBuf bm(std::max<u64>(((R + 31) / 32) * 8 + 8, R * 4 + 4), st);  // two frontier bitmaps, or delta[1] of k_kahn3
   DBuf kdelta;  // k_kahn3's delta arrays in the global-count mode
   d->bu_level.alloc(R * 4, st);
   d->td_level.alloc(R * 4, st);
   GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, R * 4, st));
   GT_CUDA(cudaMemsetAsync(d->td_level.p, 0, R * 4, st));
-  LAUNCH(k_degrees, R, d->par_off.as<u64>(), d->par_ids.as<u32>(), R, rem_td.as<u32>(), rootp.as<uint8_t>());
   // persistent top-down Kahn layering (doubles as the cycle check, carries
   // reachability): one cooperative launch
   const u64 ntask_max = Es / kChunk + R + 1;
@@ -2123,7 +2270,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     DBuf cd(8, st);
     GT_CUDA(cudaMemsetAsync(cd.p, 0, 4, st));
     GT_CUDA(cudaMemsetAsync(cd.as<u32>() + 1, 0xFF, 4, st));
-    LAUNCH(k_root_cycle, 1, d->par_off.as<u64>(), d->par_ids.as<u32>(), reach.as<uint8_t>(), cd.as<u32>());
+    LAUNCH(k_root_cycle2, Es, sub_rule.as<u32>(), d->sub_ids.as<u32>(), Es, reach.as<uint8_t>(), cd.as<u32>());
     LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, cd.as<u32>() + 1);
     GT_CUDA(cudaMemcpyAsync(&h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
     GT_CUDA(cudaMemcpyAsync(chk, cd.p, 8, cudaMemcpyDeviceToHost, st));
@@ -2150,129 +2297,40 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // ---- level-ordered edge lists (radix sort is stable: within a level the
   // edges keep (child, parent) resp. (rule, child) order) -------------------
   // host values read back once at the end of gt_open (one pinned staging
-  // buffer: te and be level offsets, root height, W)
+  // buffer: the te level offsets)
   static thread_local PinnedU64 stage_host;
-  u64* stage = stage_host.get(2 * ((u64)ntd + 3) + 3);
-  auto level_edges = [&](cudaStream_t st, const u32* group_of, const uint8_t* keep, const u32* lvl, int nl,
-                         const u32* a_src, const u32* b_src, const u32* f_src, DBuf& oa, DBuf& ob,
-                         DBuf& of, u64* off_stage, DBuf& off_dev, const u32* map) {
-    // every edge is sorted (dropped ones under key nl + 1, after all levels),
-    // so no count has to come back to the host first
-    // the edge triples travel with the level keys (one radix pass for <= 255 levels)
-    const Carve cv(st, {Es * 4 + 4, Es * 4 + 4, Es * 12 + 12, Es * 12 + 12});
-    const DPtr key{cv.at<void>(0)}, key2{cv.at<void>(1)}, v1{cv.at<void>(2)}, v2{cv.at<void>(3)};
-    LAUNCH(k_edge_level_keys2, Es, group_of, keep, lvl, (u32)nl + 1, Es, key.as<u32>());
-    if (map) LAUNCH(k_pack3_map, Es, a_src, b_src, f_src, Es, map, v1.as<U3>());
-    else LAUNCH(k_pack3, Es, a_src, b_src, f_src, Es, v1.as<U3>());
-    sort_pairs_u32_u3(key.as<u32>(), key2.as<u32>(), v1.as<U3>(), v2.as<U3>(), Es,
-                      std::max(1, bitlen((u64)nl + 1)), st);
-    oa.alloc(Es * 4 + 16, st);  // + 16: the TMA-staged level loop copies whole 16-byte words
-    ob.alloc(Es * 4 + 16, st);
-    of.alloc(Es * 4 + 16, st);
-    LAUNCH(k_unpack3, Es, v2.as<U3>(), Es, oa.as<u32>(), ob.as<u32>(), of.as<u32>());
-    DBuf koff(((u64)nl + 3) * 8, st);
-    LAUNCH(k_csr_offsets, (u64)nl + 3, key2.as<u32>(), Es, (u64)nl + 2, koff.as<u64>());
-    GT_CUDA(cudaMemcpyAsync(off_stage, koff.p, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
-    off_dev = std::move(koff);
-  };
-  // be: sub entries (grouped by rule) by the rule's TOP-DOWN level; walked in
-  // decreasing level order every child is finished before its parents (a
-  // child's td level exceeds each parent's), which is all the bottom-up sums
-  // need.  The root (td level 0) comes last.  Built on the side stream,
-  // concurrently with the tid numbering and the td lists below.
-  cudaEvent_t ev_lv, ev_be;
-  GT_CUDA(cudaEventCreateWithFlags(&ev_lv, cudaEventDisableTiming));
-  GT_CUDA(cudaEventCreateWithFlags(&ev_be, cudaEventDisableTiming));
-  GT_CUDA(cudaEventRecord(ev_lv, st));
-  GT_CUDA(cudaStreamWaitEvent(s_own, ev_lv, 0));
-  level_edges(s_own, sub_rule.as<u32>(), nullptr, d->td_level.as<u32>(), ntd, sub_rule.as<u32>(),
-              d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), d->be_rule, d->be_child, d->be_freq,
-              stage + (ntd + 3), d->be_off_dev, nullptr);
-  GT_CUDA(cudaEventRecord(ev_be, s_own));
+  u64* stage = stage_host.get((u64)ntd + 3);
   // tid: rules numbered by top-down level (stable: ascending rule id within
-  // a level, so the td edge lists stay sorted by destination)
+  // a level, so a level's rows are contiguous and ordered like the reference)
   {
-    const Carve cv(st, {R * 4, R * 4, R * 4});
-    LAUNCH(k_iota_u32, R, cv.at<u32>(0), R);
-    sort_pairs_u32_u32(d->td_level.as<u32>(), cv.at<u32>(1), cv.at<u32>(0), cv.at<u32>(2), R,
-                       std::max(1, bitlen((u64)ntd)), st);
+    const Carve cv(st, {R * 4, R * 4, R * 4, R * 4 + 4, R * 4 + 4, R * 4 + 4, ((u64)ntd + 3) * 8});
+    u32 *iota = cv.at<u32>(0), *slev = cv.at<u32>(1), *ord = cv.at<u32>(2), *degt = cv.at<u32>(3),
+        *incl = cv.at<u32>(4), *cur = cv.at<u32>(5);
+    u64* ls = cv.at<u64>(6);
+    LAUNCH(k_iota_u32, R, iota, R);
+    sort_pairs_u32_u32(d->td_level.as<u32>(), slev, iota, ord, R, std::max(1, bitlen((u64)ntd)), st);
     d->tid.alloc(R * 4, st);
-    LAUNCH(k_rank_of, R, cv.at<u32>(2), R, d->tid.as<u32>());
+    LAUNCH(k_rank_of, R, ord, R, d->tid.as<u32>());
+    // td: the non-root parent edges of every child, children in tid order
+    LAUNCH(k_csr_offsets, (u64)ntd + 2, slev, R, (u64)ntd + 1, ls);
+    LAUNCH(k_map_u32, R, ord, R, indeg.as<u32>(), degt);
+    inclusive_scan_u32(degt, incl, R, st);
+    LAUNCH(k_cursor, R, degt, incl, R, cur);
+    d->te_child.alloc(Es * 4 + 16, st);  // + 16: the TMA-staged level loop copies whole 16-byte words
+    d->te_par.alloc(Es * 4 + 16, st);
+    d->te_freq.alloc(Es * 4 + 16, st);
+    LAUNCH(k_te_scatter, Es, sub_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), Es,
+           d->tid.as<u32>(), cur, d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>());
+    d->te_off_dev.alloc(((u64)ntd + 3) * 8, st);
+    LAUNCH(k_te_level_off, (u64)ntd + 3, ls, incl, degt, R, (u64)ntd, d->te_off_dev.as<u64>());
+    GT_CUDA(cudaMemcpyAsync(stage, d->te_off_dev.p, ((u64)ntd + 3) * 8, cudaMemcpyDeviceToHost, st));
   }
-  {
-    // td: par entries (grouped by child) whose parent is not the root
-    DBuf keep(Es + 1, st);
-    LAUNCH(k_flag_nonzero_u32, Es, d->par_ids.as<u32>(), Es, keep.as<uint8_t>());
-    level_edges(st, child_sorted.as<u32>(), keep.as<uint8_t>(), d->td_level.as<u32>(), ntd,
-                child_sorted.as<u32>(), d->par_ids.as<u32>(), d->par_freqs.as<u32>(), d->te_child,
-                d->te_par, d->te_freq, stage, d->te_off_dev, d->tid.as<u32>());
-  }
-  GT_CUDA(cudaStreamWaitEvent(st, ev_be, 0));  // the bottom-up pass below reads the be lists
-  cudaEventDestroy(ev_lv);
-  cudaEventDestroy(ev_be);
-  sub_rule.release();
-  child_sorted.release();
-  // bottom-up levels = heights (leaf = 1; the reference's bottom-up rounds,
-  // engine.py:313-335), one persistent max pass in decreasing td level order
-  // heights (bottom-up levels) and exp_len in one persistent reverse pass
-  int nbu = 0;
-  d->exp_len.alloc(R * 8, st);
-  {
-    DBuf hgt(R * 8, st);
-    LAUNCH(k_fill_u64, R, hgt.as<u64>(), R, 1ull);
-    GT_CUDA(cudaMemcpyAsync(d->exp_len.p, d->own_tok.p, R * 8, cudaMemcpyDeviceToDevice, st));
-    {
-      static int per_sm = -1;
-      if (per_sm < 0) {
-        GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bu_pair, 1024, 0));
-        per_sm = std::max(per_sm, 1);
-      }
-      int nsm = 148;
-      GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-      const u32* br = d->be_rule.as<u32>();
-      const u32* bc = d->be_child.as<u32>();
-      const u32* bf = d->be_freq.as<u32>();
-      const u64* bo = d->be_off_dev.as<u64>();
-      int L1 = ntd;
-      u64* hg = hgt.as<u64>();
-      u64* el = d->exp_len.as<u64>();
-      void* args[] = {(void*)&br, (void*)&bc, (void*)&bf, (void*)&bo, (void*)&L1, (void*)&hg, (void*)&el};
-      ProfScope ps_("k_bu_pair", st);
-      GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_bu_pair, dim3((unsigned)(nsm * per_sm)), dim3(1024), args,
-                                          0, st));
-      g_launches++;
-    }
-    LAUNCH(k_u64_to_u32, R, hgt.as<u64>(), R, d->bu_level.as<u32>());
-    // height of the root (the highest rule) and W, read back at the end
-    u64* hw = stage + 2 * ((u64)ntd + 3);
-    GT_CUDA(cudaMemcpyAsync(&hw[0], hgt.p, 8, cudaMemcpyDeviceToHost, st));
-    GT_CUDA(cudaMemcpyAsync(&hw[1], d->exp_len.p, 8, cudaMemcpyDeviceToHost, st));
-  }
-  // level counts (bu.nl set from the root height at the end); the bottom-up
-  // rule lists (sequence tasks' head/tail pass) are built on first use
-  // (ensure_bu_levels), the top-down pass runs over the te edge lists
+  indeg.release();
+  d->sub_rule = std::move(sub_rule);  // kept for the lazy builds (ensure_derived, ensure_parents)
   d->td.nl = ntd;
-  // the reference's bottom-up rounds exclude the root (engine.py:305-310)
-  GT_CUDA(cudaMemsetAsync(d->bu_level.p, 0, 4, st));
   ph.mark("level lists");
 
-  // ---- exp_len by bottom-up level (grammar.py:109-124) --------------------
-  // (exp_len computed with the heights above)
-  ph.mark("segments+exp_len");
-
-  // ---- join the root side; segment tokens need exp_len ----------------------
   join_root();
-  {
-    DBuf& segof = d->root_seg;
-    d->seg_tokens.alloc(d->F * 8, st);
-    GT_CUDA(cudaMemsetAsync(d->seg_tokens.p, 0, d->F * 8, st));
-    LAUNCH(k_seg_sum_sorted, d->L0, segof.as<u32>(), d->L0,
-           (ValRootLen{d->body.as<u32>(), d->exp_len.as<u64>(), nw, base}), d->seg_tokens.as<u64>());
-    // the longest file, read back with the staging buffer below
-    DBuf mx(8, st);
-    reduce_max_u64(d->seg_tokens.as<u64>(), mx.as<u64>(), d->F, st);
-    GT_CUDA(cudaMemcpyAsync(stage + 2 * ((u64)ntd + 3) + 2, mx.p, 8, cudaMemcpyDeviceToHost, st));
-  }
   ph.mark("root side joined");
 
   // the seeds' and the reduce's rule ids in tid numbering (after the own
@@ -2292,19 +2350,9 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   stream_sync(st);
   stream_sync(s_own);
   own_rule.release();
-  {
-    d->te_off.assign(stage, stage + ntd + 3);
-    d->be_off.assign(stage + ntd + 3, stage + 2 * (ntd + 3));
-    const u64* hw = stage + 2 * ((u64)ntd + 3);
-    nbu = (int)hw[0];
-    d->depth = (i64)hw[0] - 1;
-    d->W = hw[1];
-    d->max_file_tokens = hw[2];
-    static const bool rows64 = getenv("GT_ROWS64") != nullptr;
-    d->cnt32 = !rows64 && hw[2] < (1ull << 32);
-    if (d->cnt32) d->load_flags |= 2;
-    d->bu.nl = nbu;
-  }
+  d->te_off.assign(stage, stage + ntd + 3);
+  static const bool eager = getenv("GT_EAGER_DERIVED") != nullptr;  // diagnostics: derive at open
+  if (eager) ensure_derived(d);
   ph.mark("finish");
   d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }

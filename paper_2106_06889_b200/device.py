@@ -105,9 +105,18 @@ class DeviceDag:
         self._h = h
         self.device = device
         self.grammar = GrammarView(self._blob) if self._blob is not None else None
-        inf = GtInfo()
-        L.gt_info_get(self._h, C.byref(inf))
-        self.info = inf.as_dict()
+        self._info = None
+
+    @property
+    def info(self) -> dict:
+        """gt_info_get.  The first call completes the derived DAG arrays
+        (exp_len, heights, W, segment token counts), which gt_open leaves to
+        the first task that reads them."""
+        if self._info is None:
+            inf = GtInfo()
+            raise_for_status(lib().gt_info_get(self._h, C.byref(inf)), _err())
+            self._info = inf.as_dict()
+        return self._info
 
     @property
     def num_files(self) -> int:
