@@ -2125,8 +2125,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     DeviceDag* d;
     ~StreamGuard() {
       cudaStreamSynchronize(s);
-      rebind_stream(main, {&d->ow_word, &d->ow_rule, &d->ow_freq, &d->ow_off, &d->be_rule, &d->be_child,
-                           &d->be_freq, &d->be_off_dev});
+      rebind_stream(main, {&d->ow_word, &d->ow_rule, &d->ow_freq, &d->ow_off});
       stream_release(d->device, s);
     }
   } own_guard{s_own, st, d};

@@ -529,7 +529,19 @@ struct PostArgs {
   u64* goff;
   u64* tot;
   u64* bsum;
+  // diagnostics (GT_TRACE=2): %globaltimer of block 0 at the phase
+  // boundaries — [0] entry, [1] seeds done, [2 + it] level it done, then the
+  // word reduce and the compaction
+  u64* stamps;
 };
+
+__device__ __forceinline__ void seg_stamp(u64* stamps, int k) {
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0 && k < 64) {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamps[k] = t;
+  }
+}
 
 // block-wide exclusive scan of two counters (1024 threads); returns the
 // block totals through *ta / *tb
@@ -775,6 +787,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
   using V = typename Mode::V;
   constexpr bool pair = std::is_same<Mode, WcPresMode>::value;
   cg::grid_group grid = cg::this_grid();
+  seg_stamp(post.stamps, 0);
   if (seed.row) {  // phase 0: clear the rows (and the reduce output), then the root seeds
     u64* zr = reinterpret_cast<u64*>(seed.row);
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < seed.zero_n; i += (u64)gridDim.x * blockDim.x)
@@ -788,6 +801,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
     seed_rows_body<Mode>(seed);
     grid.sync();
   }
+  seg_stamp(post.stamps, 1);
   const u64 nthreads = (u64)gridDim.x * blockDim.x;
   // warps numbered round-robin over the blocks: a level smaller than the
   // grid is spread over every SM instead of filling the first blocks
@@ -866,9 +880,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
       fetch(it + 1);
     }
     if (it + 1 < nit) grid.sync();
+    seg_stamp(post.stamps, 2 + it);
   }
   if (post.out) {  // the word reduce over the finished rows
     grid.sync();
+    seg_stamp(post.stamps, 2 + nit);
     if (post.n) {
       int K = (int)((post.n + 32 * nwarps - 1) / (32 * nwarps));
       K = K < 1 ? 1 : (K > 16 ? 16 : K);
@@ -893,7 +909,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
     }
     if (post.compact) {
       grid.sync();
+      seg_stamp(post.stamps, 3 + nit);
       post_compact(post, grid);
+      seg_stamp(post.stamps, 4 + nit);
     }
   }
 }

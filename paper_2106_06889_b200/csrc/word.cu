@@ -316,6 +316,13 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   post.goff = ii->group_off.as<u64>();
   post.tot = cv.at<u64>(3);
   post.bsum = cv.at<u64>(2);
+  static const bool tr = getenv("GT_TRACE") && atoi(getenv("GT_TRACE")) == 2;
+  DBuf stamps;
+  if (tr) {
+    stamps.alloc(64 * 8, st);
+    GT_CUDA(cudaMemsetAsync(stamps.p, 0, 64 * 8, st));
+    post.stamps = stamps.as<u64>();
+  }
   seg_reduce_levels1<WcPresMode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
                                  d->te_off_dev.as<u64>(), 1, d->td.nl, 0,
                                  d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0, &seed, &post,
@@ -323,6 +330,16 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   u64 h[2];
   GT_CUDA(cudaMemcpyAsync(h, post.tot, 16, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
+  if (tr) {
+    u64 t[64];
+    GT_CUDA(cudaMemcpy(t, stamps.p, 64 * 8, cudaMemcpyDeviceToHost));
+    const int nit = d->td.nl;
+    fprintf(stderr, "[wc+ii] seeds %.1f us | levels:", (t[1] - t[0]) / 1e3);
+    for (int i = 0; i < nit && 2 + i < 64; i++) fprintf(stderr, " %.1f", (t[2 + i] - (i ? t[1 + i] : t[1])) / 1e3);
+    if (4 + nit < 64)
+      fprintf(stderr, " | barrier %.1f | reduce+root %.1f | compact %.1f us\n", (t[2 + nit] - t[1 + nit]) / 1e3,
+              (t[3 + nit] - t[2 + nit]) / 1e3, (t[4 + nit] - t[3 + nit]) / 1e3);
+  }
   ii->n = h[0];
   ii->n_groups = h[1];
   wc->n = h[1];
