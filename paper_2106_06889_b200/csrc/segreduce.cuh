@@ -198,6 +198,9 @@ struct OutPair {
 };
 
 __device__ __forceinline__ u32 item_freq(const u32* freq, u64 i) { return freq ? freq[i] : 1u; }
+// item lists are read once per pass: streamed (evict-first), so they do not
+// push the gathered rows out of L2
+__device__ __forceinline__ u32 item_freq_cs(const u32* freq, u64 i) { return freq ? __ldcs(freq + i) : 1u; }
 
 // ---------------------------------------------------------------------------
 // one column: a warp owns tiles of 32*K consecutive items; runs are combined
@@ -226,8 +229,8 @@ __device__ __forceinline__ void segred1_body(const u32* __restrict__ dst, const 
       for (int u = 0; u < U; u++) {
         const u64 i = t0 + (u64)(k0 + u) * 32 + lane;
         const bool in_tile = k0 + u < K && i < tend;
-        dd[u] = in_tile ? dst[i] : 0xFFFFFFFFu;
-        vv[u] = in_tile ? Mode::combine(item_freq(freq, i), in(src[i], 0)) : Mode::zero();
+        dd[u] = in_tile ? __ldcs(dst + i) : 0xFFFFFFFFu;
+        vv[u] = in_tile ? Mode::combine(item_freq_cs(freq, i), in(__ldcs(src + i), 0)) : Mode::zero();
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {

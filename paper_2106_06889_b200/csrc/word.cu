@@ -176,6 +176,18 @@ static void td_levels(const DeviceDag* d, u32 C, T* row, u32 per_file = 1, const
 }
 
 
+// u64 rows -> u32 (saturating; *ovf set when a weight needs more than 32 bits)
+__global__ void k_narrow_rows(const u64* __restrict__ row, u64 n, u32* out, u32* ovf) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  bool big = false;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u64 v = row[i];
+    big |= v > 0xFFFFFFFFull;
+    out[i] = v > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)v;
+  }
+  if (__any_sync(0xFFFFFFFFu, big) && (threadIdx.x & 31u) == 0) *ovf = 1;
+}
+
 // Σ_r own_freq(r,w)·row[r] per word (reduce_words_round, _kernels.py:154-172)
 // as a gather-reduce over the word-major own pairs, then the root's plain
 // words per owned segment (root_words_round, _kernels.py:175-188).
@@ -187,6 +199,35 @@ static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool p
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
   GT_CUDA(cudaMemsetAsync(out, 0, sizeof(T) * V * C, st));
+  // C = 1 on a grammar whose u64 rows outgrow L2 (C5: 18M rules, 144 MB):
+  // the word-major gathers fetch one random row per own pair, so the rows
+  // are narrowed to u32 first (72 MB: they stay in L2 across the reduce);
+  // a weight of 2^32 or more (flagged) reruns the reduce on the u64 rows
+  static const bool wide = getenv("GT_REDUCE_U64") != nullptr;  // diagnostics: always gather u64 rows
+  if constexpr (sizeof(T) == 8) {
+    if (std::is_same<Mode, SumMode>::value && C == 1 && !wide && d->R * 8 > (64ull << 20)) {
+      const Carve cv(st, {d->R * 4 + 4, 4});
+      GT_CUDA(cudaMemsetAsync(cv.at<u32>(1), 0, 4, st));
+      KL(k_narrow_rows, grid_for(d->R, 256), reinterpret_cast<const u64*>(row), d->R, cv.at<u32>(0), cv.at<u32>(1));
+      if (row_major)
+        seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
+                         d->E_own, C, RowSrcT<u32>{cv.at<u32>(0), C}, OutRowMajorT<T>{out, C}, st);
+      else
+        seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
+                         d->E_own, C, RowSrcT<u32>{cv.at<u32>(0), C}, OutColMajorT<T>{out, V}, st);
+      u32 ovf = 0;
+      GT_CUDA(cudaMemcpyAsync(&ovf, cv.at<u32>(1), 4, cudaMemcpyDeviceToHost, st));
+      GT_CUDA(cudaStreamSynchronize(st));
+      if (!ovf) {
+        if (d->n_rw)
+          KL((k_root_words<Mode, T>), grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
+             d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, V,
+             row_major ? 1 : 0, out);
+        return;
+      }
+      GT_CUDA(cudaMemsetAsync(out, 0, sizeof(T) * V * C, st));  // a weight >= 2^32: the u64 rows
+    }
+  }
   if (row_major)
     seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
                      d->E_own, C, RowSrcT<T>{row, C}, OutRowMajorT<T>{out, C}, st);
