@@ -184,6 +184,26 @@ int gt_set_files(gt_ctx* ctx, uint64_t file_lo, uint64_t file_hi);
  * gt_device_word_counts): the assembly half of gt_run. */
 int gt_assemble_counts(gt_ctx* ctx, int task, const uint64_t* dev_counts, gt_result** out);
 
+/* Replicate a loaded context onto `device`: the DAG is built
+ * once and copied peer-to-peer (NVLink) to the other GPUs, replacing one
+ * host upload + device build (dag.py:131-230) per GPU.  The copy keeps the
+ * source's file range; shard it with gt_set_files.  Same device is allowed
+ * (several shards of one corpus on one GPU). */
+int gt_clone(const gt_ctx* src, int device, gt_ctx** out);
+
+/* Number of visible CUDA devices (0 when none). */
+int gt_device_count(void);
+
+/* Sum the dense word counts left by the last WORDCOUNT/SORT run of every
+ * context in srcs (file-range shards of one corpus, on any devices) into
+ * dst's device: one kernel on dst's device reads each shard's
+ * u64[num_words] vector in place through peer memory (NVLink) — the
+ * all-reduce of SURVEY §8e fused into the gather, no staging copy — and
+ * leaves the exact integer totals as dst's gt_device_word_counts (then
+ * gt_assemble_counts gives the corpus-wide result).  dst may be one of
+ * srcs. */
+int gt_sum_word_counts(gt_ctx* dst, gt_ctx* const* srcs, int n);
+
 /* Dense global word counts left on the device by the last WORDCOUNT/SORT run
  * (u64[num_words]); for NCCL all-reduce across shards.  Returns the device
  * pointer or NULL. */

@@ -105,6 +105,19 @@ void pinned_put(void* p, size_t cap) {
 
 using namespace gt;
 
+namespace gt {
+// the shards' dense word counts summed on one device, every shard's vector
+// read in place through peer memory (NVLink) when the devices differ
+__global__ void k_sum_shards(const u64* const* __restrict__ srcs, int n, u64 V, u64* out) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < V; i += stride) {
+    u64 t = 0;
+    for (int k = 0; k < n; k++) t += __ldcg(reinterpret_cast<const unsigned long long*>(srcs[k]) + i);
+    out[i] = t;
+  }
+}
+}  // namespace gt
+
 struct gt_ctx {
   DeviceDag d;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -472,6 +485,74 @@ int gt_set_files(gt_ctx* c, uint64_t file_lo, uint64_t file_hi) {
     if (file_lo > file_hi) fail(GT_E_USAGE, "file range [%lu, %lu) is empty-reversed", (unsigned long)file_lo, (unsigned long)file_hi);
     d.file_lo = std::min<u64>(file_lo, d.F);
     d.file_hi = std::min<u64>(file_hi, d.F);
+  });
+}
+
+int gt_clone(const gt_ctx* src, int device, gt_ctx** out) {
+  *out = nullptr;
+  gt_ctx* c = new gt_ctx();
+  int st = guard([&] {
+    int ndev = 0;
+    GT_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) fail(GT_E_USAGE, "gt_clone: no device %d (%d visible)", device, ndev);
+    clone_device_dag(src->d, device, &c->d);
+    for (auto& e : c->ev) GT_CUDA(cudaEventCreate(&e));
+  });
+  if (st != GT_OK) {
+    gt_close(c);
+    return st;
+  }
+  *out = c;
+  return GT_OK;
+}
+
+int gt_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int gt_sum_word_counts(gt_ctx* dst, gt_ctx* const* srcs, int n) {
+  return guard([&] {
+    if (n < 1) fail(GT_E_USAGE, "gt_sum_word_counts: no shards");
+    DeviceDag& d = dst->d;
+    const u64 V = d.nw;
+    for (int k = 0; k < n; k++) {
+      const DeviceDag& s = srcs[k]->d;
+      if (s.nw != V) fail(GT_E_USAGE, "gt_sum_word_counts: shard %d has %lu words, not %lu", k,
+                          (unsigned long)s.nw, (unsigned long)V);
+      if (!s.word_counts.p) fail(GT_E_USAGE, "gt_sum_word_counts: shard %d has no word counts (run WORDCOUNT first)", k);
+      GT_CUDA(cudaSetDevice(s.device));
+      GT_CUDA(cudaStreamSynchronize(s.stream));
+    }
+    GT_CUDA(cudaSetDevice(d.device));
+    cudaStream_t st = d.stream;
+    std::vector<const u64*> ptrs(n);
+    std::vector<DBuf> staged;  // shards whose memory dst's device cannot read
+    staged.reserve(n);
+    for (int k = 0; k < n; k++) {
+      const DeviceDag& s = srcs[k]->d;
+      int ok = s.device == d.device;
+      if (!ok) {
+        enable_peer(d.device, s.device);
+        GT_CUDA(cudaDeviceCanAccessPeer(&ok, d.device, s.device));
+      }
+      if (ok) {
+        ptrs[k] = s.word_counts.as<u64>();
+      } else {
+        staged.emplace_back(V * 8 + 8, st);
+        GT_CUDA(cudaMemcpyPeerAsync(staged.back().p, d.device, s.word_counts.p, s.device, V * 8, st));
+        ptrs[k] = staged.back().as<u64>();
+      }
+    }
+    DBuf dp((u64)n * 8, st), total(V * 8 + 8, st);
+    GT_CUDA(cudaMemcpyAsync(dp.p, ptrs.data(), (u64)n * 8, cudaMemcpyHostToDevice, st));
+    GT_KLAUNCH("k_sum_shards", k_sum_shards, grid_for(V, 256), 256, st, dp.as<const u64*>(), n, V, total.as<u64>());
+    GT_CUDA(cudaStreamSynchronize(st));
+    d.word_counts = std::move(total);
   });
 }
 

@@ -199,6 +199,9 @@ void build_device_dag(const uint8_t* blob, size_t n, int device, u64 file_lo, u6
 void ensure_bu_levels(DeviceDag* d);
 void ensure_parents(DeviceDag* d);  // par_* and num_in (built on first request)
 void ensure_derived(DeviceDag* d);  // see DeviceDag::derived
+// replicate a loaded DAG onto `device` (peer copies over NVLink)
+void clone_device_dag(const DeviceDag& src, int device, DeviceDag* d);
+void enable_peer(int a, int b);  // device a may read device b's memory (when supported)
 
 // cub_ops.cu (plumbing around CUB device-wide primitives)
 void sort_pairs_u64_u32(u64* keys_in, u64* keys_out, u32* vals_in, u32* vals_out, u64 n,

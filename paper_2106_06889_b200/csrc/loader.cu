@@ -2356,6 +2356,74 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// ---------------------------------------------------------------------------
+// Replication of a loaded DAG onto another device (the DAG is
+// built once and broadcast to the other GPUs over NVLink instead of N host
+// uploads and N device builds): every device array is copied peer-to-peer,
+// the host-side level tables and scalars by value.  The copy keeps the
+// source's file range; lazily built arrays travel if they exist.
+// ---------------------------------------------------------------------------
+void enable_peer(int a, int b) {
+  if (a == b) return;
+  static std::mutex mu;
+  static bool done[64][64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[a & 63][b & 63]) return;
+  done[a & 63][b & 63] = true;
+  int ok = 0;
+  GT_CUDA(cudaDeviceCanAccessPeer(&ok, a, b));
+  if (!ok) return;
+  int cur = 0;
+  GT_CUDA(cudaGetDevice(&cur));
+  GT_CUDA(cudaSetDevice(a));
+  const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) GT_CUDA(e);
+  cudaGetLastError();
+  GT_CUDA(cudaSetDevice(cur));
+}
+
+void clone_device_dag(const DeviceDag& s, int device, DeviceDag* d) {
+  auto t0 = std::chrono::steady_clock::now();
+  GT_CUDA(cudaSetDevice(s.device));
+  GT_CUDA(cudaStreamSynchronize(s.stream));  // the source is complete
+  GT_CUDA(cudaSetDevice(device));
+  d->device = device;
+  if (!d->stream) d->stream = stream_acquire(device);
+  cudaStream_t st = d->stream;
+  reserve_pool(device, st);
+  enable_peer(device, s.device);
+  auto cp = [&](const DBuf& a, DBuf& b) {
+    if (!a.p) return;
+    b.alloc(a.bytes, st);
+    GT_CUDA(cudaMemcpyPeerAsync(b.p, device, a.p, s.device, a.bytes, st));
+  };
+  const DBuf* src[] = {&s.body, &s.boff, &s.pos_owner, &s.root_seg, &s.own_ids, &s.own_freqs, &s.own_off,
+                       &s.own_tok, &s.sub_ids, &s.sub_freqs, &s.sub_off, &s.par_ids, &s.par_freqs, &s.par_off,
+                       &s.num_in, &s.num_out, &s.exp_len, &s.td_level, &s.bu_level, &s.seg_lo, &s.seg_hi,
+                       &s.seg_tokens, &s.ow_word, &s.ow_rule, &s.ow_freq, &s.ow_off, &s.rs_rule, &s.rs_seg,
+                       &s.rs_cnt, &s.rs_off, &s.rw_word, &s.rw_seg, &s.rw_cnt, &s.td.order, &s.td.off_dev,
+                       &s.bu.order, &s.bu.off_dev, &s.tid, &s.rs_rule_t, &s.ow_rule_t, &s.te_child, &s.te_par,
+                       &s.te_freq, &s.te_off_dev, &s.be_rule, &s.be_child, &s.be_freq, &s.be_off_dev, &s.sub_rule};
+  DBuf* dst[] = {&d->body, &d->boff, &d->pos_owner, &d->root_seg, &d->own_ids, &d->own_freqs, &d->own_off,
+                 &d->own_tok, &d->sub_ids, &d->sub_freqs, &d->sub_off, &d->par_ids, &d->par_freqs, &d->par_off,
+                 &d->num_in, &d->num_out, &d->exp_len, &d->td_level, &d->bu_level, &d->seg_lo, &d->seg_hi,
+                 &d->seg_tokens, &d->ow_word, &d->ow_rule, &d->ow_freq, &d->ow_off, &d->rs_rule, &d->rs_seg,
+                 &d->rs_cnt, &d->rs_off, &d->rw_word, &d->rw_seg, &d->rw_cnt, &d->td.order, &d->td.off_dev,
+                 &d->bu.order, &d->bu.off_dev, &d->tid, &d->rs_rule_t, &d->ow_rule_t, &d->te_child, &d->te_par,
+                 &d->te_freq, &d->te_off_dev, &d->be_rule, &d->be_child, &d->be_freq, &d->be_off_dev, &d->sub_rule};
+  static_assert(sizeof(src) / sizeof(src[0]) == sizeof(dst) / sizeof(dst[0]), "clone lists");
+  for (size_t i = 0; i < sizeof(src) / sizeof(src[0]); i++) cp(*src[i], *dst[i]);
+  d->nw = s.nw, d->ns = s.ns, d->R = s.R, d->E = s.E, d->F = s.F, d->L0 = s.L0, d->W = s.W;
+  d->file_lo = s.file_lo, d->file_hi = s.file_hi, d->depth = s.depth;
+  d->E_own = s.E_own, d->E_sub = s.E_sub, d->n_rs = s.n_rs, d->n_rw = s.n_rw;
+  d->td.off = s.td.off, d->td.heavy_off = s.td.heavy_off, d->td.nl = s.td.nl;
+  d->bu.off = s.bu.off, d->bu.heavy_off = s.bu.heavy_off, d->bu.nl = s.bu.nl;
+  d->te_off = s.te_off, d->be_off = s.be_off;
+  d->derived = s.derived, d->load_flags = s.load_flags, d->max_file_tokens = s.max_file_tokens, d->cnt32 = s.cnt32;
+  GT_CUDA(cudaStreamSynchronize(st));
+  d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 static std::mutex g_stream_mu;
 static std::vector<cudaStream_t> g_stream_pool[64];
 

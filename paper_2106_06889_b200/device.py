@@ -26,7 +26,8 @@ EXPORTS = ("gt_abi_version", "gt_last_error", "gt_open", "gt_info_get", "gt_run"
            "gt_dag_array", "gt_flush_l2", "gt_sync", "gt_profile", "gt_profile_report",
            "gt_set_files", "gt_assemble_counts", "gt_dict_open", "gt_dict_close", "gt_render_view",
            "gt_free_text", "gt_digest_view", "gt_sha256", "gt_table_add_batch", "gt_run_naive",
-           "gt_compress", "gt_compress_free", "gt_compress_last_error", "gt_run_many")
+           "gt_compress", "gt_compress_free", "gt_compress_last_error", "gt_run_many", "gt_clone",
+           "gt_device_count", "gt_sum_word_counts")
 _lib = None
 
 
@@ -76,8 +77,18 @@ def lib():
         L.gt_table_add_batch.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                          C.c_void_p, C.c_void_p]
         L.gt_assemble_counts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.gt_clone.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.gt_clone.restype = C.c_int
+        L.gt_device_count.restype = C.c_int
+        L.gt_sum_word_counts.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int]
+        L.gt_sum_word_counts.restype = C.c_int
         _lib = L
     return _lib
+
+
+def device_count() -> int:
+    """Visible CUDA devices (gt_device_count)."""
+    return int(lib().gt_device_count())
 
 
 def _err() -> str:
@@ -209,6 +220,32 @@ class DeviceDag:
     def device_word_counts_ptr(self) -> int:
         return lib().gt_device_word_counts(self._h) or 0
 
+    def clone(self, device: int) -> "DeviceDag":
+        """gt_clone: this DAG replicated onto `device` by peer copies (built
+        once, broadcast over NVLink); same file range, same grammar view."""
+        h = C.c_void_p()
+        raise_for_status(lib().gt_clone(self._h, device, C.byref(h)), _err())
+        c = DeviceDag.__new__(DeviceDag)
+        c._h, c._blob, c.device, c.grammar, c._info = h, self._blob, device, self.grammar, None
+        return c
+
+    def sum_word_counts(self, shards) -> None:
+        """gt_sum_word_counts: the shards' dense word counts (after a word
+        count run on each) summed on this context's device through peer
+        memory; the total becomes this context's device word counts."""
+        hs = (C.c_void_p * len(shards))(*[s._h.value for s in shards])
+        raise_for_status(lib().gt_sum_word_counts(self._h, hs, len(shards)), _err())
+
+    def sharded(self, workers: int, devices=None):
+        """The corpus sharded by token-balanced file ranges over `workers`
+        contexts (shard.ShardedDag); cached per worker count."""
+        from .shard import ShardedDag
+        cache = self.__dict__.setdefault("_sharded", {})
+        key = (workers, tuple(devices) if devices else None)
+        if key not in cache:
+            cache[key] = ShardedDag(self, workers, devices)
+        return cache[key]
+
     def dag_array(self, name: str) -> np.ndarray:
         L = lib()
         n = L.gt_dag_array(self._h, name.encode(), None, 0)
@@ -232,6 +269,8 @@ class DeviceDag:
         raise_for_status(lib().gt_sync(self._h), _err())
 
     def close(self) -> None:
+        for sd in self.__dict__.pop("_sharded", {}).values():
+            sd.close()
         if self._h is not None:
             lib().gt_close(self._h)
             self._h = None

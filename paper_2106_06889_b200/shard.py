@@ -188,11 +188,60 @@ def run_distributed(runner, task: str, seq_len: int = 3, strategy: int = 0,
         t = runner.counts_tensor()
         dist.all_reduce(t)  # exact: integer sums
         return runner.assemble(t, task) if runner.rank == 0 else None
-    got = [None] * runner.world if runner.rank == 0 else None
-    dist.gather_object(part, got, dst=0)
+    got = gather_compacts(part, runner.rank, runner.world, getattr(runner, "collective_device", "cpu"))
     if runner.rank != 0:
         return None
     return combine(got, task, runner.num_words)
+
+
+_FIELDS = ("group_off", "group_id", "group_key", "group_gram", "id", "key", "gram", "count")
+
+
+def gather_compacts(part: Compact, rank: int, world: int, device="cpu"):
+    """Rank 0 receives every rank's result arrays as flat int64 tensors
+    (torch.distributed.gather: NCCL on GPUs, gloo on CPUs) — no pickling,
+    one message per field sized by an all-gathered length table.  Returns the
+    list of Compacts (rank order) on rank 0, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    def arr(name):
+        a = getattr(part, name)
+        return np.zeros(0, np.int64) if a is None else np.asarray(a).astype(np.int64, copy=False).ravel()
+
+    arrays = [arr(f) for f in _FIELDS]
+    # per field: element count + 1 (0 = absent), then n, n_groups, wbits
+    meta = [len(a) + 1 if getattr(part, f) is not None else 0 for f, a in zip(_FIELDS, arrays)]
+    meta += [int(part.n), int(part.n_groups), int(part.wbits)]
+    mt = torch.tensor(meta, dtype=torch.int64, device=device)
+    metas = [torch.empty_like(mt) for _ in range(world)]
+    dist.all_gather(metas, mt)
+    metas = [m.cpu().numpy() for m in metas]
+    out = [dict() for _ in range(world)] if rank == 0 else None
+    for j, f in enumerate(_FIELDS):
+        L = max(max(int(m[j]) - 1, 0) for m in metas)
+        if L == 0 and all(m[j] == 0 for m in metas):
+            continue
+        buf = torch.zeros(max(L, 1), dtype=torch.int64, device=device)
+        a = torch.from_numpy(arrays[j]).to(device)
+        buf[:len(a)] = a
+        bufs = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+        dist.gather(buf, bufs, dst=0)
+        if rank == 0:
+            for r in range(world):
+                nm = int(metas[r][j])
+                out[r][f] = bufs[r][:nm - 1].cpu().numpy() if nm else None
+    if rank != 0:
+        return None
+    res = []
+    for r in range(world):
+        m = metas[r]
+        c = Compact(task=part.task, seq_len=part.seq_len, wbits=int(m[-1]), strategy=part.strategy,
+                    n_groups=int(m[-2]), n=int(m[-3]))
+        for f in _FIELDS:
+            setattr(c, f, out[r].get(f))
+        res.append(c)
+    return res
 
 
 class DeviceRunner:
@@ -205,6 +254,7 @@ class DeviceRunner:
             ranges = shard_ranges(dag.dag_array("segment_token_counts"), world)
         self.file_lo, self.file_hi = ranges[rank]
         dag.set_files(self.file_lo, self.file_hi)
+        self.collective_device = f"cuda:{dag.device}"
 
     def run(self, task_id, seq_len, strategy, fsw):
         return self.dag.run(task_id, seq_len, strategy, fsw)
@@ -222,3 +272,83 @@ class DeviceRunner:
     def assemble(self, t, task):
         from ._abi import TASK_IDS
         return self.dag.assemble_counts(t.data_ptr(), TASK_IDS[task])
+
+
+# ---------------------------------------------------------------------------
+# one process, several devices (TraversalConfig.workers > 1)
+# ---------------------------------------------------------------------------
+
+class ShardedDag:
+    """One corpus over `workers` file-range shards in ONE process
+    (`TraversalConfig.workers`, engine.py:34-48 — the reference's worker
+    count, here GPUs).  The DAG is built once (the given DeviceDag) and
+    replicated to every shard's device with gt_clone (peer copies over
+    NVLink; SURVEY §8e "uploads to GPU0 and broadcasts").  Shards run
+    concurrently (one host thread each; ctypes releases the GIL).  Word
+    count / sort: every shard's dense counts are summed on shard 0's device
+    by one kernel reading the others through peer memory
+    (gt_sum_word_counts), then assembled there (gt_assemble_counts); per-file
+    tasks combine by file order (`combine`).  Devices default to
+    ``i % device_count``: on a single GPU the shards share it (the logic and
+    the results are those of the multi-GPU run)."""
+
+    def __init__(self, dag, workers: int, devices=None):
+        from .device import device_count
+        if workers < 1:
+            raise ValueError("workers must be >= 1")
+        ndev = max(1, device_count())
+        self.devices = list(devices) if devices else [i % ndev for i in range(workers)]
+        if len(self.devices) != workers:
+            raise ValueError("one device per worker")
+        self.ranges = shard_ranges(dag.dag_array("segment_token_counts"), workers)
+        self.grammar = dag.grammar
+        self.num_words = dag.info["num_words"]
+        self._info = dict(dag.info)
+        self.shards = []
+        try:
+            for dev, (lo, hi) in zip(self.devices, self.ranges):
+                s = dag.clone(dev)
+                s.set_files(lo, hi)
+                self.shards.append(s)
+        except Exception:
+            self.close()
+            raise
+
+    @property
+    def info(self) -> dict:
+        return self._info
+
+    @property
+    def num_files(self) -> int:
+        return self._info["num_files"]
+
+    @property
+    def num_rules(self) -> int:
+        return self._info["num_rules"]
+
+    def _each(self, fn):
+        from concurrent.futures import ThreadPoolExecutor
+        if len(self.shards) == 1:
+            return [fn(self.shards[0])]
+        with ThreadPoolExecutor(len(self.shards)) as ex:
+            return list(ex.map(fn, self.shards))
+
+    def run(self, task_id: int, seq_len: int, strategy: int, file_set_width: int) -> Compact:
+        from ._abi import TASK_IDS, TASK_NAMES
+        task = TASK_NAMES[task_id]
+        if task in WORD_TASKS_GLOBAL:
+            self._each(lambda s: s.run(TASK_IDS["wordcount"], seq_len, strategy, file_set_width))
+            s0 = self.shards[0]
+            s0.sum_word_counts(self.shards)
+            return s0.assemble_counts(s0.device_word_counts_ptr(), task_id)
+        parts = self._each(lambda s: s.run(task_id, seq_len, strategy, file_set_width))
+        return combine(parts, task, self.num_words)
+
+    def run_many(self, task_ids, seq_len: int, strategy: int, file_set_width: int):
+        return [self.run(t, seq_len, strategy, file_set_width) for t in task_ids]
+
+    def close(self) -> None:
+        for s in self.shards:
+            s.close()
+        self.shards = []
+

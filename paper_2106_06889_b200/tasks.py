@@ -25,8 +25,10 @@ STRATEGIES = ("auto", "topdown", "bottomup")
 
 @dataclass
 class TraversalConfig:
-    """engine.py:34-48.  `workers` is the number of GPUs a sharded run uses
-    (bench.py / parallel.py); a single DeviceDag always runs on one device."""
+    """engine.py:34-48.  `workers` is the number of GPUs (file-range shards)
+    a task runs on: workers > 1 shards the corpus with shard.ShardedDag (the
+    DAG built once and replicated by peer copies, results combined on the
+    first device)."""
 
     strategy: str = "auto"
     workers: int = 1
@@ -81,7 +83,15 @@ def run_compact(dag, task: str, cfg: TraversalConfig | None = None,
     cfg = cfg or TraversalConfig()
     if task in ("seqcount", "rankedinvertedindex") and seq_len < 1:
         raise UsageError("sequence length must be >= 1")
-    return dag.run(TASK_IDS[task], seq_len, STRATEGY_IDS[cfg.strategy], cfg.file_set_width)
+    return _workers(dag, cfg).run(TASK_IDS[task], seq_len, STRATEGY_IDS[cfg.strategy], cfg.file_set_width)
+
+
+def _workers(dag, cfg: TraversalConfig):
+    """The sharded view of `dag` over cfg.workers devices (DeviceDag only;
+    other handles, e.g. the test oracle, run as given)."""
+    if cfg.workers > 1 and hasattr(dag, "sharded"):
+        return dag.sharded(cfg.workers)
+    return dag
 
 
 def run_compact_many(dag, tasks, cfg: TraversalConfig | None = None,
@@ -95,6 +105,7 @@ def run_compact_many(dag, tasks, cfg: TraversalConfig | None = None,
             raise UsageError(f"unknown task {task!r}; expected one of {', '.join(TASK_NAMES)}")
     if any(t in ("seqcount", "rankedinvertedindex") for t in tasks) and seq_len < 1:
         raise UsageError("sequence length must be >= 1")
+    dag = _workers(dag, cfg)
     if hasattr(dag, "run_many"):
         return dag.run_many([TASK_IDS[t] for t in tasks], seq_len, STRATEGY_IDS[cfg.strategy],
                             cfg.file_set_width)

@@ -63,3 +63,61 @@ def test_empty_shard_outputs_are_empty():
             assert c.n == 0, task
         dag.set_files(0, 1 << 62)
         assert gt.run_compact(dag, "wordcount", gt.TraversalConfig()).n > 0
+
+
+# ---------------------------------------------------------------------------
+# TraversalConfig.workers > 1 through the library: the DAG replicated with
+# gt_clone, shards run concurrently, word counts summed through peer memory
+# (gt_sum_word_counts), per-file results combined in file order
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("src", ["g1", "many_files_70", "composed_2", "c2@0.003", "c3@0.003"])
+@pytest.mark.parametrize("workers", [2, 3, 4])
+def test_workers_config_matches_single_device(src, workers):
+    import paper_2106_06889_b200 as gt
+    blob = composed(*src.split("@")[0:1], float(src.split("@")[1])) if "@" in src else gtdc(src)
+    with gt.DeviceDag(blob) as dag:
+        for l in (2, 3):
+            one = gt.run_compact_many(dag, TASKS, gt.TraversalConfig(), l)
+            many = gt.run_compact_many(dag, TASKS, gt.TraversalConfig(workers=workers), l)
+            for task, a, b in zip(TASKS, many, one):
+                same_compact(a, b)
+            # the reference containers through run_task
+            for task in ("wordcount", "invertedindex"):
+                assert gt.run_task(dag, task, gt.TraversalConfig(workers=workers)) == \
+                    gt.run_task(dag, task, gt.TraversalConfig())
+
+
+def test_clone_replicates_every_dag_array():
+    import paper_2106_06889_b200 as gt
+    with gt.DeviceDag(gtdc("many_files_70")) as dag:
+        c = dag.clone(0)
+        try:
+            for name in ("own_ids", "own_freqs", "own_off", "sub_ids", "sub_off", "par_ids", "par_off",
+                         "exp_len", "td_level", "bu_level", "segments", "segment_token_counts"):
+                assert np.array_equal(c.dag_array(name), dag.dag_array(name)), name
+            assert c.info["words"] == dag.info["words"]
+        finally:
+            c.close()
+
+
+def test_sum_word_counts_is_the_corpus_total():
+    import paper_2106_06889_b200 as gt
+    from paper_2106_06889_b200._abi import TASK_IDS
+    from paper_2106_06889_b200.shard import shard_ranges
+    with gt.DeviceDag(composed("c2", 0.003)) as dag:
+        full = gt.run_compact(dag, "wordcount", gt.TraversalConfig())
+        toks = dag.dag_array("segment_token_counts")
+        shards = []
+        try:
+            for lo, hi in shard_ranges(toks, 3):
+                s = dag.clone(0)
+                s.set_files(lo, hi)
+                s.run(TASK_IDS["wordcount"], 3, 0, 64)
+                shards.append(s)
+            shards[1].sum_word_counts(shards)  # dst may be any shard
+            got = shards[1].assemble_counts(shards[1].device_word_counts_ptr(), TASK_IDS["wordcount"])
+            same_compact(got, full)
+        finally:
+            for s in shards:
+                s.close()
