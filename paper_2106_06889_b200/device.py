@@ -17,7 +17,7 @@ from pathlib import Path
 import numpy as np
 
 from ._abi import GtInfo, GtView, compact_from_view, raise_for_status
-from .errors import ResourceError
+from .errors import UsageError, ResourceError
 from .gtdc import GrammarView
 
 LIB_PATH = Path(__file__).resolve().parent / "libgtadoc_b200.so"
@@ -321,8 +321,45 @@ def table_add_batch(keys, deltas, capacity: int, device: int = 0):
     return dict(zip(ok[occ].tolist(), ov[occ].tolist())), ok, ov
 
 
+def gtdc_of(source) -> bytes | None:
+    """GTDC bytes of a reference `Grammar` (grammar.py:30-72) or of a
+    reference `Dag` (dag.py:32-52, via its `.grammar`), serialized as the
+    reference's serialize_grammar (grammar.py:164-174) writes them; None for
+    anything else.  Duck-typed: the reference package is not imported."""
+    g = getattr(source, "grammar", source)
+    d, bodies = getattr(g, "dictionary", None), getattr(g, "bodies", None)
+    if d is None or bodies is None or not hasattr(d, "words") or not hasattr(d, "num_splitters"):
+        return None
+    from .corpus import serialize_bodies
+    return serialize_bodies(list(d.words), int(d.num_splitters), list(bodies))
+
+
 def build_dag(source, device: int = 0) -> DeviceDag:
-    """GTDC bytes (or a path to a .gtdc file) -> DeviceDag."""
+    """GTDC bytes, a path to a .gtdc file, or the reference's own `Dag` /
+    `Grammar` object (dag.py:32-52, grammar.py:30-72: its grammar is
+    serialized and loaded) -> DeviceDag."""
     if isinstance(source, (str, Path)):
         source = Path(source).read_bytes()
+    elif not isinstance(source, (bytes, bytearray, memoryview, tuple)):
+        blob = gtdc_of(source)
+        if blob is None:
+            raise UsageError(f"build_dag: cannot load a {type(source).__name__}")
+        source = blob
     return DeviceDag(source, device=device)
+
+
+def as_device_dag(dag, device: int = 0):
+    """The task entry points accept the reference's `Dag` too:
+    a reference Dag / Grammar is loaded once and the DeviceDag cached on it;
+    a DeviceDag (or any handle with `run`) passes through."""
+    if hasattr(dag, "run"):
+        return dag
+    cached = getattr(dag, "_b200_device_dag", None)
+    if cached is not None:
+        return cached
+    dd = build_dag(dag, device)
+    try:
+        setattr(dag, "_b200_device_dag", dd)
+    except (AttributeError, TypeError):
+        pass
+    return dd

@@ -87,8 +87,12 @@ def run_compact(dag, task: str, cfg: TraversalConfig | None = None,
 
 
 def _workers(dag, cfg: TraversalConfig):
-    """The sharded view of `dag` over cfg.workers devices (DeviceDag only;
-    other handles, e.g. the test oracle, run as given)."""
+    """The handle a task runs on: a reference `Dag` / `Grammar` is loaded
+    onto the device once (device.as_device_dag), and with cfg.workers > 1 a
+    DeviceDag is sharded over that many devices (other handles, e.g. the
+    test oracle, run as given)."""
+    from .device import as_device_dag
+    dag = as_device_dag(dag)
     if cfg.workers > 1 and hasattr(dag, "sharded"):
         return dag.sharded(cfg.workers)
     return dag
@@ -123,14 +127,18 @@ def output_digest(dag, task: str, cfg: TraversalConfig | None = None,
     """sha256 hex + byte length of `render(run_task(...))` — the reference
     CLI manifest's outputDigest (cli.py:121-133) — rendered natively
     (render.cpp) without building the Python containers or the text."""
+    from .device import as_device_dag
     from .native import NativeDict
+    dag = as_device_dag(dag)
     return NativeDict(dag.grammar.blob).digest(run_compact(dag, task, cfg, seq_len))
 
 
 def render_native(dag, task: str, cfg: TraversalConfig | None = None,
                   seq_len: int = DEFAULT_SEQ_LEN) -> str:
     """`render(run_task(...), dag.grammar.dictionary)`, rendered natively."""
+    from .device import as_device_dag
     from .native import NativeDict
+    dag = as_device_dag(dag)
     return NativeDict(dag.grammar.blob).render(run_compact(dag, task, cfg, seq_len))
 
 
