@@ -174,6 +174,16 @@ void gt_close(gt_ctx* ctx);
  * tasks need packed grams (seq_len * wbits <= 63). */
 int gt_run_naive(gt_ctx* ctx, int task, int seq_len, gt_result** out);
 
+/* The plain-text counterpart of gt_run_naive, for `verify` on an input
+ * directory (cli.py:137-147): count the given per-file token streams (word
+ * ids, file f = tokens[file_off[f] .. file_off[f+1]), nfiles == num_files,
+ * e.g. from gt_tokenize of the files the grammar was compressed from) with
+ * the same device counting and ordering stage — no grammar expansion and no
+ * use of the loaded DAG's arrays, so it checks the loader too.  Same result
+ * layout as gt_run; verification only. */
+int gt_count_tokens(gt_ctx* ctx, int task, int seq_len, const uint32_t* tokens, const uint64_t* file_off,
+                    uint64_t nfiles, gt_result** out);
+
 /* Multi-GPU sharding: restrict per-file work and root seeds of
  * subsequent gt_run calls to files [file_lo, file_hi) (clamped to F); the
  * DAG itself is replicated in every context. */
@@ -268,6 +278,12 @@ int gt_compress(const uint8_t* const* files, const uint64_t* lens, uint64_t nfil
                 uint64_t* out_len, uint64_t* stats);
 void gt_compress_free(uint8_t* p);
 const char* gt_compress_last_error(void);
+/* The ingest half alone: the files as word-id token streams (the ids
+ * gt_compress gives the same files), file f = tokens[file_off[f] ..
+ * file_off[f+1]) (file_off: nfiles + 1 entries, caller-allocated).
+ * *tokens is malloc'd (release with gt_compress_free). */
+int gt_tokenize(const uint8_t* const* files, const uint64_t* lens, uint64_t nfiles, uint32_t** tokens,
+                uint64_t* file_off);
 
 #ifdef __cplusplus
 }

@@ -50,3 +50,35 @@ def compress_dir(input_dir) -> tuple[bytes, dict]:
     if not names:
         raise UsageError(f"{input_dir}: contains no regular files")
     return compress_files([(name, (root / name).read_bytes()) for name in names])
+
+
+def tokenize_files(files: list[tuple[str, bytes]]):
+    """(name, raw bytes) pairs -> (u32 token ids, u64 file offsets [nfiles+1])
+    with the ids gt_compress gives the same files (gt_tokenize)."""
+    bufs = [bytes(b) for _, b in files]
+    ptrs = (C.c_void_p * len(bufs))(*[C.cast(C.c_char_p(b), C.c_void_p) for b in bufs])
+    lens = np.asarray([len(b) for b in bufs], dtype=np.uint64)
+    off = np.zeros(len(bufs) + 1, dtype=np.uint64)
+    out = C.c_void_p()
+    L = lib()
+    st = L.gt_tokenize(ptrs, lens.ctypes.data, len(bufs), C.byref(out), off.ctypes.data)
+    if st != 0:
+        raise {1: IngestError, 2: ResourceError}.get(st, UsageError)(L.gt_compress_last_error().decode())
+    try:
+        n = int(off[-1])
+        toks = np.ctypeslib.as_array((C.c_uint32 * max(n, 1)).from_address(out.value))[:n].copy()
+    finally:
+        L.gt_compress_free(out)
+    return toks, off
+
+
+def read_dir(input_dir) -> list[tuple[str, bytes]]:
+    """cli.py:69-82 _ingest_dir order: regular files, lexicographic names."""
+    root = Path(input_dir)
+    if not root.is_dir():
+        raise UsageError(f"{input_dir}: not a directory")
+    names = sorted(p.name for p in root.iterdir() if p.is_file())
+    if not names:
+        raise UsageError(f"{input_dir}: contains no regular files")
+    return [(name, (root / name).read_bytes()) for name in names]
+

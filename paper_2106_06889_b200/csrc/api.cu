@@ -479,6 +479,38 @@ int gt_run_naive(gt_ctx* c, int task, int seq_len, gt_result** out) {
   return GT_OK;
 }
 
+int gt_count_tokens(gt_ctx* c, int task, int seq_len, const uint32_t* tokens, const uint64_t* file_off,
+                    uint64_t nfiles, gt_result** out) {
+  *out = nullptr;
+  gt_result* r = new gt_result();
+  int status = guard([&] {
+    if (task < GT_WORDCOUNT || task > GT_RANKEDINVERTEDINDEX) fail(GT_E_USAGE, "unknown task %d", task);
+    if (task >= GT_SEQCOUNT && seq_len < 1) fail(GT_E_USAGE, "sequence length must be >= 1");
+    DeviceDag& d = c->d;
+    if (nfiles != d.F) fail(GT_E_USAGE, "gt_count_tokens: %lu token streams for %lu files",
+                            (unsigned long)nfiles, (unsigned long)d.F);
+    for (u64 i = 0; i < file_off[nfiles]; i++)
+      if (tokens[i] >= d.nw) fail(GT_E_USAGE, "gt_count_tokens: token %lu is word id %u >= %lu", (unsigned long)i,
+                                  tokens[i], (unsigned long)d.nw);
+    GT_CUDA(cudaSetDevice(d.device));
+    ensure_derived(&d);
+    auto t0 = std::chrono::steady_clock::now();
+    u64 launches0 = g_launches;
+    GT_CUDA(cudaEventRecord(c->ev[0], d.stream));
+    DevRecords R;
+    int wbits = 0;
+    naive_run(&d, task, seq_len, &R, &wbits, tokens, file_off);
+    GT_CUDA(cudaEventRecord(c->ev[1], d.stream));
+    finish(c, r, R, task, seq_len, wbits, GT_AUTO, t0, launches0);
+  });
+  if (status != GT_OK) {
+    delete r;
+    return status;
+  }
+  *out = r;
+  return GT_OK;
+}
+
 int gt_set_files(gt_ctx* c, uint64_t file_lo, uint64_t file_hi) {
   return guard([&] {
     DeviceDag& d = c->d;

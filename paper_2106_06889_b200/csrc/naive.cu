@@ -273,7 +273,8 @@ T rd(const void* p, cudaStream_t st) {
 
 }  // namespace
 
-void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out) {
+void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, const uint32_t* htok,
+               const uint64_t* hoff) {
   cudaStream_t st = d->stream;
   const u64 E = d->E, nw = d->nw, base = d->nw + d->ns, V = d->nw;
   const u32 nseg = (u32)(d->file_hi - d->file_lo);
@@ -283,15 +284,28 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out) {
   const int wbits = std::max(1, bitlen(nw ? nw - 1 : 1));
   if (gram_task && (u64)l * wbits > 63) fail(GT_E_USAGE, "naive sequence counting supports packed grams only");
   *wbits_out = gram_task ? wbits : 0;
+  const bool text = htok != nullptr;  // count given token streams, no expansion
+  std::vector<u64> seg_lo, seg_hi;
   // per-body symbol-length prefixes and root token offsets
-  DBuf len(E * 8 + 8, st), S(E * 8 + 8, st), pre(E * 8 + 8, st);
+  DBuf len, S, pre;
+  std::vector<u64> ftok(nseg + 1), fend(nseg);
+  if (text) {
+    for (u32 f = 0; f < nseg; f++) {
+      ftok[f] = hoff[d->file_lo + f];
+      fend[f] = hoff[d->file_lo + f + 1];
+    }
+  } else {
+  len.alloc(E * 8 + 8, st);
+  S.alloc(E * 8 + 8, st);
+  pre.alloc(E * 8 + 8, st);
   NK(k_sym_len, E, d->body.as<u32>(), E, nw, base, d->exp_len.as<u64>(), len.as<u64>());
   GT_CUDA(cudaMemsetAsync(len.as<u64>() + E, 0, 8, st));
   exclusive_scan_u64(len.as<u64>(), S.as<u64>(), E + 1, st);
   NK(k_body_prefix, E, S.as<u64>(), d->pos_owner.as<u32>(), d->boff.as<u64>(), E, pre.as<u64>());
   len.release();
   S.release();
-  std::vector<u64> seg_lo(d->F), seg_hi(d->F);
+  seg_lo.resize(d->F);
+  seg_hi.resize(d->F);
   GT_CUDA(cudaMemcpyAsync(seg_lo.data(), d->seg_lo.p, d->F * 8, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaMemcpyAsync(seg_hi.data(), d->seg_hi.p, d->F * 8, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
@@ -301,10 +315,10 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out) {
   if (d->L0) GT_CUDA(cudaMemcpyAsync(root_pre.data(), pre.p, d->L0 * 8, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
   root_pre[d->L0] = d->W;
-  std::vector<u64> ftok(nseg + 1), fend(nseg);
   for (u32 f = 0; f < nseg; f++) {
     ftok[f] = root_pre[seg_lo[d->file_lo + f]];
     fend[f] = root_pre[std::min<u64>(seg_hi[d->file_lo + f], d->L0)];
+  }
   }
   const u64 kChunk = 1ull << 29;  // tokens per chunk (4 bytes each)
   DBuf dense;
@@ -338,10 +352,14 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out) {
       GT_CUDA(cudaMemcpyAsync(fendd.p, b.data(), nf * 8, cudaMemcpyHostToDevice, st));
       GT_CUDA(cudaStreamSynchronize(st));
     }
+    DBuf cnt(32, st);
+    if (text) {
+      GT_CUDA(cudaMemcpyAsync(tok.p, htok + t0, ntok * 4, cudaMemcpyHostToDevice, st));
+    } else {
     // expansion of root positions [seg_lo[f0], seg_hi[f1-1])
     const u64 pa = seg_lo[d->file_lo + f0], pb = seg_hi[d->file_lo + f1 - 1];
     const u64 cap = std::max<u64>(pb - pa, 1);
-    DBuf ir(cap * 4, st), io(cap * 8, st), cnt(32, st);
+    DBuf ir(cap * 4, st), io(cap * 8, st);
     GT_CUDA(cudaMemsetAsync(cnt.p, 0, 32, st));
     if (pb > pa)
       NK(k_root_items, pb - pa, d->body.as<u32>(), pa, pb, pre.as<u64>(), t0, nw, base, tok.as<u32>(),
@@ -390,6 +408,7 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out) {
         NK(k_expand_small, nsmalls[k], smalls[k].first.as<u32>(), smalls[k].second.as<u64>(), nsmalls[k],
            d->body.as<u32>(), d->boff.as<u64>(), nw, base, tok.as<u32>());
     smalls.clear();
+    }
     // counting
     DBuf keys, valid;
     u64 nk = ntok;
@@ -457,7 +476,7 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out) {
     rc.clear();
   }
   const int SH = gram_task ? (int)(l * wbits) : WB;
-  const u64 Wt = d->W;
+  const u64 Wt = text ? std::max<u64>(hoff[d->F], 1) : d->W;
   const int CB = std::max(1, bitlen(Wt));
   DBuf idx(n * 4 + 4, st), idx2(n * 4 + 4, st), k1(n * 8 + 8, st), k2(n * 8 + 8, st);
   NK(k_iota32, n, idx.as<u32>(), n);

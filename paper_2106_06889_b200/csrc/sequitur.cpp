@@ -473,4 +473,45 @@ int gt_compress(const uint8_t* const* files, const uint64_t* lens, uint64_t nfil
 
 void gt_compress_free(uint8_t* p) { free(p); }
 
+// The ingest half of gt_compress alone: the corpus as word-id token streams
+// (first-appearance ids — the dictionary order of the grammar gt_compress
+// writes for the same files), one stream per file, no splitters.
+int gt_tokenize(const uint8_t* const* files, const uint64_t* lens, uint64_t nfiles, uint32_t** tokens,
+                uint64_t* file_off) {
+  using namespace gt;
+  *tokens = nullptr;
+  std::unordered_map<std::string_view, uint32_t> ids;
+  std::vector<uint32_t> stream;
+  std::vector<std::string_view> toks;
+  file_off[0] = 0;
+  for (uint64_t f = 0; f < nfiles; f++) {
+    toks.clear();
+    const int64_t bad = tokenize(files[f], lens[f], &toks);
+    if (bad >= 0) {
+      t_seq_err = "file " + std::to_string(f) + ": invalid UTF-8 at byte offset " + std::to_string(bad);
+      return GT_E_USAGE;
+    }
+    for (const auto& t : toks) {
+      auto it = ids.find(t);
+      uint32_t w;
+      if (it == ids.end()) {
+        w = (uint32_t)ids.size();
+        ids.emplace(t, w);
+      } else {
+        w = it->second;
+      }
+      stream.push_back(w);
+    }
+    file_off[f + 1] = stream.size();
+  }
+  uint32_t* p = (uint32_t*)malloc(std::max<size_t>(stream.size(), 1) * 4);
+  if (!p) {
+    t_seq_err = "out of host memory";
+    return GT_E_RESOURCE;
+  }
+  if (!stream.empty()) memcpy(p, stream.data(), stream.size() * 4);
+  *tokens = p;
+  return GT_OK;
+}
+
 }  // extern "C"

@@ -27,7 +27,7 @@ EXPORTS = ("gt_abi_version", "gt_last_error", "gt_open", "gt_info_get", "gt_run"
            "gt_set_files", "gt_assemble_counts", "gt_dict_open", "gt_dict_close", "gt_render_view",
            "gt_free_text", "gt_digest_view", "gt_sha256", "gt_table_add_batch", "gt_run_naive",
            "gt_compress", "gt_compress_free", "gt_compress_last_error", "gt_run_many", "gt_clone",
-           "gt_device_count", "gt_sum_word_counts")
+           "gt_device_count", "gt_sum_word_counts", "gt_count_tokens", "gt_tokenize")
 _lib = None
 
 
@@ -82,6 +82,11 @@ def lib():
         L.gt_device_count.restype = C.c_int
         L.gt_sum_word_counts.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int]
         L.gt_sum_word_counts.restype = C.c_int
+        L.gt_count_tokens.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
+                                      C.POINTER(C.c_void_p)]
+        L.gt_count_tokens.restype = C.c_int
+        L.gt_tokenize.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.c_void_p]
+        L.gt_tokenize.restype = C.c_int
         _lib = L
     return _lib
 
@@ -194,6 +199,22 @@ class DeviceDag:
         L = lib()
         r = C.c_void_p()
         raise_for_status(L.gt_run_naive(self._h, task, seq_len, C.byref(r)), _err())
+        try:
+            v = GtView()
+            L.gt_result_view(r, C.byref(v))
+            return compact_from_view(v)
+        finally:
+            L.gt_result_free(r)
+
+    def count_tokens(self, task: int, seq_len: int, tokens: np.ndarray, file_off: np.ndarray):
+        """gt_count_tokens: the task counted on the given per-file token
+        streams (the plain text), by the device counting stage only."""
+        L = lib()
+        tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+        file_off = np.ascontiguousarray(file_off, dtype=np.uint64)
+        r = C.c_void_p()
+        raise_for_status(L.gt_count_tokens(self._h, task, seq_len, tokens.ctypes.data, file_off.ctypes.data,
+                                           len(file_off) - 1, C.byref(r)), _err())
         try:
             v = GtView()
             L.gt_result_view(r, C.byref(v))

@@ -74,10 +74,50 @@ def test_analyze_out_file_and_verify_and_bench(tmp_path, capsys):
     for task in ("wordcount", "invertedindex", "seqcount"):
         code, out, _ = run_cli(capsys, "verify", p, task)
         assert code == 0 and out.startswith(f"{task}\tok\t")
-    code, out, _ = run_cli(capsys, "bench", p, "wordcount", "--repeat", "2")
+    code, out, _ = run_cli(capsys, "bench", p, "wordcount", "--repeat", "2", "--workers", "2")
     assert code == 0
     rows = dict(line.split("\t") for line in out.splitlines() if not line.startswith("#"))
-    assert {"compressed", "decompress-naive"} <= set(rows)
+    assert {"parallel-compressed", "sequential-compressed", "decompress-naive", "speedup-vs-sequential",
+            "speedup-vs-naive"} <= set(rows)
+
+
+@pytest.mark.gpu
+def test_verify_and_bench_on_an_input_directory(tmp_path, capsys):
+    """The reference's form (cli.py:137-193): a directory of text files,
+    compressed first; verify counts the files' own tokens on the device."""
+    import numpy as np
+    rng = np.random.default_rng(7)
+    d = tmp_path / "corpus"
+    d.mkdir()
+    vocab = [f"w{i}" for i in range(300)] + ["\u00e9t\u00e9", "na\u00efve"]
+    for f in range(6):
+        ids = np.minimum(rng.zipf(1.2, size=900 + 150 * f) - 1, len(vocab) - 1)
+        (d / f"doc{f}.txt").write_text(" ".join(vocab[i] for i in ids) + ("\n" if f % 2 else ""))
+    (d / "empty.txt").write_text("")
+    for task in ("wordcount", "sort", "invertedindex", "termvector", "seqcount", "rankedinvertedindex"):
+        for l in ((2, 4) if task in ("seqcount", "rankedinvertedindex") else (3,)):
+            code, out, _ = run_cli(capsys, "verify", d, task, "--l", l)
+            assert code == 0 and out.startswith(f"{task}\tok\t"), (task, l)
+    code, out, _ = run_cli(capsys, "bench", d, "invertedindex", "--repeat", "1")
+    assert code == 0 and "decompress-naive" in out
+
+
+@pytest.mark.gpu
+def test_count_tokens_matches_the_compressed_path():
+    """gt_count_tokens on the files' token streams == every task's compressed
+    result on the grammar of the same files."""
+    import paper_2106_06889_b200 as gt
+    from paper_2106_06889_b200._abi import TASK_IDS
+    from paper_2106_06889_b200.compress import compress_files, tokenize_files
+    from test_shard_cpu import same_compact
+    files = [("a.txt", b"a b a b c d a b"), ("b.txt", b"a b c"), ("c.txt", b""), ("d.txt", b"d d d c a b a b")]
+    blob, _ = compress_files(files)
+    toks, off = tokenize_files(files)
+    assert off.tolist() == [0, 8, 11, 11, 19]
+    with gt.DeviceDag(blob) as dag:
+        for task in ("wordcount", "sort", "invertedindex", "termvector", "seqcount", "rankedinvertedindex"):
+            for l in (1, 2, 3):
+                same_compact(dag.count_tokens(TASK_IDS[task], l, toks, off), gt.run_compact(dag, task, gt.TraversalConfig(), l))
 
 
 def test_compress_command_matches_reference_bytes(tmp_path, capsys):
@@ -98,6 +138,18 @@ def test_compress_empty_dir_usage_error(tmp_path, capsys):
     empty.mkdir()
     code, _, err = run_cli(capsys, "compress", empty, tmp_path / "x.gtdc")
     assert code == 1 and "no regular files" in err
+
+
+def test_tokenize_gives_the_compressor_word_ids():
+    """gt_tokenize's ids are the dictionary order of the GTDC gt_compress
+    writes (first appearance), one stream per file, no splitters."""
+    from paper_2106_06889_b200.compress import compress_files, tokenize_files
+    from paper_2106_06889_b200.gtdc import read_dictionary
+    files = [("A.txt", b"a b a b c"), ("B.txt", b"  a b\n c  x ")]
+    toks, off = tokenize_files(files)
+    words = read_dictionary(compress_files(files)[0]).words
+    assert [words[i] for i in toks.tolist()] == ["a", "b", "a", "b", "c", "a", "b", "c", "x"]
+    assert off.tolist() == [0, 5, 9]
 
 
 def test_compress_invalid_utf8_ingest_error(tmp_path, capsys):
