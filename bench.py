@@ -292,7 +292,11 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": W / t, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"whole {args.config} corpus, {args.steps} steps of wordcount+invertedindex "
                                    f"after {args.warmup} warm-up steps"},
-        "e2e": {"value": W / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # the contract's reference-arm e2e: the line's own value and unit
+        "e2e": {"value": W / t, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # (the reference algorithm end to end from the GTDC bytes: load +
+        # build_dag + both tasks, once — the counterpart of our e2e)
+        "e2e_incl_build": {"value": W / e2e_s, "unit": UNIT},
         "init_ms": init_s * 1e3,
         "reference_numba": reference_numba_note(),
     }

@@ -11,6 +11,7 @@ TAG=${1:-prof}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$OUT/gpu.txt" 2>&1
+cp paper_2106_06889_b200/_build/stamp "$OUT/stamp.txt" 2>/dev/null
 timeout 400 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
@@ -20,4 +21,6 @@ timeout 400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_segred1?_levels" -s 8 -c 2 \
   -o "$OUT/full" python bench.py --steps 1 --warmup 3 --no-cpu-baseline > "$OUT/full.log" 2>&1
 timeout 900 python tools/gpu_probe.py c2 c3 c4 c5 --pinned --reps 2 > "$OUT/probe.txt" 2>&1
+GT_TRACE=2 timeout 300 python tools/step_probe.py c2 --reps 4 > "$OUT/step_phases.txt" 2>&1
+GT_TRACE=2 timeout 300 python tools/gpu_probe.py c2 c5 --pinned --tasks wordcount --reps 1 > "$OUT/open_trace.txt" 2>&1
 echo done
