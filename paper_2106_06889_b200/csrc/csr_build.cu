@@ -99,7 +99,7 @@ __device__ __forceinline__ void short_rule(const u32* __restrict__ body, u64 b, 
 // (lflag: 1 = segmented sort, 2 = giant)
 __global__ void k_rules_short(const u32* __restrict__ body, const u64* __restrict__ boff, u64 R, u64 nw, u64 base,
                               u32* tsym, u32* tcnt, u32* n_own, u32* n_sub, u64* own_tok, u64* num_out,
-                              uint8_t* lflag) {
+                              uint8_t* lflag, u32* nlong) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
     const u64 b = boff[r], len = boff[r + 1] - b;
@@ -120,6 +120,7 @@ __global__ void k_rules_short(const u32* __restrict__ body, const u64* __restric
       // place and without keys to gather: it is the one long body of a
       // Sequitur grammar
       f = r == 0 ? 3 : (len > kGiant ? 2 : 1);
+      if (f != 3 && nlong) atomicAdd(nlong, 1u);
     }
     lflag[r] = f;
     n_own[r] = o.no;
@@ -267,6 +268,22 @@ __global__ void k_widen_u32(const u32* a, u64 n, u64* b) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) b[i] = i < n ? a[i] : 0;
 }
 
+// both per-rule counts in one u64 (own | sub << 32): one scan gives both CSR
+// offset arrays (every sum < 2^31 on this path)
+__global__ void k_pack_counts(const u32* __restrict__ a, const u32* __restrict__ b, u64 R, u64* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= R; i += stride)
+    out[i] = i < R ? ((u64)a[i] | ((u64)b[i] << 32)) : 0ull;
+}
+
+__global__ void k_split_offsets(const u64* __restrict__ x, u64 n, u64* own_off, u64* sub_off) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    own_off[i] = x[i] & 0xFFFFFFFFull;
+    sub_off[i] = x[i] >> 32;
+  }
+}
+
 // element-parallel compaction of the in-place runs into the CSR arrays
 __global__ void k_rules_compact(const u32* __restrict__ owner, const u64* __restrict__ boff, u64 E,
                                 const u32* __restrict__ n_own, const u32* __restrict__ n_sub,
@@ -297,7 +314,67 @@ __global__ void k_rules_compact(const u32* __restrict__ owner, const u64* __rest
 // the root's body length, known on the host before the device DAG is built
 static u64 boff_host_root_len(const DeviceDag* d) { return d->L0; }
 
+// The common shape first, without a host round trip: every body but the
+// root is at most kShort symbols (Sequitur rules; the composed configs),
+// so the only long body is the root, sorted in place and run-length encoded
+// over its L0 positions — no selects over R or E and no count read-back
+// before the offsets.  One read-back then returns the pair totals AND the
+// number of long non-root bodies; when there are any, the caller redoes
+// the build on the general path.
+static bool rule_pairs_root_only(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_rule, cudaStream_t st) {
+  const u64 R = d->R, E = d->E, nw = d->nw, base = d->nw + d->ns, L0 = d->L0;
+  const u32* body = d->body.as<u32>();
+  const u64* boff = d->boff.as<u64>();
+  enum { TSYM, TCNT, NOWN, NSUB, LFLAG, CNT, PACK, PACKS, SBODY, HEAD, HIDX, NSPL, RFIRST };
+  const Carve a(st, {E * 4 + 4, E * 4 + 4, R * 4 + 4, R * 4 + 4, R + 1, 64, (R + 1) * 8, (R + 1) * 8, L0 * 4 + 4,
+                     L0 + 1, L0 * 4 + 4, 8, 8});
+  u32 *tsym = a.at<u32>(TSYM), *tcnt = a.at<u32>(TCNT), *n_own = a.at<u32>(NOWN), *n_sub = a.at<u32>(NSUB);
+  uint8_t* lflag = a.at<uint8_t>(LFLAG);
+  u64* cnt = a.at<u64>(CNT);  // [0] nlong (u32), [2] run heads of the root
+  GT_CUDA(cudaMemsetAsync(cnt, 0, 64, st));
+  d->own_tok.alloc(R * 8, st);
+  d->num_out.alloc(R * 8, st);
+  CK(k_rules_short, R, body, boff, R, nw, base, tsym, tcnt, n_own, n_sub, d->own_tok.as<u64>(),
+     d->num_out.as<u64>(), lflag, reinterpret_cast<u32*>(cnt));
+  if (L0 > kShort) {  // the root: sorted in place, its runs written at offset 0
+    u32* sbody = a.at<u32>(SBODY);
+    sort_keys_u32(body, sbody, L0, std::max(1, bitlen(d->nw + d->ns + R - 1)), st);
+    CK(k_long_heads, L0, owner, lflag, boff, sbody, L0, a.at<uint8_t>(HEAD));
+    select_flagged_index(a.at<uint8_t>(HEAD), a.at<u32>(HIDX), cnt + 2, L0, st);
+    GT_CUDA(cudaMemsetAsync(a.at<u32>(NSPL), 0, 8, st));
+    CK(k_long_count, L0, a.at<u32>(HIDX), cnt + 2, owner, boff, sbody, nw, base, n_own, n_sub, a.at<u32>(NSPL),
+       d->own_tok.as<u64>(), d->num_out.as<u64>(), a.at<u32>(RFIRST));
+    CK(k_long_write, L0, a.at<u32>(HIDX), cnt + 2, owner, boff, sbody, nw, base, a.at<u32>(NSPL),
+       a.at<u32>(RFIRST), tsym, tcnt);
+  }
+  CK(k_pack_counts, R + 1, n_own, n_sub, R, a.at<u64>(PACK));
+  exclusive_scan_u64(a.at<u64>(PACK), a.at<u64>(PACKS), R + 1, st);
+  u64 h[2];
+  GT_CUDA(cudaMemcpyAsync(&h[0], a.at<u64>(PACKS) + R, 8, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(&h[1], cnt, 8, cudaMemcpyDeviceToHost, st));
+  stream_sync(st);
+  if ((u32)h[1] != 0) return false;  // long non-root bodies: the general path
+  d->own_off.alloc((R + 1) * 8, st);
+  d->sub_off.alloc((R + 1) * 8, st);
+  CK(k_split_offsets, R + 1, a.at<u64>(PACKS), R + 1, d->own_off.as<u64>(), d->sub_off.as<u64>());
+  d->E_own = h[0] & 0xFFFFFFFFull;
+  d->E_sub = h[0] >> 32;
+  const u64 Eo = d->E_own, Es = d->E_sub;
+  d->own_ids.alloc(Eo * 4 + 4, st);
+  d->own_freqs.alloc(Eo * 4 + 4, st);
+  own_rule.alloc(Eo * 4 + 4, st);
+  d->sub_ids.alloc(Es * 4 + 4, st);
+  d->sub_freqs.alloc(Es * 4 + 4, st);
+  sub_rule.alloc(Es * 4 + 4, st);
+  CK(k_rules_compact, E, owner, boff, E, n_own, n_sub, d->own_off.as<u64>(), d->sub_off.as<u64>(), tsym, tcnt,
+     d->own_ids.as<u32>(), d->own_freqs.as<u32>(), own_rule.as<u32>(), d->sub_ids.as<u32>(),
+     d->sub_freqs.as<u32>(), sub_rule.as<u32>());
+  return true;
+}
+
 void build_rule_pairs(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_rule, cudaStream_t st) {
+  static const bool nospec = getenv("GT_CSR_GENERAL") != nullptr;  // diagnostics: always the general path
+  if (!nospec && (u64)d->E < (1ull << 31) && rule_pairs_root_only(d, owner, own_rule, sub_rule, st)) return;
   const u64 R = d->R, E = d->E, nw = d->nw, base = d->nw + d->ns;
   const u32* body = d->body.as<u32>();
   const u64* boff = d->boff.as<u64>();
@@ -311,7 +388,7 @@ void build_rule_pairs(DeviceDag* d, const u32* owner, DBuf& own_rule, DBuf& sub_
   d->own_tok.alloc(R * 8, st);
   d->num_out.alloc(R * 8, st);
   CK(k_rules_short, R, body, boff, R, nw, base, tsym, tcnt, n_own, n_sub, d->own_tok.as<u64>(),
-     d->num_out.as<u64>(), lflag);
+     d->num_out.as<u64>(), lflag, (u32*)nullptr);
   // the longer bodies: one host round trip for their number and size
   CK(k_eq_u8, R, lflag, R, (uint8_t)1, a.at<uint8_t>(MEDF));
   select_flagged_index(a.at<uint8_t>(MEDF), a.at<u32>(LIDS), cnt, R, st);

@@ -1344,23 +1344,36 @@ __global__ void k_cursor(const u32* __restrict__ degt, const u32* __restrict__ i
   for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) cur[t] = incl[t] - degt[t];
 }
 
+// (one 12-byte record per edge: a random slot costs one write sector, not
+// three — the separate arrays come from one coalesced unpack afterwards;
+// C5: 3.2 ms with three scattered 4-byte stores per edge)
 __global__ void k_te_scatter(const u32* __restrict__ prule, const u32* __restrict__ child,
                              const u32* __restrict__ freq, u64 n, const u32* __restrict__ tid, u32* cur,
-                             u32* te_child, u32* te_par, u32* te_freq) {
+                             U3* te) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const u32 p = prule[i];
     if (p == 0) continue;
     const u32 tc = tid[child[i]];
     const u32 slot = atomicAdd(&cur[tc], 1u);
-    te_child[slot] = tc;
-    te_par[slot] = tid[p];
-    te_freq[slot] = freq[i];
+    te[slot] = U3{tc, tid[p], freq[i]};
   }
 }
 
 // level offsets of the td edge lists: off[L] = first edge whose child is in
 // level >= L (ls[L] = first tid of level >= L, L = 0..nl+1), off[nl+2] = all
+// k_unpack3 over the first *n_dev records (the count stays on the device)
+__global__ void k_unpack3_n(const U3* __restrict__ in, const u32* __restrict__ n_dev, u32* a, u32* b, u32* c) {
+  const u64 n = *n_dev;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const U3 v = in[i];
+    a[i] = v.a;
+    b[i] = v.b;
+    c[i] = v.c;
+  }
+}
+
 __global__ void k_te_level_off(const u64* __restrict__ ls, const u32* __restrict__ incl,
                                const u32* __restrict__ degt, u64 R, u64 nl, u64* off) {
   const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2129,32 +2142,6 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
       stream_release(d->device, s);
     }
   } own_guard{s_own, st, d};
-  {
-    cudaEvent_t ev;
-    GT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    GT_CUDA(cudaEventRecord(ev, st));
-    GT_CUDA(cudaStreamWaitEvent(s_own, ev, 0));
-    cudaEventDestroy(ev);
-  }
-    {
-    cudaStream_t st = s_own;
-    // (rule, freq) travel with the word keys through the radix sort: no
-    // permutation gather afterwards
-    DBuf v1(Eo * 8 + 8, st), v2(Eo * 8 + 8, st);
-    d->ow_word.alloc(Eo * 4 + 4, st);
-    d->ow_rule.alloc(Eo * 4 + 4, st);
-    d->ow_freq.alloc(Eo * 4 + 4, st);
-    d->ow_off.alloc((nw + 1) * 8, st);
-    LAUNCH(k_pack2, Eo, own_rule.as<u32>(), d->own_freqs.as<u32>(), Eo, v1.as<u64>());
-    sort_pairs_u32_u64(d->own_ids.as<u32>(), d->ow_word.as<u32>(), v1.as<u64>(), v2.as<u64>(), Eo,
-                       std::max(1, bitlen(nw ? nw - 1 : 0)), st);
-    LAUNCH(k_unpack2, Eo, v2.as<u64>(), Eo, d->ow_rule.as<u32>(), d->ow_freq.as<u32>());
-    if (Eo * 4 >= nw)  // dense keys: one coalesced pass; sparse: a search per row
-      LAUNCH(k_csr_offsets_lin, Eo + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
-    else
-      LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
-  }
-
   // ---- in-degrees straight from the sub pairs ------------------------------
   // (no parent sort on the critical path: the top-down edge lists are
   // scattered from the sub pairs below, and dag.py's parent CSR and
@@ -2260,6 +2247,35 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // (grammar.py:127-161 order: cycles before unreachable rules, dag.py:173-184)
   u64 processed = 0;
   kahn(rem_td, d->sub_off, d->sub_ids, d->td_level);
+  // the word-major own transpose on the side stream, queued behind the
+  // layering (which fills every SM: side kernels queued before it only
+  // delay its start) so it overlaps the host check and the edge lists below
+  {
+    cudaEvent_t ev;
+    GT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    GT_CUDA(cudaEventRecord(ev, st));
+    GT_CUDA(cudaStreamWaitEvent(s_own, ev, 0));
+    cudaEventDestroy(ev);
+  }
+    {
+    cudaStream_t st = s_own;
+    // (rule, freq) travel with the word keys through the radix sort: no
+    // permutation gather afterwards
+    DBuf v1(Eo * 8 + 8, st), v2(Eo * 8 + 8, st);
+    d->ow_word.alloc(Eo * 4 + 4, st);
+    d->ow_rule.alloc(Eo * 4 + 4, st);
+    d->ow_freq.alloc(Eo * 4 + 4, st);
+    d->ow_off.alloc((nw + 1) * 8, st);
+    LAUNCH(k_pack2, Eo, own_rule.as<u32>(), d->own_freqs.as<u32>(), Eo, v1.as<u64>());
+    sort_pairs_u32_u64(d->own_ids.as<u32>(), d->ow_word.as<u32>(), v1.as<u64>(), v2.as<u64>(), Eo,
+                       std::max(1, bitlen(nw ? nw - 1 : 0)), st);
+    LAUNCH(k_unpack2, Eo, v2.as<u64>(), Eo, d->ow_rule.as<u32>(), d->ow_freq.as<u32>());
+    if (Eo * 4 >= nw)  // dense keys: one coalesced pass; sparse: a search per row
+      LAUNCH(k_csr_offsets_lin, Eo + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
+    else
+      LAUNCH(k_csr_offsets, nw + 1, d->ow_word.as<u32>(), Eo, nw, d->ow_off.as<u64>());
+  }
+
   // every rule but the root must be layered, and no reachable rule (nor the
   // root itself) may reference the root: either way there is a cycle; then
   // the first unreachable rule.  One host round trip for all three checks.
@@ -2318,8 +2334,14 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     d->te_child.alloc(Es * 4 + 16, st);  // + 16: the TMA-staged level loop copies whole 16-byte words
     d->te_par.alloc(Es * 4 + 16, st);
     d->te_freq.alloc(Es * 4 + 16, st);
-    LAUNCH(k_te_scatter, Es, sub_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), Es,
-           d->tid.as<u32>(), cur, d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>());
+    {
+      DBuf te(Es * 12 + 12, st);
+      LAUNCH(k_te_scatter, Es, sub_rule.as<u32>(), d->sub_ids.as<u32>(), d->sub_freqs.as<u32>(), Es,
+             d->tid.as<u32>(), cur, te.as<U3>());
+      // (slots past the non-root edges stay unwritten: unpack only E_td)
+      LAUNCH(k_unpack3_n, Es, te.as<U3>(), incl + (R - 1), d->te_child.as<u32>(), d->te_par.as<u32>(),
+             d->te_freq.as<u32>());
+    }
     d->te_off_dev.alloc(((u64)ntd + 3) * 8, st);
     LAUNCH(k_te_level_off, (u64)ntd + 3, ls, incl, degt, R, (u64)ntd, d->te_off_dev.as<u64>());
     GT_CUDA(cudaMemcpyAsync(stage, d->te_off_dev.p, ((u64)ntd + 3) * 8, cudaMemcpyDeviceToHost, st));

@@ -81,3 +81,18 @@ def test_unknown_task_and_bad_seq_len(gt):
             gt.run_task(dag, "frequencies", gt.TraversalConfig())
         with pytest.raises(gt.UsageError):
             gt.run_task(dag, "seqcount", gt.TraversalConfig(), 0)
+
+
+def test_general_csr_path_matches_reference():
+    """gt_open builds the own/sub CSR on the root-only fast path when no
+    other body is longer than 32 symbols and redoes it on the general path
+    otherwise; GT_CSR_GENERAL=1 forces the general path for every grammar
+    (read once per process: a subprocess) — every Dag array still equal."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, GT_CSR_GENERAL="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-x", "-q", "-p", "no:cacheprovider",
+                        "-k", "test_device_dag_matches_reference"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
