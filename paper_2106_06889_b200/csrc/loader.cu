@@ -2246,7 +2246,9 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // a reference cycle, so an incomplete layering is the cycle check
   // (grammar.py:127-161 order: cycles before unreachable rules, dag.py:173-184)
   u64 processed = 0;
+  ph.mark("layering setup");
   kahn(rem_td, d->sub_off, d->sub_ids, d->td_level);
+  ph.mark("layering kernel");
   // the word-major own transpose on the side stream, queued behind the
   // layering (which fills every SM: side kernels queued before it only
   // delay its start) so it overlaps the host check and the edge lists below
