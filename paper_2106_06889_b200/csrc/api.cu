@@ -515,8 +515,7 @@ int gt_set_files(gt_ctx* c, uint64_t file_lo, uint64_t file_hi) {
   return guard([&] {
     DeviceDag& d = c->d;
     if (file_lo > file_hi) fail(GT_E_USAGE, "file range [%lu, %lu) is empty-reversed", (unsigned long)file_lo, (unsigned long)file_hi);
-    d.file_lo = std::min<u64>(file_lo, d.F);
-    d.file_hi = std::min<u64>(file_hi, d.F);
+    set_file_range(&d, file_lo, file_hi);
   });
 }
 

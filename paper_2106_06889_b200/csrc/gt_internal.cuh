@@ -164,6 +164,14 @@ struct DeviceDag {
   DBuf be_rule, be_child, be_freq;
   std::vector<u64> be_off;  // host: bu level L items [be_off[L], be_off[L+1])
   DBuf be_off_dev;
+  // root occurrence lists of the whole corpus while a file-range shard is
+  // set (gt_set_files keeps only the shard's entries in rs_* / rw_*, so its
+  // seeds and root words cost O(shard), not O(corpus))
+  struct RootLists {
+    DBuf rs_rule, rs_rule_t, rs_seg, rs_cnt, rs_off, rw_word, rw_seg, rw_cnt;
+    u64 n_rs = 0, n_rw = 0;
+    bool saved = false;
+  } full;
   DBuf sub_rule;       // u32[E_sub]: the rule of every sub pair (lazy builds)
   // derived arrays (ensure_derived): no top-down word count / inverted
   // index reads them, so gt_open leaves them to the first task that does
@@ -199,6 +207,7 @@ void build_device_dag(const uint8_t* blob, size_t n, int device, u64 file_lo, u6
 void ensure_bu_levels(DeviceDag* d);
 void ensure_parents(DeviceDag* d);  // par_* and num_in (built on first request)
 void ensure_derived(DeviceDag* d);  // see DeviceDag::derived
+void set_file_range(DeviceDag* d, u64 lo, u64 hi);  // gt_set_files
 // replicate a loaded DAG onto `device` (peer copies over NVLink)
 void clone_device_dag(const DeviceDag& src, int device, DeviceDag* d);
 void enable_peer(int a, int b);  // device a may read device b's memory (when supported)

@@ -2380,6 +2380,89 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   d->init_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// entries of (seg) lists inside [lo, lo + n)
+__global__ void k_flag_seg_range(const u32* __restrict__ seg, u64 m, u32 lo, u32 n, uint8_t* f) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) f[i] = seg[i] - lo < n;
+}
+
+__global__ void k_gather4(const u32* __restrict__ idx, const u64* __restrict__ n_dev, const u32* a, const u32* b,
+                          const u32* c, const u32* e, u32* oa, u32* ob, u32* oc, u32* oe) {
+  const u64 n = *n_dev;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 j = idx[i];
+    oa[i] = a[j];
+    ob[i] = b[j];
+    oc[i] = c[j];
+    if (e) oe[i] = e[j];
+  }
+}
+
+// gt_set_files: the owned file range, and the root occurrence lists cut to
+// it (the whole-corpus lists are kept aside in d->full and restored when
+// the range covers every file again)
+void set_file_range(DeviceDag* d, u64 lo, u64 hi) {
+  lo = std::min(lo, d->F);
+  hi = std::min(hi, d->F);
+  if (hi < lo) hi = lo;
+  d->file_lo = lo;
+  d->file_hi = hi;
+  GT_CUDA(cudaSetDevice(d->device));
+  cudaStream_t st = d->stream;
+  auto& f = d->full;
+  const bool whole = lo == 0 && hi == d->F;
+  if (whole) {
+    if (f.saved) {
+      d->rs_rule = std::move(f.rs_rule), d->rs_rule_t = std::move(f.rs_rule_t), d->rs_seg = std::move(f.rs_seg);
+      d->rs_cnt = std::move(f.rs_cnt), d->rs_off = std::move(f.rs_off);
+      d->rw_word = std::move(f.rw_word), d->rw_seg = std::move(f.rw_seg), d->rw_cnt = std::move(f.rw_cnt);
+      d->n_rs = f.n_rs, d->n_rw = f.n_rw;
+      f.saved = false;
+    }
+    return;
+  }
+  if (!f.saved) {
+    f.rs_rule = std::move(d->rs_rule), f.rs_rule_t = std::move(d->rs_rule_t), f.rs_seg = std::move(d->rs_seg);
+    f.rs_cnt = std::move(d->rs_cnt), f.rs_off = std::move(d->rs_off);
+    f.rw_word = std::move(d->rw_word), f.rw_seg = std::move(d->rw_seg), f.rw_cnt = std::move(d->rw_cnt);
+    f.n_rs = d->n_rs, f.n_rw = d->n_rw;
+    f.saved = true;
+  }
+  const u32 l32 = (u32)lo, n32 = (u32)(hi - lo);
+  const u64 m = std::max(f.n_rs, f.n_rw);
+  DBuf flag(m + 1, st), idx(m * 4 + 4, st), cnt(16, st);
+  u64 h[2] = {0, 0};
+  if (f.n_rs) {
+    LAUNCH(k_flag_seg_range, f.n_rs, f.rs_seg.as<u32>(), f.n_rs, l32, n32, flag.as<uint8_t>());
+    select_flagged_index(flag.as<uint8_t>(), idx.as<u32>(), cnt.as<u64>(), f.n_rs, st);
+    GT_CUDA(cudaMemcpyAsync(&h[0], cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    stream_sync(st);
+    const u64 n = h[0];
+    d->rs_rule.alloc(n * 4 + 4, st), d->rs_rule_t.alloc(n * 4 + 4, st), d->rs_seg.alloc(n * 4 + 4, st);
+    d->rs_cnt.alloc(n * 4 + 4, st);
+    LAUNCH(k_gather4, n, idx.as<u32>(), cnt.as<u64>(), f.rs_rule.as<u32>(), f.rs_seg.as<u32>(), f.rs_cnt.as<u32>(),
+           f.rs_rule_t.as<u32>(), d->rs_rule.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(),
+           d->rs_rule_t.as<u32>());
+    d->rs_off.alloc((d->R + 1) * 8, st);
+    LAUNCH(k_csr_offsets, d->R + 1, d->rs_rule.as<u32>(), n, d->R, d->rs_off.as<u64>());
+    d->n_rs = n;
+  }
+  if (f.n_rw) {
+    LAUNCH(k_flag_seg_range, f.n_rw, f.rw_seg.as<u32>(), f.n_rw, l32, n32, flag.as<uint8_t>());
+    select_flagged_index(flag.as<uint8_t>(), idx.as<u32>(), cnt.as<u64>() + 1, f.n_rw, st);
+    GT_CUDA(cudaMemcpyAsync(&h[1], cnt.as<u64>() + 1, 8, cudaMemcpyDeviceToHost, st));
+    stream_sync(st);
+    const u64 n = h[1];
+    d->rw_word.alloc(n * 4 + 4, st), d->rw_seg.alloc(n * 4 + 4, st), d->rw_cnt.alloc(n * 4 + 4, st);
+    LAUNCH(k_gather4, n, idx.as<u32>(), cnt.as<u64>() + 1, f.rw_word.as<u32>(), f.rw_seg.as<u32>(),
+           f.rw_cnt.as<u32>(), (const u32*)nullptr, d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(),
+           (u32*)nullptr);
+    d->n_rw = n;
+  }
+  stream_sync(st);
+}
+
 // ---------------------------------------------------------------------------
 // Replication of a loaded DAG onto another device (the DAG is
 // built once and broadcast to the other GPUs over NVLink instead of N host
@@ -2437,6 +2520,12 @@ void clone_device_dag(const DeviceDag& s, int device, DeviceDag* d) {
                  &d->te_freq, &d->te_off_dev, &d->be_rule, &d->be_child, &d->be_freq, &d->be_off_dev, &d->sub_rule};
   static_assert(sizeof(src) / sizeof(src[0]) == sizeof(dst) / sizeof(dst[0]), "clone lists");
   for (size_t i = 0; i < sizeof(src) / sizeof(src[0]); i++) cp(*src[i], *dst[i]);
+  if (s.full.saved) {  // the source is a shard: the whole-corpus lists travel too
+    cp(s.full.rs_rule, d->full.rs_rule), cp(s.full.rs_rule_t, d->full.rs_rule_t), cp(s.full.rs_seg, d->full.rs_seg);
+    cp(s.full.rs_cnt, d->full.rs_cnt), cp(s.full.rs_off, d->full.rs_off), cp(s.full.rw_word, d->full.rw_word);
+    cp(s.full.rw_seg, d->full.rw_seg), cp(s.full.rw_cnt, d->full.rw_cnt);
+    d->full.n_rs = s.full.n_rs, d->full.n_rw = s.full.n_rw, d->full.saved = true;
+  }
   d->nw = s.nw, d->ns = s.ns, d->R = s.R, d->E = s.E, d->F = s.F, d->L0 = s.L0, d->W = s.W;
   d->file_lo = s.file_lo, d->file_hi = s.file_hi, d->depth = s.depth;
   d->E_own = s.E_own, d->E_sub = s.E_sub, d->n_rs = s.n_rs, d->n_rw = s.n_rw;
