@@ -650,6 +650,9 @@ struct KahnCtl {
   u64 layers;
   u64 t[64];     // %globaltimer at the start of layers 1..63 (GT_TRACE=2 prints them)
   u64 bar;       // k_kahn3's layer barrier: arrivals (bits 0-31), active blocks of even / odd layers (32-47 / 48-63)
+  u32 root_cycle;       // k_kahn3's fused checks: a reachable rule (or the root) references the root
+  u32 first_unreached;  // smallest rule >= 1 not reachable from the root (0xFFFFFFFF: none)
+  u32 checked;          // the fused checks ran
 };
 
 __device__ __forceinline__ u64 globaltimer() {
@@ -1076,7 +1079,11 @@ __global__ void __launch_bounds__(kKahnBlock) k_kahn3(KahnCtl* ctl, const u64* _
   const bool resident = !gmode && kK3List + 2 * nr + 1 + (ee - eb) <= kK3WarpWords;
   u32* cnt = gmode ? rem + r0 : s_cnt;
   u32* delta[2] = {gmode ? gdelta0 : rem, delta1};  // smem mode: rem doubles as delta[0]
-  if (gtid == 0) ctl->t[0] = globaltimer();
+  if (gtid == 0) {
+    ctl->t[0] = globaltimer();
+    ctl->first_unreached = 0xFFFFFFFFu;
+    ctl->checked = 1;
+  }
   // prologue: 8 loads per lane in flight per step (the copies are tiny but
   // each dependent load -> store step costs a full L2 round trip)
   const u32 nr32 = (u32)nr, ne32 = (u32)(ee - eb);
@@ -1250,6 +1257,32 @@ __global__ void __launch_bounds__(kKahnBlock) k_kahn3(KahnCtl* ctl, const u64* _
       s_prev[L & 1] = f;
     }
     __syncthreads();
+  }
+  // fused checks (every reach byte is final after the last barrier): the
+  // first unreachable rule, and a reachable rule (or the root) referencing
+  // the root — replaces two launches and their host round trip
+  {
+    u32 minr = 0xFFFFFFFFu;
+    bool cyc = false;
+    for (u32 s0 = 0; s0 < nr32; s0 += 32) {  // warp-uniform trip count
+      const u32 slot = s0 + lane;
+      const u64 r = r0 + slot;
+      const bool ok = slot < nr32;
+      const bool rr = ok && (r == 0 || rv[r] != 0);
+      if (ok && !rr) minr = min(minr, (u32)r);
+      // child lists ascend, so only a rule's first child can be the root
+      if (rr) {
+        if (resident) cyc |= s_off[slot + 1] > s_off[slot] && s_ids[s_off[slot]] == 0;
+        else cyc |= off[r + 1] > off[r] && ids[off[r]] == 0;
+      }
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) minr = min(minr, __shfl_xor_sync(0xFFFFFFFFu, minr, d));
+    cyc = __any_sync(0xFFFFFFFFu, cyc);
+    if (lane == 0) {
+      if (minr != 0xFFFFFFFFu) atomicMin(&ctl->first_unreached, minr);
+      if (cyc) ctl->root_cycle = 1;
+    }
   }
   block_add_u64(found, &ctl->processed);
   if (gtid == 0) ctl->layers = L - 2;  // L - 1 was the first empty layer
@@ -2174,6 +2207,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   DBuf tasks(ntask_max * 8, st), ctl_b(sizeof(KahnCtl), st);
   KahnCtl* ctl = ctl_b.as<KahnCtl>();
   DBuf reach(R, st);
+  bool kahn_checks_fused = false;  // k_kahn3 computes the reachability / root-cycle checks itself
   auto kahn = [&](DBuf& rem, const DBuf& off, const DBuf& ids, DBuf& lvl) {
     const u64 nwords = (R + 31) / 32;
     int nsm = 148;
@@ -2198,6 +2232,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     u32* lv = lvl.as<u32>();
     u64 maxl = R + 2;
     if (mode >= 3) {
+      kahn_checks_fused = true;
       static bool attr = false;
       const size_t smem = (size_t)32 * kK3WarpWords * 4;
       u32* gd0 = nullptr;
@@ -2281,17 +2316,25 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // every rule but the root must be layered, and no reachable rule (nor the
   // root itself) may reference the root: either way there is a cycle; then
   // the first unreachable rule.  One host round trip for all three checks.
-  KahnCtl h;
+  static thread_local KahnCtl* hp = nullptr;  // pinned: a pageable read-back is staged by the driver
+  if (!hp) GT_CUDA(cudaMallocHost(&hp, sizeof(KahnCtl)));
+  KahnCtl& h = *hp;
   u32 chk[2];
   {
     DBuf cd(8, st);
-    GT_CUDA(cudaMemsetAsync(cd.p, 0, 4, st));
-    GT_CUDA(cudaMemsetAsync(cd.as<u32>() + 1, 0xFF, 4, st));
-    LAUNCH(k_root_cycle2, Es, sub_rule.as<u32>(), d->sub_ids.as<u32>(), Es, reach.as<uint8_t>(), cd.as<u32>());
-    LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, cd.as<u32>() + 1);
+    if (!kahn_checks_fused) {
+      GT_CUDA(cudaMemsetAsync(cd.p, 0, 4, st));
+      GT_CUDA(cudaMemsetAsync(cd.as<u32>() + 1, 0xFF, 4, st));
+      LAUNCH(k_root_cycle2, Es, sub_rule.as<u32>(), d->sub_ids.as<u32>(), Es, reach.as<uint8_t>(), cd.as<u32>());
+      LAUNCH(k_first_unreached, R, reach.as<uint8_t>(), R, cd.as<u32>() + 1);
+      GT_CUDA(cudaMemcpyAsync(chk, cd.p, 8, cudaMemcpyDeviceToHost, st));
+    }
     GT_CUDA(cudaMemcpyAsync(&h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
-    GT_CUDA(cudaMemcpyAsync(chk, cd.p, 8, cudaMemcpyDeviceToHost, st));
     stream_sync(st);
+    if (kahn_checks_fused) {
+      chk[0] = h.root_cycle;
+      chk[1] = h.first_unreached;
+    }
   }
   processed = h.processed;
   const int ntd = (int)h.layers;
