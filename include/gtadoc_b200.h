@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GT_ABI_VERSION 1
+#define GT_ABI_VERSION 2
 
 /* Status codes.  Exception class (errors.py) and CLI exit code in brackets. */
 enum gt_status {
@@ -132,6 +132,13 @@ typedef struct gt_view {
   double total_ms;  /* wall time of gt_run                                  */
   uint64_t d2h_bytes;
   uint64_t kernel_launches; /* kernels launched by this gt_run              */
+  /* (ABI 2) narrow copies: when every record offset fits 32 bits the group
+   * offsets travel as u32 (group_off == NULL, group_off32 set), and when the
+   * task's counts are bounded below 2^32 (per-file counts: the longest file;
+   * corpus counts: W) so do the counts (count == NULL, count32 set) — a
+   * third less PCIe traffic for the count-carrying results */
+  const uint32_t* count32;
+  const uint32_t* group_off32;
 } gt_view;
 
 int gt_abi_version(void);

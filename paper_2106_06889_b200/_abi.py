@@ -91,6 +91,8 @@ class GtView(C.Structure):
         ("total_ms", C.c_double),
         ("d2h_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint64),
+        ("count32", _P32),      # ABI 2: narrowed copies (count / group_off NULL then)
+        ("group_off32", _P32),
     ]
 
 
@@ -140,14 +142,15 @@ def compact_from_view(v: GtView) -> Compact:
     ng, n, l = int(v.n_groups), int(v.n), int(v.seq_len)
     c = Compact(task=task, seq_len=l, wbits=int(v.wbits), strategy=STRATEGY_NAMES.get(int(v.strategy), "?"),
                 n_groups=ng, n=n)
-    c.group_off = _arr(v.group_off, ng + 1, np.int64) if v.group_off else None
+    c.group_off = (_arr(v.group_off, ng + 1, np.int64) if v.group_off else
+                   _arr(v.group_off32, ng + 1, np.int64) if v.group_off32 else None)
     c.group_id = _arr(v.group_id, ng, np.int64)
     c.group_key = _arr(v.group_key, ng, np.uint64)
     c.group_gram = _arr(v.group_gram, ng * l, np.int64)
     c.id = _arr(v.id, n, np.int64)
     c.key = _arr(v.key, n, np.uint64)
     c.gram = _arr(v.gram, n * l, np.int64)
-    c.count = _arr(v.count, n, np.int64)
+    c.count = _arr(v.count, n, np.int64) if v.count else _arr(v.count32, n, np.int64)
     c.timings = dict(device_ms=v.device_ms, d2h_ms=v.d2h_ms, total_ms=v.total_ms,
                      d2h_bytes=int(v.d2h_bytes), kernel_launches=int(v.kernel_launches))
     return c

@@ -233,9 +233,26 @@ static const T* pull(gt_result* r, const DBuf& b, u64 n, cudaStream_t st, u64* b
   return (const T*)h;
 }
 
+// u64 -> u32 (the caller guarantees every value fits)
+__global__ void k_narrow_u64(const u64* __restrict__ in, u64 n, u32* out) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = (u32)in[i];
+}
+
+// a u64 device array copied to the host as u32 (narrowed on the device; the
+// temporary is freed stream-ordered after the copy)
+static const uint32_t* pull_narrow(gt_result* r, const DBuf& b, u64 n, cudaStream_t st, u64* bytes) {
+  if (!b.p) return nullptr;
+  DBuf t(n * 4 + 4, st);
+  if (n) GT_KLAUNCH("k_narrow_u64", k_narrow_u64, grid_for(n, 256), 256, st, b.as<u64>(), n, t.as<u32>());
+  return pull<uint32_t>(r, t, n, st, bytes);
+}
+
 // enqueue the D2H copies of a result's compact arrays into pinned blocks the
-// gt_result owns; returns the bytes
-static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int wbits, int strat, cudaStream_t st) {
+// gt_result owns; returns the bytes.  count_bound: an upper bound of every
+// count (0: unknown) — below 2^32 the counts travel as u32
+static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int wbits, int strat, cudaStream_t st,
+                        u64 count_bound = 0) {
   u64 bytes = 0;
   gt_view& v = r->v;
   v.task = task;
@@ -245,22 +262,34 @@ static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int 
   v.n = R.n;
   v.n_groups = R.n_groups;
   const u64 l = (u64)seq_len;
-  v.group_off = pull<uint64_t>(r, R.group_off, R.n_groups + 1, st, &bytes);
+  static const bool wide = getenv("GT_D2H_U64") != nullptr;  // diagnostics: always u64 counts / offsets
+  if (!wide && R.n < (1ull << 32)) v.group_off32 = pull_narrow(r, R.group_off, R.n_groups + 1, st, &bytes);
+  else v.group_off = pull<uint64_t>(r, R.group_off, R.n_groups + 1, st, &bytes);
   v.group_id = pull<uint32_t>(r, R.group_id, R.n_groups, st, &bytes);
   v.group_key = pull<uint64_t>(r, R.group_key, R.n_groups, st, &bytes);
   v.group_gram = pull<uint32_t>(r, R.group_gram, R.n_groups * l, st, &bytes);
   v.id = pull<uint32_t>(r, R.id, R.n, st, &bytes);
   v.key = pull<uint64_t>(r, R.key, R.n, st, &bytes);
   v.gram = pull<uint32_t>(r, R.gram, R.n * l, st, &bytes);
-  v.count = pull<uint64_t>(r, R.count, R.n, st, &bytes);
+  if (!wide && count_bound && count_bound < (1ull << 32)) v.count32 = pull_narrow(r, R.count, R.n, st, &bytes);
+  else v.count = pull<uint64_t>(r, R.count, R.n, st, &bytes);
   v.d2h_bytes = bytes;
   return bytes;
+}
+
+// every count of a task's records is at most the longest owned file's words
+// (per-file tasks) or W (corpus tasks); 0 = not known without the derived
+// arrays
+static u64 count_bound(const DeviceDag& d, int task) {
+  if (!d.derived) return 0;
+  if (task == GT_WORDCOUNT || task == GT_SORT) return std::max<u64>(d.W, 1);
+  return std::max<u64>(d.max_file_tokens, 1);
 }
 
 static void finish(gt_ctx* c, gt_result* r, DevRecords& R, int task, int seq_len, int wbits,
                    int strat, std::chrono::steady_clock::time_point t0, u64 launches0) {
   cudaStream_t st = c->d.stream;
-  pull_records(r, R, task, seq_len, wbits, strat, st);
+  pull_records(r, R, task, seq_len, wbits, strat, st, count_bound(c->d, task));
   gt_view& v = r->v;
   GT_CUDA(cudaEventRecord(c->ev[2], st));
   GT_CUDA(cudaStreamSynchronize(st));
@@ -412,7 +441,7 @@ int gt_run_many(gt_ctx* c, const int* tasks, int ntasks, int seq_len, int strate
           order_by_count(&d, &W, 0, nullptr);
         }
         GT_CUDA(cudaEventRecord(c->ev[1], st));
-        pull_records(rw, W, tasks[iw], seq_len, 0, GT_TOPDOWN, st);
+        pull_records(rw, W, tasks[iw], seq_len, 0, GT_TOPDOWN, st, count_bound(d, tasks[iw]));
         pull_records(ri, I, GT_INVERTEDINDEX, seq_len, 0, GT_TOPDOWN, st);
         GT_CUDA(cudaEventRecord(c->ev[2], st));
         GT_CUDA(cudaStreamSynchronize(st));

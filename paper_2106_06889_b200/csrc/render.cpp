@@ -233,6 +233,9 @@ struct Renderer {
   void word(std::string& s, uint64_t w) const {
     s.append(dict.bytes.data() + dict.off[w], dict.off[w + 1] - dict.off[w]);
   }
+  // counts and group offsets arrive as u64, or narrowed to u32 (ABI 2)
+  uint64_t cnt(uint64_t i) const { return v.count ? v.count[i] : (uint64_t)v.count32[i]; }
+  uint64_t goff(uint64_t g) const { return v.group_off ? v.group_off[g] : (uint64_t)v.group_off32[g]; }
   void gram_of_key(std::string& s, uint64_t key) const {
     const int l = v.seq_len;
     for (int j = 0; j < l; j++) {
@@ -255,14 +258,14 @@ struct Renderer {
         for (uint64_t i = a; i < b; i++) {
           word(s, v.id[i]);
           s.push_back('\t');
-          put_u64(s, v.count[i]);
+          put_u64(s, cnt(i));
           s.push_back('\n');
         }
         break;
       case GT_INVERTEDINDEX:
         for (uint64_t g = a; g < b; g++) {
           word(s, v.group_id[g]);
-          for (uint64_t i = v.group_off[g]; i < v.group_off[g + 1]; i++) {
+          for (uint64_t i = goff(g); i < goff(g + 1); i++) {
             s.push_back('\t');
             put_u64(s, v.id[i]);
           }
@@ -271,24 +274,24 @@ struct Renderer {
         break;
       case GT_TERMVECTOR:
         for (uint64_t f = a; f < b; f++)
-          for (uint64_t i = v.group_off[f]; i < v.group_off[f + 1]; i++) {
+          for (uint64_t i = goff(f); i < goff(f + 1); i++) {
             put_u64(s, f);
             s.push_back('\t');
             word(s, v.id[i]);
             s.push_back('\t');
-            put_u64(s, v.count[i]);
+            put_u64(s, cnt(i));
             s.push_back('\n');
           }
         break;
       case GT_SEQCOUNT:
         for (uint64_t f = a; f < b; f++)
-          for (uint64_t i = v.group_off[f]; i < v.group_off[f + 1]; i++) {
+          for (uint64_t i = goff(f); i < goff(f + 1); i++) {
             put_u64(s, f);
             s.push_back('\t');
             if (v.wbits) gram_of_key(s, v.key[i]);
             else gram_of_words(s, v.gram + i * (uint64_t)v.seq_len);
             s.push_back('\t');
-            put_u64(s, v.count[i]);
+            put_u64(s, cnt(i));
             s.push_back('\n');
           }
         break;
@@ -296,11 +299,11 @@ struct Renderer {
         for (uint64_t g = a; g < b; g++) {
           if (v.wbits) gram_of_key(s, v.group_key[g]);
           else gram_of_words(s, v.group_gram + g * (uint64_t)v.seq_len);
-          for (uint64_t i = v.group_off[g]; i < v.group_off[g + 1]; i++) {
+          for (uint64_t i = goff(g); i < goff(g + 1); i++) {
             s.push_back('\t');
             put_u64(s, v.id[i]);
             s.push_back(':');
-            put_u64(s, v.count[i]);
+            put_u64(s, cnt(i));
           }
           s.push_back('\n');
         }
@@ -316,7 +319,7 @@ struct Renderer {
   // records covered by units [0, u): for balancing chunks by output size
   uint64_t recs_before(uint64_t u) const {
     if (v.task == GT_WORDCOUNT || v.task == GT_SORT) return u;
-    return v.group_off ? v.group_off[u] + u : u;
+    return (v.group_off || v.group_off32) ? goff(u) + u : u;
   }
 };
 
