@@ -329,6 +329,31 @@ __global__ void k_heads_u32v(const u32* g, u64 n, uint8_t* h) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) h[i] = i == 0 || g[i] != g[i - 1];
 }
 
+// RANKEDINVERTEDINDEX on <= 16 owned files: the cells of one gram run
+// (files ascending, at most 16, ~3 on C2) ordered by (-count, file) in place
+// of a corpus-wide radix sort of (run | W - count) keys — a thread per cell
+// finds its run's bounds and its rank (cells of the run with a larger count,
+// or an equal count and a smaller file: files are distinct within a run)
+__global__ void k_rii_rank(const u32* __restrict__ run, u64 n, const u32* __restrict__ col,
+                           const u64* __restrict__ cnt, u32 file_lo, u32* __restrict__ out_id,
+                           u64* __restrict__ out_cnt) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 r = run[i], f = col[i];
+    const u64 c = cnt[i];
+    u64 a = i, b = i + 1;
+    while (a > 0 && run[a - 1] == r) a--;
+    while (b < n && run[b] == r) b++;
+    u64 rank = 0;
+    for (u64 j = a; j < b; j++) {
+      const u64 cj = cnt[j];
+      rank += cj > c || (cj == c && col[j] < f);
+    }
+    out_id[a + rank] = f + file_lo;
+    out_cnt[a + rank] = c;
+  }
+}
+
 __global__ void k_group_out2(const u32* gsel, const u64* ng_p, u64 n, const u32* run, const u32* run_start,
                              const u64* skey_sorted, u64* goff, u64* gkey) {
   const u64 ng = *ng_p;
@@ -581,7 +606,12 @@ int run_sequences(DeviceDag* d, int task, int l_, int mode, DevRecords* Rr, int*
   // the count field of the record sort key spans the largest cell count (one
   // reduction + read-back): C4 39 -> 32-bit keys, one radix pass fewer
   u64 Wt = d->max_file_tokens ? d->max_file_tokens : d->W;
-  if (n && bitlen(Wt) + (task == GT_SEQCOUNT ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns))) > 32) {
+  // RII on <= 16 owned files ranks each run's cells in place (k_rii_rank): no
+  // record keys, no count bound (C2: 0.29 ms of sort -> 0.15 ms; at 64 files
+  // the O(cells^2) ranks cost more than the radix sort: C4 4.2 vs ~2 ms)
+  const bool rii_rank = packed && task != GT_SEQCOUNT && C <= 16;
+  if (!rii_rank && n &&
+      bitlen(Wt) + (task == GT_SEQCOUNT ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns))) > 32) {
     DBuf mx(8, st);
     reduce_max_u64(ccnt.as<u64>(), mx.as<u64>(), n, st);
     Wt = std::max<u64>(1, d2h1<u64>(mx.p, st));
@@ -589,19 +619,23 @@ int run_sequences(DeviceDag* d, int task, int l_, int mode, DevRecords* Rr, int*
   const int CB = std::max(1, bitlen(Wt));
   const bool by_file = task == GT_SEQCOUNT;
   const int MB = by_file ? std::max(1, bitlen(C - 1)) : std::max(1, bitlen(nruns));
-  if (CB + MB > 64) fail(GT_E_RESOURCE, "sort key of %d bits exceeds 64", CB + MB);
+  if (!rii_rank && CB + MB > 64) fail(GT_E_RESOURCE, "sort key of %d bits exceeds 64", CB + MB);
   if (packed) {
     // the sort carries its payload: SEQCOUNT sorts (file | W - count) with the
     // packed gram as the value, RII (run | W - count) with the file — every
     // output field comes out of the sorted arrays, no permutation gathers
     const bool k32 = CB + MB <= 32;
-    DBuf sk(n * 8 + 8, st), sk2(n * 8 + 8, st);
-    if (k32)
-      SL(k_rec_keys2<u32>, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
-         sk.as<u32>());
-    else
-      SL(k_rec_keys2<u64>, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
-         sk.as<u64>());
+    DBuf sk, sk2;
+    if (!rii_rank) {
+      sk.alloc(n * 8 + 8, st);
+      sk2.alloc(n * 8 + 8, st);
+      if (k32)
+        SL(k_rec_keys2<u32>, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
+           sk.as<u32>());
+      else
+        SL(k_rec_keys2<u64>, n, crun.as<u32>(), ccol.as<u32>(), ccnt.as<u64>(), n, Wt, CB, by_file ? 1 : 0,
+           sk.as<u64>());
+    }
     Rr->n = n;
     Rr->count.alloc(n * 8 + 8, st);
     if (by_file) {
@@ -619,6 +653,20 @@ int run_sequences(DeviceDag* d, int task, int l_, int mode, DevRecords* Rr, int*
       Rr->n_groups = Fo;
       Rr->group_off.alloc((Fo + 1) * 8, st);
       SL(k_csr_offsets, Fo + 1, major.as<u32>(), n, (u64)Fo, Rr->group_off.as<u64>());
+    } else if (rii_rank) {
+      // runs of at most 64 cells: ranked in place, no record sort
+      Rr->id.alloc(n * 4 + 4, st);
+      DBuf gh(n + 1, st), gsel(n * 4 + 4, st);
+      SL(k_heads_u32v, n, crun.as<u32>(), n, gh.as<uint8_t>());
+      select_flagged_index(gh.as<uint8_t>(), gsel.as<u32>(), dcnt.as<u64>(), n, st);
+      const u64 ng = d2h1<u64>(dcnt.p, st);
+      SL(k_rii_rank, n, crun.as<u32>(), n, ccol.as<u32>(), ccnt.as<u64>(), (u32)d->file_lo, Rr->id.as<u32>(),
+         Rr->count.as<u64>());
+      Rr->n_groups = ng;
+      Rr->group_off.alloc((ng + 1) * 8, st);
+      Rr->group_key.alloc(ng * 8 + 8, st);
+      SL(k_group_out2, ng + 1, gsel.as<u32>(), dcnt.as<u64>(), n, crun.as<u32>(), runs.as<u32>(),
+         skey.as<u64>(), Rr->group_off.as<u64>(), Rr->group_key.as<u64>());
     } else {
       Rr->id.alloc(n * 4 + 4, st);
       DBuf rn(n * 4 + 4, st), gh(n + 1, st), gsel(n * 4 + 4, st);
