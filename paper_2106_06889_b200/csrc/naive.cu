@@ -175,6 +175,76 @@ __global__ void k_window_keys(const u32* tok, u64 n, const u64* fstart, const u6
   }
 }
 
+// ---- wide grams (64 < l * wbits <= 128): (hi, lo) keys, file sorted apart --
+__device__ __forceinline__ void shl128(u64& hi, u64& lo, int s, u64 v) {  // (hi:lo) = (hi:lo) << s | v
+  hi = s >= 64 ? (lo << (s - 64)) : ((hi << s) | (s ? (lo >> (64 - s)) : 0ull));
+  lo = s >= 64 ? 0ull : (lo << s);
+  lo |= v;
+}
+
+__global__ void k_window_keys_wide(const u32* tok, u64 n, const u64* fstart, const u64* fend, u32 nf, u32 l,
+                                   int wbits, u64* khi, u64* klo, u32* kfile, uint8_t* valid) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 lo = 0, hi = nf;
+    while (hi - lo > 1) {
+      const u32 m = (lo + hi) >> 1;
+      if (fstart[m] <= i) lo = m;
+      else hi = m;
+    }
+    const bool ok = i + l <= fend[lo];
+    u64 gh = 0, gl = 0;
+    if (ok)
+      for (u32 j = 0; j < l; j++) shl128(gh, gl, wbits, tok[i + j]);
+    khi[i] = gh;
+    klo[i] = gl;
+    kfile[i] = lo;
+    valid[i] = ok;
+  }
+}
+
+__global__ void k_heads_wide(const u32* f, const u64* hi, const u64* lo, u64 n, uint8_t* h) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    h[i] = i == 0 || f[i] != f[i - 1] || hi[i] != hi[i - 1] || lo[i] != lo[i - 1];
+}
+
+__global__ void k_heads_wide2(const u64* hi, const u64* lo, u64 n, uint8_t* h) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    h[i] = i == 0 || hi[i] != hi[i - 1] || lo[i] != lo[i - 1];
+}
+
+__global__ void k_runs_wide(const u32* f, const u64* hi, const u64* lo, const u32* hidx, u64 U, u64 n, u32 add_file,
+                            u32* ofile, u64* ohi, u64* olo, u64* ocnt) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < U; u += stride) {
+    const u64 a = hidx[u], b = u + 1 < U ? hidx[u + 1] : n;
+    ofile[u] = f[a] + add_file;
+    ohi[u] = hi[a];
+    olo[u] = lo[a];
+    ocnt[u] = b - a;
+  }
+}
+
+// (hi:lo) of record idx[i] -> its l word ids (big-endian by position)
+__global__ void k_decode_wide(const u32* idx, u64 n, const u64* hi, const u64* lo, u32 l, int wbits, u32* gram) {
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 m = (1ull << wbits) - 1;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 k = idx ? idx[i] : (u32)i;
+    const u64 h = hi[k], o = lo[k];
+    for (u32 j = 0; j < l; j++) {
+      const int sh = (int)(l - 1 - j) * wbits;
+      u64 w;
+      if (sh >= 64) w = h >> (sh - 64);
+      else if (sh + wbits <= 64) w = o >> sh;
+      else w = (o >> sh) | (h << (64 - sh));
+      gram[i * l + j] = (u32)(w & m);
+    }
+  }
+}
+
 __global__ void k_heads64(const u64* k, u64 n, uint8_t* h) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) h[i] = i == 0 || k[i] != k[i - 1];
@@ -282,8 +352,12 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, c
   const int WB = std::max(1, bitlen(nw ? nw - 1 : 0));
   const bool gram_task = task == GT_SEQCOUNT || task == GT_RANKEDINVERTEDINDEX;
   const int wbits = std::max(1, bitlen(nw ? nw - 1 : 1));
-  if (gram_task && (u64)l * wbits > 63) fail(GT_E_USAGE, "naive sequence counting supports packed grams only");
-  *wbits_out = gram_task ? wbits : 0;
+  // grams wider than 63 bits (the compressed path's gram mode) are counted on
+  // 128-bit (hi, lo) keys with the file sorted apart
+  const bool wide = gram_task && (u64)l * wbits > 63;
+  if (gram_task && (u64)l * wbits > 128)
+    fail(GT_E_USAGE, "naive sequence counting supports grams of at most 128 bits (%u words of %d bits)", l, wbits);
+  *wbits_out = gram_task && !wide ? wbits : 0;
   const bool text = htok != nullptr;  // count given token streams, no expansion
   std::vector<u64> seg_lo, seg_hi;
   // per-body symbol-length prefixes and root token offsets
@@ -326,7 +400,7 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, c
     dense.alloc(V * 8 + 8, st);
     GT_CUDA(cudaMemsetAsync(dense.p, 0, V * 8 + 8, st));
   }
-  std::vector<DBuf> rf, rk, rc;  // per-chunk (file, low key, count) records
+  std::vector<DBuf> rf, rk, rc, rh;  // per-chunk (file, low key, count[, high key]) records
   std::vector<u64> rn;
   const int FB = std::max(1, bitlen(nseg ? nseg - 1 : 0));
   u32 f0 = 0;
@@ -334,10 +408,10 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, c
     // files per chunk: bounded by tokens and, for windows, by the key bits
     // left above the packed gram (file bits + l*wbits <= 64)
     u64 max_files = ~0ull;
-    if (gram_task && (u64)l * wbits < 64) {
+    if (gram_task && !wide && (u64)l * wbits < 64) {
       const int free_bits = 64 - (int)(l * wbits);
       max_files = free_bits >= 32 ? ~0ull : (1ull << free_bits);
-    } else if (gram_task) {
+    } else if (gram_task && !wide) {
       max_files = 1;
     }
     u32 f1 = f0 + 1;
@@ -410,6 +484,42 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, c
     smalls.clear();
     }
     // counting
+    if (wide) {
+      // valid windows -> (file, hi, lo) sorted LSD: lo, hi, file (stable radix
+      // passes carrying the window index), then runs
+      const int GB = (int)(l * wbits), FB = std::max(1, bitlen(nf ? nf - 1 : 0));
+      DBuf khi(ntok * 8 + 8, st), klo(ntok * 8 + 8, st), kf(ntok * 4 + 4, st), val(ntok + 1, st);
+      NK(k_window_keys_wide, ntok, tok.as<u32>(), ntok, fstart.as<u64>(), fendd.as<u64>(), nf, l, wbits,
+         khi.as<u64>(), klo.as<u64>(), kf.as<u32>(), val.as<uint8_t>());
+      tok.release();
+      DBuf p0(ntok * 4 + 4, st), p1(ntok * 4 + 4, st), a(ntok * 8 + 8, st), b(ntok * 8 + 8, st);
+      select_flagged_index(val.as<uint8_t>(), p0.as<u32>(), cnt.as<u64>(), ntok, st);
+      const u64 nk = rd<u64>(cnt.p, st);
+      NK(k_gather64, nk, p0.as<u32>(), nk, klo.as<u64>(), a.as<u64>());
+      sort_pairs_u64_u32(a.as<u64>(), b.as<u64>(), p0.as<u32>(), p1.as<u32>(), nk, 64, st);
+      NK(k_gather64, nk, p1.as<u32>(), nk, khi.as<u64>(), a.as<u64>());
+      sort_pairs_u64_u32(a.as<u64>(), b.as<u64>(), p1.as<u32>(), p0.as<u32>(), nk, std::max(1, GB - 64), st);
+      DBuf f1b(ntok * 4 + 4, st), f2b(ntok * 4 + 4, st);
+      NK(k_gather32, nk, p0.as<u32>(), nk, kf.as<u32>(), f1b.as<u32>());
+      sort_pairs_u32_u32(f1b.as<u32>(), f2b.as<u32>(), p0.as<u32>(), p1.as<u32>(), nk, FB, st);
+      // p1: window order by (file, hi, lo); f2b: the sorted files
+      NK(k_gather64, nk, p1.as<u32>(), nk, khi.as<u64>(), a.as<u64>());
+      NK(k_gather64, nk, p1.as<u32>(), nk, klo.as<u64>(), b.as<u64>());
+      DBuf hd(nk + 1, st), hidx(nk * 4 + 4, st);
+      NK(k_heads_wide, nk, f2b.as<u32>(), a.as<u64>(), b.as<u64>(), nk, hd.as<uint8_t>());
+      select_flagged_index(hd.as<uint8_t>(), hidx.as<u32>(), cnt.as<u64>(), nk, st);
+      const u64 U = rd<u64>(cnt.p, st);
+      DBuf of(U * 4 + 4, st), oh(U * 8 + 8, st), ol(U * 8 + 8, st), oc(U * 8 + 8, st);
+      NK(k_runs_wide, U, f2b.as<u32>(), a.as<u64>(), b.as<u64>(), hidx.as<u32>(), U, nk, f0, of.as<u32>(),
+         oh.as<u64>(), ol.as<u64>(), oc.as<u64>());
+      rf.push_back(std::move(of));
+      rk.push_back(std::move(ol));
+      rh.push_back(std::move(oh));
+      rc.push_back(std::move(oc));
+      rn.push_back(U);
+      f0 = f1;
+      continue;
+    }
     DBuf keys, valid;
     u64 nk = ntok;
     int kbits;
@@ -460,7 +570,7 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, c
   // (file, word-or-gram) order
   u64 n = 0;
   for (u64 x : rn) n += x;
-  DBuf file(n * 4 + 4, st), low(n * 8 + 8, st), count(n * 8 + 8, st);
+  DBuf file(n * 4 + 4, st), low(n * 8 + 8, st), count(n * 8 + 8, st), high(wide ? n * 8 + 8 : 8, st);
   {
     u64 o = 0;
     for (size_t k = 0; k < rk.size(); k++) {
@@ -468,12 +578,14 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, c
         GT_CUDA(cudaMemcpyAsync(file.as<u32>() + o, rf[k].p, rn[k] * 4, cudaMemcpyDeviceToDevice, st));
         GT_CUDA(cudaMemcpyAsync(low.as<u64>() + o, rk[k].p, rn[k] * 8, cudaMemcpyDeviceToDevice, st));
         GT_CUDA(cudaMemcpyAsync(count.as<u64>() + o, rc[k].p, rn[k] * 8, cudaMemcpyDeviceToDevice, st));
+        if (wide) GT_CUDA(cudaMemcpyAsync(high.as<u64>() + o, rh[k].p, rn[k] * 8, cudaMemcpyDeviceToDevice, st));
       }
       o += rn[k];
     }
     rf.clear();
     rk.clear();
     rc.clear();
+    rh.clear();
   }
   const int SH = gram_task ? (int)(l * wbits) : WB;
   const u64 Wt = text ? std::max<u64>(hoff[d->F], 1) : d->W;
@@ -496,6 +608,9 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, c
       NK(k_lo32, n, low.as<u64>(), n, w32.as<u32>());
       Rr->id.alloc(n * 4 + 4, st);
       NK(k_gather32, n, idx2.as<u32>(), n, w32.as<u32>(), Rr->id.as<u32>());
+    } else if (wide) {
+      Rr->gram.alloc(n * l * 4 + 4, st);
+      NK(k_decode_wide, n, idx2.as<u32>(), n, high.as<u64>(), low.as<u64>(), l, wbits, Rr->gram.as<u32>());
     } else {
       Rr->key.alloc(n * 8 + 8, st);
       NK(k_gather64, n, idx2.as<u32>(), n, low.as<u64>(), Rr->key.as<u64>());
@@ -520,6 +635,33 @@ void naive_run(DeviceDag* d, int task, int l_, DevRecords* Rr, int* wbits_out, c
     Rr->group_off.alloc((G + 1) * 8, st);
     NK(k_groups_out, G + 1, sel.as<u32>(), ng.as<u64>(), n, w2.as<u32>(), (const u64*)nullptr,
        Rr->group_id.as<u32>(), (u64*)nullptr, Rr->group_off.as<u64>());
+  } else if (wide) {
+    // ranked inverted index on wide grams: LSD by W - count, then lo, then hi
+    NK(k_inv_count_key, n, count.as<u64>(), n, Wt, k1.as<u64>());
+    sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), idx.as<u32>(), idx2.as<u32>(), n, CB, st);
+    NK(k_gather64, n, idx2.as<u32>(), n, low.as<u64>(), k1.as<u64>());
+    sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), idx2.as<u32>(), idx.as<u32>(), n, 64, st);
+    NK(k_gather64, n, idx.as<u32>(), n, high.as<u64>(), k1.as<u64>());
+    sort_pairs_u64_u32(k1.as<u64>(), k2.as<u64>(), idx.as<u32>(), idx2.as<u32>(), n, std::max(1, (int)(l * wbits) - 64), st);
+    // idx2: the final order
+    Rr->count.alloc(n * 8 + 8, st);
+    NK(k_gather64, n, idx2.as<u32>(), n, count.as<u64>(), Rr->count.as<u64>());
+    Rr->id.alloc(n * 4 + 4, st);
+    NK(k_gather32, n, idx2.as<u32>(), n, file.as<u32>(), Rr->id.as<u32>());
+    NK(k_add32, n, Rr->id.as<u32>(), n, (u32)d->file_lo);
+    DBuf sh(n * 8 + 8, st), sl(n * 8 + 8, st);
+    NK(k_gather64, n, idx2.as<u32>(), n, high.as<u64>(), sh.as<u64>());
+    NK(k_gather64, n, idx2.as<u32>(), n, low.as<u64>(), sl.as<u64>());
+    DBuf hd(n + 1, st), sel(n * 4 + 4, st), ng(8, st);
+    NK(k_heads_wide2, n, sh.as<u64>(), sl.as<u64>(), n, hd.as<uint8_t>());
+    select_flagged_index(hd.as<uint8_t>(), sel.as<u32>(), ng.as<u64>(), n, st);
+    const u64 G = rd<u64>(ng.p, st);
+    Rr->n_groups = G;
+    Rr->group_gram.alloc(G * l * 4 + 4, st);
+    Rr->group_off.alloc((G + 1) * 8, st);
+    NK(k_groups_out, G + 1, sel.as<u32>(), ng.as<u64>(), n, (const u32*)nullptr, (const u64*)nullptr,
+       (u32*)nullptr, (u64*)nullptr, Rr->group_off.as<u64>());
+    NK(k_decode_wide, G, sel.as<u32>(), G, sh.as<u64>(), sl.as<u64>(), l, wbits, Rr->group_gram.as<u32>());
   } else {
     // ranked inverted index: gram asc, then (-count, file): LSD over the
     // (file, gram)-ordered records: by W - count, then by gram

@@ -39,7 +39,8 @@ def test_fixtures_match_naive(name):
         if dag.info["words"] > 1 << 31:
             pytest.skip("expansion too large to decompress (e.g. a doubling chain)")
         wbits = max(1, (dag.info["num_words"] - 1).bit_length())
-        lens = tuple(l for l in (1, 2, 3, 4) if l * wbits <= 63)
+        # packed grams and the wide (64..128-bit) keys of the gram mode alike
+        lens = tuple(l for l in (1, 2, 3, 4) if l * wbits <= 128)
         _check(dag, TASKS, lens)
 
 
@@ -57,3 +58,16 @@ def test_full_size_configs_match_naive(name, tasks):
         _check(dag, tasks)
     finally:
         dag.close()
+
+
+@pytest.mark.parametrize("l", [4, 5])
+def test_wide_grams_match_naive(l):
+    """Grams wider than 63 bits (the compressed path's gram mode: l words per
+    key) against the device decompress-then-count's 128-bit keys: a 1M-word
+    vocabulary (20-bit ids) at l = 4 and 5 (80 / 100 bits)."""
+    import paper_2106_06889_b200 as gt
+    blob, _ = composed("c5", 0.002)
+    with gt.DeviceDag(blob) as dag:
+        assert max(1, (dag.info["num_words"] - 1).bit_length()) * l > 63
+        _check(dag, ["seqcount", "rankedinvertedindex"], (l,))
+
