@@ -1105,7 +1105,7 @@ __global__ void __launch_bounds__(kKahnBlock) k_kahn3(KahnCtl* ctl, const u64* _
       }
     }
   }
-  if (resident) {
+  if (resident && nr32) {  // (a warp past the last rule has no range: off[r0] may not exist)
     for (u32 i0 = 0; i0 <= nr32; i0 += 256) {
       u64 t[8];
 #pragma unroll
