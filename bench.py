@@ -483,12 +483,26 @@ def main():
                 "peak_source": peak_src,
                 "kernel_timing": "CUDA events per launch on the library stream over K profiled steps "
                                  "(same workload, run after the unprofiled timed region)"}
+        # the single-parent contraction (contract.cu): built on the DAG's
+        # second top-down run (a warm-up step), then every timed step runs
+        # over the heads only — the §8(d) bytes above are the whole DAG's,
+        # the lists the pass actually reads are these
+        cs = [int(x) for x in dag.dag_array("cont_sizes")]
+        levels = info["td_levels"]
+        if cs:
+            heads, cedges, levels = cs
+            R, Eo, V, F = (info[k] for k in ("num_rules", "own_pairs", "num_words", "num_files"))
+            moved = 12 * cedges + 12 * Eo + 32 * heads + 8 * V + 4 * (F + 1) + 8 * n_ii
+            roof["contraction"] = {"heads": heads, "rules": R, "head_edges": cedges, "td_edges": info["td_edges"],
+                                   "levels": levels, "td_levels": info["td_levels"],
+                                   "list_bytes_per_step": moved,
+                                   "frac_list_bytes": moved / kern_s / 1e9 / peak}
         if fused:
             # the top-down pass is a chain of grid-barrier-separated levels:
             # its time per level against the measured per-level floor
             # (grid barrier + item load + L2 gather + RED, tools/barrier_probe.cu)
-            roof["latency_model"] = {"levels_per_launch": info["td_levels"],
-                                     "us_per_level_upper": (ms_l / n_l) * 1e3 / max(1, info["td_levels"]),
+            roof["latency_model"] = {"levels_per_launch": levels,
+                                     "us_per_level_upper": (ms_l / n_l) * 1e3 / max(1, levels),
                                      "floor_us_per_level": [2.0, 2.7], "barrier_us": 1.26,
                                      "floor_source": "profiles/r1_barrier_probe.txt"}
     kernel_table = {k: {"launches_per_step": n / K, "ms_per_step": round(ms / K, 5)} for k, (n, ms) in

@@ -89,7 +89,9 @@ typedef struct gt_info {
   double init_ms;          /* gt_open wall time (the "initialization" phase)  */
   uint64_t td_edges;       /* non-root parent edges (top-down pass items)     */
   uint64_t load_flags;     /* bit 0: rule chain parsed in the chunked form;   */
-                           /* bit 1: per-file cells held in u32 (files < 2^32 words) */
+                           /* bit 1: per-file cells held in u32 (files < 2^32 words); */
+                           /* bit 2: word count / inverted index run over the  */
+                           /* single-parent contraction (heads only)           */
 } gt_info;
 
 /*

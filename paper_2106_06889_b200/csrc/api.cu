@@ -755,6 +755,19 @@ int64_t gt_dag_array(gt_ctx* c, const char* name, int64_t* out, int64_t cap) {
     else if (nm == "num_out_edge") v = fetch64(d.num_out, d.R);
     else if (nm == "exp_len") v = fetch64(d.exp_len, d.R);
     else if (nm == "td_level") v = fetch32(d.td_level, d.R);
+    else if (nm == "tid") v = fetch32(d.tid, d.R);  // top-down row of every rule
+    // the single-parent contraction in tid space (contract.cu; diagnostics:
+    // builds it on request; empty when a multiplier outgrew 32 bits)
+    else if (nm == "cont_sizes") {  // [heads, edges, levels] of the built contraction (empty: none)
+      if (d.contracted) v = {(int64_t)d.c_R, (int64_t)d.c_te_off.back(), (int64_t)d.c_levels};
+    }
+    else if (nm == "cont_head" || nm == "cont_mult" || nm == "cont_level" || nm == "cont_row") {
+      ensure_contracted(&d);
+      if (d.contracted) {
+        const DBuf& b = nm == "cont_head" ? d.c_hd : nm == "cont_mult" ? d.c_ml : nm == "cont_level" ? d.c_lvp : d.c_tid;
+        v = fetch32(b, d.R);
+      }
+    }
     else if (nm == "bu_level") v = fetch32(d.bu_level, d.R);
     else if (nm == "segment_token_counts") v = fetch64(d.seg_tokens, d.F);
     else if (nm == "root_freq") {

@@ -1,0 +1,280 @@
+// contract.cu — the single-parent contraction of the top-down pass.
+//
+// The top-down pass (Alg. 1, engine.py:196-227; word count / inverted index,
+// tasks.py:24-84) pushes every rule's weight to its children level by level:
+// its cost on a small grammar is the chain of dependent levels, not the
+// bytes.  Most rules of a Sequitur grammar are referenced from exactly one
+// place (C2: 756k of 840k rules): a rule r with exactly one non-root parent
+// edge (p, f) and no root reference has w(r) = f·w(p), so by induction
+// w(r) = M(r)·w(H(r)) for its nearest ancestor H(r) with several parents or
+// a root reference (its "head", M(r) the product of the frequencies on the
+// way).  Every word-count / presence consumer only needs Σ_r own(r,w)·w(r)
+// = Σ_r own(r,w)·M(r)·w(H(r)) (presence: M >= 1 keeps the bits), so the pass
+// can run over the heads only:
+//   - heads by contracted level L' (1 + max L' over the heads of their
+//     parents; the root is level 0): C2 84k rules in 17 levels instead of
+//     840k in 24;
+//   - edges H(p) -> c with frequency f·M(p) for every non-root edge p -> c
+//     into a head c (C2: 325k of 1.08M);
+//   - own pairs (word, H(r), f·M(r)) in the word-major ow order (no sort:
+//     the word keys do not change).
+// The per-file columns (per-file counts, presence bitsets) are linear in the
+// same way, column by column.  A product f·M(p) or f·M(r) of 2^32 or more
+// turns the contraction off (the lists stay u32).
+//
+// Built lazily from the loader's top-down lists (tid space), once a DAG
+// serves repeated top-down word runs: gt_open stays as it was (a one-shot
+// open + query pays nothing), the second run builds the lists (~0.2 ms at
+// C2) and every later run takes the shorter chain.  GT_CONTRACT=0 never
+// builds them, GT_CONTRACT=2 builds them on the first run.
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "kernels_common.cuh"
+
+namespace gt {
+
+#define LAUNCH(k, n, ...) GT_KLAUNCH(#k, k, grid_for((n), 256), 256, st, __VA_ARGS__)
+
+namespace {
+
+// non-root parent edges per child (tid)
+__global__ void k_c_count(const u32* __restrict__ child, u64 n, u32* cnt) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(&cnt[child[i]], 1u);
+}
+
+// rules the root references (the unfiltered root lists)
+__global__ void k_c_rootp(const u32* __restrict__ rs_rule, u64 n, const u32* __restrict__ tid, uint8_t* flag) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) flag[tid[rs_rule[i]]] = 1;
+}
+
+// flag: 1 = single (exactly one non-root parent edge, no root reference)
+__global__ void k_c_single(const u32* __restrict__ cnt, u64 R, uint8_t* flag) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < R; t += stride)
+    flag[t] = t != 0 && cnt[t] == 1 && !flag[t];
+}
+
+// one top-down level's edges p -> c (every parent lies in an earlier level,
+// so its H / M / L' are final): a single child inherits (H(p), M(p)·f,
+// L'(p)); a head child raises its running max of L'(p) (lv holds the max
+// until k_c_final turns it into the head's own level)
+__global__ void k_c_level(const u32* __restrict__ child, const u32* __restrict__ par, const u32* __restrict__ freq,
+                          u64 n, const uint8_t* __restrict__ single, u32* hd, u32* ml, u32* lv, u32* ovf) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  bool o = false;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 c = child[i], p = par[i];
+    const bool ps = single[p];
+    const u32 H = ps ? hd[p] : p, M = ps ? ml[p] : 1u, L = ps ? lv[p] : lv[p] + 1u;
+    if (single[c]) {
+      const u64 m = (u64)M * freq[i];
+      o |= m > 0xFFFFFFFFull;
+      hd[c] = H;
+      ml[c] = (u32)m;
+      lv[c] = L;
+    } else {
+      atomicMax(&lv[c], L);
+    }
+  }
+  if (o) *ovf = 1;
+}
+
+// heads: H = itself, M = 1, L' = 1 + max over parents (the root: 0); the
+// tid' sort key (heads by L', singles after every level)
+__global__ void k_c_final(const uint8_t* __restrict__ single, u64 R, u32 drop, u32* hd, u32* ml, u32* lv, u32* key) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < R; t += stride) {
+    if (single[t]) {
+      key[t] = drop;
+    } else {
+      const u32 L = t ? lv[t] + 1u : 0u;
+      hd[t] = (u32)t;
+      ml[t] = 1u;
+      lv[t] = L;
+      key[t] = L;
+    }
+  }
+}
+
+// in-degrees in tid' order (singles have no list of their own)
+__global__ void k_c_degt(const u32* __restrict__ ord, u64 R, const uint8_t* __restrict__ single,
+                         const u32* __restrict__ cnt, u32* degt) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j < R; j += stride) {
+    const u32 t = ord[j];
+    degt[j] = single[t] ? 0u : cnt[t];
+  }
+}
+
+// the heads' edges H(p) -> c, f·M(p), scattered into per-child slot ranges
+// (one 12-byte record per edge, unpacked afterwards like the loader's lists)
+__global__ void k_c_scatter(const u32* __restrict__ child, const u32* __restrict__ par, const u32* __restrict__ freq,
+                            u64 n, const uint8_t* __restrict__ single, const u32* __restrict__ ctid,
+                            const u32* __restrict__ hd, const u32* __restrict__ ml, u32* cur, U3* te, u32* ovf) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  bool o = false;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 c = child[i];
+    if (single[c]) continue;
+    const u32 p = par[i];
+    const u64 m = (u64)freq[i] * ml[p];
+    o |= m > 0xFFFFFFFFull;
+    const u32 tc = ctid[c];
+    const u32 slot = atomicAdd(&cur[tc], 1u);
+    te[slot] = U3{tc, ctid[hd[p]], (u32)m};
+  }
+  if (o) *ovf = 1;
+}
+
+// own pairs in ow order: source row tid'(H(r)), frequency f·M(r)
+__global__ void k_c_own(const u32* __restrict__ rule_t, const u32* __restrict__ freq, u64 n,
+                        const u32* __restrict__ ctid, const u32* __restrict__ hd, const u32* __restrict__ ml, u32* src,
+                        u32* fr, u32* ovf) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  bool o = false;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 t = rule_t[i];
+    const u64 m = (u64)freq[i] * ml[t];
+    o |= m > 0xFFFFFFFFull;
+    src[i] = ctid[hd[t]];
+    fr[i] = (u32)m;
+  }
+  if (o) *ovf = 1;
+}
+
+}  // namespace
+
+void ensure_contracted(DeviceDag* d) {
+  if (d->c_tried) return;
+  d->c_tried = true;
+  GT_CUDA(cudaSetDevice(d->device));
+  cudaStream_t st = d->stream;
+  const u64 R = d->R;
+  const int nl = d->td.nl;
+  const u64 Etd = d->te_off.empty() ? 0 : d->te_off.back();
+  const u64 Eo = d->E_own;
+  if (R < 2 || nl < 1) return;
+  const Carve cv(st, {R * 4, R + 16, R * 4, R * 4, R * 4, R * 4, R * 4 + 4, R * 4 + 4, R * 4 + 4,
+                      ((u64)nl + 3) * 8, 16});
+  u32 *cnt = cv.at<u32>(0), *key = cv.at<u32>(2), *key2 = cv.at<u32>(3), *iota = cv.at<u32>(4),
+      *ord = cv.at<u32>(5), *degt = cv.at<u32>(6), *incl = cv.at<u32>(7), *cur = cv.at<u32>(8),
+      *ovf = cv.at<u32>(10);
+  uint8_t* single = cv.at<uint8_t>(1);
+  u64* ls = cv.at<u64>(9);
+  GT_CUDA(cudaMemsetAsync(cnt, 0, R * 4, st));
+  GT_CUDA(cudaMemsetAsync(single, 0, R, st));
+  GT_CUDA(cudaMemsetAsync(ovf, 0, 16, st));
+  d->c_hd.alloc(R * 4 + 4, st);
+  d->c_ml.alloc(R * 4 + 4, st);
+  d->c_lvp.alloc(R * 4 + 4, st);
+  u32 *hd = d->c_hd.as<u32>(), *ml = d->c_ml.as<u32>(), *lv = d->c_lvp.as<u32>();
+  GT_CUDA(cudaMemsetAsync(lv, 0, R * 4, st));
+  // singles: one non-root parent edge and no root reference (any file: the
+  // owned range only filters the seeds)
+  if (Etd) LAUNCH(k_c_count, Etd, d->te_child.as<u32>(), Etd, cnt);
+  const auto& rs = d->full.saved ? d->full.rs_rule : d->rs_rule;
+  const u64 nrs = d->full.saved ? d->full.n_rs : d->n_rs;
+  if (nrs) LAUNCH(k_c_rootp, nrs, rs.as<u32>(), nrs, d->tid.as<u32>(), single);
+  LAUNCH(k_c_single, R, cnt, R, single);
+  // H / M / L' level by level (one launch per level; built once per DAG)
+  for (int L = 1; L <= nl; L++) {
+    const u64 a = d->te_off[L], n = d->te_off[L + 1] - a;
+    if (n)
+      LAUNCH(k_c_level, n, d->te_child.as<u32>() + a, d->te_par.as<u32>() + a, d->te_freq.as<u32>() + a, n, single,
+             hd, ml, lv, ovf);
+  }
+  LAUNCH(k_c_final, R, single, R, (u32)nl + 1, hd, ml, lv, key);
+  // tid': heads by (L', tid) (stable radix sort), singles last
+  LAUNCH(k_iota_u32, R, iota, R);
+  sort_pairs_u32_u32(key, key2, iota, ord, R, std::max(1, bitlen((u64)nl + 1)), st);
+  d->c_tid.alloc(R * 4 + 4, st);
+  LAUNCH(k_rank_of, R, ord, R, d->c_tid.as<u32>());
+  LAUNCH(k_csr_offsets, (u64)nl + 3, key2, R, (u64)nl + 2, ls);  // ls[L]: first tid' of level >= L
+  LAUNCH(k_c_degt, R, ord, R, single, cnt, degt);
+  inclusive_scan_u32(degt, incl, R, st);
+  LAUNCH(k_cursor, R, degt, incl, R, cur);
+  // (+ 16: the TMA-staged level loop copies whole 16-byte words)
+  d->c_te_child.alloc(Etd * 4 + 16, st);
+  d->c_te_par.alloc(Etd * 4 + 16, st);
+  d->c_te_freq.alloc(Etd * 4 + 16, st);
+  if (Etd) {
+    DBuf te(Etd * 12 + 12, st);
+    LAUNCH(k_c_scatter, Etd, d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(), Etd, single,
+           d->c_tid.as<u32>(), hd, ml, cur, te.as<U3>(), ovf);
+    LAUNCH(k_unpack3_n, Etd, te.as<U3>(), incl + (R - 1), d->c_te_child.as<u32>(), d->c_te_par.as<u32>(),
+           d->c_te_freq.as<u32>());
+  }
+  d->c_te_off_dev.alloc(((u64)nl + 3) * 8, st);
+  LAUNCH(k_te_level_off, (u64)nl + 3, ls, incl, degt, R, (u64)nl, d->c_te_off_dev.as<u64>());
+  d->c_ow_src.alloc(Eo * 4 + 4, st);
+  d->c_ow_freq.alloc(Eo * 4 + 4, st);
+  if (Eo)
+    LAUNCH(k_c_own, Eo, d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), Eo, d->c_tid.as<u32>(), hd, ml,
+           d->c_ow_src.as<u32>(), d->c_ow_freq.as<u32>(), ovf);
+  d->contracted = true;  // (refresh_contracted_seeds maps the current seeds)
+  refresh_contracted_seeds(d);
+  std::vector<u64> h(2 * ((u64)nl + 3) + 1);
+  GT_CUDA(cudaMemcpyAsync(h.data(), ls, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(h.data() + nl + 3, d->c_te_off_dev.p, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(h.data() + 2 * (nl + 3), ovf, 4, cudaMemcpyDeviceToHost, st));
+  stream_sync(st);
+  if ((u32)h[2 * (nl + 3)]) {  // a product outgrew 32 bits: the full lists stay in use
+    d->contracted = false;
+    DBuf* bufs[] = {&d->c_tid, &d->c_te_child, &d->c_te_par, &d->c_te_freq, &d->c_te_off_dev, &d->c_ow_src,
+                    &d->c_ow_freq, &d->c_rs_rule_t};
+    for (DBuf* b : bufs) b->release();
+    if (getenv("GT_TRACE")) fprintf(stderr, "[contract] off: a frequency times multiplier needs 64 bits\n");
+    return;
+  }
+  int ncl = 0;  // the highest level holding a head
+  for (int L = 1; L <= nl; L++)
+    if (h[L + 1] > h[L]) ncl = L;
+  d->c_levels = (u32)ncl;
+  d->c_R = h[nl + 1];
+  d->c_te_off.assign(h.begin() + (nl + 3), h.begin() + (nl + 3) + (ncl + 3));
+  d->load_flags |= 4;
+  if (getenv("GT_TRACE"))
+    fprintf(stderr, "[contract] %llu heads of %llu rules, %llu of %llu edges, %d of %d levels\n",
+            (unsigned long long)d->c_R, (unsigned long long)R, (unsigned long long)d->c_te_off.back(),
+            (unsigned long long)Etd, ncl, nl);
+}
+
+void refresh_contracted_seeds(DeviceDag* d) {
+  if (!d->contracted) return;
+  cudaStream_t st = d->stream;
+  d->c_rs_rule_t.alloc(d->n_rs * 4 + 4, st);
+  if (d->n_rs)
+    LAUNCH(k_map_u32, d->n_rs, d->rs_rule_t.as<u32>(), d->n_rs, d->c_tid.as<u32>(), d->c_rs_rule_t.as<u32>());
+}
+
+TdLists td_lists(DeviceDag* d, bool contract) {
+  if (contract && !d->c_tried) {
+    static const int policy = getenv("GT_CONTRACT") ? atoi(getenv("GT_CONTRACT")) : 1;
+    if (policy == 2 || (policy == 1 && ++d->c_calls >= 2)) ensure_contracted(d);
+  }
+  TdLists t;
+  t.n_own = d->E_own;
+  t.ow_word = d->ow_word.as<u32>();
+  if (contract && d->contracted) {
+    t.rows = d->c_R;
+    t.te_child = d->c_te_child.as<u32>(), t.te_par = d->c_te_par.as<u32>(), t.te_freq = d->c_te_freq.as<u32>();
+    t.te_off_dev = d->c_te_off_dev.as<u64>(), t.te_off = &d->c_te_off, t.nl = (int)d->c_levels;
+    t.ow_src = d->c_ow_src.as<u32>(), t.ow_freq = d->c_ow_freq.as<u32>();
+    t.rs_rule_t = d->c_rs_rule_t.as<u32>();
+    t.contracted = true;
+    return t;
+  }
+  t.rows = d->R;
+  t.te_child = d->te_child.as<u32>(), t.te_par = d->te_par.as<u32>(), t.te_freq = d->te_freq.as<u32>();
+  t.te_off_dev = d->te_off_dev.as<u64>(), t.te_off = &d->te_off, t.nl = d->td.nl;
+  t.ow_src = d->ow_rule_t.as<u32>(), t.ow_freq = d->ow_freq.as<u32>();
+  t.rs_rule_t = d->rs_rule_t.as<u32>();
+  return t;
+}
+
+}  // namespace gt

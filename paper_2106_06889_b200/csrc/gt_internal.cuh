@@ -173,6 +173,22 @@ struct DeviceDag {
     bool saved = false;
   } full;
   DBuf sub_rule;       // u32[E_sub]: the rule of every sub pair (lazy builds)
+  // the single-parent contraction of the top-down pass (contract.cu, built
+  // lazily once the DAG serves repeated top-down runs): a rule with exactly
+  // one non-root parent edge (p, f) and no root reference has w(r) = f·w(p),
+  // so w(r) = M(r)·w(H(r)) for its nearest multi-parent ancestor H ("head").
+  // Tid space: c_hd / c_ml / c_lvp = H (a tid), M and the contracted level
+  // L' of every tid; c_tid maps tid -> tid' (heads by (L', tid), singles
+  // last).  The pass then runs over the heads only: edges H(p) -> c with
+  // frequency f·M(p), own pairs (word, tid'(H(r)), f·M(r)) in ow order.
+  DBuf c_hd, c_ml, c_lvp;
+  bool contracted = false;
+  bool c_tried = false;  // built (or given up: a multiplier outgrew 32 bits)
+  u32 c_calls = 0;       // top-down word runs served (the build policy)
+  u32 c_levels = 0;
+  u64 c_R = 0;           // heads
+  DBuf c_tid, c_te_child, c_te_par, c_te_freq, c_te_off_dev, c_ow_src, c_ow_freq, c_rs_rule_t;
+  std::vector<u64> c_te_off;
   // derived arrays (ensure_derived): no top-down word count / inverted
   // index reads them, so gt_open leaves them to the first task that does
   // (be lists, heights = bu_level, depth, exp_len, W, seg_tokens,
@@ -192,12 +208,39 @@ struct DeviceDag {
                          &seg_tokens, &ow_word, &ow_rule, &ow_freq, &ow_off, &rs_rule, &rs_seg,
                          &rs_cnt, &rs_off, &rw_word, &rw_seg, &rw_cnt, &td.order, &bu.order,
                          &tid, &rs_rule_t, &ow_rule_t, &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts,
-                         &te_off_dev, &be_off_dev, &sub_rule};
+                         &te_off_dev, &be_off_dev, &sub_rule, &c_hd, &c_ml, &c_lvp, &c_tid, &c_te_child, &c_te_par, &c_te_freq, &c_te_off_dev, &c_ow_src, &c_ow_freq,
+                         &c_rs_rule_t};
     u64 t = 0;
     for (const DBuf* b : all) t += b->bytes;
     return t;
   }
 };
+
+// The top-down pass's inputs: the whole DAG, or its single-parent
+// contraction (heads only) when the loader built it and the caller can use
+// head rows (word count / inverted index: every rule's own words are folded
+// into its head's list with the multiplier)
+struct TdLists {
+  u64 rows = 0;  // rows of the pass (rules or heads)
+  const u32* te_child = nullptr;
+  const u32* te_par = nullptr;
+  const u32* te_freq = nullptr;
+  const u64* te_off_dev = nullptr;
+  const std::vector<u64>* te_off = nullptr;
+  int nl = 0;
+  const u32* ow_word = nullptr;
+  const u32* ow_src = nullptr;
+  const u32* ow_freq = nullptr;
+  u64 n_own = 0;
+  const u32* rs_rule_t = nullptr;
+  bool contracted = false;
+};
+// contract.cu: the pass's lists; `contract` asks for the heads-only lists,
+// which are built on the second such request (GT_CONTRACT=0: never, 2: on
+// the first)
+TdLists td_lists(DeviceDag* d, bool contract);
+void ensure_contracted(DeviceDag* d);
+void refresh_contracted_seeds(DeviceDag* d);  // after the owned file range changed
 
 // loader.cu
 void build_device_dag(const uint8_t* blob, size_t n, int device, u64 file_lo, u64 file_hi,

@@ -12,6 +12,15 @@ __global__ void k_csr_offsets(const u32* sorted_key, u64 n, u64 R, u64* off);
 
 __global__ void k_iota_u32(u32* out, u64 n);
 
+// loader.cu kernels reused by the lazily built lists (contract.cu)
+// out[i] = map[in[i]]; rank[order[i]] = i; cur = incl - degt
+__global__ void k_map_u32(const u32* __restrict__ in, u64 n, const u32* __restrict__ map, u32* out);
+__global__ void k_rank_of(const u32* __restrict__ order, u64 n, u32* rank);
+__global__ void k_cursor(const u32* __restrict__ degt, const u32* __restrict__ incl, u64 n, u32* cur);
+__global__ void k_unpack3_n(const U3* __restrict__ in, const u32* __restrict__ n_dev, u32* a, u32* b, u32* c);
+__global__ void k_te_level_off(const u64* __restrict__ ls, const u32* __restrict__ incl,
+                               const u32* __restrict__ degt, u64 R, u64 nl, u64* off);
+
 // out[key[i]] += val(i) for keys sorted ascending, warp-aggregated atomics
 // (at most one atomic per key run per warp).
 template <class ValF>

@@ -1367,6 +1367,8 @@ __global__ void k_root_cycle2(const u32* __restrict__ prule, const u32* __restri
     }
 }
 
+}  // namespace (the list kernels below are shared with contract.cu)
+
 // top-down edge lists by scatter: every child's non-root parent edges get a
 // contiguous slot range in (td level, child) = tid order (exclusive scan of
 // the in-degrees in tid order); within a child the slot order is the order
@@ -1415,6 +1417,8 @@ __global__ void k_te_level_off(const u64* __restrict__ ls, const u32* __restrict
   const u64 t = k <= nl + 1 ? ls[k] : R;
   off[k] = t < R ? incl[t] - degt[t] : tot;
 }
+
+namespace {
 
 // rule id of every sub pair (expanding sub_off), for the lazily built parent CSR
 __global__ void k_expand_owner(const u64* __restrict__ off, u64 R, u32* owner) {
@@ -2462,6 +2466,7 @@ void set_file_range(DeviceDag* d, u64 lo, u64 hi) {
       d->rw_word = std::move(f.rw_word), d->rw_seg = std::move(f.rw_seg), d->rw_cnt = std::move(f.rw_cnt);
       d->n_rs = f.n_rs, d->n_rw = f.n_rw;
       f.saved = false;
+      refresh_contracted_seeds(d);
     }
     return;
   }
@@ -2503,6 +2508,7 @@ void set_file_range(DeviceDag* d, u64 lo, u64 hi) {
            (u32*)nullptr);
     d->n_rw = n;
   }
+  refresh_contracted_seeds(d);
   stream_sync(st);
 }
 

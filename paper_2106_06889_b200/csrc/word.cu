@@ -156,22 +156,24 @@ __global__ void k_ii_emit(const u64* __restrict__ pres, u64 V, const u64* __rest
 // seeded from the root references, then one segmented gather-reduce launch
 // per top-down level over that level's non-root parent edges.
 template <class Mode, class T = u64>
-static void td_levels(const DeviceDag* d, u32 C, T* row, u32 per_file = 1, const PostArgs* post = nullptr) {
+static void td_levels(const DeviceDag* d, const TdLists& tl, u32 C, T* row, u32 per_file = 1,
+                      const PostArgs* post = nullptr) {
   cudaStream_t st = d->stream;
-  // rows indexed by tid (DeviceDag::tid): seeds and edges carry tids
-  const SeedArgs seed{d->rs_rule_t.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
-                      (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row, (u64)C * d->R};
+  // rows indexed by tid (DeviceDag::tid) or tid' (heads): seeds and edges carry them
+  const SeedArgs seed{tl.rs_rule_t, d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
+                      (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0, C, row, (u64)C * tl.rows};
   // C = 1 with u64 rows: the zeroing and the seeds run as phase 0 of the
   // persistent launch
   const bool fused_seed = C == 1 && sizeof(T) == 8;
   if (!fused_seed) {
-    GT_CUDA(cudaMemsetAsync(row, 0, sizeof(T) * C * d->R, st));
+    GT_CUDA(cudaMemsetAsync(row, 0, sizeof(T) * C * tl.rows, st));
     if (d->n_rs) KL((k_seed<Mode, T>), grid_for(d->n_rs, 256), seed);
   }
   // all levels in one persistent launch, grid barriers between levels
-  seg_reduce_levels<Mode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
-                          d->te_off_dev.as<u64>(), 1, d->td.nl, C, RowSrcT<T>{row, C}, TdRowsT<T>{row, C}, st,
-                          false, d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0,
+  const std::vector<u64>& to = *tl.te_off;
+  seg_reduce_levels<Mode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, C,
+                          RowSrcT<T>{row, C}, TdRowsT<T>{row, C}, st, false,
+                          tl.nl ? (to[tl.nl + 1] - to[1]) / tl.nl : 0,
                           fused_seed ? &seed : nullptr, fused_seed ? post : nullptr);
 }
 
@@ -195,7 +197,8 @@ __global__ void k_narrow_rows(const u64* __restrict__ row, u64 n, u32* out, u32*
 // [V][C] with row_major (presence bitsets: a word's FW words contiguous, so
 // the team's reductions and the later bit expansion are coalesced)
 template <class Mode, class T = u64>
-static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool per_file, bool row_major = false) {
+static void reduce_words(const DeviceDag* d, const TdLists& tl, u32 C, const T* row, T* out, bool per_file,
+                         bool row_major = false) {
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
   GT_CUDA(cudaMemsetAsync(out, 0, sizeof(T) * V * C, st));
@@ -205,16 +208,15 @@ static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool p
   // a weight of 2^32 or more (flagged) reruns the reduce on the u64 rows
   static const bool wide = getenv("GT_REDUCE_U64") != nullptr;  // diagnostics: always gather u64 rows
   if constexpr (sizeof(T) == 8) {
-    if (std::is_same<Mode, SumMode>::value && C == 1 && !wide && d->R * 8 > (64ull << 20)) {
-      const Carve cv(st, {d->R * 4 + 4, 4});
+    if (std::is_same<Mode, SumMode>::value && C == 1 && !wide && tl.rows * 8 > (64ull << 20)) {
+      const Carve cv(st, {tl.rows * 4 + 4, 4});
       GT_CUDA(cudaMemsetAsync(cv.at<u32>(1), 0, 4, st));
-      KL(k_narrow_rows, grid_for(d->R, 256), reinterpret_cast<const u64*>(row), d->R, cv.at<u32>(0), cv.at<u32>(1));
+      KL(k_narrow_rows, grid_for(tl.rows, 256), reinterpret_cast<const u64*>(row), tl.rows, cv.at<u32>(0),
+         cv.at<u32>(1));
       if (row_major)
-        seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
-                         d->E_own, C, RowSrcT<u32>{cv.at<u32>(0), C}, OutRowMajorT<T>{out, C}, st);
+        seg_reduce<Mode>("k_reduce_words", tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own, C, RowSrcT<u32>{cv.at<u32>(0), C}, OutRowMajorT<T>{out, C}, st);
       else
-        seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
-                         d->E_own, C, RowSrcT<u32>{cv.at<u32>(0), C}, OutColMajorT<T>{out, V}, st);
+        seg_reduce<Mode>("k_reduce_words", tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own, C, RowSrcT<u32>{cv.at<u32>(0), C}, OutColMajorT<T>{out, V}, st);
       u32 ovf = 0;
       GT_CUDA(cudaMemcpyAsync(&ovf, cv.at<u32>(1), 4, cudaMemcpyDeviceToHost, st));
       GT_CUDA(cudaStreamSynchronize(st));
@@ -229,11 +231,9 @@ static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool p
     }
   }
   if (row_major)
-    seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
-                     d->E_own, C, RowSrcT<T>{row, C}, OutRowMajorT<T>{out, C}, st);
+    seg_reduce<Mode>("k_reduce_words", tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own, C, RowSrcT<T>{row, C}, OutRowMajorT<T>{out, C}, st);
   else
-    seg_reduce<Mode>("k_reduce_words", d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(),
-                     d->E_own, C, RowSrcT<T>{row, C}, OutColMajorT<T>{out, V}, st);
+    seg_reduce<Mode>("k_reduce_words", tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own, C, RowSrcT<T>{row, C}, OutColMajorT<T>{out, V}, st);
   if (d->n_rw)
     KL((k_root_words<Mode, T>), grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
        d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, (u32)(d->file_hi - d->file_lo),
@@ -248,13 +248,14 @@ static void reduce_words(const DeviceDag* d, u32 C, const T* row, T* out, bool p
 constexpr u64 kFusedReduceMax = 4ull << 20;
 
 template <class Mode>
-static void td_words_fused(const DeviceDag* d, u64* row, u64* out, bool per_file, PostArgs* compact = nullptr) {
+static void td_words_fused(DeviceDag* d, u64* row, u64* out, bool per_file, PostArgs* compact = nullptr) {
+  const TdLists tl = td_lists(d, true);
   if (d->E_own > kFusedReduceMax) {
-    td_levels<Mode>(d, 1, row, per_file ? 1 : 0);
-    reduce_words<Mode>(d, 1, row, out, per_file);
+    td_levels<Mode>(d, tl, 1, row, per_file ? 1 : 0);
+    reduce_words<Mode>(d, tl, 1, row, out, per_file);
     return;
   }
-  PostArgs post{d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), d->E_own, out, d->nw, nullptr,
+  PostArgs post{tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own, out, d->nw, nullptr,
                 d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo,
                 (u32)(d->file_hi - d->file_lo), per_file ? 1 : 0};
   if (compact) {
@@ -266,7 +267,7 @@ static void td_words_fused(const DeviceDag* d, u64* row, u64* out, bool per_file
     post.tot = compact->tot;
     post.bsum = compact->bsum;
   }
-  td_levels<Mode>(d, 1, row, per_file ? 1 : 0, &post);
+  td_levels<Mode>(d, tl, 1, row, per_file ? 1 : 0, &post);
 }
 
 // small grammars, one launch per task: top-down pass + word reduce + root
@@ -344,9 +345,10 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   ii->group_id.alloc(V * 4 + 4, st);
   ii->group_off.alloc((V + 1) * 8, st);
   u64* row = cv.at<u64>(0);
-  const SeedArgs seed{d->rs_rule_t.as<u32>(), d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
-                      Fo, 1, 1u, row, 2 * d->R};
-  PostArgs post{d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), d->E_own,
+  const TdLists tl = td_lists(d, true);
+  const SeedArgs seed{tl.rs_rule_t, d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
+                      Fo, 1, 1u, row, 2 * tl.rows};
+  PostArgs post{tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own,
                 d->word_counts.as<u64>(), V, cv.at<u64>(1), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
                 d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, Fo, 1};
   post.compact = 3;
@@ -364,9 +366,9 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
     GT_CUDA(cudaMemsetAsync(stamps.p, 0, 64 * 8, st));
     post.stamps = stamps.as<u64>();
   }
-  seg_reduce_levels1<WcPresMode>("k_td_levels", d->te_child.as<u32>(), d->te_par.as<u32>(), d->te_freq.as<u32>(),
-                                 d->te_off_dev.as<u64>(), 1, d->td.nl, 0,
-                                 d->td.nl ? (d->te_off[d->td.nl + 1] - d->te_off[1]) / d->td.nl : 0, &seed, &post,
+  const std::vector<u64>& to = *tl.te_off;
+  seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, 0,
+                                 tl.nl ? (to[tl.nl + 1] - to[1]) / tl.nl : 0, &seed, &post,
                                  RowSrcPair{row}, TdRowsPair{row}, st);
   u64 h[2];
   GT_CUDA(cudaMemcpyAsync(h, post.tot, 16, cudaMemcpyDeviceToHost, st));
@@ -374,7 +376,7 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   if (tr) {
     u64 t[64];
     GT_CUDA(cudaMemcpy(t, stamps.p, 64 * 8, cudaMemcpyDeviceToHost));
-    const int nit = d->td.nl;
+    const int nit = tl.nl;
     fprintf(stderr, "[wc+ii] seeds %.1f us | levels:", (t[1] - t[0]) / 1e3);
     for (int i = 0; i < nit && 2 + i < 64; i++) fprintf(stderr, " %.1f", (t[2 + i] - (i ? t[1 + i] : t[1])) / 1e3);
     if (4 + nit < 64)
@@ -433,29 +435,31 @@ void td_file_counts(DeviceDag* d, DBuf& counts, bool* is32) {
   const u32 C = (u32)(d->file_hi - d->file_lo);
   const u64 Cm = std::max<u32>(C, 1);
   *is32 = rows32(d, C);
+  const TdLists tl = td_lists(d, true);
   if (*is32) {
-    DBuf w(d->R * 4 * Cm, st);
-    td_levels<SumMode, u32>(d, C, w.as<u32>());
+    DBuf w(tl.rows * 4 * Cm, st);
+    td_levels<SumMode, u32>(d, tl, C, w.as<u32>());
     counts.alloc(d->nw * 4 * Cm + 8, st);
-    reduce_words<SumMode, u32>(d, C, w.as<u32>(), counts.as<u32>(), true);
+    reduce_words<SumMode, u32>(d, tl, C, w.as<u32>(), counts.as<u32>(), true);
     return;
   }
-  DBuf w(d->R * 8 * Cm, st);
-  td_levels<SumMode>(d, C, w.as<u64>());
+  DBuf w(tl.rows * 8 * Cm, st);
+  td_levels<SumMode>(d, tl, C, w.as<u64>());
   counts.alloc(d->nw * 8 * Cm + 8, st);
-  reduce_words<SumMode>(d, C, w.as<u64>(), counts.as<u64>(), true);
+  reduce_words<SumMode>(d, tl, C, w.as<u64>(), counts.as<u64>(), true);
 }
 
 // per-file weights only -> [R][Fo] of u64, or u32 (*is32)
 void td_file_weights(DeviceDag* d, DBuf& w, u32* C_out, bool* is32) {
   const u32 C = std::max<u32>(1, (u32)(d->file_hi - d->file_lo));
   *is32 = rows32(d, C);
+  const TdLists tl = td_lists(d, false);  // every rule's row (callers index by tid)
   if (*is32) {
     w.alloc(d->R * 4 * (u64)C, d->stream);
-    td_levels<SumMode, u32>(d, C, w.as<u32>());
+    td_levels<SumMode, u32>(d, tl, C, w.as<u32>());
   } else {
     w.alloc(d->R * 8 * (u64)C, d->stream);
-    td_levels<SumMode>(d, C, w.as<u64>());
+    td_levels<SumMode>(d, tl, C, w.as<u64>());
   }
   *C_out = C;
 }
@@ -468,11 +472,12 @@ void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out, DBuf* rows_out) {
   const u32 FW = std::max<u32>(1, (Fo + 63) / 64);
   DBuf m(d->R * 8 * (u64)FW, st);
   pres.alloc(d->nw * 8 * (u64)FW + 8, st);
-  if (FW == 1) {
+  if (FW == 1 && !rows_out) {
     td_words_fused<OrMode>(d, m.as<u64>(), pres.as<u64>(), true);
   } else {
-    td_levels<OrMode>(d, FW, m.as<u64>());
-    reduce_words<OrMode>(d, FW, m.as<u64>(), pres.as<u64>(), true, true);
+    const TdLists tl = td_lists(d, rows_out == nullptr);  // rows handed back: every rule's
+    td_levels<OrMode>(d, tl, FW, m.as<u64>());
+    reduce_words<OrMode>(d, tl, FW, m.as<u64>(), pres.as<u64>(), true, true);
   }
   *FW_out = FW;
   if (rows_out) *rows_out = std::move(m);

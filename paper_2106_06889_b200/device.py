@@ -134,6 +134,12 @@ class DeviceDag:
             self._info = inf.as_dict()
         return self._info
 
+    def refresh_info(self) -> dict:
+        """Re-read gt_info (info is a snapshot: device_bytes and load_flags
+        change when a run builds lazy structures, e.g. the contraction)."""
+        self._info = None
+        return self.info
+
     @property
     def num_files(self) -> int:
         return self.info["num_files"]

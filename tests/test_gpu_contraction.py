@@ -1,0 +1,125 @@
+"""The single-parent contraction of the top-down pass (contract.cu): for
+every rule its head H (the nearest ancestor with more than one non-root
+parent edge or a root reference), multiplier M (w(r) = M(r)·w(H(r))) and
+contracted level L' (heads: 1 + max over parents of L'(H(parent)), the root
+0; singles: their head's), against a numpy restatement over the device's own
+(reference-pinned) parent CSR and top-down levels; and the word tasks run
+over the heads-only lists (built on a DAG's second top-down run) == the
+first, full run == the oracle."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import fixture_names, gtdc
+from test_gpu_parity import composed
+
+pytestmark = pytest.mark.gpu
+
+
+def expected_contraction(dag):
+    po = dag.dag_array("par_off")
+    pid = dag.dag_array("par_ids")
+    pf = dag.dag_array("par_freqs")
+    td = dag.dag_array("td_level")
+    R = len(td)
+    npar = np.diff(po)
+    child = np.repeat(np.arange(R), npar)
+    nonroot = np.bincount(child[pid != 0], minlength=R)
+    rootref = np.zeros(R, bool)
+    rootref[child[pid == 0]] = True
+    single = (nonroot == 1) & ~rootref
+    single[0] = False
+    H = np.arange(R)
+    M = np.ones(R, np.int64)
+    L = np.zeros(R, np.int64)
+    for c in np.argsort(td, kind="stable"):
+        if c == 0:
+            continue
+        ps = pid[po[c]:po[c + 1]]
+        fs = pf[po[c]:po[c + 1]]
+        keep = ps != 0
+        ps, fs = ps[keep], fs[keep]
+        if single[c]:
+            p = ps[0]
+            H[c], M[c], L[c] = H[p], M[p] * fs[0], L[p]
+        else:
+            L[c] = 1 + max((L[p] for p in ps), default=0)
+    return H, M, L
+
+
+def _check(dag):
+    head_t = dag.dag_array("cont_head")  # tid space (builds the contraction)
+    H, M, L = expected_contraction(dag)
+    fits = M < (1 << 32)
+    if head_t.size == 0:  # nothing to contract, or a multiplier (or f·M) outgrew 32 bits
+        assert len(H) < 2 or not fits.all() or _edge_overflow(dag, H, M)
+        assert not dag.refresh_info()["load_flags"] & 4
+        return
+    assert dag.refresh_info()["load_flags"] & 4
+    tid = dag.dag_array("tid")
+    rule_of = np.argsort(tid)
+    assert np.array_equal(rule_of[head_t[tid]], H)
+    assert np.array_equal(dag.dag_array("cont_mult")[tid], M)
+    assert np.array_equal(dag.dag_array("cont_level")[tid], L)
+    # tid': heads by (L', tid), singles after every head
+    row = dag.dag_array("cont_row")[tid]
+    heads = np.flatnonzero(H == np.arange(len(H)))
+    order = heads[np.lexsort((tid[heads], L[heads]))]
+    assert np.array_equal(row[order], np.arange(len(heads)))
+    assert (row[H != np.arange(len(H))] >= len(heads)).all()
+
+
+def _edge_overflow(dag, H, M):
+    """some f·M(parent) of an edge or f·M(rule) of an own pair needs 64 bits"""
+    pid, pf = dag.dag_array("par_ids"), dag.dag_array("par_freqs")
+    if (pf.astype(object) * M[pid].astype(object) >= (1 << 32)).any():
+        return True
+    oo, of = dag.dag_array("own_off"), dag.dag_array("own_freqs")
+    rule = np.repeat(np.arange(len(oo) - 1), np.diff(oo))
+    return bool((of.astype(object) * M[rule].astype(object) >= (1 << 32)).any())
+
+
+@pytest.mark.parametrize("name", fixture_names())
+def test_contraction_on_fixtures(name):
+    import paper_2106_06889_b200 as gt
+    try:
+        dag = gt.DeviceDag(gtdc(name))
+    except gt.GtadocError:
+        pytest.skip("invalid grammar")
+    with dag:
+        _check(dag)
+
+
+@pytest.mark.parametrize("src", ["c2@0.05", "c3@0.02", "c4@0.001", "c5@0.001"])
+def test_contraction_on_composed(src):
+    import paper_2106_06889_b200 as gt
+    name, sc = src.split("@")
+    with gt.DeviceDag(composed(name, float(sc))[0]) as dag:
+        _check(dag)
+
+
+WORD_TASKS = ["wordcount", "sort", "invertedindex", "termvector"]
+
+
+@pytest.mark.parametrize("src", ["c2@0.01", "c3@0.01", "c4@0.0005", "c5@0.0003"])
+def test_second_run_is_contracted_and_identical(src):
+    import paper_2106_06889_b200 as gt
+    from oracle.oracle import OracleDag
+    from test_gpu_parity import assert_same
+    name, sc = src.split("@")
+    blob = composed(name, float(sc))[0]
+    ref = OracleDag(blob)
+    cfg = gt.TraversalConfig(strategy="topdown")
+    with gt.DeviceDag(blob) as dag:
+        first = gt.run_compact(dag, "wordcount", cfg, 3)
+        assert not dag.refresh_info()["load_flags"] & 4  # a one-shot query keeps the full lists
+        assert_same(first, gt.run_compact(ref, "wordcount", cfg, 3), (src, "wordcount", "full"))
+        second = gt.run_compact_many(dag, WORD_TASKS, cfg, 3)
+        assert dag.refresh_info()["load_flags"] & 4
+        third = [gt.run_compact(dag, t, cfg, 3) for t in WORD_TASKS]
+        for t, b, c in zip(WORD_TASKS, second, third):
+            exp = gt.run_compact(ref, t, cfg, 3)
+            assert_same(b, exp, (src, t, "contracted"))
+            assert_same(c, exp, (src, t, "contracted, single task"))
