@@ -263,7 +263,8 @@ static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int 
   v.n_groups = R.n_groups;
   const u64 l = (u64)seq_len;
   static const bool wide = getenv("GT_D2H_U64") != nullptr;  // diagnostics: always u64 counts / offsets
-  if (!wide && R.n < (1ull << 32)) v.group_off32 = pull_narrow(r, R.group_off, R.n_groups + 1, st, &bytes);
+  if (!wide && R.group_off32_ok) v.group_off32 = pull<uint32_t>(r, R.group_off32, R.n_groups + 1, st, &bytes);
+  else if (!wide && R.n < (1ull << 32)) v.group_off32 = pull_narrow(r, R.group_off, R.n_groups + 1, st, &bytes);
   else v.group_off = pull<uint64_t>(r, R.group_off, R.n_groups + 1, st, &bytes);
   v.group_id = pull<uint32_t>(r, R.group_id, R.n_groups, st, &bytes);
   v.group_key = pull<uint64_t>(r, R.group_key, R.n_groups, st, &bytes);
@@ -271,7 +272,8 @@ static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int 
   v.id = pull<uint32_t>(r, R.id, R.n, st, &bytes);
   v.key = pull<uint64_t>(r, R.key, R.n, st, &bytes);
   v.gram = pull<uint32_t>(r, R.gram, R.n * l, st, &bytes);
-  if (!wide && count_bound && count_bound < (1ull << 32)) v.count32 = pull_narrow(r, R.count, R.n, st, &bytes);
+  if (!wide && R.count32_ok) v.count32 = pull<uint32_t>(r, R.count32, R.n, st, &bytes);
+  else if (!wide && count_bound && count_bound < (1ull << 32)) v.count32 = pull_narrow(r, R.count, R.n, st, &bytes);
   else v.count = pull<uint64_t>(r, R.count, R.n, st, &bytes);
   v.d2h_bytes = bytes;
   return bytes;

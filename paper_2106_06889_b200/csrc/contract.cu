@@ -16,8 +16,8 @@
 //     840k in 24;
 //   - edges H(p) -> c with frequency f·M(p) for every non-root edge p -> c
 //     into a head c (C2: 325k of 1.08M);
-//   - own pairs (word, H(r), f·M(r)) in the word-major ow order (no sort:
-//     the word keys do not change).
+//   - own pairs (word, H(r), f·M(r)), pairs of one word whose rules share a
+//     head merged into one (word-major like ow).
 // The per-file columns (per-file counts, presence bitsets) are linear in the
 // same way, column by column.  A product f·M(p) or f·M(r) of 2^32 or more
 // turns the contraction off (the lists stay u32).
@@ -131,18 +131,29 @@ __global__ void k_c_scatter(const u32* __restrict__ child, const u32* __restrict
   if (o) *ovf = 1;
 }
 
-// own pairs in ow order: source row tid'(H(r)), frequency f·M(r)
-__global__ void k_c_own(const u32* __restrict__ rule_t, const u32* __restrict__ freq, u64 n,
-                        const u32* __restrict__ ctid, const u32* __restrict__ hd, const u32* __restrict__ ml, u32* src,
-                        u32* fr, u32* ovf) {
+// own pairs keyed (word, tid'(H(r))) with f·M(r): pairs of the same word
+// whose rules share a head merge into one (sort + reduce by key)
+__global__ void k_c_own_keys(const u32* __restrict__ word, const u32* __restrict__ rule_t,
+                             const u32* __restrict__ freq, u64 n, const u32* __restrict__ ctid,
+                             const u32* __restrict__ hd, const u32* __restrict__ ml, u64* key, u64* val) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  bool o = false;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const u32 t = rule_t[i];
-    const u64 m = (u64)freq[i] * ml[t];
-    o |= m > 0xFFFFFFFFull;
-    src[i] = ctid[hd[t]];
-    fr[i] = (u32)m;
+    key[i] = ((u64)word[i] << 32) | ctid[hd[t]];
+    val[i] = (u64)freq[i] * ml[t];
+  }
+}
+
+__global__ void k_c_own_unpack(const u64* __restrict__ key, const u64* __restrict__ sum,
+                               const u64* __restrict__ n_dev, u32* word, u32* src, u32* fr, u32* ovf) {
+  const u64 n = *n_dev, stride = (u64)gridDim.x * blockDim.x;
+  bool o = false;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u64 k = key[i], v = sum[i];
+    o |= v > 0xFFFFFFFFull;
+    word[i] = (u32)(k >> 32);
+    src[i] = (u32)k;
+    fr[i] = (u32)v;
   }
   if (o) *ovf = 1;
 }
@@ -211,22 +222,32 @@ void ensure_contracted(DeviceDag* d) {
   }
   d->c_te_off_dev.alloc(((u64)nl + 3) * 8, st);
   LAUNCH(k_te_level_off, (u64)nl + 3, ls, incl, degt, R, (u64)nl, d->c_te_off_dev.as<u64>());
+  d->c_ow_word.alloc(Eo * 4 + 4, st);
   d->c_ow_src.alloc(Eo * 4 + 4, st);
   d->c_ow_freq.alloc(Eo * 4 + 4, st);
-  if (Eo)
-    LAUNCH(k_c_own, Eo, d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), Eo, d->c_tid.as<u32>(), hd, ml,
-           d->c_ow_src.as<u32>(), d->c_ow_freq.as<u32>(), ovf);
+  u64* n_own_dev = reinterpret_cast<u64*>(ovf) + 1;
+  GT_CUDA(cudaMemsetAsync(n_own_dev, 0, 8, st));
+  if (Eo) {
+    const Carve ow(st, {Eo * 8, Eo * 8, Eo * 8, Eo * 8});
+    u64 *k1 = ow.at<u64>(0), *k2 = ow.at<u64>(1), *v1 = ow.at<u64>(2), *v2 = ow.at<u64>(3);
+    LAUNCH(k_c_own_keys, Eo, d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), Eo,
+           d->c_tid.as<u32>(), hd, ml, k1, v1);
+    sort_pairs_u64_u64(k1, k2, v1, v2, Eo, 32 + std::max(1, bitlen(d->nw ? d->nw - 1 : 0)), st);
+    reduce_by_key_u64(k2, v2, k1, v1, n_own_dev, Eo, st);
+    LAUNCH(k_c_own_unpack, Eo, k1, v1, n_own_dev, d->c_ow_word.as<u32>(), d->c_ow_src.as<u32>(),
+           d->c_ow_freq.as<u32>(), ovf);
+  }
   d->contracted = true;  // (refresh_contracted_seeds maps the current seeds)
   refresh_contracted_seeds(d);
-  std::vector<u64> h(2 * ((u64)nl + 3) + 1);
+  std::vector<u64> h(2 * ((u64)nl + 3) + 2);
   GT_CUDA(cudaMemcpyAsync(h.data(), ls, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaMemcpyAsync(h.data() + nl + 3, d->c_te_off_dev.p, ((u64)nl + 3) * 8, cudaMemcpyDeviceToHost, st));
-  GT_CUDA(cudaMemcpyAsync(h.data() + 2 * (nl + 3), ovf, 4, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(h.data() + 2 * (nl + 3), ovf, 16, cudaMemcpyDeviceToHost, st));
   stream_sync(st);
   if ((u32)h[2 * (nl + 3)]) {  // a product outgrew 32 bits: the full lists stay in use
     d->contracted = false;
-    DBuf* bufs[] = {&d->c_tid, &d->c_te_child, &d->c_te_par, &d->c_te_freq, &d->c_te_off_dev, &d->c_ow_src,
-                    &d->c_ow_freq, &d->c_rs_rule_t};
+    DBuf* bufs[] = {&d->c_tid, &d->c_te_child, &d->c_te_par, &d->c_te_freq, &d->c_te_off_dev, &d->c_ow_word,
+                    &d->c_ow_src, &d->c_ow_freq, &d->c_rs_rule_t};
     for (DBuf* b : bufs) b->release();
     if (getenv("GT_TRACE")) fprintf(stderr, "[contract] off: a frequency times multiplier needs 64 bits\n");
     return;
@@ -236,12 +257,13 @@ void ensure_contracted(DeviceDag* d) {
     if (h[L + 1] > h[L]) ncl = L;
   d->c_levels = (u32)ncl;
   d->c_R = h[nl + 1];
+  d->c_n_own = h[2 * (nl + 3) + 1];
   d->c_te_off.assign(h.begin() + (nl + 3), h.begin() + (nl + 3) + (ncl + 3));
   d->load_flags |= 4;
   if (getenv("GT_TRACE"))
-    fprintf(stderr, "[contract] %llu heads of %llu rules, %llu of %llu edges, %d of %d levels\n",
+    fprintf(stderr, "[contract] %llu heads of %llu rules, %llu of %llu edges, %d of %d levels, %llu of %llu own pairs\n",
             (unsigned long long)d->c_R, (unsigned long long)R, (unsigned long long)d->c_te_off.back(),
-            (unsigned long long)Etd, ncl, nl);
+            (unsigned long long)Etd, ncl, nl, (unsigned long long)d->c_n_own, (unsigned long long)Eo);
 }
 
 void refresh_contracted_seeds(DeviceDag* d) {
@@ -258,9 +280,9 @@ TdLists td_lists(DeviceDag* d, bool contract) {
     if (policy == 2 || (policy == 1 && ++d->c_calls >= 2)) ensure_contracted(d);
   }
   TdLists t;
-  t.n_own = d->E_own;
-  t.ow_word = d->ow_word.as<u32>();
   if (contract && d->contracted) {
+    t.n_own = d->c_n_own;
+    t.ow_word = d->c_ow_word.as<u32>();
     t.rows = d->c_R;
     t.te_child = d->c_te_child.as<u32>(), t.te_par = d->c_te_par.as<u32>(), t.te_freq = d->c_te_freq.as<u32>();
     t.te_off_dev = d->c_te_off_dev.as<u64>(), t.te_off = &d->c_te_off, t.nl = (int)d->c_levels;
@@ -270,6 +292,8 @@ TdLists td_lists(DeviceDag* d, bool contract) {
     return t;
   }
   t.rows = d->R;
+  t.n_own = d->E_own;
+  t.ow_word = d->ow_word.as<u32>();
   t.te_child = d->te_child.as<u32>(), t.te_par = d->te_par.as<u32>(), t.te_freq = d->te_freq.as<u32>();
   t.te_off_dev = d->te_off_dev.as<u64>(), t.te_off = &d->te_off, t.nl = d->td.nl;
   t.ow_src = d->ow_rule_t.as<u32>(), t.ow_freq = d->ow_freq.as<u32>();

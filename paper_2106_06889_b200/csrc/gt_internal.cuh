@@ -180,14 +180,15 @@ struct DeviceDag {
   // Tid space: c_hd / c_ml / c_lvp = H (a tid), M and the contracted level
   // L' of every tid; c_tid maps tid -> tid' (heads by (L', tid), singles
   // last).  The pass then runs over the heads only: edges H(p) -> c with
-  // frequency f·M(p), own pairs (word, tid'(H(r)), f·M(r)) in ow order.
+  // frequency f·M(p), own pairs (word, tid'(H(r)), Σ f·M(r)) word-major.
   DBuf c_hd, c_ml, c_lvp;
   bool contracted = false;
   bool c_tried = false;  // built (or given up: a multiplier outgrew 32 bits)
   u32 c_calls = 0;       // top-down word runs served (the build policy)
   u32 c_levels = 0;
   u64 c_R = 0;           // heads
-  DBuf c_tid, c_te_child, c_te_par, c_te_freq, c_te_off_dev, c_ow_src, c_ow_freq, c_rs_rule_t;
+  u64 c_n_own = 0;       // merged own pairs
+  DBuf c_tid, c_te_child, c_te_par, c_te_freq, c_te_off_dev, c_ow_word, c_ow_src, c_ow_freq, c_rs_rule_t;
   std::vector<u64> c_te_off;
   // derived arrays (ensure_derived): no top-down word count / inverted
   // index reads them, so gt_open leaves them to the first task that does
@@ -208,7 +209,7 @@ struct DeviceDag {
                          &seg_tokens, &ow_word, &ow_rule, &ow_freq, &ow_off, &rs_rule, &rs_seg,
                          &rs_cnt, &rs_off, &rw_word, &rw_seg, &rw_cnt, &td.order, &bu.order,
                          &tid, &rs_rule_t, &ow_rule_t, &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts,
-                         &te_off_dev, &be_off_dev, &sub_rule, &c_hd, &c_ml, &c_lvp, &c_tid, &c_te_child, &c_te_par, &c_te_freq, &c_te_off_dev, &c_ow_src, &c_ow_freq,
+                         &te_off_dev, &be_off_dev, &sub_rule, &c_hd, &c_ml, &c_lvp, &c_tid, &c_te_child, &c_te_par, &c_te_freq, &c_te_off_dev, &c_ow_word, &c_ow_src, &c_ow_freq,
                          &c_rs_rule_t};
     u64 t = 0;
     for (const DBuf* b : all) t += b->bytes;

@@ -536,6 +536,10 @@ struct PostArgs {
   // boundaries — [0] entry, [1] seeds done, [2 + it] level it done, then the
   // word reduce and the compaction
   u64* stamps;
+  // compaction: u32 copies of the counts (saturating; tot[2] != 0 when one
+  // needed 64 bits) and of the group offsets, written beside the u64 ones
+  u32* rcnt32;
+  u32* goff32;
 };
 
 __device__ __forceinline__ void seg_stamp(u64* stamps, int k) {
@@ -651,11 +655,13 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
         p.tot[0] = xa + __ldcg(reinterpret_cast<const unsigned long long*>(p.bsum + blockIdx.x));
         p.tot[1] = xb + __ldcg(reinterpret_cast<const unsigned long long*>(p.bsum + nb + blockIdx.x));
         if (groups) p.goff[p.tot[1]] = p.tot[0];
+        if (groups && p.goff32) p.goff32[p.tot[1]] = (u32)p.tot[0];
       }
     }
   }
   __syncthreads();
   u64 ba = oa, bb = ob;
+  bool big = false;
   for (u64 t0 = lo; t0 < hi; t0 += blockDim.x) {  // block-uniform trip count
     const u64 w = t0 + threadIdx.x;
     u64 v = 0, pr = 0;
@@ -665,16 +671,21 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
     u32 ea, eb, ta, tb;
     block_scan2(a, b, &ea, &eb, &ta, &tb);
     if (nz) {
+      const u32 v32 = v > 0xFFFFFFFFull ? 0xFFFFFFFFu : (u32)v;
+      big |= v > 0xFFFFFFFFull;
       if (!groups) {
         p.rid[ba + ea] = (u32)w;
         p.rcnt[ba + ea] = v;
+        if (p.rcnt32) p.rcnt32[ba + ea] = v32;
       } else {
         if (p.compact == 3) {  // the word-count record of this word
           p.wid[bb + eb] = (u32)w;
           p.rcnt[bb + eb] = v;
+          if (p.rcnt32) p.rcnt32[bb + eb] = v32;
         }
         p.gid[bb + eb] = (u32)w;
         p.goff[bb + eb] = ba + ea;
+        if (p.goff32) p.goff32[bb + eb] = (u32)(ba + ea);
         u64 q = ba + ea, x = pr;
         while (x) {
           p.rid[q++] = p.file_lo + (u32)(__ffsll((long long)x) - 1);
@@ -685,6 +696,7 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
     ba += ta;
     bb += tb;
   }
+  if (big && p.rcnt32) atomicOr(reinterpret_cast<unsigned long long*>(p.tot + 2), 1ull);
 }
 
 template <class Mode, class T = u64>
@@ -791,6 +803,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
   constexpr bool pair = std::is_same<Mode, WcPresMode>::value;
   cg::grid_group grid = cg::this_grid();
   seg_stamp(post.stamps, 0);
+  if (post.rcnt32 && blockIdx.x == 0 && threadIdx.x == 0) post.tot[2] = 0;  // read after the compaction
   if (seed.row) {  // phase 0: clear the rows (and the reduce output), then the root seeds
     u64* zr = reinterpret_cast<u64*>(seed.row);
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < seed.zero_n; i += (u64)gridDim.x * blockDim.x)

@@ -336,14 +336,16 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   if (!small_task(d) || Fo > 64) return false;
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
-  // rows (pairs), presence, block sums, totals
-  const Carve cv(st, {d->R * 16, V * 8 + 8, 2 * 1024 * 8, 16});
+  // rows (pairs), presence, block sums, totals (+ the u32 overflow flag)
+  const Carve cv(st, {d->R * 16, V * 8 + 8, 2 * 1024 * 8, 24});
   d->word_counts.alloc(V * 8 + 8, st);
   wc->id.alloc(V * 4 + 4, st);
   wc->count.alloc(V * 8 + 8, st);
   ii->id.alloc(V * (u64)std::max<u32>(Fo, 1) * 4 + 4, st);
   ii->group_id.alloc(V * 4 + 4, st);
   ii->group_off.alloc((V + 1) * 8, st);
+  wc->count32.alloc(V * 4 + 4, st);
+  ii->group_off32.alloc((V + 1) * 4, st);  // (offsets < V * 64 < 2^32: small_task)
   u64* row = cv.at<u64>(0);
   const TdLists tl = td_lists(d, true);
   const SeedArgs seed{tl.rs_rule_t, d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
@@ -359,6 +361,8 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   post.goff = ii->group_off.as<u64>();
   post.tot = cv.at<u64>(3);
   post.bsum = cv.at<u64>(2);
+  post.rcnt32 = wc->count32.as<u32>();
+  post.goff32 = ii->group_off32.as<u32>();
   static const bool tr = getenv("GT_TRACE") && atoi(getenv("GT_TRACE")) == 2;
   DBuf stamps;
   if (tr) {
@@ -370,9 +374,11 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, 0,
                                  tl.nl ? (to[tl.nl + 1] - to[1]) / tl.nl : 0, &seed, &post,
                                  RowSrcPair{row}, TdRowsPair{row}, st);
-  u64 h[2];
-  GT_CUDA(cudaMemcpyAsync(h, post.tot, 16, cudaMemcpyDeviceToHost, st));
+  u64 h[3];
+  GT_CUDA(cudaMemcpyAsync(h, post.tot, 24, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
+  wc->count32_ok = h[2] == 0;
+  ii->group_off32_ok = true;
   if (tr) {
     u64 t[64];
     GT_CUDA(cudaMemcpy(t, stamps.p, 64 * 8, cudaMemcpyDeviceToHost));
@@ -489,6 +495,7 @@ void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW_out, DBuf* rows_out) {
 // one stable radix sort on (file << CB) | (W - count) carrying the id
 void order_by_count(DeviceDag* d, DevRecords* R, u32 ncols, const u32* file) {
   cudaStream_t st = d->stream;
+  R->count32_ok = false;  // (reordered below: the u32 copy no longer matches)
   const u64 n = R->n;
   const bool pf = ncols > 0;
   if (!n) return;

@@ -9,6 +9,10 @@ struct DevRecords {
   u64 n = 0, n_groups = 0;
   DBuf group_off, group_id, group_key, group_gram;  // u64, u32, u64, u32
   DBuf id, key, gram, count;                        // u32, u64, u32, u64
+  // u32 forms written by the producing kernel itself (the D2H skips the
+  // narrowing launch); valid only when the flag is set
+  DBuf count32, group_off32;
+  bool count32_ok = false, group_off32_ok = false;
 };
 
 void td_word_counts(DeviceDag* d, DBuf& counts);
