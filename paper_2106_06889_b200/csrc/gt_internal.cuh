@@ -59,7 +59,15 @@ struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaStream_t s = nullptr;
+  bool own = true;  // false: a view into memory held elsewhere (never freed here)
   DBuf() = default;
+  static DBuf view(void* q, size_t n) {
+    DBuf b;
+    b.p = q;
+    b.bytes = n;
+    b.own = false;
+    return b;
+  }
   DBuf(size_t n, cudaStream_t st) { alloc(n, st); }
   void alloc(size_t n, cudaStream_t st);
   void release();
@@ -73,8 +81,10 @@ struct DBuf {
       p = o.p;
       bytes = o.bytes;
       s = o.s;
+      own = o.own;
       o.p = nullptr;
       o.bytes = 0;
+      o.own = true;
     }
     return *this;
   }
@@ -201,6 +211,7 @@ struct DeviceDag {
   double init_ms = 0;
   // scratch kept across runs
   DBuf word_counts;  // u64[V] of the last global run
+  DBuf step_cache;   // the fused word count + inverted index step's buffers (grow-only)
 
   u64 bytes_held() const {
     const DBuf* all[] = {&body, &boff, &pos_owner, &root_seg, &own_ids, &own_freqs, &own_off,
@@ -209,7 +220,7 @@ struct DeviceDag {
                          &seg_tokens, &ow_word, &ow_rule, &ow_freq, &ow_off, &rs_rule, &rs_seg,
                          &rs_cnt, &rs_off, &rw_word, &rw_seg, &rw_cnt, &td.order, &bu.order,
                          &tid, &rs_rule_t, &ow_rule_t, &te_child, &te_par, &te_freq, &be_rule, &be_child, &be_freq, &word_counts,
-                         &te_off_dev, &be_off_dev, &sub_rule, &c_hd, &c_ml, &c_lvp, &c_tid, &c_te_child, &c_te_par, &c_te_freq, &c_te_off_dev, &c_ow_word, &c_ow_src, &c_ow_freq,
+                         &te_off_dev, &be_off_dev, &sub_rule, &step_cache, &c_hd, &c_ml, &c_lvp, &c_tid, &c_te_child, &c_te_par, &c_te_freq, &c_te_off_dev, &c_ow_word, &c_ow_src, &c_ow_freq,
                          &c_rs_rule_t};
     u64 t = 0;
     for (const DBuf* b : all) t += b->bytes;

@@ -64,6 +64,12 @@ void DBuf::alloc(size_t n, cudaStream_t st) {
 }
 
 void DBuf::release() {
+  if (p && !own) {
+    p = nullptr;
+    bytes = 0;
+    own = true;
+    return;
+  }
   if (p) {
     if (!trace2()) {
       cudaFreeAsync(p, s);

@@ -336,22 +336,34 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   if (!small_task(d) || Fo > 64) return false;
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
-  // rows (pairs), presence, block sums, totals (+ the u32 overflow flag)
-  const Carve cv(st, {d->R * 16, V * 8 + 8, 2 * 1024 * 8, 24});
-  d->word_counts.alloc(V * 8 + 8, st);
-  wc->id.alloc(V * 4 + 4, st);
-  wc->count.alloc(V * 8 + 8, st);
-  ii->id.alloc(V * (u64)std::max<u32>(Fo, 1) * 4 + 4, st);
-  ii->group_id.alloc(V * 4 + 4, st);
-  ii->group_off.alloc((V + 1) * 8, st);
-  wc->count32.alloc(V * 4 + 4, st);
-  ii->group_off32.alloc((V + 1) * 4, st);  // (offsets < V * 64 < 2^32: small_task)
-  u64* row = cv.at<u64>(0);
+  // every buffer of the step is carved from one grow-only block kept on the
+  // DAG (repeated steps allocate nothing; the records are views that the
+  // stream-ordered D2H reads before the next step on the stream rewrites
+  // them): rows (pairs), presence, block sums, totals (+ the u32 overflow
+  // flag), the dense counts, then the records
+  const size_t sz[] = {d->R * 16, V * 8 + 8, 2 * 1024 * 8, 24, V * 8 + 8, V * 4 + 4, V * 8 + 8, V * 4 + 4,
+                       V * (u64)std::max<u32>(Fo, 1) * 4 + 4, V * 4 + 4, (V + 1) * 8,
+                       (V + 1) * 4};  // (offsets < V * 64 < 2^32: small_task)
+  constexpr int NB = sizeof(sz) / sizeof(sz[0]);
+  size_t off[NB + 1] = {0};
+  for (int i = 0; i < NB; i++) off[i + 1] = off[i] + ((sz[i] + 255) & ~(size_t)255);
+  if (d->step_cache.bytes < off[NB]) d->step_cache.alloc(off[NB], st);
+  char* base = d->step_cache.as<char>();
+  auto at = [&](int i) { return base + off[i]; };
+  d->word_counts = DBuf::view(at(4), sz[4]);
+  wc->id = DBuf::view(at(5), sz[5]);
+  wc->count = DBuf::view(at(6), sz[6]);
+  wc->count32 = DBuf::view(at(7), sz[7]);
+  ii->id = DBuf::view(at(8), sz[8]);
+  ii->group_id = DBuf::view(at(9), sz[9]);
+  ii->group_off = DBuf::view(at(10), sz[10]);
+  ii->group_off32 = DBuf::view(at(11), sz[11]);
+  u64* row = reinterpret_cast<u64*>(at(0));
   const TdLists tl = td_lists(d, true);
   const SeedArgs seed{tl.rs_rule_t, d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
                       Fo, 1, 1u, row, 2 * tl.rows};
   PostArgs post{tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own,
-                d->word_counts.as<u64>(), V, cv.at<u64>(1), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
+                d->word_counts.as<u64>(), V, reinterpret_cast<u64*>(at(1)), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
                 d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, Fo, 1};
   post.compact = 3;
   post.wid = wc->id.as<u32>();
@@ -359,8 +371,8 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   post.rid = ii->id.as<u32>();
   post.gid = ii->group_id.as<u32>();
   post.goff = ii->group_off.as<u64>();
-  post.tot = cv.at<u64>(3);
-  post.bsum = cv.at<u64>(2);
+  post.tot = reinterpret_cast<u64*>(at(3));
+  post.bsum = reinterpret_cast<u64*>(at(2));
   post.rcnt32 = wc->count32.as<u32>();
   post.goff32 = ii->group_off32.as<u32>();
   static const bool tr = getenv("GT_TRACE") && atoi(getenv("GT_TRACE")) == 2;
