@@ -31,8 +31,13 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <chrono>
+
+#include <cooperative_groups.h>
 
 #include "kernels_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gt {
 
@@ -40,10 +45,18 @@ namespace gt {
 
 namespace {
 
-// non-root parent edges per child (tid)
+// non-root parent edges per child (tid).  A child's edges are contiguous in
+// the td lists, so one atomic per (warp, child) run: same-address atomics of
+// a warp would serialise in one L2 slice
 __global__ void k_c_count(const u32* __restrict__ child, u64 n, u32* cnt) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(&cnt[child[i]], 1u);
+  for (u64 b = (u64)blockIdx.x * blockDim.x; b < n; b += stride) {
+    const u64 i = b + threadIdx.x;
+    const bool ok = i < n;
+    const u32 c = ok ? child[i] : 0xFFFFFFFFu;
+    const unsigned same = __match_any_sync(0xFFFFFFFFu, c);
+    if (ok && (threadIdx.x & 31u) == (unsigned)(__ffs(same) - 1)) atomicAdd(&cnt[c], (u32)__popc(same));
+  }
 }
 
 // rules the root references (the unfiltered root lists)
@@ -62,24 +75,34 @@ __global__ void k_c_single(const u32* __restrict__ cnt, u64 R, uint8_t* flag) {
 // one top-down level's edges p -> c (every parent lies in an earlier level,
 // so its H / M / L' are final): a single child inherits (H(p), M(p)·f,
 // L'(p)); a head child raises its running max of L'(p) (lv holds the max
-// until k_c_final turns it into the head's own level)
-__global__ void k_c_level(const u32* __restrict__ child, const u32* __restrict__ par, const u32* __restrict__ freq,
-                          u64 n, const uint8_t* __restrict__ single, u32* hd, u32* ml, u32* lv, u32* ovf) {
-  const u64 stride = (u64)gridDim.x * blockDim.x;
+// until k_c_final turns it into the head's own level).
+// Every level in ONE cooperative launch (grid barriers between levels;
+// parents' H / M / L' written by other SMs are read through L2).
+__global__ void __launch_bounds__(512) k_c_levels(const u32* __restrict__ child, const u32* __restrict__ par,
+                                                  const u32* __restrict__ freq, const u64* __restrict__ off, int nl,
+                                                  const uint8_t* __restrict__ single, u32* hd, u32* ml, u32* lv,
+                                                  u32* ovf) {
+  cg::grid_group grid = cg::this_grid();
+  const u64 stride = (u64)gridDim.x * blockDim.x, t0 = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   bool o = false;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const u32 c = child[i], p = par[i];
-    const bool ps = single[p];
-    const u32 H = ps ? hd[p] : p, M = ps ? ml[p] : 1u, L = ps ? lv[p] : lv[p] + 1u;
-    if (single[c]) {
-      const u64 m = (u64)M * freq[i];
-      o |= m > 0xFFFFFFFFull;
-      hd[c] = H;
-      ml[c] = (u32)m;
-      lv[c] = L;
-    } else {
-      atomicMax(&lv[c], L);
+  for (int L = 1; L <= nl; L++) {
+    const u64 a = off[L], e = off[L + 1];
+    for (u64 i = a + t0; i < e; i += stride) {
+      const u32 c = child[i], p = par[i];
+      const bool ps = single[p];
+      const u32 H = ps ? __ldcg(hd + p) : p, M = ps ? __ldcg(ml + p) : 1u;
+      const u32 L2 = ps ? __ldcg(lv + p) : __ldcg(lv + p) + 1u;
+      if (single[c]) {
+        const u64 m = (u64)M * freq[i];
+        o |= m > 0xFFFFFFFFull;
+        hd[c] = H;
+        ml[c] = (u32)m;
+        lv[c] = L2;
+      } else {
+        atomicMax(&lv[c], L2);
+      }
     }
+    if (L < nl) grid.sync();
   }
   if (o) *ovf = 1;
 }
@@ -135,24 +158,24 @@ __global__ void k_c_scatter(const u32* __restrict__ child, const u32* __restrict
 // whose rules share a head merge into one (sort + reduce by key)
 __global__ void k_c_own_keys(const u32* __restrict__ word, const u32* __restrict__ rule_t,
                              const u32* __restrict__ freq, u64 n, const u32* __restrict__ ctid,
-                             const u32* __restrict__ hd, const u32* __restrict__ ml, u64* key, u64* val) {
+                             const u32* __restrict__ hd, const u32* __restrict__ ml, int sb, u64* key, u64* val) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const u32 t = rule_t[i];
-    key[i] = ((u64)word[i] << 32) | ctid[hd[t]];
+    key[i] = ((u64)word[i] << sb) | ctid[hd[t]];
     val[i] = (u64)freq[i] * ml[t];
   }
 }
 
 __global__ void k_c_own_unpack(const u64* __restrict__ key, const u64* __restrict__ sum,
-                               const u64* __restrict__ n_dev, u32* word, u32* src, u32* fr, u32* ovf) {
+                               const u64* __restrict__ n_dev, int sb, u32* word, u32* src, u32* fr, u32* ovf) {
   const u64 n = *n_dev, stride = (u64)gridDim.x * blockDim.x;
   bool o = false;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const u64 k = key[i], v = sum[i];
     o |= v > 0xFFFFFFFFull;
-    word[i] = (u32)(k >> 32);
-    src[i] = (u32)k;
+    word[i] = (u32)(k >> sb);
+    src[i] = (u32)(k & ((1ull << sb) - 1));
     fr[i] = (u32)v;
   }
   if (o) *ovf = 1;
@@ -163,6 +186,7 @@ __global__ void k_c_own_unpack(const u64* __restrict__ key, const u64* __restric
 void ensure_contracted(DeviceDag* d) {
   if (d->c_tried) return;
   d->c_tried = true;
+  const auto t0 = std::chrono::steady_clock::now();
   GT_CUDA(cudaSetDevice(d->device));
   cudaStream_t st = d->stream;
   const u64 R = d->R;
@@ -193,11 +217,26 @@ void ensure_contracted(DeviceDag* d) {
   if (nrs) LAUNCH(k_c_rootp, nrs, rs.as<u32>(), nrs, d->tid.as<u32>(), single);
   LAUNCH(k_c_single, R, cnt, R, single);
   // H / M / L' level by level (one launch per level; built once per DAG)
-  for (int L = 1; L <= nl; L++) {
-    const u64 a = d->te_off[L], n = d->te_off[L + 1] - a;
-    if (n)
-      LAUNCH(k_c_level, n, d->te_child.as<u32>() + a, d->te_par.as<u32>() + a, d->te_freq.as<u32>() + a, n, single,
-             hd, ml, lv, ovf);
+  {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_c_levels, 512, 0));
+      per_sm = std::max(1, std::min(per_sm, 4));
+    }
+    int nsm = 148;
+    GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d->device));
+    const u32* tc = d->te_child.as<u32>();
+    const u32* tp = d->te_par.as<u32>();
+    const u32* tf = d->te_freq.as<u32>();
+    const u64* to = d->te_off_dev.as<u64>();
+    int nlv = nl;
+    const uint8_t* sg = single;
+    void* args[] = {(void*)&tc, (void*)&tp, (void*)&tf, (void*)&to, (void*)&nlv, (void*)&sg,
+                    (void*)&hd, (void*)&ml, (void*)&lv, (void*)&ovf};
+    ProfScope ps("k_c_levels", st);
+    GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_c_levels, dim3((unsigned)(nsm * per_sm)), dim3(512), args, 0,
+                                        st));
+    g_launches++;
   }
   LAUNCH(k_c_final, R, single, R, (u32)nl + 1, hd, ml, lv, key);
   // tid': heads by (L', tid) (stable radix sort), singles last
@@ -230,11 +269,13 @@ void ensure_contracted(DeviceDag* d) {
   if (Eo) {
     const Carve ow(st, {Eo * 8, Eo * 8, Eo * 8, Eo * 8});
     u64 *k1 = ow.at<u64>(0), *k2 = ow.at<u64>(1), *v1 = ow.at<u64>(2), *v2 = ow.at<u64>(3);
+    // key (word, tid'): bitlen(R) + bitlen(V) bits (C2: 37, 5 radix passes)
+    const int sb = std::max(1, bitlen(R - 1));
     LAUNCH(k_c_own_keys, Eo, d->ow_word.as<u32>(), d->ow_rule_t.as<u32>(), d->ow_freq.as<u32>(), Eo,
-           d->c_tid.as<u32>(), hd, ml, k1, v1);
-    sort_pairs_u64_u64(k1, k2, v1, v2, Eo, 32 + std::max(1, bitlen(d->nw ? d->nw - 1 : 0)), st);
+           d->c_tid.as<u32>(), hd, ml, sb, k1, v1);
+    sort_pairs_u64_u64(k1, k2, v1, v2, Eo, sb + std::max(1, bitlen(d->nw ? d->nw - 1 : 0)), st);
     reduce_by_key_u64(k2, v2, k1, v1, n_own_dev, Eo, st);
-    LAUNCH(k_c_own_unpack, Eo, k1, v1, n_own_dev, d->c_ow_word.as<u32>(), d->c_ow_src.as<u32>(),
+    LAUNCH(k_c_own_unpack, Eo, k1, v1, n_own_dev, sb, d->c_ow_word.as<u32>(), d->c_ow_src.as<u32>(),
            d->c_ow_freq.as<u32>(), ovf);
   }
   d->contracted = true;  // (refresh_contracted_seeds maps the current seeds)
@@ -261,9 +302,12 @@ void ensure_contracted(DeviceDag* d) {
   d->c_te_off.assign(h.begin() + (nl + 3), h.begin() + (nl + 3) + (ncl + 3));
   d->load_flags |= 4;
   if (getenv("GT_TRACE"))
-    fprintf(stderr, "[contract] %llu heads of %llu rules, %llu of %llu edges, %d of %d levels, %llu of %llu own pairs\n",
+    fprintf(stderr,
+            "[contract] %llu heads of %llu rules, %llu of %llu edges, %d of %d levels, %llu of %llu own pairs; "
+            "built in %.3f ms\n",
             (unsigned long long)d->c_R, (unsigned long long)R, (unsigned long long)d->c_te_off.back(),
-            (unsigned long long)Etd, ncl, nl, (unsigned long long)d->c_n_own, (unsigned long long)Eo);
+            (unsigned long long)Etd, ncl, nl, (unsigned long long)d->c_n_own, (unsigned long long)Eo,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
 }
 
 void refresh_contracted_seeds(DeviceDag* d) {
