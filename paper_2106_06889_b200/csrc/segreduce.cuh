@@ -686,6 +686,8 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
         p.gid[bb + eb] = (u32)w;
         p.goff[bb + eb] = ba + ea;
         if (p.goff32) p.goff32[bb + eb] = (u32)(ba + ea);
+        // (each lane writes its own word's files; a warp-cooperative
+        // coalesced emission measured slower: C5 0.27 -> 0.32 ms)
         u64 q = ba + ea, x = pr;
         while (x) {
           p.rid[q++] = p.file_lo + (u32)(__ffsll((long long)x) - 1);

@@ -58,6 +58,27 @@ __global__ void k_root_words(const u32* __restrict__ rw_word, const u32* __restr
   }
 }
 
+// the compaction alone (large grammars: the level pass and the word reduce run
+// as their own full-occupancy launches before it); cooperative, one block per SM
+__global__ void __launch_bounds__(512) k_post_compact(PostArgs p) {
+  cg::grid_group grid = cg::this_grid();
+  post_compact(p, grid);
+}
+
+// the root's plain words into the {count, presence} pair outputs
+__global__ void k_root_words_pair(const u32* __restrict__ rw_word, const u32* __restrict__ rw_seg,
+                                  const u32* __restrict__ rw_cnt, u64 n, u32 file_lo, u32 nseg, u64* cnt,
+                                  u64* pres) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 sg = rw_seg[i] - file_lo;
+    if (sg >= nseg) continue;
+    const u32 w = rw_word[i];
+    atomicAdd((unsigned long long*)&cnt[w], (unsigned long long)rw_cnt[i]);
+    atomicOr((unsigned long long*)&pres[w], 1ull << (sg & 63u));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // assembly
 // ---------------------------------------------------------------------------
@@ -333,7 +354,14 @@ bool td_presence_records(DeviceDag* d, DevRecords* R) {
 // counts in d->word_counts like td_word_records.
 bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   const u32 Fo = (u32)(d->file_hi - d->file_lo);
-  if (!small_task(d) || Fo > 64) return false;
+  if (Fo > 64 || d->nw * 64 >= (1ull << 32)) return false;
+  // large grammars (> 4·10^6 own pairs) share the pass only over the
+  // contraction's heads, whose 16-byte pair rows stay in L2 for the word
+  // reduce's gathers (C5: 20 MB instead of 288 MB); then the level pass, the
+  // full-occupancy word reduce and the compaction are separate launches
+  const bool small = small_task(d);
+  const TdLists tl = td_lists(d, true);
+  if (!small && !tl.contracted) return false;
   cudaStream_t st = d->stream;
   const u64 V = d->nw;
   // every buffer of the step is carved from one grow-only block kept on the
@@ -359,7 +387,6 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   ii->group_off = DBuf::view(at(10), sz[10]);
   ii->group_off32 = DBuf::view(at(11), sz[11]);
   u64* row = reinterpret_cast<u64*>(at(0));
-  const TdLists tl = td_lists(d, true);
   const SeedArgs seed{tl.rs_rule_t, d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
                       Fo, 1, 1u, row, 2 * tl.rows};
   PostArgs post{tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own,
@@ -383,9 +410,40 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
     post.stamps = stamps.as<u64>();
   }
   const std::vector<u64>& to = *tl.te_off;
-  seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, 0,
-                                 tl.nl ? (to[tl.nl + 1] - to[1]) / tl.nl : 0, &seed, &post,
-                                 RowSrcPair{row}, TdRowsPair{row}, st);
+  const u64 avg = tl.nl ? (to[tl.nl + 1] - to[1]) / tl.nl : 0;
+  if (small) {
+    seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, 0, avg,
+                                   &seed, &post, RowSrcPair{row}, TdRowsPair{row}, st);
+  } else {
+    GT_CUDA(cudaMemsetAsync(post.out, 0, V * 8, st));
+    GT_CUDA(cudaMemsetAsync(post.out2, 0, V * 8, st));
+    GT_CUDA(cudaMemsetAsync(post.tot, 0, 24, st));
+    seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, 0, avg,
+                                   &seed, nullptr, RowSrcPair{row}, TdRowsPair{row}, st);
+    {  // (seg_reduce's C = 1 launch; its multi-column forms have no pair mode)
+      const u64 n = tl.n_own;
+      const int K = (int)std::min<u64>(16, std::max<u64>(1, pow2_floor(n / kResidentThreads)));
+      const u64 tiles = (n + 32ull * K - 1) / (32ull * K);
+      if (n)
+        GT_KLAUNCH("k_reduce_words", (k_segred1<WcPresMode, RowSrcPair, OutPair>), grid_for(tiles * 32, 256, 148u * 32u),
+                   256, st, tl.ow_word, tl.ow_src, tl.ow_freq, n, K, RowSrcPair{row}, OutPair{post.out, post.out2});
+    }
+    if (d->n_rw)
+      KL(k_root_words_pair, grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(),
+         d->n_rw, (u32)d->file_lo, Fo, post.out, post.out2);
+    int nsm = 148;
+    GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d->device));
+    static int per_sm = -1;  // every resident block (bsum holds 2 * 1024 block counts)
+    if (per_sm < 0) {
+      GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_post_compact, 512, 0));
+      per_sm = std::max(1, std::min(per_sm, 4));
+    }
+    void* args[] = {(void*)&post};
+    ProfScope ps("k_post_compact", st);
+    GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_post_compact, dim3((unsigned)(nsm * per_sm)), dim3(512), args,
+                                        0, st));
+    g_launches++;
+  }
   u64 h[3];
   GT_CUDA(cudaMemcpyAsync(h, post.tot, 24, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));

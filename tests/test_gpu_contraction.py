@@ -123,3 +123,29 @@ def test_second_run_is_contracted_and_identical(src):
             exp = gt.run_compact(ref, t, cfg, 3)
             assert_same(b, exp, (src, t, "contracted"))
             assert_same(c, exp, (src, t, "contracted, single task"))
+
+
+@pytest.mark.parametrize("src", ["c4@0.2", "c5@0.12"])
+def test_large_grammar_shared_pair_pass(src):
+    """> 4·10^6 own pairs: once contracted, word count + inverted index share
+    one pair pass (level launch, full-occupancy word reduce, compaction
+    launch) instead of two separate passes; both equal the oracle."""
+    import paper_2106_06889_b200 as gt
+    from oracle.oracle import OracleDag
+    from test_gpu_parity import assert_same
+    name, sc = src.split("@")
+    blob = composed(name, float(sc))[0]
+    cfg = gt.TraversalConfig(strategy="topdown")
+    tasks = ["wordcount", "invertedindex"]
+    with gt.DeviceDag(blob) as dag:
+        assert dag.info["own_pairs"] > 4 << 20
+        first = gt.run_compact_many(dag, tasks, cfg, 3)  # separate passes over every rule
+        second = gt.run_compact_many(dag, tasks, cfg, 3)  # builds the contraction, shared pass
+        assert dag.refresh_info()["load_flags"] & 4
+        third = gt.run_compact_many(dag, tasks, cfg, 3)
+    ref = OracleDag(blob)
+    for t, a, b, c in zip(tasks, first, second, third):
+        exp = gt.run_compact(ref, t, cfg, 3)
+        assert_same(a, exp, (src, t, "full"))
+        assert_same(b, exp, (src, t, "contracted"))
+        assert_same(c, exp, (src, t, "contracted again"))
