@@ -431,6 +431,17 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
     if (d->n_rw)
       KL(k_root_words_pair, grid_for(d->n_rw, 256), d->rw_word.as<u32>(), d->rw_seg.as<u32>(), d->rw_cnt.as<u32>(),
          d->n_rw, (u32)d->file_lo, Fo, post.out, post.out2);
+    // the records: one cooperative compaction, or on a large vocabulary the
+    // full-occupancy select / scan / emit kernels (the compaction walks each
+    // block's word range in barrier-separated steps: C5, 10^6 words, 0.26 vs
+    // 0.17 ms; C4, 10^5 words, 0.04 vs 0.09 ms).  GT_LARGE_ASSEMBLE=0/1 forces
+    static const int force = getenv("GT_LARGE_ASSEMBLE") ? atoi(getenv("GT_LARGE_ASSEMBLE")) : -1;
+    if (force == 1 || (force < 0 && V >= (1ull << 19))) {
+      assemble_counts(d, post.out, V, 0, false, wc);
+      assemble_presence(d, post.out2, 1, ii);
+      wc->count32_ok = ii->group_off32_ok = false;
+      return true;
+    }
     int nsm = 148;
     GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d->device));
     static int per_sm = -1;  // every resident block (bsum holds 2 * 1024 block counts)
