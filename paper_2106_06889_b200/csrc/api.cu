@@ -306,7 +306,18 @@ static void finish(gt_ctx* c, gt_result* r, DevRecords& R, int task, int seq_len
 
 extern "C" {
 
+// one count per public run call (gt_run, gt_run_many; a gt_run inside
+// gt_run_many is the same call): the contraction is built on a DAG's second
+static thread_local int g_run_depth = 0;
+struct RunCount {
+  RunCount(gt_ctx* c) {
+    if (g_run_depth++ == 0 && c) c->d.runs++;
+  }
+  ~RunCount() { g_run_depth--; }
+};
+
 int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, gt_result** out) {
+  RunCount rc_(c);
   *out = nullptr;
   gt_result* r = new gt_result();
   int status = guard([&] {
@@ -407,6 +418,7 @@ int gt_run(gt_ctx* c, int task, int seq_len, int strategy, int file_set_width, g
 
 int gt_run_many(gt_ctx* c, const int* tasks, int ntasks, int seq_len, int strategy, int file_set_width,
                 gt_result** outs) {
+  RunCount rc_(c);
   for (int i = 0; i < ntasks; i++) outs[i] = nullptr;
   if (ntasks < 0) {
     set_last_error("gt_run_many: negative task count");

@@ -194,7 +194,7 @@ struct DeviceDag {
   DBuf c_hd, c_ml, c_lvp;
   bool contracted = false;
   bool c_tried = false;  // built (or given up: a multiplier outgrew 32 bits)
-  u32 c_calls = 0;       // top-down word runs served (the build policy)
+  u32 runs = 0;          // public run calls served (gt_run / gt_run_many): the build policy
   u32 c_levels = 0;
   u64 c_R = 0;           // heads
   u64 c_n_own = 0;       // merged own pairs
@@ -248,8 +248,8 @@ struct TdLists {
   bool contracted = false;
 };
 // contract.cu: the pass's lists; `contract` asks for the heads-only lists,
-// which are built on the second such request (GT_CONTRACT=0: never, 2: on
-// the first)
+// which are built during the DAG's second public run call (GT_CONTRACT=0:
+// never, 2: on the first request)
 TdLists td_lists(DeviceDag* d, bool contract);
 void ensure_contracted(DeviceDag* d);
 void refresh_contracted_seeds(DeviceDag* d);  // after the owned file range changed
