@@ -400,10 +400,10 @@ __global__ void k_chain_check(const u32* pos, const u32* raw, u64 R, u64 n, u32*
 // chunk c at one of its first kWin words, so each chunk is summarised by a
 // kWin-entry table: entry offset -> (entry offset into chunk c+1, records
 // started in c) — one warp per chunk, one lane per candidate entry, walking
-// the chunk through L1.  Pointer doubling then runs over chunk STATES
-// (nchunks*kWin + END, ~n/32 of them, log2(nchunks) passes) instead of over
-// every word of the section (log2(R) passes over n words), and a final walk
-// per chunk writes the rule starts.  A table entry that would need a wider
+// the chunk through L1.  The chunk tables are then composed by groups of 32
+// (k_chain_up / k_chain_top / k_chain_down below) instead of pointer
+// doubling over every word of the section (log2(R) passes over n words), and
+// a final walk per chunk writes the rule starts.  A table entry that would need a wider
 // window is INVALID; if the true chain meets one (a record of >= kWin words
 // other than the root) or the section is malformed, the word-level doubling
 // above runs instead, and after it the host walk for the exact error.
@@ -453,52 +453,115 @@ __global__ void __launch_bounds__(kTabWarps * 32) k_chunk_tables(const u32* __re
   }
 }
 
-// all doubling levels in one cooperative launch: J_k = J_{k-1} o J_{k-1}
-// over the chunk states (counts summed; INVALID absorbs)
-__global__ void k_state_double_all(u32* nx, u32* ct, u64 S, int K) {
-  cg::grid_group grid = cg::this_grid();
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (int k = 1; k < K; k++) {
-    const u32* a_nx = nx + (u64)(k - 1) * S;
-    const u32* a_ct = ct + (u64)(k - 1) * S;
-    u32* b_nx = nx + (u64)k * S;
-    u32* b_ct = ct + (u64)k * S;
-    for (u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += stride) {
-      const u32 a = __ldcg(a_nx + s);
-      if (a == kStInvalid) {
-        b_nx[s] = kStInvalid;
-        b_ct[s] = 0;
-      } else {
-        b_nx[s] = __ldcg(a_nx + a);
-        b_ct[s] = __ldcg(a_ct + s) + __ldcg(a_ct + a);
-      }
-    }
-    grid.sync();
+// ---- chunk-chain composition by groups of 32 (replaces the doubling) -----
+// Level k has n_k "chunks", each a 32-entry table (state c*32 + o: entry
+// offset o into chunk c; END = n_k*32).  One warp per group of 32 chunks
+// stages the group's tables in shared memory and walks them from each of the
+// 32 entries of its first chunk (lane o), recording the entry state and the
+// records before each chunk of the path (path tables, for the way down) and
+// the group's exit as a level-(k+1) state.  ceil(log32(chunks)) levels up,
+// one warp-walk at the top, one expansion per level down: C2 2 levels (3.3k
+// chunks), C5 4 (70k), instead of log2(chunks) grid-synchronised doubling
+// passes over every state.
+constexpr int kChainWarps = 4;
+__global__ void __launch_bounds__(kChainWarps * 32) k_chain_up(const u32* __restrict__ nx, const u32* __restrict__ ct,
+                                                              u64 nck, u32* nx_up, u32* ct_up, u32* path_s,
+                                                              u32* path_c) {
+  __shared__ u32 snx[kChainWarps][32][33], sct[kChainWarps][32][33];
+  const u32 wib = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const u64 ng = (nck + 31) / 32;
+  const u64 g = (u64)blockIdx.x * kChainWarps + wib;
+  if (g >= ng) return;
+  const u64 c0 = g * 32, nc = nck - c0 < 32 ? nck - c0 : 32;
+  const u32 END = (u32)(nck * 32), END_UP = (u32)(ng * 32);
+#pragma unroll 4
+  for (u32 j = 0; j < (u32)nc; j++) {  // coalesced: chunk j's 32 entries
+    snx[wib][j][lane] = nx[(c0 + j) * 32 + lane];
+    sct[wib][j][lane] = ct[(c0 + j) * 32 + lane];
   }
+  __syncwarp();
+  u32 s = (u32)(c0 * 32 + lane), cum = 0;
+  u32* ps = path_s + (g * 32 + lane) * 32;
+  u32* pc = path_c + (g * 32 + lane) * 32;
+  for (u32 j = 0; j < (u32)nc; j++) {
+    ps[j] = s;
+    pc[j] = cum;
+    if (s == END || s == kStInvalid) continue;
+    if (s / 32 != c0 + j) {  // (cannot happen on a well-formed table)
+      s = kStInvalid;
+      continue;
+    }
+    const u32 x = s & 31u;
+    cum += sct[wib][j][x];
+    s = snx[wib][j][x];
+  }
+  u32 up;
+  if (s == END) up = END_UP;
+  else if (s == kStInvalid || s / 32 != c0 + 32 || (s / 32) % 32 != 0) up = kStInvalid;
+  else up = (u32)((g + 1) * 32 + (s & 31u));
+  nx_up[g * 32 + lane] = up;
+  ct_up[g * 32 + lane] = cum;
 }
 
-// the state of the chain after c chunk steps from (chunk 0, offset 0) and the
-// records started before chunk c; c == nch checks the end of the section
-__global__ void k_chunk_entry(const u32* __restrict__ nx, const u32* __restrict__ ct, u64 S, int K, u64 nch,
-                              u64 R, u32* entry, u32* base, u32* bad) {
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  const u32 END = (u32)(nch * kWin);
-  for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c <= nch; c += stride) {
-    u32 st = 0;
-    u64 b = 0;
-    for (int k = K - 1; k >= 0 && st != kStInvalid; k--)
-      if ((c >> k) & 1) {
-        b += ct[(u64)k * S + st];
-        st = nx[(u64)k * S + st];
-      }
-    if (c == nch) {
-      if (st != END || b != R - 1) *bad = 1;
-    } else if (st == kStInvalid || (st != END && st / kWin != c)) {
+// the top level (<= 32 chunks): one warp stages the tables, lane 0 walks the
+// chain from state 0; the walk must end at END having started R - 1 records
+__global__ void k_chain_top(const u32* __restrict__ nx, const u32* __restrict__ ct, u64 nck, u64 R, u32* entry,
+                            u32* base, u32* bad) {
+  __shared__ u32 snx[32][33], sct[32][33];
+  const u32 lane = threadIdx.x & 31u;
+  for (u32 j = 0; j < (u32)nck; j++) {
+    snx[j][lane] = nx[j * 32 + lane];
+    sct[j][lane] = ct[j * 32 + lane];
+  }
+  __syncwarp();
+  if (lane) return;
+  const u32 END = (u32)(nck * 32);
+  u32 s = 0;
+  u64 cum = 0;
+  for (u32 j = 0; j < (u32)nck; j++) {
+    entry[j] = s;
+    base[j] = (u32)cum;
+    if (s == END) continue;
+    if (s == kStInvalid || s / 32 != j) {
       *bad = 1;
-    } else {
-      entry[c] = st;
-      base[c] = (u32)b;
+      return;
     }
+    cum += sct[j][s & 31u];
+    s = snx[j][s & 31u];
+  }
+  if (s != END || cum != R - 1) *bad = 1;
+}
+
+// one level down: chunk c of level k enters at the path state of its group's
+// true entry (thread per chunk)
+__global__ void k_chain_down(const u32* __restrict__ path_s, const u32* __restrict__ path_c,
+                             const u32* __restrict__ entry_up, const u32* __restrict__ base_up, u64 nck, u32* entry,
+                             u32* base, u32* bad) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 ng = (nck + 31) / 32;
+  const u32 END = (u32)(nck * 32), END_UP = (u32)(ng * 32);
+  for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c < nck; c += stride) {
+    const u64 g = c / 32, j = c % 32;
+    const u32 e = entry_up[g];
+    if (e == END_UP) {
+      entry[c] = END;
+      base[c] = base_up[g];
+      continue;
+    }
+    if (e == kStInvalid || e / 32 != g) {
+      *bad = 1;
+      entry[c] = END;
+      continue;
+    }
+    const u64 k = (g * 32 + (e & 31u)) * 32 + j;
+    const u32 st = path_s[k];
+    if (st == kStInvalid || (st != END && st / 32 != c)) {
+      *bad = 1;
+      entry[c] = END;
+      continue;
+    }
+    entry[c] = st;
+    base[c] = base_up[g] + path_c[k];
   }
 }
 
@@ -1868,33 +1931,60 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     const u64 p1 = ok ? 1 + (u64)rd32(blob + P.rules_pos) : 0;  // the first record after the root
     if (ok && !words_only && P.R >= 2 && p1 < n) {
       const u64 nch = (n - p1 + kChunkB - 1) / kChunkB, S = nch * kWin + 1;
-      const int K2 = bitlen(nch);  // J_0 .. J_{K2-1} cover c <= nch chunk steps
-      const Carve cv(st, {(u64)K2 * S * 4, (u64)K2 * S * 4, nch * 4, nch * 4, 4, nch * kWin * kMaskW * 4});
-      const DPtr nx{cv.at<void>(0)}, ct{cv.at<void>(1)}, entry{cv.at<void>(2)}, base{cv.at<void>(3)},
-          bad{cv.at<void>(4)}, mask{cv.at<void>(5)};
-      GT_KLAUNCH("k_chunk_tables", k_chunk_tables, grid_for(nch * 32, kTabWarps * 32), kTabWarps * 32, st,
-                 raw.as<u32>(), n, p1, nch, nx.as<u32>(), ct.as<u32>(), mask.as<u32>());
-      if (K2 > 1) {
-        static int per_sm = -1;
-        if (per_sm < 0) {
-          GT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_state_double_all, 256, 0));
-          per_sm = std::max(1, std::min(per_sm, 4));
+      // level tables: level 0 from the chunk walks, then one per 32x fewer
+      // chunks up to <= 32 (sizes summed into one carve)
+      std::vector<u64> nk{nch};
+      while (nk.back() > 32) nk.push_back((nk.back() + 31) / 32);
+      const int NL = (int)nk.size();  // levels 0 .. NL-1; NL-1 is the top
+      std::vector<size_t> sz;
+      for (int k = 0; k < NL; k++) {
+        const u64 st_k = (k ? nk[k] * 32 : S) * 4;
+        sz.push_back(st_k);  // nx_k
+        sz.push_back(st_k);  // ct_k
+        sz.push_back(nk[k] * 4 + 4);  // entry_k
+        sz.push_back(nk[k] * 4 + 4);  // base_k
+        if (k + 1 < NL) {
+          sz.push_back(nk[k + 1] * 32 * 32 * 4);  // path_s_k
+          sz.push_back(nk[k + 1] * 32 * 32 * 4);  // path_c_k
         }
-        int nsm = 148;
-        GT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-        const unsigned blocks = (unsigned)std::max<u64>(1, std::min<u64>((u64)nsm * per_sm, (S + 255) / 256));
-        u32* nxp = nx.as<u32>();
-        u32* ctp = ct.as<u32>();
-        u64 Sv = S;
-        int Kv = K2;
-        void* args[] = {(void*)&nxp, (void*)&ctp, (void*)&Sv, (void*)&Kv};
-        ProfScope ps("k_state_double_all", st);
-        GT_CUDA(cudaLaunchCooperativeKernel((const void*)k_state_double_all, dim3(blocks), dim3(256), args, 0, st));
-        g_launches++;
       }
+      sz.push_back(4);                                 // bad
+      sz.push_back(nch * kWin * kMaskW * 4);           // masks
+      std::vector<size_t> off(sz.size());
+      size_t tot = 0;
+      for (size_t i = 0; i < sz.size(); i++) {
+        off[i] = tot;
+        tot += (sz[i] + 255) & ~(size_t)255;
+      }
+      DBuf blk(tot, st);
+      int ix = 0;
+      auto take = [&]() { return reinterpret_cast<u32*>(blk.as<char>() + off[ix++]); };
+      std::vector<u32*> nxk(NL), ctk(NL), enk(NL), bak(NL), psk(NL, nullptr), pck(NL, nullptr);
+      for (int k = 0; k < NL; k++) {
+        nxk[k] = take();
+        ctk[k] = take();
+        enk[k] = take();
+        bak[k] = take();
+        if (k + 1 < NL) {
+          psk[k] = take();
+          pck[k] = take();
+        }
+      }
+      u32* badp = take();
+      u32* maskp = take();
+      const DPtr entry{enk[0]}, base{bak[0]}, bad{badp}, mask{maskp};
+      GT_KLAUNCH("k_chunk_tables", k_chunk_tables, grid_for(nch * 32, kTabWarps * 32), kTabWarps * 32, st,
+                 raw.as<u32>(), n, p1, nch, nxk[0], ctk[0], mask.as<u32>());
       GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
-      LAUNCH(k_chunk_entry, nch + 1, nx.as<u32>(), ct.as<u32>(), S, K2, nch, P.R, entry.as<u32>(), base.as<u32>(),
-             bad.as<u32>());
+      for (int k = 0; k + 1 < NL; k++) {
+        const u64 ng = nk[k + 1];
+        GT_KLAUNCH("k_chain_up", k_chain_up, (unsigned)((ng + kChainWarps - 1) / kChainWarps), kChainWarps * 32, st,
+                   nxk[k], ctk[k], nk[k], nxk[k + 1], ctk[k + 1], psk[k], pck[k]);
+      }
+      GT_KLAUNCH("k_chain_top", k_chain_top, 1, 32, st, nxk[NL - 1], ctk[NL - 1], nk[NL - 1], P.R, enk[NL - 1],
+                 bak[NL - 1], badp);
+      for (int k = NL - 2; k >= 0; k--)
+        LAUNCH(k_chain_down, nk[k], psk[k], pck[k], enk[k + 1], bak[k + 1], nk[k], enk[k], bak[k], badp);
       LAUNCH(k_chunk_starts, nch * 32, p1, nch, P.R, entry.as<u32>(), base.as<u32>(), mask.as<u32>(),
              rstart.as<u32>());
       u32 b = 0;
