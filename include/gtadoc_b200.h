@@ -232,8 +232,13 @@ uint64_t* gt_device_word_counts(gt_ctx* ctx);
  * reference Dag field): name in {own_ids, own_freqs, own_off,
  * own_token_count, sub_ids, sub_freqs, sub_off, par_ids, par_freqs, par_off,
  * num_in_edge, num_out_edge, root_freq, exp_len, segments, td_level,
- * bu_level, weight}.  Returns the element count (call with out=NULL to
- * size), or -1 on error. */
+ * bu_level, weight}; device-layout diagnostics: tid (the top-down row of
+ * every rule), cont_head / cont_mult / cont_level / cont_row (the
+ * single-parent contraction in tid space: head tid, multiplier, contracted
+ * level, head row; building it if needed; empty when a multiplier outgrew
+ * 32 bits) and cont_sizes ([heads, head edges, levels] of a built
+ * contraction, else empty).  Returns the element count (call with out=NULL
+ * to size), or -1 on error. */
 int64_t gt_dag_array(gt_ctx* ctx, const char* name, int64_t* out, int64_t cap);
 
 /* Per-kernel timing: while enabled, every kernel launched by this thread is
