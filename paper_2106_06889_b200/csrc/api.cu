@@ -194,16 +194,16 @@ int gt_info_get(const gt_ctx* c, gt_info* o) {
 void gt_close(gt_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->d.device);
-  if (c->d.stream) cudaStreamSynchronize(c->d.stream);
+  // no host synchronisation: every device array is freed stream-ordered on
+  // the context's stream (after any work still queued there), events may be
+  // destroyed while pending, and the stream goes back to the pool for the
+  // next gt_open, whose work queues behind those frees
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   cudaStream_t s = c->d.stream;
   const int dev = c->d.device;
   delete c;  // DBuf destructors free on the stream
-  if (s) {
-    cudaStreamSynchronize(s);
-    stream_release(dev, s);
-  }
+  if (s) stream_release(dev, s);
 }
 
 }  // extern "C"
