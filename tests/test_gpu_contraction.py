@@ -149,3 +149,33 @@ def test_large_grammar_shared_pair_pass(src):
         assert_same(a, exp, (src, t, "full"))
         assert_same(b, exp, (src, t, "contracted"))
         assert_same(c, exp, (src, t, "contracted again"))
+
+
+def test_large_contracted_pass_on_file_shards():
+    """The shared large-grammar pass after gt_set_files: the contracted seeds
+    follow the owned file range, and the shards' word counts (summed) and
+    inverted indexes (combined in file order) equal the whole corpus."""
+    import torch
+
+    import paper_2106_06889_b200 as gt
+    from paper_2106_06889_b200._abi import TASK_IDS
+    from paper_2106_06889_b200.shard import DeviceRunner, combine
+    from test_shard_cpu import same_compact
+    blob = composed("c4", 0.2)[0]
+    cfg = gt.TraversalConfig(strategy="topdown")
+    with gt.DeviceDag(blob) as dag:
+        V = dag.info["num_words"]
+        gt.run_compact_many(dag, ["wordcount", "invertedindex"], cfg, 3)
+        whole = gt.run_compact_many(dag, ["wordcount", "invertedindex"], cfg, 3)  # contracted
+        assert dag.refresh_info()["load_flags"] & 4
+        acc = torch.zeros(V, dtype=torch.int64, device="cuda")
+        parts = []
+        for rank in range(3):
+            r = DeviceRunner(dag, rank, 3)
+            wc, ii = dag.run_many([TASK_IDS["wordcount"], TASK_IDS["invertedindex"]], 3, 0, 64)
+            acc += r.counts_tensor()
+            parts.append(ii)
+        same_compact(r.assemble(acc, "wordcount"), whole[0])
+        same_compact(combine(parts, "invertedindex", V), whole[1])
+        dag.set_files(0, 1 << 62)
+        same_compact(gt.run_compact_many(dag, ["wordcount", "invertedindex"], cfg, 3)[1], whole[1])
