@@ -448,13 +448,14 @@ int gt_run_many(gt_ctx* c, const int* tasks, int ntasks, int seq_len, int strate
         u64 launches0 = g_launches;
         GT_CUDA(cudaEventRecord(c->ev[0], st));
         DevRecords W, I;
-        if (!td_wc_ii_records(&d, &W, &I)) return;
+        const bool sort = tasks[iw] == GT_SORT;
+        if (!td_wc_ii_records(&d, &W, &I, sort ? nullptr : c->ev[1])) return;
         fused = true;
-        if (tasks[iw] == GT_SORT) {
+        if (sort) {
           ensure_derived(&d);
           order_by_count(&d, &W, 0, nullptr);
+          GT_CUDA(cudaEventRecord(c->ev[1], st));
         }
-        GT_CUDA(cudaEventRecord(c->ev[1], st));
         pull_records(rw, W, tasks[iw], seq_len, 0, GT_TOPDOWN, st, count_bound(d, tasks[iw]));
         pull_records(ri, I, GT_INVERTEDINDEX, seq_len, 0, GT_TOPDOWN, st);
         GT_CUDA(cudaEventRecord(c->ev[2], st));

@@ -352,7 +352,7 @@ bool td_presence_records(DeviceDag* d, DevRecords* R) {
 // compaction (compact 3: the word-count records and the inverted-index
 // groups have the same words in the same order).  Leaves the dense u64[V]
 // counts in d->word_counts like td_word_records.
-bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
+bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t done) {
   const u32 Fo = (u32)(d->file_hi - d->file_lo);
   if (Fo > 64 || d->nw * 64 >= (1ull << 32)) return false;
   // large grammars (> 4·10^6 own pairs) share the pass only over the
@@ -440,6 +440,7 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
       assemble_counts(d, post.out, V, 0, false, wc);
       assemble_presence(d, post.out2, 1, ii);
       wc->count32_ok = ii->group_off32_ok = false;
+      if (done) GT_CUDA(cudaEventRecord(done, st));
       return true;
     }
     int nsm = 148;
@@ -457,6 +458,7 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii) {
   }
   u64 h[3];
   GT_CUDA(cudaMemcpyAsync(h, post.tot, 24, cudaMemcpyDeviceToHost, st));
+  if (done) GT_CUDA(cudaEventRecord(done, st));
   GT_CUDA(cudaStreamSynchronize(st));
   wc->count32_ok = h[2] == 0;
   ii->group_off32_ok = true;

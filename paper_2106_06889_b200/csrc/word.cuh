@@ -19,7 +19,10 @@ void td_word_counts(DeviceDag* d, DBuf& counts);
 void td_file_counts(DeviceDag* d, DBuf& counts, bool* is32);
 bool td_word_records(DeviceDag* d, DevRecords* R);
 bool td_presence_records(DeviceDag* d, DevRecords* R);
-bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii);
+// done (optional): recorded on the stream once the device work is queued —
+// before the host waits for the record totals, so that an event pair around
+// the call times the device, not the host's wake-up
+bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t done = nullptr);
 void order_by_count(DeviceDag* d, DevRecords* R, u32 ncols, const u32* file);
 void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW, DBuf* rows_out = nullptr);
 void td_file_weights(DeviceDag* d, DBuf& w, u32* C, bool* is32);
