@@ -263,6 +263,58 @@ __global__ void k_long_write(const u32* __restrict__ hidx, const u64* __restrict
   }
 }
 
+// The root's distinct symbols by a dense histogram over the symbol space
+// when that space is not much larger than the root (C2: 9.4·10^5 symbols
+// for a 5.5·10^4-symbol root, C3: 2.0·10^5 for 6.5·10^6): one memset, one
+// atomic pass (one atomic per (warp, symbol)), one ordered select of the
+// nonzero counts — instead of radix-sorting the root.
+__global__ void k_root_hist(const u32* __restrict__ body, u64 L0, u32* hist) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 b = (u64)blockIdx.x * blockDim.x; b < L0; b += stride) {
+    const u64 p = b + threadIdx.x;
+    const bool ok = p < L0;
+    const u32 sym = ok ? body[p] : 0xFFFFFFFFu;
+    const unsigned same = __match_any_sync(0xFFFFFFFFu, sym);
+    if (ok && (threadIdx.x & 31u) == (unsigned)(__ffs(same) - 1)) atomicAdd(&hist[sym], (u32)__popc(same));
+  }
+}
+
+// the root's runs (ascending symbols: words, then rules; the splitter range
+// was cleared) into its tsym / tcnt rows at body offset 0, and its counts
+__global__ void k_root_runs(const u32* __restrict__ idx, const u64* __restrict__ n_dev,
+                            const u32* __restrict__ hist, u64 nw, u64 base, u32* tsym, u32* tcnt, u32* n_own,
+                            u32* n_sub, u64* own_tok, u64* num_out) {
+  const u64 n = *n_dev;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 b = (u64)blockIdx.x * blockDim.x; b < n; b += stride) {
+    const u64 u = b + threadIdx.x;
+    u32 a = 0, c = 0;
+    u64 t = 0, o = 0;
+    if (u < n) {
+      const u32 sym = idx[u], k = hist[sym];
+      const bool own = sym < nw;
+      tsym[u] = own ? sym : (u32)(sym - base);
+      tcnt[u] = k;
+      a = own, c = !own;
+      t = own ? k : 0;
+      o = own ? 0 : k;
+    }
+    a = __reduce_add_sync(0xFFFFFFFFu, a);
+    c = __reduce_add_sync(0xFFFFFFFFu, c);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      t += __shfl_xor_sync(0xFFFFFFFFu, t, d);
+      o += __shfl_xor_sync(0xFFFFFFFFu, o, d);
+    }
+    if ((threadIdx.x & 31u) == 0) {
+      if (a) atomicAdd(&n_own[0], a);
+      if (c) atomicAdd(&n_sub[0], c);
+      if (t) atomicAdd((unsigned long long*)&own_tok[0], (unsigned long long)t);
+      if (o) atomicAdd((unsigned long long*)&num_out[0], (unsigned long long)o);
+    }
+  }
+}
+
 __global__ void k_widen_u32(const u32* a, u64 n, u64* b) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) b[i] = i < n ? a[i] : 0;
@@ -336,7 +388,18 @@ static bool rule_pairs_root_only(DeviceDag* d, const u32* owner, DBuf& own_rule,
   d->num_out.alloc(R * 8, st);
   CK(k_rules_short, R, body, boff, R, nw, base, tsym, tcnt, n_own, n_sub, d->own_tok.as<u64>(),
      d->num_out.as<u64>(), lflag, reinterpret_cast<u32*>(cnt));
-  if (L0 > kShort) {  // the root: sorted in place, its runs written at offset 0
+  const u64 limit = nw + d->ns + R;
+  static const bool root_sort = getenv("GT_ROOT_SORT") != nullptr;  // diagnostics: always sort the root
+  if (L0 > kShort && !root_sort && limit <= std::max<u64>(4 * L0, 1ull << 22)) {
+    // the root's runs from a dense histogram (k_root_hist)
+    DBuf hist(limit * 4 + 4, st), idx(std::min(limit, L0) * 4 + 4, st);
+    GT_CUDA(cudaMemsetAsync(hist.p, 0, limit * 4, st));
+    CK(k_root_hist, L0, body, L0, hist.as<u32>());
+    if (d->ns) GT_CUDA(cudaMemsetAsync(hist.as<u32>() + nw, 0, d->ns * 4, st));  // splitters are no pairs
+    select_nonzero_index(hist.p, true, idx.as<u32>(), cnt + 2, limit, st);
+    CK(k_root_runs, std::min(limit, L0), idx.as<u32>(), cnt + 2, hist.as<u32>(), nw, base, tsym, tcnt, n_own, n_sub,
+       d->own_tok.as<u64>(), d->num_out.as<u64>());
+  } else if (L0 > kShort) {  // the root: sorted in place, its runs written at offset 0
     u32* sbody = a.at<u32>(SBODY);
     sort_keys_u32(body, sbody, L0, std::max(1, bitlen(d->nw + d->ns + R - 1)), st);
     CK(k_long_heads, L0, owner, lflag, boff, sbody, L0, a.at<uint8_t>(HEAD));
