@@ -1466,6 +1466,108 @@ __global__ void k_te_scatter(const u32* __restrict__ prule, const u32* __restric
 
 // level offsets of the td edge lists: off[L] = first edge whose child is in
 // level >= L (ls[L] = first tid of level >= L, L = 0..nl+1), off[nl+2] = all
+// ---- stable counting sort by a small key (the level numberings) -----------
+// n keys in [0, nb) with nb <= kLoBins: ord[i] = the i-th element in (key,
+// index) order, rank[e] = its position, starts[k] = the first position of
+// key k (k = 0..nb; starts[nb] = n).  Three launches (per-block counts, one
+// single-block scan, a stable block-ordered scatter) instead of a radix sort,
+// a rank pass and a binary search per key.
+constexpr int kLoBins = 64, kLoBlock = 1024;
+__global__ void __launch_bounds__(kLoBlock) k_lo_count(const u32* __restrict__ key, u64 n, u64 chunk, u32 nb,
+                                                     u32* cnt) {
+  __shared__ u32 h[kLoBins];
+  for (u32 i = threadIdx.x; i < kLoBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const u64 lo = (u64)blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+  for (u64 b = lo; b < hi; b += blockDim.x) {
+    const u64 i = b + threadIdx.x;
+    const u32 k = i < hi ? key[i] : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, k);
+    if (k != 0xFFFFFFFFu && (threadIdx.x & 31u) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&h[k], (u32)__popc(peers));
+  }
+  __syncthreads();
+  for (u32 k = threadIdx.x; k < nb; k += blockDim.x) cnt[(u64)k * gridDim.x + blockIdx.x] = h[k];
+}
+
+// exclusive scan of the (key-major) block counts in place; starts[k] = the
+// offset of key k in block 0
+__global__ void __launch_bounds__(kLoBlock) k_lo_scan(u32* cnt, u32 nblk, u32 nb, u64 n, u64* starts) {
+  __shared__ u32 wsum[32];
+  __shared__ u32 carry;
+  const u32 m = nblk * nb, lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 t0 = 0; t0 < m; t0 += blockDim.x) {
+    const u32 i = t0 + threadIdx.x;
+    const u32 v = i < m ? cnt[i] : 0u;
+    u32 x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+      if (lane >= (u32)d) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      u32 z = lane < blockDim.x / 32 ? wsum[lane] : 0u;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(0xFFFFFFFFu, z, d);
+        if (lane >= (u32)d) z += y;
+      }
+      wsum[lane] = z;  // inclusive over warps
+    }
+    __syncthreads();
+    const u32 c0 = carry;
+    const u32 ex = c0 + (w ? wsum[w - 1] : 0u) + x - v;
+    if (i < m) {
+      cnt[i] = ex;
+      if (i % nblk == 0) starts[i / nblk] = ex;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c0 + wsum[blockDim.x / 32 - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) starts[nb] = n;
+}
+
+__global__ void __launch_bounds__(kLoBlock) k_lo_scatter(const u32* __restrict__ key, u64 n, u64 chunk, u32 nb,
+                                                       const u32* __restrict__ off, u32* ord, u32* rank) {
+  __shared__ u32 run[kLoBins], tt[kLoBins];
+  __shared__ u32 wc[kLoBlock / 32][kLoBins];
+  const u32 lane = threadIdx.x & 31u, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (u32 k = threadIdx.x; k < nb; k += blockDim.x) run[k] = off[(u64)k * gridDim.x + blockIdx.x];
+  const u64 lo = (u64)blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+  for (u64 b = lo; b < hi; b += blockDim.x) {
+    for (u32 k = lane; k < kLoBins; k += 32) wc[w][k] = 0;
+    __syncthreads();
+    const u64 i = b + threadIdx.x;
+    const bool ok = i < hi;
+    const u32 k = ok ? key[i] : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, k);
+    const u32 r = __popc(peers & ((1u << lane) - 1u));
+    if (ok && r == 0) wc[w][k] = (u32)__popc(peers);
+    __syncthreads();
+    if (threadIdx.x < nb) {  // exclusive prefix over the warps, per key
+      u32 a = 0;
+      for (u32 q = 0; q < nw; q++) {
+        const u32 c = wc[q][threadIdx.x];
+        wc[q][threadIdx.x] = a;
+        a += c;
+      }
+      tt[threadIdx.x] = a;
+    }
+    __syncthreads();
+    if (ok) {
+      const u32 pos = run[k] + wc[w][k] + r;
+      ord[pos] = (u32)i;
+      rank[i] = pos;
+    }
+    __syncthreads();
+    if (threadIdx.x < nb) run[threadIdx.x] += tt[threadIdx.x];
+  }
+}
+
 // k_unpack3 over the first *n_dev records (the count stays on the device)
 __global__ void k_unpack3_n(const U3* __restrict__ in, const u32* __restrict__ n_dev, u32* a, u32* b, u32* c) {
   const u64 n = *n_dev;
@@ -2467,12 +2569,25 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     u32 *iota = cv.at<u32>(0), *slev = cv.at<u32>(1), *ord = cv.at<u32>(2), *degt = cv.at<u32>(3),
         *incl = cv.at<u32>(4), *cur = cv.at<u32>(5);
     u64* ls = cv.at<u64>(6);
-    LAUNCH(k_iota_u32, R, iota, R);
-    sort_pairs_u32_u32(d->td_level.as<u32>(), slev, iota, ord, R, std::max(1, bitlen((u64)ntd)), st);
     d->tid.alloc(R * 4, st);
-    LAUNCH(k_rank_of, R, ord, R, d->tid.as<u32>());
-    // td: the non-root parent edges of every child, children in tid order
-    LAUNCH(k_csr_offsets, (u64)ntd + 2, slev, R, (u64)ntd + 1, ls);
+    if ((u64)ntd + 1 <= (u64)kLoBins && R < (1ull << 32)) {
+      // levels 0..ntd: the stable counting sort gives ord, tid and the level starts
+      const u64 nblk = std::min<u64>(1024, std::max<u64>(1, (R + 4095) / 4096));
+      const u64 chunk = (R + nblk - 1) / nblk;
+      const u32 nb = (u32)ntd + 1;
+      DBuf lcb(nblk * nb * 4 + 4, st);
+      u32* lcnt = lcb.as<u32>();
+      GT_KLAUNCH("k_lo_count", k_lo_count, (unsigned)nblk, kLoBlock, st, d->td_level.as<u32>(), R, chunk, nb, lcnt);
+      GT_KLAUNCH("k_lo_scan", k_lo_scan, 1, kLoBlock, st, lcnt, (u32)nblk, nb, R, ls);
+      GT_KLAUNCH("k_lo_scatter", k_lo_scatter, (unsigned)nblk, kLoBlock, st, d->td_level.as<u32>(), R, chunk, nb,
+                 (const u32*)lcnt, ord, d->tid.as<u32>());
+    } else {
+      LAUNCH(k_iota_u32, R, iota, R);
+      sort_pairs_u32_u32(d->td_level.as<u32>(), slev, iota, ord, R, std::max(1, bitlen((u64)ntd)), st);
+      LAUNCH(k_rank_of, R, ord, R, d->tid.as<u32>());
+      // td: the non-root parent edges of every child, children in tid order
+      LAUNCH(k_csr_offsets, (u64)ntd + 2, slev, R, (u64)ntd + 1, ls);
+    }
     LAUNCH(k_map_u32, R, ord, R, indeg.as<u32>(), degt);
     inclusive_scan_u32(degt, incl, R, st);
     LAUNCH(k_cursor, R, degt, incl, R, cur);
