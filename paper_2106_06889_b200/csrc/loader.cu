@@ -342,11 +342,6 @@ static void host_range_check(const uint8_t* d, const Parse& P, u64 upto) {
 // device kernels of the build
 // ---------------------------------------------------------------------------
 
-__global__ void k_mark_len(const u32* rstart, u64 R, u32* mark) {
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += stride)
-    mark[rstart[i] - 1] = 1;
-}
 
 // ---- rule-chain parse on the device (pointer doubling) ----------------------
 // The rules section is a chain of (length, body) records: record i starts at
@@ -604,19 +599,78 @@ __global__ void k_boff(const u32* rstart, u64 R, u64 E, u64* boff) {
     boff[i] = i < R ? (u64)rstart[i] - (i + 1) : E;
 }
 
-__global__ void k_unpack(const u32* raw, const u32* mark, const u32* incl, u64 n, u32* body,
-                         u32* owner, u64 limit, u32* bad_rule) {
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
-    if (mark[p]) continue;
-    u32 r = incl[p] - 1;
-    u64 i = p - ((u64)r + 1);
-    u32 s = raw[p];
-    body[i] = s;
-    owner[i] = r;
-    if ((u64)s >= limit) atomicMin(bad_rule, r);
+// Rule bodies unpacked straight from the records (rstart[r] = first body
+// word of rule r; the body runs to the next record's length word): a thread
+// per rule of at most 32 symbols; longer bodies (the root) are queued for
+// k_unpack_long, which spreads them over the grid.  Replaces a mark array
+// over every raw word, its scan and a pass over every raw word.
+constexpr u32 kUnpackShort = 32;
+__global__ void k_unpack_rules(const u32* __restrict__ raw, const u32* __restrict__ rstart, u64 R, u64 nraw,
+                               u32* body, u32* owner, u64 limit, u32* bad_rule, u32* longq, u32* nlong) {
+  // a warp takes 32 consecutive rules and writes their (contiguous) bodies
+  // together: output q of the warp goes to lane q % 32 (coalesced), its rule
+  // found by a shuffle search over the lanes' body offsets
+  const unsigned lane = threadIdx.x & 31u;
+  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 r0 = warp * 32; r0 < R; r0 += nwarps * 32) {
+    const u64 r = r0 + lane;
+    u32 len = 0, s = 0;
+    if (r < R) {
+      s = rstart[r];
+      const u64 e = r + 1 < R ? (u64)rstart[r + 1] - 1 : nraw;
+      if (e - s > kUnpackShort) longq[atomicAdd(nlong, 1u)] = (u32)r;  // the long body: k_unpack_long
+      else len = (u32)(e - s);
+    }
+    u32 x = len;  // inclusive prefix of the short lengths
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+      if (lane >= (unsigned)d) x += y;
+    }
+    const u32 pre = x - len, tot = __shfl_sync(0xFFFFFFFFu, x, 31);
+    for (u32 q0 = 0; q0 < tot; q0 += 32) {
+      const u32 q = q0 + lane;
+      int o = 0;  // the last lane whose short body starts at or before q
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const u32 pv = __shfl_sync(0xFFFFFFFFu, pre, (o + step) & 31);
+        if (o + step < 32 && pv <= q) o += step;
+      }
+      const u32 so = __shfl_sync(0xFFFFFFFFu, s, o), po = __shfl_sync(0xFFFFFFFFu, pre, o);
+      if (q < tot) {
+        const u64 ro = r0 + (u64)o, p = (u64)so + (q - po);
+        const u32 v = raw[p];
+        body[p - (ro + 1)] = v;
+        owner[p - (ro + 1)] = (u32)ro;
+        if ((u64)v >= limit) atomicMin(bad_rule, (u32)ro);
+      }
+    }
   }
 }
+
+__global__ void k_unpack_long(const u32* __restrict__ raw, const u32* __restrict__ rstart, u64 R, u64 nraw,
+                              const u32* __restrict__ longq, const u32* __restrict__ nlong, u32* body, u32* owner,
+                              u64 limit, u32* bad_rule) {
+  const u32 n = *nlong;
+  // few long bodies (the root): each over the whole grid; many: a block each
+  const bool spread = n <= 64;
+  const u64 stride = spread ? (u64)gridDim.x * blockDim.x : blockDim.x;
+  const u64 t0 = spread ? (u64)blockIdx.x * blockDim.x + threadIdx.x : threadIdx.x;
+  for (u32 q = spread ? 0 : blockIdx.x; q < n; q += spread ? 1 : gridDim.x) {
+    const u64 r = longq[q];
+    const u64 s = rstart[r], e = r + 1 < R ? (u64)rstart[r + 1] - 1 : nraw, b = s - (r + 1);
+    bool bad = false;
+    for (u64 p = s + t0; p < e; p += stride) {
+      const u32 v = raw[p];
+      body[b + (p - s)] = v;
+      owner[b + (p - s)] = (u32)r;
+      bad |= (u64)v >= limit;
+    }
+    if (bad) atomicMin(bad_rule, (u32)r);
+  }
+}
+
 
 __global__ void k_make_keys(const u32* body, const u32* owner, u64 E, int SB, u64* keys) {
   u64 stride = (u64)gridDim.x * blockDim.x;
@@ -2134,23 +2188,22 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   const u64 nraw = E + R;
 
   // ---- unpack --------------------------------------------------------------
-  DBuf mark(nraw * 4 + 4, st), incl(nraw * 4 + 4, st);
   DBuf& owner = d->pos_owner;
   owner.alloc(E * 4 + 4, st);
-  DBuf bad(4, st);
+  DBuf bad(16, st), longq(R * 4 + 4, st);
   d->body.alloc(E * 4 + 4, st);
   d->boff.alloc((R + 1) * 8, st);
   if (host_chain) GT_CUDA(cudaMemcpyAsync(rstart.p, P.rstart, R * 4, cudaMemcpyHostToDevice, st));
   LAUNCH(k_boff, R + 1, rstart.as<u32>(), R, E, d->boff.as<u64>());
-  GT_CUDA(cudaMemsetAsync(mark.p, 0, nraw * 4, st));
   GT_CUDA(cudaMemsetAsync(bad.p, 0xFF, 4, st));
-  LAUNCH(k_mark_len, R, rstart.as<u32>(), R, mark.as<u32>());
-  inclusive_scan_u32(mark.as<u32>(), incl.as<u32>(), nraw, st);
-  LAUNCH(k_unpack, nraw, raw.as<u32>(), mark.as<u32>(), incl.as<u32>(), nraw, d->body.as<u32>(),
-         owner.as<u32>(), limit, bad.as<u32>());
+  GT_CUDA(cudaMemsetAsync(bad.as<u32>() + 1, 0, 4, st));
+  LAUNCH(k_unpack_rules, R, raw.as<u32>(), rstart.as<u32>(), R, nraw, d->body.as<u32>(), owner.as<u32>(), limit,
+         bad.as<u32>(), longq.as<u32>(), bad.as<u32>() + 1);
+  GT_KLAUNCH("k_unpack_long", k_unpack_long, grid_for(nraw, 256), 256, st, raw.as<u32>(),
+             rstart.as<u32>(), R, nraw, longq.as<u32>(), bad.as<u32>() + 1, d->body.as<u32>(), owner.as<u32>(), limit,
+             bad.as<u32>());
   raw.release();
-  mark.release();
-  incl.release();
+  longq.release();
   rstart.release();
   u32 bad_rule;
   d2h(&bad_rule, bad.p, 1, st);
