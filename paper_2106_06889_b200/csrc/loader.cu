@@ -1709,7 +1709,7 @@ __global__ void k_segments(const u32* spos, u64 F, u64 L0, bool headless, u64* l
 }
 
 // root positions -> (rule|word, segment) keys; class flags
-__global__ void k_root_keys(const u32* body, const u32* seg_incl, u64 L0, u64 nw, u64 base,
+__global__ void k_root_keys(const u32* body, const u32* seg_incl, u64 L0, u64 nw, u64 base, u64 limit,
                             int SBF, bool headless, u64* rkey, uint8_t* isr, u64* wkey,
                             uint8_t* isw, u32* seg_of) {
   u64 stride = (u64)gridDim.x * blockDim.x;
@@ -1717,7 +1717,8 @@ __global__ void k_root_keys(const u32* body, const u32* seg_incl, u64 L0, u64 nw
     u32 s = body[p];
     u32 seg = headless ? 0u : seg_incl[p];  // splitters before p (p itself not a splitter)
     seg_of[p] = seg;
-    bool rr = s >= base, ww = s < nw;
+    // (a symbol past the rules is reported by the unpack; here it is no occurrence)
+    bool rr = s >= base && s < limit, ww = s < nw;
     isr[p] = rr;
     isw[p] = ww;
     rkey[p] = rr ? (((u64)(s - base) << SBF) | seg) : 0;
@@ -2065,6 +2066,135 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   DBuf raw(nsec * 4 + 4, st);
   if (nsec) GT_CUDA(cudaMemcpyAsync(raw.p, dblob.as<uint8_t>() + P.rules_pos, nsec * 4, cudaMemcpyDeviceToDevice, st));
   dblob.release();
+  // ---- root side (splitters, segments, root occurrence lists): only needs
+  // the root body, so it runs on its own stream and host thread while the
+  // main pipeline builds the CSR, the layering and the level lists; its
+  // errors are raised after the main pipeline's, in the reference's order
+  // (dag.py:131-230: cycle, unreachable, then _segments_of_root)
+  // (the root is the first record of the section: its body is raw[1, 1 + L0)
+  // whatever the rest of the chain holds; a length past the section fails
+  // the chain parse below, the root side then reads a clamped range)
+  const u64 rR = P.R, rnw = P.nw, rns = P.ns, rbase = rnw + rns, rlimit = rbase + rR;
+  const u64 L0 = rR && nsec ? std::min<u64>(rd32(blob + P.rules_pos), nsec - 1) : 0;  // the root's body length
+  const u32* rbody = raw.as<u32>() + 1;
+  d->L0 = L0;
+  cudaEvent_t ev_body;
+  GT_CUDA(cudaEventCreateWithFlags(&ev_body, cudaEventDisableTiming));
+  GT_CUDA(cudaEventRecord(ev_body, st));
+  Error root_err{GT_OK, ""};
+  cudaStream_t s_root = stream_acquire(device);
+  auto root_side = [&]() {
+    try {
+      GT_CUDA(cudaSetDevice(device));
+      cudaStream_t st = s_root;
+      GT_CUDA(cudaStreamWaitEvent(st, ev_body, 0));
+      DBuf cnt(16, st);
+  // ---- root segments (dag.py:107-128) -------------------------------------
+    const bool headless = rns == 0;
+    DBuf spl(L0 + 1, st), splu(L0 * 4 + 4, st), sincl(L0 * 4 + 4, st), spos(L0 * 4 + 4, st);
+    LAUNCH(k_root_flags, L0, rbody, L0, rnw, rbase, spl.as<uint8_t>(), splu.as<u32>());
+    select_flagged_index(spl.as<uint8_t>(), spos.as<u32>(), cnt.as<u64>(), L0, st);
+    inclusive_scan_u32(splu.as<u32>(), sincl.as<u32>(), L0, st);
+    u64 nspl;
+    d2h(&nspl, cnt.p, 1, st);
+    if (!headless) {
+      DBuf fb(4, st);
+      GT_CUDA(cudaMemsetAsync(fb.p, 0xFF, 4, st));
+      LAUNCH(k_check_splitters, nspl ? nspl : 1, rbody, spos.as<u32>(), cnt.as<u64>(), rnw,
+             fb.as<u32>());
+      u32 k;
+      d2h(&k, fb.p, 1, st);
+      if (k != 0xFFFFFFFFu) {
+        u32 pos, sym;
+        d2h(&pos, spos.as<u32>() + k, 1, st);
+        d2h(&sym, rbody + pos, 1, st);
+        fail(GT_E_CORRUPTION, "splitter %u out of order at root position %u", sym, pos);
+      }
+      if (nspl != rns) fail(GT_E_CORRUPTION, "root body is missing file splitters");
+      u32 last = 0;
+      if (nspl) d2h(&last, spos.as<u32>() + nspl - 1, 1, st);
+      if (!nspl || (u64)last + 1 != L0) fail(GT_E_CORRUPTION, "root body has content after the last splitter");
+    }
+    const u64 F = headless ? 1 : rns;
+    d->F = F;
+    d->file_lo = std::min(file_lo, F);
+    d->file_hi = std::min(file_hi, F);
+    if (d->file_hi < d->file_lo) d->file_hi = d->file_lo;
+    d->seg_lo.alloc(F * 8, st);
+    d->seg_hi.alloc(F * 8, st);
+    LAUNCH(k_segments, F, spos.as<u32>(), F, L0, headless, d->seg_lo.as<u64>(), d->seg_hi.as<u64>());
+  // ---- segment tokens + root occurrence lists ------------------------------
+    const int SBF = std::max(1, bitlen(F - 1));
+    DBuf rkey(L0 * 8 + 8, st), wkey(L0 * 8 + 8, st), isr(L0 + 1, st), isw(L0 + 1, st);
+    DBuf& segof = d->root_seg;
+    segof.alloc(L0 * 4 + 4, st);
+    LAUNCH(k_root_keys, L0, rbody, sincl.as<u32>(), L0, rnw, rbase, rlimit, SBF, headless,
+           rkey.as<u64>(), isr.as<uint8_t>(), wkey.as<u64>(), isw.as<uint8_t>(), segof.as<u32>());
+    auto occ_list = [&](DBuf& key, DBuf& is, int idbits, DBuf& oid, DBuf& oseg, DBuf& ocnt, u64* nout) {
+      DBuf sidx2(L0 * 4 + 4, st), k2(L0 * 8 + 8, st), k3(L0 * 8 + 8, st), h2(L0 + 1, st), hi2(L0 * 4 + 4, st);
+      select_flagged_index(is.as<uint8_t>(), sidx2.as<u32>(), cnt.as<u64>(), L0, st);
+      u64 m;
+      d2h(&m, cnt.p, 1, st);
+      LAUNCH(k_gather_u64, m, sidx2.as<u32>(), m, key.as<u64>(), k2.as<u64>());
+      sort_keys_u64(k2.as<u64>(), k3.as<u64>(), m, idbits + SBF, st);
+      LAUNCH(k_heads, m, k3.as<u64>(), m, h2.as<uint8_t>());
+      select_flagged_index(h2.as<uint8_t>(), hi2.as<u32>(), cnt.as<u64>(), m, st);
+      u64 u;
+      d2h(&u, cnt.p, 1, st);
+      oid.alloc(u * 4 + 4, st);
+      oseg.alloc(u * 4 + 4, st);
+      ocnt.alloc(u * 4 + 4, st);
+      LAUNCH(k_rle_keys, u, k3.as<u64>(), hi2.as<u32>(), u, m, SBF, oid.as<u32>(), oseg.as<u32>(),
+             ocnt.as<u32>());
+      *nout = u;
+    };
+    occ_list(rkey, isr, std::max(1, bitlen(rR - 1)), d->rs_rule, d->rs_seg, d->rs_cnt, &d->n_rs);
+    occ_list(wkey, isw, std::max(1, bitlen(rnw ? rnw - 1 : 0)), d->rw_word, d->rw_seg, d->rw_cnt, &d->n_rw);
+    d->rs_off.alloc((rR + 1) * 8, st);
+    if (d->n_rs * 4 >= rR)  // dense keys: one coalesced pass; sparse: a search per row
+      LAUNCH(k_csr_offsets_lin, d->n_rs + 1, d->rs_rule.as<u32>(), d->n_rs, rR, d->rs_off.as<u64>());
+    else
+      LAUNCH(k_csr_offsets, rR + 1, d->rs_rule.as<u32>(), d->n_rs, rR, d->rs_off.as<u64>());
+      GT_CUDA(cudaStreamSynchronize(st));
+    } catch (const Error& e) {
+      root_err = e;
+    } catch (const std::bad_alloc&) {
+      root_err = Error{GT_E_RESOURCE, "out of host memory"};
+    }
+  };
+  std::thread root_thread(root_side);
+  bool root_joined = false;
+  auto join_root = [&]() {
+    if (root_joined) return;
+    root_thread.join();
+    root_joined = true;
+    cudaEventDestroy(ev_body);
+    rebind_stream(st, {&d->seg_lo, &d->seg_hi, &d->root_seg, &d->rs_rule, &d->rs_seg, &d->rs_cnt, &d->rs_off,
+                       &d->rw_word, &d->rw_seg, &d->rw_cnt});
+    stream_release(device, s_root);
+    if (root_err.code != GT_OK) throw root_err;
+  };
+  struct JoinGuard {
+    std::function<void()> f;
+    ~JoinGuard() {
+      try {
+        f();
+      } catch (...) {
+      }
+    }
+  } join_guard{[&] {
+    if (!root_joined) {  // error path of the main pipeline
+      root_thread.join();
+      root_joined = true;
+      cudaStreamSynchronize(s_root);
+      cudaEventDestroy(ev_body);
+      rebind_stream(st, {&d->seg_lo, &d->seg_hi, &d->root_seg, &d->rs_rule, &d->rs_seg, &d->rs_cnt,
+                         &d->rs_off, &d->rw_word, &d->rw_seg, &d->rw_cnt});
+      stream_release(device, s_root);
+    }
+  }};
+
+
   // the rule-start table: on the device by pointer doubling; the host walk
   // (parse_rules, the reference's sequential reader) runs only to produce the
   // exact error of a malformed section, or when an error path needs it
@@ -2202,7 +2332,6 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   GT_KLAUNCH("k_unpack_long", k_unpack_long, grid_for(nraw, 256), 256, st, raw.as<u32>(),
              rstart.as<u32>(), R, nraw, longq.as<u32>(), bad.as<u32>() + 1, d->body.as<u32>(), owner.as<u32>(), limit,
              bad.as<u32>());
-  raw.release();
   longq.release();
   rstart.release();
   u32 bad_rule;
@@ -2212,130 +2341,6 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     host_range_check(blob, P, bad_rule + 1);
   }
   ph.mark("upload+unpack");
-
-  // ---- root side (splitters, segments, root occurrence lists): only needs
-  // the root body, so it runs on its own stream and host thread while the
-  // main pipeline builds the CSR, the layering and the level lists; its
-  // errors are raised after the main pipeline's, in the reference's order
-  // (dag.py:131-230: cycle, unreachable, then _segments_of_root)
-  const u64 L0 = R ? rd32(blob + P.rules_pos) : 0;  // the root's body length
-  d->L0 = L0;
-  cudaEvent_t ev_body;
-  GT_CUDA(cudaEventCreateWithFlags(&ev_body, cudaEventDisableTiming));
-  GT_CUDA(cudaEventRecord(ev_body, st));
-  Error root_err{GT_OK, ""};
-  cudaStream_t s_root = stream_acquire(device);
-  auto root_side = [&]() {
-    try {
-      GT_CUDA(cudaSetDevice(device));
-      cudaStream_t st = s_root;
-      GT_CUDA(cudaStreamWaitEvent(st, ev_body, 0));
-      DBuf cnt(16, st);
-  // ---- root segments (dag.py:107-128) -------------------------------------
-    const bool headless = ns == 0;
-    DBuf spl(L0 + 1, st), splu(L0 * 4 + 4, st), sincl(L0 * 4 + 4, st), spos(L0 * 4 + 4, st);
-    LAUNCH(k_root_flags, L0, d->body.as<u32>(), L0, nw, base, spl.as<uint8_t>(), splu.as<u32>());
-    select_flagged_index(spl.as<uint8_t>(), spos.as<u32>(), cnt.as<u64>(), L0, st);
-    inclusive_scan_u32(splu.as<u32>(), sincl.as<u32>(), L0, st);
-    u64 nspl;
-    d2h(&nspl, cnt.p, 1, st);
-    if (!headless) {
-      DBuf fb(4, st);
-      GT_CUDA(cudaMemsetAsync(fb.p, 0xFF, 4, st));
-      LAUNCH(k_check_splitters, nspl ? nspl : 1, d->body.as<u32>(), spos.as<u32>(), cnt.as<u64>(), nw,
-             fb.as<u32>());
-      u32 k;
-      d2h(&k, fb.p, 1, st);
-      if (k != 0xFFFFFFFFu) {
-        u32 pos, sym;
-        d2h(&pos, spos.as<u32>() + k, 1, st);
-        d2h(&sym, d->body.as<u32>() + pos, 1, st);
-        fail(GT_E_CORRUPTION, "splitter %u out of order at root position %u", sym, pos);
-      }
-      if (nspl != ns) fail(GT_E_CORRUPTION, "root body is missing file splitters");
-      u32 last = 0;
-      if (nspl) d2h(&last, spos.as<u32>() + nspl - 1, 1, st);
-      if (!nspl || (u64)last + 1 != L0) fail(GT_E_CORRUPTION, "root body has content after the last splitter");
-    }
-    const u64 F = headless ? 1 : ns;
-    d->F = F;
-    d->file_lo = std::min(file_lo, F);
-    d->file_hi = std::min(file_hi, F);
-    if (d->file_hi < d->file_lo) d->file_hi = d->file_lo;
-    d->seg_lo.alloc(F * 8, st);
-    d->seg_hi.alloc(F * 8, st);
-    LAUNCH(k_segments, F, spos.as<u32>(), F, L0, headless, d->seg_lo.as<u64>(), d->seg_hi.as<u64>());
-  // ---- segment tokens + root occurrence lists ------------------------------
-    const int SBF = std::max(1, bitlen(F - 1));
-    DBuf rkey(L0 * 8 + 8, st), wkey(L0 * 8 + 8, st), isr(L0 + 1, st), isw(L0 + 1, st);
-    DBuf& segof = d->root_seg;
-    segof.alloc(L0 * 4 + 4, st);
-    LAUNCH(k_root_keys, L0, d->body.as<u32>(), sincl.as<u32>(), L0, nw, base, SBF, headless,
-           rkey.as<u64>(), isr.as<uint8_t>(), wkey.as<u64>(), isw.as<uint8_t>(), segof.as<u32>());
-    auto occ_list = [&](DBuf& key, DBuf& is, int idbits, DBuf& oid, DBuf& oseg, DBuf& ocnt, u64* nout) {
-      DBuf sidx2(L0 * 4 + 4, st), k2(L0 * 8 + 8, st), k3(L0 * 8 + 8, st), h2(L0 + 1, st), hi2(L0 * 4 + 4, st);
-      select_flagged_index(is.as<uint8_t>(), sidx2.as<u32>(), cnt.as<u64>(), L0, st);
-      u64 m;
-      d2h(&m, cnt.p, 1, st);
-      LAUNCH(k_gather_u64, m, sidx2.as<u32>(), m, key.as<u64>(), k2.as<u64>());
-      sort_keys_u64(k2.as<u64>(), k3.as<u64>(), m, idbits + SBF, st);
-      LAUNCH(k_heads, m, k3.as<u64>(), m, h2.as<uint8_t>());
-      select_flagged_index(h2.as<uint8_t>(), hi2.as<u32>(), cnt.as<u64>(), m, st);
-      u64 u;
-      d2h(&u, cnt.p, 1, st);
-      oid.alloc(u * 4 + 4, st);
-      oseg.alloc(u * 4 + 4, st);
-      ocnt.alloc(u * 4 + 4, st);
-      LAUNCH(k_rle_keys, u, k3.as<u64>(), hi2.as<u32>(), u, m, SBF, oid.as<u32>(), oseg.as<u32>(),
-             ocnt.as<u32>());
-      *nout = u;
-    };
-    occ_list(rkey, isr, std::max(1, bitlen(R - 1)), d->rs_rule, d->rs_seg, d->rs_cnt, &d->n_rs);
-    occ_list(wkey, isw, std::max(1, bitlen(nw ? nw - 1 : 0)), d->rw_word, d->rw_seg, d->rw_cnt, &d->n_rw);
-    d->rs_off.alloc((R + 1) * 8, st);
-    if (d->n_rs * 4 >= R)  // dense keys: one coalesced pass; sparse: a search per row
-      LAUNCH(k_csr_offsets_lin, d->n_rs + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
-    else
-      LAUNCH(k_csr_offsets, R + 1, d->rs_rule.as<u32>(), d->n_rs, R, d->rs_off.as<u64>());
-      GT_CUDA(cudaStreamSynchronize(st));
-    } catch (const Error& e) {
-      root_err = e;
-    } catch (const std::bad_alloc&) {
-      root_err = Error{GT_E_RESOURCE, "out of host memory"};
-    }
-  };
-  std::thread root_thread(root_side);
-  bool root_joined = false;
-  auto join_root = [&]() {
-    if (root_joined) return;
-    root_thread.join();
-    root_joined = true;
-    cudaEventDestroy(ev_body);
-    rebind_stream(st, {&d->seg_lo, &d->seg_hi, &d->root_seg, &d->rs_rule, &d->rs_seg, &d->rs_cnt, &d->rs_off,
-                       &d->rw_word, &d->rw_seg, &d->rw_cnt});
-    stream_release(device, s_root);
-    if (root_err.code != GT_OK) throw root_err;
-  };
-  struct JoinGuard {
-    std::function<void()> f;
-    ~JoinGuard() {
-      try {
-        f();
-      } catch (...) {
-      }
-    }
-  } join_guard{[&] {
-    if (!root_joined) {  // error path of the main pipeline
-      root_thread.join();
-      root_joined = true;
-      cudaStreamSynchronize(s_root);
-      cudaEventDestroy(ev_body);
-      rebind_stream(st, {&d->seg_lo, &d->seg_hi, &d->root_seg, &d->rs_rule, &d->rs_seg, &d->rs_cnt,
-                         &d->rs_off, &d->rw_word, &d->rw_seg, &d->rw_cnt});
-      stream_release(device, s_root);
-    }
-  }};
-
 
   // ---- own / sub CSR: per-rule sort + RLE (csr_build.cu); the global
   // (rule, symbol) sort below remains for sections beyond 2^31 symbols
@@ -2665,6 +2670,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   ph.mark("level lists");
 
   join_root();
+  raw.release();  // (the root side read the root body from it)
   ph.mark("root side joined");
 
   // the seeds' and the reduce's rule ids in tid numbering (after the own
