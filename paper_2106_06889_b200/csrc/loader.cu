@@ -411,14 +411,15 @@ constexpr u32 kMaskW = kChunkB / 32;  // 32-bit words of one candidate's start m
 // the mask of the true entry)
 constexpr int kTabWarps = 8;
 __global__ void __launch_bounds__(kTabWarps * 32) k_chunk_tables(const u32* __restrict__ raw, u64 n, u64 p1,
-                                                                  u64 nch, u32* nxt, u32* cnt, u32* mask) {
+                                                                  u64 nch, u64 c0, u64 c1, u32* nxt, u32* cnt,
+                                                                  u32* mask) {
   __shared__ u32 sm[kTabWarps][kWin][kMaskW + 1];
   const u32 wib = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const u64 warp = (u64)blockIdx.x * kTabWarps + wib;
   const u64 nwarps = (u64)gridDim.x * kTabWarps;
   const u32 END = (u32)(nch * kWin);
   u32(*m)[kMaskW + 1] = sm[wib];
-  for (u64 c = warp; c < nch; c += nwarps) {
+  for (u64 c = c0 + warp; c < c1; c += nwarps) {
     for (u32 w = 0; w < kMaskW; w++) m[lane][w] = 0;
     const u64 cs = p1 + c * kChunkB, ce = cs + kChunkB < n ? cs + kChunkB : n;
     u64 p = cs + lane;
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(kTabWarps * 32) k_chunk_tables(const u32* __re
     for (u32 r = 0; r < kWin; r++) mg[r * kMaskW + lane] = m[r][lane];  // row r = candidate r, coalesced
     __syncwarp();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && lane == 0 && c1 == nch) {
     nxt[END] = END;
     cnt[END] = 0;
   }
@@ -2053,7 +2054,54 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // header and dictionary (overlaps when `blob` is pinned); the rules section
   // is then re-aligned on the device (the dictionary has byte lengths)
   DBuf dblob(nbytes + 4, st);
-  h2d_blob(dblob.p, blob, nbytes, st);
+  // a pinned (or small) blob streams in pieces on a copy stream, one event
+  // each: the rules section is re-aligned piece by piece and the rule-chain
+  // tables start on the chunks that have arrived while the rest streams
+  std::vector<std::pair<size_t, cudaEvent_t>> pieces;  // (end byte, arrival)
+  cudaStream_t s_cp = nullptr;
+  {
+    bool direct = nbytes < (32ull << 20);
+    if (!direct) {
+      cudaPointerAttributes at{};
+      direct = cudaPointerGetAttributes(&at, blob) == cudaSuccess && at.type == cudaMemoryTypeHost;
+      if (!direct) cudaGetLastError();
+    }
+    // (a small blob arrives about when the host has parsed its dictionary:
+    // pieces only add waits and launches there — C2, 18 MB: 1.15 vs 1.44 ms)
+    static const bool one_copy = getenv("GT_H2D_ONE") != nullptr;  // diagnostics: one copy on the main stream
+    if (direct && !one_copy && nbytes >= (64ull << 20)) {
+      s_cp = stream_acquire(device);
+      cudaEvent_t alloc_ev;
+      GT_CUDA(cudaEventCreateWithFlags(&alloc_ev, cudaEventDisableTiming));
+      GT_CUDA(cudaEventRecord(alloc_ev, st));  // (dblob is a stream-ordered allocation on st)
+      GT_CUDA(cudaStreamWaitEvent(s_cp, alloc_ev, 0));
+      cudaEventDestroy(alloc_ev);
+      const size_t piece = std::max<size_t>(16ull << 20, (nbytes + 7) / 8);
+      for (size_t o = 0; o < nbytes; o += piece) {
+        const size_t len = std::min(piece, nbytes - o);
+        GT_CUDA(cudaMemcpyAsync(dblob.as<uint8_t>() + o, blob + o, len, cudaMemcpyHostToDevice, s_cp));
+        cudaEvent_t ev;
+        GT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        GT_CUDA(cudaEventRecord(ev, s_cp));
+        pieces.push_back({o + len, ev});
+      }
+    } else {
+      h2d_blob(dblob.p, blob, nbytes, st);
+    }
+  }
+  struct PieceGuard {  // error paths: the copy stream and events go back
+    std::vector<std::pair<size_t, cudaEvent_t>>* pc;
+    cudaStream_t* s;
+    int device;
+    ~PieceGuard() {
+      for (auto& x : *pc)
+        if (x.second) cudaEventDestroy(x.second);
+      if (*s) {
+        cudaStreamSynchronize(*s);
+        stream_release(device, *s);
+      }
+    }
+  } piece_guard{&pieces, &s_cp, device};
   parse_dict(blob, nbytes, &P);
   ph.mark("host parse: dictionary");
   const u64 nsec = (nbytes - P.rules_pos) / 4;
@@ -2064,8 +2112,42 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     fail(GT_E_RESOURCE, "grammar too large: rules section of %lu words exceeds the 2^32 - 2 word limit",
          (unsigned long)nsec);
   DBuf raw(nsec * 4 + 4, st);
-  if (nsec) GT_CUDA(cudaMemcpyAsync(raw.p, dblob.as<uint8_t>() + P.rules_pos, nsec * 4, cudaMemcpyDeviceToDevice, st));
-  dblob.release();
+  u64 w_done = 0;       // raw words re-aligned (queued on st)
+  size_t piece_at = 0;  // next piece to wait for
+  auto realign_to = [&](u64 w_hi) {
+    if (w_hi > w_done)
+      GT_CUDA(cudaMemcpyAsync(raw.as<uint8_t>() + w_done * 4, dblob.as<uint8_t>() + P.rules_pos + w_done * 4,
+                              (w_hi - w_done) * 4, cudaMemcpyDeviceToDevice, st));
+    w_done = std::max(w_done, w_hi);
+  };
+  // the next piece: st waits for its arrival and re-aligns the words it completes
+  auto arrive_piece = [&]() {
+    if (piece_at >= pieces.size()) return false;
+    auto& pc = pieces[piece_at++];
+    GT_CUDA(cudaStreamWaitEvent(st, pc.second, 0));
+    cudaEventDestroy(pc.second);
+    pc.second = nullptr;
+    const size_t end = pc.first;
+    realign_to(end >= nbytes ? nsec : std::min<u64>(nsec, end > P.rules_pos ? (end - P.rules_pos) / 4 : 0));
+    return true;
+  };
+  auto arrive_all = [&]() {
+    while (arrive_piece()) {
+    }
+    realign_to(nsec);
+    if (s_cp) {
+      stream_release(device, s_cp);  // (every later use of the blob waits on st, which waited on each piece)
+      s_cp = nullptr;
+    }
+    dblob.release();
+  };
+  // the root record first (the root side below reads it)
+  {
+    const u64 root_words = nsec ? std::min<u64>(nsec, 1 + (u64)rd32(blob + P.rules_pos)) : 0;
+    if (pieces.empty()) arrive_all();
+    while (w_done < root_words && arrive_piece()) {
+    }
+  }
   // ---- root side (splitters, segments, root occurrence lists): only needs
   // the root body, so it runs on its own stream and host thread while the
   // main pipeline builds the CSR, the layering and the level lists; its
@@ -2259,8 +2341,18 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
       u32* badp = take();
       u32* maskp = take();
       const DPtr entry{enk[0]}, base{bak[0]}, bad{badp}, mask{maskp};
-      GT_KLAUNCH("k_chunk_tables", k_chunk_tables, grid_for(nch * 32, kTabWarps * 32), kTabWarps * 32, st,
-                 raw.as<u32>(), n, p1, nch, nxk[0], ctk[0], mask.as<u32>());
+      u64 c_done = 0;
+      auto tables_to_here = [&]() {  // the chunks complete in the re-aligned words
+        const u64 c_new = w_done >= n ? nch : (w_done > p1 ? (w_done - p1) / kChunkB : 0);
+        if (c_new > c_done)
+          GT_KLAUNCH("k_chunk_tables", k_chunk_tables, grid_for((c_new - c_done) * 32, kTabWarps * 32),
+                     kTabWarps * 32, st, raw.as<u32>(), n, p1, nch, c_done, c_new, nxk[0], ctk[0], mask.as<u32>());
+        c_done = std::max(c_done, c_new);
+      };
+      tables_to_here();
+      while (arrive_piece()) tables_to_here();
+      arrive_all();
+      tables_to_here();
       GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
       for (int k = 0; k + 1 < NL; k++) {
         const u64 ng = nk[k + 1];
@@ -2278,6 +2370,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
       done = b == 0;
       if (done) d->load_flags |= 1;
     }
+    arrive_all();  // (a no-op after the chunked path)
     if (ok && !done) {
       DBuf J((u64)std::max(K, 1) * (n + 1) * 4, st), pos(P.R * 4, st), bad(4, st);
       u32* Jb = J.as<u32>();
