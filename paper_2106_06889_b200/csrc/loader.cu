@@ -620,7 +620,10 @@ __global__ void k_unpack_rules(const u32* __restrict__ raw, const u32* __restric
     if (r < R) {
       s = rstart[r];
       const u64 e = r + 1 < R ? (u64)rstart[r + 1] - 1 : nraw;
-      if (e - s > kUnpackShort) longq[atomicAdd(nlong, 1u)] = (u32)r;  // the long body: k_unpack_long
+      // (a speculative chain parse that failed leaves rule starts that are
+      // not a chain: nothing outside the section is touched, the run is redone)
+      if (e < s || e > nraw || s < r + 1 || e - (r + 1) > nraw - R) atomicMin(bad_rule, (u32)r);
+      else if (e - s > kUnpackShort) longq[atomicAdd(nlong, 1u)] = (u32)r;  // the long body: k_unpack_long
       else len = (u32)(e - s);
     }
     u32 x = len;  // inclusive prefix of the short lengths
@@ -2290,6 +2293,37 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     host_chain = true;
   };
   DBuf rstart(P.R * 4 + 4, st);
+  // flags read back once after the unpack: [0] first rule with a symbol past
+  // the rules, [1] long bodies queued, [2] the chunked chain parse failed
+  DBuf uflags(16, st);
+  GT_CUDA(cudaMemsetAsync(uflags.p, 0, 16, st));
+  bool chain_speculative = false;  // the chunked parse's check is read with the unpack's
+  auto word_chain = [&](u64 n, int K) {  // the word-level doubling (and its check)
+    DBuf J((u64)std::max(K, 1) * (n + 1) * 4, st), pos(P.R * 4, st), bad(4, st);
+    u32* Jb = J.as<u32>();
+    LAUNCH(k_jump0, n + 1, raw.as<u32>(), n, Jb);
+    for (int k = 1; k < K; k++)
+      LAUNCH(k_jump_double, n + 1, Jb + (u64)(k - 1) * (n + 1), n, Jb + (u64)k * (n + 1));
+    LAUNCH(k_chain_pos, P.R, Jb, n, K, P.R, pos.as<u32>());
+    GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+    LAUNCH(k_chain_check, P.R, pos.as<u32>(), raw.as<u32>(), P.R, n, bad.as<u32>(), rstart.as<u32>());
+    u32 b = 0;
+    d2h(&b, bad.p, 1, st);
+    return b == 0;
+  };
+  auto chain_error = [&]() {  // malformed: reproduce the reference's error
+    need_host_chain();
+    if (P.trunc_rule >= 0) {
+      host_range_check(blob, P, (u64)P.trunc_rule);
+      char buf[96];
+      snprintf(buf, sizeof buf, P.trunc_what.c_str(), P.trunc_rule);
+      fail(GT_E_FORMAT, "truncated input while reading %s", buf);
+    }
+    if (P.trailing) {
+      host_range_check(blob, P, P.R);
+      fail(GT_E_FORMAT, "%lu trailing bytes after rules section", (unsigned long)P.trailing);
+    }
+  };
   {
     const u64 n = nsec;
     const int K = bitlen(P.R - 1);  // J_0 .. J_{K-1}
@@ -2297,7 +2331,7 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
     bool done = false;
     static const bool words_only = getenv("GT_CHAIN_WORDS") != nullptr;  // diagnostics: skip the chunked form
     const u64 p1 = ok ? 1 + (u64)rd32(blob + P.rules_pos) : 0;  // the first record after the root
-    if (ok && !words_only && P.R >= 2 && p1 < n) {
+    if (ok && !words_only && P.R >= 2 && p1 < n && n >= P.R) {
       const u64 nch = (n - p1 + kChunkB - 1) / kChunkB, S = nch * kWin + 1;
       // level tables: level 0 from the chunk walks, then one per 32x fewer
       // chunks up to <= 32 (sizes summed into one carve)
@@ -2365,41 +2399,19 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
         LAUNCH(k_chain_down, nk[k], psk[k], pck[k], enk[k + 1], bak[k + 1], nk[k], enk[k], bak[k], badp);
       LAUNCH(k_chunk_starts, nch * 32, p1, nch, P.R, entry.as<u32>(), base.as<u32>(), mask.as<u32>(),
              rstart.as<u32>());
-      u32 b = 0;
-      d2h(&b, bad.p, 1, st);
-      done = b == 0;
-      if (done) d->load_flags |= 1;
+      // the check travels with the unpack's flags (no host round trip here):
+      // the unpack runs on these starts and is redone if they were no chain
+      GT_CUDA(cudaMemcpyAsync(uflags.as<u32>() + 2, badp, 4, cudaMemcpyDeviceToDevice, st));
+      done = chain_speculative = true;
     }
     arrive_all();  // (a no-op after the chunked path)
-    if (ok && !done) {
-      DBuf J((u64)std::max(K, 1) * (n + 1) * 4, st), pos(P.R * 4, st), bad(4, st);
-      u32* Jb = J.as<u32>();
-      LAUNCH(k_jump0, n + 1, raw.as<u32>(), n, Jb);
-      for (int k = 1; k < K; k++)
-        LAUNCH(k_jump_double, n + 1, Jb + (u64)(k - 1) * (n + 1), n, Jb + (u64)k * (n + 1));
-      LAUNCH(k_chain_pos, P.R, Jb, n, K, P.R, pos.as<u32>());
-      GT_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
-      LAUNCH(k_chain_check, P.R, pos.as<u32>(), raw.as<u32>(), P.R, n, bad.as<u32>(), rstart.as<u32>());
-      u32 b = 0;
-      d2h(&b, bad.p, 1, st);
-      ok = b == 0;
-    }
+    if (ok && !done) ok = word_chain(n, K);
     if (ok) {
       P.E = n - P.R;
       P.Rp = P.R;
       P.trailing = 0;
     } else {
-      need_host_chain();  // malformed: reproduce the reference's error
-      if (P.trunc_rule >= 0) {
-        host_range_check(blob, P, (u64)P.trunc_rule);
-        char buf[96];
-        snprintf(buf, sizeof buf, P.trunc_what.c_str(), P.trunc_rule);
-        fail(GT_E_FORMAT, "truncated input while reading %s", buf);
-      }
-      if (P.trailing) {
-        host_range_check(blob, P, P.R);
-        fail(GT_E_FORMAT, "%lu trailing bytes after rules section", (unsigned long)P.trailing);
-      }
+      chain_error();
     }
   }
   ph.mark("rule chain (device)");
@@ -2413,22 +2425,35 @@ void build_device_dag(const uint8_t* blob, size_t nbytes, int device, u64 file_l
   // ---- unpack --------------------------------------------------------------
   DBuf& owner = d->pos_owner;
   owner.alloc(E * 4 + 4, st);
-  DBuf bad(16, st), longq(R * 4 + 4, st);
+  DBuf longq(R * 4 + 4, st);
   d->body.alloc(E * 4 + 4, st);
   d->boff.alloc((R + 1) * 8, st);
-  if (host_chain) GT_CUDA(cudaMemcpyAsync(rstart.p, P.rstart, R * 4, cudaMemcpyHostToDevice, st));
-  LAUNCH(k_boff, R + 1, rstart.as<u32>(), R, E, d->boff.as<u64>());
-  GT_CUDA(cudaMemsetAsync(bad.p, 0xFF, 4, st));
-  GT_CUDA(cudaMemsetAsync(bad.as<u32>() + 1, 0, 4, st));
-  LAUNCH(k_unpack_rules, R, raw.as<u32>(), rstart.as<u32>(), R, nraw, d->body.as<u32>(), owner.as<u32>(), limit,
-         bad.as<u32>(), longq.as<u32>(), bad.as<u32>() + 1);
-  GT_KLAUNCH("k_unpack_long", k_unpack_long, grid_for(nraw, 256), 256, st, raw.as<u32>(),
-             rstart.as<u32>(), R, nraw, longq.as<u32>(), bad.as<u32>() + 1, d->body.as<u32>(), owner.as<u32>(), limit,
-             bad.as<u32>());
+  u32 uf[3] = {0, 0, 0};
+  auto unpack = [&]() {
+    if (host_chain) GT_CUDA(cudaMemcpyAsync(rstart.p, P.rstart, R * 4, cudaMemcpyHostToDevice, st));
+    LAUNCH(k_boff, R + 1, rstart.as<u32>(), R, E, d->boff.as<u64>());
+    GT_CUDA(cudaMemsetAsync(uflags.p, 0xFF, 4, st));
+    GT_CUDA(cudaMemsetAsync(uflags.as<u32>() + 1, 0, 4, st));
+    LAUNCH(k_unpack_rules, R, raw.as<u32>(), rstart.as<u32>(), R, nraw, d->body.as<u32>(), owner.as<u32>(),
+           limit, uflags.as<u32>(), longq.as<u32>(), uflags.as<u32>() + 1);
+    GT_KLAUNCH("k_unpack_long", k_unpack_long, grid_for(nraw, 256), 256, st, raw.as<u32>(), rstart.as<u32>(), R,
+               nraw, longq.as<u32>(), uflags.as<u32>() + 1, d->body.as<u32>(), owner.as<u32>(), limit,
+               uflags.as<u32>());
+    d2h(uf, uflags.p, 3, st);
+  };
+  unpack();
+  if (chain_speculative) {
+    if (uf[2]) {  // the chunked parse met a record of 32+ words (or a malformed section)
+      GT_CUDA(cudaMemsetAsync(uflags.as<u32>() + 2, 0, 4, st));
+      if (!word_chain(nsec, bitlen(P.R - 1))) chain_error();
+      unpack();
+    } else {
+      d->load_flags |= 1;
+    }
+  }
   longq.release();
   rstart.release();
-  u32 bad_rule;
-  d2h(&bad_rule, bad.p, 1, st);
+  const u32 bad_rule = uf[0];
   if (bad_rule != 0xFFFFFFFFu) {
     need_host_chain();
     host_range_check(blob, P, bad_rule + 1);
