@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GT_ABI_VERSION 2
+#define GT_ABI_VERSION 3
 
 /* Status codes.  Exception class (errors.py) and CLI exit code in brackets. */
 enum gt_status {
@@ -141,6 +141,13 @@ typedef struct gt_view {
    * third less PCIe traffic for the count-carrying results */
   const uint32_t* count32;
   const uint32_t* group_off32;
+  /* (ABI 3) narrow ids: when every record id is below 2^8 or 2^16 (file ids
+   * of an inverted index / ranked inverted index on <= 256 / 65536 files,
+   * word ids of a vocabulary that small) the ids travel id_bytes (1 or 2)
+   * wide in id_narrow and id == NULL; otherwise id_narrow == NULL, id_bytes == 4 */
+  const void* id_narrow;
+  int32_t id_bytes;
+  int32_t reserved_;
 } gt_view;
 
 int gt_abi_version(void);

@@ -93,6 +93,9 @@ class GtView(C.Structure):
         ("kernel_launches", C.c_uint64),
         ("count32", _P32),      # ABI 2: narrowed copies (count / group_off NULL then)
         ("group_off32", _P32),
+        ("id_narrow", C.c_void_p),  # ABI 3: ids id_bytes (1 / 2) wide (id NULL then)
+        ("id_bytes", C.c_int32),
+        ("reserved_", C.c_int32),
     ]
 
 
@@ -147,7 +150,11 @@ def compact_from_view(v: GtView) -> Compact:
     c.group_id = _arr(v.group_id, ng, np.int64)
     c.group_key = _arr(v.group_key, ng, np.uint64)
     c.group_gram = _arr(v.group_gram, ng * l, np.int64)
-    c.id = _arr(v.id, n, np.int64)
+    if v.id_narrow:
+        cty = C.c_uint8 if v.id_bytes == 1 else C.c_uint16
+        c.id = _arr(C.cast(v.id_narrow, C.POINTER(cty)), n, np.int64)
+    else:
+        c.id = _arr(v.id, n, np.int64)
     c.key = _arr(v.key, n, np.uint64)
     c.gram = _arr(v.gram, n * l, np.int64)
     c.count = _arr(v.count, n, np.int64) if v.count else _arr(v.count32, n, np.int64)

@@ -248,11 +248,22 @@ static const uint32_t* pull_narrow(gt_result* r, const DBuf& b, u64 n, cudaStrea
   return pull<uint32_t>(r, t, n, st, bytes);
 }
 
+// u32 ids -> 1 / 2 bytes (the caller guarantees every id fits)
+__global__ void k_narrow_ids(const u32* __restrict__ in, u64 n, int bytes, void* out) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (bytes == 1) static_cast<uint8_t*>(out)[i] = (uint8_t)in[i];
+    else static_cast<unsigned short*>(out)[i] = (unsigned short)in[i];
+  }
+}
+
 // enqueue the D2H copies of a result's compact arrays into pinned blocks the
 // gt_result owns; returns the bytes.  count_bound: an upper bound of every
-// count (0: unknown) — below 2^32 the counts travel as u32
+// count (0: unknown) — below 2^32 the counts travel as u32; id_bound: one
+// past the largest record id (0: unknown) — ids below 2^8 / 2^16 travel 1 / 2
+// bytes wide (ABI 3)
 static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int wbits, int strat, cudaStream_t st,
-                        u64 count_bound = 0) {
+                        u64 count_bound = 0, u64 id_bound = 0) {
   u64 bytes = 0;
   gt_view& v = r->v;
   v.task = task;
@@ -269,7 +280,21 @@ static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int 
   v.group_id = pull<uint32_t>(r, R.group_id, R.n_groups, st, &bytes);
   v.group_key = pull<uint64_t>(r, R.group_key, R.n_groups, st, &bytes);
   v.group_gram = pull<uint32_t>(r, R.group_gram, R.n_groups * l, st, &bytes);
-  v.id = pull<uint32_t>(r, R.id, R.n, st, &bytes);
+  v.id_bytes = 4;
+  if (!wide && R.id_bytes < 4 && R.id_narrow.p) {  // written narrow by the producing kernel
+    v.id_bytes = R.id_bytes;
+    v.id_narrow = R.id_bytes == 1 ? (const void*)pull<uint8_t>(r, R.id_narrow, R.n, st, &bytes)
+                                   : (const void*)pull<uint16_t>(r, R.id_narrow, R.n, st, &bytes);
+  } else if (!wide && R.id.p && id_bound && id_bound <= 65536) {
+    const int nb = id_bound <= 256 ? 1 : 2;
+    DBuf t(R.n * nb + 8, st);
+    if (R.n) GT_KLAUNCH("k_narrow_ids", k_narrow_ids, grid_for(R.n, 256), 256, st, R.id.as<u32>(), R.n, nb, t.p);
+    v.id_bytes = nb;
+    v.id_narrow = nb == 1 ? (const void*)pull<uint8_t>(r, t, R.n, st, &bytes)
+                          : (const void*)pull<uint16_t>(r, t, R.n, st, &bytes);
+  } else {
+    v.id = pull<uint32_t>(r, R.id, R.n, st, &bytes);
+  }
   v.key = pull<uint64_t>(r, R.key, R.n, st, &bytes);
   v.gram = pull<uint32_t>(r, R.gram, R.n * l, st, &bytes);
   if (!wide && R.count32_ok) v.count32 = pull<uint32_t>(r, R.count32, R.n, st, &bytes);
@@ -277,6 +302,14 @@ static u64 pull_records(gt_result* r, DevRecords& R, int task, int seq_len, int 
   else v.count = pull<uint64_t>(r, R.count, R.n, st, &bytes);
   v.d2h_bytes = bytes;
   return bytes;
+}
+
+// one past the largest record id of a task: files for the inverted indexes,
+// words for the word-id records
+static u64 id_bound(const DeviceDag& d, int task) {
+  if (task == GT_INVERTEDINDEX || task == GT_RANKEDINVERTEDINDEX) return std::max<u64>(d.file_hi, 1);
+  if (task == GT_WORDCOUNT || task == GT_SORT || task == GT_TERMVECTOR) return std::max<u64>(d.nw, 1);
+  return 0;
 }
 
 // every count of a task's records is at most the longest owned file's words
@@ -291,7 +324,7 @@ static u64 count_bound(const DeviceDag& d, int task) {
 static void finish(gt_ctx* c, gt_result* r, DevRecords& R, int task, int seq_len, int wbits,
                    int strat, std::chrono::steady_clock::time_point t0, u64 launches0) {
   cudaStream_t st = c->d.stream;
-  pull_records(r, R, task, seq_len, wbits, strat, st, count_bound(c->d, task));
+  pull_records(r, R, task, seq_len, wbits, strat, st, count_bound(c->d, task), id_bound(c->d, task));
   gt_view& v = r->v;
   GT_CUDA(cudaEventRecord(c->ev[2], st));
   GT_CUDA(cudaStreamSynchronize(st));
@@ -456,8 +489,8 @@ int gt_run_many(gt_ctx* c, const int* tasks, int ntasks, int seq_len, int strate
           order_by_count(&d, &W, 0, nullptr);
           GT_CUDA(cudaEventRecord(c->ev[1], st));
         }
-        pull_records(rw, W, tasks[iw], seq_len, 0, GT_TOPDOWN, st, count_bound(d, tasks[iw]));
-        pull_records(ri, I, GT_INVERTEDINDEX, seq_len, 0, GT_TOPDOWN, st);
+        pull_records(rw, W, tasks[iw], seq_len, 0, GT_TOPDOWN, st, count_bound(d, tasks[iw]), id_bound(d, tasks[iw]));
+        pull_records(ri, I, GT_INVERTEDINDEX, seq_len, 0, GT_TOPDOWN, st, 0, id_bound(d, GT_INVERTEDINDEX));
         GT_CUDA(cudaEventRecord(c->ev[2], st));
         GT_CUDA(cudaStreamSynchronize(st));
         float ms = 0, ms2 = 0;

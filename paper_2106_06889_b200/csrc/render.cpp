@@ -235,6 +235,12 @@ struct Renderer {
   }
   // counts and group offsets arrive as u64, or narrowed to u32 (ABI 2)
   uint64_t cnt(uint64_t i) const { return v.count ? v.count[i] : (uint64_t)v.count32[i]; }
+  uint64_t idv(uint64_t i) const {  // (ABI 3: ids may travel 1 / 2 bytes wide)
+    if (v.id) return v.id[i];
+    if (!v.id_narrow) return 0;
+    return v.id_bytes == 1 ? (uint64_t) static_cast<const uint8_t*>(v.id_narrow)[i]
+                           : (uint64_t) static_cast<const uint16_t*>(v.id_narrow)[i];
+  }
   uint64_t goff(uint64_t g) const { return v.group_off ? v.group_off[g] : (uint64_t)v.group_off32[g]; }
   void gram_of_key(std::string& s, uint64_t key) const {
     const int l = v.seq_len;
@@ -256,7 +262,7 @@ struct Renderer {
       case GT_WORDCOUNT:
       case GT_SORT:
         for (uint64_t i = a; i < b; i++) {
-          word(s, v.id[i]);
+          word(s, idv(i));
           s.push_back('\t');
           put_u64(s, cnt(i));
           s.push_back('\n');
@@ -267,7 +273,7 @@ struct Renderer {
           word(s, v.group_id[g]);
           for (uint64_t i = goff(g); i < goff(g + 1); i++) {
             s.push_back('\t');
-            put_u64(s, v.id[i]);
+            put_u64(s, idv(i));
           }
           s.push_back('\n');
         }
@@ -277,7 +283,7 @@ struct Renderer {
           for (uint64_t i = goff(f); i < goff(f + 1); i++) {
             put_u64(s, f);
             s.push_back('\t');
-            word(s, v.id[i]);
+            word(s, idv(i));
             s.push_back('\t');
             put_u64(s, cnt(i));
             s.push_back('\n');
@@ -301,7 +307,7 @@ struct Renderer {
           else gram_of_words(s, v.group_gram + g * (uint64_t)v.seq_len);
           for (uint64_t i = goff(g); i < goff(g + 1); i++) {
             s.push_back('\t');
-            put_u64(s, v.id[i]);
+            put_u64(s, idv(i));
             s.push_back(':');
             put_u64(s, cnt(i));
           }

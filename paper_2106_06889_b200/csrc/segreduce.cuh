@@ -540,6 +540,10 @@ struct PostArgs {
   // needed 64 bits) and of the group offsets, written beside the u64 ones
   u32* rcnt32;
   u32* goff32;
+  // compact 2 / 3: the file ids written rid_bytes (1 / 2) wide into rid_n
+  // instead of rid (4: rid)
+  void* rid_n;
+  int rid_bytes;
 };
 
 __device__ __forceinline__ void seg_stamp(u64* stamps, int k) {
@@ -689,9 +693,23 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
         // (each lane writes its own word's files; a warp-cooperative
         // coalesced emission measured slower: C5 0.27 -> 0.32 ms)
         u64 q = ba + ea, x = pr;
-        while (x) {
-          p.rid[q++] = p.file_lo + (u32)(__ffsll((long long)x) - 1);
-          x &= x - 1;
+        if (p.rid_bytes == 1) {
+          uint8_t* o = static_cast<uint8_t*>(p.rid_n);
+          while (x) {
+            o[q++] = (uint8_t)(p.file_lo + (u32)(__ffsll((long long)x) - 1));
+            x &= x - 1;
+          }
+        } else if (p.rid_bytes == 2) {
+          unsigned short* o = static_cast<unsigned short*>(p.rid_n);
+          while (x) {
+            o[q++] = (unsigned short)(p.file_lo + (u32)(__ffsll((long long)x) - 1));
+            x &= x - 1;
+          }
+        } else {
+          while (x) {
+            p.rid[q++] = p.file_lo + (u32)(__ffsll((long long)x) - 1);
+            x &= x - 1;
+          }
         }
       }
     }

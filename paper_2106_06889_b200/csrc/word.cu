@@ -379,10 +379,17 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t 
   char* base = d->step_cache.as<char>();
   auto at = [&](int i) { return base + off[i]; };
   d->word_counts = DBuf::view(at(4), sz[4]);
+  // the inverted index's file ids narrow when every owned file id fits
+  const int rid_bytes = d->file_hi <= 256 ? 1 : d->file_hi <= 65536 ? 2 : 4;
   wc->id = DBuf::view(at(5), sz[5]);
   wc->count = DBuf::view(at(6), sz[6]);
   wc->count32 = DBuf::view(at(7), sz[7]);
-  ii->id = DBuf::view(at(8), sz[8]);
+  if (rid_bytes < 4) {
+    ii->id_narrow = DBuf::view(at(8), sz[8]);
+    ii->id_bytes = rid_bytes;
+  } else {
+    ii->id = DBuf::view(at(8), sz[8]);
+  }
   ii->group_id = DBuf::view(at(9), sz[9]);
   ii->group_off = DBuf::view(at(10), sz[10]);
   ii->group_off32 = DBuf::view(at(11), sz[11]);
@@ -396,6 +403,8 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t 
   post.wid = wc->id.as<u32>();
   post.rcnt = wc->count.as<u64>();
   post.rid = ii->id.as<u32>();
+  post.rid_n = ii->id_narrow.p;
+  post.rid_bytes = rid_bytes;
   post.gid = ii->group_id.as<u32>();
   post.goff = ii->group_off.as<u64>();
   post.tot = reinterpret_cast<u64*>(at(3));
@@ -440,6 +449,8 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t 
       assemble_counts(d, post.out, V, 0, false, wc);
       assemble_presence(d, post.out2, 1, ii);
       wc->count32_ok = ii->group_off32_ok = false;
+      ii->id_narrow.release();
+      ii->id_bytes = 4;
       if (done) GT_CUDA(cudaEventRecord(done, st));
       return true;
     }

@@ -13,6 +13,8 @@ struct DevRecords {
   // narrowing launch); valid only when the flag is set
   DBuf count32, group_off32;
   bool count32_ok = false, group_off32_ok = false;
+  DBuf id_narrow;   // ids id_bytes (1 / 2) wide, written by the producing kernel
+  int id_bytes = 4; // 4: no narrow copy
 };
 
 void td_word_counts(DeviceDag* d, DBuf& counts);

@@ -27,7 +27,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     lib.gt_abi_version.restype = ctypes.c_int
-    assert lib.gt_abi_version() == 2
+    assert lib.gt_abi_version() == 3
 
 
 def test_python_facade_lists_the_header_exports():
