@@ -195,6 +195,12 @@ def ncu_evidence(symbol: str):
     capture was taken of the library built from these sources
     (profiles/<tag>_stamp.txt == the build stamp)."""
     caps = sorted((ROOT / "profiles").glob("*_metrics.csv"), key=lambda p: p.name)
+
+    def same(cap):
+        f = cap.with_name(cap.name.replace("_metrics.csv", "_stamp.txt"))
+        return f.exists() and f.read_text().strip() == build_stamp()
+    # a capture of this very build first, then the newest by name
+    caps = [c for c in caps if not same(c)] + [c for c in caps if same(c)]
     for cap in reversed(caps):
         rows = list(csv.reader(cap.open()))
         try:
