@@ -412,6 +412,22 @@ __global__ void k_group_out(const u32* gsel, const u64* ng_p, const u32* rec, co
 
 // window sources from rule ids to weight-row ids (tid) after a bottom-up
 // attempt fell back to the top-down path
+// window sources in tid numbering -> the contraction's head rows, with the
+// rule's multiplier (root windows, src >= R, keep their file column, x1)
+__global__ void k_src_head(u32* src, u64 n, u32 R, const u32* __restrict__ ctid, const u32* __restrict__ hd,
+                           const u32* __restrict__ ml, u32* mult) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u32 s = src[i];
+    if (s < R) {
+      src[i] = ctid[hd[s]];
+      mult[i] = ml[s];
+    } else {
+      mult[i] = 1u;
+    }
+  }
+}
+
 __global__ void k_src_tid(u32* src, u64 n, const u32* tid, u32 R) {
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -477,7 +493,7 @@ int run_sequences(DeviceDag* d, int task, int l_, int mode, DevRecords* Rr, int*
   bool bottomup = mode == GT_BOTTOMUP;
   bool sparse = mode == GT_TOPDOWN_SPARSE;
   DBuf w;
-  bool w32 = false;
+  bool w32 = false, wheads = false;
   SparseW sw;
   auto weights = [&] {
     if (sparse) {
@@ -485,7 +501,12 @@ int run_sequences(DeviceDag* d, int task, int l_, int mode, DevRecords* Rr, int*
       sparse_file_weights(d, &sw, nullptr, &FW);
     } else {
       u32 Cw;
-      td_file_weights(d, w, &Cw, &w32);
+      // the dense rows of the contraction's heads when it is in use (a
+      // window's weight is its rule's multiplier times its head's row) on
+      // up to 16 owned files (C2 sequence count 1.54 -> 1.50 ms); on 64 the
+      // scaled gathers of the window pass cost more than the shorter level
+      // pass saves (C4 ranked inverted index 19.5 vs 21.0 ms)
+      td_file_weights(d, w, &Cw, &w32, C <= 16, &wheads);
     }
   };
   if (!bottomup) weights();
@@ -575,15 +596,23 @@ int run_sequences(DeviceDag* d, int task, int l_, int mode, DevRecords* Rr, int*
     const u64 eb = r32 ? 4 : 8;
     DBuf rows(NR * eb + 8, st);
     GT_CUDA(cudaMemsetAsync(rows.p, 0, NR * eb, st));
+    DBuf mult;
+    const u32* wf = nullptr;  // per-window multiplier (contraction), or none
+    if (wheads && N) {
+      mult.alloc(N * 4 + 4, st);
+      SL(k_src_head, N, ssrc.as<u32>(), N, (u32)R, d->c_tid.as<u32>(), d->c_hd.as<u32>(), d->c_ml.as<u32>(),
+         mult.as<u32>());
+      wf = mult.as<u32>();
+    }
     if (nruns) {
       if (w32 && r32)
-        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
+        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), wf, N, C,
                             SeqSrc<u32>{w.as<u32>(), (u32)R, C}, OutRowMajorT<u32>{rows.as<u32>(), C}, st);
       else if (w32)
-        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
+        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), wf, N, C,
                             SeqSrc<u32>{w.as<u32>(), (u32)R, C}, OutRowMajor{rows.as<u64>(), C}, st);
       else
-        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), nullptr, N, C,
+        seg_reduce<SumMode>("k_run_rows", rid.as<u32>(), ssrc.as<u32>(), wf, N, C,
                             SeqSrc<u64>{w.as<u64>(), (u32)R, C}, OutRowMajor{rows.as<u64>(), C}, st);
     }
     w.release();

@@ -550,15 +550,16 @@ void td_file_counts(DeviceDag* d, DBuf& counts, bool* is32) {
 }
 
 // per-file weights only -> [R][Fo] of u64, or u32 (*is32)
-void td_file_weights(DeviceDag* d, DBuf& w, u32* C_out, bool* is32) {
+void td_file_weights(DeviceDag* d, DBuf& w, u32* C_out, bool* is32, bool heads, bool* contracted) {
   const u32 C = std::max<u32>(1, (u32)(d->file_hi - d->file_lo));
   *is32 = rows32(d, C);
-  const TdLists tl = td_lists(d, false);  // every rule's row (callers index by tid)
+  const TdLists tl = td_lists(d, heads);  // every rule's row (callers index by tid), or the heads'
+  if (contracted) *contracted = tl.contracted;
   if (*is32) {
-    w.alloc(d->R * 4 * (u64)C, d->stream);
+    w.alloc(tl.rows * 4 * (u64)C, d->stream);
     td_levels<SumMode, u32>(d, tl, C, w.as<u32>());
   } else {
-    w.alloc(d->R * 8 * (u64)C, d->stream);
+    w.alloc(tl.rows * 8 * (u64)C, d->stream);
     td_levels<SumMode>(d, tl, C, w.as<u64>());
   }
   *C_out = C;

@@ -27,7 +27,9 @@ bool td_presence_records(DeviceDag* d, DevRecords* R);
 bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t done = nullptr);
 void order_by_count(DeviceDag* d, DevRecords* R, u32 ncols, const u32* file);
 void td_file_presence(DeviceDag* d, DBuf& pres, u32* FW, DBuf* rows_out = nullptr);
-void td_file_weights(DeviceDag* d, DBuf& w, u32* C, bool* is32);
+// heads: the contraction's head rows when it is in use (*contracted set; the
+// caller maps a rule's tid t to row c_tid[c_hd[t]] with multiplier c_ml[t])
+void td_file_weights(DeviceDag* d, DBuf& w, u32* C, bool* is32, bool heads = false, bool* contracted = nullptr);
 void assemble_counts(DeviceDag* d, const void* dense, u64 V, u32 ncols, bool by_count, DevRecords* R,
                      bool dense32 = false);
 void assemble_presence(DeviceDag* d, const u64* pres, u32 FW, DevRecords* R);
