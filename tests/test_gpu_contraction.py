@@ -179,3 +179,34 @@ def test_large_contracted_pass_on_file_shards():
         same_compact(combine(parts, "invertedindex", V), whole[1])
         dag.set_files(0, 1 << 62)
         same_compact(gt.run_compact_many(dag, ["wordcount", "invertedindex"], cfg, 3)[1], whole[1])
+
+
+@pytest.mark.parametrize("policy,expect", [("0", [False, False, False]), ("2", [True, True, True]),
+                                           ("1", [False, True, True])])
+def test_contraction_build_policy(policy, expect):
+    """GT_CONTRACT=0 never builds the contraction, 2 on the first run, the
+    default (1) on the DAG's second public run call (read once per process:
+    a subprocess per policy)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "import paper_2106_06889_b200 as gt\n"
+        "from paper_2106_06889_b200.corpus import compose, config_spec\n"
+        "blob, _ = compose(config_spec('c2', scale=0.01))\n"
+        "dag = gt.DeviceDag(blob)\n"
+        "ref = gt.run_compact(dag, 'wordcount', gt.TraversalConfig())\n"
+        "flags = [bool(dag.refresh_info()['load_flags'] & 4)]\n"
+        "for _ in range(2):\n"
+        "    c = gt.run_compact(dag, 'wordcount', gt.TraversalConfig())\n"
+        "    assert (c.id == ref.id).all() and (c.count == ref.count).all()\n"
+        "    flags.append(bool(dag.refresh_info()['load_flags'] & 4))\n"
+        "print(json.dumps(flags))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, GT_CONTRACT=policy),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1]) == expect
