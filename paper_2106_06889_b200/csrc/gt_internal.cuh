@@ -223,7 +223,7 @@ struct DeviceDag {
                          &te_off_dev, &be_off_dev, &sub_rule, &step_cache, &c_hd, &c_ml, &c_lvp, &c_tid, &c_te_child, &c_te_par, &c_te_freq, &c_te_off_dev, &c_ow_word, &c_ow_src, &c_ow_freq,
                          &c_rs_rule_t};
     u64 t = 0;
-    for (const DBuf* b : all) t += b->bytes;
+    for (const DBuf* b : all) t += b->own ? b->bytes : 0;  // (views into step_cache count once)
     return t;
   }
 };
