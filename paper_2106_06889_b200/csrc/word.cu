@@ -173,6 +173,11 @@ __global__ void k_ii_emit(const u64* __restrict__ pres, u64 V, const u64* __rest
 
 #define KL(k, grid, ...) GT_KLAUNCH(#k, k, grid, 256, st, __VA_ARGS__)
 
+// Level 1 holds the rules (heads) whose every parent is the root: no
+// non-root edge enters it (a non-root parent sits at level >= 1), so the
+// passes start at level 2 — one grid barrier fewer per pass.
+constexpr int kFirstEdgeLevel = 2;
+
 // Top-down weights (Alg. 1, engine.py:196-227): rows of C columns per rule,
 // seeded from the root references, then one segmented gather-reduce launch
 // per top-down level over that level's non-root parent edges.
@@ -192,7 +197,7 @@ static void td_levels(const DeviceDag* d, const TdLists& tl, u32 C, T* row, u32 
   }
   // all levels in one persistent launch, grid barriers between levels
   const std::vector<u64>& to = *tl.te_off;
-  seg_reduce_levels<Mode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, C,
+  seg_reduce_levels<Mode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, kFirstEdgeLevel, tl.nl, C,
                           RowSrcT<T>{row, C}, TdRowsT<T>{row, C}, st, false,
                           tl.nl ? (to[tl.nl + 1] - to[1]) / tl.nl : 0,
                           fused_seed ? &seed : nullptr, fused_seed ? post : nullptr);
@@ -421,13 +426,13 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t 
   const std::vector<u64>& to = *tl.te_off;
   const u64 avg = tl.nl ? (to[tl.nl + 1] - to[1]) / tl.nl : 0;
   if (small) {
-    seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, 0, avg,
+    seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, kFirstEdgeLevel, tl.nl, 0, avg,
                                    &seed, &post, RowSrcPair{row}, TdRowsPair{row}, st);
   } else {
     GT_CUDA(cudaMemsetAsync(post.out, 0, V * 8, st));
     GT_CUDA(cudaMemsetAsync(post.out2, 0, V * 8, st));
     GT_CUDA(cudaMemsetAsync(post.tot, 0, 24, st));
-    seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, 1, tl.nl, 0, avg,
+    seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, kFirstEdgeLevel, tl.nl, 0, avg,
                                    &seed, nullptr, RowSrcPair{row}, TdRowsPair{row}, st);
     {  // (seg_reduce's C = 1 launch; its multi-column forms have no pair mode)
       const u64 n = tl.n_own;
