@@ -212,6 +212,8 @@ struct DeviceDag {
   // scratch kept across runs
   DBuf word_counts;  // u64[V] of the last global run
   DBuf step_cache;   // the fused word count + inverted index step's buffers (grow-only)
+  u64 rows_clean = 0;             // leading u64 words of the step's rows left zeroed by the last step
+  const void* rows_clean_at = nullptr;  // (at this step_cache block)
 
   u64 bytes_held() const {
     const DBuf* all[] = {&body, &boff, &pos_owner, &root_seg, &own_ids, &own_freqs, &own_off,

@@ -544,6 +544,11 @@ struct PostArgs {
   // instead of rid (4: rid)
   void* rid_n;
   int rid_bytes;
+  // rows cleared again after the word reduce has read them (while the
+  // compaction runs): the next step's phase 0 then seeds them without a
+  // clearing pass and its grid barrier
+  u64* zero_tail;
+  u64 zero_tail_n;
 };
 
 __device__ __forceinline__ void seg_stamp(u64* stamps, int k) {
@@ -828,12 +833,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
     u64* zr = reinterpret_cast<u64*>(seed.row);
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < seed.zero_n; i += (u64)gridDim.x * blockDim.x)
       zr[i] = 0;
+    // (the reduce output is only written after many level barriers)
     if (post.out)
       for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < post.out_n; i += (u64)gridDim.x * blockDim.x) {
         post.out[i] = 0;
         if (pair) post.out2[i] = 0;
       }
-    grid.sync();
+    if (seed.zero_n) grid.sync();  // (zero_n == 0: the rows were cleared by the last step)
     seed_rows_body<Mode>(seed);
     grid.sync();
   }
@@ -946,6 +952,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
     if (post.compact) {
       grid.sync();
       seg_stamp(post.stamps, 3 + nit);
+      // the rows are read by no one after the reduce: clear them for the
+      // next step (the compaction only reads the outputs)
+      for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < post.zero_tail_n; i += nthreads)
+        post.zero_tail[i] = 0;
       post_compact(post, grid);
       seg_stamp(post.stamps, 4 + nit);
     }

@@ -399,8 +399,11 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t 
   ii->group_off = DBuf::view(at(10), sz[10]);
   ii->group_off32 = DBuf::view(at(11), sz[11]);
   u64* row = reinterpret_cast<u64*>(at(0));
+  // rows left zeroed by the last small step on this block need no clearing
+  const u64 rows_n = 2 * tl.rows;
+  const bool clean = small && d->rows_clean_at == (const void*)row && d->rows_clean >= rows_n;
   const SeedArgs seed{tl.rs_rule_t, d->rs_seg.as<u32>(), d->rs_cnt.as<u32>(), d->n_rs, (u32)d->file_lo,
-                      Fo, 1, 1u, row, 2 * tl.rows};
+                      Fo, 1, 1u, row, clean ? 0 : rows_n};
   PostArgs post{tl.ow_word, tl.ow_src, tl.ow_freq, tl.n_own,
                 d->word_counts.as<u64>(), V, reinterpret_cast<u64*>(at(1)), d->rw_word.as<u32>(), d->rw_seg.as<u32>(),
                 d->rw_cnt.as<u32>(), d->n_rw, (u32)d->file_lo, Fo, 1};
@@ -426,9 +429,14 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t 
   const std::vector<u64>& to = *tl.te_off;
   const u64 avg = tl.nl ? (to[tl.nl + 1] - to[1]) / tl.nl : 0;
   if (small) {
+    post.zero_tail = row;
+    post.zero_tail_n = rows_n;
     seg_reduce_levels1<WcPresMode>("k_td_levels", tl.te_child, tl.te_par, tl.te_freq, tl.te_off_dev, kFirstEdgeLevel, tl.nl, 0, avg,
                                    &seed, &post, RowSrcPair{row}, TdRowsPair{row}, st);
+    d->rows_clean = rows_n;
+    d->rows_clean_at = row;
   } else {
+    d->rows_clean = 0;
     GT_CUDA(cudaMemsetAsync(post.out, 0, V * 8, st));
     GT_CUDA(cudaMemsetAsync(post.out2, 0, V * 8, st));
     GT_CUDA(cudaMemsetAsync(post.tot, 0, 24, st));
