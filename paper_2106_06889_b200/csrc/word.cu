@@ -489,7 +489,7 @@ bool td_wc_ii_records(DeviceDag* d, DevRecords* wc, DevRecords* ii, cudaEvent_t 
   if (tr) {
     u64 t[64];
     GT_CUDA(cudaMemcpy(t, stamps.p, 64 * 8, cudaMemcpyDeviceToHost));
-    const int nit = tl.nl;
+    const int nit = std::max(0, tl.nl - kFirstEdgeLevel + 1);  // (levels run by the pass)
     fprintf(stderr, "[wc+ii] seeds %.1f us | levels:", (t[1] - t[0]) / 1e3);
     for (int i = 0; i < nit && 2 + i < 64; i++) fprintf(stderr, " %.1f", (t[2 + i] - (i ? t[1 + i] : t[1])) / 1e3);
     if (4 + nit < 64)
