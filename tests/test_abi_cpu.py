@@ -76,3 +76,36 @@ def test_product_package_never_imports_the_oracle():
         assert "import oracle" not in src and "from oracle" not in src, p
     for p in (pkg / "csrc").glob("*"):
         assert "gt_oracle" not in p.read_text(), p
+
+
+def test_view_layout_matches_the_header_and_narrow_ids_decode():
+    """ABI 3: the ctypes GtView mirrors gt_view field for field (offsets from
+    the header's declaration order), and a view whose ids travel 1 or 2 bytes
+    wide decodes to the same ids as the u32 form."""
+    import ctypes as C
+    import re
+    from pathlib import Path
+
+    import numpy as np
+
+    from paper_2106_06889_b200._abi import GtView, compact_from_view
+    hdr = (Path(__file__).resolve().parents[1] / "include" / "gtadoc_b200.h").read_text()
+    body = hdr[hdr.index("typedef struct gt_view {"):hdr.index("} gt_view;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)  # (comments)
+    names = re.findall(r"\b(\w+);", body)
+    assert [f[0] for f in GtView._fields_] == names
+    ids = np.array([3, 0, 7, 255, 1], dtype=np.uint32)
+    cnt = np.array([5, 4, 3, 2, 1], dtype=np.uint64)
+    for width, dt in ((4, np.uint32), (2, np.uint16), (1, np.uint8)):
+        v = GtView()
+        v.task = 0  # wordcount
+        v.n = len(ids)
+        a = ids.astype(dt)
+        if width == 4:
+            v.id = a.ctypes.data_as(C.POINTER(C.c_uint32))
+        else:
+            v.id_narrow = a.ctypes.data
+            v.id_bytes = width
+        v.count = cnt.ctypes.data_as(C.POINTER(C.c_uint64))
+        c = compact_from_view(v)
+        assert c.id.tolist() == ids.tolist() and c.count.tolist() == cnt.tolist()
