@@ -724,6 +724,30 @@ __device__ __forceinline__ void post_compact(const PostArgs& p, cg::grid_group& 
   if (big && p.rcnt32) atomicOr(reinterpret_cast<unsigned long long*>(p.tot + 2), 1ull);
 }
 
+// The root's plain words arrive sorted by (word, segment): a word of a
+// many-file corpus has one entry per file (C3: up to 10^5), and one atomic
+// per entry serialised them in one L2 slice (the C3 word count spent most of
+// its 0.25 ms there).  A warp combines each run of equal keys first (sum of
+// a, OR of b) and its last lane issues the run's atomics.  Every lane of the
+// warp must call it (key ~0: no entry).
+__device__ __forceinline__ void key_run_atomics(u64 key, u64 a, u64 b, u64* outA, u64* outB) {
+  const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u64 oa = __shfl_up_sync(0xFFFFFFFFu, a, d), ob = __shfl_up_sync(0xFFFFFFFFu, b, d);
+    const u64 ok = __shfl_up_sync(0xFFFFFFFFu, key, d);
+    if (lane >= (unsigned)d && ok == key) {
+      a += oa;
+      b |= ob;
+    }
+  }
+  const u64 nk = __shfl_down_sync(0xFFFFFFFFu, key, 1);
+  if (key != ~0ull && (lane == 31 || nk != key)) {
+    if (a && outA) atomicAdd((unsigned long long*)(outA + key), (unsigned long long)a);
+    if (b && outB) atomicOr((unsigned long long*)(outB + key), (unsigned long long)b);
+  }
+}
+
 template <class Mode, class T = u64>
 __device__ __forceinline__ void seed_rows_body(const SeedArgs& a) {
   using V = typename Mode::V;
@@ -937,17 +961,20 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segred1_levels(const u32* __restri
                            warp, nwarps);
     }
     const bool is_or = std::is_same<Mode, OrMode>::value;
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < post.n_rw; i += nthreads) {
-      const u32 sg = post.rw_seg[i] - post.file_lo;
-      if (sg >= post.nseg) continue;
-      const u32 w = post.rw_word[i];
-      if constexpr (pair) {
-        atomicAdd((unsigned long long*)&post.out[w], (unsigned long long)post.rw_cnt[i]);
-        atomicOr((unsigned long long*)&post.out2[w], 1ull << (sg & 63u));
-      } else {
-        if (!post.per_file) Mode::atomic(&post.out[w], Mode::combine(post.rw_cnt[i], 1ull));
-        else Mode::atomic(&post.out[w], is_or ? (1ull << (sg & 63u)) : (u64)post.rw_cnt[i]);
+    // (one atomic per run of a word within a warp: key_run_atomics)
+    for (u64 b0 = ((u64)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; b0 < post.n_rw; b0 += nthreads) {
+      const u64 i = b0 + (threadIdx.x & 31u);
+      u64 key = ~0ull, a = 0, bits = 0;
+      if (i < post.n_rw) {
+        const u32 sg = post.rw_seg[i] - post.file_lo;
+        if (sg < post.nseg) {
+          key = post.rw_word[i];
+          if (pair) a = post.rw_cnt[i], bits = 1ull << (sg & 63u);
+          else if (is_or) bits = post.per_file ? 1ull << (sg & 63u) : 1ull;
+          else a = post.rw_cnt[i];
+        }
       }
+      key_run_atomics(key, a, bits, is_or ? nullptr : post.out, pair ? post.out2 : (is_or ? post.out : nullptr));
     }
     if (post.compact) {
       grid.sync();

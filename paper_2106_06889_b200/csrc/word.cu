@@ -43,6 +43,33 @@ __global__ void k_root_words(const u32* __restrict__ rw_word, const u32* __restr
                              const u32* __restrict__ rw_cnt, u64 n, u32 file_lo, u32 nseg,
                              int per_file, u32 C, u64 V, int row_major, T* __restrict__ out) {
   u64 stride = (u64)gridDim.x * blockDim.x;
+  const bool is_or = std::is_same<Mode, OrMode>::value;
+  if (sizeof(T) == 8 && (!per_file || is_or)) {
+    // corpus counts and presence: a word's entries (one per file) combined
+    // per warp run first (key_run_atomics)
+    for (u64 b0 = ((u64)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; b0 < n; b0 += stride) {
+      const u64 i = b0 + (threadIdx.x & 31u);
+      u64 key = ~0ull, a = 0, bits = 0;
+      if (i < n) {
+        const u32 sg = rw_seg[i] - file_lo;
+        if (sg < nseg) {
+          const u64 w = rw_word[i];
+          if (!per_file) {
+            key = w;
+            if (is_or) bits = 1ull;
+            else a = rw_cnt[i];
+          } else {  // presence bitsets: cell (word, segment / 64)
+            const u64 col = sg >> 6;
+            key = row_major ? w * C + col : col * V + w;
+            bits = 1ull << (sg & 63u);
+          }
+        }
+      }
+      u64* o = reinterpret_cast<u64*>(out);
+      key_run_atomics(key, a, bits, is_or ? nullptr : o, is_or ? o : nullptr);
+    }
+    return;
+  }
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     u32 sg = rw_seg[i] - file_lo;
     if (sg >= nseg) continue;
@@ -50,7 +77,6 @@ __global__ void k_root_words(const u32* __restrict__ rw_word, const u32* __restr
     if (!per_file) {
       Mode::atomic(&out[w], Mode::combine(rw_cnt[i], 1ull));
     } else {
-      const bool is_or = std::is_same<Mode, OrMode>::value;
       const u32 col = is_or ? (sg >> 6) : sg;
       const u64 v = is_or ? (1ull << (sg & 63u)) : (u64)rw_cnt[i];
       Mode::atomic(&out[row_major ? (u64)w * C + col : (u64)col * V + w], v);
@@ -70,12 +96,14 @@ __global__ void k_root_words_pair(const u32* __restrict__ rw_word, const u32* __
                                   const u32* __restrict__ rw_cnt, u64 n, u32 file_lo, u32 nseg, u64* cnt,
                                   u64* pres) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const u32 sg = rw_seg[i] - file_lo;
-    if (sg >= nseg) continue;
-    const u32 w = rw_word[i];
-    atomicAdd((unsigned long long*)&cnt[w], (unsigned long long)rw_cnt[i]);
-    atomicOr((unsigned long long*)&pres[w], 1ull << (sg & 63u));
+  for (u64 b0 = ((u64)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; b0 < n; b0 += stride) {
+    const u64 i = b0 + (threadIdx.x & 31u);
+    u64 key = ~0ull, a = 0, bits = 0;
+    if (i < n) {
+      const u32 sg = rw_seg[i] - file_lo;
+      if (sg < nseg) key = rw_word[i], a = rw_cnt[i], bits = 1ull << (sg & 63u);
+    }
+    key_run_atomics(key, a, bits, cnt, pres);
   }
 }
 
